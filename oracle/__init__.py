@@ -1,0 +1,178 @@
+"""CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2412_19437_b200`` never imports it and shares no code with it.
+
+Thin ctypes wrappers around ``oracle/liboracle.so`` (built from ``oracle/oracle.c`` by
+``__graft_entry__.build()``), taking/returning CPU torch tensors.  Every function
+follows the paper's definition; see ``oracle/oracle.c`` for the citations.
+
+Pins (tests/test_oracle.py): E4M3 table invariants + torch float8 decode; encoder vs
+an independent brute-force nearest search and vs torch's cast in the non-saturating
+range; SPEC/worked-example goldens (tests/golden/); quantizer closed forms and
+transpose/permutation invariants; GEMM closed form (exact integer arithmetic) and vs
+numpy float64 matmul of dequantized operands.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle.so")
+SRC_PATH = os.path.join(_HERE, "oracle.c")
+
+BF16, FP32 = 0, 1
+FPROP, DGRAD, WGRAD = 0, 1, 2
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with IEEE-strict flags."""
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
+            os.path.getmtime(SRC_PATH), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC",
+               "-shared", "-std=c11", "-Wall", "-o", LIB_PATH, SRC_PATH, "-lm"]
+        subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        i64, vp, i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+        L.oracle_e4m3_decode.restype = ctypes.c_double
+        L.oracle_e4m3_decode.argtypes = [ctypes.c_uint8]
+        L.oracle_e4m3_encode.restype = ctypes.c_uint8
+        L.oracle_e4m3_encode.argtypes = [ctypes.c_float]
+        L.oracle_e4m3_encode_array.argtypes = [vp, i64, vp]
+        L.oracle_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
+        L.oracle_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
+        L.oracle_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
+        L.oracle_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32]
+        L.oracle_grouped_gemm.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, i32]
+        L.oracle_rel_err_normwise.restype = ctypes.c_double
+        L.oracle_rel_err_normwise.argtypes = [vp, vp, i64]
+        L.oracle_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    assert t.device.type == "cpu" and t.is_contiguous()
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dt(x: torch.Tensor) -> int:
+    if x.dtype == torch.bfloat16:
+        return BF16
+    if x.dtype == torch.float32:
+        return FP32
+    raise TypeError(f"unsupported dtype {x.dtype}")
+
+
+def e4m3_decode(code: int) -> float:
+    return lib().oracle_e4m3_decode(code)
+
+
+def e4m3_encode(y: float) -> int:
+    return lib().oracle_e4m3_encode(y)
+
+
+def decode_table() -> torch.Tensor:
+    """float64 [256] values of every E4M3 code (NaN at 0x7F/0xFF)."""
+    return torch.tensor([e4m3_decode(c) for c in range(256)], dtype=torch.float64)
+
+
+def encode_tensor(y: torch.Tensor) -> torch.Tensor:
+    """Element-wise E4M3 encode of a float32 tensor."""
+    flat = y.to(torch.float32).contiguous().reshape(-1)
+    out = torch.empty(flat.numel(), dtype=torch.uint8)
+    lib().oracle_e4m3_encode_array(_ptr(flat), flat.numel(), _ptr(out))
+    return out.reshape(y.shape)
+
+
+def quantize_act_1x128(x: torch.Tensor):
+    """x [M,K] bf16/fp32 -> (q uint8 [M,K], s fp32 [ceil(K/128), M])."""
+    x = x.contiguous()
+    M, K = x.shape
+    q = torch.empty(M, K, dtype=torch.uint8)
+    s = torch.empty((K + 127) // 128, M, dtype=torch.float32)
+    lib().oracle_quantize_act_1x128(_ptr(x), _dt(x), M, K, K, _ptr(q), K, _ptr(s), M)
+    return q, s
+
+
+def quantize_act_128x1(x: torch.Tensor):
+    """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C])."""
+    x = x.contiguous()
+    M, C = x.shape
+    qT = torch.empty(C, M, dtype=torch.uint8)
+    sT = torch.empty((M + 127) // 128, C, dtype=torch.float32)
+    lib().oracle_quantize_act_128x1(_ptr(x), _dt(x), M, C, C, _ptr(qT), M, _ptr(sT), C)
+    return qT, sT
+
+
+def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True):
+    """w [N,K] -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None)."""
+    w = w.contiguous()
+    N, K = w.shape
+    KB = (K + 127) // 128
+    q = torch.empty(N, K, dtype=torch.uint8)
+    s = torch.empty((N + 127) // 128, KB, dtype=torch.float32)
+    qT = torch.empty(K, N, dtype=torch.uint8) if want_t else None
+    lib().oracle_quantize_weight_128x128(_ptr(w), _dt(w), N, K, K, _ptr(q), K, _ptr(s), KB,
+                                         _ptr(qT), N)
+    return q, s, qT
+
+
+def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+         rows: torch.Tensor | None = None, threads: int = 0) -> torch.Tensor:
+    """FP64 block-scaled GEMM.  A [M,K] codes, sA [K/128, M]; B [N,K] codes;
+    sB: FPROP [ceil(N/128), K/128], DGRAD [K/128, ceil(N/128)], WGRAD [K/128, N].
+    Returns O float64 [len(rows) or M, N]."""
+    A, B, sA, sB = A.contiguous(), B.contiguous(), sA.contiguous(), sB.contiguous()
+    M, K = A.shape
+    N = B.shape[0]
+    assert K % 128 == 0 and B.shape[1] == K
+    if rows is not None:
+        rows = rows.to(torch.int64).contiguous()
+    nr = M if rows is None else rows.numel()
+    O = torch.empty(nr, N, dtype=torch.float64)
+    lib().oracle_gemm(layout, M, N, K, _ptr(A), K, _ptr(sA), sA.shape[1], _ptr(B), K, _ptr(sB),
+                      sB.shape[1], _ptr(rows), nr, _ptr(O), threads)
+    return O
+
+
+def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor,
+                 sB: torch.Tensor, rows: torch.Tensor | None = None, threads: int = 0) -> torch.Tensor:
+    """Grouped FPROP.  offsets int64 [G+1]; A [R,K]; sA [K/128, R]; B [G,N,K]; sB [G,ceil(N/128),K/128]."""
+    offsets = offsets.to(torch.int64).contiguous()
+    A, B, sA, sB = A.contiguous(), B.contiguous(), sA.contiguous(), sB.contiguous()
+    G, N, K = B.shape
+    R = A.shape[0]
+    if rows is not None:
+        rows = rows.to(torch.int64).contiguous()
+    nr = R if rows is None else rows.numel()
+    O = torch.empty(nr, N, dtype=torch.float64)
+    lib().oracle_grouped_gemm(G, _ptr(offsets), N, K, _ptr(A), K, _ptr(sA), sA.shape[1], _ptr(B),
+                              _ptr(sB), _ptr(rows), nr, _ptr(O), threads)
+    return O
+
+
+def rel_err_normwise(D: torch.Tensor, O: torch.Tensor) -> float:
+    D = D.to(torch.float64).contiguous()
+    O = O.to(torch.float64).contiguous()
+    return lib().oracle_rel_err_normwise(_ptr(D), _ptr(O), O.numel())
+
+
+def max_threads() -> int:
+    return lib().oracle_max_threads()

@@ -1,0 +1,258 @@
+/* oracle/oracle.c — plain, slow, obviously-correct CPU oracle.
+ *
+ * TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py.  Never part of the product path.
+ * Shares no code with paper_2412_19437_b200/csrc (different language, no common
+ * header, table or generator).
+ *
+ * Build: gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp -fPIC -shared
+ * (IEEE binary32/binary64 arithmetic, no FMA contraction, no flush-to-zero).
+ *
+ * Every function follows the paper's definition in the paper's order:
+ *   - fine-grained groupings 1x128 (activations, per token per 128 channels) and
+ *     128x128 (weights), PAPER.md P:503-510;
+ *   - online quantization: max-abs of the group -> scaling factor -> cast to FP8,
+ *     P:541-544; the scale maps amax onto the maximum representable E4M3 value
+ *     ("scaling the maximum absolute value ... to the maximum representable
+ *     value of FP8"), i.e. s = amax / 448 (readings R1, R2);
+ *   - E4M3 on all tensors, P:536-539;
+ *   - GEMM with per-group scales along K, partial sums over each N_C = 128 interval
+ *     multiplied by the scaling factors and added into a high-precision accumulator,
+ *     P:512-514, P:529-531 (here FP64);
+ *   - 128x1 tiles for the Wgrad operands, P:558, P:672-673 (reading R10).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------------------------------------------------------- E4M3 ---- */
+/* Bit definition: sign(1) | exponent(4, bias 7) | mantissa(3).
+ * exponent 0: subnormal, value = m * 2^-9.  exponent 15 with mantissa 7: NaN (no Inf).
+ * Otherwise value = (1 + m/8) * 2^(e-7).  Max finite = 1.75 * 2^8 = 448. */
+double oracle_e4m3_decode(uint8_t code) {
+    int sign = code >> 7;
+    int e = (code >> 3) & 0xF;
+    int m = code & 0x7;
+    double v;
+    if (e == 0xF && m == 0x7) return NAN;
+    if (e == 0) v = ldexp((double)m, -9);
+    else v = ldexp(1.0 + m / 8.0, e - 7);
+    return sign ? -v : v;
+}
+
+/* Round-to-nearest-even onto the E4M3 grid, saturating to +-448 (R3):
+ * the value is written as n * quantum with quantum the grid spacing of |y|'s binade
+ * (2^-9 below the smallest normal 2^-6), n rounded to the nearest integer with ties
+ * to even (an even n is an even mantissa), and the result re-encoded from the bit
+ * definition above.  NaN -> canonical 0x7F (R6). */
+uint8_t oracle_e4m3_encode(float y) {
+    if (isnan(y)) return 0x7F;
+    uint8_t sign = signbit(y) ? 0x80 : 0x00;
+    double a = fabs((double)y);                   /* exact */
+    if (a >= 448.0) return sign | 0x7E;           /* saturate (includes +-Inf) */
+    double quantum;
+    if (a < ldexp(1.0, -6)) {
+        quantum = ldexp(1.0, -9);                 /* subnormal grid */
+    } else {
+        int ex;
+        frexp(a, &ex);                            /* a = f * 2^ex, f in [0.5, 1) */
+        quantum = ldexp(1.0, (ex - 1) - 3);       /* 3 mantissa bits in binade 2^(ex-1) */
+    }
+    double n = a / quantum;                       /* exact: power-of-two division */
+    double r = nearbyint(n);                      /* default mode = round half to even */
+    double v = r * quantum;                       /* exact */
+    if (v == 0.0) return sign;
+    if (v < ldexp(1.0, -6)) return sign | (uint8_t)r;   /* subnormal code = multiple of 2^-9 */
+    int ex;
+    double f = frexp(v, &ex);                     /* v = f * 2^ex, f in [0.5,1) */
+    int e = (ex - 1) + 7;                         /* biased exponent */
+    int m = (int)((2.0 * f - 1.0) * 8.0);         /* exact: v is on the grid */
+    if (e > 15 || (e == 15 && m == 7)) return sign | 0x7E;  /* cannot happen below 448 */
+    return sign | (uint8_t)((e << 3) | m);
+}
+
+void oracle_e4m3_encode_array(const float* y, int64_t n, uint8_t* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_e4m3_encode(y[i]);
+}
+
+float oracle_bf16_to_float(uint16_t bits) {
+    uint32_t u = ((uint32_t)bits) << 16;         /* BF16 is the top half of binary32 */
+    float f;
+    memcpy(&f, &u, sizeof f);
+    return f;
+}
+
+static float load_elem(const void* x, int dt, int64_t idx) {
+    if (dt == ORACLE_BF16) return oracle_bf16_to_float(((const uint16_t*)x)[idx]);
+    return ((const float*)x)[idx];
+}
+
+/* scale of a group from its max-abs: s = amax / 448 in binary32 (IEEE division);
+ * an all-zero group (or one whose quotient underflows to 0) takes s = 1
+ * (R4). */
+static float group_scale(float amax) {
+    float s = amax / 448.0f;
+    if (s == 0.0f) s = 1.0f;
+    return s;
+}
+
+/* ------------------------------------------------------ quantizers ---- */
+/* 1x128 tiles: per token m, per 128 channels kb ("per token per 128 channels"). */
+void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                               uint8_t* q, int64_t ldq, float* s, int64_t lds) {
+    int64_t KB = (K + 127) / 128;
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t kb = 0; kb < KB; ++kb) {
+            int64_t k0 = kb * 128, k1 = k0 + 128 < K ? k0 + 128 : K;   /* short last group */
+            float amax = 0.0f;
+            for (int64_t k = k0; k < k1; ++k) amax = fmaxf(amax, fabsf(load_elem(x, xdt, m * ldx + k)));
+            float sc = group_scale(amax);
+            s[kb * lds + m] = sc;
+            for (int64_t k = k0; k < k1; ++k) q[m * ldq + k] = oracle_e4m3_encode(load_elem(x, xdt, m * ldx + k) / sc);
+        }
+    }
+}
+
+/* 128x1 tiles: per channel c, per 128 tokens mb; stored transposed (qT[c][m]) so the
+ * Wgrad contraction (tokens) is contiguous. */
+void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                               uint8_t* qT, int64_t ldq, float* sT, int64_t lds) {
+    int64_t MB = (M + 127) / 128;
+    for (int64_t c = 0; c < C; ++c) {
+        for (int64_t mb = 0; mb < MB; ++mb) {
+            int64_t m0 = mb * 128, m1 = m0 + 128 < M ? m0 + 128 : M;
+            float amax = 0.0f;
+            for (int64_t m = m0; m < m1; ++m) amax = fmaxf(amax, fabsf(load_elem(x, xdt, m * ldx + c)));
+            float sc = group_scale(amax);
+            sT[mb * lds + c] = sc;
+            for (int64_t m = m0; m < m1; ++m) qT[c * ldq + m] = oracle_e4m3_encode(load_elem(x, xdt, m * ldx + c) / sc);
+        }
+    }
+}
+
+/* 128x128 blocks: per 128 output channels nb, per 128 input channels kb. */
+void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                    uint8_t* qT, int64_t ldqT) {
+    int64_t NB = (N + 127) / 128, KB = (K + 127) / 128;
+    for (int64_t nb = 0; nb < NB; ++nb) {
+        int64_t n0 = nb * 128, n1 = n0 + 128 < N ? n0 + 128 : N;
+        for (int64_t kb = 0; kb < KB; ++kb) {
+            int64_t k0 = kb * 128, k1 = k0 + 128 < K ? k0 + 128 : K;
+            float amax = 0.0f;
+            for (int64_t n = n0; n < n1; ++n)
+                for (int64_t k = k0; k < k1; ++k) amax = fmaxf(amax, fabsf(load_elem(w, wdt, n * ldw + k)));
+            float sc = group_scale(amax);
+            s[nb * ldsw + kb] = sc;
+            for (int64_t n = n0; n < n1; ++n)
+                for (int64_t k = k0; k < k1; ++k) {
+                    uint8_t c = oracle_e4m3_encode(load_elem(w, wdt, n * ldw + k) / sc);
+                    q[n * ldq + k] = c;
+                    if (qT) qT[k * ldqT + n] = c;
+                }
+        }
+    }
+}
+
+/* ------------------------------------------------------------ GEMM ---- */
+static double g_dec[256];
+static int g_dec_ready = 0;
+static void dec_table_init(void) {
+    if (g_dec_ready) return;
+    for (int c = 0; c < 256; ++c) g_dec[c] = oracle_e4m3_decode((uint8_t)c);
+    g_dec_ready = 1;
+}
+
+static double scale_b(int layout, const float* sB, int64_t ldsB, int64_t kb, int64_t j) {
+    if (layout == ORACLE_FPROP) return sB[(j / 128) * ldsB + kb];
+    if (layout == ORACLE_DGRAD) return sB[kb * ldsB + j / 128];
+    return sB[kb * ldsB + j];                                  /* WGRAD: per row of B */
+}
+
+/* One output row.  For each N_C = 128 interval kb: the partial sum P_kb of exact
+ * FP8 x FP8 products, multiplied by the two group scales and added into the FP64
+ * accumulator.  Every product dec(a)*dec(b) is exact in binary64 and each
+ * 128-term P_kb is exact too (products are multiples of 2^-18 below 2^18), so FP64
+ * rounding enters only through the scale multiply and the kb sum. */
+static void gemm_row(int layout, int64_t i, int64_t N, int64_t K,
+                     const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                     const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB, double* out) {
+    int64_t KB = K / 128;
+    const uint8_t* a = A + i * lda;
+    for (int64_t j = 0; j < N; ++j) {
+        const uint8_t* b = B + j * ldb;
+        double acc = 0.0;
+        for (int64_t kb = 0; kb < KB; ++kb) {
+            double p = 0.0;
+            for (int64_t c = kb * 128; c < kb * 128 + 128; ++c) p += g_dec[a[c]] * g_dec[b[c]];
+            double sa = sA[kb * ldsA + i];
+            double sb = scale_b(layout, sB, ldsB, kb, j);
+            acc += (sa * sb) * p;
+        }
+        out[j] = acc;
+    }
+}
+
+void oracle_gemm(int layout, int64_t M, int64_t N, int64_t K,
+                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                 const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                 const int64_t* rows, int64_t nrows, double* O, int threads) {
+    dec_table_init();
+    if (!rows) nrows = M;
+#ifdef _OPENMP
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int64_t r = 0; r < nrows; ++r) {
+        int64_t i = rows ? rows[r] : r;
+        gemm_row(layout, i, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, O + r * N);
+    }
+    (void)threads;
+}
+
+void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                         const uint8_t* B, const float* sB,
+                         const int64_t* rows, int64_t nrows, double* O, int threads) {
+    dec_table_init();
+    int64_t total = offsets[G];
+    if (!rows) nrows = total;
+    int64_t NB = (N + 127) / 128, KB = K / 128;
+#ifdef _OPENMP
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int64_t r = 0; r < nrows; ++r) {
+        int64_t i = rows ? rows[r] : r;
+        int32_t e = 0;                                  /* the expert segment holding row i */
+        while (e < G && !(offsets[e] <= i && i < offsets[e + 1])) ++e;
+        if (e == G) { for (int64_t j = 0; j < N; ++j) O[r * N + j] = NAN; continue; }
+        gemm_row(ORACLE_FPROP, i, N, K, A, lda, sA, ldsA,
+                 B + (int64_t)e * N * K, K, sB + (int64_t)e * NB * KB, KB, O + r * N);
+    }
+    (void)threads;
+}
+
+double oracle_rel_err_normwise(const double* D, const double* O, int64_t n) {
+    double num = 0.0, den = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double d = fabs(D[i] - O[i]);
+        if (d > num || isnan(d)) num = isnan(d) ? INFINITY : (d > num ? d : num);
+        if (fabs(O[i]) > den) den = fabs(O[i]);
+    }
+    if (den == 0.0) return num == 0.0 ? 0.0 : INFINITY;
+    return num / den;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

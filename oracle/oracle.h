@@ -1,0 +1,70 @@
+/* oracle/oracle.h — CPU oracle for DeepSeek-V3 fine-grained FP8 quantization + block-scaled GEMM.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2412_19437_b200, include/fp8bs.h) never includes, links or calls it, and
+ * this file shares no code, header, table or constant generator with csrc/.
+ *
+ * Host pointers only, no state.  Layouts mirror include/fp8bs.h so buffers
+ * compare with memcmp:
+ *   activations 1x128   q[m*ldq + k],  s[(k/128)*lds + m]
+ *   activations 128x1   qT[c*ldq + m], sT[(m/128)*lds + c]
+ *   weights 128x128     q[n*ldq + k],  s[(n/128)*ldsw + k/128], optional qT[k*ldqT + n]
+ * Citations: PAPER.md P:503-510 (groupings), P:541-544 (online amax -> scale -> cast),
+ * P:536-539 (E4M3 everywhere), P:512-514 + P:529-531 (per-group scales along K,
+ * FP32-promoted partial sums every N_C = 128), P:477 + P:487 (BF16/FP32 outputs).
+ */
+#ifndef FP8_ORACLE_H
+#define FP8_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORACLE_BF16 0
+#define ORACLE_FP32 1
+
+#define ORACLE_FPROP 0
+#define ORACLE_DGRAD 1
+#define ORACLE_WGRAD 2
+
+/* E4M3 ("fn": bias 7, no Inf, NaN = S.1111.111, max 448) */
+double  oracle_e4m3_decode(uint8_t code);          /* NaN for 0x7F / 0xFF */
+uint8_t oracle_e4m3_encode(float y);               /* RNE, saturate-to-finite, NaN -> 0x7F */
+void    oracle_e4m3_encode_array(const float* y, int64_t n, uint8_t* out);
+float   oracle_bf16_to_float(uint16_t bits);
+
+void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                               uint8_t* q, int64_t ldq, float* s, int64_t lds);
+void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                               uint8_t* qT, int64_t ldq, float* sT, int64_t lds);
+void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                    uint8_t* qT, int64_t ldqT);
+
+/* O[r*N + j] = sum_kb sA(kb,i)*sB(kb,j) * sum_{c in kb} dec(A[i,c])*dec(B[j,c]),  FP64.
+ * i = rows[r] (rows == NULL -> i = r, nrows = M).  Contraction K % 128 == 0.
+ * sA(kb,i) = sA[kb*ldsA + i]
+ * sB(kb,j) = FPROP: sB[(j/128)*ldsB + kb]; DGRAD: sB[kb*ldsB + j/128]; WGRAD: sB[kb*ldsB + j]
+ * threads <= 0 -> all available cores. */
+void oracle_gemm(int layout, int64_t M, int64_t N, int64_t K,
+                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                 const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                 const int64_t* rows, int64_t nrows, double* O, int threads);
+
+/* Grouped FPROP over expert segments [offsets[e], offsets[e+1]) of A's rows.
+ * B is [G][N][K] (ld K), sB is [G][ceil(N/128)][K/128].  Rows as in oracle_gemm. */
+void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                         const uint8_t* B, const float* sB,
+                         const int64_t* rows, int64_t nrows, double* O, int threads);
+
+/* max_ij |D - O| / max_ij |O|  (reading R14) */
+double oracle_rel_err_normwise(const double* D, const double* O, int64_t n);
+
+int oracle_max_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,435 @@
+"""Pins for the CPU oracle (runs without a GPU).
+
+The oracle is pinned to things other than itself:
+  * the E4M3 bit definition's invariants and torch's float8_e4m3fn decoder;
+  * an independent brute-force nearest-value search (numpy) and torch's own cast in
+    the non-saturating range, for the encoder;
+  * hand-derived goldens (tests/golden/e4m3_worked_example.txt);
+  * closed forms for the quantizers (power-of-two scales -> exact recovery) and the
+    GEMM (small-integer operands -> exact arithmetic in any order);
+  * numpy float64 matmul of dequantized operands; a naive numpy re-implementation of
+    the groupings on tiny tensors; transpose / permutation invariants.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "e4m3_worked_example.txt")
+
+
+# ------------------------------------------------------------------ helpers ----
+def torch_decode_table() -> np.ndarray:
+    """E4M3 values of codes 0..255 from torch's float8_e4m3fn (independent decoder)."""
+    return torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+
+
+MAGS = torch_decode_table()[:127]          # codes 0x00..0x7E: 0 .. 448, ascending
+
+
+def brute_encode(y: np.ndarray) -> np.ndarray:
+    """Nearest finite E4M3 magnitude by exhaustive distance over all 127 non-negative
+    finite values, ties -> even code (the mantissa LSB is the code LSB), the sign copied
+    from y.  Inf saturates to 448 (satfinite); NaN -> 0x7F."""
+    y = np.asarray(y, dtype=np.float32)
+    out = np.empty(y.shape, dtype=np.uint8)
+    flat = y.reshape(-1)
+    res = out.reshape(-1)
+    for s in range(0, flat.size, 1 << 15):
+        v = flat[s:s + (1 << 15)]
+        a = np.abs(v.astype(np.float64))
+        finite = np.isfinite(a)
+        # every candidate is <= 448, so for |y| >= 448 the distance ORDER does not depend
+        # on |y|; clipping to 1024 keeps a - m exact in float64 (no false ties).
+        a2 = np.minimum(np.where(finite, a, 0.0), 1024.0)
+        d = np.abs(a2[:, None] - MAGS[None, :])              # [n, 127] brute force
+        dmin = d.min(axis=1, keepdims=True)
+        cand = d == dmin
+        codes = np.arange(127)[None, :]
+        # among equidistant candidates prefer the even code
+        even = cand & (codes % 2 == 0)
+        pick = np.where(even.any(axis=1), np.argmax(even, axis=1), np.argmax(cand, axis=1))
+        pick = np.where(np.isinf(v), 126, pick)
+        c = pick.astype(np.uint8) | np.where(np.signbit(v), 0x80, 0).astype(np.uint8)
+        c = np.where(np.isnan(v), 0x7F, c)
+        res[s:s + v.size] = c
+    return out
+
+
+def oracle_encode(y: np.ndarray) -> np.ndarray:
+    return oracle.encode_tensor(torch.from_numpy(np.ascontiguousarray(y, dtype=np.float32))).numpy()
+
+
+def naive_quant_groups(x: np.ndarray, groups):
+    """Naive numpy grouping quantizer: for each group (list of flat indices) compute the
+    float32 amax, s = f32(amax)/f32(448) (1 if 0), codes = brute_encode(f32(x)/s)."""
+    x = x.astype(np.float32)
+    q = np.zeros(x.shape, dtype=np.uint8)
+    scales = []
+    for idx in groups:
+        v = x[idx]
+        amax = np.float32(np.max(np.abs(v))) if v.size else np.float32(0)
+        s = np.float32(amax) / np.float32(448.0)
+        if s == 0:
+            s = np.float32(1.0)
+        q[idx] = brute_encode((v / s).astype(np.float32))
+        scales.append(s)
+    return q, scales
+
+
+# ------------------------------------------------------------ E4M3 table ----
+def test_decode_table_invariants():
+    t = oracle.decode_table().numpy()
+    assert np.isnan(t[0x7F]) and np.isnan(t[0xFF])
+    assert np.isfinite(t).sum() == 254
+    assert t[0x7E] == 448.0 and t[0xFE] == -448.0           # max finite
+    assert t[0x08] == 2.0 ** -6                             # min normal
+    assert t[0x01] == 2.0 ** -9                             # min subnormal
+    assert t[0x00] == 0.0 and t[0x80] == 0.0 and math.copysign(1, t[0x80]) < 0
+    pos = t[:127]
+    assert np.all(np.diff(pos) > 0)                         # monotone in code
+    assert np.all(t[128:255] == -pos)                       # sign symmetry
+    assert ((pos > 0) & (pos < 2.0 ** -6)).sum() == 7       # 7 subnormals
+    assert (pos >= 2.0 ** -6).sum() == 119                  # 119 normals
+
+
+def test_decode_matches_torch_float8():
+    t = oracle.decode_table().numpy()
+    ref = torch_decode_table()
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isnan(t), np.isnan(ref))
+    assert np.array_equal(t[fin], ref[fin])
+    assert np.array_equal(np.signbit(t[fin]), np.signbit(ref[fin]))
+
+
+def test_encode_decode_roundtrip_all_codes():
+    t = oracle.decode_table().numpy()
+    for c in range(256):
+        if np.isnan(t[c]):
+            continue
+        assert oracle.e4m3_encode(float(t[c])) == c, hex(c)
+
+
+def test_spec_codec_examples():
+    # 0.0 <-> code 0; 1.0 exact; encode(449) saturates to 448.
+    assert oracle.e4m3_encode(0.0) == 0x00
+    assert oracle.e4m3_decode(oracle.e4m3_encode(1.0)) == 1.0
+    assert oracle.e4m3_decode(oracle.e4m3_encode(449.0)) == 448.0
+    assert oracle.e4m3_encode(float("inf")) == 0x7E and oracle.e4m3_encode(float("-inf")) == 0xFE
+    assert oracle.e4m3_encode(float("nan")) == 0x7F
+
+
+# ------------------------------------------------------------- encoder ----
+def _encoder_probe_values() -> np.ndarray:
+    rng = np.random.default_rng(1234)
+    vals = [MAGS.astype(np.float32)]
+    mids = ((MAGS[1:] + MAGS[:-1]) / 2).astype(np.float32)   # exact in binary32
+    vals.append(mids)
+    base = np.concatenate(vals)
+    up = np.nextafter(base, np.float32(np.inf))
+    dn = np.nextafter(base, np.float32(-np.inf))
+    rand_bits = rng.integers(0, 2 ** 32, size=1 << 18, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    rand_bits = rand_bits[~np.isnan(rand_bits)]
+    uni = rng.uniform(-520, 520, size=1 << 18).astype(np.float32)
+    small = (rng.standard_normal(1 << 17) * 2.0 ** rng.integers(-14, 2, 1 << 17)).astype(np.float32)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, 1e-45, -1e-45, 448, 449, 463.99997, 464,
+                        464.00003, 480, 1e38, 2.0 ** -10, 2.0 ** -11, 3 * 2.0 ** -11], dtype=np.float32)
+    allv = np.concatenate([base, up, dn, rand_bits, uni, small, special])
+    return np.concatenate([allv, -allv]).astype(np.float32)
+
+
+def test_encoder_vs_bruteforce_nearest():
+    v = _encoder_probe_values()
+    got = oracle_encode(v)
+    ref = brute_encode(v)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, [(float(v[i]), hex(got[i]), hex(ref[i])) for i in bad[:10]]
+
+
+def test_encoder_vs_torch_cast_nonsaturating_range():
+    # torch's cast is RNE but NON-saturating (|x| > 464 -> NaN, R3), so only
+    # compare where both agree on semantics: |x| <= 448.
+    rng = np.random.default_rng(7)
+    v = np.concatenate([rng.uniform(-448, 448, 1 << 18),
+                        rng.standard_normal(1 << 18) * 2.0 ** rng.integers(-16, 8, 1 << 18)]).astype(np.float32)
+    v = v[np.abs(v) <= 448]
+    ref = torch.from_numpy(v).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    got = oracle_encode(v)
+    assert np.array_equal(got, ref)
+
+
+def test_encoder_monotone():
+    v = np.sort(np.random.default_rng(3).uniform(-500, 500, 1 << 16).astype(np.float32))
+    dec = oracle.decode_table().numpy()[oracle_encode(v)]
+    assert np.all(np.diff(dec) >= 0)
+
+
+# ------------------------------------------------------------ goldens ----
+def _read_golden():
+    tiles = []
+    for line in open(GOLDEN):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        f = line.split()
+        if f[0] == "tile":
+            tiles.append({"scale": float.fromhex(f[3]), "xs": [], "codes": []})
+        else:
+            x = float.fromhex(f[1]) if f[1].startswith(("0x", "-0x")) else float(f[1])
+            tiles[-1]["xs"].append(x)
+            tiles[-1]["codes"].append(int(f[3], 16))
+    return tiles
+
+
+def test_golden_worked_example():
+    tiles = _read_golden()
+    assert len(tiles) == 3
+    x = torch.zeros(len(tiles), 128, dtype=torch.float32)
+    for r, t in enumerate(tiles):
+        x[r, :len(t["xs"])] = torch.tensor(t["xs"], dtype=torch.float32)
+    q, s = oracle.quantize_act_1x128(x)
+    # s = 3/448 for amax 3.0 (binary32 quotient, computed here by numpy).
+    assert s[0, 0].item() == float(np.float32(3.0) / np.float32(448.0))
+    for r, t in enumerate(tiles):
+        assert s[0, r].item() == t["scale"], r
+        n = len(t["xs"])
+        assert q[r, :n].tolist() == t["codes"], (r, [hex(c) for c in q[r, :n].tolist()])
+        assert torch.all(q[r, n:] == 0)
+
+
+def test_spec_quantize_examples():
+    # all-zero tile -> scale 1, codes 0.  S:378: amax 3.0 -> s ~= 0.0066964.
+    q, s = oracle.quantize_act_1x128(torch.zeros(2, 256))
+    assert torch.all(s == 1.0) and torch.all(q == 0)
+    x = torch.zeros(1, 128)
+    x[0, 5] = -3.0
+    q, s = oracle.quantize_act_1x128(x)
+    assert abs(s.item() - 0.0066964) < 1e-7
+    assert q[0, 5].item() == 0xFE
+
+
+# --------------------------------------------------------- quantizers ----
+def _closed_form_tile(rng, n, s0):
+    """A group whose scale is exactly s0 (power of two) and whose codes are recovered:
+    values s0*e with e on the E4M3 grid, one element = 448*s0 (=amax)."""
+    codes = rng.integers(0, 127, n).astype(np.uint8)
+    codes = codes | (rng.integers(0, 2, n).astype(np.uint8) << 7)
+    codes[rng.integers(0, n)] = 0x7E
+    vals = torch_decode_table()[codes] * s0
+    return codes, vals
+
+
+@pytest.mark.parametrize("s0", [2.0 ** -20, 2.0 ** -3, 1.0, 2.0 ** 10])
+def test_quant_1x128_closed_form_exact_recovery(s0):
+    rng = np.random.default_rng(11)
+    M, K = 3, 384
+    x = np.zeros((M, K), np.float32)
+    want = np.zeros((M, K), np.uint8)
+    for m in range(M):
+        for kb in range(K // 128):
+            c, v = _closed_form_tile(rng, 128, s0)
+            x[m, kb * 128:(kb + 1) * 128] = v
+            want[m, kb * 128:(kb + 1) * 128] = c
+    # -0 codes (0x80) decode to -0.0 and re-encode to 0x80; all recovered exactly.
+    q, s = oracle.quantize_act_1x128(torch.from_numpy(x))
+    assert torch.all(s == s0)
+    assert np.array_equal(q.numpy(), want)
+
+
+def test_quant_weight_closed_form_exact_recovery():
+    rng = np.random.default_rng(12)
+    N, K, s0 = 256, 256, 2.0 ** -7
+    w = np.zeros((N, K), np.float32)
+    want = np.zeros((N, K), np.uint8)
+    for nb in range(2):
+        for kb in range(2):
+            c, v = _closed_form_tile(rng, 128 * 128, s0)
+            w[nb * 128:(nb + 1) * 128, kb * 128:(kb + 1) * 128] = v.reshape(128, 128)
+            want[nb * 128:(nb + 1) * 128, kb * 128:(kb + 1) * 128] = c.reshape(128, 128)
+    q, s, qT = oracle.quantize_weight_128x128(torch.from_numpy(w))
+    assert torch.all(s == s0)
+    assert np.array_equal(q.numpy(), want)
+    assert np.array_equal(qT.numpy(), want.T)
+
+
+@pytest.mark.parametrize("M,K", [(3, 300), (2, 128), (1, 5)])
+def test_quant_1x128_vs_naive_groups(M, K):
+    x = W.special_values_act(M, K, seed=M * 1000 + K).numpy()
+    x = np.where(np.isfinite(x), x, 0).astype(np.float32)
+    groups = [np.ravel_multi_index((np.full(min(128, K - k0), m), np.arange(k0, min(K, k0 + 128))), (M, K))
+              for m in range(M) for k0 in range(0, K, 128)]
+    qn, sn = naive_quant_groups(x.reshape(-1), groups)
+    q, s = oracle.quantize_act_1x128(torch.from_numpy(x))
+    assert np.array_equal(q.numpy().reshape(-1), qn)
+    KB = (K + 127) // 128
+    assert np.array_equal(s.numpy(), np.array(sn, np.float32).reshape(M, KB).T)
+
+
+@pytest.mark.parametrize("M,C", [(300, 3), (128, 2), (5, 4)])
+def test_quant_128x1_vs_naive_groups(M, C):
+    x = W.gaussian_act(M, C, seed=5).float().numpy() * np.float32(3.0)
+    groups = [np.ravel_multi_index((np.arange(m0, min(M, m0 + 128)), np.full(min(128, M - m0), c)), (M, C))
+              for c in range(C) for m0 in range(0, M, 128)]
+    qn, sn = naive_quant_groups(x.reshape(-1), groups)
+    qT, sT = oracle.quantize_act_128x1(torch.from_numpy(x))
+    assert np.array_equal(qT.numpy(), qn.reshape(M, C).T)
+    MB = (M + 127) // 128
+    assert np.array_equal(sT.numpy(), np.array(sn, np.float32).reshape(C, MB).T)
+
+
+@pytest.mark.parametrize("N,K", [(130, 200), (128, 128), (64, 300)])
+def test_quant_weight_vs_naive_groups(N, K):
+    w = W.master_weight(N, K, seed=9).numpy()
+    groups, keys = [], []
+    for n0 in range(0, N, 128):
+        for k0 in range(0, K, 128):
+            nn, kk = np.meshgrid(np.arange(n0, min(N, n0 + 128)), np.arange(k0, min(K, k0 + 128)), indexing="ij")
+            groups.append(np.ravel_multi_index((nn.ravel(), kk.ravel()), (N, K)))
+    qn, sn = naive_quant_groups(w.reshape(-1), groups)
+    q, s, qT = oracle.quantize_weight_128x128(torch.from_numpy(w))
+    assert np.array_equal(q.numpy().reshape(-1), qn)
+    assert np.array_equal(qT.numpy(), q.numpy().T)
+    assert np.array_equal(s.numpy().reshape(-1), np.array(sn, np.float32))
+
+
+def test_quant_invariants_transpose_and_permutation():
+    x = W.outlier_act(200, 260, seed=4)
+    q1, s1 = oracle.quantize_act_1x128(x)
+    qT, sT = oracle.quantize_act_128x1(x.t().contiguous())
+    assert torch.equal(qT, q1) and torch.equal(sT, s1)      # 128x1(X^T) == 1x128(X)
+    perm = torch.randperm(200, generator=torch.Generator().manual_seed(0))
+    qp, sp = oracle.quantize_act_1x128(x[perm])
+    assert torch.equal(qp, q1[perm]) and torch.equal(sp, s1[:, perm])   # dispatch commutes
+    w = W.master_weight(300, 200, seed=3)
+    qa, sa, _ = oracle.quantize_weight_128x128(w)
+    qb, sb, _ = oracle.quantize_weight_128x128(w.t().contiguous())
+    assert torch.equal(qb, qa.t()) and torch.equal(sb, sa.t())
+
+
+def test_fine_grained_beats_tensorwise_on_outliers():
+    # with one element x1000 per row, 1x128 error <= tensor-wise error.
+    x = W.outlier_act(64, 1024, seed=1).float()
+    q, s = oracle.quantize_act_1x128(x)
+    dec = torch.from_numpy(torch_decode_table())
+    deq = dec[q.long()] * s.t().repeat_interleave(128, dim=1)[:, :1024].double()
+    err_tile = (deq - x.double()).abs().mean().item()
+    amax = x.abs().max()
+    st = (amax / 448.0).item()
+    qt = oracle.encode_tensor(x / st)
+    err_tensor = (dec[qt.long()] * st - x.double()).abs().mean().item()
+    assert err_tile < err_tensor
+
+
+# ---------------------------------------------------------------- GEMM ----
+def _expand_scale_b(layout, sB, N, KB):
+    """sB(kb, j) as a dense [KB, N] float64 matrix, from the layout's index rule."""
+    j = torch.arange(N)
+    if layout == oracle.FPROP:
+        return sB.double()[j // 128, :].t()
+    if layout == oracle.DGRAD:
+        return sB.double()[:, j // 128]
+    return sB.double()
+
+
+def _exact_reference(layout, A, sA, B, sB):
+    """Closed form for small-integer operands: P_kb = intA_kb @ intB_kb^T exactly (int64),
+    then sum_kb sA*sB*P_kb with all terms integers < 2^53 (exact in float64)."""
+    dec = torch.from_numpy(torch_decode_table())
+    Ai = dec[A.long()].to(torch.int64)
+    Bi = dec[B.long()].to(torch.int64)
+    M, K = A.shape
+    N = B.shape[0]
+    KB = K // 128
+    sBx = _expand_scale_b(layout, sB, N, KB)
+    O = torch.zeros(M, N, dtype=torch.float64)
+    for kb in range(KB):
+        P = Ai[:, kb * 128:(kb + 1) * 128] @ Bi[:, kb * 128:(kb + 1) * 128].t()
+        O += sA[kb].double()[:, None] * sBx[kb][None, :] * P.double()
+    return O
+
+
+@pytest.mark.parametrize("layout", [oracle.FPROP, oracle.DGRAD, oracle.WGRAD])
+def test_gemm_closed_form_exact(layout):
+    M, N, K = 96, 200, 384
+    KB = K // 128
+    A = W.codes_small(M, K, seed=1)
+    B = W.codes_small(N, K, seed=2)
+    sA = W.scales_pow2(KB, M, seed=3)
+    NB = (N + 127) // 128
+    sB = {oracle.FPROP: W.scales_pow2(NB, KB, seed=4), oracle.DGRAD: W.scales_pow2(KB, NB, seed=4),
+          oracle.WGRAD: W.scales_pow2(KB, N, seed=4)}[layout]
+    O = oracle.gemm(layout, A, sA, B, sB)
+    ref = _exact_reference(layout, A, sA, B, sB)
+    assert torch.equal(O, ref)
+
+
+@pytest.mark.parametrize("layout", [oracle.FPROP, oracle.DGRAD, oracle.WGRAD])
+def test_gemm_vs_numpy_dequantized_matmul(layout):
+    g = torch.Generator().manual_seed(5)
+    M, N, K = 64, 160, 512
+    KB, NB = K // 128, (N + 127) // 128
+    A = torch.randint(0, 256, (M, K), generator=g, dtype=torch.uint8)
+    B = torch.randint(0, 256, (N, K), generator=g, dtype=torch.uint8)
+    A[A & 0x7F == 0x7F] = 0x00   # no NaN codes
+    B[B & 0x7F == 0x7F] = 0x00
+    sA = torch.rand(KB, M, generator=g) + 0.01
+    sB = {oracle.FPROP: torch.rand(NB, KB, generator=g), oracle.DGRAD: torch.rand(KB, NB, generator=g),
+          oracle.WGRAD: torch.rand(KB, N, generator=g)}[layout] + 0.01
+    dec = torch_decode_table()
+    dA = dec[A.numpy()] * np.repeat(sA.double().numpy().T, 128, axis=1)
+    dB = dec[B.numpy()] * np.repeat(_expand_scale_b(layout, sB, N, KB).numpy().T, 128, axis=1)
+    ref = dA @ dB.T
+    O = oracle.gemm(layout, A, sA, B, sB).numpy()
+    assert np.max(np.abs(O - ref)) / np.max(np.abs(ref)) < 1e-13
+
+
+def test_gemm_identity_gives_dequant():
+    # identity (exactly representable) x X in full precision = dequant(quant(X)).
+    x = W.outlier_act(40, 256, seed=2)
+    q, s = oracle.quantize_act_1x128(x)
+    I = torch.zeros(256, 256, dtype=torch.uint8)
+    I[torch.arange(256), torch.arange(256)] = 0x38           # E4M3 1.0
+    O = oracle.gemm(oracle.FPROP, q, s, I, torch.ones(2, 2))
+    dec = torch.from_numpy(torch_decode_table())
+    deq = dec[q.long()] * s.t().double().repeat_interleave(128, dim=1)
+    assert torch.equal(O, deq)
+
+
+def test_gemm_row_sampling_matches_full():
+    A = W.codes_small(50, 256, seed=8)
+    B = W.codes_small(30, 256, seed=9)
+    sA = torch.rand(2, 50) + 0.5
+    sB = torch.rand(1, 2) + 0.5
+    full = oracle.gemm(oracle.FPROP, A, sA, B, sB)
+    rows = torch.tensor([49, 0, 17])
+    part = oracle.gemm(oracle.FPROP, A, sA, B, sB, rows=rows)
+    assert torch.equal(part, full[rows])
+
+
+def test_grouped_gemm_equals_per_expert_gemm():
+    G, N, K = 5, 136, 256
+    counts = [0, 7, 130, 1, 64]
+    offsets = torch.tensor([0] + list(np.cumsum(counts)), dtype=torch.int64)
+    R = int(offsets[-1])
+    A = W.codes_small(R, K, seed=1)
+    sA = torch.rand(K // 128, R) + 0.1
+    B = torch.stack([W.codes_small(N, K, seed=10 + e) for e in range(G)])
+    sB = torch.rand(G, (N + 127) // 128, K // 128) + 0.1
+    O = oracle.grouped_gemm(offsets, A, sA, B, sB)
+    for e in range(G):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        ref = oracle.gemm(oracle.FPROP, A[a:b], sA[:, a:b], B[e], sB[e])
+        assert torch.equal(O[a:b], ref)
+
+
+def test_rel_err_normwise():
+    O = torch.tensor([1.0, -2.0, 4.0], dtype=torch.float64)
+    assert oracle.rel_err_normwise(O, O) == 0.0
+    assert abs(oracle.rel_err_normwise(O * 1.01, O) - 0.01) < 1e-15
