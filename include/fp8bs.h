@@ -1,0 +1,148 @@
+/* include/fp8bs.h — C-ABI of libfp8bs.so: DeepSeek-V3 fine-grained FP8 quantization and
+ * block-scaled FP8 GEMMs with FP32 accumulation, hand-written for B200 (sm_100a).
+ *
+ * Paper: arXiv 2412.19437 (DeepSeek-V3), §3.3 "FP8 Training", /root/reference/PAPER.md:
+ *   P:503-510  fine-grained quantization: 1x128 tiles for activations ("per token per 128
+ *              channels"), 128x128 blocks for weights;
+ *   P:512-514  per-group scaling factors along the GEMM inner dimension K;
+ *   P:526-534  FP32 promotion of tensor-core partial sums every N_C = 128 elements, where
+ *              the per-group scales are multiplied in;
+ *   P:536-539  E4M3 on all tensors;  P:541-544  online max-abs scaling;
+ *   P:476-481  Fprop / Dgrad / Wgrad GEMMs all in FP8, outputs BF16 or FP32;
+ *   P:558, P:672-673, P:1568-1571  128x1 tiles for the backward (Wgrad) operands.
+ * Numerical contract (readings R1-R8): s = RN32(amax / 448.0f) (1 if 0),
+ * q = E4M3_RNE_SATFINITE(RN32(x / s)); quantizer outputs are bit-exact vs the CPU oracle.
+ *
+ * CONVENTIONS (all functions)
+ *   - Every tensor pointer is a DEVICE pointer (cudaMalloc / torch CUDA memory) on the
+ *     current device; all matrices are row-major with explicit leading dimensions `ld*`
+ *     counted in ELEMENTS.  E4M3 codes are stored as uint8_t.
+ *   - Ownership: the caller allocates and frees every buffer.  The library never
+ *     allocates, frees or retains device memory and keeps no state across calls (except a
+ *     once-only lookup of the driver entry point cuTensorMapEncodeTiled).
+ *   - Asynchrony: compute calls validate their arguments on the host, enqueue kernels on
+ *     `stream` and return; there is no implicit synchronisation and no device->host read.
+ *   - Errors: validation happens before any launch; a failing call has no side effects and
+ *     returns a non-zero fp8bs_status.  fp8bs_last_error_detail() (thread-local) explains
+ *     the last failure.  Kernel launch failures are reported as FP8BS_ERR_CUDA.
+ *   - Thread safety: reentrant; concurrent calls on different streams / devices are safe.
+ */
+#ifndef FP8BS_H
+#define FP8BS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP8BS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FP8BS_API __attribute__((visibility("default")))
+#else
+#define FP8BS_API
+#endif
+
+typedef struct CUstream_st* fp8bs_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    FP8BS_OK = 0,
+    FP8BS_ERR_INVALID_ARG = 1,   /* NULL pointer, negative size, bad enum */
+    FP8BS_ERR_SHAPE = 2,         /* inconsistent sizes / leading dimensions, K % 128 != 0 */
+    FP8BS_ERR_ALIGN = 3,         /* pointer or row pitch not 16-byte aligned (TMA) */
+    FP8BS_ERR_UNSUPPORTED = 4,   /* valid but unsupported combination (e.g. BF16 + accumulate) */
+    FP8BS_ERR_DEVICE = 5,        /* no CUDA device, or not compute capability 10.0 (sm_100) */
+    FP8BS_ERR_CUDA = 6           /* CUDA runtime / driver error during launch */
+} fp8bs_status;
+
+typedef enum { FP8BS_BF16 = 0, FP8BS_FP32 = 1 } fp8bs_dtype;
+
+/* GEMM layouts of a Linear with weight W [out, in] over T tokens.  In every layout
+ * D[i,j] (+)= sum_c deq(A)[i,c] * deq(B)[j,c]; A [M,K] and B [N,K] are both K-major.
+ *   FPROP: A = Xq [T, in]     (1x128),      B = Wq  [out, in] (128x128) -> D = Y  [T, out]
+ *   DGRAD: A = dYq [T, out]   (1x128),      B = WqT [in, out] (128x128) -> D = dX [T, in]
+ *   WGRAD: A = dYqT [out, T]  (128x1),      B = XqT [in, T]   (128x1)   -> D = dW [out, in] FP32 */
+typedef enum { FP8BS_FPROP = 0, FP8BS_DGRAD = 1, FP8BS_WGRAD = 2 } fp8bs_layout;
+
+FP8BS_API int          fp8bs_abi_version(void);                  /* returns FP8BS_ABI_VERSION */
+FP8BS_API const char*  fp8bs_status_string(fp8bs_status status); /* static string; never NULL */
+FP8BS_API const char*  fp8bs_last_error_detail(void);            /* thread-local; "" if none */
+FP8BS_API fp8bs_status fp8bs_device_supported(int device);       /* FP8BS_OK iff CC 10.0 (sm_100) */
+
+/* ---- quantize_act_1x128 ("per token per 128 channels", P:541-544 online) ----------
+ * x   : [M, K] activations, dtype xdt (BF16 or FP32), leading dimension ldx >= K.
+ * q   : [M, K] uint8 E4M3 codes, ldq >= K:   q[m*ldq + k] = E4M3(x[m,k] / s[kb][m]).
+ * s   : [ceil(K/128), lds] FP32 scales, lds >= M ("contraction-block-major", so a GEMM can load
+ *       one contiguous vector of 128 row scales per K block):  s[kb*lds + m] = amax/448 (1 if 0),
+ *       amax = max |x[m, kb*128 .. kb*128+127]| (NaN ignored; a short last group uses the
+ *       elements that exist).
+ * Any M, K >= 0 (M == 0 or K == 0 is a no-op).  No alignment requirement (unaligned or odd
+ * shapes take a slower generic kernel). */
+FP8BS_API fp8bs_status fp8bs_quantize_act_1x128(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                      uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                      fp8bs_stream_t stream);
+
+/* ---- quantize_act_128x1: transpose-quantize for Wgrad operands --------
+ * x   : [M, C] activations (M tokens, C channels), ldx >= C.
+ * qT  : [C, M] uint8 codes, ldq >= M:  qT[c*ldq + m] = E4M3(x[m,c] / sT[mb][c]), mb = m/128.
+ * sT  : [ceil(M/128), lds] FP32, lds >= C:  sT[mb*lds + c] = amax over x[mb*128 .. +127, c] / 448.
+ * Built from BF16/FP32 (single rounding; reading R10).  Any M, C >= 0. */
+FP8BS_API fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, int64_t M, int64_t C, int64_t ldx,
+                                      uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
+                                      fp8bs_stream_t stream);
+
+/* ---- quantize_weight_128x128 ("per 128 input channels per 128 output channels") ----
+ * w   : [N, K] weights (FP32 master weights, or BF16), ldw >= K.
+ * q   : [N, K] uint8 codes, ldq >= K.
+ * s   : [ceil(N/128), ldsw] FP32, ldsw >= ceil(K/128):  s[nb*ldsw + kb] = block amax / 448.
+ * qT  : optional [K, N] transposed copy of q (qT[k*ldqT + n] == q[n*ldq + k]), ldqT >= N, used as
+ *       the Dgrad B operand; pass NULL to skip.  Any N, K >= 0. */
+FP8BS_API fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                           uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream);
+
+/* ---- gemm: block-scaled FP8 GEMM, FP32 accumulation -----
+ * D[i,j] (+)= sum_kb sA(kb,i) * sB(kb,j) * sum_{c in kb} dec(A[i,c]) * dec(B[j,c])
+ *   i < M, j < N, contraction K with K % 128 == 0 ("misaligned groups" otherwise).
+ * A   : [M, K] uint8 codes, lda >= K.          sA : [K/128, ldsA], ldsA >= M: sA(kb,i) = sA[kb*ldsA + i].
+ * B   : [N, K] uint8 codes, ldb >= K.
+ * sB  : FPROP  [ceil(N/128), ldsB], ldsB >= K/128 : sB(kb,j) = sB[(j/128)*ldsB + kb]
+ *       DGRAD  [K/128, ldsB], ldsB >= ceil(N/128) : sB(kb,j) = sB[kb*ldsB + j/128]
+ *                (the SAME sW array quantize_weight_128x128 wrote, read as [out-block][in-block])
+ *       WGRAD  [K/128, ldsB], ldsB >= N            : sB(kb,j) = sB[kb*ldsB + j]   (128x1 scales)
+ * D   : [M, N] of dtype ddt, ldd >= N.  FPROP/DGRAD: BF16 (round-to-nearest-even) or FP32.
+ *       WGRAD: FP32 only; accumulate != 0 adds into D (gradient accumulation).
+ *       accumulate with BF16 output -> FP8BS_ERR_UNSUPPORTED.
+ * Alignment: A, B, D 16-byte aligned; lda, ldb multiples of 16; sA, sB 16-byte aligned with ldsA
+ * (and WGRAD ldsB) multiples of 4; ldd*sizeof(ddt) a multiple of 16; N a multiple of 8 (BF16)
+ * or 4 (FP32) -> else FP8BS_ERR_ALIGN.  M, N, K <= 2^31 - 1.  M == 0 or N == 0 is a no-op. */
+FP8BS_API fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                        const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                        const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                        void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
+                        fp8bs_stream_t stream);
+
+/* ---- grouped_gemm: MoE expert Fprop over token rows grouped by expert
+ * offsets : DEVICE int64 [G+1], offsets[0] = 0, non-decreasing, offsets[G] = total_M; rows
+ *           [offsets[e], offsets[e+1]) of A belong to expert e.  Any M_e >= 0 (no token
+ *           dropping, no capacity padding).  Never read by the host (no device->host sync).
+ *           Violations (decreasing offsets) are undefined behaviour (clamped, no trap).
+ * A   : [total_M, K] uint8 codes, lda >= K;  sA : [K/128, ldsA], ldsA >= total_M (1x128 scales).
+ * B   : [G, N, K] uint8 codes, contiguous (expert stride N*K);
+ * sB  : [G, ceil(N/128), K/128] FP32, contiguous (FPROP 128x128 scales per expert).
+ * D   : [total_M, N], BF16 or FP32, ldd >= N.
+ * workspace : unused in ABI v1 (may be NULL); fp8bs_grouped_gemm_workspace_size returns 0.
+ * 1 <= G <= 1024.  K a multiple of 128.  Same alignment rules as fp8bs_gemm. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                const uint8_t* B, const float* sB,
+                                void* D, fp8bs_dtype ddt, int64_t ldd,
+                                void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FP8BS_H */

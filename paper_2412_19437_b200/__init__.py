@@ -1,0 +1,14 @@
+"""paper_2412_19437_b200 — B200-native (sm_100a) FP8 fine-grained quantization and block-scaled
+FP8 GEMMs with FP32 accumulation: the data-parallel hot path of DeepSeek-V3's FP8 training
+framework (arXiv 2412.19437 §3.3).
+
+All compute runs in ``libfp8bs.so`` (hand-written CUDA for sm_100a behind the C-ABI in
+``include/fp8bs.h``); this package is the thin Python binding plus the expert-parallel sharding
+layer (``ep``).  PyTorch supplies device memory, streams and process groups only.
+"""
+from ._lib import (BF16, DGRAD, FP32, FPROP, WGRAD, Fp8bsError, abi_version, device_supported, gemm,  # noqa: F401
+                   grouped_gemm, header_symbols, last_error_detail, lib, quantize_act_1x128, quantize_act_128x1,
+                   quantize_weight_128x128, status_string)
+
+__all__ = ["quantize_act_1x128", "quantize_act_128x1", "quantize_weight_128x128", "gemm", "grouped_gemm",
+           "FPROP", "DGRAD", "WGRAD", "Fp8bsError", "abi_version", "device_supported", "lib"]

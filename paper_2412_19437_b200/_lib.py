@@ -1,0 +1,198 @@
+"""ctypes binding of libfp8bs.so (include/fp8bs.h) — argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind the C-ABI; this module only turns torch
+tensors into (device pointer, size, leading dimension) tuples, allocates outputs with torch's
+CUDA allocator, and passes torch's current CUDA stream.  There is no CPU fallback: if the
+shared library is missing or fails to load, importing the functions raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfp8bs.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "fp8bs.h")
+
+OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_ALIGN, ERR_UNSUPPORTED, ERR_DEVICE, ERR_CUDA = range(7)
+BF16, FP32 = 0, 1
+FPROP, DGRAD, WGRAD = 0, 1, 2
+
+_lib = None
+
+
+class Fp8bsError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        self.status = status
+        super().__init__(f"{fn} -> {status_string(status)} ({detail})")
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfp8bs.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2412_19437_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, vp, i32, st = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+        L.fp8bs_abi_version.restype = ctypes.c_int
+        L.fp8bs_status_string.restype = ctypes.c_char_p
+        L.fp8bs_status_string.argtypes = [st]
+        L.fp8bs_last_error_detail.restype = ctypes.c_char_p
+        L.fp8bs_device_supported.restype = st
+        L.fp8bs_device_supported.argtypes = [i32]
+        L.fp8bs_quantize_act_1x128.restype = st
+        L.fp8bs_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_quantize_act_128x1.restype = st
+        L.fp8bs_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_quantize_weight_128x128.restype = st
+        L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_gemm.restype = st
+        L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
+        L.fp8bs_grouped_gemm.restype = st
+        L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
+                                         vp, ctypes.c_size_t, vp]
+        L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
+        L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
+        _lib = L
+    return _lib
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fp8bs_[a-z0-9_]+)\s*\(", txt)))
+
+
+def status_string(status: int) -> str:
+    return lib().fp8bs_status_string(status).decode()
+
+
+def last_error_detail() -> str:
+    return lib().fp8bs_last_error_detail().decode()
+
+
+def abi_version() -> int:
+    return lib().fp8bs_abi_version()
+
+
+def device_supported(device: int = 0) -> bool:
+    return lib().fp8bs_device_supported(device) == OK
+
+
+def _check(status: int, fn: str):
+    if status != OK:
+        raise Fp8bsError(status, fn, last_error_detail())
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return FP32
+    raise TypeError(f"unsupported dtype {t.dtype} (BF16 or FP32)")
+
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def _cuda2d(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+
+
+# ------------------------------------------------------------------ quantizers ----
+def quantize_act_1x128(x: torch.Tensor, q: torch.Tensor | None = None, s: torch.Tensor | None = None):
+    """x [M,K] BF16/FP32 -> (q uint8 [M,K], s fp32 [ceil(K/128), M])  (include/fp8bs.h)."""
+    _cuda2d(x, "x")
+    M, K = x.shape
+    if q is None:
+        q = torch.empty(M, K, dtype=torch.uint8, device=x.device)
+    if s is None:   # leading dimension padded to a multiple of 4 (16 B rows for the GEMM's TMA)
+        s = torch.empty((K + 127) // 128, _pad4(M), dtype=torch.float32, device=x.device)[:, :M]
+    _check(lib().fp8bs_quantize_act_1x128(_p(x), _dt(x), M, K, x.stride(0), _p(q), q.stride(0), _p(s), s.stride(0),
+                                          _stream(x)), "fp8bs_quantize_act_1x128")
+    return q, s
+
+
+def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torch.Tensor | None = None):
+    """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C])."""
+    _cuda2d(x, "x")
+    M, C = x.shape
+    if qT is None:
+        qT = torch.empty(C, M, dtype=torch.uint8, device=x.device)
+    if sT is None:
+        sT = torch.empty((M + 127) // 128, _pad4(C), dtype=torch.float32, device=x.device)[:, :C]
+    _check(lib().fp8bs_quantize_act_128x1(_p(x), _dt(x), M, C, x.stride(0), _p(qT), qT.stride(0), _p(sT),
+                                          sT.stride(0), _stream(x)), "fp8bs_quantize_act_128x1")
+    return qT, sT
+
+
+def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None, qT=None):
+    """w [N,K] FP32/BF16 -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None)."""
+    _cuda2d(w, "w")
+    N, K = w.shape
+    if q is None:
+        q = torch.empty(N, K, dtype=torch.uint8, device=w.device)
+    if s is None:
+        s = torch.empty((N + 127) // 128, (K + 127) // 128, dtype=torch.float32, device=w.device)
+    if want_t and qT is None:
+        qT = torch.empty(K, N, dtype=torch.uint8, device=w.device)
+    _check(lib().fp8bs_quantize_weight_128x128(_p(w), _dt(w), N, K, w.stride(0), _p(q), q.stride(0), _p(s),
+                                               s.stride(0), _p(qT) if want_t else None,
+                                               qT.stride(0) if want_t else 0, _stream(w)),
+           "fp8bs_quantize_weight_128x128")
+    return q, s, (qT if want_t else None)
+
+
+# ------------------------------------------------------------------------ GEMM ----
+def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+         out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, accumulate: bool = False):
+    """D [M,N] (+)= block-scaled A [M,K] x B [N,K]^T (see include/fp8bs.h for the sB layout per
+    layout).  Returns D."""
+    for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
+        _cuda2d(t, n)
+    M, K = A.shape
+    N = B.shape[0]
+    if B.shape[1] != K:
+        raise ValueError("A and B contraction sizes differ")
+    if out is None:
+        out = torch.empty(M, N, dtype=out_dtype, device=A.device)
+    _cuda2d(out, "out")
+    _check(lib().fp8bs_gemm(layout, M, N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
+                            sB.stride(0), _p(out), _dt(out), out.stride(0), 1 if accumulate else 0, _stream(A)),
+           "fp8bs_gemm")
+    return out
+
+
+def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+                 out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None):
+    """MoE expert Fprop: offsets int64 [G+1] (device), A [R,K], sA [K/128, R], B [G,N,K], sB [G,ceil(N/128),K/128]."""
+    _cuda2d(A, "A")
+    _cuda2d(sA, "sA")
+    if offsets.dtype != torch.int64 or not offsets.is_cuda:
+        raise ValueError("offsets must be a CUDA int64 tensor")
+    if not (B.is_cuda and B.is_contiguous() and sB.is_cuda and sB.is_contiguous()):
+        raise ValueError("B and sB must be contiguous CUDA tensors")
+    G, N, K = B.shape
+    R = A.shape[0]
+    if out is None:
+        out = torch.empty(R, N, dtype=out_dtype, device=A.device)
+    _check(lib().fp8bs_grouped_gemm(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
+                                    _p(out), _dt(out), out.stride(0), None, 0, _stream(A)), "fp8bs_grouped_gemm")
+    return out

@@ -1,0 +1,219 @@
+// api.cu — C-ABI entry points of libfp8bs.so (include/fp8bs.h): argument validation, device
+// check, then kernel launch on the caller's stream.  Validation runs before any CUDA call so a
+// failing call has no side effects (and the validation paths are testable without a GPU).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/fp8bs.h"
+#include "internal.h"
+
+namespace fp8bs {
+
+static thread_local char g_detail[512] = "";
+
+static fp8bs_status fail(fp8bs_status st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_detail, sizeof g_detail, fmt, ap);
+    va_end(ap);
+    return st;
+}
+static fp8bs_status ok() { g_detail[0] = 0; return FP8BS_OK; }
+
+int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cache[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+static fp8bs_status check_device() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(FP8BS_ERR_DEVICE, "no CUDA device: %s", cudaGetErrorString(e)); }
+    static int verdict[64] = {0};   // 0 unknown, 1 ok, 2 bad
+    if (dev >= 0 && dev < 64 && verdict[dev] == 1) return FP8BS_OK;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) {
+        if (dev >= 0 && dev < 64) verdict[dev] = 2;
+        return fail(FP8BS_ERR_DEVICE, "device %d is compute capability %d.%d; libfp8bs is built for sm_100a (10.0)", dev, major, minor);
+    }
+    if (dev >= 0 && dev < 64) verdict[dev] = 1;
+    return FP8BS_OK;
+}
+
+static fp8bs_status from_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return ok();
+    return fail(FP8BS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static bool valid_dtype(int d) { return d == FP8BS_BF16 || d == FP8BS_FP32; }
+
+}  // namespace fp8bs
+
+using namespace fp8bs;
+
+extern "C" {
+
+int fp8bs_abi_version(void) { return FP8BS_ABI_VERSION; }
+
+const char* fp8bs_status_string(fp8bs_status s) {
+    switch (s) {
+        case FP8BS_OK: return "FP8BS_OK";
+        case FP8BS_ERR_INVALID_ARG: return "FP8BS_ERR_INVALID_ARG: null pointer, negative size or bad enum";
+        case FP8BS_ERR_SHAPE: return "FP8BS_ERR_SHAPE: inconsistent sizes or leading dimensions";
+        case FP8BS_ERR_ALIGN: return "FP8BS_ERR_ALIGN: pointer or pitch not aligned as required";
+        case FP8BS_ERR_UNSUPPORTED: return "FP8BS_ERR_UNSUPPORTED: unsupported combination";
+        case FP8BS_ERR_DEVICE: return "FP8BS_ERR_DEVICE: no sm_100 device";
+        case FP8BS_ERR_CUDA: return "FP8BS_ERR_CUDA: CUDA error";
+    }
+    return "FP8BS_ERR_UNKNOWN";
+}
+
+const char* fp8bs_last_error_detail(void) { return g_detail; }
+
+fp8bs_status fp8bs_device_supported(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(FP8BS_ERR_DEVICE, "cudaGetDeviceCount: %s", cudaGetErrorString(e)); }
+    if (device < 0 || device >= n) return fail(FP8BS_ERR_DEVICE, "device %d out of range (%d devices)", device, n);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0) return fail(FP8BS_ERR_DEVICE, "compute capability %d.%d is not 10.0", major, minor);
+    return ok();
+}
+
+fp8bs_status fp8bs_quantize_act_1x128(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                      uint8_t* q, int64_t ldq, float* s, int64_t lds, fp8bs_stream_t stream) {
+    if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
+    if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
+    if (M == 0 || K == 0) return ok();
+    if (!x || !q || !s) return fail(FP8BS_ERR_INVALID_ARG, "null pointer (x=%p q=%p s=%p)", x, (void*)q, (void*)s);
+    if (ldx < K || ldq < K || lds < M) return fail(FP8BS_ERR_SHAPE, "need ldx>=K, ldq>=K, lds>=M (ldx=%lld ldq=%lld lds=%lld)",
+                                                   (long long)ldx, (long long)ldq, (long long)lds);
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_quant_act_1x128(x, (int)xdt, M, K, ldx, q, ldq, s, lds, (cudaStream_t)stream),
+                     "quantize_act_1x128 launch");
+}
+
+fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, int64_t M, int64_t C, int64_t ldx,
+                                      uint8_t* qT, int64_t ldq, float* sT, int64_t lds, fp8bs_stream_t stream) {
+    if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
+    if (M < 0 || C < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld C=%lld", (long long)M, (long long)C);
+    if (M == 0 || C == 0) return ok();
+    if (!x || !qT || !sT) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldx < C || ldq < M || lds < C) return fail(FP8BS_ERR_SHAPE, "need ldx>=C, ldq>=M, lds>=C");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_quant_act_128x1(x, (int)xdt, M, C, ldx, qT, ldq, sT, lds, (cudaStream_t)stream),
+                     "quantize_act_128x1 launch");
+}
+
+fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                           uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {
+    if (!valid_dtype(wdt)) return fail(FP8BS_ERR_INVALID_ARG, "wdt=%d", (int)wdt);
+    if (N < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
+    if (N == 0 || K == 0) return ok();
+    if (!w || !q || !s) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldw < K || ldq < K || ldsw < (K + 127) / 128) return fail(FP8BS_ERR_SHAPE, "need ldw>=K, ldq>=K, ldsw>=ceil(K/128)");
+    if (qT && ldqT < N) return fail(FP8BS_ERR_SHAPE, "need ldqT>=N");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_quant_weight_128x128(w, (int)wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, (cudaStream_t)stream),
+                     "quantize_weight_128x128 launch");
+}
+
+static fp8bs_status check_gemm_common(int64_t M, int64_t N, int64_t K, const uint8_t* A, int64_t lda, const float* sA,
+                                      int64_t ldsA, const uint8_t* B, int64_t ldb, const float* sB, void* D,
+                                      fp8bs_dtype ddt, int64_t ldd) {
+    if (!valid_dtype(ddt)) return fail(FP8BS_ERR_INVALID_ARG, "ddt=%d", (int)ddt);
+    if (M < 0 || N < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
+    if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return fail(FP8BS_ERR_SHAPE, "sizes must be < 2^31");
+    if (M == 0 || N == 0) return FP8BS_OK;
+    if (K == 0 || K % 128) return fail(FP8BS_ERR_SHAPE, "misaligned groups: contraction K=%lld must be a positive multiple of 128", (long long)K);
+    if (!A || !sA || !B || !sB || !D) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (lda < K || ldb < K || ldd < N || ldsA < M) return fail(FP8BS_ERR_SHAPE, "need lda>=K, ldb>=K, ldd>=N, ldsA>=M");
+    if (!aligned16(A) || !aligned16(B) || !aligned16(D) || !aligned16(sA) || !aligned16(sB))
+        return fail(FP8BS_ERR_ALIGN, "A, B, D, sA, sB must be 16-byte aligned");
+    if (lda % 16 || ldb % 16 || ldsA % 4) return fail(FP8BS_ERR_ALIGN, "lda, ldb must be multiples of 16 and ldsA of 4");
+    const int64_t esz = ddt == FP8BS_BF16 ? 2 : 4;
+    if ((ldd * esz) % 16) return fail(FP8BS_ERR_ALIGN, "ldd*sizeof(D) must be a multiple of 16");
+    if (N % (ddt == FP8BS_BF16 ? 8 : 4)) return fail(FP8BS_ERR_ALIGN, "N must be a multiple of 8 (BF16 out) or 4 (FP32 out)");
+    return FP8BS_OK;
+}
+
+fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                        const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                        const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                        void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    if (layout != FP8BS_FPROP && layout != FP8BS_DGRAD && layout != FP8BS_WGRAD)
+        return fail(FP8BS_ERR_INVALID_ARG, "layout=%d", (int)layout);
+    fp8bs_status c = check_gemm_common(M, N, K, A, lda, sA, ldsA, B, ldb, sB, D, ddt, ldd);
+    if (c != FP8BS_OK) return c;
+    if (M == 0 || N == 0) return ok();
+    const int64_t KB = K / 128, NB = (N + 127) / 128;
+    if (layout == FP8BS_FPROP && ldsB < KB) return fail(FP8BS_ERR_SHAPE, "FPROP needs ldsB >= K/128");
+    if (layout == FP8BS_DGRAD && ldsB < NB) return fail(FP8BS_ERR_SHAPE, "DGRAD needs ldsB >= ceil(N/128)");
+    if (layout == FP8BS_WGRAD) {
+        if (ldsB < N) return fail(FP8BS_ERR_SHAPE, "WGRAD needs ldsB >= N");
+        if (ldsB % 4) return fail(FP8BS_ERR_ALIGN, "WGRAD needs ldsB % 4 == 0");
+        if (ddt != FP8BS_FP32) return fail(FP8BS_ERR_UNSUPPORTED, "WGRAD writes FP32 weight gradients (P:487, P:551)");
+    }
+    if (accumulate && ddt != FP8BS_FP32) return fail(FP8BS_ERR_UNSUPPORTED, "accumulate requires FP32 output");
+    if (accumulate && layout != FP8BS_WGRAD) return fail(FP8BS_ERR_UNSUPPORTED, "accumulate is supported for WGRAD only");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    GemmArgs a{};
+    a.layout = (int)layout; a.M = M; a.N = N; a.K = K;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = ldb; a.sB = sB; a.ldsB = ldsB;
+    a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = accumulate ? 1 : 0;
+    a.grouped = 0; a.G = 0; a.offsets = nullptr;
+    const char* detail = nullptr;
+    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
+    return from_cuda(e, "gemm launch");
+}
+
+size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K) {
+    (void)G; (void)total_M; (void)N; (void)K;
+    return 0;
+}
+
+fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                const uint8_t* B, const float* sB,
+                                void* D, fp8bs_dtype ddt, int64_t ldd,
+                                void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    (void)workspace; (void)workspace_bytes;
+    if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
+    if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
+    fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
+    if (c != FP8BS_OK) return c;
+    if (total_M == 0 || N == 0) return ok();
+    if (K % 16) return fail(FP8BS_ERR_ALIGN, "K must be a multiple of 16");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    GemmArgs a{};
+    a.layout = FP8BS_FPROP; a.M = total_M; a.N = N; a.K = K;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = K; a.sB = sB; a.ldsB = K / 128;
+    a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
+    a.grouped = 1; a.G = G; a.offsets = offsets;
+    const char* detail = nullptr;
+    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
+    return from_cuda(e, "grouped_gemm launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+// gemm.cu — block-scaled FP8 GEMM with FP32 promotion for B200 (sm_100a).
+//
+// What it computes (§3.3.2; include/fp8bs.h):
+//   D[i,j] (+)= sum_kb  sA(kb,i) * sB(kb,j) * P_kb[i,j],   P_kb = sum_{c in kb} dec(A[i,c]) dec(B[j,c])
+// with one scale per N_C = 128 contraction elements.  The paper (H800) promotes WGMMA partials
+// to CUDA-core registers every 128 elements; here the promotion interval is the same (it is
+// forced by the per-128 scales) but the machinery is Blackwell's:
+//   * TMA (SWIZZLE_128B) stages A [128 x 128] and B [BN x 128] K-blocks into a smem ring;
+//   * one thread issues 4x tcgen05.mma.kind::f8f6f4 (K = 32 each) per K-block into a FRESH
+//     TMEM buffer P (FP32; double-buffered so the tensor core runs ahead of the promotion);
+//   * 8 promotion warps read P with tcgen05.ld, multiply by sA(kb,i)*sB(kb,j) and accumulate
+//     in registers (FP32), then write BF16 (RNE) or FP32 (optionally += for Wgrad);
+//   * a scale warp streams sA (and Wgrad's per-column sB) with TMA into its own ring.
+// Warp roles (384 threads): w0 TMA A/B producer, w1 MMA issuer, w2 TMEM allocator, w3 scale
+// producer, w4..w11 promotion + epilogue (warpgroup h owns columns [h*BN/2, (h+1)*BN/2)).
+// Persistent CTAs walk a static tile schedule; the grouped (MoE) variant maps tiles to
+// (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "sm100.cuh"
+#include "internal.h"
+
+namespace fp8bs {
+
+constexpr int BM = 128, BK = 128;
+constexpr int kMaxGroups = 1024;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kSStages = 8;
+    static constexpr int A_BYTES = BM * BK;
+    static constexpr int B_BYTES = BN * BK;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    // sA box: BM + 4 floats starting at the 4-aligned row at or below row0 (a TMA box must start
+    // 16-byte aligned in its inner dimension; grouped tiles start at arbitrary rows).
+    static constexpr int SA_BOX = BM + 4;
+    static constexpr int SA_BYTES = 640;                    // >= SA_BOX * 4, multiple of 128
+    static constexpr int SB_BYTES = BN * 4;                 // WGRAD per-column scales
+    // + up to 2 block scalars (FPROP/DGRAD); TMA destinations must be 128-byte aligned
+    static constexpr int SSTAGE = SA_BYTES + SB_BYTES + 128;
+    static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int NC = BN / 2;                       // columns per promotion thread
+    static constexpr int OFF_SS = kStages * STAGE;
+    static constexpr int OFF_BAR = OFF_SS + kSStages * SSTAGE;
+    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 4;
+    static constexpr int OFF_GRP = OFF_BAR + NBAR * 8 + 16;
+    static constexpr int SMEM_DENSE = 1024 + OFF_GRP;
+    static constexpr int SMEM_GROUPED = 1024 + OFF_GRP + 2 * (kMaxGroups + 1) * 4;
+};
+
+struct KParams {
+    int M, N, K, KB;
+    int num_m, num_n;
+    const float* sB;              // FPROP/DGRAD/grouped block scalars
+    int64_t sb_nb_stride, sb_kb_stride, sb_expert_stride;
+    int NB;                       // ceil(N/128)
+    void* D; int64_t ldd; int accumulate;
+    int G; const int64_t* offsets;
+};
+
+struct Tile { int row0, row_end, n0, e; };
+
+__device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
+    if (t >= p.num_m * p.num_n) return false;
+    const int m = t % p.num_m, n = t / p.num_m;
+    tl.row0 = m * BM; tl.row_end = p.M; tl.n0 = n; tl.e = 0;   // n0 is scaled by BN by the caller
+    return true;
+}
+
+// cum[e] = number of tiles of experts < e; off[e] = first row of expert e.
+__device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cum, const int* off, int t, Tile& tl) {
+    if (t >= cum[p.G]) return false;
+    int lo = 0, hi = p.G;                       // find e: cum[e] <= t < cum[e+1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (cum[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int e = lo;
+    const int seg = off[e + 1] - off[e];
+    const int mt = (seg + BM - 1) / BM;
+    const int local = t - cum[e];
+    const int m = local % mt, n = local / mt;
+    tl.row0 = off[e] + m * BM; tl.row_end = off[e + 1]; tl.n0 = n; tl.e = e;
+    return true;
+}
+
+#define FP8BS_REG_FENCE(r) asm volatile("" : "+r"(r))
+
+template <int BN, bool kWgrad, bool kOutF32, bool kGrouped>
+__global__ void __launch_bounds__(384, 1)
+k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+          const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
+          const KParams p) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + C::OFF_BAR;
+    auto full_bar   = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar  = [&](int s) { return bar0 + 8u * (C::kStages + s); };
+    auto sfull_bar  = [&](int s) { return bar0 + 8u * (2 * C::kStages + s); };
+    auto sempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + C::kSStages + s); };
+    auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
+    auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + 2 + b); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + C::NBAR * 8);
+    int* cum = reinterpret_cast<int*>(smem + C::OFF_GRP);
+    int* off = cum + (kMaxGroups + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
+        for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), 8); }
+        for (int b = 0; b < 2; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 8); }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmSA);
+        if (kWgrad) tma_prefetch_desc(&tmSB);
+    }
+    if (warp == 2) tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_slot));
+    if constexpr (kGrouped) {
+        if (warp == 4) {
+            // tile prefix over experts: cum[e+1] = cum[e] + ceil(M_e/128) * num_n
+            const int G = p.G;
+            const int per = (G + 31) / 32;
+            const int e0 = lane * per, e1 = min(G, e0 + per);
+            int local = 0;
+            for (int e = e0; e < e1; ++e) {
+                const int64_t a = p.offsets[e], b = p.offsets[e + 1];
+                const int seg = b > a ? (int)(b - a) : 0;
+                off[e] = (int)a;
+                local += ((seg + BM - 1) / BM) * p.num_n;
+            }
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int run = incl - local;
+            for (int e = e0; e < e1; ++e) {
+                cum[e] = run;
+                const int a = off[e];
+                const int64_t b = p.offsets[e + 1];
+                const int seg = b > a ? (int)(b - a) : 0;
+                run += ((seg + BM - 1) / BM) * p.num_n;
+            }
+            if (lane == 31) { cum[G] = incl; off[G] = (int)p.offsets[G]; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto next_tile = [&](int t, Tile& tl) -> bool {
+        bool ok;
+        if constexpr (kGrouped) ok = get_tile_grouped(p, cum, off, t, tl);
+        else ok = get_tile_dense(p, t, tl);
+        tl.n0 *= BN;
+        return ok;
+    };
+
+    if (warp < 4) {
+        setmaxnreg_dec<40>();
+        if (warp == 0 && lane == 0) {
+            // ---------------- TMA producer: A and B K-blocks ----------------
+            int it = 0;
+            Tile tl;
+            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+                for (int kb = 0; kb < p.KB; ++kb, ++it) {
+                    const int s = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    mbar_wait(empty_bar(s), ph ^ 1);
+                    mbar_arrive_expect_tx(full_bar(s), C::STAGE);
+                    const uint32_t sa = sbase + s * C::STAGE;
+                    tma_load_2d(sa, &tmA, full_bar(s), kb * BK, tl.row0);
+                    if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kb * BK, tl.n0, tl.e);
+                    else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kb * BK, tl.n0);
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = idesc_e4m3_f32(BM, BN);
+            int it = 0, pit = 0;
+            Tile tl;
+            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+                for (int kb = 0; kb < p.KB; ++kb, ++it, ++pit) {
+                    const int s = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    const int pb = pit & 1;
+                    const uint32_t pph = (pit >> 1) & 1;
+                    mbar_wait(pempty_bar(pb), pph ^ 1);
+                    mbar_wait(full_bar(s), ph);
+                    tc_fence_after();
+                    const uint32_t sa = sbase + s * C::STAGE;
+                    const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + C::A_BYTES);
+                    const uint32_t d = tmem_base + pb * BN;
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k)
+                        mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                    mma_commit(empty_bar(s));
+                    mma_commit(pfull_bar(pb));
+                }
+            }
+        } else if (warp == 3) {
+            // ---------------- scale producer ----------------
+            int sit = 0;
+            Tile tl;
+            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+                const float* sbp = p.sB;
+                if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
+                const int nb0 = tl.n0 / 128;
+                for (int kb0 = 0; kb0 < p.KB; kb0 += 32) {
+                    float v0 = 0.0f, v1 = 0.0f;
+                    if constexpr (!kWgrad) {
+                        const int kb = kb0 + lane;
+                        if (kb < p.KB) {
+                            v0 = __ldg(sbp + nb0 * p.sb_nb_stride + kb * p.sb_kb_stride);
+                            if (BN == 256 && nb0 + 1 < p.NB) v1 = __ldg(sbp + (nb0 + 1) * p.sb_nb_stride + kb * p.sb_kb_stride);
+                        }
+                    }
+                    const int nk = min(32, p.KB - kb0);
+                    for (int j = 0; j < nk; ++j, ++sit) {
+                        const float b0 = __shfl_sync(0xffffffffu, v0, j);
+                        const float b1 = __shfl_sync(0xffffffffu, v1, j);
+                        if (lane == 0) {
+                            const int ss = sit % C::kSStages;
+                            const uint32_t sph = (sit / C::kSStages) & 1;
+                            mbar_wait(sempty_bar(ss), sph ^ 1);
+                            uint8_t* st = smem + C::OFF_SS + ss * C::SSTAGE;
+                            if constexpr (!kWgrad) {
+                                float* sc = reinterpret_cast<float*>(st + C::SA_BYTES + C::SB_BYTES);
+                                sc[0] = b0; sc[1] = b1;
+                            }
+                            const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
+                            mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? C::SB_BYTES : 0));
+                            tma_load_2d(sst, &tmSA, sfull_bar(ss), tl.row0 & ~3, kb0 + j);
+                            if constexpr (kWgrad) tma_load_2d(sst + C::SA_BYTES, &tmSB, sfull_bar(ss), tl.n0, kb0 + j);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        setmaxnreg_inc<232>();
+        // ---------------- promotion + epilogue ----------------
+        const int h = (warp - 4) >> 2;                  // column half
+        const int quad = warp & 3;                      // TMEM lane quadrant
+        const int row = quad * 32 + lane;               // row within the tile
+        constexpr int NC = C::NC;
+        constexpr int CW = 32;
+        float acc[NC];
+        int sit = 0, pit = 0;
+        Tile tl;
+        for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
+            for (int kb = 0; kb < p.KB; ++kb, ++sit, ++pit) {
+                const int ss = sit % C::kSStages;
+                const uint32_t sph = (sit / C::kSStages) & 1;
+                mbar_wait(sfull_bar(ss), sph);
+                const uint8_t* st = smem + C::OFF_SS + ss * C::SSTAGE;
+                const float sa = reinterpret_cast<const float*>(st)[(tl.row0 & 3) + row];
+                float f = 0.0f;
+                if constexpr (!kWgrad) {
+                    f = __fmul_rn(sa, reinterpret_cast<const float*>(st + C::SA_BYTES + C::SB_BYTES)[(h * NC) / 128]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(sempty_bar(ss));
+                }
+                const int pb = pit & 1;
+                const uint32_t pph = (pit >> 1) & 1;
+                mbar_wait(pfull_bar(pb), pph);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + pb * BN + h * NC;
+#pragma unroll
+                for (int c = 0; c < NC / CW; ++c) {
+                    uint32_t r[CW];
+                    FP8BS_TMEM_LD32(taddr + c * CW, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) FP8BS_REG_FENCE(r[j]);
+                    if (c == NC / CW - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(pempty_bar(pb));
+                    }
+                    if constexpr (kWgrad) {
+                        const float4* sbv = reinterpret_cast<const float4*>(st + C::SA_BYTES) + (h * NC + c * CW) / 4;
+#pragma unroll
+                        for (int j4 = 0; j4 < CW / 4; ++j4) {
+                            const float4 b = sbv[j4];
+                            const int j = c * CW + j4 * 4;
+                            acc[j + 0] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 0]), __fmul_rn(sa, b.x), acc[j + 0]);
+                            acc[j + 1] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 1]), __fmul_rn(sa, b.y), acc[j + 1]);
+                            acc[j + 2] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 2]), __fmul_rn(sa, b.z), acc[j + 2]);
+                            acc[j + 3] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 3]), __fmul_rn(sa, b.w), acc[j + 3]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < CW; ++j) acc[c * CW + j] = __fmaf_rn(__uint_as_float(r[j]), f, acc[c * CW + j]);
+                    }
+                }
+                if constexpr (kWgrad) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(sempty_bar(ss));
+                }
+            }
+            // ---------------- epilogue ----------------
+            const int grow = tl.row0 + row;
+            if (grow < tl.row_end) {
+                const int col0 = tl.n0 + h * NC;
+                if constexpr (kOutF32) {
+                    float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
+#pragma unroll
+                    for (int i = 0; i < NC / 4; ++i) {
+                        if (col0 + 4 * i < p.N) {
+                            float4 v = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+                            if (p.accumulate) {
+                                const float4 o = *reinterpret_cast<const float4*>(drow + 4 * i);
+                                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                            }
+                            *reinterpret_cast<float4*>(drow + 4 * i) = v;
+                        }
+                    }
+                } else {
+                    __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.D) + (int64_t)grow * p.ldd + col0;
+#pragma unroll
+                    for (int i = 0; i < NC / 8; ++i) {
+                        if (col0 + 8 * i < p.N) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k], acc[8 * i + 2 * k + 1]);
+                                w[k] = *reinterpret_cast<uint32_t*>(&b2);
+                            }
+                            *reinterpret_cast<uint4*>(drow + 8 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ===========================================================================================
+// host side: tensor maps + launch
+// ===========================================================================================
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
+                     const uint64_t* strides_bytes /* rank-1 */, const uint32_t* box, CUtensorMapSwizzle sw) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    uint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, dt, (cuuint32_t)rank, const_cast<void*>(base), (const cuuint64_t*)dims,
+                     (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool kWgrad, bool kOutF32, bool kGrouped>
+static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
+    using C = Cfg<BN>;
+    const int KB = (int)(a.K / BK);
+    const int64_t rows = a.M;   // total rows of A (total_M for grouped)
+    CUtensorMap tA, tB, tSA, tSB;
+    {
+        uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)rows};
+        uint64_t str[1] = {(uint64_t)a.lda};
+        uint32_t box[2] = {BK, BM};
+        if (!make_map(&tA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            *detail = "cuTensorMapEncodeTiled failed for A"; return cudaErrorInvalidValue;
+        }
+    }
+    if (kGrouped) {
+        uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
+        uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
+        uint32_t box[3] = {BK, BN, 1};
+        if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            *detail = "cuTensorMapEncodeTiled failed for B (grouped)"; return cudaErrorInvalidValue;
+        }
+    } else {
+        uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
+        uint64_t str[1] = {(uint64_t)a.ldb};
+        uint32_t box[2] = {BK, BN};
+        if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            *detail = "cuTensorMapEncodeTiled failed for B"; return cudaErrorInvalidValue;
+        }
+    }
+    {
+        uint64_t dims[2] = {(uint64_t)rows, (uint64_t)KB};
+        uint64_t str[1] = {(uint64_t)a.ldsA * 4};
+        uint32_t box[2] = {C::SA_BOX, 1};
+        if (!make_map(&tSA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.sA, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+            *detail = "cuTensorMapEncodeTiled failed for sA"; return cudaErrorInvalidValue;
+        }
+    }
+    if (kWgrad) {
+        uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)KB};
+        uint64_t str[1] = {(uint64_t)a.ldsB * 4};
+        uint32_t box[2] = {BN, 1};
+        if (!make_map(&tSB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.sB, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+            *detail = "cuTensorMapEncodeTiled failed for sB"; return cudaErrorInvalidValue;
+        }
+    } else {
+        tSB = tSA;
+    }
+    KParams p{};
+    p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
+    p.num_m = (int)((a.M + BM - 1) / BM); p.num_n = (int)((a.N + BN - 1) / BN);
+    p.NB = (int)((a.N + 127) / 128);
+    p.sB = a.sB;
+    if (kGrouped) { p.sb_nb_stride = KB; p.sb_kb_stride = 1; p.sb_expert_stride = (int64_t)p.NB * KB; }
+    else if (a.layout == 0) { p.sb_nb_stride = a.ldsB; p.sb_kb_stride = 1; p.sb_expert_stride = 0; }
+    else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
+    p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
+    p.G = a.G; p.offsets = a.offsets;
+
+    int64_t tiles_ub;
+    if (kGrouped) tiles_ub = ((a.M + BM - 1) / BM + a.G) * (int64_t)p.num_n;
+    else tiles_ub = (int64_t)p.num_m * p.num_n;
+    int grid = (int)(tiles_ub < num_sms() ? tiles_ub : num_sms());
+    if (grid < 1) grid = 1;
+    const int smem = kGrouped ? C::SMEM_GROUPED : C::SMEM_DENSE;
+    auto kern = k_gemm_bs<BN, kWgrad, kOutF32, kGrouped>;
+    static bool attr[64] = {false};   // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    kern<<<grid, 384, smem, st>>>(tA, tB, tSA, tSB, p);
+    return cudaPeekAtLastError();
+}
+
+int gemm_bn_override = 0;   // test hook: force BN (128/256); 0 = heuristic
+
+template <int BN>
+static cudaError_t launch_bn(const GemmArgs& a, cudaStream_t st, const char** detail) {
+    if (a.grouped) {
+        return a.out_f32 ? launch_cfg<BN, false, true, true>(a, st, detail)
+                         : launch_cfg<BN, false, false, true>(a, st, detail);
+    }
+    if (a.layout == 2) return launch_cfg<BN, true, true, false>(a, st, detail);
+    return a.out_f32 ? launch_cfg<BN, false, true, false>(a, st, detail)
+                     : launch_cfg<BN, false, false, false>(a, st, detail);
+}
+
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail) {
+    int bn = gemm_bn_override;
+    if (bn != 128 && bn != 256) bn = (a.N <= 128) ? 128 : 256;
+    return bn == 128 ? launch_bn<128>(a, st, detail) : launch_bn<256>(a, st, detail);
+}
+
+}  // namespace fp8bs

@@ -1,0 +1,35 @@
+// internal.h — declarations shared between the C-ABI layer (api.cu) and the kernel files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fp8bs {
+
+int num_sms();                                   // SM count of the current device (cached per device)
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cudaError_t launch_quant_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
+                                   int64_t ldq, float* s, int64_t lds, cudaStream_t st);
+cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx, uint8_t* qT,
+                                   int64_t ldq, float* sT, int64_t lds, cudaStream_t st);
+cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw, uint8_t* q,
+                                        int64_t ldq, float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT,
+                                        cudaStream_t st);
+
+struct GemmArgs {
+    int layout;              // 0 FPROP, 1 DGRAD, 2 WGRAD
+    int64_t M, N, K;
+    const uint8_t* A; int64_t lda;
+    const float* sA; int64_t ldsA;
+    const uint8_t* B; int64_t ldb;
+    const float* sB; int64_t ldsB;
+    void* D; int out_f32; int64_t ldd; int accumulate;
+    // grouped
+    int grouped; int32_t G; const int64_t* offsets;
+};
+
+// Returns cudaSuccess or the launch error; *detail gets a static message on host-side failures
+// (tensor-map encoding).
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail);
+
+}  // namespace fp8bs

