@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py — DeepSeek-V3 FP8 Linear training step on B200 (BASELINE.json configs[1]).
+
+One STEP = the whole hot path for a Linear W [out=18432, in=7168]
+over T=4096 tokens, synthetic seeded inputs (workloads.py):
+    quantize_act_1x128(X) ; quantize_weight_128x128(W) (+ transposed copy)
+    Fprop  Y  = Xq  . Wq^T          (BF16 out)
+    quantize_act_1x128(dY)
+    Dgrad  dX = dYq . WqT^T         (BF16 out)
+    quantize_act_128x1(dY) ; quantize_act_128x1(X)
+    Wgrad  dW = dYqT . XqT^T        (FP32 out)
+value = 3 * 2*T*in*out GEMM FLOP per step / device time (TFLOP/s), whole job over all ranks.
+Multi-GPU (torchrun): the dense step does not shard -> independent replicas, "scaling": "weak".
+`--workload ep` times the expert-parallel grouped GEMM (BASELINE configs[4]) instead.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload dense|ep]
+
+`--impl reference` times the CPU oracle (oracle/, as it stands) on a bounded sample of the same
+workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "FP8 block-scaled GEMM TFLOPS (% of B200 FP8 peak); quantizer HBM GB/s"
+T_TOK, D_IN, D_OUT = 4096, 7168, 18432
+# CPU sample of the same step (cpu_baseline / --impl reference): 128 tokens x all 7168 inputs x
+# the first CPU_OUT output channels.
+CPU_TOK, CPU_OUT = 128, 2048
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+# ------------------------------------------------------------------------ clocks ----
+class ClockSampler:
+    """NVML sampler of SM clock + throttle reasons while the timed region runs."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k, None): n for k, n in [
+            ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"), ("nvmlClocksEventReasonHwSlowdown", "hw_slowdown"),
+            ("nvmlClocksEventReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+            ("nvmlClocksEventReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+            ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown")] if getattr(nv, k, None)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, n in names.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------- dense step ----
+class DenseStep:
+    """Preallocated buffers + the 8 launches of one FP8 Linear training step."""
+
+    def __init__(self, dev, T=T_TOK, IN=D_IN, OUT=D_OUT, seed=0):
+        import paper_2412_19437_b200 as fp
+        self.fp = fp
+        self.T, self.IN, self.OUT = T, IN, OUT
+        self.h_x = W.gaussian_act(T, IN, seed=seed)                 # BF16 activations
+        self.h_w = W.master_weight(OUT, IN, seed=seed + 1)          # FP32 master weight
+        self.h_dy = W.grad_out(T, OUT, seed=seed + 2)               # BF16 output gradient
+        self.x, self.w, self.dy = self.h_x.to(dev), self.h_w.to(dev), self.h_dy.to(dev)
+        u8, f32, bf = torch.uint8, torch.float32, torch.bfloat16
+        e = lambda *s, dt=u8: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
+        p4 = lambda n: (n + 3) // 4 * 4  # noqa: E731
+        self.xq, self.sx = e(T, IN), e(IN // 128, p4(T), dt=f32)[:, :T]
+        self.wq, self.sw, self.wqT = e(OUT, IN), e(OUT // 128, IN // 128, dt=f32), e(IN, OUT)
+        self.y = e(T, OUT, dt=bf)
+        self.dyq, self.sdy = e(T, OUT), e(OUT // 128, p4(T), dt=f32)[:, :T]
+        self.dx = e(T, IN, dt=bf)
+        self.dyqT, self.sdyT = e(OUT, T), e(T // 128, p4(OUT), dt=f32)[:, :OUT]
+        self.xqT, self.sxT = e(IN, T), e(T // 128, p4(IN), dt=f32)[:, :IN]
+        self.dw = e(OUT, IN, dt=f32)
+        gf = 2.0 * T * IN * OUT
+        B2 = lambda m, k: 2 * m * k + m * k + 4 * m * ((k + 127) // 128)  # noqa: E731  bf16 in, codes + scales out
+        # name -> (callable, kind, algorithmic amount per launch: FLOP for gemm, bytes for quantizers)
+        self.launches = [
+            ("quant_act_1x128(X)", self.q_x, "hbm", B2(T, IN)),
+            ("quant_weight_128x128(W)+T", self.q_w, "hbm", 4 * OUT * IN + 2 * OUT * IN + 4 * (OUT // 128) * (IN // 128)),
+            ("gemm_fprop", self.g_fprop, "tensor", gf),
+            ("quant_act_1x128(dY)", self.q_dy, "hbm", B2(T, OUT)),
+            ("gemm_dgrad", self.g_dgrad, "tensor", gf),
+            ("quant_act_128x1(dY)", self.qt_dy, "hbm", B2(T, OUT)),
+            ("quant_act_128x1(X)", self.qt_x, "hbm", B2(T, IN)),
+            ("gemm_wgrad", self.g_wgrad, "tensor", gf),
+        ]
+        self.flops = 3 * gf
+        self.h2d_bytes = self.h_x.numel() * 2 + self.h_w.numel() * 4 + self.h_dy.numel() * 2
+        self.d2h_bytes = self.y.numel() * 2 + self.dx.numel() * 2 + self.dw.numel() * 4
+
+    def q_x(self):
+        self.fp.quantize_act_1x128(self.x, self.xq, self.sx)
+
+    def q_w(self):
+        self.fp.quantize_weight_128x128(self.w, True, self.wq, self.sw, self.wqT)
+
+    def g_fprop(self):
+        self.fp.gemm(self.fp.FPROP, self.xq, self.sx, self.wq, self.sw, out=self.y)
+
+    def q_dy(self):
+        self.fp.quantize_act_1x128(self.dy, self.dyq, self.sdy)
+
+    def g_dgrad(self):
+        self.fp.gemm(self.fp.DGRAD, self.dyq, self.sdy, self.wqT, self.sw, out=self.dx)
+
+    def qt_dy(self):
+        self.fp.quantize_act_128x1(self.dy, self.dyqT, self.sdyT)
+
+    def qt_x(self):
+        self.fp.quantize_act_128x1(self.x, self.xqT, self.sxT)
+
+    def g_wgrad(self):
+        self.fp.gemm(self.fp.WGRAD, self.dyqT, self.sdyT, self.xqT, self.sxT, out=self.dw)
+
+    def run(self):
+        for _, fn, _, _ in self.launches:
+            fn()
+
+
+def cpu_sample_step():
+    """The same step restricted to CPU_TOK tokens x CPU_OUT output channels, on the CPU oracle.
+    Returns (seconds, GEMM FLOP)."""
+    import oracle
+    x = W.gaussian_act(T_TOK, D_IN, seed=0)[:CPU_TOK].contiguous()
+    w = W.master_weight(CPU_OUT, D_IN, seed=1)
+    dy = W.grad_out(CPU_TOK, CPU_OUT, seed=2)
+    t0 = time.perf_counter()
+    qx, sx = oracle.quantize_act_1x128(x)
+    qw, sw, qwT = oracle.quantize_weight_128x128(w)
+    oracle.gemm(oracle.FPROP, qx, sx, qw, sw)
+    qdy, sdy = oracle.quantize_act_1x128(dy)
+    oracle.gemm(oracle.DGRAD, qdy, sdy, qwT, sw)
+    qdyT, sdyT = oracle.quantize_act_128x1(dy)
+    qxT, sxT = oracle.quantize_act_128x1(x)
+    oracle.gemm(oracle.WGRAD, qdyT, sdyT, qxT, sxT)
+    return time.perf_counter() - t0, 3 * 2.0 * CPU_TOK * D_IN * CPU_OUT
+
+
+def cpu_baseline_block(min_seconds=10.0):
+    """Time the oracle on repeated samples until at least min_seconds of CPU work."""
+    import oracle
+    dt, fl = 0.0, 0.0
+    while dt < min_seconds:
+        d, f = cpu_sample_step()
+        dt += d
+        fl += f
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"the C1 step restricted to {CPU_TOK} tokens x {D_IN} in x {CPU_OUT} out channels "
+                      f"(all 8 stages: 3 quantizers + weight quantizer + Fprop/Dgrad/Wgrad FP64 oracle GEMMs), "
+                      f"{fl / 1e9:.2f} GFLOP in {dt:.2f} s"}
+
+
+# ------------------------------------------------------------------------ main ----
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_sample_step()
+    t, f = 0.0, 0.0
+    for _ in range(args.steps):
+        d, fl = cpu_sample_step()
+        t += d
+        f += fl
+    import oracle
+    v = f / t / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(args, world),
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": f"each step: the C1 step restricted to {CPU_TOK} tokens x {D_IN} in x "
+                                       f"{CPU_OUT} out channels on the CPU oracle"},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config_block(args, world):
+    if args.workload == "ep":
+        return {"workload": "C4 expert-parallel grouped GEMM: 256 experts (K=7168, N=2048) sharded over ranks, "
+                            "65536 tokens x top-8, skewed load", "parallelism": f"ep{world}",
+                "l2": "inputs larger than L2"}
+    return {"workload": "C1 dense FP8 Linear training step (quantize + Fprop/Dgrad/Wgrad), BASELINE configs[1]",
+            "tokens": T_TOK, "in": D_IN, "out": D_OUT, "global_batch": T_TOK * world,
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "inputs larger than L2 (738 MB read per step: X, W, dY)"}
+
+
+def time_dense(args, world, rank, dev):
+    peaks = load_peaks()
+    st = DenseStep(dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        st.run()
+    torch.cuda.synchronize()
+    nL = len(st.launches)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nL)]
+          for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            for i, (_, fn, _, _) in enumerate(st.launches):
+                ev[k][i][0].record(stream)
+                fn()
+                ev[k][i][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_local = start.elapsed_time(stop)
+    ms = max_over_ranks(ms_local, world, dev)
+    per = {}
+    for i, (name, _, kind, amount) in enumerate(st.launches):
+        d = statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
+        if kind == "tensor":
+            ach = amount / (d * 1e-3) / 1e12
+            peak = 2.0 * peaks["bf16_tflops"]       # FP8 = 2x BF16 (guide's nominal ratio)
+            per[name] = {"ms": d, "achieved": ach, "unit": "TFLOP/s", "peak": peak, "frac": ach / peak}
+        else:
+            ach = amount / (d * 1e-3) / 1e9
+            per[name] = {"ms": d, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]}
+    dom = max(per, key=lambda n: per[n]["ms"])
+    dk = next(l for l in st.launches if l[0] == dom)
+    roof = {"kernel": dom, "bound": "tensor" if dk[2] == "tensor" else "hbm", "achieved": per[dom]["achieved"],
+            "peak": per[dom]["peak"], "unit": per[dom]["unit"], "frac": per[dom]["frac"], "traffic": None,
+            "peak_src": f"{peaks['src']}: " + ("2 x bf16_tflops (burst) of MEASURED_PEAKS.json" if dk[2] == "tensor"
+                                               else "hbm_gbs of MEASURED_PEAKS.json"),
+            "share_of_step": per[dom]["ms"] * args.steps / (ms_local)}
+    value = world * st.flops * args.steps / (ms * 1e-3) / 1e12
+    gemm_ms = sum(per[n]["ms"] for n in per if n.startswith("gemm"))
+    q_ms = sum(per[n]["ms"] for n in per if not n.startswith("gemm"))
+    q_bytes = sum(l[3] for l in st.launches if l[2] == "hbm")
+    result = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "e4m3", "data": "synthetic", "config": config_block(args, world),
+        "roofline": roof, "clocks": clk.summary(), "gpu_launches": nL * args.steps,
+        "gemm_tflops": st.flops / (gemm_ms * 1e-3) / 1e12, "gemm_frac_fp8_peak_4500": st.flops / (gemm_ms * 1e-3) / 4.5e15,
+        "quantizer_gbs": q_bytes / (q_ms * 1e-3) / 1e9, "quantizer_frac_hbm": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "kernels": per,
+    }
+    if args.e2e:
+        result["e2e"] = time_e2e(args, world, st, dev)
+    return result
+
+
+def time_e2e(args, world, st, dev):
+    """Same metric through the public API with host buffers: every step copies X, W, dY from
+    pinned host memory, runs the 8 launches, and copies Y, dX, dW back to pinned host memory."""
+    hx, hw, hdy = st.h_x.pin_memory(), st.h_w.pin_memory(), st.h_dy.pin_memory()
+    hy = torch.empty(st.y.shape, dtype=st.y.dtype).pin_memory()
+    hdx = torch.empty(st.dx.shape, dtype=st.dx.dtype).pin_memory()
+    hdw = torch.empty(st.dw.shape, dtype=st.dw.dtype).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        st.x.copy_(hx, non_blocking=True)
+        st.w.copy_(hw, non_blocking=True)
+        st.dy.copy_(hdy, non_blocking=True)
+        st.run()
+        hy.copy_(st.y, non_blocking=True)
+        hdx.copy_(st.dx, non_blocking=True)
+        hdw.copy_(st.dw, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    n = max(2, args.steps // 4)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(n):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(a.elapsed_time(b), world, dev)
+    return {"value": world * st.flops * n / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": n,
+            "h2d_bytes_per_step": st.h2d_bytes, "d2h_bytes_per_step": st.d2h_bytes,
+            "ms_per_step": ms / n}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="dense", choices=["dense", "ep"])
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if args.workload == "ep":
+        from paper_2412_19437_b200 import ep
+        result = ep.bench(args, world, rank, dev, barrier, max_over_ranks, ClockSampler, load_peaks)
+        result["config"] = config_block(args, world)
+        result["metric"] = METRIC
+    else:
+        result = time_dense(args, world, rank, dev)
+    if rank == 0:
+        if args.cpu and world == 1:
+            result["cpu_baseline"] = cpu_baseline_block()
+        print(json.dumps(result))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -3,38 +3,49 @@
 // What it computes (§3.3.2; include/fp8bs.h):
 //   D[i,j] (+)= sum_kb  sA(kb,i) * sB(kb,j) * P_kb[i,j],   P_kb = sum_{c in kb} dec(A[i,c]) dec(B[j,c])
 // with one scale per N_C = 128 contraction elements.  The paper (H800) promotes WGMMA partials
-// to CUDA-core registers every 128 elements; here the promotion interval is the same (it is
-// forced by the per-128 scales) but the machinery is Blackwell's:
-//   * TMA (SWIZZLE_128B) stages A [128 x 128] and B [BN x 128] K-blocks into a smem ring;
+// to CUDA-core registers every 128 elements; here the promotion interval is the same (forced by
+// the per-128 scales) but the machinery is Blackwell's:
+//   * TMA (SWIZZLE_128B) stages A and B K-blocks (128 wide) into a shared-memory ring;
 //   * one thread issues 4x tcgen05.mma.kind::f8f6f4 (K = 32 each) per K-block into a FRESH
 //     TMEM buffer P (FP32; double-buffered so the tensor core runs ahead of the promotion);
-//   * 8 promotion warps read P with tcgen05.ld, multiply by sA(kb,i)*sB(kb,j) and accumulate
-//     in registers (FP32), then write BF16 (RNE) or FP32 (optionally += for Wgrad);
+//   * 16 promotion warps per CTA read P with tcgen05.ld, multiply by sA(kb,i)*sB(kb,j) and
+//     accumulate in registers with packed FFMA2, then write BF16 (RNE) or FP32 (+= for Wgrad);
 //   * a scale warp streams sA (and Wgrad's per-column sB) with TMA into its own ring.
-// Warp roles (384 threads): w0 TMA A/B producer, w1 MMA issuer, w2 TMEM allocator, w3 scale
-// producer, w4..w11 promotion + epilogue (warpgroup h owns columns [h*BN/2, (h+1)*BN/2)).
-// Persistent CTAs walk a static tile schedule; the grouped (MoE) variant maps tiles to
+// kPair = true: a cluster of 2 CTAs on a TPC runs tcgen05.mma.cta_group::2 with M = 256 (128 rows
+// per CTA) and N = BN: each CTA stages its own 128 rows of A and BN/2 rows of B, so per-SM
+// shared-memory traffic per MAC halves versus one CTA (the 1-CTA 128x256 tile measured ~53%
+// tensor-pipe activity, shared-memory-bandwidth bound).  The leader CTA
+// issues the MMAs; both CTAs' TMA loads complete on the leader's barrier; commits multicast to
+// both CTAs; promotion warps release a TMEM buffer by arriving on the leader's barrier.
+// Warp roles (640 threads): w0 TMA A/B producer, w1 MMA issuer, w2 TMEM allocator, w3 scale
+// producer, w4..w19 promotion + epilogue (warpgroup h owns columns [h*BN/4, (h+1)*BN/4)).
+// Persistent clusters walk a static tile schedule; the grouped (MoE) variant maps tiles to
 // (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "sm100.cuh"
 #include "internal.h"
 
 namespace fp8bs {
 
-constexpr int BM = 128, BK = 128;
+constexpr int BM = 128, BK = 128;     // rows per CTA, K-block (= N_C)
 constexpr int kMaxGroups = 1024;
 
-template <int BN>
+template <int BN, bool kPair>
 struct Cfg {
-    static constexpr int kStages = BN == 256 ? 4 : 6;
-    static constexpr int kSStages = 8;
+    static constexpr int CS = kPair ? 2 : 1;                // CTAs per cluster
+    static constexpr int ROWS = BM * CS;                    // rows per cluster tile
+    static constexpr int BROWS = kPair ? BN / 2 : BN;       // B rows staged per CTA
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = BN * BK;
+    static constexpr int B_BYTES = BROWS * BK;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    // sA box: BM + 4 floats starting at the 4-aligned row at or below row0 (a TMA box must start
-    // 16-byte aligned in its inner dimension; grouped tiles start at arbitrary rows).
+    static constexpr int kStages = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
+    static constexpr int kSStages = 8;
+    // sA box: BM + 4 floats starting at the 4-aligned row at or below the CTA's first row (a TMA
+    // box must start 16-byte aligned in its inner dimension; grouped tiles start at any row).
     static constexpr int SA_BOX = BM + 4;
     static constexpr int SA_BYTES = 640;                    // >= SA_BOX * 4, multiple of 128
     static constexpr int SB_BYTES = BN * 4;                 // WGRAD per-column scales
@@ -42,7 +53,13 @@ struct Cfg {
     static constexpr int SSTAGE = SA_BYTES + SB_BYTES + 128;
     static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int NC = BN / 2;                       // columns per promotion thread
+    // 4 promotion warpgroups (16 warps): TMEM->register bandwidth and FFMA2 issue both scale with
+    // the number of warps (tools/microbench.cu: 322 B/clk at 8 warps, ~470 at 16).
+    static constexpr int NWG = 4;
+    static constexpr int THREADS = 128 * (1 + NWG);
+    static constexpr int NC = BN / NWG;                     // columns per promotion thread
+    static constexpr int CW = 16;                           // TMEM load width (columns)
+    static constexpr int REG_OTHER = 40, REG_PROMO = 104;   // setmaxnreg split of the 96 x 640 pool
     static constexpr int OFF_SS = kStages * STAGE;
     static constexpr int OFF_BAR = OFF_SS + kSStages * SSTAGE;
     static constexpr int NBAR = 2 * kStages + 2 * kSStages + 4;
@@ -59,18 +76,22 @@ struct KParams {
     int NB;                       // ceil(N/128)
     void* D; int64_t ldd; int accumulate;
     int G; const int64_t* offsets;
+    int debug;                    // experiments only (FP8BS_GEMM_DEBUG): 1 skip promotion math,
+                                  // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident)
 };
 
-struct Tile { int row0, row_end, n0, e; };
+struct Tile { int row0, row_end, n0, e; };   // row0: first row of the CLUSTER tile
 
+template <int ROWS>
 __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
     if (t >= p.num_m * p.num_n) return false;
     const int m = t % p.num_m, n = t / p.num_m;
-    tl.row0 = m * BM; tl.row_end = p.M; tl.n0 = n; tl.e = 0;   // n0 is scaled by BN by the caller
+    tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n; tl.e = 0;   // n0 is scaled by BN by the caller
     return true;
 }
 
 // cum[e] = number of tiles of experts < e; off[e] = first row of expert e.
+template <int ROWS>
 __device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cum, const int* off, int t, Tile& tl) {
     if (t >= cum[p.G]) return false;
     int lo = 0, hi = p.G;                       // find e: cum[e] <= t < cum[e+1]
@@ -80,21 +101,19 @@ __device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cu
     }
     const int e = lo;
     const int seg = off[e + 1] - off[e];
-    const int mt = (seg + BM - 1) / BM;
+    const int mt = (seg + ROWS - 1) / ROWS;
     const int local = t - cum[e];
     const int m = local % mt, n = local / mt;
-    tl.row0 = off[e] + m * BM; tl.row_end = off[e + 1]; tl.n0 = n; tl.e = e;
+    tl.row0 = off[e] + m * ROWS; tl.row_end = off[e + 1]; tl.n0 = n; tl.e = e;
     return true;
 }
 
-#define FP8BS_REG_FENCE(r) asm volatile("" : "+r"(r))
-
-template <int BN, bool kWgrad, bool kOutF32, bool kGrouped>
-__global__ void __launch_bounds__(384, 1)
+template <int BN, bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
+__global__ void __launch_bounds__(Cfg<BN, kPair>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
           const KParams p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, kPair>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -110,21 +129,26 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int* off = cum + (kMaxGroups + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+    const int cid = blockIdx.x / C::CS, ncl = gridDim.x / C::CS;
 
     if (threadIdx.x == 32) {
         for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
-        for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), 8); }
-        for (int b = 0; b < 2; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 8); }
+        for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), 4 * C::NWG); }
+        for (int b = 0; b < 2; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 4 * C::NWG * C::CS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmSA);
         if (kWgrad) tma_prefetch_desc(&tmSB);
     }
-    if (warp == 2) tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_slot));
+    if (warp == 2) {
+        if constexpr (kPair) tmem_alloc_pair<C::TMEM_COLS>(smem_u32(tmem_slot));
+        else tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_slot));
+    }
     if constexpr (kGrouped) {
         if (warp == 4) {
-            // tile prefix over experts: cum[e+1] = cum[e] + ceil(M_e/128) * num_n
+            // tile prefix over experts: cum[e+1] = cum[e] + ceil(M_e/ROWS) * num_n
             const int G = p.G;
             const int per = (G + 31) / 32;
             const int e0 = lane * per, e1 = min(G, e0 + per);
@@ -133,7 +157,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int64_t a = p.offsets[e], b = p.offsets[e + 1];
                 const int seg = b > a ? (int)(b - a) : 0;
                 off[e] = (int)a;
-                local += ((seg + BM - 1) / BM) * p.num_n;
+                local += ((seg + C::ROWS - 1) / C::ROWS) * p.num_n;
             }
             int incl = local;
 #pragma unroll
@@ -147,48 +171,59 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int a = off[e];
                 const int64_t b = p.offsets[e + 1];
                 const int seg = b > a ? (int)(b - a) : 0;
-                run += ((seg + BM - 1) / BM) * p.num_n;
+                run += ((seg + C::ROWS - 1) / C::ROWS) * p.num_n;
             }
             if (lane == 31) { cum[G] = incl; off[G] = (int)p.offsets[G]; }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair) cluster_sync();        // peer barriers initialised before any remote arrive / TMA
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     auto next_tile = [&](int t, Tile& tl) -> bool {
         bool ok;
-        if constexpr (kGrouped) ok = get_tile_grouped(p, cum, off, t, tl);
-        else ok = get_tile_dense(p, t, tl);
+        if constexpr (kGrouped) ok = get_tile_grouped<C::ROWS>(p, cum, off, t, tl);
+        else ok = get_tile_dense<C::ROWS>(p, t, tl);
         tl.n0 *= BN;
         return ok;
     };
 
     if (warp < 4) {
-        setmaxnreg_dec<40>();
+        setmaxnreg_dec<C::REG_OTHER>();
         if (warp == 0 && lane == 0) {
-            // ---------------- TMA producer: A and B K-blocks ----------------
+            // ---------------- TMA producer: A and B K-blocks (this CTA's halves) ----------------
             int it = 0;
             Tile tl;
-            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+            for (int t = cid; next_tile(t, tl); t += ncl) {
+                const int arow = tl.row0 + (int)rank * BM;
+                const int brow = tl.n0 + (int)rank * C::BROWS;
                 for (int kb = 0; kb < p.KB; ++kb, ++it) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
-                    mbar_arrive_expect_tx(full_bar(s), C::STAGE);
                     const uint32_t sa = sbase + s * C::STAGE;
-                    tma_load_2d(sa, &tmA, full_bar(s), kb * BK, tl.row0);
-                    if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kb * BK, tl.n0, tl.e);
-                    else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kb * BK, tl.n0);
+                    const int kc = (p.debug & 4) ? 0 : kb * BK;
+                    if constexpr (kPair) {
+                        if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::STAGE);
+                        tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
+                        if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
+                        else tma_load_2d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
+                    } else {
+                        mbar_arrive_expect_tx(full_bar(s), C::STAGE);
+                        tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
+                        if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
+                        else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
+                    }
                 }
             }
-        } else if (warp == 1 && lane == 0) {
-            // ---------------- MMA issuer ----------------
-            constexpr uint32_t idesc = idesc_e4m3_f32(BM, BN);
+        } else if (warp == 1 && lane == 0 && rank == 0) {
+            // ---------------- MMA issuer (leader CTA) ----------------
+            constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, BN);
             int it = 0, pit = 0;
             Tile tl;
-            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+            for (int t = cid; next_tile(t, tl); t += ncl) {
                 for (int kb = 0; kb < p.KB; ++kb, ++it, ++pit) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
@@ -201,19 +236,28 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + C::A_BYTES);
                     const uint32_t d = tmem_base + pb * BN;
 #pragma unroll
-                    for (int k = 0; k < BK / 32; ++k)
-                        mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
-                    mma_commit(empty_bar(s));
-                    mma_commit(pfull_bar(pb));
+                    for (int k = 0; k < BK / 32; ++k) {
+                        if (p.debug & 2) break;
+                        if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                        else mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                    }
+                    if constexpr (kPair) {
+                        mma_commit_pair(empty_bar(s), 3);
+                        mma_commit_pair(pfull_bar(pb), 3);
+                    } else {
+                        mma_commit(empty_bar(s));
+                        mma_commit(pfull_bar(pb));
+                    }
                 }
             }
         } else if (warp == 3) {
-            // ---------------- scale producer ----------------
+            // ---------------- scale producer (this CTA's rows) ----------------
             int sit = 0;
             Tile tl;
-            for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+            for (int t = cid; next_tile(t, tl); t += ncl) {
                 const float* sbp = p.sB;
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
+                const int arow = tl.row0 + (int)rank * BM;
                 const int nb0 = tl.n0 / 128;
                 for (int kb0 = 0; kb0 < p.KB; kb0 += 32) {
                     float v0 = 0.0f, v1 = 0.0f;
@@ -239,7 +283,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                             }
                             const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
                             mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? C::SB_BYTES : 0));
-                            tma_load_2d(sst, &tmSA, sfull_bar(ss), tl.row0 & ~3, kb0 + j);
+                            tma_load_2d(sst, &tmSA, sfull_bar(ss), arow & ~3, kb0 + j);
                             if constexpr (kWgrad) tma_load_2d(sst + C::SA_BYTES, &tmSB, sfull_bar(ss), tl.n0, kb0 + j);
                         }
                     }
@@ -248,28 +292,31 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
     } else {
-        setmaxnreg_inc<232>();
+        setmaxnreg_inc<C::REG_PROMO>();
         // ---------------- promotion + epilogue ----------------
-        const int h = (warp - 4) >> 2;                  // column half
+        const int h = (warp - 4) >> 2;                  // promotion warpgroup = column slice
         const int quad = warp & 3;                      // TMEM lane quadrant
-        const int row = quad * 32 + lane;               // row within the tile
+        const int row = quad * 32 + lane;               // row within this CTA's 128
         constexpr int NC = C::NC;
-        constexpr int CW = 32;
+        constexpr int CW = C::CW;
+        const uint32_t pempty_addr0 = kPair ? mapa_shared(pempty_bar(0), 0) : pempty_bar(0);
         float acc[NC];
         int sit = 0, pit = 0;
         Tile tl;
-        for (int t = blockIdx.x; next_tile(t, tl); t += gridDim.x) {
+        for (int t = cid; next_tile(t, tl); t += ncl) {
+            const int arow = tl.row0 + (int)rank * BM;
 #pragma unroll
             for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
             for (int kb = 0; kb < p.KB; ++kb, ++sit, ++pit) {
                 const int ss = sit % C::kSStages;
                 const uint32_t sph = (sit / C::kSStages) & 1;
                 mbar_wait(sfull_bar(ss), sph);
-                const uint8_t* st = smem + C::OFF_SS + ss * C::SSTAGE;
-                const float sa = reinterpret_cast<const float*>(st)[(tl.row0 & 3) + row];
-                float f = 0.0f;
+                const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
+                const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
+                float2 f2 = make_float2(0.0f, 0.0f);
                 if constexpr (!kWgrad) {
-                    f = __fmul_rn(sa, reinterpret_cast<const float*>(st + C::SA_BYTES + C::SB_BYTES)[(h * NC) / 128]);
+                    const float f = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + C::SB_BYTES + 4u * ((h * NC) / 128)));
+                    f2 = make_float2(f, f);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(sempty_bar(ss));
                 }
@@ -278,32 +325,54 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 mbar_wait(pfull_bar(pb), pph);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + pb * BN + h * NC;
+                if (p.debug & 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (kPair) mbar_arrive_cluster(pempty_addr0 + 8u * pb);
+                        else mbar_arrive(pempty_bar(pb));
+                    }
+                    if constexpr (kWgrad) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(sempty_bar(ss));
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int c = 0; c < NC / CW; ++c) {
                     uint32_t r[CW];
-                    FP8BS_TMEM_LD32(taddr + c * CW, r);
+                    if constexpr (CW == 32) FP8BS_TMEM_LD32(taddr + c * CW, r);
+                    else FP8BS_TMEM_LD16(taddr + c * CW, r);
                     tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < CW; ++j) FP8BS_REG_FENCE(r[j]);
                     if (c == NC / CW - 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(pempty_bar(pb));
+                        if (lane == 0) {
+                            if constexpr (kPair) mbar_arrive_cluster(pempty_addr0 + 8u * pb);
+                            else mbar_arrive(pempty_bar(pb));
+                        }
                     }
                     if constexpr (kWgrad) {
-                        const float4* sbv = reinterpret_cast<const float4*>(st + C::SA_BYTES) + (h * NC + c * CW) / 4;
+                        const float2 sa2 = make_float2(sa, sa);
 #pragma unroll
                         for (int j4 = 0; j4 < CW / 4; ++j4) {
-                            const float4 b = sbv[j4];
+                            const float4 b = lds_f32x4(sst + C::SA_BYTES + 4u * (h * NC + c * CW + j4 * 4));
                             const int j = c * CW + j4 * 4;
-                            acc[j + 0] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 0]), __fmul_rn(sa, b.x), acc[j + 0]);
-                            acc[j + 1] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 1]), __fmul_rn(sa, b.y), acc[j + 1]);
-                            acc[j + 2] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 2]), __fmul_rn(sa, b.z), acc[j + 2]);
-                            acc[j + 3] = __fmaf_rn(__uint_as_float(r[j4 * 4 + 3]), __fmul_rn(sa, b.w), acc[j + 3]);
+                            const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
+                            const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
+                            float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 0]), __uint_as_float(r[j4 * 4 + 1])), fa,
+                                                   make_float2(acc[j + 0], acc[j + 1]));
+                            float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 2]), __uint_as_float(r[j4 * 4 + 3])), fb,
+                                                   make_float2(acc[j + 2], acc[j + 3]));
+                            acc[j + 0] = a0.x; acc[j + 1] = a0.y; acc[j + 2] = a1.x; acc[j + 3] = a1.y;
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < CW; ++j) acc[c * CW + j] = __fmaf_rn(__uint_as_float(r[j]), f, acc[c * CW + j]);
+                        for (int j = 0; j < CW; j += 2) {
+                            float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
+                                                  make_float2(acc[c * CW + j], acc[c * CW + j + 1]));
+                            acc[c * CW + j] = a.x; acc[c * CW + j + 1] = a.y;
+                        }
                     }
                 }
                 if constexpr (kWgrad) {
@@ -312,7 +381,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
             }
             // ---------------- epilogue ----------------
-            const int grow = tl.row0 + row;
+            const int grow = arow + row;
             if (grow < tl.row_end) {
                 const int col0 = tl.n0 + h * NC;
                 if constexpr (kOutF32) {
@@ -348,9 +417,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair) cluster_sync();        // no CTA leaves while its peer may still arrive on it
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<C::TMEM_COLS>(tmem_base);
+        if constexpr (kPair) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+        else tmem_dealloc<C::TMEM_COLS>(tmem_base);
     }
 }
 
@@ -383,9 +454,9 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool kWgrad, bool kOutF32, bool kGrouped>
+template <int BN, bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, kPair>;
     const int KB = (int)(a.K / BK);
     const int64_t rows = a.M;   // total rows of A (total_M for grouped)
     CUtensorMap tA, tB, tSA, tSB;
@@ -400,14 +471,14 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     if (kGrouped) {
         uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
-        uint32_t box[3] = {BK, BN, 1};
+        uint32_t box[3] = {BK, (uint32_t)C::BROWS, 1};
         if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
             *detail = "cuTensorMapEncodeTiled failed for B (grouped)"; return cudaErrorInvalidValue;
         }
     } else {
         uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
         uint64_t str[1] = {(uint64_t)a.ldb};
-        uint32_t box[2] = {BK, BN};
+        uint32_t box[2] = {BK, (uint32_t)C::BROWS};
         if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
             *detail = "cuTensorMapEncodeTiled failed for B"; return cudaErrorInvalidValue;
         }
@@ -432,7 +503,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     }
     KParams p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
-    p.num_m = (int)((a.M + BM - 1) / BM); p.num_n = (int)((a.N + BN - 1) / BN);
+    p.num_m = (int)((a.M + C::ROWS - 1) / C::ROWS); p.num_n = (int)((a.N + BN - 1) / BN);
     p.NB = (int)((a.N + 127) / 128);
     p.sB = a.sB;
     if (kGrouped) { p.sb_nb_stride = KB; p.sb_kb_stride = 1; p.sb_expert_stride = (int64_t)p.NB * KB; }
@@ -440,14 +511,20 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.G = a.G; p.offsets = a.offsets;
+    {
+        static int dbg = -1;
+        if (dbg < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); dbg = e ? atoi(e) : 0; }
+        p.debug = dbg;
+    }
 
     int64_t tiles_ub;
-    if (kGrouped) tiles_ub = ((a.M + BM - 1) / BM + a.G) * (int64_t)p.num_n;
+    if (kGrouped) tiles_ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;
     else tiles_ub = (int64_t)p.num_m * p.num_n;
-    int grid = (int)(tiles_ub < num_sms() ? tiles_ub : num_sms());
-    if (grid < 1) grid = 1;
+    const int64_t max_clusters = num_sms() / C::CS;
+    int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
+    if (clusters < 1) clusters = 1;
     const int smem = kGrouped ? C::SMEM_GROUPED : C::SMEM_DENSE;
-    auto kern = k_gemm_bs<BN, kWgrad, kOutF32, kGrouped>;
+    auto kern = k_gemm_bs<BN, kWgrad, kOutF32, kGrouped, kPair>;
     static bool attr[64] = {false};   // per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -456,27 +533,49 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
-    kern<<<grid, 384, smem, st>>>(tA, tB, tSA, tSB, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * C::CS);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C::CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, p);
+    if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
 }
 
-int gemm_bn_override = 0;   // test hook: force BN (128/256); 0 = heuristic
+int gemm_variant_override = 0;   // test hook: 1 = 1-CTA BN=128, 2 = 1-CTA BN=256, 3 = CTA pair BN=256
 
-template <int BN>
-static cudaError_t launch_bn(const GemmArgs& a, cudaStream_t st, const char** detail) {
+template <int BN, bool kPair>
+static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
     if (a.grouped) {
-        return a.out_f32 ? launch_cfg<BN, false, true, true>(a, st, detail)
-                         : launch_cfg<BN, false, false, true>(a, st, detail);
+        return a.out_f32 ? launch_cfg<BN, false, true, true, kPair>(a, st, detail)
+                         : launch_cfg<BN, false, false, true, kPair>(a, st, detail);
     }
-    if (a.layout == 2) return launch_cfg<BN, true, true, false>(a, st, detail);
-    return a.out_f32 ? launch_cfg<BN, false, true, false>(a, st, detail)
-                     : launch_cfg<BN, false, false, false>(a, st, detail);
+    if (a.layout == 2) return launch_cfg<BN, true, true, false, kPair>(a, st, detail);
+    return a.out_f32 ? launch_cfg<BN, false, true, false, kPair>(a, st, detail)
+                     : launch_cfg<BN, false, false, false, kPair>(a, st, detail);
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    int bn = gemm_bn_override;
-    if (bn != 128 && bn != 256) bn = (a.N <= 128) ? 128 : 256;
-    return bn == 128 ? launch_bn<128>(a, st, detail) : launch_bn<256>(a, st, detail);
+    static int env_variant = -1;   // FP8BS_GEMM_VARIANT (experiments only; read once)
+    if (env_variant < 0) {
+        const char* e = getenv("FP8BS_GEMM_VARIANT");
+        env_variant = e ? atoi(e) : 0;
+    }
+    int v = env_variant ? env_variant : gemm_variant_override;
+    if (v < 1 || v > 3) {
+        if (a.N <= 128) v = 1;
+        else if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 3 : 2;   // ~128-row experts: 1-CTA tiles
+        else v = (a.M <= 128) ? 2 : 3;
+    }
+    if (v == 1) return launch_v<128, false>(a, st, detail);
+    if (v == 2) return launch_v<256, false>(a, st, detail);
+    return launch_v<256, true>(a, st, detail);
 }
 
 }  // namespace fp8bs

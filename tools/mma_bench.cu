@@ -1,0 +1,114 @@
+// tools/mma_bench.cu — tcgen05.mma kind::f8f6f4 peak throughput with operands resident in smem
+// (no TMA), for 1-CTA (M=128) and CTA-pair (M=256) shapes.  Experiments only, not product code.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_bench tools/mma_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../paper_2412_19437_b200/csrc/sm100.cuh"
+
+using namespace fp8bs;
+
+// iters K-blocks of 4 MMAs each; buffers alternate between TMEM columns [0,N) and [N,2N);
+// commit every kb to an mbarrier; the issuing thread waits on the commit of kb-depth (depth in-flight).
+template <int N, bool kPair, int DEPTH>
+__global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bars[8];
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = kPair ? cluster_ctarank() : 0;
+    const uint32_t sa = smem_u32(smem);
+    const uint32_t sb = sa + 16384;
+    for (int i = threadIdx.x; i < (16384 + N * 128 / (kPair ? 2 : 1)) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = 0x38383838u;   // E4M3 1.0
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&bars[i]), 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        if constexpr (kPair) tmem_alloc_pair<512>(smem_u32(&slot));
+        else tmem_alloc<512>(smem_u32(&slot));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (kPair) cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (warp == 0 && lane == 0 && rank == 0) {
+        constexpr uint32_t idesc = idesc_e4m3_f32(kPair ? 256 : 128, N);
+        const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sb);
+        unsigned long long t0 = clock64();
+        for (int kb = 0; kb < iters; ++kb) {
+            if (kb >= DEPTH) mbar_wait(smem_u32(&bars[(kb - DEPTH) & 7]), ((kb - DEPTH) >> 3) & 1);
+            const uint32_t d = tmem + (kb & 1) * N;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0);
+                else mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0);
+            }
+            if constexpr (kPair) mma_commit_pair(smem_u32(&bars[kb & 7]), 1);
+            else mma_commit(smem_u32(&bars[kb & 7]));
+        }
+        for (int kb = iters - DEPTH > 0 ? iters - DEPTH : 0; kb < iters; ++kb)
+            mbar_wait(smem_u32(&bars[kb & 7]), (kb >> 3) & 1);
+        unsigned long long t1 = clock64();
+        cyc[blockIdx.x / (kPair ? 2 : 1)] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (kPair) cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        if constexpr (kPair) tmem_dealloc_pair<512>(tmem);
+        else tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int N, bool kPair, int DEPTH>
+static void run(const char* name, int iters) {
+    auto kern = k_mma<N, kPair, DEPTH>;
+    const int smem = 1024 + 16384 + N * 128;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long* dcyc;
+    cudaMalloc(&dcyc, 148 * 8);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(148);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kPair ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaLaunchKernelEx(&cfg, kern, iters, dcyc);
+    cudaEventRecord(a);
+    cudaLaunchKernelEx(&cfg, kern, iters, dcyc);
+    cudaEventRecord(b);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    unsigned long long h[148];
+    cudaMemcpy(h, dcyc, sizeof h, cudaMemcpyDeviceToHost);
+    const int nunits = kPair ? 74 : 148;
+    double avg = 0; for (int i = 0; i < nunits; ++i) avg += h[i]; avg /= nunits;
+    const double macs_per_kb_per_sm = 128.0 * N * 128;    // per SM (pair: each SM does 128 rows)
+    const double flops = 2.0 * macs_per_kb_per_sm * iters * 148;
+    printf("%-28s N=%3d depth=%d: %7.1f cyc/kb  (ideal %d)  %6.0f MAC/clk/SM  %7.1f TFLOP/s (events)\n", name, N, DEPTH,
+           avg / iters, (int)(macs_per_kb_per_sm / 8192), macs_per_kb_per_sm * iters / avg, flops / (ms * 1e-3) / 1e12);
+}
+
+int main() {
+    const int it = 20000;
+    run<256, false, 1>("1-CTA M=128", it);
+    run<256, false, 2>("1-CTA M=128", it);
+    run<256, false, 4>("1-CTA M=128", it);
+    run<128, false, 4>("1-CTA M=128", it);
+    run<256, true, 1>("pair M=256", it);
+    run<256, true, 2>("pair M=256", it);
+    run<256, true, 4>("pair M=256", it);
+    run<128, true, 4>("pair M=256", it);
+    return 0;
+}
