@@ -44,25 +44,32 @@ struct Cfg {
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int kStages = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
     static constexpr int kSStages = 8;
+    // TMEM partial buffers: as many BN-column buffers as fit in 512 columns.  The promotion's
+    // release of buffer kb gates MMA(kb + NBUF); with N=256 only 2 fit and the release chain
+    // (commit -> wake -> TMEM read -> arrive -> wake) exceeds one 512-cycle MMA block, so N=160
+    // with 3 buffers is the default dense tile.
+    static constexpr int NBUF = 512 / BN;
+    static constexpr int TMEM_COLS = 512;
     // sA box: BM + 4 floats starting at the 4-aligned row at or below the CTA's first row (a TMA
     // box must start 16-byte aligned in its inner dimension; grouped tiles start at any row).
     static constexpr int SA_BOX = BM + 4;
     static constexpr int SA_BYTES = 640;                    // >= SA_BOX * 4, multiple of 128
-    static constexpr int SB_BYTES = BN * 4;                 // WGRAD per-column scales
-    // + up to 2 block scalars (FPROP/DGRAD); TMA destinations must be 128-byte aligned
-    static constexpr int SSTAGE = SA_BYTES + SB_BYTES + 128;
+    // per-column sB of the tile for this K-block (Wgrad: TMA; Fprop/Dgrad: expanded from the
+    // 128-column block scalars by the scale warp); TMA destinations must be 128-byte aligned
+    static constexpr int SB_BYTES = (BN * 4 + 127) / 128 * 128;
+    static constexpr int SSTAGE = SA_BYTES + SB_BYTES;
     static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
-    static constexpr int TMEM_COLS = 2 * BN;
     // 4 promotion warpgroups (16 warps): TMEM->register bandwidth and FFMA2 issue both scale with
     // the number of warps (tools/microbench.cu: 322 B/clk at 8 warps, ~470 at 16).
     static constexpr int NWG = 4;
     static constexpr int THREADS = 128 * (1 + NWG);
     static constexpr int NC = BN / NWG;                     // columns per promotion thread
-    static constexpr int CW = 16;                           // TMEM load width (columns)
+    static_assert(NC % 8 == 0, "promotion slices are multiples of 8 columns");
+    static constexpr bool kOneShot = NC <= 40;              // load the whole slice, then one wait
     static constexpr int REG_OTHER = 40, REG_PROMO = 104;   // setmaxnreg split of the 96 x 640 pool
     static constexpr int OFF_SS = kStages * STAGE;
     static constexpr int OFF_BAR = OFF_SS + kSStages * SSTAGE;
-    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 4;
+    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NBUF;
     static constexpr int OFF_GRP = OFF_BAR + NBAR * 8 + 16;
     static constexpr int SMEM_DENSE = 1024 + OFF_GRP;
     static constexpr int SMEM_GROUPED = 1024 + OFF_GRP + 2 * (kMaxGroups + 1) * 4;
@@ -77,8 +84,12 @@ struct KParams {
     void* D; int64_t ldd; int accumulate;
     int G; const int64_t* offsets;
     int debug;                    // experiments only (FP8BS_GEMM_DEBUG): 1 skip promotion math,
-                                  // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident)
+                                  // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident),
+                                  // 8 load A only, 16 record clock64 timestamps of CTA 0
+    unsigned long long* ts;       // [8][kTsN] timestamps (debug & 16)
 };
+constexpr int kTsN = 512;
+#define FP8BS_TS(slot, kb) do { if ((p.debug & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
 
 struct Tile { int row0, row_end, n0, e; };   // row0: first row of the CLUSTER tile
 
@@ -123,19 +134,20 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     auto sfull_bar  = [&](int s) { return bar0 + 8u * (2 * C::kStages + s); };
     auto sempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + C::kSStages + s); };
     auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
-    auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + 2 + b); };
+    auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NBUF + b); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + C::NBAR * 8);
     int* cum = reinterpret_cast<int*>(smem + C::OFF_GRP);
     int* off = cum + (kMaxGroups + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index broadcast from lane 0 so the compiler knows role branches are warp-uniform
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const uint32_t rank = kPair ? cluster_ctarank() : 0u;
     const int cid = blockIdx.x / C::CS, ncl = gridDim.x / C::CS;
 
     if (threadIdx.x == 32) {
         for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
         for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), 4 * C::NWG); }
-        for (int b = 0; b < 2; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 4 * C::NWG * C::CS); }
+        for (int b = 0; b < C::NBUF; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 4 * C::NWG * C::CS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -192,7 +204,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     if (warp < 4) {
         setmaxnreg_dec<C::REG_OTHER>();
-        if (warp == 0 && lane == 0) {
+        if (warp == 0) {
+          if (lane == 0) {
             // ---------------- TMA producer: A and B K-blocks (this CTA's halves) ----------------
             int it = 0;
             Tile tl;
@@ -205,6 +218,16 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t sa = sbase + s * C::STAGE;
                     const int kc = (p.debug & 4) ? 0 : kb * BK;
+                    if (p.debug & 8) {   // experiment: A only (halves TMA bytes)
+                        if constexpr (kPair) {
+                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::A_BYTES);
+                            tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
+                        } else {
+                            mbar_arrive_expect_tx(full_bar(s), C::A_BYTES);
+                            tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
+                        }
+                        continue;
+                    }
                     if constexpr (kPair) {
                         if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::STAGE);
                         tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
@@ -218,7 +241,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                 }
             }
-        } else if (warp == 1 && lane == 0 && rank == 0) {
+          }
+        } else if (warp == 1) {
+          if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (leader CTA) ----------------
             constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, BN);
             int it = 0, pit = 0;
@@ -227,10 +252,12 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 for (int kb = 0; kb < p.KB; ++kb, ++it, ++pit) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
-                    const int pb = pit & 1;
-                    const uint32_t pph = (pit >> 1) & 1;
+                    const int pb = pit % C::NBUF;
+                    const uint32_t pph = (pit / C::NBUF) & 1;
                     mbar_wait(pempty_bar(pb), pph ^ 1);
+                    FP8BS_TS(0, pit);
                     mbar_wait(full_bar(s), ph);
+                    FP8BS_TS(1, pit);
                     tc_fence_after();
                     const uint32_t sa = sbase + s * C::STAGE;
                     const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + C::A_BYTES);
@@ -248,10 +275,12 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         mma_commit(empty_bar(s));
                         mma_commit(pfull_bar(pb));
                     }
+                    FP8BS_TS(2, pit);
                 }
             }
+          }
         } else if (warp == 3) {
-            // ---------------- scale producer (this CTA's rows) ----------------
+            // ---------------- scale producer (this CTA's rows; the tile's per-column sB) ----------------
             int sit = 0;
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
@@ -260,32 +289,37 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int arow = tl.row0 + (int)rank * BM;
                 const int nb0 = tl.n0 / 128;
                 for (int kb0 = 0; kb0 < p.KB; kb0 += 32) {
-                    float v0 = 0.0f, v1 = 0.0f;
+                    // lane j holds the <= 3 block scalars the tile's columns need at K-block kb0 + j
+                    float v[3] = {0.0f, 0.0f, 0.0f};
                     if constexpr (!kWgrad) {
                         const int kb = kb0 + lane;
                         if (kb < p.KB) {
-                            v0 = __ldg(sbp + nb0 * p.sb_nb_stride + kb * p.sb_kb_stride);
-                            if (BN == 256 && nb0 + 1 < p.NB) v1 = __ldg(sbp + (nb0 + 1) * p.sb_nb_stride + kb * p.sb_kb_stride);
+#pragma unroll
+                            for (int b = 0; b < 3; ++b)
+                                if (nb0 + b < p.NB && b * 128 < (tl.n0 % 128) + BN)
+                                    v[b] = __ldg(sbp + (nb0 + b) * p.sb_nb_stride + kb * p.sb_kb_stride);
                         }
                     }
                     const int nk = min(32, p.KB - kb0);
                     for (int j = 0; j < nk; ++j, ++sit) {
-                        const float b0 = __shfl_sync(0xffffffffu, v0, j);
-                        const float b1 = __shfl_sync(0xffffffffu, v1, j);
+                        const int ss = sit % C::kSStages;
+                        const uint32_t sph = (sit / C::kSStages) & 1;
+                        mbar_wait(sempty_bar(ss), sph ^ 1);          // whole warp: shuffles stay convergent
+                        const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
+                        // Fprop/Dgrad: the <= 3 block scalars of the tile's 128-column weight blocks
+                        const float b0 = __shfl_sync(0xffffffffu, v[0], j);
+                        const float b1 = __shfl_sync(0xffffffffu, v[1], j);
+                        const float b2 = __shfl_sync(0xffffffffu, v[2], j);
                         if (lane == 0) {
-                            const int ss = sit % C::kSStages;
-                            const uint32_t sph = (sit / C::kSStages) & 1;
-                            mbar_wait(sempty_bar(ss), sph ^ 1);
-                            uint8_t* st = smem + C::OFF_SS + ss * C::SSTAGE;
                             if constexpr (!kWgrad) {
-                                float* sc = reinterpret_cast<float*>(st + C::SA_BYTES + C::SB_BYTES);
-                                sc[0] = b0; sc[1] = b1;
+                                float* sbs = reinterpret_cast<float*>(smem + C::OFF_SS + ss * C::SSTAGE + C::SA_BYTES);
+                                sbs[0] = b0; sbs[1] = b1; sbs[2] = b2;
                             }
-                            const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
-                            mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? C::SB_BYTES : 0));
+                            mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? BN * 4 : 0));
                             tma_load_2d(sst, &tmSA, sfull_bar(ss), arow & ~3, kb0 + j);
                             if constexpr (kWgrad) tma_load_2d(sst + C::SA_BYTES, &tmSB, sfull_bar(ss), tl.n0, kb0 + j);
                         }
+                        __syncwarp();
                     }
                 }
             }
@@ -298,13 +332,17 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int quad = warp & 3;                      // TMEM lane quadrant
         const int row = quad * 32 + lane;               // row within this CTA's 128
         constexpr int NC = C::NC;
-        constexpr int CW = C::CW;
         const uint32_t pempty_addr0 = kPair ? mapa_shared(pempty_bar(0), 0) : pempty_bar(0);
         float acc[NC];
         int sit = 0, pit = 0;
         Tile tl;
         for (int t = cid; next_tile(t, tl); t += ncl) {
             const int arow = tl.row0 + (int)rank * BM;
+            // weight block (relative to the tile's first) of this slice's first column, and the number
+            // of 8-column groups of the slice that lie in that block
+            const int c_first = tl.n0 + h * NC;
+            const int blo = c_first / 128 - tl.n0 / 128;
+            const int gsplit = (((c_first / 128) + 1) * 128 - c_first) / 8;
 #pragma unroll
             for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
             for (int kb = 0; kb < p.KB; ++kb, ++sit, ++pit) {
@@ -313,72 +351,87 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 mbar_wait(sfull_bar(ss), sph);
                 const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
                 const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
-                float2 f2 = make_float2(0.0f, 0.0f);
+                const float2 sa2 = make_float2(sa, sa);
+                const uint32_t sbv = sst + C::SA_BYTES + 4u * (h * NC);   // Wgrad: this slice's per-column sB
+                // Fprop/Dgrad: the slice spans <= 2 weight blocks; groups of 8 columns before gsplit use
+                // f_lo = sA*sB(blo), the rest f_hi = sA*sB(blo+1) (block edges fall on multiples of 8
+                // columns: n0 is a multiple of 32 and slices of NC are multiples of 8)
+                float f_lo = 0.0f, f_hi = 0.0f;
                 if constexpr (!kWgrad) {
-                    const float f = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + C::SB_BYTES + 4u * ((h * NC) / 128)));
-                    f2 = make_float2(f, f);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(sempty_bar(ss));
+                    f_lo = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + 4u * blo));
+                    f_hi = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + 4u * (blo + 1)));
                 }
-                const int pb = pit & 1;
-                const uint32_t pph = (pit >> 1) & 1;
+                const int pb = pit % C::NBUF;
+                const uint32_t pph = (pit / C::NBUF) & 1;
+                if (lane == 0 && (warp == 4 || warp == C::THREADS / 32 - 1)) FP8BS_TS(warp == 4 ? 3 : 5, pit);
                 mbar_wait(pfull_bar(pb), pph);
+                if (lane == 0 && (warp == 4 || warp == C::THREADS / 32 - 1)) FP8BS_TS(warp == 4 ? 4 : 6, pit);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + pb * BN + h * NC;
-                if (p.debug & 1) {
+                auto release_p = [&]() {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
                         if constexpr (kPair) mbar_arrive_cluster(pempty_addr0 + 8u * pb);
                         else mbar_arrive(pempty_bar(pb));
+                        if (warp == C::THREADS / 32 - 1) FP8BS_TS(7, pit);
                     }
-                    if constexpr (kWgrad) {
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(sempty_bar(ss));
-                    }
-                    continue;
-                }
+                };
+                // acc[c0 + j] += P[j] * (sA(kb,row) * sB(kb, col)) for a chunk of W columns:
+                // Fprop/Dgrad one FFMA2 per column pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
+                auto fma_chunk = [&](const uint32_t* r, int c0, int W) {
+                    if constexpr (!kWgrad) {
 #pragma unroll
-                for (int c = 0; c < NC / CW; ++c) {
-                    uint32_t r[CW];
-                    if constexpr (CW == 32) FP8BS_TMEM_LD32(taddr + c * CW, r);
-                    else FP8BS_TMEM_LD16(taddr + c * CW, r);
+                        for (int g = 0; g < W / 8; ++g) {
+                            const float f = ((c0 >> 3) + g < gsplit) ? f_lo : f_hi;
+                            const float2 f2 = make_float2(f, f);
+#pragma unroll
+                            for (int j = 8 * g; j < 8 * g + 8; j += 2) {
+                                const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
+                                                            make_float2(acc[c0 + j], acc[c0 + j + 1]));
+                                acc[c0 + j] = a.x; acc[c0 + j + 1] = a.y;
+                            }
+                        }
+                        return;
+                    }
+#pragma unroll
+                    for (int j4 = 0; j4 < W / 4; ++j4) {
+                        const float4 b = lds_f32x4(sbv + 4u * (c0 + j4 * 4));
+                        const int j = c0 + j4 * 4;
+                        const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
+                        const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
+                        const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 0]), __uint_as_float(r[j4 * 4 + 1])), fa,
+                                                     make_float2(acc[j + 0], acc[j + 1]));
+                        const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 2]), __uint_as_float(r[j4 * 4 + 3])), fb,
+                                                     make_float2(acc[j + 2], acc[j + 3]));
+                        acc[j + 0] = a0.x; acc[j + 1] = a0.y; acc[j + 2] = a1.x; acc[j + 3] = a1.y;
+                    }
+                };
+                if (p.debug & 1) {
+                    release_p();
+                } else if constexpr (C::kOneShot) {
+                    // whole slice in flight at once, one wait, release the buffer, then the math
+                    uint32_t r[NC];
+#pragma unroll
+                    for (int c = 0; c + 32 <= NC; c += 32) FP8BS_TMEM_LD32(taddr + c, (r + c));
+                    if constexpr (NC % 32 >= 16) FP8BS_TMEM_LD16(taddr + NC / 32 * 32, (r + NC / 32 * 32));
+                    if constexpr (NC % 16 == 8) FP8BS_TMEM_LD8(taddr + NC - 8, (r + NC - 8));
                     tmem_ld_wait();
-                    if (c == NC / CW - 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if constexpr (kPair) mbar_arrive_cluster(pempty_addr0 + 8u * pb);
-                            else mbar_arrive(pempty_bar(pb));
-                        }
-                    }
-                    if constexpr (kWgrad) {
-                        const float2 sa2 = make_float2(sa, sa);
+                    release_p();
+                    fma_chunk(r, 0, NC);
+                } else {
+                    constexpr int CW = 16;
 #pragma unroll
-                        for (int j4 = 0; j4 < CW / 4; ++j4) {
-                            const float4 b = lds_f32x4(sst + C::SA_BYTES + 4u * (h * NC + c * CW + j4 * 4));
-                            const int j = c * CW + j4 * 4;
-                            const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
-                            const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
-                            float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 0]), __uint_as_float(r[j4 * 4 + 1])), fa,
-                                                   make_float2(acc[j + 0], acc[j + 1]));
-                            float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 2]), __uint_as_float(r[j4 * 4 + 3])), fb,
-                                                   make_float2(acc[j + 2], acc[j + 3]));
-                            acc[j + 0] = a0.x; acc[j + 1] = a0.y; acc[j + 2] = a1.x; acc[j + 3] = a1.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < CW; j += 2) {
-                            float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
-                                                  make_float2(acc[c * CW + j], acc[c * CW + j + 1]));
-                            acc[c * CW + j] = a.x; acc[c * CW + j + 1] = a.y;
-                        }
+                    for (int c = 0; c < NC / CW; ++c) {
+                        uint32_t r[CW];
+                        FP8BS_TMEM_LD16(taddr + c * CW, r);
+                        tmem_ld_wait();
+                        if (c == NC / CW - 1) release_p();
+                        fma_chunk(r, c * CW, CW);
                     }
                 }
-                if constexpr (kWgrad) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(sempty_bar(ss));
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sempty_bar(ss));
             }
             // ---------------- epilogue ----------------
             const int grow = arow + row;
@@ -454,6 +507,8 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
     return r == CUDA_SUCCESS;
 }
 
+static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)
+
 template <int BN, bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
     using C = Cfg<BN, kPair>;
@@ -494,7 +549,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     if (kWgrad) {
         uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)KB};
         uint64_t str[1] = {(uint64_t)a.ldsB * 4};
-        uint32_t box[2] = {BN, 1};
+        uint32_t box[2] = {(uint32_t)BN, 1};
         if (!make_map(&tSB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.sB, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) {
             *detail = "cuTensorMapEncodeTiled failed for sB"; return cudaErrorInvalidValue;
         }
@@ -515,6 +570,11 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         static int dbg = -1;
         if (dbg < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); dbg = e ? atoi(e) : 0; }
         p.debug = dbg;
+        if (dbg & 16) {
+            if (!g_ts) cudaMalloc(&g_ts, 8 * kTsN * sizeof(unsigned long long));
+            cudaMemsetAsync(g_ts, 0, 8 * kTsN * sizeof(unsigned long long), st);
+            p.ts = g_ts;
+        }
     }
 
     int64_t tiles_ub;
@@ -548,7 +608,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     return cudaPeekAtLastError();
 }
 
-int gemm_variant_override = 0;   // test hook: 1 = 1-CTA BN=128, 2 = 1-CTA BN=256, 3 = CTA pair BN=256
+int gemm_variant_override = 0;   // test hook (also FP8BS_GEMM_VARIANT): see launch_gemm
 
 template <int BN, bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
@@ -561,6 +621,8 @@ static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** det
                      : launch_cfg<BN, false, false, false, kPair>(a, st, detail);
 }
 
+// Variants: 1 = 1-CTA N=128 (4 TMEM buffers), 2 = 1-CTA N=256 (2), 3 = CTA pair N=256 (2),
+//           4 = CTA pair N=160 (3), 5 = 1-CTA N=160 (3).
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail) {
     static int env_variant = -1;   // FP8BS_GEMM_VARIANT (experiments only; read once)
     if (env_variant < 0) {
@@ -568,14 +630,29 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
         env_variant = e ? atoi(e) : 0;
     }
     int v = env_variant ? env_variant : gemm_variant_override;
-    if (v < 1 || v > 3) {
+    if (v < 1 || v > 5) {
+        // measured on B200 (tools/gemm_perf.py, C1 shapes): pair N=256 is fastest for large M;
+        // ~128-row experts / small M waste half of a 256-row pair tile -> 1-CTA N=256.
         if (a.N <= 128) v = 1;
-        else if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 3 : 2;   // ~128-row experts: 1-CTA tiles
+        else if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 3 : 2;
         else v = (a.M <= 128) ? 2 : 3;
     }
-    if (v == 1) return launch_v<128, false>(a, st, detail);
-    if (v == 2) return launch_v<256, false>(a, st, detail);
-    return launch_v<256, true>(a, st, detail);
+    switch (v) {
+        case 1: return launch_v<128, false>(a, st, detail);
+        case 2: return launch_v<256, false>(a, st, detail);
+        case 3: return launch_v<256, true>(a, st, detail);
+        case 5: return launch_v<160, false>(a, st, detail);
+        default: return launch_v<160, true>(a, st, detail);
+    }
 }
 
 }  // namespace fp8bs
+
+// Experiments only (not in include/fp8bs.h): copy the debug timestamps of the last GEMM launch.
+extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_timestamps(unsigned long long* host, int n) {
+    if (!fp8bs::g_ts) return 0;
+    if (n > 8 * fp8bs::kTsN) n = 8 * fp8bs::kTsN;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, fp8bs::g_ts, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    return n;
+}

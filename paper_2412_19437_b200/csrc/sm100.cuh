@@ -162,6 +162,12 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
                    "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                               \
                  : "r"(taddr))
 
+#define FP8BS_TMEM_LD8(taddr, r)                                                                   \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"           \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),           \
+                   "=r"(r[6]), "=r"(r[7])                                                           \
+                 : "r"(taddr))
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------------------------------

@@ -10,7 +10,7 @@ using namespace fp8bs;
 
 // iters K-blocks of 4 MMAs each; buffers alternate between TMEM columns [0,N) and [N,2N);
 // commit every kb to an mbarrier; the issuing thread waits on the commit of kb-depth (depth in-flight).
-template <int N, bool kPair, int DEPTH>
+template <int N, bool kPair, int DEPTH, int MP = 256>
 __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* cyc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -37,12 +37,12 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
     tc_fence_after();
     const uint32_t tmem = slot;
     if (warp == 0 && lane == 0 && rank == 0) {
-        constexpr uint32_t idesc = idesc_e4m3_f32(kPair ? 256 : 128, N);
+        constexpr uint32_t idesc = idesc_e4m3_f32(kPair ? MP : 128, N);
         const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sb);
         unsigned long long t0 = clock64();
         for (int kb = 0; kb < iters; ++kb) {
             if (kb >= DEPTH) mbar_wait(smem_u32(&bars[(kb - DEPTH) & 7]), ((kb - DEPTH) >> 3) & 1);
-            const uint32_t d = tmem + (kb & 1) * N;
+            const uint32_t d = tmem + (kb % (512 / N)) * N;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0);
@@ -66,10 +66,10 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
     }
 }
 
-template <int N, bool kPair, int DEPTH>
+template <int N, bool kPair, int DEPTH, int MP = 256>
 static void run(const char* name, int iters) {
-    auto kern = k_mma<N, kPair, DEPTH>;
-    const int smem = 1024 + 16384 + N * 128;
+    auto kern = k_mma<N, kPair, DEPTH, MP>;
+    const int smem = 1024 + 16384 + ((N * 128 + 1023) / 1024) * 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* dcyc;
     cudaMalloc(&dcyc, 148 * 8);
@@ -94,7 +94,7 @@ static void run(const char* name, int iters) {
     cudaMemcpy(h, dcyc, sizeof h, cudaMemcpyDeviceToHost);
     const int nunits = kPair ? 74 : 148;
     double avg = 0; for (int i = 0; i < nunits; ++i) avg += h[i]; avg /= nunits;
-    const double macs_per_kb_per_sm = 128.0 * N * 128;    // per SM (pair: each SM does 128 rows)
+    const double macs_per_kb_per_sm = (kPair ? MP / 2.0 : 128.0) * N * 128;    // per SM (pair: each SM does 128 rows)
     const double flops = 2.0 * macs_per_kb_per_sm * iters * 148;
     printf("%-28s N=%3d depth=%d: %7.1f cyc/kb  (ideal %d)  %6.0f MAC/clk/SM  %7.1f TFLOP/s (events)\n", name, N, DEPTH,
            avg / iters, (int)(macs_per_kb_per_sm / 8192), macs_per_kb_per_sm * iters / avg, flops / (ms * 1e-3) / 1e12);
@@ -102,13 +102,20 @@ static void run(const char* name, int iters) {
 
 int main() {
     const int it = 20000;
-    run<256, false, 1>("1-CTA M=128", it);
+    run<256, true, 2, 128>("pair M=128", it);
+    run<256, true, 3, 128>("pair M=128", it);
+    run<256, true, 4, 128>("pair M=128", it);
     run<256, false, 2>("1-CTA M=128", it);
-    run<256, false, 4>("1-CTA M=128", it);
-    run<128, false, 4>("1-CTA M=128", it);
-    run<256, true, 1>("pair M=256", it);
+    run<224, false, 2>("1-CTA M=128", it);
+    run<192, false, 2>("1-CTA M=128", it);
+    run<176, false, 2>("1-CTA M=128", it);
+    run<160, false, 2>("1-CTA M=128", it);
+    run<160, false, 3>("1-CTA M=128", it);
+    run<144, false, 3>("1-CTA M=128", it);
+    run<128, false, 3>("1-CTA M=128", it);
     run<256, true, 2>("pair M=256", it);
-    run<256, true, 4>("pair M=256", it);
-    run<128, true, 4>("pair M=256", it);
+    run<192, true, 2>("pair M=256", it);
+    run<160, true, 3>("pair M=256", it);
+    run<128, true, 3>("pair M=256", it);
     return 0;
 }
