@@ -37,14 +37,26 @@ __device__ __forceinline__ float load_scalar(const T* p) {
     else return *reinterpret_cast<const float*>(p);
 }
 
-// E codes of one 16-byte chunk, packed little-endian (element 0 in the lowest byte).
+// E codes of one 16-byte chunk, packed little-endian (element 0 in the lowest byte).  `fast` is
+// uniform per group, so the branch is taken once per chunk (not per element): the fast path is
+// the packed Markstein quotient, the slow path (tiny / huge scales, reading R2) IEEE division.
 template <int E>
 __device__ __forceinline__ void encode_chunk(const float* f, float sc, float r, bool fast, uint32_t* w) {
+    if (fast) {
+        const float2 r2 = make_float2(r, r), ns2 = make_float2(-sc, -sc);
 #pragma unroll
-    for (int i = 0; i < E / 4; ++i) {
-        uint32_t lo = cvt_e4m3x2(div_scale(f[4 * i + 0], sc, r, fast), div_scale(f[4 * i + 1], sc, r, fast));
-        uint32_t hi = cvt_e4m3x2(div_scale(f[4 * i + 2], sc, r, fast), div_scale(f[4 * i + 3], sc, r, fast));
-        w[i] = lo | (hi << 16);
+        for (int i = 0; i < E / 4; ++i) {
+            const float2 a = div_scale2_fast(make_float2(f[4 * i + 0], f[4 * i + 1]), r2, ns2);
+            const float2 b = div_scale2_fast(make_float2(f[4 * i + 2], f[4 * i + 3]), r2, ns2);
+            w[i] = cvt_e4m3x2(a.x, a.y) | (cvt_e4m3x2(b.x, b.y) << 16);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < E / 4; ++i) {
+            const uint32_t lo = cvt_e4m3x2(__fdiv_rn(f[4 * i + 0], sc), __fdiv_rn(f[4 * i + 1], sc));
+            const uint32_t hi = cvt_e4m3x2(__fdiv_rn(f[4 * i + 2], sc), __fdiv_rn(f[4 * i + 3], sc));
+            w[i] = lo | (hi << 16);
+        }
     }
 }
 
@@ -80,6 +92,8 @@ k_quant_act_1x128(const T* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
             ok[j] = (kb < KB) && (col < K);
             v[j] = ok[j] ? ld_stream16(xr + col) : make_uint4(0, 0, 0, 0);
         }
+        // all shuffle reductions first (convergent), then the per-tile encode
+        float sc[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             float f[E];
@@ -89,19 +103,128 @@ k_quant_act_1x128(const T* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
             for (int e = 0; e < E; ++e) amax = fmaxf(amax, fabsf(f[e]));
 #pragma unroll
             for (int o = L / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            const float sc = group_scale(amax);
-            const float r = __frcp_rn(sc);
-            const bool fast = fast_div_ok(sc);
+            sc[j] = group_scale(amax);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            float f[E];
+            Vec<T>::unpack(v[j], f);
+            const float r = __frcp_rn(sc[j]);
             uint32_t w[E / 4];
-            encode_chunk<E>(f, sc, r, fast, w);
+            encode_chunk<E>(f, sc[j], r, fast_div_ok(sc[j]), w);
             const int64_t kb = kbase + j * TPW + sub;
             if (ok[j]) {
                 uint8_t* dst = q + m * ldq + kb * 128 + li * E;
                 if constexpr (E == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
                 else *reinterpret_cast<uint32_t*>(dst) = w[0];
-                if (li == 0) s[kb * lds + m] = sc;
+                if (li == 0) s[kb * lds + m] = sc[j];
             }
         }
+    }
+}
+
+// ===========================================================================================
+// 1x128, streamed with TMA bulk copies (fast path: contiguous rows, K % 128 == 0, ldq == K).
+// The input is then a flat sequence of T = M*KB tiles.  One producer warp streams 16 KB chunks
+// of tiles with cp.async.bulk into a 6-stage shared-memory ring (mbarrier full/empty); 8
+// consumer warps encode from shared memory and store codes/scales directly.  Memory traffic is
+// decoupled from the encode arithmetic, so up to 192 KB per SM stays in flight.
+// ===========================================================================================
+template <typename T>
+struct Q1Cfg {
+    static constexpr int EL = 16;                           // elements per lane (8 lanes per tile)
+    static constexpr int L = 128 / EL;
+    static constexpr int VEC = EL * (int)sizeof(T) / 16;    // 16-byte smem loads per lane: 2 / 4
+    static constexpr int TILE_BYTES = 128 * (int)sizeof(T);
+    static constexpr int CONSUMERS = 16;                    // warps
+    static constexpr int TILES_PER_PASS = CONSUMERS * (32 / L);    // 64
+    static constexpr int PASSES = 1;
+    static constexpr int CHUNK_TILES = TILES_PER_PASS * PASSES;
+    static constexpr int CHUNK_BYTES = CHUNK_TILES * TILE_BYTES;   // 16 KB (BF16) / 32 KB (FP32)
+    static constexpr int STAGES = 98304 / CHUNK_BYTES;             // 96 KB ring: 2 CTAs per SM
+    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int SMEM = STAGES * CHUNK_BYTES + 2 * STAGES * 8;
+};
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(Q1Cfg<T>::THREADS)
+k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __restrict__ q,
+                      float* __restrict__ s, int64_t lds) {
+    using C = Q1Cfg<T>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + C::STAGES * C::CHUNK_BYTES;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::STAGES; ++i) { mbar_init(bar0 + 8 * i, 1); mbar_init(bar0 + 8 * (C::STAGES + i), C::CONSUMERS); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int KB = (int)(K >> 7);
+    const int NT = (int)(M * KB);                            // < 2^31 (host-checked)
+    const int nchunks = (NT + C::CHUNK_TILES - 1) / C::CHUNK_TILES;
+    if (warp == C::CONSUMERS) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            int it = 0;
+            for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+                const int st = it % C::STAGES;
+                mbar_wait(bar0 + 8 * (C::STAGES + st), ((it / C::STAGES) & 1) ^ 1);
+                const int t0 = c * C::CHUNK_TILES;
+                const uint32_t bytes = (uint32_t)min(C::CHUNK_TILES, NT - t0) * C::TILE_BYTES;
+                mbar_arrive_expect_tx(bar0 + 8 * st, bytes);
+                bulk_load(sbase + st * C::CHUNK_BYTES, reinterpret_cast<const uint8_t*>(x) + (int64_t)t0 * C::TILE_BYTES,
+                          bytes, bar0 + 8 * st);
+            }
+        }
+        return;
+    }
+    // ---------------- consumers: lane = (tile slot, 16-element slice) ----------------
+    const int sub = lane / C::L, li = lane % C::L;
+    int it = 0;
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int st = it % C::STAGES;
+        mbar_wait(bar0 + 8 * st, (it / C::STAGES) & 1);
+        const int t0 = c * C::CHUNK_TILES;
+        const int ntl = min(C::CHUNK_TILES, NT - t0);
+#pragma unroll
+        for (int pass = 0; pass < C::PASSES; ++pass) {
+            const int d = pass * C::TILES_PER_PASS + warp * (32 / C::L) + sub;   // tile within the chunk
+            const bool ok = d < ntl;
+            float f[C::EL];
+#pragma unroll
+            for (int v = 0; v < C::VEC; ++v) {
+                const uint4 u = ok ? lds128(sbase + st * C::CHUNK_BYTES + d * C::TILE_BYTES + li * (C::EL * (int)sizeof(T)) + v * 16)
+                                   : make_uint4(0, 0, 0, 0);
+                Vec<T>::unpack(u, f + v * Vec<T>::E);
+            }
+            float amax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < C::EL; ++e) amax = fmaxf(amax, fabsf(f[e]));
+#pragma unroll
+            for (int o = C::L / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const float sc = group_scale(amax);
+            const float r = __frcp_rn(sc);
+            uint32_t w[4];
+            if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w);   // warp-uniform
+            else encode_chunk<16>(f, sc, r, false, w);
+            if (ok) {
+                const int t = t0 + d;
+                *reinterpret_cast<uint4*>(q + (int64_t)t * 128 + li * C::EL) = make_uint4(w[0], w[1], w[2], w[3]);
+                if (li == 0) {
+                    const int m = t / KB, kb = t - m * KB;
+                    s[(int64_t)kb * lds + m] = sc;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (C::STAGES + st));
     }
 }
 
@@ -350,7 +473,20 @@ static cudaError_t launch_1x128_t(const void* x, int64_t M, int64_t K, int64_t l
     constexpr int E = Vec<T>::E;
     const bool fast = aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (K % E == 0) &&
                       (reinterpret_cast<uintptr_t>(q) % E == 0) && (ldq % E == 0);
-    if (fast) {
+    const bool flat = fast && (ldx == K) && (K % 128 == 0) && (ldq == K) && aligned16(q) && (M * (K / 128) < (1ll << 31));
+    if (flat) {
+        using C = Q1Cfg<T>;
+        static bool attr_set[64] = {false};   // per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+            cudaFuncSetAttribute(k_quant_act_1x128_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+        }
+        const int64_t chunks = (M * (K / 128) + C::CHUNK_TILES - 1) / C::CHUNK_TILES;
+        k_quant_act_1x128_tma<T><<<grid_for(chunks, 2, 2), C::THREADS, C::SMEM, st>>>(
+            reinterpret_cast<const T*>(x), M, K, q, s, lds);
+    } else if (fast) {
         constexpr int U = 4;
         constexpr int TPU = (32 / (128 / E)) * U;
         const int64_t KB = (K + 127) / 128;

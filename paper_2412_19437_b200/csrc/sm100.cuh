@@ -37,6 +37,14 @@ __device__ __forceinline__ float div_scale(float x, float s, float r, bool fast)
     return __fdiv_rn(x, s);
 }
 
+// Packed (FMUL2/FFMA2) form of div_scale for two elements; ns = -s so that x - q0*s is one FFMA2.
+__device__ __forceinline__ float2 div_scale2_fast(float2 x, float2 r2, float2 ns2) {
+    const float2 q0 = __fmul2_rn(x, r2);
+    const float2 e = __ffma2_rn(q0, ns2, x);
+    const float2 q1 = __ffma2_rn(e, r2, q0);
+    return make_float2(copysignf(q1.x, x.x), copysignf(q1.y, x.y));
+}
+
 // Two FP32 -> packed E4M3x2 with round-to-nearest-even and saturation to +-448
 // (cvt.rn.satfinite.e4m3x2.f32).  Result: low byte = lo, high byte = hi.
 __device__ __forceinline__ uint32_t cvt_e4m3x2(float lo, float hi) {
@@ -88,6 +96,11 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         :: "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+// 1-D bulk copy global -> shared (size multiple of 16, both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1, int32_t c2) {
     asm volatile(
