@@ -14,7 +14,7 @@ import re
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfp8bs.so")
+LIB_PATH = os.environ.get("FP8BS_LIB") or os.path.join(_PKG, "libfp8bs.so")   # FP8BS_LIB: A/B experiments
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "fp8bs.h")
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_ALIGN, ERR_UNSUPPORTED, ERR_DEVICE, ERR_CUDA = range(7)

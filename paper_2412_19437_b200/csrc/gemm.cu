@@ -481,30 +481,10 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // ===========================================================================================
 // host side: tensor maps + launch
 // ===========================================================================================
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
-    return fn;
-}
-
 static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
                      const uint64_t* strides_bytes /* rank-1 */, const uint32_t* box, CUtensorMapSwizzle sw) {
-    auto enc = get_encode();
-    if (!enc) return false;
-    uint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, dt, (cuuint32_t)rank, const_cast<void*>(base), (const cuuint64_t*)dims,
-                     (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    const int d = dt == CU_TENSOR_MAP_DATA_TYPE_UINT8 ? TMAP_U8 : TMAP_F32;
+    return make_tmap(m, d, rank, base, dims, strides_bytes, box, sw == CU_TENSOR_MAP_SWIZZLE_128B ? 128 : 0);
 }
 
 static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)

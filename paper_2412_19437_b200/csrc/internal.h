@@ -6,6 +6,10 @@
 namespace fp8bs {
 
 int num_sms();                                   // SM count of the current device (cached per device)
+// TMA tensor map (a CUtensorMap, 64-byte aligned, 128 bytes) — tmap.cu
+enum { TMAP_U8 = 0, TMAP_BF16 = 1, TMAP_F32 = 2 };
+bool make_tmap(void* map, int dtype, int rank, const void* base, const uint64_t* dims,
+               const uint64_t* strides_bytes /* rank-1 */, const uint32_t* box, int swizzle /* 0, 64, 128 bytes */);
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 cudaError_t launch_quant_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,

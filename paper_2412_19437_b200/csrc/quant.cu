@@ -3,6 +3,8 @@
 //   128x128 blocks for weights.  All are HBM-bound: one read of the input, one write of the codes
 //   (+ 1/128 or 1/16384 of scales).  Per group: amax (maxNum over |x|, warp shuffles), s = amax/448
 //   (IEEE division), then per element RN32(x/s) (Markstein sequence) and cvt.rn.satfinite.e4m3x2.
+#include <cuda.h>
+
 #include "sm100.cuh"
 #include "internal.h"
 
@@ -324,6 +326,276 @@ k_quant_act_128x1(const T* __restrict__ x, int64_t M, int64_t C, int64_t ldx,
 }
 
 // ===========================================================================================
+// 128x1, TMA-streamed (fast path): a producer warp loads 128-token x 256-byte tiles of x with a
+// 2-D tensor map into a 3-stage ring (OOB rows/channels zero-filled); 8 consumer warps own one
+// 32-bit word column (2 BF16 / 1 FP32 channels) x 32 rows each: column amax via smem across the 4
+// row groups, packed Markstein encode of row pairs (cvt of rows r, r+1 gives adjacent code bytes of
+// the transposed row directly), codes staged per channel and written as 128-byte rows of qT.
+// ===========================================================================================
+template <typename T>
+struct QTCfg {
+    static constexpr int CH = 256 / (int)sizeof(T);         // channels per tile: 128 BF16 / 64 FP32
+    static constexpr int CPW = 4 / (int)sizeof(T);          // channels per 32-bit word
+    static constexpr int TILE_BYTES = 128 * 256;
+    static constexpr int STAGES = 3;
+    static constexpr int CONSUMERS = 8;
+    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int QSTR = 144;
+    static constexpr int OFF_Q = STAGES * TILE_BYTES;       // code staging [CH][QSTR]
+    static constexpr int OFF_RED = OFF_Q + CH * QSTR;       // partial amax [4][CH]
+    static constexpr int OFF_BAR = OFF_RED + 4 * CH * 4;
+    static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
+};
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ float word_elem(uint32_t w, int j) {
+    if constexpr (sizeof(T) == 2) return j == 0 ? bf16_lo(w) : bf16_hi(w);
+    else return __uint_as_float(w);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(QTCfg<T>::THREADS)
+k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C, uint8_t* __restrict__ qT,
+                      int64_t ldq, float* __restrict__ sT, int64_t lds) {
+    using P = QTCfg<T>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + P::OFF_BAR;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < P::STAGES; ++i) { mbar_init(bar0 + 8 * i, 1); mbar_init(bar0 + 8 * (P::STAGES + i), P::CONSUMERS); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int MB = (int)((M + 127) >> 7), NCB = (int)((C + P::CH - 1) / P::CH);
+    const int ntiles = MB * NCB;
+    if (warp == P::CONSUMERS) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmX);
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int st = it % P::STAGES;
+                mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
+                mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
+                tma_load_2d(sbase + st * P::TILE_BYTES, &tmX, bar0 + 8 * st, (t % NCB) * P::CH, (t / NCB) * 128);
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x, wc = tid & 63, rg = tid >> 6;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % P::STAGES;
+        const int mb = t / NCB, cb = t - mb * NCB;
+        const int64_t m0 = (int64_t)mb * 128, c0 = (int64_t)cb * P::CH;
+        mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
+        uint32_t w[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) w[r] = lds32(sbase + st * P::TILE_BYTES + (rg * 32 + r) * 256 + wc * 4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
+        float sc[P::CPW];
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            float a = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) a = fmaxf(a, fabsf(word_elem<T>(w[r], j)));
+            reinterpret_cast<float*>(smem + P::OFF_RED)[rg * P::CH + wc * P::CPW + j] = a;
+        }
+        named_bar_sync(1, 32 * P::CONSUMERS);
+        bool fast = true;
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            const int ch = wc * P::CPW + j;
+            const float* red = reinterpret_cast<const float*>(smem + P::OFF_RED);
+            const float a = fmaxf(fmaxf(red[ch], red[P::CH + ch]), fmaxf(red[2 * P::CH + ch], red[3 * P::CH + ch]));
+            sc[j] = group_scale(a);
+            fast = fast && fast_div_ok(sc[j]);
+            if (rg == 0 && c0 + ch < C) sT[(int64_t)mb * lds + c0 + ch] = sc[j];
+        }
+        fast = __all_sync(0xffffffffu, fast);
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            const float r = __frcp_rn(sc[j]);
+            uint32_t code[8];
+            if (fast) {
+                const float2 r2 = make_float2(r, r), ns2 = make_float2(-sc[j], -sc[j]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float2 a = div_scale2_fast(make_float2(word_elem<T>(w[4 * k], j), word_elem<T>(w[4 * k + 1], j)), r2, ns2);
+                    const float2 b = div_scale2_fast(make_float2(word_elem<T>(w[4 * k + 2], j), word_elem<T>(w[4 * k + 3], j)), r2, ns2);
+                    code[k] = cvt_e4m3x2(a.x, a.y) | (cvt_e4m3x2(b.x, b.y) << 16);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    code[k] = cvt_e4m3x2(__fdiv_rn(word_elem<T>(w[4 * k], j), sc[j]), __fdiv_rn(word_elem<T>(w[4 * k + 1], j), sc[j])) |
+                              (cvt_e4m3x2(__fdiv_rn(word_elem<T>(w[4 * k + 2], j), sc[j]), __fdiv_rn(word_elem<T>(w[4 * k + 3], j), sc[j])) << 16);
+                }
+            }
+            const uint32_t qa = sbase + P::OFF_Q + (wc * P::CPW + j) * P::QSTR + rg * 32;
+            sts128(qa, make_uint4(code[0], code[1], code[2], code[3]));
+            sts128(qa + 16, make_uint4(code[4], code[5], code[6], code[7]));
+        }
+        named_bar_sync(1, 32 * P::CONSUMERS);
+#pragma unroll
+        for (int i = 0; i < P::CH * 8 / (32 * P::CONSUMERS); ++i) {
+            const int idx = i * 32 * P::CONSUMERS + tid, chl = idx >> 3, pk = idx & 7;
+            const int64_t c = c0 + chl, m = m0 + pk * 16;
+            if (c < C && m < M) {
+                const uint4 val = lds128(sbase + P::OFF_Q + chl * P::QSTR + pk * 16);
+                uint8_t* dst = qT + c * ldq + m;
+                if (m + 16 <= M) {
+                    *reinterpret_cast<uint4*>(dst) = val;
+                } else {
+                    const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
+                    for (int e = 0; e < 16 && m + e < M; ++e) dst[e] = b[e];
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================================
+// 128x128 weights, TMA-streamed (fast path): one 128x128 block per stage (64 KB FP32 / 32 KB BF16)
+// loaded by a producer warp; 16 consumer warps read 16-byte chunks (lane-contiguous, conflict-free),
+// block amax via shuffles + smem, codes written row-major straight to global (coalesced 128-byte
+// rows); the transposed copy goes through a row-major code tile in smem and 4-row byte gathers.
+// ===========================================================================================
+template <typename T>
+struct QWCfg {
+    static constexpr int E = Vec<T>::E;                     // elements per 16-byte chunk
+    static constexpr int CPR = 128 / E;                     // chunks per block row
+    static constexpr int BLOCK_BYTES = 128 * 128 * (int)sizeof(T);
+    static constexpr int STAGES = sizeof(T) == 4 ? 3 : 4;
+    static constexpr int CONSUMERS = 16;
+    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int NCH = 128 * CPR / (32 * CONSUMERS); // chunks per consumer thread: 8 / 4
+    static constexpr int OFF_C = STAGES * BLOCK_BYTES;      // code tile [128][128]
+    static constexpr int OFF_RED = OFF_C + 128 * 128;
+    static constexpr int OFF_BAR = OFF_RED + CONSUMERS * 4;
+    static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(QWCfg<T>::THREADS)
+k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K, uint8_t* __restrict__ q, int64_t ldq,
+                   float* __restrict__ s, int64_t ldsw, uint8_t* __restrict__ qT, int64_t ldqT) {
+    using P = QWCfg<T>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + P::OFF_BAR;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < P::STAGES; ++i) { mbar_init(bar0 + 8 * i, 1); mbar_init(bar0 + 8 * (P::STAGES + i), P::CONSUMERS); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int NB = (int)((N + 127) >> 7), KB = (int)((K + 127) >> 7);
+    const int nblocks = NB * KB;
+    if (warp == P::CONSUMERS) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmW);
+            int it = 0;
+            for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+                const int st = it % P::STAGES;
+                mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
+                mbar_arrive_expect_tx(bar0 + 8 * st, P::BLOCK_BYTES);
+                tma_load_2d(sbase + st * P::BLOCK_BYTES, &tmW, bar0 + 8 * st, (b % KB) * 128, (b / KB) * 128);
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x;
+    float* red = reinterpret_cast<float*>(smem + P::OFF_RED);
+    int it = 0;
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+        const int st = it % P::STAGES;
+        const int nb = b / KB, kb = b - nb * KB;
+        const int64_t n0 = (int64_t)nb * 128, k0 = (int64_t)kb * 128;
+        mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
+        uint4 v[P::NCH];
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) v[i] = lds128(sbase + st * P::BLOCK_BYTES + (i * 32 * P::CONSUMERS + tid) * 16);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));
+        float amax = 0.0f;
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) {
+            float f[P::E];
+            Vec<T>::unpack(v[i], f);
+#pragma unroll
+            for (int e = 0; e < P::E; ++e) amax = fmaxf(amax, fabsf(f[e]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) red[warp] = amax;
+        named_bar_sync(1, 32 * P::CONSUMERS);
+        amax = red[0];
+#pragma unroll
+        for (int i = 1; i < P::CONSUMERS; ++i) amax = fmaxf(amax, red[i]);
+        const float sc = group_scale(amax);
+        const float rc = __frcp_rn(sc);
+        const bool fast = fast_div_ok(sc);                  // block-uniform
+#pragma unroll
+        for (int i = 0; i < P::NCH; ++i) {
+            const int idx = i * 32 * P::CONSUMERS + tid, row = idx / P::CPR, col = (idx % P::CPR) * P::E;
+            float f[P::E];
+            Vec<T>::unpack(v[i], f);
+            uint32_t wd[P::E / 4];
+            encode_chunk<P::E>(f, sc, rc, fast, wd);
+            if (n0 + row < N && k0 + col < K) {
+                uint8_t* dst = q + (n0 + row) * ldq + k0 + col;
+                if constexpr (P::E == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(wd[0], wd[1]);
+                else *reinterpret_cast<uint32_t*>(dst) = wd[0];
+            }
+            if (qT) {   // code tile word (row, kw) lives at row*128 + 4*(kw ^ (row/4 % 32)): conflict-free both ways
+#pragma unroll
+                for (int e = 0; e < P::E / 4; ++e) {
+                    const int kw = col / 4 + e;
+                    asm volatile("st.shared.u32 [%0], %1;" :: "r"(sbase + P::OFF_C + row * 128 + 4 * (kw ^ ((row >> 2) & 31))),
+                                 "r"(wd[e]) : "memory");
+                }
+            }
+        }
+        if (tid == 0) s[(int64_t)nb * ldsw + kb] = sc;
+        if (qT) {
+            named_bar_sync(1, 32 * P::CONSUMERS);
+#pragma unroll
+            for (int i = 0; i < 32 * 32 / (32 * P::CONSUMERS); ++i) {
+                const int idx = i * 32 * P::CONSUMERS + tid, kw = idx >> 5, l = idx & 31;   // rows 4l..4l+3, k 4kw..4kw+3
+                uint32_t a[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[j] = lds32(sbase + P::OFF_C + (4 * l + j) * 128 + 4 * (kw ^ l));
+                // 4x4 byte transpose: b[e] = bytes e of a[0..3]
+                const uint32_t t0 = __byte_perm(a[0], a[1], 0x5140), t1 = __byte_perm(a[0], a[1], 0x7362);
+                const uint32_t t2 = __byte_perm(a[2], a[3], 0x5140), t3 = __byte_perm(a[2], a[3], 0x7362);
+                const uint32_t b[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632),
+                                       __byte_perm(t1, t3, 0x5410), __byte_perm(t1, t3, 0x7632)};
+                const int64_t n = n0 + 4 * l;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t kk = k0 + 4 * kw + e;
+                    if (kk < K && n < N) {
+                        uint8_t* dst = qT + kk * ldqT + n;
+                        if (n + 4 <= N) *reinterpret_cast<uint32_t*>(dst) = b[e];
+                        else for (int x = 0; x < 4 && n + x < N; ++x) dst[x] = (uint8_t)(b[e] >> (8 * x));
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================================
 // 128x128 weight blocks.  CTA per block: 16-byte loads held in registers, block amax via warp
 // shuffles + smem, codes written row-major; the optional transposed copy is staged in smem
 // ([k][n], 132-byte rows) and written as contiguous 128-byte rows of qT.
@@ -513,7 +785,26 @@ static cudaError_t launch_128x1_t(const void* x, int64_t M, int64_t C, int64_t l
     using P = T128x1<T>;
     const bool fast = aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (C % P::E == 0) &&
                       aligned16(qT) && (ldq % 16 == 0);
-    if (fast) {
+    alignas(64) CUtensorMap tm;
+    bool tma = fast && (M * ((C + P::CH - 1) / P::CH) / 128 < (1ll << 31));
+    if (tma) {
+        const uint64_t dims[2] = {(uint64_t)C, (uint64_t)M};
+        const uint64_t str[1] = {(uint64_t)ldx * sizeof(T)};
+        const uint32_t box[2] = {(uint32_t)P::CH, 128};
+        tma = make_tmap(&tm, sizeof(T) == 2 ? TMAP_BF16 : TMAP_F32, 2, x, dims, str, box, 0);
+    }
+    if (tma) {
+        using Q = QTCfg<T>;
+        static bool attr_tma[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_tma[dev]) {
+            cudaFuncSetAttribute(k_quant_act_128x1_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+            if (dev >= 0 && dev < 64) attr_tma[dev] = true;
+        }
+        const int64_t tiles = ((M + 127) / 128) * ((C + Q::CH - 1) / Q::CH);
+        k_quant_act_128x1_tma<T><<<grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st>>>(tm, M, C, qT, ldq, sT, lds);
+    } else if (fast) {
         static bool attr_set[64] = {false};   // per device; idempotent, benign race
         int dev = 0;
         cudaGetDevice(&dev);
@@ -546,7 +837,25 @@ static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, 
                       (reinterpret_cast<uintptr_t>(q) % P::E == 0) && (ldq % P::E == 0) &&
                       (qT == nullptr || ((reinterpret_cast<uintptr_t>(qT) % 4 == 0) && (ldqT % 4 == 0)));
     const int64_t blocks = ((N + 127) / 128) * ((K + 127) / 128);
-    if (fast) {
+    alignas(64) CUtensorMap tm;
+    bool tma = fast && blocks < (1ll << 31);
+    if (tma) {
+        const uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
+        const uint64_t str[1] = {(uint64_t)ldw * sizeof(T)};
+        const uint32_t box[2] = {128, 128};
+        tma = make_tmap(&tm, sizeof(T) == 2 ? TMAP_BF16 : TMAP_F32, 2, w, dims, str, box, 0);
+    }
+    if (tma) {
+        using Q = QWCfg<T>;
+        static bool attr_tma[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_tma[dev]) {
+            cudaFuncSetAttribute(k_quant_weight_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+            if (dev >= 0 && dev < 64) attr_tma[dev] = true;
+        }
+        k_quant_weight_tma<T><<<grid_for(blocks, 1, 1), Q::THREADS, Q::SMEM, st>>>(tm, N, K, q, ldq, s, ldsw, qT, ldqT);
+    } else if (fast) {
         k_quant_weight_128x128<T><<<grid_for(blocks, 4, 4), 256, 0, st>>>(
             reinterpret_cast<const T*>(w), N, K, ldw, q, ldq, s, ldsw, qT, ldqT);
     } else {

@@ -86,6 +86,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         :: "r"(bar), "r"(parity) : "memory");
 }
 
+// Busy-poll variant (test_wait never suspends): for the single MMA-issuing thread, whose wake-up
+// latency after the last promotion arrive sits on the critical TMEM-buffer release chain.
+__device__ __forceinline__ void mbar_wait_poll(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "POLL_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra POLL_%=;\n\t}"
+        :: "r"(bar), "r"(parity) : "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor) — tensor maps are __grid_constant__ kernel parameters
 // ------------------------------------------------------------------------------------------
@@ -139,6 +150,18 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 // N>>3 at bits 17-22, M>>4 at bits 24-28.
 __host__ __device__ constexpr uint32_t idesc_e4m3_f32(uint32_t M, uint32_t N) {
     return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// K-major descriptor for a stage whose rows are `row_bytes` (128 -> SWIZZLE_128B, SBO 1024;
+// 64 -> SWIZZLE_64B, SBO 512), as written by TMA with the matching swizzle.
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t smem_addr, int row_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((8 * row_bytes) >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)(row_bytes == 128 ? 2 : 4) << 61;
+    return d;
 }
 
 // Shared-memory matrix descriptor (sm100 "version 1"), K-major operand in the canonical

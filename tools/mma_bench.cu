@@ -5,24 +5,27 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../paper_2412_19437_b200/csrc/sm100.cuh"
+#define LD32X(taddr, r) FP8BS_TMEM_LD32(taddr, r)
 
 using namespace fp8bs;
 
 // iters K-blocks of 4 MMAs each; buffers alternate between TMEM columns [0,N) and [N,2N);
 // commit every kb to an mbarrier; the issuing thread waits on the commit of kb-depth (depth in-flight).
-template <int N, bool kPair, int DEPTH, int MP = 256>
-__global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* cyc) {
+template <int N, bool kPair, int DEPTH, int MP = 256, int MODE = 0>
+__global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* cyc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bars[8];
     __shared__ uint32_t slot;
+    __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = kPair ? cluster_ctarank() : 0;
     const uint32_t sa = smem_u32(smem);
     const uint32_t sb = sa + 16384;
     for (int i = threadIdx.x; i < (16384 + N * 128 / (kPair ? 2 : 1)) / 4; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(smem)[i] = 0x38383838u;   // E4M3 1.0
+        reinterpret_cast<uint32_t*>(smem)[i] = MODE == 3 ? ((uint32_t)(i * 2654435761u + blockIdx.x * 40503u) & 0x77777777u) : 0x38383838u;   // MODE 3: random codes
     if (threadIdx.x == 0) {
+        stop = 0;
         for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&bars[i]), 1);
         fence_mbar_init();
     }
@@ -42,7 +45,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
         unsigned long long t0 = clock64();
         for (int kb = 0; kb < iters; ++kb) {
             if (kb >= DEPTH) mbar_wait(smem_u32(&bars[(kb - DEPTH) & 7]), ((kb - DEPTH) >> 3) & 1);
-            const uint32_t d = tmem + (kb % (512 / N)) * N;
+            const uint32_t d = tmem + (MODE == 1 ? 0u : (kb % (512 / N)) * N);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0);
@@ -55,6 +58,25 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
             mbar_wait(smem_u32(&bars[kb & 7]), (kb >> 3) & 1);
         unsigned long long t1 = clock64();
         cyc[blockIdx.x / (kPair ? 2 : 1)] = t1 - t0;
+        stop = 1;
+    } else if (MODE == 1 && warp >= 4) {
+        // interference: continuous tcgen05.ld of 64 columns per thread (TMEM read traffic)
+        const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + ((warp >> 2) - 1) * 64 % 256;
+        uint32_t acc = 0;
+        while (!stop) {
+            uint32_t r[32];
+            LD32X(base, r); asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int j = 0; j < 32; ++j) acc += r[j];
+        }
+        if (acc == 12345) cyc[200] = acc;
+    } else if (MODE == 2 && warp >= 4 && warp < 12) {
+        // interference: continuous 16-byte smem stores into a scratch region (like TMA writes)
+        uint32_t a = smem_u32(smem) + 65536 + (threadIdx.x % 256) * 16;
+        uint32_t v = threadIdx.x;
+        while (!stop) {
+            for (int i = 0; i < 16; ++i)
+                asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" :: "r"(a + (i % 8) * 4096), "r"(v) : "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -66,16 +88,16 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
     }
 }
 
-template <int N, bool kPair, int DEPTH, int MP = 256>
+template <int N, bool kPair, int DEPTH, int MP = 256, int MODE = 0>
 static void run(const char* name, int iters) {
-    auto kern = k_mma<N, kPair, DEPTH, MP>;
-    const int smem = 1024 + 16384 + ((N * 128 + 1023) / 1024) * 1024;
+    auto kern = k_mma<N, kPair, DEPTH, MP, MODE>;
+    const int smem = 1024 + 65536 + 32768 + 4096;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* dcyc;
-    cudaMalloc(&dcyc, 148 * 8);
+    cudaMalloc(&dcyc, 256 * 8);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(148);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3((MODE == 1 || MODE == 2) ? 640 : 128);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -98,24 +120,15 @@ static void run(const char* name, int iters) {
     const double flops = 2.0 * macs_per_kb_per_sm * iters * 148;
     printf("%-28s N=%3d depth=%d: %7.1f cyc/kb  (ideal %d)  %6.0f MAC/clk/SM  %7.1f TFLOP/s (events)\n", name, N, DEPTH,
            avg / iters, (int)(macs_per_kb_per_sm / 8192), macs_per_kb_per_sm * iters / avg, flops / (ms * 1e-3) / 1e12);
+    fflush(stdout);
 }
 
 int main() {
     const int it = 20000;
-    run<256, true, 2, 128>("pair M=128", it);
-    run<256, true, 3, 128>("pair M=128", it);
-    run<256, true, 4, 128>("pair M=128", it);
-    run<256, false, 2>("1-CTA M=128", it);
-    run<224, false, 2>("1-CTA M=128", it);
-    run<192, false, 2>("1-CTA M=128", it);
-    run<176, false, 2>("1-CTA M=128", it);
-    run<160, false, 2>("1-CTA M=128", it);
-    run<160, false, 3>("1-CTA M=128", it);
-    run<144, false, 3>("1-CTA M=128", it);
-    run<128, false, 3>("1-CTA M=128", it);
-    run<256, true, 2>("pair M=256", it);
-    run<192, true, 2>("pair M=256", it);
-    run<160, true, 3>("pair M=256", it);
-    run<128, true, 3>("pair M=256", it);
+    run<256, false, 2, 256, 0>("1-CTA N=256 const 1.0", it);
+    run<256, false, 2, 256, 3>("1-CTA N=256 random", it);
+    run<256, true, 2, 256, 0>("pair N=256 const 1.0", it);
+    run<256, true, 2, 256, 3>("pair N=256 random", it);
+    run<256, true, 4, 256, 3>("pair N=256 random d4", it);
     return 0;
 }
