@@ -282,6 +282,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         } else if (warp == 3) {
             // ---------------- scale producer (this CTA's rows; the tile's per-column sB) ----------------
             int sit = 0;
+            if (p.debug & 512) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
                 const float* sbp = p.sB;
@@ -348,7 +349,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int kb = 0; kb < p.KB; ++kb, ++sit, ++pit) {
                 const int ss = sit % C::kSStages;
                 const uint32_t sph = (sit / C::kSStages) & 1;
-                mbar_wait(sfull_bar(ss), sph);
+                if (!(p.debug & 512)) mbar_wait(sfull_bar(ss), sph);
                 const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
                 const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
                 const float2 sa2 = make_float2(sa, sa);
@@ -431,7 +432,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(sempty_bar(ss));
+                if (lane == 0 && !(p.debug & 512)) mbar_arrive(sempty_bar(ss));
             }
             // ---------------- epilogue ----------------
             const int grow = arow + row;

@@ -243,6 +243,13 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const void* tmap,
         "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
         :: "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
+// TMA load multicast to every CTA in cta_mask (same smem offset; complete_tx on each CTA's barrier
+// at the same offset).
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "h"(mask) : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t dst_smem) {   // whole warp, same warp id in both CTAs
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(dst_smem), "n"(kCols) : "memory");
