@@ -309,8 +309,16 @@ def time_dense(args, world, rank, dev):
             per[name] = {"ms": d, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]}
     dom = max(per, key=lambda n: per[n]["ms"])
     dk = next(l for l in st.launches if l[0] == dom)
+    traffic, traffic_src = None, None
+    try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+        traffic = tj["dram_bytes_per_launch"].get(dom)
+        traffic_src = tj["source"]
+    except Exception:
+        pass
     roof = {"kernel": dom, "bound": "tensor" if dk[2] == "tensor" else "hbm", "achieved": per[dom]["achieved"],
-            "peak": per[dom]["peak"], "unit": per[dom]["unit"], "frac": per[dom]["frac"], "traffic": None,
+            "peak": per[dom]["peak"], "unit": per[dom]["unit"], "frac": per[dom]["frac"], "traffic": traffic,
+            "traffic_unit": "bytes per launch", "traffic_src": traffic_src,
             "peak_src": f"{peaks['src']}: " + ("2 x bf16_tflops (burst) of MEASURED_PEAKS.json" if dk[2] == "tensor"
                                                else "hbm_gbs of MEASURED_PEAKS.json"),
             "share_of_step": per[dom]["ms"] * args.steps / (ms_local)}

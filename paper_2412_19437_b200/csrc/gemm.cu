@@ -83,12 +83,14 @@ struct KParams {
     int NB;                       // ceil(N/128)
     void* D; int64_t ldd; int accumulate;
     int G; const int64_t* offsets;
+    int gm;                       // raster band height in m-tiles (dense)
     int debug;                    // experiments only (FP8BS_GEMM_DEBUG): 1 skip promotion math,
                                   // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident),
                                   // 8 load A only, 16 record clock64 timestamps of CTA 0
     unsigned long long* ts;       // [8][kTsN] timestamps (debug & 16)
 };
 constexpr int kTsN = 512;
+constexpr int kTsSlots = 12;
 #define FP8BS_TS(slot, kb) do { if ((p.debug & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
 
 struct Tile { int row0, row_end, n0, e; };   // row0: first row of the CLUSTER tile
@@ -96,7 +98,13 @@ struct Tile { int row0, row_end, n0, e; };   // row0: first row of the CLUSTER t
 template <int ROWS>
 __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
     if (t >= p.num_m * p.num_n) return false;
-    const int m = t % p.num_m, n = t / p.num_m;
+    // banded raster: m-fastest inside bands of gm m-tiles whose A rows fit in L2, so A is read from
+    // DRAM once per band instead of once per group of concurrent n-tiles (ncu: Dgrad read 627 MB,
+    // Wgrad 1.05 GB of DRAM with plain m-fastest order)
+    const int band = t / (p.gm * p.num_n);
+    const int gmb = min(p.gm, p.num_m - band * p.gm);
+    const int local = t - band * p.gm * p.num_n;
+    const int m = band * p.gm + local % gmb, n = local / gmb;
     tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n; tl.e = 0;   // n0 is scaled by BN by the caller
     return true;
 }
@@ -204,8 +212,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     if (warp < 4) {
         setmaxnreg_dec<C::REG_OTHER>();
+        // Producer and MMA roles run on the WHOLE warp (all lanes keep identical, provably uniform
+        // values) and only the issuing instructions are under elect.sync.  With the loops on lane 0
+        // alone, ptxas wrapped every tcgen05.mma in an ELECT / R2UR.BROADCAST waterfall loop:
+        // ~100 cycles per MMA instruction and ~600 per K-block of issue (measured with clock64).
         if (warp == 0) {
-          if (lane == 0) {
             // ---------------- TMA producer: A and B K-blocks (this CTA's halves) ----------------
             int it = 0;
             Tile tl;
@@ -217,33 +228,25 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t sa = sbase + s * C::STAGE;
-                    const int kc = (p.debug & 4) ? 0 : kb * BK;
-                    if (p.debug & 8) {   // experiment: A only (halves TMA bytes)
+                    const int kc = kb * BK;
+                    if (elect_one()) {
                         if constexpr (kPair) {
-                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::A_BYTES);
+                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::STAGE);
                             tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
+                            if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
+                            else tma_load_2d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
                         } else {
-                            mbar_arrive_expect_tx(full_bar(s), C::A_BYTES);
+                            mbar_arrive_expect_tx(full_bar(s), C::STAGE);
                             tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
+                            if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
+                            else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
                         }
-                        continue;
                     }
-                    if constexpr (kPair) {
-                        if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::STAGE);
-                        tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
-                        if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
-                        else tma_load_2d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
-                    } else {
-                        mbar_arrive_expect_tx(full_bar(s), C::STAGE);
-                        tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
-                        if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
-                        else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
-                    }
+                    __syncwarp();
                 }
             }
-          }
         } else if (warp == 1) {
-          if (lane == 0 && rank == 0) {
+          if (rank == 0) {
             // ---------------- MMA issuer (leader CTA) ----------------
             constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, BN);
             int it = 0, pit = 0;
@@ -254,7 +257,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t ph = (it / C::kStages) & 1;
                     const int pb = pit % C::NBUF;
                     const uint32_t pph = (pit / C::NBUF) & 1;
-                    mbar_wait(pempty_bar(pb), pph ^ 1);
+                    if (!(p.debug & 64)) mbar_wait(pempty_bar(pb), pph ^ 1);
                     FP8BS_TS(0, pit);
                     mbar_wait(full_bar(s), ph);
                     FP8BS_TS(1, pit);
@@ -262,20 +265,25 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t sa = sbase + s * C::STAGE;
                     const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + C::A_BYTES);
                     const uint32_t d = tmem_base + pb * BN;
+                    if (elect_one()) {
+                        if (!(p.debug & 2)) {
 #pragma unroll
-                    for (int k = 0; k < BK / 32; ++k) {
-                        if (p.debug & 2) break;
-                        if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
-                        else mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                            for (int k = 0; k < BK / 32; ++k) {
+                                if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                                else mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                                FP8BS_TS(8 + k, pit);
+                            }
+                        }
+                        if constexpr (kPair) {
+                            mma_commit_pair(empty_bar(s), 3);
+                            mma_commit_pair(pfull_bar(pb), 3);
+                        } else {
+                            mma_commit(empty_bar(s));
+                            mma_commit(pfull_bar(pb));
+                        }
+                        FP8BS_TS(2, pit);
                     }
-                    if constexpr (kPair) {
-                        mma_commit_pair(empty_bar(s), 3);
-                        mma_commit_pair(pfull_bar(pb), 3);
-                    } else {
-                        mma_commit(empty_bar(s));
-                        mma_commit(pfull_bar(pb));
-                    }
-                    FP8BS_TS(2, pit);
+                    __syncwarp();
                 }
             }
           }
@@ -548,12 +556,19 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.G = a.G; p.offsets = a.offsets;
     {
+        // band only when the K extent is long (Dgrad-like: measured -2%); Wgrad-like shapes keep
+        // plain m-fastest order (banding measured +4% there)
+        const int64_t band_bytes = a.K > 8192 ? (48ll << 20) : (int64_t)1 << 62;   // A rows kept L2-resident per band
+        int64_t gm = band_bytes / ((int64_t)C::ROWS * a.K);
+        p.gm = (int)(gm < 1 ? 1 : (gm > p.num_m ? p.num_m : gm));
+    }
+    {
         static int dbg = -1;
         if (dbg < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); dbg = e ? atoi(e) : 0; }
         p.debug = dbg;
         if (dbg & 16) {
-            if (!g_ts) cudaMalloc(&g_ts, 8 * kTsN * sizeof(unsigned long long));
-            cudaMemsetAsync(g_ts, 0, 8 * kTsN * sizeof(unsigned long long), st);
+            if (!g_ts) cudaMalloc(&g_ts, kTsSlots * kTsN * sizeof(unsigned long long));
+            cudaMemsetAsync(g_ts, 0, kTsSlots * kTsN * sizeof(unsigned long long), st);
             p.ts = g_ts;
         }
     }
@@ -632,7 +647,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
 // Experiments only (not in include/fp8bs.h): copy the debug timestamps of the last GEMM launch.
 extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_timestamps(unsigned long long* host, int n) {
     if (!fp8bs::g_ts) return 0;
-    if (n > 8 * fp8bs::kTsN) n = 8 * fp8bs::kTsN;
+    if (n > fp8bs::kTsSlots * fp8bs::kTsN) n = fp8bs::kTsSlots * fp8bs::kTsN;
     cudaDeviceSynchronize();
     cudaMemcpy(host, fp8bs::g_ts, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return n;

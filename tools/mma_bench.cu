@@ -4,20 +4,25 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "../paper_2412_19437_b200/csrc/sm100.cuh"
 #define LD32X(taddr, r) FP8BS_TMEM_LD32(taddr, r)
 
 using namespace fp8bs;
+__device__ int tma_count[148];
+static CUtensorMap g_tmx;
 
 // iters K-blocks of 4 MMAs each; buffers alternate between TMEM columns [0,N) and [N,2N);
 // commit every kb to an mbarrier; the issuing thread waits on the commit of kb-depth (depth in-flight).
 template <int N, bool kPair, int DEPTH, int MP = 256, int MODE = 0>
-__global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* cyc) {
+__global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* cyc, const __grid_constant__ CUtensorMap tmx) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bars[8];
     __shared__ uint32_t slot;
     __shared__ volatile int stop;
+    __shared__ uint64_t tbar[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = kPair ? cluster_ctarank() : 0;
     const uint32_t sa = smem_u32(smem);
@@ -27,6 +32,7 @@ __global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* c
     if (threadIdx.x == 0) {
         stop = 0;
         for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&bars[i]), 1);
+        for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&tbar[i]), 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -59,6 +65,21 @@ __global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* c
         unsigned long long t1 = clock64();
         cyc[blockIdx.x / (kPair ? 2 : 1)] = t1 - t0;
         stop = 1;
+    } else if (MODE == 4 && warp == 2 && lane == 0) {
+        // interference: a TMA stream into a 4 x 32 KB ring (immediately re-armed), ~rate of a GEMM feed
+        const uint32_t ring = smem_u32(smem) + 65536;
+        uint32_t bars = smem_u32(&tbar[0]);
+        int it = 0;
+        while (!stop) {
+            const int s = it & 3;
+            if (it >= 4) mbar_wait(bars + 8 * s, ((it >> 2) - 1) & 1);
+            mbar_arrive_expect_tx(bars + 8 * s, 32768);
+            tma_load_2d(ring + s * 32768, &tmx, bars + 8 * s, 0, (it * 256) % 3840);
+            tma_load_2d(ring + s * 32768 + 16384, &tmx, bars + 8 * s, 128, (it * 256) % 3840);
+            ++it;
+        }
+        for (int j = it - 4 < 0 ? 0 : it - 4; j < it; ++j) mbar_wait(bars + 8 * (j & 3), (j >> 2) & 1);
+        tma_count[blockIdx.x] = it;
     } else if (MODE == 1 && warp >= 4) {
         // interference: continuous tcgen05.ld of 64 columns per thread (TMEM read traffic)
         const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + ((warp >> 2) - 1) * 64 % 256;
@@ -91,7 +112,7 @@ __global__ void __launch_bounds__(640, 1) k_mma(int iters, unsigned long long* c
 template <int N, bool kPair, int DEPTH, int MP = 256, int MODE = 0>
 static void run(const char* name, int iters) {
     auto kern = k_mma<N, kPair, DEPTH, MP, MODE>;
-    const int smem = 1024 + 65536 + 32768 + 4096;
+    const int smem = 1024 + 65536 + 131072 + 4096;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* dcyc;
     cudaMalloc(&dcyc, 256 * 8);
@@ -105,9 +126,9 @@ static void run(const char* name, int iters) {
     cfg.attrs = at; cfg.numAttrs = 1;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    cudaLaunchKernelEx(&cfg, kern, iters, dcyc);
+    cudaLaunchKernelEx(&cfg, kern, iters, dcyc, g_tmx);
     cudaEventRecord(a);
-    cudaLaunchKernelEx(&cfg, kern, iters, dcyc);
+    cudaLaunchKernelEx(&cfg, kern, iters, dcyc, g_tmx);
     cudaEventRecord(b);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
@@ -120,15 +141,21 @@ static void run(const char* name, int iters) {
     const double flops = 2.0 * macs_per_kb_per_sm * iters * 148;
     printf("%-28s N=%3d depth=%d: %7.1f cyc/kb  (ideal %d)  %6.0f MAC/clk/SM  %7.1f TFLOP/s (events)\n", name, N, DEPTH,
            avg / iters, (int)(macs_per_kb_per_sm / 8192), macs_per_kb_per_sm * iters / avg, flops / (ms * 1e-3) / 1e12);
+    if (MODE == 4) { int tc[148]; cudaMemcpyFromSymbol(tc, tma_count, sizeof tc); printf("    concurrent TMA: %.1f B/clk/SM\n", 32768.0 * tc[0] / h[0]); }
     fflush(stdout);
 }
 
 int main() {
+    PFN_cuTensorMapEncodeTiled_v12000 enc;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+    void* buf; cudaMalloc(&buf, (size_t)7168 * 4096); cudaMemset(buf, 0x38, (size_t)7168 * 4096);
+    uint64_t dims[2] = {7168, 4096}, str[1] = {7168}; uint32_t box[2] = {128, 128}, es[2] = {1, 1};
+    enc(&g_tmx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int it = 20000;
-    run<256, false, 2, 256, 0>("1-CTA N=256 const 1.0", it);
-    run<256, false, 2, 256, 3>("1-CTA N=256 random", it);
-    run<256, true, 2, 256, 0>("pair N=256 const 1.0", it);
-    run<256, true, 2, 256, 3>("pair N=256 random", it);
-    run<256, true, 4, 256, 3>("pair N=256 random d4", it);
+    run<256, false, 2, 256, 0>("1-CTA N=256 alone", it);
+    run<256, false, 2, 256, 4>("1-CTA N=256 + TMA stream", it);
+    run<256, true, 2, 256, 0>("pair N=256 alone", it);
     return 0;
 }

@@ -16,15 +16,16 @@ __global__ void __launch_bounds__(64, 1) k_tma(const __grid_constant__ CUtensorM
                                                unsigned long long* cyc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full[16], empty[16];
+    __shared__ uint64_t full[16], empty[16], extra[2];
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) { mbar_init(smem_u32(&full[i]), 1); mbar_init(smem_u32(&empty[i]), GEMMLIKE == 3 ? 2 : 1); }
+        mbar_init(smem_u32(&extra[0]), 1); mbar_init(smem_u32(&extra[1]), 1);
         fence_mbar_init();
     }
     const uint32_t rank = (PAIR || GEMMLIKE == 3) ? cluster_ctarank() : 0;
-    if (RELEASE == 1 && warp == 1) {
+    if (RELEASE >= 1 && warp == 1) {
         if (PAIR) tmem_alloc_pair<32>(smem_u32(&slot)); else tmem_alloc<32>(smem_u32(&slot));
     }
     tc_fence_before();
@@ -80,12 +81,13 @@ __global__ void __launch_bounds__(64, 1) k_tma(const __grid_constant__ CUtensorM
             if (PAIR) mma_commit_pair(smem_u32(&empty[s]), 3);
             else if (RELEASE == 0) mbar_arrive(smem_u32(&empty[s]));
             else mma_commit(smem_u32(&empty[s]));
+            if (RELEASE == 2) mma_commit(smem_u32(&extra[it & 1]));   // second commit per stage (GEMM: pfull)
         }
     }
     tc_fence_before();
     __syncthreads();
     if (PAIR || GEMMLIKE == 3) cluster_sync();
-    if (RELEASE == 1 && warp == 1) {
+    if (RELEASE >= 1 && warp == 1) {
         tc_fence_after();
         if (PAIR) tmem_dealloc_pair<32>(slot); else tmem_dealloc<32>(slot);
     }
@@ -153,7 +155,8 @@ int main() {
     cudaMalloc(&wbig, (size_t)7168 * 18432);
     cudaMemset(wbig, 0x38, (size_t)7168 * 18432);
     run<6, 1>("L2 commit-release", small, 2048, 148);
+    run<6, 2>("L2 commit-release + 2nd commit", small, 2048, 148);
     run<4, 1, false, 1>("GEMM-like A(4096)+B(18432) 48KB", big, 4096, 148, wbig);
-    run<4, 1, false, 3>("GEMM-like, B multicast in 2-CTA cluster", big, 4096, 148, wbig);
+    run<4, 2, false, 1>("GEMM-like 48KB + 2nd commit", big, 4096, 148, wbig);
     return 0;
 }
