@@ -6,21 +6,23 @@
 // to CUDA-core registers every 128 elements; here the promotion interval is the same (forced by
 // the per-128 scales) but the machinery is Blackwell's:
 //   * TMA (SWIZZLE_128B) stages A and B K-blocks (128 wide) into a shared-memory ring;
-//   * one thread issues 4x tcgen05.mma.kind::f8f6f4 (K = 32 each) per K-block into a FRESH
-//     TMEM buffer P (FP32; double-buffered so the tensor core runs ahead of the promotion);
-//   * 16 promotion warps per CTA read P with tcgen05.ld, multiply by sA(kb,i)*sB(kb,j) and
-//     accumulate in registers with packed FFMA2, then write BF16 (RNE) or FP32 (+= for Wgrad);
+//   * a 256-column tile is computed as two N = 128 halves, each with its own MMA-issuing warp
+//     (one thread issues a tcgen05.mma only every ~70 cycles) and its own two TMEM slots: per
+//     K-block each issuer runs 4x tcgen05.mma.kind::f8f6f4 (K = 32) into a fresh FP32 slot P;
+//   * 16 promotion warps read each P with one tcgen05.ld (32 columns per thread), release the slot
+//     at once, then accumulate P * sA(kb,i) * sB(kb,j) in registers with packed FFMA2 and finally
+//     write BF16 (RNE) or FP32 (+= for Wgrad).  A slot is reused two K-blocks later, so its release
+//     has three other N = 128 MMA groups (768 cycles at peak) to land;
 //   * a scale warp streams sA (and Wgrad's per-column sB) with TMA into its own ring.
 // kPair = true: a cluster of 2 CTAs on a TPC runs tcgen05.mma.cta_group::2 with M = 256 (128 rows
-// per CTA) and N = BN: each CTA stages its own 128 rows of A and BN/2 rows of B, so per-SM
-// shared-memory traffic per MAC halves versus one CTA (the 1-CTA 128x256 tile measured ~53%
-// tensor-pipe activity, shared-memory-bandwidth bound).  The leader CTA
-// issues the MMAs; both CTAs' TMA loads complete on the leader's barrier; commits multicast to
-// both CTAs; promotion warps release a TMEM buffer by arriving on the leader's barrier.
-// Warp roles (640 threads): w0 TMA A/B producer, w1 MMA issuer, w2 TMEM allocator, w3 scale
-// producer, w4..w19 promotion + epilogue (warpgroup h owns columns [h*BN/4, (h+1)*BN/4)).
-// Persistent clusters walk a static tile schedule; the grouped (MoE) variant maps tiles to
-// (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
+// per CTA): each CTA stages its own 128 rows of A and 64 rows of each B half, so per-SM L2->SMEM
+// traffic per MAC is that of a 256 x 256 tile.  The leader CTA issues the MMAs; both CTAs' TMA loads
+// complete on the leader's barrier; commits multicast to both CTAs; promotion warps release a TMEM
+// slot by arriving on the leader's barrier.
+// Warp roles (640 threads): w0 TMA A/B producer, w1/w2 MMA issuers (half 0/1; w2 also allocates
+// TMEM), w3 scale producer, w4..w19 promotion + epilogue (warpgroup g owns columns [32g, 32g + 32)
+// of each half).  Persistent clusters walk a static tile schedule; the grouped (MoE) variant maps
+// tiles to (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,47 +34,48 @@
 namespace fp8bs {
 
 constexpr int BM = 128, BK = 128;     // rows per CTA, K-block (= N_C)
+constexpr int BN = 256;               // tile columns, issued as two N = 128 MMA halves
+constexpr int HN = 128;               // columns per half (= one TMEM slot, = one weight block)
 constexpr int kMaxGroups = 1024;
 
-template <int BN, bool kPair>
+template <bool kPair, bool kWgrad>
 struct Cfg {
     static constexpr int CS = kPair ? 2 : 1;                // CTAs per cluster
     static constexpr int ROWS = BM * CS;                    // rows per cluster tile
-    static constexpr int BROWS = kPair ? BN / 2 : BN;       // B rows staged per CTA
+    // B rows staged per CTA per half: a CTA pair splits each N = 128 half into 2 x 64 rows
+    static constexpr int BH_ROWS = kPair ? HN / 2 : HN;
+    static constexpr int BH_BYTES = BH_ROWS * BK;
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = BROWS * BK;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int kStages = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
-    static constexpr int kSStages = 8;
-    // TMEM partial buffers: as many BN-column buffers as fit in 512 columns.  The promotion's
-    // release of buffer kb gates MMA(kb + NBUF); with N=256 only 2 fit and the release chain
-    // (commit -> wake -> TMEM read -> arrive -> wake) exceeds one 512-cycle MMA block, so N=160
-    // with 3 buffers is the default dense tile.
-    static constexpr int NBUF = 512 / BN;
+    static constexpr int STAGE = A_BYTES + 2 * BH_BYTES;
+    static constexpr int kSStages = 8;                     // power of two (promotion indexes with a mask)
+    // TMEM: 4 slots of 128 FP32 columns; half h of a K-block alternates between slots 2h and 2h + 1,
+    // so a slot's promotion overlaps three other N = 128 MMA groups (768 cycles at peak) before the
+    // MMA that reuses it (a 2 x 256-column double buffer gave 512).
+    static constexpr int NSLOT = 4;
     static constexpr int TMEM_COLS = 512;
     // sA box: BM + 4 floats starting at the 4-aligned row at or below the CTA's first row (a TMA
     // box must start 16-byte aligned in its inner dimension; grouped tiles start at any row).
     static constexpr int SA_BOX = BM + 4;
     static constexpr int SA_BYTES = 640;                    // >= SA_BOX * 4, multiple of 128
-    // per-column sB of the tile for this K-block (Wgrad: TMA; Fprop/Dgrad: expanded from the
-    // 128-column block scalars by the scale warp); TMA destinations must be 128-byte aligned
-    static constexpr int SB_BYTES = (BN * 4 + 127) / 128 * 128;
+    // Wgrad: per-column sB of the tile for this K-block (TMA); Fprop/Dgrad: the two 128-column
+    // weight-block scalars of the tile.  TMA destinations must be 128-byte aligned.
+    static constexpr int SB_BYTES = kWgrad ? BN * 4 : 128;
     static constexpr int SSTAGE = SA_BYTES + SB_BYTES;
     static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
-    // 4 promotion warpgroups (16 warps): TMEM->register bandwidth and FFMA2 issue both scale with
-    // the number of warps (tools/microbench.cu: 322 B/clk at 8 warps, ~470 at 16).
-    static constexpr int NWG = 4;
-    static constexpr int THREADS = 128 * (1 + NWG);
-    static constexpr int NC = BN / NWG;                     // columns per promotion thread
-    static_assert(NC % 8 == 0, "promotion slices are multiples of 8 columns");
-    static constexpr bool kOneShot = NC <= 40;              // load the whole slice, then one wait
-    static constexpr int REG_OTHER = 40, REG_PROMO = 104;   // setmaxnreg split of the 96 x 640 pool
-    static constexpr int OFF_SS = kStages * STAGE;
-    static constexpr int OFF_BAR = OFF_SS + kSStages * SSTAGE;
-    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NBUF;
-    static constexpr int OFF_GRP = OFF_BAR + NBAR * 8 + 16;
-    static constexpr int SMEM_DENSE = 1024 + OFF_GRP;
-    static constexpr int SMEM_GROUPED = 1024 + OFF_GRP + 2 * (kMaxGroups + 1) * 4;
+    // Operand stages fill the dynamic shared memory left after the static scale ring and barriers.
+    static constexpr int kStages = (222 * 1024 - kSStages * SSTAGE) / STAGE > 8 ? 8 : (222 * 1024 - kSStages * SSTAGE) / STAGE;
+    // 8 promotion warps: warp (h, quad) owns rows [32 quad, 32 quad + 32) x all 128 columns of half h.
+    // Fewer, wider warps: the per-K-block barrier/scale overhead is paid once per 128 columns, which
+    // keeps the promotion inside the SM's issue budget at tensor-core peak (one K-block = 512 cycles).
+    static constexpr int NPW = 8;
+    static constexpr int THREADS = 128 + 32 * NPW;          // 384
+    static constexpr int NC = HN;                           // columns per promotion thread (128)
+    static constexpr int REG_LAUNCH = 168;                  // 65536 / 384 rounded down to 8
+    static constexpr int REG_OTHER = 24, REG_PROMO = 240;   // setmaxnreg split of the CTA's 168 x 384 registers
+    static_assert((REG_LAUNCH - REG_OTHER) * 128 >= (REG_PROMO - REG_LAUNCH) * 32 * NPW, "setmaxnreg.inc would wait forever: the CTA's pool is fixed at launch");
+    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NSLOT;
+    static constexpr int SMEM_DENSE = 1024 + kStages * STAGE;
+    static constexpr int SMEM_GROUPED = SMEM_DENSE + 2 * (kMaxGroups + 1) * 4;
 };
 
 struct KParams {
@@ -86,14 +89,23 @@ struct KParams {
     int gm;                       // raster band height in m-tiles (dense)
     int debug;                    // experiments only (FP8BS_GEMM_DEBUG): 1 skip promotion math,
                                   // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident),
-                                  // 8 load A only, 16 record clock64 timestamps of CTA 0
-    unsigned long long* ts;       // [8][kTsN] timestamps (debug & 16)
+                                  // 16 record clock64 timestamps of CTA 0, 64 MMA ignores slot release,
+                                  // 128 promotion ignores slot completion (with 64: free-running
+                                  // TMA + MMA pipeline), 256 issuers pace on their own commits (with 128: MMA + TMA only),
+                                  // 512 no scale ring
+    unsigned long long* ts;       // [kTsSlots][kTsN] timestamps (debug & 16)
 };
 constexpr int kTsN = 512;
 constexpr int kTsSlots = 12;
-#define FP8BS_TS(slot, kb) do { if ((p.debug & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
+#ifndef FP8BS_GEMM_TRACE
+#define FP8BS_GEMM_TRACE 0
+#endif
+// Experiments (tools/build_trace.sh): the debug bits and clock64 timestamps exist only in trace builds,
+// so the product kernel carries none of their instructions.
+constexpr bool kTrace = FP8BS_GEMM_TRACE != 0;
+#define FP8BS_TS(slot, kb) do { if (kTrace && (p.debug & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
 
-struct Tile { int row0, row_end, n0, e; };   // row0: first row of the CLUSTER tile
+struct Tile { int row0, row_end, n0, e, nh; };   // row0: first row of the CLUSTER tile; nh: halves in range
 
 template <int ROWS>
 __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
@@ -105,7 +117,8 @@ __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl
     const int gmb = min(p.gm, p.num_m - band * p.gm);
     const int local = t - band * p.gm * p.num_n;
     const int m = band * p.gm + local % gmb, n = local / gmb;
-    tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n; tl.e = 0;   // n0 is scaled by BN by the caller
+    tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n * BN; tl.e = 0;
+    tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
     return true;
 }
 
@@ -123,28 +136,35 @@ __device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cu
     const int mt = (seg + ROWS - 1) / ROWS;
     const int local = t - cum[e];
     const int m = local % mt, n = local / mt;
-    tl.row0 = off[e] + m * ROWS; tl.row_end = off[e + 1]; tl.n0 = n; tl.e = e;
+    tl.row0 = off[e] + m * ROWS; tl.row_end = off[e + 1]; tl.n0 = n * BN; tl.e = e;
+    tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
     return true;
 }
 
-template <int BN, bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
-__global__ void __launch_bounds__(Cfg<BN, kPair>::THREADS, 1)
+template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
+__global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
           const KParams p) {
-    using C = Cfg<BN, kPair>;
+    using C = Cfg<kPair, kWgrad>;
     extern __shared__ uint8_t smem_raw[];
+    // barriers and the scale ring live in static shared memory: their addresses are constants, so
+    // the promotion loop does not re-derive the aligned dynamic base every K-block
+    __shared__ __align__(1024) uint8_t s_scale[C::kSStages * C::SSTAGE];
+    __shared__ __align__(8) uint64_t s_bar[C::NBAR];
+    __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar0 = sbase + C::OFF_BAR;
+    const uint32_t bar0 = smem_u32(s_bar);
+    const uint32_t sring = smem_u32(s_scale);
     auto full_bar   = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar  = [&](int s) { return bar0 + 8u * (C::kStages + s); };
     auto sfull_bar  = [&](int s) { return bar0 + 8u * (2 * C::kStages + s); };
     auto sempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + C::kSStages + s); };
     auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
-    auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NBUF + b); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + C::NBAR * 8);
-    int* cum = reinterpret_cast<int*>(smem + C::OFF_GRP);
+    auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NSLOT + b); };
+    uint32_t* tmem_slot = &s_tmem;
+    int* cum = reinterpret_cast<int*>(smem + C::kStages * C::STAGE);
     int* off = cum + (kMaxGroups + 1);
 
     // warp index broadcast from lane 0 so the compiler knows role branches are warp-uniform
@@ -153,9 +173,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int cid = blockIdx.x / C::CS, ncl = gridDim.x / C::CS;
 
     if (threadIdx.x == 32) {
-        for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
-        for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), 4 * C::NWG); }
-        for (int b = 0; b < C::NBUF; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), 4 * C::NWG * C::CS); }
+        for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 2); }
+        for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), C::NPW); }
+        for (int b = 0; b < C::NSLOT; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), (C::NPW / 2) * C::CS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -203,11 +223,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint32_t tmem_base = *tmem_slot;
 
     auto next_tile = [&](int t, Tile& tl) -> bool {
-        bool ok;
-        if constexpr (kGrouped) ok = get_tile_grouped<C::ROWS>(p, cum, off, t, tl);
-        else ok = get_tile_dense<C::ROWS>(p, t, tl);
-        tl.n0 *= BN;
-        return ok;
+        if constexpr (kGrouped) return get_tile_grouped<C::ROWS>(p, cum, off, t, tl);
+        else return get_tile_dense<C::ROWS>(p, t, tl);
     };
 
     if (warp < 4) {
@@ -215,82 +232,93 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // Producer and MMA roles run on the WHOLE warp (all lanes keep identical, provably uniform
         // values) and only the issuing instructions are under elect.sync.  With the loops on lane 0
         // alone, ptxas wrapped every tcgen05.mma in an ELECT / R2UR.BROADCAST waterfall loop:
-        // ~100 cycles per MMA instruction and ~600 per K-block of issue (measured with clock64).
+        // ~100 cycles per MMA instruction (measured with clock64; tools/mma_bench.cu).
         if (warp == 0) {
-            // ---------------- TMA producer: A and B K-blocks (this CTA's halves) ----------------
+            // ---------------- TMA producer: A and the two B halves (this CTA's rows) ----------------
             int it = 0;
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
                 const int arow = tl.row0 + (int)rank * BM;
-                const int brow = tl.n0 + (int)rank * C::BROWS;
+                const int brow = tl.n0 + (int)rank * C::BH_ROWS;
                 for (int kb = 0; kb < p.KB; ++kb, ++it) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t sa = sbase + s * C::STAGE;
-                    const int kc = kb * BK;
+                    const int kc = (kTrace && (p.debug & 4)) ? 0 : kb * BK;
                     if (elect_one()) {
                         if constexpr (kPair) {
-                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * C::STAGE);
+                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (C::A_BYTES + tl.nh * C::BH_BYTES));
                             tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
-                            if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
-                            else tma_load_2d_pair(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
+                            for (int h = 0; h < tl.nh; ++h) {
+                                if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
+                                else tma_load_2d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN);
+                            }
                         } else {
-                            mbar_arrive_expect_tx(full_bar(s), C::STAGE);
+                            mbar_arrive_expect_tx(full_bar(s), C::A_BYTES + tl.nh * C::BH_BYTES);
                             tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
-                            if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow, tl.e);
-                            else tma_load_2d(sa + C::A_BYTES, &tmB, full_bar(s), kc, brow);
+                            for (int h = 0; h < tl.nh; ++h) {
+                                if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
+                                else tma_load_2d(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN);
+                            }
                         }
                     }
                     __syncwarp();
                 }
             }
-        } else if (warp == 1) {
+        } else if (warp == 1 || warp == 2) {
           if (rank == 0) {
-            // ---------------- MMA issuer (leader CTA) ----------------
-            constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, BN);
-            int it = 0, pit = 0;
+            // ---------------- MMA issuers (leader CTA): warp 1 half 0, warp 2 half 1 ----------------
+            // One thread issues a tcgen05.mma about every 70 cycles (tools/mma_bench.cu), so the 8
+            // N = 128 MMAs of a K-block (512 cycles at peak) need two issuers.  Each half has its own
+            // two TMEM slots (2h, 2h + 1); a stage is released by one commit per half.
+            const int h = warp - 1;
+            constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, HN);
+            int it = 0, qh = 0;
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
-                for (int kb = 0; kb < p.KB; ++kb, ++it, ++pit) {
+                if (h >= tl.nh) { it += p.KB; continue; }
+                for (int kb = 0; kb < p.KB; ++kb, ++it, ++qh) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
-                    const int pb = pit % C::NBUF;
-                    const uint32_t pph = (pit / C::NBUF) & 1;
-                    if (!(p.debug & 64)) mbar_wait(pempty_bar(pb), pph ^ 1);
-                    FP8BS_TS(0, pit);
+                    const int pb = 2 * h + (qh & 1);
+                    const uint32_t pph = (qh >> 1) & 1;
+                    if (kTrace && (p.debug & 256)) { if (qh >= 2) mbar_wait(pfull_bar(pb), pph ^ 1); }   // self-paced
+                    else if (!(kTrace && (p.debug & 64))) mbar_wait(pempty_bar(pb), pph ^ 1);
+                    if (h == 0) FP8BS_TS(0, it);
                     mbar_wait(full_bar(s), ph);
-                    FP8BS_TS(1, pit);
+                    if (h == 0) FP8BS_TS(1, it);
                     tc_fence_after();
                     const uint32_t sa = sbase + s * C::STAGE;
-                    const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + C::A_BYTES);
-                    const uint32_t d = tmem_base + pb * BN;
+                    const uint64_t ad = sdesc_k_sw128(sa);
+                    const uint64_t bd = sdesc_k_sw128(sa + C::A_BYTES + h * C::BH_BYTES);
+                    const uint32_t d = tmem_base + pb * HN;
                     if (elect_one()) {
-                        if (!(p.debug & 2)) {
+                        if (!(kTrace && (p.debug & 2))) {
 #pragma unroll
                             for (int k = 0; k < BK / 32; ++k) {
                                 if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
                                 else mma_f8f6f4(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
-                                FP8BS_TS(8 + k, pit);
                             }
                         }
-                        if constexpr (kPair) {
-                            mma_commit_pair(empty_bar(s), 3);
-                            mma_commit_pair(pfull_bar(pb), 3);
-                        } else {
-                            mma_commit(empty_bar(s));
-                            mma_commit(pfull_bar(pb));
+                        if constexpr (kPair) mma_commit_pair(pfull_bar(pb), 3);
+                        else mma_commit(pfull_bar(pb));
+                        // release the smem stage once this half's MMAs have read it (the barrier
+                        // counts one commit per half; a one-half tile commits twice)
+                        for (int c = 0; c < (tl.nh == 1 ? 2 : 1); ++c) {
+                            if constexpr (kPair) mma_commit_pair(empty_bar(s), 3);
+                            else mma_commit(empty_bar(s));
                         }
-                        FP8BS_TS(2, pit);
                     }
                     __syncwarp();
+                    if (h == 0) FP8BS_TS(2, it);
                 }
             }
           }
         } else if (warp == 3) {
-            // ---------------- scale producer (this CTA's rows; the tile's per-column sB) ----------------
+            // ---------------- scale producer (this CTA's rows; the tile's sB) ----------------
             int sit = 0;
-            if (p.debug & 512) return;   // experiment: no scale ring traffic (promotion uses stale scales)
+            if (kTrace && (p.debug & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
                 const float* sbp = p.sB;
@@ -298,15 +326,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int arow = tl.row0 + (int)rank * BM;
                 const int nb0 = tl.n0 / 128;
                 for (int kb0 = 0; kb0 < p.KB; kb0 += 32) {
-                    // lane j holds the <= 3 block scalars the tile's columns need at K-block kb0 + j
-                    float v[3] = {0.0f, 0.0f, 0.0f};
+                    // lane j holds the 2 block scalars the tile's columns need at K-block kb0 + j
+                    float v0 = 0.0f, v1 = 0.0f;
                     if constexpr (!kWgrad) {
                         const int kb = kb0 + lane;
                         if (kb < p.KB) {
-#pragma unroll
-                            for (int b = 0; b < 3; ++b)
-                                if (nb0 + b < p.NB && b * 128 < (tl.n0 % 128) + BN)
-                                    v[b] = __ldg(sbp + (nb0 + b) * p.sb_nb_stride + kb * p.sb_kb_stride);
+                            v0 = __ldg(sbp + nb0 * p.sb_nb_stride + kb * p.sb_kb_stride);
+                            if (nb0 + 1 < p.NB) v1 = __ldg(sbp + (nb0 + 1) * p.sb_nb_stride + kb * p.sb_kb_stride);
                         }
                     }
                     const int nk = min(32, p.KB - kb0);
@@ -314,15 +340,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         const int ss = sit % C::kSStages;
                         const uint32_t sph = (sit / C::kSStages) & 1;
                         mbar_wait(sempty_bar(ss), sph ^ 1);          // whole warp: shuffles stay convergent
-                        const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
-                        // Fprop/Dgrad: the <= 3 block scalars of the tile's 128-column weight blocks
-                        const float b0 = __shfl_sync(0xffffffffu, v[0], j);
-                        const float b1 = __shfl_sync(0xffffffffu, v[1], j);
-                        const float b2 = __shfl_sync(0xffffffffu, v[2], j);
+                        const uint32_t sst = sring + ss * C::SSTAGE;
+                        const float b0 = __shfl_sync(0xffffffffu, v0, j);
+                        const float b1 = __shfl_sync(0xffffffffu, v1, j);
                         if (lane == 0) {
                             if constexpr (!kWgrad) {
-                                float* sbs = reinterpret_cast<float*>(smem + C::OFF_SS + ss * C::SSTAGE + C::SA_BYTES);
-                                sbs[0] = b0; sbs[1] = b1; sbs[2] = b2;
+                                float* sbs = reinterpret_cast<float*>(s_scale + ss * C::SSTAGE + C::SA_BYTES);
+                                sbs[0] = b0; sbs[1] = b1;
                             }
                             mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? BN * 4 : 0));
                             tma_load_2d(sst, &tmSA, sfull_bar(ss), arow & ~3, kb0 + j);
@@ -337,115 +361,102 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     } else {
         setmaxnreg_inc<C::REG_PROMO>();
         // ---------------- promotion + epilogue ----------------
-        const int h = (warp - 4) >> 2;                  // promotion warpgroup = column slice
+        // Warps 4..7 promote half 0, warps 8..11 half 1 (each SMSP runs one warp of each half).
+        const int h = (warp - 4) >> 2;                  // half
         const int quad = warp & 3;                      // TMEM lane quadrant
         const int row = quad * 32 + lane;               // row within this CTA's 128
-        constexpr int NC = C::NC;
-        const uint32_t pempty_addr0 = kPair ? mapa_shared(pempty_bar(0), 0) : pempty_bar(0);
+        constexpr int NC = C::NC;                       // 128
         float acc[NC];
-        int sit = 0, pit = 0;
+        const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16);
+        const uint32_t sb_off = C::SA_BYTES + 4u * (kWgrad ? h * HN : h);
+        int sit = 0, qh = 0;                            // K-block, slot uses of this half
         Tile tl;
         for (int t = cid; next_tile(t, tl); t += ncl) {
             const int arow = tl.row0 + (int)rank * BM;
-            // weight block (relative to the tile's first) of this slice's first column, and the number
-            // of 8-column groups of the slice that lie in that block
-            const int c_first = tl.n0 + h * NC;
-            const int blo = c_first / 128 - tl.n0 / 128;
-            const int gsplit = (((c_first / 128) + 1) * 128 - c_first) / 8;
+            const bool active = h < tl.nh;
 #pragma unroll
             for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
-            for (int kb = 0; kb < p.KB; ++kb, ++sit, ++pit) {
-                const int ss = sit % C::kSStages;
+            for (int kb = 0; kb < p.KB; ++kb, ++sit) {
+                const int ss = sit & (C::kSStages - 1);
                 const uint32_t sph = (sit / C::kSStages) & 1;
-                if (!(p.debug & 512)) mbar_wait(sfull_bar(ss), sph);
-                const uint32_t sst = sbase + C::OFF_SS + ss * C::SSTAGE;
-                const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
-                const float2 sa2 = make_float2(sa, sa);
-                const uint32_t sbv = sst + C::SA_BYTES + 4u * (h * NC);   // Wgrad: this slice's per-column sB
-                // Fprop/Dgrad: the slice spans <= 2 weight blocks; groups of 8 columns before gsplit use
-                // f_lo = sA*sB(blo), the rest f_hi = sA*sB(blo+1) (block edges fall on multiples of 8
-                // columns: n0 is a multiple of 32 and slices of NC are multiples of 8)
-                float f_lo = 0.0f, f_hi = 0.0f;
-                if constexpr (!kWgrad) {
-                    f_lo = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + 4u * blo));
-                    f_hi = __fmul_rn(sa, lds_f32(sst + C::SA_BYTES + 4u * (blo + 1)));
-                }
-                const int pb = pit % C::NBUF;
-                const uint32_t pph = (pit / C::NBUF) & 1;
-                if (lane == 0 && (warp == 4 || warp == C::THREADS / 32 - 1)) FP8BS_TS(warp == 4 ? 3 : 5, pit);
-                mbar_wait(pfull_bar(pb), pph);
-                if (lane == 0 && (warp == 4 || warp == C::THREADS / 32 - 1)) FP8BS_TS(warp == 4 ? 4 : 6, pit);
-                tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + pb * BN + h * NC;
-                auto release_p = [&]() {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (kPair) mbar_arrive_cluster(pempty_addr0 + 8u * pb);
-                        else mbar_arrive(pempty_bar(pb));
-                        if (warp == C::THREADS / 32 - 1) FP8BS_TS(7, pit);
-                    }
-                };
-                // acc[c0 + j] += P[j] * (sA(kb,row) * sB(kb, col)) for a chunk of W columns:
-                // Fprop/Dgrad one FFMA2 per column pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
-                auto fma_chunk = [&](const uint32_t* r, int c0, int W) {
-                    if constexpr (!kWgrad) {
-#pragma unroll
-                        for (int g = 0; g < W / 8; ++g) {
-                            const float f = ((c0 >> 3) + g < gsplit) ? f_lo : f_hi;
+                if (!(kTrace && (p.debug & 512))) mbar_wait(sfull_bar(ss), sph);
+                if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(11, sit);
+                const uint32_t sst = sring + ss * C::SSTAGE;
+                if (active) {
+                    const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
+                    // Fprop/Dgrad: half h is exactly weight block n0/128 + h (n0 is a multiple of 256),
+                    // so one factor sA(kb,row) * sB(kb, block) per warp: one FFMA per element.
+                    float f = 0.0f;
+                    if constexpr (!kWgrad) f = __fmul_rn(sa, lds_f32(sst + sb_off));
+                    const int pb = 2 * h + (qh & 1);
+                    const uint32_t pph = (qh >> 1) & 1;
+                    ++qh;
+                    if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
+                    if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
+                    if (!(kTrace && (p.debug & 128))) mbar_wait(pfull_bar(pb), pph);
+                    if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(9, sit);
+                    if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 4 : 6, sit);
+                    tc_fence_after();
+                    // acc[c0 + j] += P[j] * sA(kb,row) * sB(kb, col): Fprop/Dgrad one FFMA2 per column
+                    // pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
+                    auto fma32 = [&](const uint32_t* r, int c0) {
+                        if constexpr (!kWgrad) {
                             const float2 f2 = make_float2(f, f);
 #pragma unroll
-                            for (int j = 8 * g; j < 8 * g + 8; j += 2) {
+                            for (int j = 0; j < 32; j += 2) {
                                 const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
                                                             make_float2(acc[c0 + j], acc[c0 + j + 1]));
                                 acc[c0 + j] = a.x; acc[c0 + j + 1] = a.y;
                             }
+                        } else {
+                            const float2 sa2 = make_float2(sa, sa);
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                const float4 b = lds_f32x4(sst + sb_off + 4u * (c0 + j));
+                                const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
+                                const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
+                                const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), fa,
+                                                             make_float2(acc[c0 + j], acc[c0 + j + 1]));
+                                const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])), fb,
+                                                             make_float2(acc[c0 + j + 2], acc[c0 + j + 3]));
+                                acc[c0 + j] = a0.x; acc[c0 + j + 1] = a0.y; acc[c0 + j + 2] = a1.x; acc[c0 + j + 3] = a1.y;
+                            }
                         }
-                        return;
-                    }
+                    };
+                    const uint32_t ta = tbase + pb * HN;
+                    uint32_t r[32];
 #pragma unroll
-                    for (int j4 = 0; j4 < W / 4; ++j4) {
-                        const float4 b = lds_f32x4(sbv + 4u * (c0 + j4 * 4));
-                        const int j = c0 + j4 * 4;
-                        const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
-                        const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
-                        const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 0]), __uint_as_float(r[j4 * 4 + 1])), fa,
-                                                     make_float2(acc[j + 0], acc[j + 1]));
-                        const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j4 * 4 + 2]), __uint_as_float(r[j4 * 4 + 3])), fb,
-                                                     make_float2(acc[j + 2], acc[j + 3]));
-                        acc[j + 0] = a0.x; acc[j + 1] = a0.y; acc[j + 2] = a1.x; acc[j + 3] = a1.y;
-                    }
-                };
-                if (p.debug & 1) {
-                    release_p();
-                } else if constexpr (C::kOneShot) {
-                    // whole slice in flight at once, one wait, release the buffer, then the math
-                    uint32_t r[NC];
-#pragma unroll
-                    for (int c = 0; c + 32 <= NC; c += 32) FP8BS_TMEM_LD32(taddr + c, (r + c));
-                    if constexpr (NC % 32 >= 16) FP8BS_TMEM_LD16(taddr + NC / 32 * 32, (r + NC / 32 * 32));
-                    if constexpr (NC % 16 == 8) FP8BS_TMEM_LD8(taddr + NC - 8, (r + NC - 8));
-                    tmem_ld_wait();
-                    release_p();
-                    fma_chunk(r, 0, NC);
-                } else {
-                    constexpr int CW = 16;
-#pragma unroll
-                    for (int c = 0; c < NC / CW; ++c) {
-                        uint32_t r[CW];
-                        FP8BS_TMEM_LD16(taddr + c * CW, r);
+                    for (int c = 0; c < 3; ++c) {
+                        FP8BS_TMEM_LD32(ta + 32 * c, r);
                         tmem_ld_wait();
-                        if (c == NC / CW - 1) release_p();
-                        fma_chunk(r, c * CW, CW);
+                        fma32(r, 32 * c);
+                        // keep this chunk's FMAs ahead of the next tcgen05.ld: otherwise ptxas overlaps
+                        // two chunks and spills accumulators at the 240-register budget
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) asm volatile("" : "+f"(acc[32 * c + j]));
                     }
+                    FP8BS_TMEM_LD32(ta + 96, r);
+                    tmem_ld_wait();
+                    // release the slot before the last math: the registers hold this warp's part now
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        // the leader's barrier: clear the CTA-rank bit of the shared address (a mapa'd address held
+                        // across the loop made ptxas spill ~30 accumulators)
+                        if constexpr (kPair) mbar_arrive_cluster(pempty_bar(pb) & kPeerBitMask);
+                        else mbar_arrive(pempty_bar(pb));
+                        if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
+                        if (kTrace && warp == 7) FP8BS_TS(7, sit);
+                    }
+                    fma32(r, 96);
                 }
                 __syncwarp();
-                if (lane == 0 && !(p.debug & 512)) mbar_arrive(sempty_bar(ss));
+                if (lane == 0 && !(kTrace && (p.debug & 512))) mbar_arrive(sempty_bar(ss));
             }
             // ---------------- epilogue ----------------
             const int grow = arow + row;
-            if (grow < tl.row_end) {
-                const int col0 = tl.n0 + h * NC;
+            if (active && grow < tl.row_end) {
+                const int col0 = tl.n0 + h * HN;
                 if constexpr (kOutF32) {
                     float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
 #pragma unroll
@@ -497,10 +508,11 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
 }
 
 static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)
+static int g_debug = -1;                      // FP8BS_GEMM_DEBUG, or fp8bs_internal_set_gemm_debug
 
-template <int BN, bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
+template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    using C = Cfg<BN, kPair>;
+    using C = Cfg<kPair, kWgrad>;
     const int KB = (int)(a.K / BK);
     const int64_t rows = a.M;   // total rows of A (total_M for grouped)
     CUtensorMap tA, tB, tSA, tSB;
@@ -515,14 +527,14 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     if (kGrouped) {
         uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
-        uint32_t box[3] = {BK, (uint32_t)C::BROWS, 1};
+        uint32_t box[3] = {BK, (uint32_t)C::BH_ROWS, 1};
         if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
             *detail = "cuTensorMapEncodeTiled failed for B (grouped)"; return cudaErrorInvalidValue;
         }
     } else {
         uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
         uint64_t str[1] = {(uint64_t)a.ldb};
-        uint32_t box[2] = {BK, (uint32_t)C::BROWS};
+        uint32_t box[2] = {BK, (uint32_t)C::BH_ROWS};
         if (!make_map(&tB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a.B, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
             *detail = "cuTensorMapEncodeTiled failed for B"; return cudaErrorInvalidValue;
         }
@@ -563,8 +575,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         p.gm = (int)(gm < 1 ? 1 : (gm > p.num_m ? p.num_m : gm));
     }
     {
-        static int dbg = -1;
-        if (dbg < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); dbg = e ? atoi(e) : 0; }
+        if (g_debug < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); g_debug = e ? atoi(e) : 0; }
+        const int dbg = g_debug;
         p.debug = dbg;
         if (dbg & 16) {
             if (!g_ts) cudaMalloc(&g_ts, kTsSlots * kTsN * sizeof(unsigned long long));
@@ -580,7 +592,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
     if (clusters < 1) clusters = 1;
     const int smem = kGrouped ? C::SMEM_GROUPED : C::SMEM_DENSE;
-    auto kern = k_gemm_bs<BN, kWgrad, kOutF32, kGrouped, kPair>;
+    auto kern = k_gemm_bs<kWgrad, kOutF32, kGrouped, kPair>;
     static bool attr[64] = {false};   // per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -605,41 +617,32 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
 }
 
 int gemm_variant_override = 0;   // test hook (also FP8BS_GEMM_VARIANT): see launch_gemm
+static int g_env_variant = -1;   // FP8BS_GEMM_VARIANT (experiments only; read once)
 
-template <int BN, bool kPair>
+template <bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
     if (a.grouped) {
-        return a.out_f32 ? launch_cfg<BN, false, true, true, kPair>(a, st, detail)
-                         : launch_cfg<BN, false, false, true, kPair>(a, st, detail);
+        return a.out_f32 ? launch_cfg<false, true, true, kPair>(a, st, detail)
+                         : launch_cfg<false, false, true, kPair>(a, st, detail);
     }
-    if (a.layout == 2) return launch_cfg<BN, true, true, false, kPair>(a, st, detail);
-    return a.out_f32 ? launch_cfg<BN, false, true, false, kPair>(a, st, detail)
-                     : launch_cfg<BN, false, false, false, kPair>(a, st, detail);
+    if (a.layout == 2) return launch_cfg<true, true, false, kPair>(a, st, detail);
+    return a.out_f32 ? launch_cfg<false, true, false, kPair>(a, st, detail)
+                     : launch_cfg<false, false, false, kPair>(a, st, detail);
 }
 
-// Variants: 1 = 1-CTA N=128 (4 TMEM buffers), 2 = 1-CTA N=256 (2), 3 = CTA pair N=256 (2),
-//           4 = CTA pair N=160 (3), 5 = 1-CTA N=160 (3).
+// Variants: 1 = one CTA per 128 x 256 tile, 2 = CTA pair (cta_group::2) per 256 x 256 tile.
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    static int env_variant = -1;   // FP8BS_GEMM_VARIANT (experiments only; read once)
-    if (env_variant < 0) {
+    if (g_env_variant < 0) {
         const char* e = getenv("FP8BS_GEMM_VARIANT");
-        env_variant = e ? atoi(e) : 0;
+        g_env_variant = e ? atoi(e) : 0;
     }
-    int v = env_variant ? env_variant : gemm_variant_override;
-    if (v < 1 || v > 5) {
-        // measured on B200 (tools/gemm_perf.py, C1 shapes): pair N=256 is fastest for large M;
-        // ~128-row experts / small M waste half of a 256-row pair tile -> 1-CTA N=256.
-        if (a.N <= 128) v = 1;
-        else if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 3 : 2;
-        else v = (a.M <= 128) ? 2 : 3;
+    int v = g_env_variant ? g_env_variant : gemm_variant_override;
+    if (v < 1 || v > 2) {
+        // ~128-row experts / small M would waste half of a 256-row pair tile -> one CTA per tile
+        if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 2 : 1;
+        else v = (a.M <= 128) ? 1 : 2;
     }
-    switch (v) {
-        case 1: return launch_v<128, false>(a, st, detail);
-        case 2: return launch_v<256, false>(a, st, detail);
-        case 3: return launch_v<256, true>(a, st, detail);
-        case 5: return launch_v<160, false>(a, st, detail);
-        default: return launch_v<160, true>(a, st, detail);
-    }
+    return v == 1 ? launch_v<false>(a, st, detail) : launch_v<true>(a, st, detail);
 }
 
 }  // namespace fp8bs
@@ -652,3 +655,7 @@ extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_times
     cudaMemcpy(host, fp8bs::g_ts, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return n;
 }
+
+// Experiments only: set the GEMM debug bits / variant for subsequent launches in this process.
+extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_debug(int bits) { fp8bs::g_debug = bits; }
+extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_variant(int v) { fp8bs::g_env_variant = v; }

@@ -33,6 +33,18 @@ def dev_scales(s):
     return buf[:, :n]
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "pair"])
+def variant(request):
+    """Force the GEMM tile variant (1: one CTA per 128x256 tile, 2: CTA pair per 256x256 tile)
+    through the library's experiment hook, so both paths are covered at every shape."""
+    import ctypes
+    L = fp.lib()
+    L.fp8bs_internal_set_gemm_variant.argtypes = [ctypes.c_int]
+    L.fp8bs_internal_set_gemm_variant(request.param)
+    yield request.param
+    L.fp8bs_internal_set_gemm_variant(0)
+
+
 def assert_bits_equal(got: torch.Tensor, want: torch.Tensor, what: str):
     got = got.cpu()
     if got.dtype == torch.float32:
@@ -130,12 +142,12 @@ def scale_b_shape(layout, N, K):
     return {fp.FPROP: (NB, KB), fp.DGRAD: (KB, NB), fp.WGRAD: (KB, N)}[layout]
 
 
-GEMM_SHAPES = [(128, 128, 256), (256, 512, 512), (200, 136, 384), (300, 520, 1024), (1000, 264, 256)]
+GEMM_SHAPES = [(128, 128, 256), (256, 512, 512), (200, 136, 384), (300, 520, 1024), (1000, 264, 256), (520, 1160, 640)]
 
 
 @pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_closed_form_bitexact(layout, M, N, K):
+def test_gemm_closed_form_bitexact(layout, M, N, K, variant):
     A = W.codes_small(M, K, seed=M)
     B = W.codes_small(N, K, seed=N + 1)
     sA = W.scales_pow2(K // 128, M, seed=3)
@@ -164,7 +176,7 @@ def quantized_operands(layout, M, N, K, seed=0):
 
 @pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_vs_oracle_fp32(layout, M, N, K):
+def test_gemm_vs_oracle_fp32(layout, M, N, K, variant):
     qa, sa, qb, sb = quantized_operands(layout, M, N, K)
     O = oracle.gemm(layout, qa, sa, qb, sb)
     D = fp.gemm(layout, dev(qa), dev(sa), dev(qb), dev(sb), out_dtype=torch.float32)
@@ -239,7 +251,7 @@ def grouped_case(counts, N, K, seed=0):
 
 
 @pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [128, 128, 128], [5], [0, 0, 257]])
-def test_grouped_vs_dense_bitwise_and_oracle(counts):
+def test_grouped_vs_dense_bitwise_and_oracle(counts, variant):
     N, K = 264, 512
     offsets, qa, sa, qb, sb = grouped_case(counts, N, K)
     D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32)

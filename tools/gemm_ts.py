@@ -20,15 +20,15 @@ for _ in range(3):
     fp.gemm(L, A, sA, B, sB, out=out)
 torch.cuda.synchronize()
 lib = fp.lib()
-buf = (ctypes.c_ulonglong * (8 * 512))()
-lib.fp8bs_internal_debug_timestamps(buf, 8 * 512)
-t = np.array(buf, dtype=np.int64).reshape(8, 512)
-names = ["mma_pempty_ok", "mma_full_ok", "mma_committed", "p4_wait_pfull", "p4_pfull_ok", "pL_wait_pfull", "pL_pfull_ok", "pL_arrived"]
+buf = (ctypes.c_ulonglong * (12 * 512))()
+lib.fp8bs_internal_debug_timestamps(buf, 12 * 512)
+t = np.array(buf, dtype=np.int64).reshape(12, 512)
+names = ["i0_pempty_ok", "i0_full_ok", "i0_committed", "p4_wait0", "p4_ok0", "pL_wait0", "pL_ok0", "pL_rel0", "pL_wait1", "pL_ok1", "pL_rel1", "pL_sfull_ok"]
 t0 = t[0, 0]
 n = int((t[2] > 0).sum())
 print(f"{layout} K-blocks recorded: {n}")
 for kb in list(range(0, 12)) + list(range(100, 108)):
-    print(kb, " ".join(f"{names[i]}={t[i, kb] - t0:>8d}" for i in range(8)))
+    print(kb, " ".join(f"{names[i]}={t[i, kb] - t0:>8d}" for i in range(12)))
 d = np.diff(t[2, 60:n - 1])
 print("median cycles per K-block (commit to commit, steady):", np.median(d))
 print("median pfull-ok -> last-arrive (promotion of one kb):", np.median((t[7] - t[6])[60:n - 1]))
