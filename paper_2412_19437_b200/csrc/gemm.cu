@@ -86,8 +86,9 @@ struct KParams {
     int NB;                       // ceil(N/128)
     void* D; int64_t ldd; int accumulate;
     int G; const int64_t* offsets;
-    int gm;                       // raster band height in m-tiles (dense)
-    int debug;                    // experiments only (FP8BS_GEMM_DEBUG): 1 skip promotion math,
+    int gm;                       // raster band width (dense): tiles of the resident operand per band
+    int rast_n;                   // 1: n-fastest (B resident, A streamed), 0: m-fastest
+    int debug;                    // unused (debug bits are compile-time: FP8BS_GEMM_DEBUG_BITS): 1 skip promotion math,
                                   // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident),
                                   // 16 record clock64 timestamps of CTA 0, 64 MMA ignores slot release,
                                   // 128 promotion ignores slot completion (with 64: free-running
@@ -97,26 +98,36 @@ struct KParams {
 };
 constexpr int kTsN = 512;
 constexpr int kTsSlots = 12;
-#ifndef FP8BS_GEMM_TRACE
-#define FP8BS_GEMM_TRACE 0
+#ifndef FP8BS_PROMO_POLL
+#define FP8BS_PROMO_POLL 0
 #endif
-// Experiments (tools/build_trace.sh): the debug bits and clock64 timestamps exist only in trace builds,
-// so the product kernel carries none of their instructions.
-constexpr bool kTrace = FP8BS_GEMM_TRACE != 0;
-#define FP8BS_TS(slot, kb) do { if (kTrace && (p.debug & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
+#ifndef FP8BS_ISSUER_POLL
+#define FP8BS_ISSUER_POLL 0
+#endif
+#ifndef FP8BS_GEMM_DEBUG_BITS
+#define FP8BS_GEMM_DEBUG_BITS 0
+#endif
+// Experiments (tools/build_rev.sh WORKTREE <name> -DFP8BS_GEMM_DEBUG_BITS=<bits>): the debug bits are
+// compile-time, so the product kernel (bits 0) carries none of their instructions.
+constexpr int kDbg = FP8BS_GEMM_DEBUG_BITS;
+constexpr bool kTrace = kDbg != 0;
+#define FP8BS_TS(slot, kb) do { if ((kDbg & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
 
 struct Tile { int row0, row_end, n0, e, nh; };   // row0: first row of the CLUSTER tile; nh: halves in range
 
 template <int ROWS>
 __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
     if (t >= p.num_m * p.num_n) return false;
-    // banded raster: m-fastest inside bands of gm m-tiles whose A rows fit in L2, so A is read from
-    // DRAM once per band instead of once per group of concurrent n-tiles (ncu: Dgrad read 627 MB,
-    // Wgrad 1.05 GB of DRAM with plain m-fastest order)
-    const int band = t / (p.gm * p.num_n);
-    const int gmb = min(p.gm, p.num_m - band * p.gm);
-    const int local = t - band * p.gm * p.num_n;
-    const int m = band * p.gm + local % gmb, n = local / gmb;
+    // Banded raster.  The operand with fewer bytes stays L2-resident and the other streams from
+    // DRAM once: inside a band of gm tiles of the resident operand, consecutive tiles walk the
+    // resident operand fastest, so the concurrent clusters share each streamed tile through L2.
+    // (ncu, m-fastest only: Wgrad C1 read 1.05 GB of DRAM for 104 MB of operands.)
+    const int nres = p.rast_n ? p.num_n : p.num_m, nstr = p.rast_n ? p.num_m : p.num_n;
+    const int band = t / (p.gm * nstr);
+    const int gb = min(p.gm, nres - band * p.gm);
+    const int local = t - band * p.gm * nstr;
+    const int ires = band * p.gm + local % gb, istr = local / gb;
+    const int m = p.rast_n ? istr : ires, n = p.rast_n ? ires : istr;
     tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n * BN; tl.e = 0;
     tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
     return true;
@@ -245,7 +256,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t sa = sbase + s * C::STAGE;
-                    const int kc = (kTrace && (p.debug & 4)) ? 0 : kb * BK;
+                    const int kc = ((kDbg & 4)) ? 0 : kb * BK;
                     if (elect_one()) {
                         if constexpr (kPair) {
                             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (C::A_BYTES + tl.nh * C::BH_BYTES));
@@ -283,8 +294,14 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t ph = (it / C::kStages) & 1;
                     const int pb = 2 * h + (qh & 1);
                     const uint32_t pph = (qh >> 1) & 1;
-                    if (kTrace && (p.debug & 256)) { if (qh >= 2) mbar_wait(pfull_bar(pb), pph ^ 1); }   // self-paced
-                    else if (!(kTrace && (p.debug & 64))) mbar_wait(pempty_bar(pb), pph ^ 1);
+                    if ((kDbg & 256)) { if (qh >= 2) mbar_wait(pfull_bar(pb), pph ^ 1); }   // self-paced
+                    else if (!((kDbg & 64))) {
+#if FP8BS_ISSUER_POLL
+                        mbar_wait_poll(pempty_bar(pb), pph ^ 1);
+#else
+                        mbar_wait(pempty_bar(pb), pph ^ 1);
+#endif
+                    }
                     if (h == 0) FP8BS_TS(0, it);
                     mbar_wait(full_bar(s), ph);
                     if (h == 0) FP8BS_TS(1, it);
@@ -294,7 +311,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint64_t bd = sdesc_k_sw128(sa + C::A_BYTES + h * C::BH_BYTES);
                     const uint32_t d = tmem_base + pb * HN;
                     if (elect_one()) {
-                        if (!(kTrace && (p.debug & 2))) {
+                        if (!((kDbg & 2))) {
 #pragma unroll
                             for (int k = 0; k < BK / 32; ++k) {
                                 if constexpr (kPair) mma_f8f6f4_pair(d, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
@@ -318,7 +335,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         } else if (warp == 3) {
             // ---------------- scale producer (this CTA's rows; the tile's sB) ----------------
             int sit = 0;
-            if (kTrace && (p.debug & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
+            if ((kDbg & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
                 const float* sbp = p.sB;
@@ -379,7 +396,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int kb = 0; kb < p.KB; ++kb, ++sit) {
                 const int ss = sit & (C::kSStages - 1);
                 const uint32_t sph = (sit / C::kSStages) & 1;
-                if (!(kTrace && (p.debug & 512))) mbar_wait(sfull_bar(ss), sph);
+                if (!((kDbg & 512))) mbar_wait(sfull_bar(ss), sph);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(11, sit);
                 const uint32_t sst = sring + ss * C::SSTAGE;
                 if (active) {
@@ -393,13 +410,23 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     ++qh;
                     if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
                     if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
-                    if (!(kTrace && (p.debug & 128))) mbar_wait(pfull_bar(pb), pph);
+                    if (!((kDbg & 128))) {
+#if FP8BS_PROMO_POLL
+                        mbar_wait_poll(pfull_bar(pb), pph);
+#else
+                        mbar_wait(pfull_bar(pb), pph);
+#endif
+                    }
                     if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(9, sit);
                     if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 4 : 6, sit);
                     tc_fence_after();
                     // acc[c0 + j] += P[j] * sA(kb,row) * sB(kb, col): Fprop/Dgrad one FFMA2 per column
                     // pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
                     auto fma32 = [&](const uint32_t* r, int c0) {
+                        if ((kDbg & 1)) {   // experiment: loads only
+                            if (r[0] == 0x7fffffffu) acc[c0] += 1.0f;
+                            return;
+                        }
                         if constexpr (!kWgrad) {
                             const float2 f2 = make_float2(f, f);
 #pragma unroll
@@ -424,18 +451,27 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                     };
                     const uint32_t ta = tbase + pb * HN;
-                    uint32_t r[32];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        FP8BS_TMEM_LD32(ta + 32 * c, r);
-                        tmem_ld_wait();
-                        fma32(r, 32 * c);
-                        // keep this chunk's FMAs ahead of the next tcgen05.ld: otherwise ptxas overlaps
-                        // two chunks and spills accumulators at the 240-register budget
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) asm volatile("" : "+f"(acc[32 * c + j]));
+                    if ((kDbg & 8)) {     // experiment: no TMEM reads, no math
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (kPair) mbar_arrive_cluster(pempty_bar(pb) & kPeerBitMask);
+                            else mbar_arrive(pempty_bar(pb));
+                        }
+                        goto half_done;
                     }
-                    FP8BS_TMEM_LD32(ta + 96, r);
+                    // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
+                    // soon as the second round has landed (32 FFMA2 after the first wait)
+                    uint32_t r0[32], r1[32];
+                    FP8BS_TMEM_LD32(ta, r0);
+                    FP8BS_TMEM_LD32(ta + 32, r1);
+                    tmem_ld_wait();
+                    fma32(r0, 0);
+                    fma32(r1, 32);
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
+                    FP8BS_TMEM_LD32(ta + 64, r0);
+                    FP8BS_TMEM_LD32(ta + 96, r1);
                     tmem_ld_wait();
                     // release the slot before the last math: the registers hold this warp's part now
                     tc_fence_before();
@@ -448,10 +484,12 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
                         if (kTrace && warp == 7) FP8BS_TS(7, sit);
                     }
-                    fma32(r, 96);
+                    fma32(r0, 64);
+                    fma32(r1, 96);
+                half_done:;
                 }
                 __syncwarp();
-                if (lane == 0 && !(kTrace && (p.debug & 512))) mbar_arrive(sempty_bar(ss));
+                if (lane == 0 && !((kDbg & 512))) mbar_arrive(sempty_bar(ss));
             }
             // ---------------- epilogue ----------------
             const int grow = arow + row;
@@ -508,7 +546,6 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
 }
 
 static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)
-static int g_debug = -1;                      // FP8BS_GEMM_DEBUG, or fp8bs_internal_set_gemm_debug
 
 template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
@@ -568,17 +605,15 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.G = a.G; p.offsets = a.offsets;
     {
-        // band only when the K extent is long (Dgrad-like: measured -2%); Wgrad-like shapes keep
-        // plain m-fastest order (banding measured +4% there)
-        const int64_t band_bytes = a.K > 8192 ? (48ll << 20) : (int64_t)1 << 62;   // A rows kept L2-resident per band
-        int64_t gm = band_bytes / ((int64_t)C::ROWS * a.K);
-        p.gm = (int)(gm < 1 ? 1 : (gm > p.num_m ? p.num_m : gm));
+        // keep the smaller operand resident; band it to ~48 MB of L2 when it is larger than that
+        p.rast_n = a.M > a.N ? 1 : 0;
+        const int64_t res_rows = p.rast_n ? (int64_t)BN : (int64_t)C::ROWS;   // rows per resident tile
+        const int nres = p.rast_n ? p.num_n : p.num_m;
+        int64_t gb = (48ll << 20) / (res_rows * a.K);
+        p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
     }
     {
-        if (g_debug < 0) { const char* e = getenv("FP8BS_GEMM_DEBUG"); g_debug = e ? atoi(e) : 0; }
-        const int dbg = g_debug;
-        p.debug = dbg;
-        if (dbg & 16) {
+        if (kDbg & 16) {
             if (!g_ts) cudaMalloc(&g_ts, kTsSlots * kTsN * sizeof(unsigned long long));
             cudaMemsetAsync(g_ts, 0, kTsSlots * kTsN * sizeof(unsigned long long), st);
             p.ts = g_ts;
@@ -657,5 +692,4 @@ extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_times
 }
 
 // Experiments only: set the GEMM debug bits / variant for subsequent launches in this process.
-extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_debug(int bits) { fp8bs::g_debug = bits; }
 extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_variant(int v) { fp8bs::g_env_variant = v; }

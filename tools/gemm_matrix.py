@@ -3,9 +3,10 @@ C2 grouped shape for several kernel variants and debug bits, all in one process.
 
     FP8BS_LIB=<other .so> python tools/gemm_matrix.py [variants=2,1] [debugs=0,1] [cases=fprop,dgrad,wgrad,grouped_C2]
 
-Debug bits (gemm.cu KParams::debug): 1 skip promotion math, 2 skip MMAs, 4 TMA re-reads K-block 0
-(L2-resident operands), 64 MMA issuer ignores TMEM-slot release, 128 promotion ignores slot completion,
-512 no scale ring.
+Debug bits are compile-time (tools/build_rev.sh WORKTREE <name> -DFP8BS_GEMM_DEBUG_BITS=<bits>, see
+gemm.cu): 1 skip promotion math, 2 skip MMAs, 4 TMA re-reads K-block 0 (L2-resident operands), 8 no TMEM
+reads, 16 timestamps, 64 MMA issuer ignores TMEM-slot release, 128 promotion ignores slot completion,
+256 issuers pace on their own commits, 512 no scale ring.  The debugs argument only labels the rows.
 """
 import ctypes
 import os
@@ -41,7 +42,6 @@ def main():
     only = sys.argv[3].split(",") if len(sys.argv) > 3 else None
     dev = "cuda"
     lib = fp.lib()
-    lib.fp8bs_internal_set_gemm_debug.argtypes = [ctypes.c_int]
     lib.fp8bs_internal_set_gemm_variant.argtypes = [ctypes.c_int]
     T, IN, OUT = 4096, 7168, 18432
     cases = []
@@ -68,13 +68,11 @@ def main():
     for v in variants:
         lib.fp8bs_internal_set_gemm_variant(v)
         for d in debugs:
-            lib.fp8bs_internal_set_gemm_debug(d)
             for name, flop, fn in cases:
                 if only and name not in only:
                     continue
                 ms = timeit(fn)
                 print(f"variant={v} debug={d:4d} {name:11s} {ms * 1e3:8.1f} us  {flop / ms / 1e9:7.0f} TFLOP/s", flush=True)
-    lib.fp8bs_internal_set_gemm_debug(0)
     lib.fp8bs_internal_set_gemm_variant(0)
 
 
