@@ -62,8 +62,12 @@ struct Cfg {
     static constexpr int SB_BYTES = kWgrad ? BN * 4 : 128;
     static constexpr int SSTAGE = SA_BYTES + SB_BYTES;
     static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
-    // Operand stages fill the dynamic shared memory left after the static scale ring and barriers.
-    static constexpr int kStages = (222 * 1024 - kSStages * SSTAGE) / STAGE > 8 ? 8 : (222 * 1024 - kSStages * SSTAGE) / STAGE;
+    // Epilogue: each promotion warp stages 32 rows x 128 bytes (SWIZZLE_128B) for a TMA store.
+    static constexpr int EPI_WARP_BYTES = 32 * 128;
+    // Operand stages fill the dynamic shared memory left after the static scale ring, the epilogue
+    // buffers and the barriers (227 KB per CTA, 1 KB of alignment slack).
+    static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - 8 * EPI_WARP_BYTES;
+    static constexpr int kStages = SMEM_FREE / STAGE > 8 ? 8 : SMEM_FREE / STAGE;
     // 8 promotion warps: warp (h, quad) owns rows [32 quad, 32 quad + 32) x all 128 columns of half h.
     // Fewer, wider warps: the per-K-block barrier/scale overhead is paid once per 128 columns, which
     // keeps the promotion inside the SM's issue budget at tensor-core peak (one K-block = 512 cycles).
@@ -93,6 +97,7 @@ struct KParams {
                                   // 16 record clock64 timestamps of CTA 0, 64 MMA ignores slot release,
                                   // 128 promotion ignores slot completion (with 64: free-running
                                   // TMA + MMA pipeline), 256 issuers pace on their own commits (with 128: MMA + TMA only),
+                                  // 1024 no epilogue stores,
                                   // 512 no scale ring
     unsigned long long* ts;       // [kTsSlots][kTsN] timestamps (debug & 16)
 };
@@ -156,12 +161,13 @@ template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 __global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-          const KParams p) {
+          const __grid_constant__ CUtensorMap tmD, const KParams p) {
     using C = Cfg<kPair, kWgrad>;
     extern __shared__ uint8_t smem_raw[];
     // barriers and the scale ring live in static shared memory: their addresses are constants, so
     // the promotion loop does not re-derive the aligned dynamic base every K-block
     __shared__ __align__(1024) uint8_t s_scale[C::kSStages * C::SSTAGE];
+    __shared__ __align__(1024) uint8_t s_epi[C::NPW * C::EPI_WARP_BYTES];
     __shared__ __align__(8) uint64_t s_bar[C::NBAR];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -190,7 +196,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmSA);
+        tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmSA); tma_prefetch_desc(&tmD);
         if (kWgrad) tma_prefetch_desc(&tmSB);
     }
     if (warp == 2) {
@@ -492,39 +498,75 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (lane == 0 && !((kDbg & 512))) mbar_arrive(sempty_bar(ss));
             }
             // ---------------- epilogue ----------------
-            const int grow = arow + row;
-            if (active && grow < tl.row_end) {
-                const int col0 = tl.n0 + h * HN;
-                if constexpr (kOutF32) {
-                    float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
+            // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or
+            // 64 BF16 columns) in its own SWIZZLE_128B buffer and writes them with asynchronous TMA
+            // stores (reduce-add for Wgrad's D += acc): a warp store used to touch 32 rows at once.
+            // TMA clips rows >= M and columns >= N; a grouped warp whose 32 rows cross the expert's
+            // end stores its rows directly (rows past row_end belong to the next expert).
+            const int grow0 = arow + quad * 32;
+            const int rows_here = tl.row_end - grow0;
+            if (active && rows_here > 0 && !(kDbg & 1024)) {
+                constexpr int ESZ = kOutF32 ? 4 : 2;
+                constexpr int CW = 128 / ESZ;                   // columns per 128-byte chunk
+                if (!kGrouped || rows_here >= 32) {
+                    const uint32_t ebuf = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
 #pragma unroll
-                    for (int i = 0; i < NC / 4; ++i) {
-                        if (col0 + 4 * i < p.N) {
-                            float4 v = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-                            if (p.accumulate) {
-                                const float4 o = *reinterpret_cast<const float4*>(drow + 4 * i);
-                                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                    for (int c = 0; c < NC / CW; ++c) {
+                        if (lane == 0) bulk_wait_group_read<0>();       // the previous chunk's store has read the buffer
+                        __syncwarp();
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {                   // 16-byte units of this lane's row
+                            uint32_t w[4];
+                            if constexpr (kOutF32) {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(acc[c * CW + 4 * u + k]);
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[c * CW + 8 * u + 2 * k], acc[c * CW + 8 * u + 2 * k + 1]);
+                                    w[k] = *reinterpret_cast<uint32_t*>(&b2);
+                                }
                             }
-                            *reinterpret_cast<float4*>(drow + 4 * i) = v;
+                            sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int col = tl.n0 + h * HN + c * CW;
+                            if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, grow0);
+                            else tma_store_2d(&tmD, ebuf, col, grow0);
+                            bulk_commit_group();
                         }
                     }
-                } else {
-                    __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.D) + (int64_t)grow * p.ldd + col0;
+                } else if (row < tl.row_end - arow) {
+                    const int grow = arow + row;
+                    const int col0 = tl.n0 + h * HN;
+                    if constexpr (kOutF32) {
+                        float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
 #pragma unroll
-                    for (int i = 0; i < NC / 8; ++i) {
-                        if (col0 + 8 * i < p.N) {
-                            uint32_t w[4];
+                        for (int i = 0; i < NC / 4; ++i) {
+                            if (col0 + 4 * i < p.N)
+                                *reinterpret_cast<float4*>(drow + 4 * i) = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+                        }
+                    } else {
+                        __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.D) + (int64_t)grow * p.ldd + col0;
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k], acc[8 * i + 2 * k + 1]);
-                                w[k] = *reinterpret_cast<uint32_t*>(&b2);
+                        for (int i = 0; i < NC / 8; ++i) {
+                            if (col0 + 8 * i < p.N) {
+                                uint32_t w[4];
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k], acc[8 * i + 2 * k + 1]);
+                                    w[k] = *reinterpret_cast<uint32_t*>(&b2);
+                                }
+                                *reinterpret_cast<uint4*>(drow + 8 * i) = make_uint4(w[0], w[1], w[2], w[3]);
                             }
-                            *reinterpret_cast<uint4*>(drow + 8 * i) = make_uint4(w[0], w[1], w[2], w[3]);
                         }
                     }
                 }
             }
         }
+        if (lane == 0) bulk_wait_group<0>();           // all TMA stores of this warp complete
     }
     tc_fence_before();
     __syncthreads();
@@ -594,6 +636,16 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     } else {
         tSB = tSA;
     }
+    CUtensorMap tD;
+    {
+        const uint64_t esz = kOutF32 ? 4 : 2;
+        uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)rows};
+        uint64_t str[1] = {(uint64_t)a.ldd * esz};
+        uint32_t box[2] = {(uint32_t)(128 / esz), 32};
+        if (!make_tmap(&tD, kOutF32 ? TMAP_F32 : TMAP_BF16, 2, a.D, dims, str, box, 128)) {
+            *detail = "cuTensorMapEncodeTiled failed for D"; return cudaErrorInvalidValue;
+        }
+    }
     KParams p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
     p.num_m = (int)((a.M + C::ROWS - 1) / C::ROWS); p.num_n = (int)((a.N + BN - 1) / BN);
@@ -646,7 +698,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     at[0].val.clusterDim.x = C::CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, p);
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
 }
