@@ -3,11 +3,11 @@
 
 One STEP = the whole hot path for a Linear W [out=18432, in=7168]
 over T=4096 tokens, synthetic seeded inputs (workloads.py):
-    quantize_act_1x128(X) ; quantize_weight_128x128(W) (+ transposed copy)
+    quantize_act_dual(X)  (1x128 for Fprop + 128x1 for Wgrad, one read of X)
+    quantize_weight_128x128(W) (+ transposed copy for Dgrad)
     Fprop  Y  = Xq  . Wq^T          (BF16 out)
-    quantize_act_1x128(dY)
+    quantize_act_dual(dY) (1x128 for Dgrad + 128x1 for Wgrad, one read of dY)
     Dgrad  dX = dYq . WqT^T         (BF16 out)
-    quantize_act_128x1(dY) ; quantize_act_128x1(X)
     Wgrad  dW = dYqT . XqT^T        (FP32 out)
 value = 3 * 2*T*in*out GEMM FLOP per step / device time (TFLOP/s), whole job over all ranks.
 Multi-GPU (torchrun): the dense step does not shard -> independent replicas, "scaling": "weak".
@@ -108,7 +108,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------------- dense step ----
 class DenseStep:
-    """Preallocated buffers + the 8 launches of one FP8 Linear training step."""
+    """Preallocated buffers + the 6 launches of one FP8 Linear training step."""
 
     def __init__(self, dev, T=T_TOK, IN=D_IN, OUT=D_OUT, seed=0):
         import paper_2412_19437_b200 as fp
@@ -130,16 +130,15 @@ class DenseStep:
         self.xqT, self.sxT = e(IN, T), e(T // 128, p4(IN), dt=f32)[:, :IN]
         self.dw = e(OUT, IN, dt=f32)
         gf = 2.0 * T * IN * OUT
-        B2 = lambda m, k: 2 * m * k + m * k + 4 * m * ((k + 127) // 128)  # noqa: E731  bf16 in, codes + scales out
+        # dual quantizer: bf16 in, codes of both groupings and both scale sets out
+        BD = lambda m, k: 2 * m * k + 2 * m * k + 4 * m * ((k + 127) // 128) + 4 * k * ((m + 127) // 128)  # noqa: E731
         # name -> (callable, kind, algorithmic amount per launch: FLOP for gemm, bytes for quantizers)
         self.launches = [
-            ("quant_act_1x128(X)", self.q_x, "hbm", B2(T, IN)),
+            ("quant_act_dual(X)", self.q_x, "hbm", BD(T, IN)),
             ("quant_weight_128x128(W)+T", self.q_w, "hbm", 4 * OUT * IN + 2 * OUT * IN + 4 * (OUT // 128) * (IN // 128)),
             ("gemm_fprop", self.g_fprop, "tensor", gf),
-            ("quant_act_1x128(dY)", self.q_dy, "hbm", B2(T, OUT)),
+            ("quant_act_dual(dY)", self.q_dy, "hbm", BD(T, OUT)),
             ("gemm_dgrad", self.g_dgrad, "tensor", gf),
-            ("quant_act_128x1(dY)", self.qt_dy, "hbm", B2(T, OUT)),
-            ("quant_act_128x1(X)", self.qt_x, "hbm", B2(T, IN)),
             ("gemm_wgrad", self.g_wgrad, "tensor", gf),
         ]
         self.flops = 3 * gf
@@ -147,7 +146,7 @@ class DenseStep:
         self.d2h_bytes = self.y.numel() * 2 + self.dx.numel() * 2 + self.dw.numel() * 4
 
     def q_x(self):
-        self.fp.quantize_act_1x128(self.x, self.xq, self.sx)
+        self.fp.quantize_act_dual(self.x, self.xq, self.sx, self.xqT, self.sxT)
 
     def q_w(self):
         self.fp.quantize_weight_128x128(self.w, True, self.wq, self.sw, self.wqT)
@@ -156,16 +155,10 @@ class DenseStep:
         self.fp.gemm(self.fp.FPROP, self.xq, self.sx, self.wq, self.sw, out=self.y)
 
     def q_dy(self):
-        self.fp.quantize_act_1x128(self.dy, self.dyq, self.sdy)
+        self.fp.quantize_act_dual(self.dy, self.dyq, self.sdy, self.dyqT, self.sdyT)
 
     def g_dgrad(self):
         self.fp.gemm(self.fp.DGRAD, self.dyq, self.sdy, self.wqT, self.sw, out=self.dx)
-
-    def qt_dy(self):
-        self.fp.quantize_act_128x1(self.dy, self.dyqT, self.sdyT)
-
-    def qt_x(self):
-        self.fp.quantize_act_128x1(self.x, self.xqT, self.sxT)
 
     def g_wgrad(self):
         self.fp.gemm(self.fp.WGRAD, self.dyqT, self.sdyT, self.xqT, self.sxT, out=self.dw)
@@ -342,7 +335,7 @@ def time_dense(args, world, rank, dev):
 
 def time_e2e(args, world, st, dev):
     """Same metric through the public API with host buffers: every step copies X, W, dY from
-    pinned host memory, runs the 8 launches, and copies Y, dX, dW back to pinned host memory."""
+    pinned host memory, runs the 6 launches, and copies Y, dX, dW back to pinned host memory."""
     hx, hw, hdy = st.h_x.pin_memory(), st.h_w.pin_memory(), st.h_dy.pin_memory()
     hy = torch.empty(st.y.shape, dtype=st.y.dtype).pin_memory()
     hdx = torch.empty(st.dx.shape, dtype=st.dx.dtype).pin_memory()

@@ -93,6 +93,19 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, 
                                       uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
                                       fp8bs_stream_t stream);
 
+/* ---- quantize_act_dual: 1x128 AND 128x1 groupings of one activation from a single read -------
+ * The same outputs as fp8bs_quantize_act_1x128(x -> q, s) followed by
+ * fp8bs_quantize_act_128x1(x -> qT, sT), bit for bit (P:508 groupings, P:558 / P:1568-1569 128x1
+ * tiles for Wgrad).  A training step needs both groupings of X (Fprop, Wgrad) and of dY (Dgrad,
+ * Wgrad); reading x once follows the paper's call to fuse the FP8 cast with the memory access
+ * (§3.5.2).  Fused for BF16 x with 16-byte aligned rows and K % 16 == 0; otherwise it
+ * runs the two single-grouping kernels.  Layouts, ownership and errors as the two calls above
+ * (ldx >= K, ldq >= K, lds >= M, ldqT >= M, ldsT >= K). */
+FP8BS_API fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                     uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                     uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
+                                     fp8bs_stream_t stream);
+
 /* ---- quantize_weight_128x128 ("per 128 input channels per 128 output channels") ----
  * w   : [N, K] weights (FP32 master weights, or BF16), ldw >= K.
  * q   : [N, K] uint8 codes, ldq >= K.

@@ -50,6 +50,8 @@ def lib() -> ctypes.CDLL:
         L.fp8bs_quantize_act_128x1.restype = st
         L.fp8bs_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
         L.fp8bs_quantize_weight_128x128.restype = st
+        L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_quantize_act_dual.restype = st
         L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
         L.fp8bs_gemm.restype = st
         L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
@@ -141,6 +143,24 @@ def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torc
     _check(lib().fp8bs_quantize_act_128x1(_p(x), _dt(x), M, C, x.stride(0), _p(qT), qT.stride(0), _p(sT),
                                           sT.stride(0), _stream(x)), "fp8bs_quantize_act_128x1")
     return qT, sT
+
+
+def quantize_act_dual(x: torch.Tensor, q=None, s=None, qT=None, sT=None):
+    """x [M,K] -> (q [M,K], s [ceil(K/128), M], qT [K,M], sT [ceil(M/128), K]): both groupings from one
+    read of x (bit-identical to quantize_act_1x128 + quantize_act_128x1)."""
+    _cuda2d(x, "x")
+    M, K = x.shape
+    if q is None:
+        q = torch.empty(M, K, dtype=torch.uint8, device=x.device)
+    if s is None:
+        s = torch.empty((K + 127) // 128, _pad4(M), dtype=torch.float32, device=x.device)[:, :M]
+    if qT is None:
+        qT = torch.empty(K, M, dtype=torch.uint8, device=x.device)
+    if sT is None:
+        sT = torch.empty((M + 127) // 128, _pad4(K), dtype=torch.float32, device=x.device)[:, :K]
+    _check(lib().fp8bs_quantize_act_dual(_p(x), _dt(x), M, K, x.stride(0), _p(q), q.stride(0), _p(s), s.stride(0),
+                                         _p(qT), qT.stride(0), _p(sT), sT.stride(0), _stream(x)), "fp8bs_quantize_act_dual")
+    return q, s, qT, sT
 
 
 def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None, qT=None):

@@ -120,6 +120,21 @@ fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, int64_t M,
                      "quantize_act_128x1 launch");
 }
 
+fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                    uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+    if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
+    if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
+    if (M == 0 || K == 0) return ok();
+    if (!x || !q || !s || !qT || !sT) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldx < K || ldq < K || lds < M || ldqT < M || ldsT < K)
+        return fail(FP8BS_ERR_SHAPE, "need ldx>=K, ldq>=K, lds>=M, ldqT>=M, ldsT>=K");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_quant_act_dual(x, (int)xdt, M, K, ldx, q, ldq, s, lds, qT, ldqT, sT, ldsT, (cudaStream_t)stream),
+                     "quantize_act_dual launch");
+}
+
 fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
                                            uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                            uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {

@@ -337,7 +337,7 @@ struct QTCfg {
     static constexpr int CH = 256 / (int)sizeof(T);         // channels per tile: 128 BF16 / 64 FP32
     static constexpr int CPW = 4 / (int)sizeof(T);          // channels per 32-bit word
     static constexpr int TILE_BYTES = 128 * 256;
-    static constexpr int STAGES = 3;
+    static constexpr int STAGES = 2;                        // 84 KB per CTA: two CTAs (16 consumer warps) per SM
     static constexpr int CONSUMERS = 8;
     static constexpr int THREADS = 32 * (CONSUMERS + 1);
     static constexpr int QSTR = 144;
@@ -362,7 +362,7 @@ __device__ __forceinline__ float word_elem(uint32_t w, int j) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(QTCfg<T>::THREADS)
+__global__ void __launch_bounds__(QTCfg<T>::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
 k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C, uint8_t* __restrict__ qT,
                       int64_t ldq, float* __restrict__ sT, int64_t lds) {
     using P = QTCfg<T>;
@@ -453,6 +453,145 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
             if (c < C && m < M) {
                 const uint4 val = lds128(sbase + P::OFF_Q + chl * P::QSTR + pk * 16);
                 uint8_t* dst = qT + c * ldq + m;
+                if (m + 16 <= M) {
+                    *reinterpret_cast<uint4*>(dst) = val;
+                } else {
+                    const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
+                    for (int e = 0; e < 16 && m + e < M; ++e) dst[e] = b[e];
+                }
+            }
+        }
+    }
+}
+
+// ===========================================================================================
+// Dual 1x128 + 128x1 activation quantization from ONE read of a BF16 tile (the paper, §3.5.2
+// P:672-673, asks for the FP8 cast to be fused with the memory access; a training step needs both
+// groupings of X and of dY).  Same TMA ring and 128x1 column path as k_quant_act_128x1_tma; before a
+// stage is released the 8 consumer warps also quantize its 128 rows along the channels (a BF16 tile
+// is exactly one 128-wide K group per row): 8 lanes per row, 16 elements per lane, shuffle amax,
+// 16-byte code stores (128-byte row segments) and one coalesced 512-byte scale vector per tile.
+// Outputs are bit-identical to the two separate kernels.
+// ===========================================================================================
+__global__ void __launch_bounds__(QTCfg<__nv_bfloat16>::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
+k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C,
+                     uint8_t* __restrict__ q, int64_t ldq, float* __restrict__ s, int64_t lds,
+                     uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
+    using T = __nv_bfloat16;
+    using P = QTCfg<T>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + P::OFF_BAR;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < P::STAGES; ++i) { mbar_init(bar0 + 8 * i, 1); mbar_init(bar0 + 8 * (P::STAGES + i), P::CONSUMERS); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int MB = (int)((M + 127) >> 7), NCB = (int)((C + P::CH - 1) / P::CH);
+    const int ntiles = MB * NCB;
+    if (warp == P::CONSUMERS) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmX);
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int st = it % P::STAGES;
+                mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
+                mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
+                tma_load_2d(sbase + st * P::TILE_BYTES, &tmX, bar0 + 8 * st, (t % NCB) * P::CH, (t / NCB) * 128);
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x, wc = tid & 63, rg = tid >> 6;
+    const int sub = lane >> 3, li = lane & 7;          // row phase: 4 rows per warp pass, 8 lanes per row
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % P::STAGES;
+        const int mb = t / NCB, cb = t - mb * NCB;
+        const int64_t m0 = (int64_t)mb * 128, c0 = (int64_t)cb * P::CH;
+        const uint32_t tile = sbase + st * P::TILE_BYTES;
+        mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
+        // ---- 1x128 along the channels: rows of the tile ----
+#pragma unroll 1
+        for (int pass = 0; pass < 4; ++pass) {
+            const int row = pass * 32 + warp * 4 + sub;
+            float f[16];
+            Vec<T>::unpack(lds128(tile + row * 256 + li * 32), f);
+            Vec<T>::unpack(lds128(tile + row * 256 + li * 32 + 16), f + 8);
+            float amax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) amax = fmaxf(amax, fabsf(f[e]));
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const float sc = group_scale(amax);
+            const float r = __frcp_rn(sc);
+            uint32_t w4[4];
+            if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w4);   // warp-uniform
+            else encode_chunk<16>(f, sc, r, false, w4);
+            const int64_t m = m0 + row, c = c0 + li * 16;
+            if (m < M) {
+                if (c < C) *reinterpret_cast<uint4*>(q + m * ldq + c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                if (li == 0) s[(int64_t)cb * lds + m] = sc;
+            }
+        }
+        // ---- 128x1 along the tokens: columns of the tile (as k_quant_act_128x1_tma) ----
+        uint32_t w[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) w[r] = lds32(tile + (rg * 32 + r) * 256 + wc * 4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
+        float sc[P::CPW];
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            float a = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) a = fmaxf(a, fabsf(word_elem<T>(w[r], j)));
+            reinterpret_cast<float*>(smem + P::OFF_RED)[rg * P::CH + wc * P::CPW + j] = a;
+        }
+        named_bar_sync(1, 32 * P::CONSUMERS);
+        bool fast = true;
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            const int ch = wc * P::CPW + j;
+            const float* red = reinterpret_cast<const float*>(smem + P::OFF_RED);
+            const float a = fmaxf(fmaxf(red[ch], red[P::CH + ch]), fmaxf(red[2 * P::CH + ch], red[3 * P::CH + ch]));
+            sc[j] = group_scale(a);
+            fast = fast && fast_div_ok(sc[j]);
+            if (rg == 0 && c0 + ch < C) sT[(int64_t)mb * ldsT + c0 + ch] = sc[j];
+        }
+        fast = __all_sync(0xffffffffu, fast);
+#pragma unroll
+        for (int j = 0; j < P::CPW; ++j) {
+            const float r = __frcp_rn(sc[j]);
+            uint32_t code[8];
+            if (fast) {
+                const float2 r2 = make_float2(r, r), ns2 = make_float2(-sc[j], -sc[j]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float2 a = div_scale2_fast(make_float2(word_elem<T>(w[4 * k], j), word_elem<T>(w[4 * k + 1], j)), r2, ns2);
+                    const float2 b = div_scale2_fast(make_float2(word_elem<T>(w[4 * k + 2], j), word_elem<T>(w[4 * k + 3], j)), r2, ns2);
+                    code[k] = cvt_e4m3x2(a.x, a.y) | (cvt_e4m3x2(b.x, b.y) << 16);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    code[k] = cvt_e4m3x2(__fdiv_rn(word_elem<T>(w[4 * k], j), sc[j]), __fdiv_rn(word_elem<T>(w[4 * k + 1], j), sc[j])) |
+                              (cvt_e4m3x2(__fdiv_rn(word_elem<T>(w[4 * k + 2], j), sc[j]), __fdiv_rn(word_elem<T>(w[4 * k + 3], j), sc[j])) << 16);
+                }
+            }
+            const uint32_t qa = sbase + P::OFF_Q + (wc * P::CPW + j) * P::QSTR + rg * 32;
+            sts128(qa, make_uint4(code[0], code[1], code[2], code[3]));
+            sts128(qa + 16, make_uint4(code[4], code[5], code[6], code[7]));
+        }
+        named_bar_sync(1, 32 * P::CONSUMERS);
+#pragma unroll
+        for (int i = 0; i < P::CH * 8 / (32 * P::CONSUMERS); ++i) {
+            const int idx = i * 32 * P::CONSUMERS + tid, chl = idx >> 3, pk = idx & 7;
+            const int64_t c = c0 + chl, m = m0 + pk * 16;
+            if (c < C && m < M) {
+                const uint4 val = lds128(sbase + P::OFF_Q + chl * P::QSTR + pk * 16);
+                uint8_t* dst = qT + c * ldqT + m;
                 if (m + 16 <= M) {
                     *reinterpret_cast<uint4*>(dst) = val;
                 } else {
@@ -827,6 +966,37 @@ cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C,
                                    int64_t ldq, float* sT, int64_t lds, cudaStream_t st) {
     if (xdt == 0) return launch_128x1_t<__nv_bfloat16>(x, M, C, ldx, qT, ldq, sT, lds, st);
     return launch_128x1_t<float>(x, M, C, ldx, qT, ldq, sT, lds, st);
+}
+
+cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
+                                  float* s, int64_t lds, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
+                                  cudaStream_t st) {
+    using Q = QTCfg<__nv_bfloat16>;
+    // fused path: BF16 (a 128-channel tile row is one 1x128 group), 16-byte aligned rows and codes
+    bool fused = xdt == 0 && aligned16(x) && ((ldx * 2) % 16 == 0) && (K % 16 == 0) && aligned16(q) && (ldq % 16 == 0) &&
+                 aligned16(qT) && (ldqT % 16 == 0) && (M * ((K + Q::CH - 1) / Q::CH) / 128 < (1ll << 31));
+    alignas(64) CUtensorMap tm;
+    if (fused) {
+        const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
+        const uint64_t str[1] = {(uint64_t)ldx * 2};
+        const uint32_t box[2] = {(uint32_t)Q::CH, 128};
+        fused = make_tmap(&tm, TMAP_BF16, 2, x, dims, str, box, 0);
+    }
+    if (!fused) {   // two passes over x
+        cudaError_t e = launch_quant_act_1x128(x, xdt, M, K, ldx, q, ldq, s, lds, st);
+        if (e != cudaSuccess) return e;
+        return launch_quant_act_128x1(x, xdt, M, K, ldx, qT, ldqT, sT, ldsT, st);
+    }
+    static bool attr[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+        cudaFuncSetAttribute(k_quant_act_dual_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    const int64_t tiles = ((M + 127) / 128) * ((K + Q::CH - 1) / Q::CH);
+    k_quant_act_dual_tma<<<grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st>>>(tm, M, K, q, ldq, s, lds, qT, ldqT, sT, ldsT);
+    return cudaPeekAtLastError();
 }
 
 template <typename T>

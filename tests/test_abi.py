@@ -46,6 +46,12 @@ def test_quantize_validation():
     lib = fp.lib()
     assert lib.fp8bs_quantize_act_128x1(FAKE, 0, 10, 8, 8, FAKE, 5, FAKE, 8, None) == L.ERR_SHAPE   # ldq < M
     assert lib.fp8bs_quantize_weight_128x128(FAKE, 1, 10, 300, 300, FAKE, 300, FAKE, 2, None, 0, None) == L.ERR_SHAPE
+    # dual: every output is required and every leading dimension checked
+    assert lib.fp8bs_quantize_act_dual(FAKE, 0, 10, 8, 8, FAKE, 8, FAKE, 10, None, 10, FAKE, 8, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_quantize_act_dual(FAKE, 0, 10, 8, 8, FAKE, 8, FAKE, 10, FAKE, 9, FAKE, 8, None) == L.ERR_SHAPE   # ldqT < M
+    assert lib.fp8bs_quantize_act_dual(FAKE, 0, 10, 8, 8, FAKE, 8, FAKE, 10, FAKE, 10, FAKE, 7, None) == L.ERR_SHAPE  # ldsT < K
+    assert lib.fp8bs_quantize_act_dual(FAKE, 3, 10, 8, 8, FAKE, 8, FAKE, 10, FAKE, 10, FAKE, 8, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_quantize_act_dual(FAKE, 0, 0, 8, 8, FAKE, 8, FAKE, 10, FAKE, 10, FAKE, 8, None) == L.OK
     assert lib.fp8bs_quantize_weight_128x128(FAKE, 1, 10, 300, 300, FAKE, 300, FAKE, 3, FAKE, 5, None) == L.ERR_SHAPE
 
 

@@ -116,6 +116,31 @@ def test_quantize_act_128x1_bitexact(name, M, C, kind, dtype):
     assert_bits_equal(q, q_ref, "codes")
 
 
+DUAL_CASES = [
+    ("tiny_C0", 128, 256, "gauss", torch.bfloat16),
+    ("ragged_fused", 300, 1104, "outlier", torch.bfloat16),    # M % 128, K % 128 != 0, K % 16 == 0: fused
+    ("specials_fused", 64, 640, "special", torch.bfloat16),
+    ("odd_K_fallback", 37, 1001, "gauss", torch.bfloat16),     # K % 16 != 0: two-kernel fallback
+    ("fp32_fallback", 130, 384, "outlier", torch.float32),
+    ("C1_dY", 4096, 18432, "gauss", torch.bfloat16),
+    ("C3_X_outlier", 2048, 7168, "outlier", torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("name,M,K,kind,dtype", DUAL_CASES, ids=[c[0] for c in DUAL_CASES])
+def test_quantize_act_dual_bitexact(name, M, K, kind, dtype):
+    """Both groupings from one read: bit-exact vs the oracle's 1x128 and 128x1 quantizers."""
+    x = make_act(kind, M, K, dtype, seed=4)
+    q_ref, s_ref = oracle.quantize_act_1x128(x)
+    qT_ref, sT_ref = oracle.quantize_act_128x1(x)
+    q, s, qT, sT = fp.quantize_act_dual(dev(x))
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "1x128 scales")
+    assert_bits_equal(q, q_ref, "1x128 codes")
+    assert_bits_equal(sT, sT_ref, "128x1 scales")
+    assert_bits_equal(qT, qT_ref, "128x1 codes")
+
+
 W_CASES = [
     ("C0", 128, 256, torch.float32),
     ("ragged", 300, 200, torch.float32),

@@ -14,5 +14,5 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c
     --log-file $OUT/launches_$TAG.csv $PROF > $OUT/ncu_launches_$TAG.log 2>&1; echo "ncu launches rc=$?"
 timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm_bs -s 9 -c 3 \
     -o $OUT/prof_gemm_$TAG $PROF > $OUT/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
-timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 15 -c 5 \
+timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 9 -c 3 \
     -o $OUT/prof_quant_$TAG $PROF > $OUT/ncu_quant_$TAG.log 2>&1; echo "ncu quant rc=$?"
