@@ -50,8 +50,9 @@ def lib() -> ctypes.CDLL:
         L.fp8bs_quantize_act_128x1.restype = st
         L.fp8bs_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
         L.fp8bs_quantize_weight_128x128.restype = st
-        L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
-        L.fp8bs_quantize_act_dual.restype = st
+        if hasattr(L, "fp8bs_quantize_act_dual"):   # (older builds, loaded via FP8BS_LIB for A/B runs, lack it)
+            L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+            L.fp8bs_quantize_act_dual.restype = st
         L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
         L.fp8bs_gemm.restype = st
         L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
