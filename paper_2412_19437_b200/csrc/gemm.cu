@@ -38,6 +38,10 @@ constexpr int BN = 256;               // tile columns, issued as two N = 128 MMA
 constexpr int HN = 128;               // columns per half (= one TMEM slot, = one weight block)
 constexpr int kMaxGroups = 1024;
 
+#ifndef FP8BS_NPW
+#define FP8BS_NPW 8
+#endif
+
 template <bool kPair, bool kWgrad>
 struct Cfg {
     static constexpr int CS = kPair ? 2 : 1;                // CTAs per cluster
@@ -66,19 +70,21 @@ struct Cfg {
     static constexpr int EPI_WARP_BYTES = 32 * 128;
     // Operand stages fill the dynamic shared memory left after the static scale ring, the epilogue
     // buffers and the barriers (227 KB per CTA, 1 KB of alignment slack).
-    static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - 8 * EPI_WARP_BYTES;
+    static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - FP8BS_NPW * EPI_WARP_BYTES;
     static constexpr int kStages = SMEM_FREE / STAGE > 8 ? 8 : SMEM_FREE / STAGE;
-    // 8 promotion warps: warp (h, quad) owns rows [32 quad, 32 quad + 32) x all 128 columns of half h.
-    // Fewer, wider warps: the per-K-block barrier/scale overhead is paid once per 128 columns, which
-    // keeps the promotion inside the SM's issue budget at tensor-core peak (one K-block = 512 cycles).
-    static constexpr int NPW = 8;
-    static constexpr int THREADS = 128 + 32 * NPW;          // 384
-    static constexpr int NC = HN;                           // columns per promotion thread (128)
-    static constexpr int REG_LAUNCH = 168;                  // 65536 / 384 rounded down to 8
-    static constexpr int REG_OTHER = 24, REG_PROMO = 240;   // setmaxnreg split of the CTA's 168 x 384 registers
+    // Promotion warps (FP8BS_NPW, 8 or 16): warp (h, gg, quad) owns rows [32 quad, 32 quad + 32) x
+    // NC = 128 * 8 / NPW columns (group gg) of half h.  8 wide warps pay the per-K-block barrier and
+    // scale overhead once per 128 columns; 16 narrower warps halve each warp's FFMA2 chain.
+    static constexpr int NPW = FP8BS_NPW;
+    static_assert(NPW == 8 || NPW == 16, "8 or 16 promotion warps");
+    static constexpr int THREADS = 128 + 32 * NPW;          // 384 / 640
+    static constexpr int NC = HN * 8 / NPW;                 // columns per promotion thread (128 / 64)
+    static constexpr int REG_LAUNCH = NPW == 8 ? 168 : 96;  // 65536 / THREADS rounded down to 8
+    static constexpr int REG_OTHER = 24, REG_PROMO = NPW == 8 ? 240 : 112;   // setmaxnreg split of the launch pool
     static_assert((REG_LAUNCH - REG_OTHER) * 128 >= (REG_PROMO - REG_LAUNCH) * 32 * NPW, "setmaxnreg.inc would wait forever: the CTA's pool is fixed at launch");
     static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NSLOT;
-    static constexpr int SMEM_DENSE = 1024 + kStages * STAGE;
+    static constexpr int OFF_EPI = kStages * STAGE;
+    static constexpr int SMEM_DENSE = 1024 + OFF_EPI + NPW * EPI_WARP_BYTES;
     static constexpr int SMEM_GROUPED = SMEM_DENSE + 2 * (kMaxGroups + 1) * 4;
 };
 
@@ -151,7 +157,10 @@ __device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cu
     const int seg = off[e + 1] - off[e];
     const int mt = (seg + ROWS - 1) / ROWS;
     const int local = t - cum[e];
-    const int m = local % mt, n = local / mt;
+    // per expert, keep the smaller operand L2-resident: an expert with more rows than N walks its
+    // n-tiles fastest (its A rows are read once, B_e stays in L2); small experts walk m fastest
+    const bool nfast = seg > p.N;
+    const int m = nfast ? local / p.num_n : local % mt, n = nfast ? local % p.num_n : local / mt;
     tl.row0 = off[e] + m * ROWS; tl.row_end = off[e + 1]; tl.n0 = n * BN; tl.e = e;
     tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
     return true;
@@ -167,7 +176,6 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // barriers and the scale ring live in static shared memory: their addresses are constants, so
     // the promotion loop does not re-derive the aligned dynamic base every K-block
     __shared__ __align__(1024) uint8_t s_scale[C::kSStages * C::SSTAGE];
-    __shared__ __align__(1024) uint8_t s_epi[C::NPW * C::EPI_WARP_BYTES];
     __shared__ __align__(8) uint64_t s_bar[C::NBAR];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -181,7 +189,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
     auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NSLOT + b); };
     uint32_t* tmem_slot = &s_tmem;
-    int* cum = reinterpret_cast<int*>(smem + C::kStages * C::STAGE);
+    uint8_t* s_epi = smem + C::OFF_EPI;                // epilogue staging (1024-aligned, dynamic)
+    int* cum = reinterpret_cast<int*>(smem + C::OFF_EPI + C::NPW * C::EPI_WARP_BYTES);
     int* off = cum + (kMaxGroups + 1);
 
     // warp index broadcast from lane 0 so the compiler knows role branches are warp-uniform
@@ -385,13 +394,14 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         setmaxnreg_inc<C::REG_PROMO>();
         // ---------------- promotion + epilogue ----------------
         // Warps 4..7 promote half 0, warps 8..11 half 1 (each SMSP runs one warp of each half).
-        const int h = (warp - 4) >> 2;                  // half
+        const int h = (warp - 4) / (C::NPW / 2);        // half
+        const int gg = ((warp - 4) >> 2) % (C::NPW / 8); // column group within the half
         const int quad = warp & 3;                      // TMEM lane quadrant
         const int row = quad * 32 + lane;               // row within this CTA's 128
-        constexpr int NC = C::NC;                       // 128
+        constexpr int NC = C::NC;                       // 128 / 64
         float acc[NC];
-        const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16);
-        const uint32_t sb_off = C::SA_BYTES + 4u * (kWgrad ? h * HN : h);
+        const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + gg * NC;
+        const uint32_t sb_off = C::SA_BYTES + 4u * (kWgrad ? h * HN + gg * NC : h);
         int sit = 0, qh = 0;                            // K-block, slot uses of this half
         Tile tl;
         for (int t = cid; next_tile(t, tl); t += ncl) {
@@ -436,7 +446,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         if constexpr (!kWgrad) {
                             const float2 f2 = make_float2(f, f);
 #pragma unroll
-                            for (int j = 0; j < 32; j += 2) {
+                            for (int j = 0; j < ((kDbg & 4096) ? 16 : 32); j += 2) {   // 4096: half the math (experiment)
                                 const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
                                                             make_float2(acc[c0 + j], acc[c0 + j + 1]));
                                 acc[c0 + j] = a.x; acc[c0 + j + 1] = a.y;
@@ -466,19 +476,30 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                         goto half_done;
                     }
-                    // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
-                    // soon as the second round has landed (32 FFMA2 after the first wait)
                     uint32_t r0[32], r1[32];
-                    FP8BS_TMEM_LD32(ta, r0);
-                    FP8BS_TMEM_LD32(ta + 32, r1);
-                    tmem_ld_wait();
-                    fma32(r0, 0);
-                    fma32(r1, 32);
+                    if constexpr (NC == 128) {
+                        // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
+                        // soon as the second round has landed (32 FFMA2 after the first wait)
+                        FP8BS_TMEM_LD32(ta, r0);
+                        FP8BS_TMEM_LD32(ta + 32, r1);
+                        tmem_ld_wait();
+                        fma32(r0, 0);
+                        fma32(r1, 32);
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
-                    FP8BS_TMEM_LD32(ta + 64, r0);
-                    FP8BS_TMEM_LD32(ta + 96, r1);
-                    tmem_ld_wait();
+                        for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
+                        FP8BS_TMEM_LD32(ta + 64, r0);
+                        FP8BS_TMEM_LD32(ta + 96, r1);
+                        tmem_ld_wait();
+                    } else {
+                        // 64 columns: one 32-column round, its math, then the second round
+                        FP8BS_TMEM_LD32(ta, r0);
+                        tmem_ld_wait();
+                        fma32(r0, 0);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) asm volatile("" : "+f"(acc[j]));
+                        FP8BS_TMEM_LD32(ta + 32, r1);
+                        tmem_ld_wait();
+                    }
                     // release the slot before the last math: the registers hold this warp's part now.
                     // tcgen05.wait::ld is warp-collective, so one elected lane may arrive; ptxas schedules
                     // Wgrad better with elect.sync and Fprop/Dgrad better with lane 0 after __syncwarp
@@ -499,8 +520,12 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
                         if (kTrace && warp == 7) FP8BS_TS(7, sit);
                     }
-                    fma32(r0, 64);
-                    fma32(r1, 96);
+                    if constexpr (NC == 128) {
+                        fma32(r0, 64);
+                        fma32(r1, 96);
+                    } else {
+                        fma32(r1, 32);
+                    }
                 half_done:;
                 }
                 if (elect_one() && !((kDbg & 512))) mbar_arrive(sempty_bar(ss));
@@ -545,7 +570,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            const int col = tl.n0 + h * HN + c * CW;
+                            const int col = tl.n0 + h * HN + gg * NC + c * CW;
                             if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, grow0);
                             else tma_store_2d(&tmD, ebuf, col, grow0);
                             bulk_commit_group();
@@ -553,7 +578,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                 } else if (row < tl.row_end - arow) {
                     const int grow = arow + row;
-                    const int col0 = tl.n0 + h * HN;
+                    const int col0 = tl.n0 + h * HN + gg * NC;
                     if constexpr (kOutF32) {
                         float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
 #pragma unroll
