@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstddef>
 #include <cstdlib>
 
 #include "sm100.cuh"
@@ -115,6 +116,9 @@ constexpr int kTsSlots = 12;
 #ifndef FP8BS_ISSUER_POLL
 #define FP8BS_ISSUER_POLL 0
 #endif
+#ifndef FP8BS_REL_MODE
+#define FP8BS_REL_MODE 0
+#endif
 #ifndef FP8BS_GEMM_DEBUG_BITS
 #define FP8BS_GEMM_DEBUG_BITS 0
 #endif
@@ -175,20 +179,29 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     extern __shared__ uint8_t smem_raw[];
     // barriers and the scale ring live in static shared memory: their addresses are constants, so
     // the promotion loop does not re-derive the aligned dynamic base every K-block
-    __shared__ __align__(1024) uint8_t s_scale[C::kSStages * C::SSTAGE];
-    __shared__ __align__(8) uint64_t s_bar[C::NBAR];
-    __shared__ uint32_t s_tmem;
+    // one static block (scale ring, barriers, TMEM address): every static shared address is a
+    // constant offset from one pinned base register
+    struct __align__(1024) StaticSmem {
+        uint8_t scale[C::kSStages * C::SSTAGE];
+        uint64_t bar[C::NBAR];
+        uint32_t tmem;
+    };
+    __shared__ StaticSmem s_static;
+    uint8_t* s_scale = s_static.scale;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar0 = smem_u32(s_bar);
-    const uint32_t sring = smem_u32(s_scale);
+    // Wgrad: pinned (ptxas otherwise re-derives the base with S2UR SR_CgaCtaId at every use in the
+    // promotion loop: 292 -> 259 instructions per K-block).  Fprop/Dgrad: the pinned base costs the
+    // register that makes ptxas spill accumulators, so the base stays rematerializable there.
+    const uint32_t sring = kWgrad ? smem_u32_pinned(&s_static) : smem_u32(&s_static);
+    const uint32_t bar0 = sring + (uint32_t)offsetof(StaticSmem, bar);
     auto full_bar   = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar  = [&](int s) { return bar0 + 8u * (C::kStages + s); };
     auto sfull_bar  = [&](int s) { return bar0 + 8u * (2 * C::kStages + s); };
     auto sempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + C::kSStages + s); };
     auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
     auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NSLOT + b); };
-    uint32_t* tmem_slot = &s_tmem;
+    uint32_t* tmem_slot = &s_static.tmem;
     uint8_t* s_epi = smem + C::OFF_EPI;                // epilogue staging (1024-aligned, dynamic)
     int* cum = reinterpret_cast<int*>(smem + C::OFF_EPI + C::NPW * C::EPI_WARP_BYTES);
     int* off = cum + (kMaxGroups + 1);
@@ -407,6 +420,18 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int t = cid; next_tile(t, tl); t += ncl) {
             const int arow = tl.row0 + (int)rank * BM;
             const bool active = h < tl.nh;
+            if (kWgrad && !active) {
+                // this half lies past N (last column tile): only keep the scale ring moving.  A
+                // separate loop keeps the tile-dependent test out of Wgrad's promotion loop below
+                // (Fprop/Dgrad: ptxas then spills accumulators, so they test per K-block).
+                for (int kb = 0; kb < p.KB; ++kb, ++sit) {
+                    if (!(kDbg & 512)) {
+                        mbar_wait(sfull_bar(sit & (C::kSStages - 1)), (sit / C::kSStages) & 1);
+                        if (elect_one()) mbar_arrive(sempty_bar(sit & (C::kSStages - 1)));
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
             for (int kb = 0; kb < p.KB; ++kb, ++sit) {
@@ -415,7 +440,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (!(kDbg & 512)) mbar_wait(sfull_bar(ss), sph);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(11, sit);
                 const uint32_t sst = sring + ss * C::SSTAGE;
-                if (active) {
+                if (kWgrad || active) {
                     const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
                     // Fprop/Dgrad: half h is exactly weight block n0/128 + h (n0 is a multiple of 256),
                     // so one factor sA(kb,row) * sB(kb, block) per warp: one FFMA per element.
@@ -506,7 +531,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     // (measured: Wgrad +8% / Fprop -13% with elect)
                     tc_fence_before();
                     bool rel_lane;
-                    if constexpr (kWgrad) {
+                    if constexpr (kWgrad || FP8BS_REL_MODE == 1) {
                         rel_lane = elect_one();
                     } else {
                         __syncwarp();
@@ -519,6 +544,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         else mbar_arrive(pempty_bar(pb));
                         if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
                         if (kTrace && warp == 7) FP8BS_TS(7, sit);
+                    }
+                    if constexpr (!kWgrad && FP8BS_REL_MODE == 2) {
+                        // re-read the factor after the release: the shared loads stay behind the
+                        // arrive, so ptxas cannot hoist the last math above the slot release
+                        f = __fmul_rn(lds_f32(sst + 4u * ((arow & 3) + row)), lds_f32(sst + sb_off));
                     }
                     if constexpr (NC == 128) {
                         fma32(r0, 64);

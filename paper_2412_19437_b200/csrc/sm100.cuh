@@ -63,6 +63,14 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// The same conversion as an opaque (volatile) instruction: the compiler keeps the result in a
+// register instead of sinking a fresh cvta (S2UR SR_CgaCtaId + ULEA in a cluster launch) into every
+// use inside hot loops.
+__device__ __forceinline__ uint32_t smem_u32_pinned(const void* p) {
+    uint32_t r;
+    asm volatile("{\n\t.reg .u64 t;\n\tcvta.to.shared.u64 t, %1;\n\tcvt.u32.u64 %0, t;\n\t}" : "=r"(r) : "l"(p));
+    return r;
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");

@@ -65,6 +65,15 @@ def main():
     o2 = offs.to(dev)
     out2 = torch.empty(R, N2, dtype=torch.bfloat16, device=dev)
     cases.append(("grouped_C2", 2.0 * R * N2 * K2, lambda: fp.grouped_gemm(o2, A2, sA2, B2, sB2, out=out2)))
+    if only and "grouped_C4" in only:
+        # C4 at one GPU: 65536 tokens x top-8, skewed routing (alpha 0.5), all 256 experts
+        _, offs4 = W.group_rows(W.route_skewed(65536, E, 8), E)
+        R4 = int(offs4[-1])
+        A4 = torch.randint(0, 120, (R4, K2), dtype=torch.uint8, device=dev)
+        sA4 = torch.rand(K2 // 128, R4, device=dev)
+        o4 = offs4.to(dev)
+        out4 = torch.empty(R4, N2, dtype=torch.bfloat16, device=dev)
+        cases.append(("grouped_C4", 2.0 * R4 * N2 * K2, lambda: fp.grouped_gemm(o4, A4, sA4, B2, sB2, out=out4)))
     for v in variants:
         lib.fp8bs_internal_set_gemm_variant(v)
         for d in debugs:
