@@ -25,24 +25,28 @@ __device__ __forceinline__ bool fast_div_ok(float s) {
     return s >= 0x1p-90f && s <= 0x1p+100f;
 }
 
-// RN32(x / s): with r = RN32(1/s), q0 = RN(x*r), e = x - q0*s (exact by FMA), q1 = RN(q0 + e*r)
-// (Markstein's correction).  copysign restores the sign of zero / underflowed quotients.
+// RN32(x / s): with r = RN32(1/s), q0 = RN(x*r), the residual x - q0*s is exact by FMA, and
+// q1 = RN(q0 + residual*r) (Markstein's correction).  The residual is formed NEGATED,
+// en = RN(q0*s - x) = -RN(x - q0*s) (round-to-nearest is sign-symmetric), and applied as
+// q1 = RN(q0 - en*r): the same value for every nonzero quotient, and the sign of zero now follows
+// x (x = -0: en = +0 and q1 = -0*r + -0 = -0), so no copysign is needed.  Negations are free FFMA
+// operand modifiers: 3 FP instructions per element pair in the packed form.
 __device__ __forceinline__ float div_scale(float x, float s, float r, bool fast) {
     if (fast) {
-        float q0 = __fmul_rn(x, r);
-        float e = __fmaf_rn(-q0, s, x);
-        float q1 = __fmaf_rn(e, r, q0);
-        return copysignf(q1, x);
+        const float q0 = __fmul_rn(x, r);
+        const float en = __fmaf_rn(q0, s, -x);
+        return __fmaf_rn(-en, r, q0);
     }
     return __fdiv_rn(x, s);
 }
 
-// Packed (FMUL2/FFMA2) form of div_scale for two elements; ns = -s so that x - q0*s is one FFMA2.
+// Packed (FMUL2/FFMA2) form of div_scale for two elements.  ns2 = -s (kept for the callers'
+// signature): en = q0*s - x = -(q0*ns2 + x).
 __device__ __forceinline__ float2 div_scale2_fast(float2 x, float2 r2, float2 ns2) {
     const float2 q0 = __fmul2_rn(x, r2);
-    const float2 e = __ffma2_rn(q0, ns2, x);
-    const float2 q1 = __ffma2_rn(e, r2, q0);
-    return make_float2(copysignf(q1.x, x.x), copysignf(q1.y, x.y));
+    const float2 s2 = make_float2(-ns2.x, -ns2.y);
+    const float2 en = __ffma2_rn(q0, s2, make_float2(-x.x, -x.y));
+    return __ffma2_rn(make_float2(-en.x, -en.y), r2, q0);
 }
 
 // Two FP32 -> packed E4M3x2 with round-to-nearest-even and saturation to +-448
