@@ -420,10 +420,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int t = cid; next_tile(t, tl); t += ncl) {
             const int arow = tl.row0 + (int)rank * BM;
             const bool active = h < tl.nh;
-            if (kWgrad && !active) {
-                // this half lies past N (last column tile): only keep the scale ring moving.  A
-                // separate loop keeps the tile-dependent test out of Wgrad's promotion loop below
-                // (Fprop/Dgrad: ptxas then spills accumulators, so they test per K-block).
+            if (!active) {
+                // this half lies past N (last column tile): only keep the scale ring moving (the
+                // issuer skips its MMAs and slot uses too)
                 for (int kb = 0; kb < p.KB; ++kb, ++sit) {
                     if (!(kDbg & 512)) {
                         mbar_wait(sfull_bar(sit & (C::kSStages - 1)), (sit / C::kSStages) & 1);
@@ -434,131 +433,164 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
 #pragma unroll
             for (int i = 0; i < NC; ++i) acc[i] = 0.0f;
-            for (int kb = 0; kb < p.KB; ++kb, ++sit) {
-                const int ss = sit & (C::kSStages - 1);
-                const uint32_t sph = (sit / C::kSStages) & 1;
+            // One K-block of promotion for this warp: wait for the scale stage and the TMEM slot, read
+            // the slot, release it, accumulate.  ss/pb/pph are compile-time in the unrolled loop below.
+            auto promote_kb = [&](const int ss, const uint32_t sph, const int pb, const uint32_t pph, const int sit) __attribute__((always_inline)) {
                 if (!(kDbg & 512)) mbar_wait(sfull_bar(ss), sph);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(11, sit);
                 const uint32_t sst = sring + ss * C::SSTAGE;
-                if (kWgrad || active) {
-                    const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
-                    // Fprop/Dgrad: half h is exactly weight block n0/128 + h (n0 is a multiple of 256),
-                    // so one factor sA(kb,row) * sB(kb, block) per warp: one FFMA per element.
-                    float f = 0.0f;
-                    if constexpr (!kWgrad) f = __fmul_rn(sa, lds_f32(sst + sb_off));
-                    const int pb = 2 * h + (qh & 1);
-                    const uint32_t pph = (qh >> 1) & 1;
-                    ++qh;
-                    if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
-                    if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
-                    if (!((kDbg & 128))) {
+                const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
+                // Fprop/Dgrad: half h is exactly weight block n0/128 + h (n0 is a multiple of 256),
+                // so one factor sA(kb,row) * sB(kb, block) per warp: one FFMA per element.
+                float f = 0.0f, sbk = 0.0f;
+                if constexpr (!kWgrad) { sbk = lds_f32(sst + sb_off); f = __fmul_rn(sa, sbk); }
+
+                if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
+                if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
+                if (!((kDbg & 128))) {
 #if FP8BS_PROMO_POLL
-                        mbar_wait_poll(pfull_bar(pb), pph);
+                    mbar_wait_poll(pfull_bar(pb), pph);
 #else
-                        mbar_wait(pfull_bar(pb), pph);
+                    mbar_wait(pfull_bar(pb), pph);
 #endif
+                }
+                if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(9, sit);
+                if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 4 : 6, sit);
+                tc_fence_after();
+                // acc[c0 + j] += P[j] * sA(kb,row) * sB(kb, col): Fprop/Dgrad one FFMA2 per column
+                // pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
+                auto fma32 = [&](const uint32_t* r, int c0) {
+                    if ((kDbg & 1)) {   // experiment: loads only
+                        if (r[0] == 0x7fffffffu) acc[c0] += 1.0f;
+                        return;
                     }
-                    if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(9, sit);
-                    if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 4 : 6, sit);
-                    tc_fence_after();
-                    // acc[c0 + j] += P[j] * sA(kb,row) * sB(kb, col): Fprop/Dgrad one FFMA2 per column
-                    // pair; Wgrad FMUL2 + FFMA2 (outer-product scales)
-                    auto fma32 = [&](const uint32_t* r, int c0) {
-                        if ((kDbg & 1)) {   // experiment: loads only
-                            if (r[0] == 0x7fffffffu) acc[c0] += 1.0f;
-                            return;
-                        }
-                        if constexpr (!kWgrad) {
-                            const float2 f2 = make_float2(f, f);
+                    if constexpr (!kWgrad) {
+                        const float2 f2 = make_float2(f, f);
 #pragma unroll
-                            for (int j = 0; j < ((kDbg & 4096) ? 16 : 32); j += 2) {   // 4096: half the math (experiment)
-                                const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
-                                                            make_float2(acc[c0 + j], acc[c0 + j + 1]));
-                                acc[c0 + j] = a.x; acc[c0 + j + 1] = a.y;
-                            }
-                        } else {
-                            const float2 sa2 = make_float2(sa, sa);
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                const float4 b = lds_f32x4(sst + sb_off + 4u * (c0 + j));
-                                const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
-                                const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
-                                const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), fa,
-                                                             make_float2(acc[c0 + j], acc[c0 + j + 1]));
-                                const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])), fb,
-                                                             make_float2(acc[c0 + j + 2], acc[c0 + j + 3]));
-                                acc[c0 + j] = a0.x; acc[c0 + j + 1] = a0.y; acc[c0 + j + 2] = a1.x; acc[c0 + j + 3] = a1.y;
-                            }
+                        for (int j = 0; j < ((kDbg & 4096) ? 16 : 32); j += 2) {   // 4096: half the math (experiment)
+                            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2,
+                                                        make_float2(acc[c0 + j], acc[c0 + j + 1]));
+                            acc[c0 + j] = a.x; acc[c0 + j + 1] = a.y;
                         }
-                    };
-                    const uint32_t ta = tbase + pb * HN;
-                    if ((kDbg & 8)) {     // experiment: no TMEM reads, no math
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if constexpr (kPair) mbar_arrive_cluster(pempty_bar(pb) & kPeerBitMask);
-                            else mbar_arrive(pempty_bar(pb));
-                        }
-                        goto half_done;
-                    }
-                    uint32_t r0[32], r1[32];
-                    if constexpr (NC == 128) {
-                        // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
-                        // soon as the second round has landed (32 FFMA2 after the first wait)
-                        FP8BS_TMEM_LD32(ta, r0);
-                        FP8BS_TMEM_LD32(ta + 32, r1);
-                        tmem_ld_wait();
-                        fma32(r0, 0);
-                        fma32(r1, 32);
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
-                        FP8BS_TMEM_LD32(ta + 64, r0);
-                        FP8BS_TMEM_LD32(ta + 96, r1);
-                        tmem_ld_wait();
                     } else {
-                        // 64 columns: one 32-column round, its math, then the second round
-                        FP8BS_TMEM_LD32(ta, r0);
-                        tmem_ld_wait();
-                        fma32(r0, 0);
+                        const float2 sa2 = make_float2(sa, sa);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) asm volatile("" : "+f"(acc[j]));
-                        FP8BS_TMEM_LD32(ta + 32, r1);
-                        tmem_ld_wait();
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 b = lds_f32x4(sst + sb_off + 4u * (c0 + j));
+                            const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
+                            const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
+                            const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), fa,
+                                                         make_float2(acc[c0 + j], acc[c0 + j + 1]));
+                            const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])), fb,
+                                                         make_float2(acc[c0 + j + 2], acc[c0 + j + 3]));
+                            acc[c0 + j] = a0.x; acc[c0 + j + 1] = a0.y; acc[c0 + j + 2] = a1.x; acc[c0 + j + 3] = a1.y;
+                        }
                     }
-                    // release the slot before the last math: the registers hold this warp's part now.
-                    // tcgen05.wait::ld is warp-collective, so one elected lane may arrive; ptxas schedules
-                    // Wgrad better with elect.sync and Fprop/Dgrad better with lane 0 after __syncwarp
-                    // (measured: Wgrad +8% / Fprop -13% with elect)
+                };
+                const uint32_t ta = tbase + pb * HN;
+                if ((kDbg & 8)) {     // experiment: no TMEM reads, no math
                     tc_fence_before();
-                    bool rel_lane;
-                    if constexpr (kWgrad || FP8BS_REL_MODE == 1) {
-                        rel_lane = elect_one();
-                    } else {
-                        __syncwarp();
-                        rel_lane = lane == 0;
-                    }
-                    if (rel_lane) {
-                        // the leader's barrier: clear the CTA-rank bit of the shared address (a mapa'd address held
-                        // across the loop made ptxas spill ~30 accumulators)
+                    __syncwarp();
+                    if (lane == 0) {
                         if constexpr (kPair) mbar_arrive_cluster(pempty_bar(pb) & kPeerBitMask);
                         else mbar_arrive(pempty_bar(pb));
-                        if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
-                        if (kTrace && warp == 7) FP8BS_TS(7, sit);
                     }
-                    if constexpr (!kWgrad && FP8BS_REL_MODE == 2) {
-                        // re-read the factor after the release: the shared loads stay behind the
-                        // arrive, so ptxas cannot hoist the last math above the slot release
-                        f = __fmul_rn(lds_f32(sst + 4u * ((arow & 3) + row)), lds_f32(sst + sb_off));
-                    }
-                    if constexpr (NC == 128) {
-                        fma32(r0, 64);
-                        fma32(r1, 96);
-                    } else {
-                        fma32(r1, 32);
-                    }
-                half_done:;
+                    return;
                 }
+                uint32_t r0[32], r1[32];
+                if constexpr (NC == 128) {
+                    // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
+                    // soon as the second round has landed (32 FFMA2 after the first wait)
+                    FP8BS_TMEM_LD32(ta, r0);
+                    FP8BS_TMEM_LD32(ta + 32, r1);
+                    tmem_ld_wait();
+                    fma32(r0, 0);
+                    fma32(r1, 32);
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
+                    FP8BS_TMEM_LD32(ta + 64, r0);
+                    FP8BS_TMEM_LD32(ta + 96, r1);
+                    tmem_ld_wait();
+                } else {
+                    // 64 columns: one 32-column round, its math, then the second round
+                    FP8BS_TMEM_LD32(ta, r0);
+                    tmem_ld_wait();
+                    fma32(r0, 0);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) asm volatile("" : "+f"(acc[j]));
+                    FP8BS_TMEM_LD32(ta + 32, r1);
+                    tmem_ld_wait();
+                }
+                // release the slot before the last math: the registers hold this warp's part now.
+                // tcgen05.wait::ld is warp-collective, so one elected lane may arrive; ptxas schedules
+                // Wgrad better with elect.sync and Fprop/Dgrad better with lane 0 after __syncwarp
+                // (measured: Wgrad +8% / Fprop -13% with elect)
+                tc_fence_before();
+                bool rel_lane;
+                if constexpr (kWgrad || FP8BS_REL_MODE == 1) {
+                    rel_lane = elect_one();
+                } else {
+                    __syncwarp();
+                    rel_lane = lane == 0;
+                }
+                if (rel_lane) {
+                    // the leader's barrier: clear the CTA-rank bit of the shared address (a mapa'd address held
+                    // across the loop made ptxas spill ~30 accumulators)
+                    if constexpr (kPair) mbar_arrive_cluster(pempty_bar(pb) & kPeerBitMask);
+                    else mbar_arrive(pempty_bar(pb));
+                    if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
+                    if (kTrace && warp == 7) FP8BS_TS(7, sit);
+                }
+                if constexpr (!kWgrad && FP8BS_REL_MODE == 3) {
+                    // Keep the last math behind the slot release.  ptxas otherwise schedules most of
+                    // it above the arrive, lengthening the slot turnaround (tools/gemm_trace.py).  The
+                    // factor is re-selected through the result of a barrier probe issued after the
+                    // arrive (always true: this slot's phase has completed); fma(sa, sb, 0) equals
+                    // sa*sb for the positive scales, and ptxas cannot fold the select away.
+                    const bool done = mbar_test_wait(pfull_bar(pb), pph);
+                    f = done ? f : __fmaf_rn(sa, sbk, 0.0f);
+                }
+                if constexpr (!kWgrad && FP8BS_REL_MODE == 2) {
+                    // re-read the factor after the release: the shared loads stay behind the
+                    // arrive, so ptxas cannot hoist the last math above the slot release
+                    f = __fmul_rn(lds_f32(sst + 4u * ((arow & 3) + row)), lds_f32(sst + sb_off));
+                }
+                if constexpr (NC == 128) {
+                    fma32(r0, 64);
+                    fma32(r1, 96);
+                } else {
+                    fma32(r1, 32);
+                }
+            };
+            auto release_scales = [&](const int ss) __attribute__((always_inline)) {
+                // The stage was written by TMA (async proxy) and read here with ld.shared (generic
+                // proxy); the producer's next TMA into it must not overtake those reads, so a proxy
+                // fence precedes the arrive.  Without it Wgrad's late per-column scale reads saw the
+                // refilled stage, nondeterministically (tools/dbg_race.py: columns 96..127 of a half).
+                if (!(kDbg & 512)) fence_proxy_async_smem();
                 if (elect_one() && !((kDbg & 512))) mbar_arrive(sempty_bar(ss));
+            };
+            bool unrolled = false;
+            // dense Fprop/Dgrad only: in the Wgrad and grouped kernels the unrolled body makes ptxas
+            // spill accumulators (measured: Wgrad -7%, grouped C4 -18%)
+            if constexpr (!kWgrad && !kGrouped) unrolled = p.KB % C::kSStages == 0;
+            if (unrolled) {
+                // K-blocks in groups of kSStages (8): the scale stage is the index in the group, the TMEM
+                // slot alternates 2h, 2h + 1 and its phase flips every 2 K-blocks (sit and qh are
+                // multiples of 8 at every tile start), so only the scale phase is a runtime value.
+                for (int kb0 = 0; kb0 < p.KB; kb0 += C::kSStages, sit += C::kSStages, qh += C::kSStages) {
+                    const uint32_t sph = (sit / C::kSStages) & 1;
+#pragma unroll
+                    for (int i = 0; i < C::kSStages; ++i) {
+                        promote_kb(i, sph, 2 * h + (i & 1), (i >> 1) & 1, sit + i);
+                        release_scales(i);
+                    }
+                }
+            } else {
+                for (int kb = 0; kb < p.KB; ++kb, ++sit, ++qh) {
+                    promote_kb(sit & (C::kSStages - 1), (sit / C::kSStages) & 1, 2 * h + (qh & 1), (qh >> 1) & 1, sit);
+                    release_scales(sit & (C::kSStages - 1));
+                }
             }
             // ---------------- epilogue ----------------
             // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or

@@ -225,6 +225,10 @@ k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __
                 }
             }
         }
+        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
+        // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
+        // does not; see gemm.cu release_scales)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (C::STAGES + st));
     }
@@ -400,6 +404,10 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
         uint32_t w[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) w[r] = lds32(sbase + st * P::TILE_BYTES + (rg * 32 + r) * 256 + wc * 4);
+        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
+        // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
+        // does not; see gemm.cu release_scales)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
         float sc[P::CPW];
@@ -539,6 +547,10 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         uint32_t w[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) w[r] = lds32(tile + (rg * 32 + r) * 256 + wc * 4);
+        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
+        // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
+        // does not; see gemm.cu release_scales)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
         float sc[P::CPW];
@@ -664,6 +676,10 @@ k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K
         uint4 v[P::NCH];
 #pragma unroll
         for (int i = 0; i < P::NCH; ++i) v[i] = lds128(sbase + st * P::BLOCK_BYTES + (i * 32 * P::CONSUMERS + tid) * 16);
+        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
+        // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
+        // does not; see gemm.cu release_scales)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));
         float amax = 0.0f;
