@@ -116,9 +116,6 @@ constexpr int kTsSlots = 12;
 #ifndef FP8BS_ISSUER_POLL
 #define FP8BS_ISSUER_POLL 0
 #endif
-#ifndef FP8BS_REL_MODE
-#define FP8BS_REL_MODE 0
-#endif
 #ifndef FP8BS_GEMM_DEBUG_BITS
 #define FP8BS_GEMM_DEBUG_BITS 0
 #endif
@@ -418,7 +415,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         int sit = 0, qh = 0;                            // K-block, slot uses of this half
         Tile tl;
         for (int t = cid; next_tile(t, tl); t += ncl) {
-            const int arow = tl.row0 + (int)rank * BM;
+            const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
             const bool active = h < tl.nh;
             if (!active) {
                 // this half lies past N (last column tile): only keep the scale ring moving (the
@@ -439,11 +436,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (!(kDbg & 512)) mbar_wait(sfull_bar(ss), sph);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(11, sit);
                 const uint32_t sst = sring + ss * C::SSTAGE;
-                const float sa = lds_f32(sst + 4u * ((arow & 3) + row));
+                const float sa = lds_f32(sst + sa_off);
                 // Fprop/Dgrad: half h is exactly weight block n0/128 + h (n0 is a multiple of 256),
                 // so one factor sA(kb,row) * sB(kb, block) per warp: one FFMA per element.
-                float f = 0.0f, sbk = 0.0f;
-                if constexpr (!kWgrad) { sbk = lds_f32(sst + sb_off); f = __fmul_rn(sa, sbk); }
+                float f = 0.0f;
+                if constexpr (!kWgrad) f = __fmul_rn(sa, lds_f32(sst + sb_off));
 
                 if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
@@ -527,7 +524,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 // (measured: Wgrad +8% / Fprop -13% with elect)
                 tc_fence_before();
                 bool rel_lane;
-                if constexpr (kWgrad || FP8BS_REL_MODE == 1) {
+                if constexpr (kWgrad) {
                     rel_lane = elect_one();
                 } else {
                     __syncwarp();
@@ -540,20 +537,6 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     else mbar_arrive(pempty_bar(pb));
                     if (kTrace && warp == C::THREADS / 32 - 1) FP8BS_TS(10, sit);
                     if (kTrace && warp == 7) FP8BS_TS(7, sit);
-                }
-                if constexpr (!kWgrad && FP8BS_REL_MODE == 3) {
-                    // Keep the last math behind the slot release.  ptxas otherwise schedules most of
-                    // it above the arrive, lengthening the slot turnaround (tools/gemm_trace.py).  The
-                    // factor is re-selected through the result of a barrier probe issued after the
-                    // arrive (always true: this slot's phase has completed); fma(sa, sb, 0) equals
-                    // sa*sb for the positive scales, and ptxas cannot fold the select away.
-                    const bool done = mbar_test_wait(pfull_bar(pb), pph);
-                    f = done ? f : __fmaf_rn(sa, sbk, 0.0f);
-                }
-                if constexpr (!kWgrad && FP8BS_REL_MODE == 2) {
-                    // re-read the factor after the release: the shared loads stay behind the
-                    // arrive, so ptxas cannot hoist the last math above the slot release
-                    f = __fmul_rn(lds_f32(sst + 4u * ((arow & 3) + row)), lds_f32(sst + sb_off));
                 }
                 if constexpr (NC == 128) {
                     fma32(r0, 64);
@@ -572,7 +555,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             };
             bool unrolled = false;
             // dense Fprop/Dgrad only: in the Wgrad and grouped kernels the unrolled body makes ptxas
-            // spill accumulators (measured: Wgrad -7%, grouped C4 -18%)
+            // spill loop state into local memory (measured: Wgrad -7%, grouped C4 -20%)
             if constexpr (!kWgrad && !kGrouped) unrolled = p.KB % C::kSStages == 0;
             if (unrolled) {
                 // K-blocks in groups of kSStages (8): the scale stage is the index in the group, the TMEM
@@ -593,6 +576,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
             }
             // ---------------- epilogue ----------------
+            const int arow = tl.row0 + (int)rank * BM;
             // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or
             // 64 BF16 columns) in its own SWIZZLE_128B buffer and writes them with asynchronous TMA
             // stores (reduce-add for Wgrad's D += acc): a warp store used to touch 32 rows at once.
