@@ -14,6 +14,7 @@ else
 fi
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -prec-div=true -prec-sqrt=true -ftz=false -fmad=true -Xcompiler -fPIC,-O2,-fvisibility=hidden -cudart static --expt-relaxed-constexpr"
 for f in $TMP/p/csrc/*.cu; do nvcc $FLAGS "$@" -I $TMP/include -c $f -o $f.o & done; wait
+for f in $TMP/p/csrc/*.cu; do [ -f $f.o ] || { echo "build failed: $f"; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -Xcompiler -fPIC -o $ROOT/tools/libfp8bs_$NAME.so $TMP/p/csrc/*.o -lpthread -ldl -lrt
 rm -rf $TMP
 echo $ROOT/tools/libfp8bs_$NAME.so
