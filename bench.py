@@ -251,7 +251,7 @@ def run_reference(args, world, rank):
                              "sample": f"each step: the C1 step restricted to {CPU_TOK} tokens x {D_IN} in x "
                                        f"{CPU_OUT} out channels on the CPU oracle"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 def config_block(args, world):
@@ -427,7 +427,7 @@ def main():
     if rank == 0:
         if args.cpu and world == 1:
             result["cpu_baseline"] = cpu_baseline_block()
-        print(json.dumps(result))
+        print(json.dumps(result), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
