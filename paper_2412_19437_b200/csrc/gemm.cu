@@ -42,6 +42,9 @@ constexpr int kMaxGroups = 1024;
 #ifndef FP8BS_NPW
 #define FP8BS_NPW 8
 #endif
+#ifndef FP8BS_EPI_BUFS
+#define FP8BS_EPI_BUFS 1   // 2 measured no faster (one fewer operand stage; Wgrad -2%)
+#endif
 
 template <bool kPair, bool kWgrad>
 struct Cfg {
@@ -68,7 +71,8 @@ struct Cfg {
     static constexpr int SSTAGE = SA_BYTES + SB_BYTES;
     static_assert(SSTAGE % 128 == 0 && STAGE % 1024 == 0, "TMA smem destinations need 128 B (1024 B swizzled) alignment");
     // Epilogue: each promotion warp stages 32 rows x 128 bytes (SWIZZLE_128B) for a TMA store.
-    static constexpr int EPI_WARP_BYTES = 32 * 128;
+    static constexpr int EPI_BUFS = FP8BS_EPI_BUFS;          // staging buffers per warp (2: chunk c+1 is staged while chunk c's TMA store reads)
+    static constexpr int EPI_WARP_BYTES = 32 * 128 * EPI_BUFS;
     // Operand stages fill the dynamic shared memory left after the static scale ring, the epilogue
     // buffers and the barriers (227 KB per CTA, 1 KB of alignment slack).
     static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - FP8BS_NPW * EPI_WARP_BYTES;
@@ -115,6 +119,9 @@ constexpr int kTsSlots = 12;
 #endif
 #ifndef FP8BS_ISSUER_POLL
 #define FP8BS_ISSUER_POLL 0
+#endif
+#ifndef FP8BS_WG_NOSB
+#define FP8BS_WG_NOSB 0
 #endif
 #ifndef FP8BS_GEMM_DEBUG_BITS
 #define FP8BS_GEMM_DEBUG_BITS 0
@@ -473,7 +480,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         const float2 sa2 = make_float2(sa, sa);
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
+#if FP8BS_WG_NOSB   // experiment: no per-column scale loads (wrong results; timing only)
+                            const float4 b = make_float4(sa, sa, sa, sa);
+#else
                             const float4 b = lds_f32x4(sst + sb_off + 4u * (c0 + j));
+#endif
                             const float2 fa = __fmul2_rn(sa2, make_float2(b.x, b.y));
                             const float2 fb = __fmul2_rn(sa2, make_float2(b.z, b.w));
                             const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), fa,
@@ -593,10 +604,12 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 constexpr int ESZ = kOutF32 ? 4 : 2;
                 constexpr int CW = 128 / ESZ;                   // columns per 128-byte chunk
                 if (!kGrouped || rows_here >= 32) {
-                    const uint32_t ebuf = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
+                    const uint32_t ebuf0 = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
 #pragma unroll
                     for (int c = 0; c < NC / CW; ++c) {
-                        if (lane == 0) bulk_wait_group_read<0>();       // the previous chunk's store has read the buffer
+                        const uint32_t ebuf = ebuf0 + (c % C::EPI_BUFS) * (32 * 128);
+                        // the store that last used this buffer has read it
+                        if (lane == 0) bulk_wait_group_read<C::EPI_BUFS - 1>();
                         __syncwarp();
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {                   // 16-byte units of this lane's row
