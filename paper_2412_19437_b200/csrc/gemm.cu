@@ -9,20 +9,23 @@
 //   * a 256-column tile is computed as two N = 128 halves, each with its own MMA-issuing warp
 //     (one thread issues a tcgen05.mma only every ~70 cycles) and its own two TMEM slots: per
 //     K-block each issuer runs 4x tcgen05.mma.kind::f8f6f4 (K = 32) into a fresh FP32 slot P;
-//   * 16 promotion warps read each P with one tcgen05.ld (32 columns per thread), release the slot
-//     at once, then accumulate P * sA(kb,i) * sB(kb,j) in registers with packed FFMA2 and finally
-//     write BF16 (RNE) or FP32 (+= for Wgrad).  A slot is reused two K-blocks later, so its release
-//     has three other N = 128 MMA groups (768 cycles at peak) to land;
-//   * a scale warp streams sA (and Wgrad's per-column sB) with TMA into its own ring.
+//   * 8 promotion warps (FP8BS_NPW) read each P with four tcgen05.ld.32x32b.x32 (a warp owns one
+//     TMEM lane quadrant = 32 rows x 128 columns of a half), release the slot, and accumulate
+//     P * sA(kb,i) * sB(kb,j) in 128 registers with packed FFMA2 (Wgrad: FMUL2 + FFMA2), finally
+//     writing BF16 (RNE) or FP32 (+= for Wgrad) through TMA stores.  A slot is reused two K-blocks
+//     later, so its release has three other N = 128 MMA groups (768 cycles at peak) to land;
+//   * a scale warp streams sA (and Wgrad's per-column sB) with TMA into its own 8-stage ring; every
+//     release of a TMA-filled stage read with ld.shared is preceded by a proxy fence (release_scales).
 // kPair = true: a cluster of 2 CTAs on a TPC runs tcgen05.mma.cta_group::2 with M = 256 (128 rows
 // per CTA): each CTA stages its own 128 rows of A and 64 rows of each B half, so per-SM L2->SMEM
 // traffic per MAC is that of a 256 x 256 tile.  The leader CTA issues the MMAs; both CTAs' TMA loads
 // complete on the leader's barrier; commits multicast to both CTAs; promotion warps release a TMEM
 // slot by arriving on the leader's barrier.
-// Warp roles (640 threads): w0 TMA A/B producer, w1/w2 MMA issuers (half 0/1; w2 also allocates
-// TMEM), w3 scale producer, w4..w19 promotion + epilogue (warpgroup g owns columns [32g, 32g + 32)
-// of each half).  Persistent clusters walk a static tile schedule; the grouped (MoE) variant maps
-// tiles to (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
+// Warp roles (384 threads): w0 TMA A/B producer, w1/w2 MMA issuers (half 0/1; w2 also allocates
+// TMEM), w3 scale producer, w4..w11 promotion + epilogue (w4..w7 half 0, w8..w11 half 1; lane
+// quadrant = warp % 4).  Persistent clusters walk a static tile schedule; the grouped (MoE) variant
+// maps tiles to (expert, m-tile, n-tile) from device-side offsets with no host synchronisation.
+// DESIGN.md §5 has the measurements behind these choices.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
