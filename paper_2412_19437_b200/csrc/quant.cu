@@ -646,7 +646,7 @@ struct QWCfg {
     static constexpr int NCH = 128 * CPR / (32 * CONSUMERS); // chunks per consumer thread: 8 / 4
     static constexpr int OFF_C = STAGES * BLOCK_BYTES;      // code tile [128][128]
     static constexpr int OFF_RED = OFF_C + 128 * 128;
-    static constexpr int OFF_BAR = OFF_RED + CONSUMERS * 4;
+    static constexpr int OFF_BAR = OFF_RED + 2 * CONSUMERS * 4;   // per-warp amax, double-buffered by block parity
     static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
 };
 
@@ -706,14 +706,67 @@ k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        if (lane == 0) red[warp] = amax;
+        // per-block parity: without the transposed copy there is no second barrier, and a fast warp
+        // would otherwise overwrite its slot for the next block while a slow one still reads this one
+        float* rb = red + (it & 1) * P::CONSUMERS;
+        if (lane == 0) rb[warp] = amax;
         named_bar_sync(1, 32 * P::CONSUMERS);
-        amax = red[0];
+        amax = rb[0];
 #pragma unroll
-        for (int i = 1; i < P::CONSUMERS; ++i) amax = fmaxf(amax, red[i]);
+        for (int i = 1; i < P::CONSUMERS; ++i) amax = fmaxf(amax, rb[i]);
         const float sc = group_scale(amax);
         const float rc = __frcp_rn(sc);
         const bool fast = fast_div_ok(sc);                  // block-uniform
+        // Interior block (every block of the C1/C2 weights): branch-free stores from one base pointer
+        // per thread; the integer bounds arithmetic of the general path below was most of this
+        // kernel's instructions (ncu: ~22 instructions per element).
+        const bool full = (n0 + 128 <= N) && (k0 + 128 <= K);
+        if (full && fast) {
+            constexpr int RSTEP = 32 * P::CONSUMERS / P::CPR;             // rows between a thread's chunks
+            const int row0 = tid / P::CPR, col = (tid % P::CPR) * P::E;
+            uint8_t* qb = q + (n0 + row0) * ldq + k0 + col;
+            const int64_t qstep = (int64_t)RSTEP * ldq;
+            const uint32_t cbase = sbase + P::OFF_C;
+#pragma unroll
+            for (int i = 0; i < P::NCH; ++i) {
+                float f[P::E];
+                Vec<T>::unpack(v[i], f);
+                uint32_t wd[P::E / 4];
+                encode_chunk<P::E>(f, sc, rc, true, wd);
+                if constexpr (P::E == 8) *reinterpret_cast<uint2*>(qb + i * qstep) = make_uint2(wd[0], wd[1]);
+                else *reinterpret_cast<uint32_t*>(qb + i * qstep) = wd[0];
+                if (qT) {
+                    const int row = row0 + i * RSTEP;
+#pragma unroll
+                    for (int e = 0; e < P::E / 4; ++e) {
+                        const int kw = col / 4 + e;
+                        asm volatile("st.shared.u32 [%0], %1;" :: "r"(cbase + row * 128 + 4 * (kw ^ ((row >> 2) & 31))),
+                                     "r"(wd[e]) : "memory");
+                    }
+                }
+            }
+            if (tid == 0) s[(int64_t)nb * ldsw + kb] = sc;
+            if (qT) {
+                named_bar_sync(1, 32 * P::CONSUMERS);
+                const int l = tid & 31;
+                uint8_t* tb = qT + k0 * ldqT + n0 + 4 * l;
+#pragma unroll
+                for (int i = 0; i < 32 * 32 / (32 * P::CONSUMERS); ++i) {
+                    const int kw = (i * 32 * P::CONSUMERS + tid) >> 5;          // rows 4l..4l+3, k 4kw..4kw+3
+                    uint32_t a[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a[j] = lds32(cbase + (4 * l + j) * 128 + 4 * (kw ^ l));
+                    const uint32_t t0 = __byte_perm(a[0], a[1], 0x5140), t1 = __byte_perm(a[0], a[1], 0x7362);
+                    const uint32_t t2 = __byte_perm(a[2], a[3], 0x5140), t3 = __byte_perm(a[2], a[3], 0x7362);
+                    const uint32_t b4[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632),
+                                            __byte_perm(t1, t3, 0x5410), __byte_perm(t1, t3, 0x7632)};
+                    uint8_t* d = tb + (int64_t)(4 * kw) * ldqT;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(d + e * ldqT) = b4[e];
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < P::NCH; ++i) {
             const int idx = i * 32 * P::CONSUMERS + tid, row = idx / P::CPR, col = (idx % P::CPR) * P::E;
