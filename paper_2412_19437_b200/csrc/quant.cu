@@ -540,6 +540,11 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         const int64_t m0 = (int64_t)mb * 128, c0 = (int64_t)cb * P::CH;
         const uint32_t tile = sbase + st * P::TILE_BYTES;
         mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
+        // Interior tile (all tiles of M, C multiples of 128): stores through per-thread base pointers
+        // advanced by constant strides, without per-store bounds arithmetic.
+        const bool full = (m0 + 128 <= M) && (c0 + P::CH <= C);
+        uint8_t* qrow = q + (m0 + warp * 4 + sub) * ldq + c0 + li * 16;     // + pass * 32 rows
+        float* srow = s + (int64_t)cb * lds + m0 + warp * 4 + sub;
         // ---- 1x128 along the channels: rows of the tile ----
 #pragma unroll 1
         for (int pass = 0; pass < 4; ++pass) {
@@ -557,10 +562,15 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             uint32_t w4[4];
             if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w4);   // warp-uniform
             else encode_chunk<16>(f, sc, r, false, w4);
-            const int64_t m = m0 + row, c = c0 + li * 16;
-            if (m < M) {
-                if (c < C) *reinterpret_cast<uint4*>(q + m * ldq + c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                if (li == 0) s[(int64_t)cb * lds + m] = sc;
+            if (full) {
+                *reinterpret_cast<uint4*>(qrow + pass * 32 * ldq) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                if (li == 0) srow[pass * 32] = sc;
+            } else {
+                const int64_t m = m0 + row, c = c0 + li * 16;
+                if (m < M) {
+                    if (c < C) *reinterpret_cast<uint4*>(q + m * ldq + c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    if (li == 0) s[(int64_t)cb * lds + m] = sc;
+                }
             }
         }
         // ---- 128x1 along the tokens: columns of the tile (as k_quant_act_128x1_tma) ----
@@ -584,7 +594,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             const float a = fmaxf(fmaxf(red[ch], red[P::CH + ch]), fmaxf(red[2 * P::CH + ch], red[3 * P::CH + ch]));
             sc[j] = group_scale(a);
             fast = fast && fast_div_ok(sc[j]);
-            if (rg == 0 && c0 + ch < C) sT[(int64_t)mb * ldsT + c0 + ch] = sc[j];
+            if (rg == 0 && (full || c0 + ch < C)) sT[(int64_t)mb * ldsT + c0 + ch] = sc[j];
         }
         fast = __all_sync(0xffffffffu, fast);
 #pragma unroll
@@ -611,6 +621,15 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             sts128(qa + 16, make_uint4(code[4], code[5], code[6], code[7]));
         }
         named_bar_sync(1, 32 * P::CONSUMERS);
+        if (full) {
+            // thread -> channel i * 32 + tid / 8, tokens (tid & 7) * 16 .. + 16 of the tile
+            uint8_t* tb = qT + (c0 + (tid >> 3)) * ldqT + m0 + (tid & 7) * 16;
+            const uint32_t qs = sbase + P::OFF_Q + (tid >> 3) * P::QSTR + (tid & 7) * 16;
+#pragma unroll
+            for (int i = 0; i < P::CH * 8 / (32 * P::CONSUMERS); ++i)
+                *reinterpret_cast<uint4*>(tb + (int64_t)(i * 32) * ldqT) = lds128(qs + i * 32 * P::QSTR);
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < P::CH * 8 / (32 * P::CONSUMERS); ++i) {
             const int idx = i * 32 * P::CONSUMERS + tid, chl = idx >> 3, pk = idx & 7;
