@@ -184,6 +184,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const __grid_constant__ CUtensorMap tmD, const KParams p) {
     using C = Cfg<kPair, kWgrad>;
     extern __shared__ uint8_t smem_raw[];
+    griddep_wait();                 // PDL: previous grid complete, its writes visible
+    griddep_launch_dependents();
     // barriers and the scale ring live in static shared memory: their addresses are constants, so
     // the promotion loop does not re-derive the aligned dynamic base every K-block
     // one static block (scale ring, barriers, TMEM address): every static shared address is a
@@ -793,11 +795,13 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     cfg.blockDim = dim3(C::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = C::CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (internal.h launch_pdl)
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, p);
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

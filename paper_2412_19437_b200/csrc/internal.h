@@ -23,6 +23,26 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
                                         int64_t ldq, float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT,
                                         cudaStream_t st);
 
+// Programmatic dependent launch (PDL): the kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so its CTAs may be scheduled while the
+// previous kernel in the stream drains; every PDL kernel executes griddepcontrol.wait (sm100.cuh
+// griddep_wait) before its first global-memory access, which waits for the previous grid to
+// complete and its writes to be visible.  This hides the launch gap between the step's kernels.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 struct GemmArgs {
     int layout;              // 0 FPROP, 1 DGRAD, 2 WGRAD
     int64_t M, N, K;

@@ -160,6 +160,8 @@ k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __
                       float* __restrict__ s, int64_t lds) {
     using C = Q1Cfg<T>;
     extern __shared__ __align__(128) uint8_t smem[];
+    griddep_wait();                 // PDL: previous grid complete, its writes visible
+    griddep_launch_dependents();
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + C::STAGES * C::CHUNK_BYTES;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -397,6 +399,8 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
                       int64_t ldq, float* __restrict__ sT, int64_t lds) {
     using P = QTCfg<T>;
     extern __shared__ __align__(128) uint8_t smem[];
+    griddep_wait();                 // PDL: previous grid complete, its writes visible
+    griddep_launch_dependents();
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + P::OFF_BAR;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -508,6 +512,8 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
     using T = __nv_bfloat16;
     using P = QTCfg<T>;
     extern __shared__ __align__(128) uint8_t smem[];
+    griddep_wait();                 // PDL: previous grid complete, its writes visible
+    griddep_launch_dependents();
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + P::OFF_BAR;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -675,6 +681,8 @@ k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K
                    float* __restrict__ s, int64_t ldsw, uint8_t* __restrict__ qT, int64_t ldqT) {
     using P = QWCfg<T>;
     extern __shared__ __align__(128) uint8_t smem[];
+    griddep_wait();                 // PDL: previous grid complete, its writes visible
+    griddep_launch_dependents();
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + P::OFF_BAR;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -997,7 +1005,7 @@ static cudaError_t launch_1x128_t(const void* x, int64_t M, int64_t K, int64_t l
             if (dev >= 0 && dev < 64) attr_set[dev] = true;
         }
         const int64_t chunks = (M * (K / 128) + C::CHUNK_TILES - 1) / C::CHUNK_TILES;
-        k_quant_act_1x128_tma<T><<<grid_for(chunks, 2, 2), C::THREADS, C::SMEM, st>>>(
+        return launch_pdl(k_quant_act_1x128_tma<T>, grid_for(chunks, 2, 2), C::THREADS, C::SMEM, st, 
             reinterpret_cast<const T*>(x), M, K, q, s, lds);
     } else if (fast) {
         constexpr int U = 4;
@@ -1044,7 +1052,7 @@ static cudaError_t launch_128x1_t(const void* x, int64_t M, int64_t C, int64_t l
             if (dev >= 0 && dev < 64) attr_tma[dev] = true;
         }
         const int64_t tiles = ((M + 127) / 128) * ((C + Q::CH - 1) / Q::CH);
-        k_quant_act_128x1_tma<T><<<grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st>>>(tm, M, C, qT, ldq, sT, lds);
+        return launch_pdl(k_quant_act_128x1_tma<T>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, C, qT, ldq, sT, lds);
     } else if (fast) {
         static bool attr_set[64] = {false};   // per device; idempotent, benign race
         int dev = 0;
@@ -1097,8 +1105,7 @@ cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, 
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     const int64_t tiles = ((M + 127) / 128) * ((K + Q::CH - 1) / Q::CH);
-    k_quant_act_dual_tma<<<grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st>>>(tm, M, K, q, ldq, s, lds, qT, ldqT, sT, ldsT);
-    return cudaPeekAtLastError();
+    return launch_pdl(k_quant_act_dual_tma, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, K, q, ldq, s, lds, qT, ldqT, sT, ldsT);
 }
 
 template <typename T>
@@ -1126,7 +1133,7 @@ static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, 
             cudaFuncSetAttribute(k_quant_weight_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
             if (dev >= 0 && dev < 64) attr_tma[dev] = true;
         }
-        k_quant_weight_tma<T><<<grid_for(blocks, 1, 1), Q::THREADS, Q::SMEM, st>>>(tm, N, K, q, ldq, s, ldsw, qT, ldqT);
+        return launch_pdl(k_quant_weight_tma<T>, grid_for(blocks, 1, 1), Q::THREADS, Q::SMEM, st, tm, N, K, q, ldq, s, ldsw, qT, ldqT);
     } else if (fast) {
         k_quant_weight_128x128<T><<<grid_for(blocks, 4, 4), 256, 0, st>>>(
             reinterpret_cast<const T*>(w), N, K, ldw, q, ldq, s, ldsw, qT, ldqT);

@@ -346,6 +346,11 @@ __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.
 template <uint32_t kRegs>
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kRegs)); }
 
+// Programmatic dependent launch (see internal.h launch_pdl): wait for the previous grid in the stream
+// (complete, writes visible) / let the next grid's CTAs be scheduled.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One lane of the (fully active) warp returns true.
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
