@@ -273,24 +273,8 @@ def time_dense(args, world, rank, dev):
         st.run()
     torch.cuda.synchronize()
     nL = len(st.launches)
-
-    def kernel_ms(ev):
-        return [statistics.mean(e[i][0].elapsed_time(e[i][1]) for e in ev) for i in range(nL)]
-
-    # Per-kernel breakdown: K steps with events around every launch (before the timed region; events
-    # between launches would also block the programmatic dependent launch overlap of the kernels).
-    evb = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nL)]
-           for _ in range(args.steps)]
-    for k in range(args.steps):
-        for i, (_, fn, _, _) in enumerate(st.launches):
-            evb[k][i][0].record(stream)
-            fn()
-            evb[k][i][1].record(stream)
-    torch.cuda.synchronize()
-    bd = kernel_ms(evb)
-    dom_i = max(range(nL), key=lambda i: bd[i])
-    # Timed region: K steps; events only around the dominant (roofline) kernel
-    evd = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nL)]
+          for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
@@ -298,20 +282,17 @@ def time_dense(args, world, rank, dev):
         start.record(stream)
         for k in range(args.steps):
             for i, (_, fn, _, _) in enumerate(st.launches):
-                if i == dom_i:
-                    evd[k][0].record(stream)
+                ev[k][i][0].record(stream)
                 fn()
-                if i == dom_i:
-                    evd[k][1].record(stream)
+                ev[k][i][1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     barrier(world)
     ms_local = start.elapsed_time(stop)
     ms = max_over_ranks(ms_local, world, dev)
-    dom_ms = statistics.mean(a.elapsed_time(b) for a, b in evd)
     per = {}
     for i, (name, _, kind, amount) in enumerate(st.launches):
-        d = dom_ms if i == dom_i else bd[i]
+        d = statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
         if kind == "tensor":
             ach = amount / (d * 1e-3) / 1e12
             peak = 2.0 * peaks["bf16_tflops"]       # FP8 = 2x BF16 (guide's nominal ratio)
@@ -319,9 +300,8 @@ def time_dense(args, world, rank, dev):
         else:
             ach = amount / (d * 1e-3) / 1e9
             per[name] = {"ms": d, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]}
-        per[name]["timing"] = "timed region" if i == dom_i else "breakdown pass before the timed region"
-    dom = st.launches[dom_i][0]
-    dk = st.launches[dom_i]
+    dom = max(per, key=lambda n: per[n]["ms"])
+    dk = next(l for l in st.launches if l[0] == dom)
     traffic, traffic_src = None, None
     try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
