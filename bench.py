@@ -309,11 +309,20 @@ def time_dense(args, world, rank, dev):
         traffic_src = tj["source"]
     except Exception:
         pass
+    # Tensor-bound roofline kernel: the guide's sustained peak applies to a kernel timed inside a long
+    # step; the timed region is taken as "long" when the clock sampler saw the power cap.  The burst
+    # fraction is reported next to it.
+    clocks = clk.summary()
+    sustained = dk[2] == "tensor" and "sw_power_cap" in clocks.get("reasons", [])
+    peak_t = 2.0 * (peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"])
+    roof_peak = peak_t if dk[2] == "tensor" else per[dom]["peak"]
     roof = {"kernel": dom, "bound": "tensor" if dk[2] == "tensor" else "hbm", "achieved": per[dom]["achieved"],
-            "peak": per[dom]["peak"], "unit": per[dom]["unit"], "frac": per[dom]["frac"], "traffic": traffic,
+            "peak": roof_peak, "unit": per[dom]["unit"], "frac": per[dom]["achieved"] / roof_peak, "traffic": traffic,
             "traffic_unit": "bytes per launch", "traffic_src": traffic_src,
-            "peak_src": f"{peaks['src']}: " + ("2 x bf16_tflops (burst) of MEASURED_PEAKS.json" if dk[2] == "tensor"
+            "peak_src": f"{peaks['src']}: " + (("2 x bf16_tflops_sustained (timed region power-capped: sw_power_cap)" if sustained
+                                                else "2 x bf16_tflops (burst)") + " of MEASURED_PEAKS.json" if dk[2] == "tensor"
                                                else "hbm_gbs of MEASURED_PEAKS.json"),
+            "frac_vs_burst_peak": per[dom]["frac"],
             "share_of_step": per[dom]["ms"] * args.steps / (ms_local)}
     value = world * st.flops * args.steps / (ms * 1e-3) / 1e12
     gemm_ms = sum(per[n]["ms"] for n in per if n.startswith("gemm"))
@@ -323,7 +332,7 @@ def time_dense(args, world, rank, dev):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "e4m3", "data": "synthetic", "config": config_block(args, world),
-        "roofline": roof, "clocks": clk.summary(), "gpu_launches": nL * args.steps,
+        "roofline": roof, "clocks": clocks, "gpu_launches": nL * args.steps,
         "gemm_tflops": st.flops / (gemm_ms * 1e-3) / 1e12, "gemm_frac_fp8_peak_4500": st.flops / (gemm_ms * 1e-3) / 4.5e15,
         "quantizer_gbs": q_bytes / (q_ms * 1e-3) / 1e9, "quantizer_frac_hbm": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
         "kernels": per,
