@@ -54,6 +54,16 @@ def main():
               fp.WGRAD: torch.rand(K // 128, N, device=dev)}[L]
         out = torch.empty(M, N, dtype=torch.float32 if L == fp.WGRAD else torch.bfloat16, device=dev)
         cases.append((name, 2.0 * M * N * K, (lambda L=L, A=A, sA=sA, B=B, sB=sB, out=out: fp.gemm(L, A, sA, B, sB, out=out))))
+    # C3: MLA projections over 16384 tokens (q-lora 7168 -> 1536, kv-lora 7168 -> 576), Fprop BF16 out
+    for name, (M, N, K) in (("C3_q", (16384, 1536, 7168)), ("C3_kv", (16384, 576, 7168))):
+        if only and name not in only:
+            continue
+        A = torch.randint(0, 120, (M, K), dtype=torch.uint8, device=dev)
+        B = torch.randint(0, 120, (N, K), dtype=torch.uint8, device=dev)
+        sA = torch.rand(K // 128, M, device=dev)
+        sB = torch.rand((N + 127) // 128, K // 128, device=dev)
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
+        cases.append((name, 2.0 * M * N * K, (lambda A=A, sA=sA, B=B, sB=sB, out=out: fp.gemm(fp.FPROP, A, sA, B, sB, out=out))))
     # C2: 256 experts, K=7168, N=2048, 4096 tokens x top-8 uniform
     E, N2, K2 = 256, 2048, 7168
     _, offs = W.group_rows(W.route_uniform(4096, E, 8), E)
