@@ -56,6 +56,7 @@ def lib():
         L.oracle_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
+        L.oracle_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32]
         L.oracle_grouped_gemm.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, i32]
         L.oracle_rel_err_normwise.restype = ctypes.c_double
@@ -132,6 +133,17 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True):
     lib().oracle_quantize_weight_128x128(_ptr(w), _dt(w), N, K, K, _ptr(q), K, _ptr(s), KB,
                                          _ptr(qT), N)
     return q, s, qT
+
+
+def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor):
+    """FP8 1x128 codes q [M,K] + scales s [ceil(K/128), M] -> dequantize (FP32) -> 128x1:
+    (qT uint8 [K,M], sT fp32 [ceil(M/128), K]).  P:558."""
+    q, s = q.contiguous(), s.contiguous()
+    M, K = q.shape
+    qT = torch.empty(K, M, dtype=torch.uint8)
+    sT = torch.empty((M + 127) // 128, K, dtype=torch.float32)
+    lib().oracle_requantize_1x128_to_128x1(_ptr(q), K, _ptr(s), s.shape[1], M, K, _ptr(qT), M, _ptr(sT), K)
+    return qT, sT
 
 
 def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,

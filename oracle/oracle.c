@@ -159,6 +159,22 @@ void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K
     }
 }
 
+/* FP8 -> FP8 re-quantization of a cached activation (§3.5.2: the FP8 activations
+ * of the forward pass "need to be read out, dequantized, transposed, re-quantized into 128x1
+ * tiles").  Step 1, dequantize: xhat[m,k] = RN32(dec(q[m,k]) * s(k/128, m)), the product taken
+ * exactly in FP64 (4 x 24 significant bits) and rounded once to FP32 (reading R19: the
+ * dequantized tensor is FP32).  Step 2: the 128x1 quantization of xhat (the function above). */
+void oracle_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
+                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT) {
+    float* xhat = (float*)malloc((size_t)(M > 0 ? M : 1) * (size_t)(K > 0 ? K : 1) * sizeof(float));
+    if (!xhat) return;
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t k = 0; k < K; ++k)
+            xhat[m * K + k] = (float)(oracle_e4m3_decode(q[m * ldq + k]) * (double)s[(k / 128) * lds + m]);
+    oracle_quantize_act_128x1(xhat, 1, M, K, K, qT, ldqT, sT, ldsT);
+    free(xhat);
+}
+
 /* ------------------------------------------------------------ GEMM ---- */
 static double g_dec[256];
 static int g_dec_ready = 0;

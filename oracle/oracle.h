@@ -42,6 +42,11 @@ void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K
                                     uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                     uint8_t* qT, int64_t ldqT);
 
+/* FP8 1x128 (q[m*ldq+k], s[(k/128)*lds+m]) -> dequantize to FP32 -> 128x1 (qT[k*ldqT+m],
+ * sT[(m/128)*ldsT+k]).  P:558. */
+void oracle_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
+                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT);
+
 /* O[r*N + j] = sum_kb sA(kb,i)*sB(kb,j) * sum_{c in kb} dec(A[i,c])*dec(B[j,c]),  FP64.
  * i = rows[r] (rows == NULL -> i = r, nrows = M).  Contraction K % 128 == 0.
  * sA(kb,i) = sA[kb*ldsA + i]

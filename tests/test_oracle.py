@@ -433,3 +433,39 @@ def test_rel_err_normwise():
     O = torch.tensor([1.0, -2.0, 4.0], dtype=torch.float64)
     assert oracle.rel_err_normwise(O, O) == 0.0
     assert abs(oracle.rel_err_normwise(O * 1.01, O) - 0.01) < 1e-15
+
+
+# ------------------------------------------------------- FP8 -> FP8 re-quantization ----
+@pytest.mark.parametrize("M,K", [(300, 200), (128, 256), (5, 130)])
+def test_requantize_vs_naive_dequant_then_groups(M, K):
+    """requantize_1x128_to_128x1 == an independent composition: dequantize with
+    torch's float8 decoder x float64 scale, round once to float32, then the naive 128x1 grouping
+    quantizer (brute-force encoder); ragged M and K (short last groups on both axes)."""
+    x = W.outlier_act(M, K, seed=4)
+    q, s = oracle.quantize_act_1x128(x)
+    dec = torch_decode_table()
+    xhat = (dec[q.numpy()] * np.repeat(s.numpy().T.astype(np.float64), 128, axis=1)[:, :K]).astype(np.float32)
+    groups = [np.ravel_multi_index((np.arange(m0, min(M, m0 + 128)), np.full(min(128, M - m0), c)), (M, K))
+              for c in range(K) for m0 in range(0, M, 128)]
+    qn, sn = naive_quant_groups(xhat.reshape(-1), groups)
+    qT, sT = oracle.requantize_1x128_to_128x1(q, s)
+    assert np.array_equal(qT.numpy(), qn.reshape(M, K).T)
+    assert np.array_equal(sT.numpy(), np.array(sn, np.float32).reshape(K, (M + 127) // 128).T)
+
+
+def test_requantize_closed_form_is_a_transpose():
+    """Closed form: every value is an E4M3 grid value times one power of two 2^p, and every 1x128 row
+    group and every 128x1 column group holds +-448*2^p (a diagonal of 448s in each 128x128 block).
+    Both quantizations are then exact with s = 2^p, so the re-quantized codes are the transpose."""
+    rng = np.random.default_rng(8)
+    M, K, p = 256, 384, -7
+    mags = torch_decode_table()[:127]
+    v = rng.choice(mags, size=(M, K)) * rng.choice([-1.0, 1.0], size=(M, K))
+    r, c = np.meshgrid(np.arange(M), np.arange(K), indexing="ij")
+    v = np.where((r % 128) == (c % 128), 448.0, v)
+    x = torch.from_numpy((v * 2.0 ** p).astype(np.float32))
+    q, s = oracle.quantize_act_1x128(x)
+    assert torch.all(s == 2.0 ** p)
+    qT, sT = oracle.requantize_1x128_to_128x1(q, s)
+    assert torch.all(sT == 2.0 ** p)
+    assert torch.equal(qT, q.t().contiguous())
