@@ -106,6 +106,20 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, i
                                      uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
                                      fp8bs_stream_t stream);
 
+/* ---- requantize_1x128_to_128x1: FP8 -> FP8 re-quantization of a cached activation ---------
+ * P:558 (§3.3.3) and P:672-673 (§3.5.2): the FP8 activations kept from the forward pass are "read
+ * out, dequantized, transposed, re-quantized into 128x1 tiles" for the Wgrad GEMM.
+ * q   : [M, K] uint8 codes in 1x128 tiles (fp8bs_quantize_act_1x128 output), ldq >= K.
+ * s   : [ceil(K/128), lds] FP32, lds >= M: s[(k/128)*lds + m].
+ * Dequantized value xhat[m,k] = RN32(dec(q[m,k]) * s[(k/128)*lds + m]) (FP32), then the 128x1
+ * quantization of xhat exactly as fp8bs_quantize_act_128x1 (same contract, same outputs):
+ * qT  : [K, M] uint8, ldqT >= M: qT[k*ldqT + m].    sT : [ceil(M/128), ldsT] FP32, ldsT >= K.
+ * Alignment: q, qT 16-byte aligned, ldq and ldqT multiples of 16 (else FP8BS_ERR_ALIGN).
+ * Any M, K >= 0 (short last groups on both axes).  Bit-exact vs the CPU oracle. */
+FP8BS_API fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
+                                             int64_t M, int64_t K, uint8_t* qT, int64_t ldqT,
+                                             float* sT, int64_t ldsT, fp8bs_stream_t stream);
+
 /* ---- quantize_weight_128x128 ("per 128 input channels per 128 output channels") ----
  * w   : [N, K] weights (FP32 master weights, or BF16), ldw >= K.
  * q   : [N, K] uint8 codes, ldq >= K.

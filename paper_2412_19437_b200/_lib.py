@@ -54,6 +54,9 @@ def lib() -> ctypes.CDLL:
             L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
             L.fp8bs_quantize_act_dual.restype = st
         L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+        if hasattr(L, "fp8bs_requantize_1x128_to_128x1"):
+            L.fp8bs_requantize_1x128_to_128x1.restype = st
+            L.fp8bs_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, vp]
         L.fp8bs_gemm.restype = st
         L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
         L.fp8bs_grouped_gemm.restype = st
@@ -143,6 +146,21 @@ def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torc
         sT = torch.empty((M + 127) // 128, _pad4(C), dtype=torch.float32, device=x.device)[:, :C]
     _check(lib().fp8bs_quantize_act_128x1(_p(x), _dt(x), M, C, x.stride(0), _p(qT), qT.stride(0), _p(sT),
                                           sT.stride(0), _stream(x)), "fp8bs_quantize_act_128x1")
+    return qT, sT
+
+
+def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor | None = None,
+                              sT: torch.Tensor | None = None):
+    """Cached FP8 activation q [M,K] (1x128 codes) + s [ceil(K/128), M] -> dequantize -> 128x1:
+    (qT uint8 [K,M], sT fp32 [ceil(M/128), K])  (include/fp8bs.h)."""
+    _cuda2d(q, "q")
+    M, K = q.shape
+    if qT is None:   # row pitch padded to 16 bytes (16-byte code stores)
+        qT = torch.empty(K, (M + 15) // 16 * 16, dtype=torch.uint8, device=q.device)[:, :M]
+    if sT is None:
+        sT = torch.empty((M + 127) // 128, _pad4(K), dtype=torch.float32, device=q.device)[:, :K]
+    _check(lib().fp8bs_requantize_1x128_to_128x1(_p(q), q.stride(0), _p(s), s.stride(0), M, K, _p(qT), qT.stride(0),
+                                                 _p(sT), sT.stride(0), _stream(q)), "fp8bs_requantize_1x128_to_128x1")
     return qT, sT
 
 

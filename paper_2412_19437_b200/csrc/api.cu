@@ -135,6 +135,21 @@ fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, 
                      "quantize_act_dual launch");
 }
 
+fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
+                                             int64_t M, int64_t K, uint8_t* qT, int64_t ldqT,
+                                             float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+    if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
+    if (M == 0 || K == 0) return ok();
+    if (!q || !s || !qT || !sT) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldq < K || lds < M || ldqT < M || ldsT < K) return fail(FP8BS_ERR_SHAPE, "need ldq>=K, lds>=M, ldqT>=M, ldsT>=K");
+    if (!aligned16(q) || !aligned16(qT) || ldq % 16 || ldqT % 16)
+        return fail(FP8BS_ERR_ALIGN, "q, qT must be 16-byte aligned with ldq, ldqT multiples of 16");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_requant_1x128_to_128x1(q, ldq, s, lds, M, K, qT, ldqT, sT, ldsT, (cudaStream_t)stream),
+                     "requantize_1x128_to_128x1 launch");
+}
+
 fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
                                            uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                            uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {

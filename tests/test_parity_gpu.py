@@ -150,6 +150,42 @@ W_CASES = [
 ]
 
 
+REQ_CASES = [
+    ("tiny_C0", 128, 256, "gauss"),
+    ("ragged_M_and_K", 300, 1104, "outlier"),      # short last groups on both axes
+    ("C1_X", 4096, 7168, "gauss"),                  # the bench's X: the Wgrad operand from cached FP8
+    ("special", 256, 384, "special"),               # signed zeros, subnormals, 448 boundary, huge/tiny rows
+]
+
+
+@pytest.mark.parametrize("name,M,K,kind", REQ_CASES, ids=[c[0] for c in REQ_CASES])
+def test_requantize_1x128_to_128x1_bitexact(name, M, K, kind):
+    """FP8 -> FP8 re-quantization of a cached 1x128 activation into 128x1 tiles:
+    the CUDA path through the C-ABI vs the oracle, codes and scales bit-exact."""
+    x = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act}[kind](M, K, seed=3)
+    q, s = oracle.quantize_act_1x128(x)
+    qT, sT = fp.requantize_1x128_to_128x1(dev(q), dev_scales(s))
+    rqT, rsT = oracle.requantize_1x128_to_128x1(q, s)
+    assert_bits_equal(qT, rqT, "requant codes")
+    assert_bits_equal(sT, rsT, "requant scales")
+
+
+def test_requantize_matches_direct_128x1_on_exact_inputs():
+    """When the 1x128 quantization is lossless (E4M3 grid values times a power of two with a 448 in
+    every row group), the re-quantized tiles equal the direct 128x1 quantization of the BF16 input."""
+    g = torch.Generator().manual_seed(6)
+    dec = torch.arange(127, dtype=torch.uint8).view(torch.float8_e4m3fn).float()
+    M, K = 256, 512
+    v = dec[torch.randint(0, 127, (M, K), generator=g)] * (torch.randint(0, 2, (M, K), generator=g) * 2 - 1)
+    v[:, ::128] = 448.0
+    x = (v * 2.0 ** -5).to(torch.bfloat16)
+    q, s = fp.quantize_act_1x128(dev(x))
+    qT, sT = fp.requantize_1x128_to_128x1(q, s)
+    dqT, dsT = fp.quantize_act_128x1(dev(x))
+    assert_bits_equal(qT, dqT.cpu(), "requant vs direct codes")
+    assert_bits_equal(sT, dsT.cpu(), "requant vs direct scales")
+
+
 @pytest.mark.parametrize("name,N,K,dtype", W_CASES, ids=[c[0] for c in W_CASES])
 def test_quantize_weight_bitexact(name, N, K, dtype):
     w = W.master_weight(N, K, seed=1, dtype=dtype)

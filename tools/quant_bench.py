@@ -47,6 +47,11 @@ def main():
         q1, s1 = e(M, C), e(C // 128, p4(M), dt=torch.float32)[:, :M]
         cases.append((name.replace("dual", "1x128"), 3 * M * C + 4 * M * (C // 128),
                       lambda x=x, q1=q1, s1=s1: fp.quantize_act_1x128(x, q1, s1)))
+    # FP8 -> FP8 re-quantization of the cached X (1x128 -> 128x1), the Wgrad operand
+    xq, xs = fp.quantize_act_1x128(W.gaussian_act(T, IN, seed=0).to(dev))
+    rqT, rsT = e(IN, T), e(T // 128, p4(IN), dt=torch.float32)[:, :IN]
+    cases.append(("requant(X)", T * IN * 2 + 4 * T * (IN // 128) + 4 * IN * (T // 128),
+                  lambda: fp.requantize_1x128_to_128x1(xq, xs, rqT, rsT)))
     w = W.master_weight(OUT, IN, seed=1).to(dev)
     wq, sw, wqT = e(OUT, IN), e(OUT // 128, IN // 128, dt=torch.float32), e(IN, OUT)
     cases.append(("weight(W)+T", 6 * OUT * IN + 4 * (OUT // 128) * (IN // 128),
