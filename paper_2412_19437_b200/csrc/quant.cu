@@ -1161,42 +1161,48 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
 // (§3.3.3, §3.5.2: the forward's FP8 activations are "read out,
 // dequantized, transposed, re-quantized into 128x1 tiles" for the backward pass).
 // One CTA per 128-token x 128-channel tile (exactly one 1x128 scale group per row).  Thread
-// (wc = tid & 31, rg = tid >> 5): 4 channels (one 32-bit code word) x 16 tokens.  Dequantized value
+// (wc = tid & 31, rg = tid >> 5): 4 channels (one 32-bit code word) x 8 tokens, 16 warps per CTA.  Dequantized value
 // xhat = RN32(dec(q) * s) (E4M3 -> FP16 -> FP32 is exact, one rounded FP32 multiply); column amax
-// over the tile's 128 tokens via shared memory; codes of 16 consecutive tokens per channel stored as
-// one 16-byte row segment of qT.
+// over the tile's 128 tokens via shared memory; codes staged per channel in shared memory and written
+// as 128-byte qT row segments.
 // ===========================================================================================
 namespace fp8bs {
-__global__ void __launch_bounds__(256)
+constexpr int RQ_ROWS = 8;                      // tokens per thread
+constexpr int RQ_GROUPS = 128 / RQ_ROWS;        // row groups per tile (warps per CTA)
+__global__ void __launch_bounds__(32 * RQ_GROUPS, 2)
 k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float* __restrict__ s, int64_t lds,
                          int64_t M, int64_t K, uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
-    __shared__ float red[8][128];
+    __shared__ float red[RQ_GROUPS][128];
     __shared__ float scl[128];
+    constexpr int QS = 144;                        // code staging row pitch (bytes): 128 tokens + 16
+    __shared__ __align__(16) uint8_t stage[128 * QS];
     const int tid = threadIdx.x, wc = tid & 31, rg = tid >> 5;
     const int64_t KB = (K + 127) / 128;
     const int64_t mb = blockIdx.x / KB, kb = blockIdx.x % KB;
-    const int64_t m0 = mb * 128 + rg * 16, k0 = kb * 128 + 4 * wc;
-    float v[16][4];
+    const int64_t m0 = mb * 128 + rg * RQ_ROWS, k0 = kb * 128 + 4 * wc;
+    float v[RQ_ROWS][4];
     float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    uint32_t w[RQ_ROWS];
+    float sr[RQ_ROWS];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < RQ_ROWS; ++r) {          // all loads first (RQ_ROWS in flight per thread)
         const int64_t m = m0 + r;
-        uint32_t w = 0;
-        float sr = 0.0f;
-        if (m < M && k0 < K) {
-            w = *reinterpret_cast<const uint32_t*>(q + m * ldq + k0);
-            sr = s[kb * lds + m];
-        }
-        const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w & 0xFFFFu), __NV_E4M3);
-        const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w >> 16), __NV_E4M3);
+        const bool in = m < M && k0 < K;
+        w[r] = in ? __ldg(reinterpret_cast<const uint32_t*>(q + m * ldq + k0)) : 0u;
+        sr[r] = in ? __ldg(s + kb * lds + m) : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < RQ_ROWS; ++r) {
+        const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] & 0xFFFFu), __NV_E4M3);
+        const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] >> 16), __NV_E4M3);
         const float2 d01 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
         const float2 d23 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
         const float d[4] = {d01.x, d01.y, d23.x, d23.y};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            v[r][j] = (k0 + j < K) ? __fmul_rn(d[j], sr) : 0.0f;
+            v[r][j] = (k0 + j < K) ? __fmul_rn(d[j], sr[r]) : 0.0f;
             a4[j] = fmaxf(a4[j], fabsf(v[r][j]));
         }
     }
@@ -1206,7 +1212,7 @@ k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float
     if (tid < 128) {
         float a = red[0][tid];
 #pragma unroll
-        for (int i = 1; i < 8; ++i) a = fmaxf(a, red[i][tid]);
+        for (int i = 1; i < RQ_GROUPS; ++i) a = fmaxf(a, red[i][tid]);
         const float sc = group_scale(a);
         scl[tid] = sc;
         if (kb * 128 + tid < K) sT[mb * ldsT + kb * 128 + tid] = sc;
@@ -1218,18 +1224,30 @@ k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float
         const float sc = scl[4 * wc + j];
         const float rc = __frcp_rn(sc);
         const bool fast = fast_div_ok(sc);
-        uint32_t code[4];
+        uint32_t code[RQ_ROWS / 4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RQ_ROWS / 4; ++u) {
             const float x0 = div_scale(v[4 * u][j], sc, rc, fast), x1 = div_scale(v[4 * u + 1][j], sc, rc, fast);
             const float x2 = div_scale(v[4 * u + 2][j], sc, rc, fast), x3 = div_scale(v[4 * u + 3][j], sc, rc, fast);
             code[u] = cvt_e4m3x2(x0, x1) | (cvt_e4m3x2(x2, x3) << 16);
         }
-        uint8_t* dst = qT + (k0 + j) * ldqT + m0;
-        if (m0 + 16 <= M) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(code[0], code[1], code[2], code[3]);
+        *reinterpret_cast<uint2*>(stage + (4 * wc + j) * QS + rg * RQ_ROWS) = make_uint2(code[0], code[1]);
+    }
+    // Full 128-byte qT row segments per channel (a warp writes 4 channels per instruction) instead of
+    // 8-byte pieces scattered over 32 rows.
+    __syncthreads();
+    const int64_t mt = mb * 128, kt = kb * 128;
+#pragma unroll
+    for (int i = 0; i < 1024 / (32 * RQ_GROUPS); ++i) {
+        const int pc = i * 32 * RQ_GROUPS + tid, ch = pc >> 3, off = (pc & 7) * 16;
+        if (kt + ch >= K || mt + off >= M) continue;
+        const uint4 val = *reinterpret_cast<const uint4*>(stage + ch * QS + off);
+        uint8_t* dst = qT + (kt + ch) * ldqT + mt + off;
+        if (mt + off + 16 <= M) {
+            *reinterpret_cast<uint4*>(dst) = val;
         } else {
-            for (int r = 0; r < 16 && m0 + r < M; ++r) dst[r] = (uint8_t)(code[r >> 2] >> (8 * (r & 3)));
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
+            for (int e = 0; e < 16 && mt + off + e < M; ++e) dst[e] = b[e];
         }
     }
 }
@@ -1238,6 +1256,7 @@ cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const f
                                           uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, cudaStream_t st) {
     const int64_t tiles = ((M + 127) / 128) * ((K + 127) / 128);
     if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-    return launch_pdl(k_requant_1x128_to_128x1, dim3((unsigned)tiles), dim3(256), 0, st, q, ldq, s, lds, M, K, qT, ldqT, sT, ldsT);
+    return launch_pdl(k_requant_1x128_to_128x1, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K, qT, ldqT,
+                      sT, ldsT);
 }
 }  // namespace fp8bs
