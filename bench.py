@@ -234,6 +234,8 @@ def max_over_ranks(v: float, world: int, dev) -> float:
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    # torchrun exports OMP_NUM_THREADS=1; rank 0 runs the oracle alone on the box's host cores
+    torch.set_num_threads(len(os.sched_getaffinity(0)))   # the process's OpenMP pool (shared with the oracle)
     for _ in range(args.warmup):
         cpu_sample_step()
     t, f = 0.0, 0.0
