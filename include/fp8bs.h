@@ -169,6 +169,21 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K);
 
+/* ---- grouped_gemm_dgrad: MoE expert Dgrad (NEXT-3; the backward of the grouped Fprop above) ----
+ * dX rows of expert e = dY rows of e (1x128 along the expert's output channels) x W_e:
+ * offsets, A = dYq [total_M, K] (K = the experts' output width, the contraction), sA [K/128, ldsA],
+ * D [total_M, N] (N = the experts' input width) as in fp8bs_grouped_gemm;
+ * B   : [G, N, K] uint8, contiguous: per expert the transposed weight codes WqT_e [in, out] (the qT
+ *       output of fp8bs_quantize_weight_128x128 on W_e [out, in]);
+ * sB  : [G, K/128, ceil(N/128)] FP32, contiguous: per expert the SAME sW_e array the weight quantizer
+ *       wrote ([out-block][in-block]), i.e. sB(e, kb, j) = sB[(e*(K/128) + kb)*ceil(N/128) + j/128].
+ * Same sizes, alignment and workspace rules as fp8bs_grouped_gemm. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                      const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                      const uint8_t* B, const float* sB,
+                                      void* D, fp8bs_dtype ddt, int64_t ldd,
+                                      void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

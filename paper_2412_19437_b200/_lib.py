@@ -62,6 +62,9 @@ def lib() -> ctypes.CDLL:
         L.fp8bs_grouped_gemm.restype = st
         L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
                                          vp, ctypes.c_size_t, vp]
+        if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
+            L.fp8bs_grouped_gemm_dgrad.restype = st
+            L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
         L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
         L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
         _lib = L
@@ -220,8 +223,10 @@ def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: to
 
 
 def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
-                 out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None):
-    """MoE expert Fprop: offsets int64 [G+1] (device), A [R,K], sA [K/128, R], B [G,N,K], sB [G,ceil(N/128),K/128]."""
+                 out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, layout: int = FPROP):
+    """MoE expert GEMM over token rows grouped by expert: offsets int64 [G+1] (device), A [R,K],
+    sA [K/128, R], B [G,N,K].  FPROP: sB [G,ceil(N/128),K/128] (fp8bs_grouped_gemm).  DGRAD: B holds
+    each expert's WqT [in, out], sB [G,K/128,ceil(N/128)] each expert's sW (fp8bs_grouped_gemm_dgrad)."""
     _cuda2d(A, "A")
     _cuda2d(sA, "sA")
     if offsets.dtype != torch.int64 or not offsets.is_cuda:
@@ -232,6 +237,10 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
     R = A.shape[0]
     if out is None:
         out = torch.empty(R, N, dtype=out_dtype, device=A.device)
-    _check(lib().fp8bs_grouped_gemm(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
-                                    _p(out), _dt(out), out.stride(0), None, 0, _stream(A)), "fp8bs_grouped_gemm")
+    if layout not in (FPROP, DGRAD):
+        raise ValueError("grouped layouts: FPROP, DGRAD")
+    fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
+                else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))
+    _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
+              _p(out), _dt(out), out.stride(0), None, 0, _stream(A)), name)
     return out

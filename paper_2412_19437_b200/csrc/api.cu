@@ -221,12 +221,33 @@ size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, 
     return 0;
 }
 
+static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
+                                        const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
+                                        int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
+                                        int64_t ldd, fp8bs_stream_t stream);
+
 fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                 const uint8_t* B, const float* sB,
                                 void* D, fp8bs_dtype ddt, int64_t ldd,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
     (void)workspace; (void)workspace_bytes;
+    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream);
+}
+
+fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                      const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                      const uint8_t* B, const float* sB,
+                                      void* D, fp8bs_dtype ddt, int64_t ldd,
+                                      void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    (void)workspace; (void)workspace_bytes;
+    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream);
+}
+
+static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
+                                        const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
+                                        int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
+                                        int64_t ldd, fp8bs_stream_t stream) {
     if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
     if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
     fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
@@ -236,8 +257,9 @@ fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
     GemmArgs a{};
-    a.layout = FP8BS_FPROP; a.M = total_M; a.N = N; a.K = K;
-    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = K; a.sB = sB; a.ldsB = K / 128;
+    a.layout = layout; a.M = total_M; a.N = N; a.K = K;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = K; a.sB = sB;
+    a.ldsB = layout == FP8BS_DGRAD ? (N + 127) / 128 : K / 128;
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
     a.grouped = 1; a.G = G; a.offsets = offsets;
     const char* detail = nullptr;

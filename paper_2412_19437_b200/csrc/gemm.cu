@@ -753,7 +753,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     p.num_m = (int)((a.M + C::ROWS - 1) / C::ROWS); p.num_n = (int)((a.N + BN - 1) / BN);
     p.NB = (int)((a.N + 127) / 128);
     p.sB = a.sB;
-    if (kGrouped) { p.sb_nb_stride = KB; p.sb_kb_stride = 1; p.sb_expert_stride = (int64_t)p.NB * KB; }
+    if (kGrouped && a.layout == 1) { p.sb_nb_stride = 1; p.sb_kb_stride = p.NB; p.sb_expert_stride = (int64_t)p.NB * KB; }   // grouped Dgrad
+    else if (kGrouped) { p.sb_nb_stride = KB; p.sb_kb_stride = 1; p.sb_expert_stride = (int64_t)p.NB * KB; }
     else if (a.layout == 0) { p.sb_nb_stride = a.ldsB; p.sb_kb_stride = 1; p.sb_expert_stride = 0; }
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;

@@ -328,6 +328,35 @@ def test_grouped_vs_dense_bitwise_and_oracle(counts, variant):
     assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
 
 
+@pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [256, 256], [3]])
+def test_grouped_dgrad_vs_dense_bitwise_and_oracle(counts, variant):
+    """MoE expert Dgrad (fp8bs_grouped_gemm_dgrad): per expert, dX_e = dY_e (1x128 along the expert's
+    output channels) x W_e through WqT_e and the expert's sW read [out-block][in-block]; bitwise equal to
+    the dense DGRAD GEMM on each segment, and within 1e-3 of the oracle."""
+    G, out_c, in_c = len(counts), 384, 264           # expert W_e [out, in]; contraction = out
+    offsets = torch.zeros(G + 1, dtype=torch.int64)
+    offsets[1:] = torch.cumsum(torch.tensor(counts, dtype=torch.int64), 0)
+    R = int(offsets[-1])
+    qa, sa = oracle.quantize_act_1x128(W.grad_out(R, out_c, seed=9))
+    w = W.expert_weights(G, out_c, in_c, seed=10, dtype=torch.float32)
+    qbT = torch.empty(G, in_c, out_c, dtype=torch.uint8)
+    sb = torch.empty(G, out_c // 128, (in_c + 127) // 128)
+    for e in range(G):
+        _, sb[e], qbT[e] = oracle.quantize_weight_128x128(w[e])
+    D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qbT), dev(sb), out_dtype=torch.float32,
+                        layout=fp.DGRAD)
+    torch.cuda.synchronize()
+    for e in range(G):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        De = fp.gemm(fp.DGRAD, dev(qa[a:b].contiguous()), dev_scales(sa[:, a:b].contiguous()), dev(qbT[e]), dev(sb[e]),
+                     out_dtype=torch.float32)
+        assert_bits_equal(D[a:b], De.cpu(), f"expert {e}")
+        O = oracle.gemm(oracle.DGRAD, qa[a:b].contiguous(), sa[:, a:b].contiguous(), qbT[e], sb[e])
+        assert oracle.rel_err_normwise(D[a:b].cpu().double(), O) <= TOL
+
+
 def test_grouped_C2_shape_sampled():
     """BASELINE configs[2] per-expert shape (K=7168, N=2048, ~128 rows/expert, top-8 uniform
     routing) over 32 experts so the CPU oracle stays within seconds; bench.py runs all 256."""
