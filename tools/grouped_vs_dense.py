@@ -53,6 +53,14 @@ def main():
     o4 = offs4.to(dev)
     ms = timeit(lambda: fp.grouped_gemm(o4, A4, sA4, B, sB, out=out))
     print(f"grouped C4 routing (8192 tok, {R4} rows) {ms * 1e3:8.1f} us {2 * R4 * N * K / ms / 1e9:6.0f} TFLOP/s", flush=True)
+    # the matching expert Dgrad: dY [R4, 2048] x W_e -> dX [R4, 7168] (contraction over the 2048 outputs)
+    Bd = torch.randint(0, 120, (E, K, N), dtype=torch.uint8, device=dev)        # WqT_e [in=7168, out=2048]
+    sBd = torch.rand(E, N // 128, K // 128, device=dev)
+    dYq = torch.randint(0, 120, (R4, N), dtype=torch.uint8, device=dev)
+    sdY = torch.rand(N // 128, R4, device=dev)
+    dX = torch.empty(R4, K, dtype=torch.bfloat16, device=dev)
+    ms = timeit(lambda: fp.grouped_gemm(o4, dYq, sdY, Bd, sBd, out=dX, layout=fp.DGRAD))
+    print(f"grouped Dgrad C4 routing ({R4} rows)      {ms * 1e3:8.1f} us {2 * R4 * N * K / ms / 1e9:6.0f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":
