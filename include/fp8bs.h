@@ -84,6 +84,16 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_1x128(const void* x, fp8bs_dtype xdt, 
                                       uint8_t* q, int64_t ldq, float* s, int64_t lds,
                                       fp8bs_stream_t stream);
 
+/* ---- quantize_act_1x128_pow2: 1x128 tiles with power-of-two scales --------------------------
+ * P:558 ("integral power of 2" scaling factors for the inputs of the Linear after attention) and
+ * P:565 (the activations quantized before MoE dispatch).  As fp8bs_quantize_act_1x128 except
+ * s = 2^e, the smallest power of two with 448 * 2^e >= amax (reading R23: rounded up from the exact
+ * quotient, so nothing saturates; amax 3.0 -> s = 2^-7, 3.0 / s = 384), e >= -149,
+ * 1 for an all-zero tile.  The quotient x / s is then exact before the E4M3 rounding.  Same layouts,
+ * ownership and errors as fp8bs_quantize_act_1x128; the scales feed fp8bs_gemm unchanged. */
+FP8BS_API fp8bs_status fp8bs_quantize_act_1x128_pow2(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t lds, fp8bs_stream_t stream);
+
 /* ---- quantize_act_128x1: transpose-quantize for Wgrad operands --------
  * x   : [M, C] activations (M tokens, C channels), ldx >= C.
  * qT  : [C, M] uint8 codes, ldq >= M:  qT[c*ldq + m] = E4M3(x[m,c] / sT[mb][c]), mb = m/128.
@@ -114,11 +124,15 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, i
  * Dequantized value xhat[m,k] = RN32(dec(q[m,k]) * s[(k/128)*lds + m]) (FP32), then the 128x1
  * quantization of xhat exactly as fp8bs_quantize_act_128x1 (same contract, same outputs):
  * qT  : [K, M] uint8, ldqT >= M: qT[k*ldqT + m].    sT : [ceil(M/128), ldsT] FP32, ldsT >= K.
+ * pow2 != 0: the output scales are powers of two (the paper's choice for this conversion, P:558:
+ *   s = the smallest 2^e with 448 * 2^e >= amax, see fp8bs_quantize_act_1x128_pow2).  With pow2
+ *   input scales too, every re-quantized code is the input code shifted by a power of two: no extra
+ *   rounding unless it falls below E4M3's normal range (the paper's rationale).
  * Alignment: q, qT 16-byte aligned, ldq and ldqT multiples of 16 (else FP8BS_ERR_ALIGN).
  * Any M, K >= 0 (short last groups on both axes).  Bit-exact vs the CPU oracle. */
 FP8BS_API fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
                                              int64_t M, int64_t K, uint8_t* qT, int64_t ldqT,
-                                             float* sT, int64_t ldsT, fp8bs_stream_t stream);
+                                             float* sT, int64_t ldsT, int pow2, fp8bs_stream_t stream);
 
 /* ---- quantize_weight_128x128 ("per 128 input channels per 128 output channels") ----
  * w   : [N, K] weights (FP32 master weights, or BF16), ldw >= K.

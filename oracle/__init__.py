@@ -56,7 +56,8 @@ def lib():
         L.oracle_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
-        L.oracle_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64]
+        L.oracle_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, i32]
+        L.oracle_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
         L.oracle_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32]
         L.oracle_grouped_gemm.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, i32]
         L.oracle_rel_err_normwise.restype = ctypes.c_double
@@ -112,6 +113,16 @@ def quantize_act_1x128(x: torch.Tensor):
     return q, s
 
 
+def quantize_act_1x128_pow2(x: torch.Tensor):
+    """1x128 tiles with power-of-two scales: x [M,K] -> (q [M,K], s [ceil(K/128), M])."""
+    x = x.contiguous()
+    M, K = x.shape
+    q = torch.empty(M, K, dtype=torch.uint8)
+    s = torch.empty((K + 127) // 128, M, dtype=torch.float32)
+    lib().oracle_quantize_act_1x128_pow2(_ptr(x), _dt(x), M, K, K, _ptr(q), K, _ptr(s), M)
+    return q, s
+
+
 def quantize_act_128x1(x: torch.Tensor):
     """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C])."""
     x = x.contiguous()
@@ -135,14 +146,14 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True):
     return q, s, qT
 
 
-def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor):
+def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, pow2: bool = False):
     """FP8 1x128 codes q [M,K] + scales s [ceil(K/128), M] -> dequantize (FP32) -> 128x1:
     (qT uint8 [K,M], sT fp32 [ceil(M/128), K]).  P:558."""
     q, s = q.contiguous(), s.contiguous()
     M, K = q.shape
     qT = torch.empty(K, M, dtype=torch.uint8)
     sT = torch.empty((M + 127) // 128, K, dtype=torch.float32)
-    lib().oracle_requantize_1x128_to_128x1(_ptr(q), K, _ptr(s), s.shape[1], M, K, _ptr(qT), M, _ptr(sT), K)
+    lib().oracle_requantize_1x128_to_128x1(_ptr(q), K, _ptr(s), s.shape[1], M, K, _ptr(qT), M, _ptr(sT), K, int(pow2))
     return qT, sT
 
 

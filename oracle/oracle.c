@@ -101,17 +101,41 @@ static float group_scale(float amax) {
     return s;
 }
 
+/* power-of-two scale ("integral power of 2"; SPEC S:374 / S:417 round UP): the
+ * smallest s = 2^e with 448 * s >= amax, computed on exact values (448 * 2^e is exact in double);
+ * e >= -149 (the smallest float subnormal); 1 for an all-zero group; a non-finite amax passes
+ * through (as amax / 448 does in group_scale). */
+static float group_scale_pow2(float amax) {
+    if (amax == 0.0f) return 1.0f;
+    if (!isfinite(amax)) return amax;
+    int e = -160;
+    while (ldexp(448.0, e) < (double)amax) ++e;    /* plain linear search from below */
+    if (e < -149) e = -149;
+    return ldexpf(1.0f, e);
+}
+
 /* ------------------------------------------------------ quantizers ---- */
 /* 1x128 tiles: per token m, per 128 channels kb ("per token per 128 channels"). */
+static void quantize_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                           uint8_t* q, int64_t ldq, float* s, int64_t lds, float (*scale)(float));
 void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
                                uint8_t* q, int64_t ldq, float* s, int64_t lds) {
+    quantize_1x128(x, xdt, M, K, ldx, q, ldq, s, lds, group_scale);
+}
+/* the same tiles with power-of-two scales */
+void oracle_quantize_act_1x128_pow2(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t lds) {
+    quantize_1x128(x, xdt, M, K, ldx, q, ldq, s, lds, group_scale_pow2);
+}
+static void quantize_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                           uint8_t* q, int64_t ldq, float* s, int64_t lds, float (*scale)(float)) {
     int64_t KB = (K + 127) / 128;
     for (int64_t m = 0; m < M; ++m) {
         for (int64_t kb = 0; kb < KB; ++kb) {
             int64_t k0 = kb * 128, k1 = k0 + 128 < K ? k0 + 128 : K;   /* short last group */
             float amax = 0.0f;
             for (int64_t k = k0; k < k1; ++k) amax = fmaxf(amax, fabsf(load_elem(x, xdt, m * ldx + k)));
-            float sc = group_scale(amax);
+            float sc = scale(amax);
             s[kb * lds + m] = sc;
             for (int64_t k = k0; k < k1; ++k) q[m * ldq + k] = oracle_e4m3_encode(load_elem(x, xdt, m * ldx + k) / sc);
         }
@@ -120,15 +144,21 @@ void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int
 
 /* 128x1 tiles: per channel c, per 128 tokens mb; stored transposed (qT[c][m]) so the
  * Wgrad contraction (tokens) is contiguous. */
+static void quantize_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                           uint8_t* qT, int64_t ldq, float* sT, int64_t lds, float (*scale)(float));
 void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
                                uint8_t* qT, int64_t ldq, float* sT, int64_t lds) {
+    quantize_128x1(x, xdt, M, C, ldx, qT, ldq, sT, lds, group_scale);
+}
+static void quantize_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                           uint8_t* qT, int64_t ldq, float* sT, int64_t lds, float (*scale)(float)) {
     int64_t MB = (M + 127) / 128;
     for (int64_t c = 0; c < C; ++c) {
         for (int64_t mb = 0; mb < MB; ++mb) {
             int64_t m0 = mb * 128, m1 = m0 + 128 < M ? m0 + 128 : M;
             float amax = 0.0f;
             for (int64_t m = m0; m < m1; ++m) amax = fmaxf(amax, fabsf(load_elem(x, xdt, m * ldx + c)));
-            float sc = group_scale(amax);
+            float sc = scale(amax);
             sT[mb * lds + c] = sc;
             for (int64_t m = m0; m < m1; ++m) qT[c * ldq + m] = oracle_e4m3_encode(load_elem(x, xdt, m * ldx + c) / sc);
         }
@@ -165,13 +195,14 @@ void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K
  * exactly in FP64 (4 x 24 significant bits) and rounded once to FP32 (reading R19: the
  * dequantized tensor is FP32).  Step 2: the 128x1 quantization of xhat (the function above). */
 void oracle_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
-                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT) {
+                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
+                                      int pow2) {
     float* xhat = (float*)malloc((size_t)(M > 0 ? M : 1) * (size_t)(K > 0 ? K : 1) * sizeof(float));
     if (!xhat) return;
     for (int64_t m = 0; m < M; ++m)
         for (int64_t k = 0; k < K; ++k)
             xhat[m * K + k] = (float)(oracle_e4m3_decode(q[m * ldq + k]) * (double)s[(k / 128) * lds + m]);
-    oracle_quantize_act_128x1(xhat, 1, M, K, K, qT, ldqT, sT, ldsT);
+    quantize_128x1(xhat, 1, M, K, K, qT, ldqT, sT, ldsT, pow2 ? group_scale_pow2 : group_scale);
     free(xhat);
 }
 

@@ -36,6 +36,9 @@ float   oracle_bf16_to_float(uint16_t bits);
 
 void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
                                uint8_t* q, int64_t ldq, float* s, int64_t lds);
+/* 1x128 with power-of-two scales: s = smallest 2^e with 448*2^e >= amax (e >= -149; 1 if amax == 0) */
+void oracle_quantize_act_1x128_pow2(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t lds);
 void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
                                uint8_t* qT, int64_t ldq, float* sT, int64_t lds);
 void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
@@ -45,7 +48,8 @@ void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K
 /* FP8 1x128 (q[m*ldq+k], s[(k/128)*lds+m]) -> dequantize to FP32 -> 128x1 (qT[k*ldqT+m],
  * sT[(m/128)*ldsT+k]).  P:558. */
 void oracle_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
-                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT);
+                                      int64_t M, int64_t K, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
+                                      int pow2);   /* pow2 != 0: power-of-two output scales */
 
 /* O[r*N + j] = sum_kb sA(kb,i)*sB(kb,j) * sum_{c in kb} dec(A[i,c])*dec(B[j,c]),  FP64.
  * i = rows[r] (rows == NULL -> i = r, nrows = M).  Contraction K % 128 == 0.

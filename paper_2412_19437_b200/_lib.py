@@ -56,7 +56,10 @@ def lib() -> ctypes.CDLL:
         L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
         if hasattr(L, "fp8bs_requantize_1x128_to_128x1"):
             L.fp8bs_requantize_1x128_to_128x1.restype = st
-            L.fp8bs_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, vp]
+            L.fp8bs_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, i32, vp]
+        if hasattr(L, "fp8bs_quantize_act_1x128_pow2"):
+            L.fp8bs_quantize_act_1x128_pow2.restype = st
+            L.fp8bs_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
         L.fp8bs_gemm.restype = st
         L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
         L.fp8bs_grouped_gemm.restype = st
@@ -139,6 +142,19 @@ def quantize_act_1x128(x: torch.Tensor, q: torch.Tensor | None = None, s: torch.
     return q, s
 
 
+def quantize_act_1x128_pow2(x: torch.Tensor, q: torch.Tensor | None = None, s: torch.Tensor | None = None):
+    """x [M,K] -> (q uint8 [M,K], s fp32 [ceil(K/128), M]) with power-of-two scales."""
+    _cuda2d(x, "x")
+    M, K = x.shape
+    if q is None:
+        q = torch.empty(M, K, dtype=torch.uint8, device=x.device)
+    if s is None:
+        s = torch.empty((K + 127) // 128, _pad4(M), dtype=torch.float32, device=x.device)[:, :M]
+    _check(lib().fp8bs_quantize_act_1x128_pow2(_p(x), _dt(x), M, K, x.stride(0), _p(q), q.stride(0), _p(s), s.stride(0),
+                                               _stream(x)), "fp8bs_quantize_act_1x128_pow2")
+    return q, s
+
+
 def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torch.Tensor | None = None):
     """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C])."""
     _cuda2d(x, "x")
@@ -153,7 +169,7 @@ def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torc
 
 
 def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor | None = None,
-                              sT: torch.Tensor | None = None):
+                              sT: torch.Tensor | None = None, pow2: bool = False):
     """Cached FP8 activation q [M,K] (1x128 codes) + s [ceil(K/128), M] -> dequantize -> 128x1:
     (qT uint8 [K,M], sT fp32 [ceil(M/128), K])  (include/fp8bs.h)."""
     _cuda2d(q, "q")
@@ -163,7 +179,7 @@ def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor
     if sT is None:
         sT = torch.empty((M + 127) // 128, _pad4(K), dtype=torch.float32, device=q.device)[:, :K]
     _check(lib().fp8bs_requantize_1x128_to_128x1(_p(q), q.stride(0), _p(s), s.stride(0), M, K, _p(qT), qT.stride(0),
-                                                 _p(sT), sT.stride(0), _stream(q)), "fp8bs_requantize_1x128_to_128x1")
+                                                 _p(sT), sT.stride(0), int(pow2), _stream(q)), "fp8bs_requantize_1x128_to_128x1")
     return qT, sT
 
 

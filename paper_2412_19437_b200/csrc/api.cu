@@ -107,6 +107,20 @@ fp8bs_status fp8bs_quantize_act_1x128(const void* x, fp8bs_dtype xdt, int64_t M,
                      "quantize_act_1x128 launch");
 }
 
+fp8bs_status fp8bs_quantize_act_1x128_pow2(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t lds, fp8bs_stream_t stream) {
+    if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
+    if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
+    if (M == 0 || K == 0) return ok();
+    if (!x || !q || !s) return fail(FP8BS_ERR_INVALID_ARG, "null pointer (x=%p q=%p s=%p)", x, (void*)q, (void*)s);
+    if (ldx < K || ldq < K || lds < M) return fail(FP8BS_ERR_SHAPE, "need ldx>=K, ldq>=K, lds>=M (ldx=%lld ldq=%lld lds=%lld)",
+                                                   (long long)ldx, (long long)ldq, (long long)lds);
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_quant_act_1x128_pow2(x, (int)xdt, M, K, ldx, q, ldq, s, lds, (cudaStream_t)stream),
+                     "quantize_act_1x128_pow2 launch");
+}
+
 fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, int64_t M, int64_t C, int64_t ldx,
                                       uint8_t* qT, int64_t ldq, float* sT, int64_t lds, fp8bs_stream_t stream) {
     if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
@@ -137,7 +151,7 @@ fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, 
 
 fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
                                              int64_t M, int64_t K, uint8_t* qT, int64_t ldqT,
-                                             float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+                                             float* sT, int64_t ldsT, int pow2, fp8bs_stream_t stream) {
     if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
     if (M == 0 || K == 0) return ok();
     if (!q || !s || !qT || !sT) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
@@ -146,7 +160,7 @@ fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, cons
         return fail(FP8BS_ERR_ALIGN, "q, qT must be 16-byte aligned with ldq, ldqT multiples of 16");
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
-    return from_cuda(launch_requant_1x128_to_128x1(q, ldq, s, lds, M, K, qT, ldqT, sT, ldsT, (cudaStream_t)stream),
+    return from_cuda(launch_requant_1x128_to_128x1(q, ldq, s, lds, M, K, qT, ldqT, sT, ldsT, pow2 != 0, (cudaStream_t)stream),
                      "requantize_1x128_to_128x1 launch");
 }
 

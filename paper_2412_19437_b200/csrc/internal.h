@@ -24,7 +24,9 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
                                         cudaStream_t st);
 
 cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds, int64_t M, int64_t K,
-                                          uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, cudaStream_t st);
+                                          uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, int pow2, cudaStream_t st);
+cudaError_t launch_quant_act_1x128_pow2(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
+                                        int64_t ldq, float* s, int64_t lds, cudaStream_t st);
 
 // Programmatic dependent launch (PDL): the kernel is launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so its CTAs may be scheduled while the

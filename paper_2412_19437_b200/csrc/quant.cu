@@ -157,7 +157,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
-template <typename T>
+template <typename T, bool kPow2 = false>
 __global__ void __launch_bounds__(Q1Cfg<T>::THREADS)
 k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __restrict__ q,
                       float* __restrict__ s, int64_t lds) {
@@ -216,7 +216,7 @@ k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __
             for (int e = 0; e < C::EL; ++e) amax = fmaxf(amax, fabsf(f[e]));
 #pragma unroll
             for (int o = C::L / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            const float sc = group_scale(amax);
+            const float sc = group_scale_t<kPow2>(amax);
             const float r = __frcp_rn(sc);
             uint32_t w[4];
             if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w);   // warp-uniform
@@ -942,7 +942,7 @@ k_quant_weight_128x128(const T* __restrict__ w, int64_t N, int64_t K, int64_t ld
 // [gi*gr, +gr) x cols [gj*gc, +gc); codes go to q[r*qr + c*qc] (and q2[r*q2r + c*q2c] if q2),
 // the scale to s[gi*sr + gj*sc].
 // ===========================================================================================
-template <typename T>
+template <typename T, bool kPow2 = false>
 __global__ void __launch_bounds__(128)
 k_quant_generic(const T* __restrict__ x, int64_t R, int64_t Cn, int64_t xr, int64_t xc, int gr, int gc,
                 uint8_t* __restrict__ q, int64_t qr, int64_t qc, uint8_t* __restrict__ q2, int64_t q2r, int64_t q2c,
@@ -964,7 +964,7 @@ k_quant_generic(const T* __restrict__ x, int64_t R, int64_t Cn, int64_t xr, int6
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
         __syncthreads();
         amax = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-        const float scl = group_scale(amax);
+        const float scl = group_scale_t<kPow2>(amax);
         const float rc = __frcp_rn(scl);
         const bool fast = fast_div_ok(scl);
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1023,6 +1023,39 @@ static cudaError_t launch_1x128_t(const void* x, int64_t M, int64_t K, int64_t l
             reinterpret_cast<const T*>(x), M, K, ldx, 1, 1, 128, q, ldq, 1, nullptr, 0, 0, s, 1, lds);
     }
     return cudaPeekAtLastError();
+}
+
+// Power-of-two scales (fp8bs_quantize_act_1x128_pow2): the TMA kernel for flat aligned inputs, the
+// generic kernel otherwise.
+template <typename T>
+static cudaError_t launch_1x128_pow2_t(const void* x, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
+                                       float* s, int64_t lds, cudaStream_t st) {
+    constexpr int E = Vec<T>::E;
+    const bool flat = aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (K % E == 0) && (ldx == K) &&
+                      (K % 128 == 0) && (ldq == K) && aligned16(q) && (M * (K / 128) < (1ll << 31));
+    if (flat) {
+        using C = Q1Cfg<T>;
+        static bool attr_set[64] = {false};   // per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+            cudaFuncSetAttribute(k_quant_act_1x128_tma<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+        }
+        const int64_t chunks = (M * (K / 128) + C::CHUNK_TILES - 1) / C::CHUNK_TILES;
+        return launch_pdl(k_quant_act_1x128_tma<T, true>, grid_for(chunks, 2, 2), C::THREADS, C::SMEM, st,
+                          reinterpret_cast<const T*>(x), M, K, q, s, lds);
+    }
+    const int64_t groups = M * ((K + 127) / 128);
+    k_quant_generic<T, true><<<grid_for(groups, 16, 16), 128, 0, st>>>(
+        reinterpret_cast<const T*>(x), M, K, ldx, 1, 1, 128, q, ldq, 1, nullptr, 0, 0, s, 1, lds);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_quant_act_1x128_pow2(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
+                                        int64_t ldq, float* s, int64_t lds, cudaStream_t st) {
+    if (xdt == 0) return launch_1x128_pow2_t<__nv_bfloat16>(x, M, K, ldx, q, ldq, s, lds, st);
+    return launch_1x128_pow2_t<float>(x, M, K, ldx, q, ldq, s, lds, st);
 }
 
 cudaError_t launch_quant_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
@@ -1169,6 +1202,7 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
 namespace fp8bs {
 constexpr int RQ_ROWS = 8;                      // tokens per thread
 constexpr int RQ_GROUPS = 128 / RQ_ROWS;        // row groups per tile (warps per CTA)
+template <bool kPow2>
 __global__ void __launch_bounds__(32 * RQ_GROUPS, 2)
 k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float* __restrict__ s, int64_t lds,
                          int64_t M, int64_t K, uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
@@ -1213,7 +1247,7 @@ k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float
         float a = red[0][tid];
 #pragma unroll
         for (int i = 1; i < RQ_GROUPS; ++i) a = fmaxf(a, red[i][tid]);
-        const float sc = group_scale(a);
+        const float sc = group_scale_t<kPow2>(a);
         scl[tid] = sc;
         if (kb * 128 + tid < K) sT[mb * ldsT + kb * 128 + tid] = sc;
     }
@@ -1253,10 +1287,13 @@ k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float
 }
 
 cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds, int64_t M, int64_t K,
-                                          uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, cudaStream_t st) {
+                                          uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, int pow2, cudaStream_t st) {
     const int64_t tiles = ((M + 127) / 128) * ((K + 127) / 128);
     if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-    return launch_pdl(k_requant_1x128_to_128x1, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K, qT, ldqT,
-                      sT, ldsT);
+    if (pow2)
+        return launch_pdl(k_requant_1x128_to_128x1<true>, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K,
+                          qT, ldqT, sT, ldsT);
+    return launch_pdl(k_requant_1x128_to_128x1<false>, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K,
+                      qT, ldqT, sT, ldsT);
 }
 }  // namespace fp8bs

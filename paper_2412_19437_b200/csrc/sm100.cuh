@@ -19,6 +19,25 @@ __device__ __forceinline__ float group_scale(float amax) {
     return s == 0.0f ? 1.0f : s;
 }
 
+// Power-of-two scale of a group ("integral power of 2"; reading R23: rounded UP, as
+// SPEC S:374/S:417, from the EXACT quotient): the smallest s = 2^e with 448 * s >= amax, so no
+// element saturates; e >= -149 (the smallest subnormal; amax < 448 * 2^-149 then still fits); 1
+// when amax is 0; non-finite amax gives amax (like group_scale's amax / 448).
+__device__ __forceinline__ float group_scale_pow2(float amax) {
+    if (amax == 0.0f) return 1.0f;
+    if (!(amax <= 3.4028234663852886e38f)) return amax;
+    const double a = amax;
+    int e = ilogb(a) - 9;                       // 448 * 2^e < amax here
+    while (ldexp(448.0, e) < a) ++e;            // at most three steps
+    if (e < -149) e = -149;
+    return ldexpf(1.0f, e);
+}
+template <bool kPow2>
+__device__ __forceinline__ float group_scale_t(float amax) {
+    if constexpr (kPow2) return group_scale_pow2(amax);
+    else return group_scale(amax);
+}
+
 // Whether the division-free quotient sequence is exact-equivalent for this scale
 // (reading R2: validated exhaustively for normal s in [2^-90, 2^100]; outside, true division).
 __device__ __forceinline__ bool fast_div_ok(float s) {

@@ -469,3 +469,64 @@ def test_requantize_closed_form_is_a_transpose():
     qT, sT = oracle.requantize_1x128_to_128x1(q, s)
     assert torch.all(sT == 2.0 ** p)
     assert torch.equal(qT, q.t().contiguous())
+
+
+# ------------------------------------------------------------ power-of-two scales ----
+def _pow2_scale_exact(amax: float) -> float:
+    """Independent reading R23 with exact rationals: the smallest 2^e (e >= -149) with 448 * 2^e >= amax."""
+    from fractions import Fraction
+    if amax == 0:
+        return 1.0
+    a = Fraction(amax)
+    e = -149
+    while Fraction(448) * Fraction(2) ** e < a:
+        e += 1
+    return float(Fraction(2) ** e)
+
+
+def test_pow2_scale_spec_example():
+    """tile amax 3.0 -> pow2 s = 2^-7 and 3.0 / s = 384 <= 448 (no overflow)."""
+    x = torch.zeros(1, 128, dtype=torch.float32)
+    x[0, 0], x[0, 1], x[0, 2] = 3.0, 1.0, -0.5
+    q, s = oracle.quantize_act_1x128_pow2(x)
+    assert float(s[0, 0]) == 2.0 ** -7
+    assert oracle.e4m3_decode(int(q[0, 0])) == 384.0          # exact: 3 * 2^7
+    assert oracle.e4m3_decode(int(q[0, 1])) == 128.0
+    assert oracle.e4m3_decode(int(q[0, 2])) == -64.0
+
+
+@pytest.mark.parametrize("kind", ["gauss", "outlier", "special"])
+def test_pow2_quantizer_vs_exact_rationals_and_bruteforce(kind):
+    """quantize_act_1x128_pow2 == an independent composition: exact-rational pow2 scale per group, the
+    exact quotient x / s (a power-of-two division), brute-force nearest E4M3 code; and |x / s| <= 448
+    everywhere (rounding UP never saturates)."""
+    M, K = 24, 300
+    x = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act}[kind](M, K, seed=12).float()
+    q, s = oracle.quantize_act_1x128_pow2(x)
+    xn = x.numpy()
+    for m in range(M):
+        for kb in range((K + 127) // 128):
+            v = xn[m, kb * 128:(kb + 1) * 128]
+            sc = _pow2_scale_exact(float(np.max(np.abs(v))))
+            assert float(s[kb, m]) == np.float32(sc)
+            quot = (v.astype(np.float64) / sc).astype(np.float32)     # exact unless below float's range
+            assert np.all(np.abs(quot) <= 448.0)
+            assert np.array_equal(q[m, kb * 128:(kb + 1) * 128].numpy(), brute_encode(quot))
+
+
+def test_requantize_pow2_loses_nothing():
+    """P:558's rationale for power-of-two scales: re-quantizing pow2-scaled FP8 into 128x1 tiles with
+    pow2 scales only shifts exponents, so every dequantized value whose new quotient stays in E4M3's
+    normal range (>= 2^-6) is unchanged."""
+    M, K = 256, 384
+    x = W.gaussian_act(M, K, seed=13)
+    q, s = oracle.quantize_act_1x128_pow2(x)
+    qT, sT = oracle.requantize_1x128_to_128x1(q, s, pow2=True)
+    dec = torch_decode_table()
+    s_mk = np.repeat(s.numpy().T.astype(np.float64), 128, axis=1)[:, :K]      # s(k // 128, m) at [m, k]
+    sT_mk = np.repeat(sT.numpy().astype(np.float64), 128, axis=0)[:M, :]      # sT(m // 128, k) at [m, k]
+    before = dec[q.numpy()] * s_mk
+    after = dec[qT.numpy()].T * sT_mk
+    normal = np.abs(before) >= sT_mk * 2.0 ** -6
+    assert normal.mean() > 0.9
+    assert np.array_equal(before[normal], after[normal])

@@ -170,6 +170,44 @@ def test_requantize_1x128_to_128x1_bitexact(name, M, K, kind):
     assert_bits_equal(sT, rsT, "requant scales")
 
 
+POW2_CASES = [
+    ("flat_tma", 256, 1024, "outlier", torch.bfloat16),    # the TMA 1x128 kernel
+    ("ragged_generic", 300, 1100, "gauss", torch.bfloat16),  # K % 128 != 0 -> generic kernel
+    ("special_fp32", 64, 384, "special", torch.float32),    # subnormal / huge groups, FP32 input
+]
+
+
+@pytest.mark.parametrize("name,M,K,kind,dtype", POW2_CASES, ids=[c[0] for c in POW2_CASES])
+def test_quantize_act_1x128_pow2_bitexact(name, M, K, kind, dtype):
+    """Power-of-two 1x128 scales: codes and scales bit-exact vs the oracle."""
+    x = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act}[kind](M, K, seed=14).to(dtype)
+    q, s = fp.quantize_act_1x128_pow2(dev(x))
+    rq, rs = oracle.quantize_act_1x128_pow2(x)
+    assert_bits_equal(q, rq, "pow2 codes")
+    assert_bits_equal(s, rs, "pow2 scales")
+
+
+@pytest.mark.parametrize("name,M,K,kind", REQ_CASES, ids=[c[0] for c in REQ_CASES])
+def test_requantize_pow2_bitexact(name, M, K, kind):
+    """The paper's re-quantization with power-of-two scales on both sides: bit-exact."""
+    x = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act}[kind](M, K, seed=15)
+    q, s = oracle.quantize_act_1x128_pow2(x)
+    qT, sT = fp.requantize_1x128_to_128x1(dev(q), dev_scales(s), pow2=True)
+    rqT, rsT = oracle.requantize_1x128_to_128x1(q, s, pow2=True)
+    assert_bits_equal(qT, rqT, "pow2 requant codes")
+    assert_bits_equal(sT, rsT, "pow2 requant scales")
+
+
+def test_gemm_with_pow2_scales_vs_oracle():
+    """Power-of-two scales feed the same block-scaled GEMM (scales are arbitrary FP32 there)."""
+    M, N, K = 256, 512, 1024
+    qa, sa = oracle.quantize_act_1x128_pow2(W.outlier_act(M, K, seed=16))
+    qb, sb, _ = oracle.quantize_weight_128x128(W.master_weight(N, K, seed=17))
+    D = fp.gemm(fp.FPROP, dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32)
+    O = oracle.gemm(oracle.FPROP, qa, sa, qb, sb)
+    assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+
+
 def test_requantize_matches_direct_128x1_on_exact_inputs():
     """When the 1x128 quantization is lossless (E4M3 grid values times a power of two with a 448 in
     every row group), the re-quantized tiles equal the direct 128x1 quantization of the BF16 input."""
