@@ -102,3 +102,21 @@ def test_grouped_validation():
 def test_python_binding_rejects_cpu_tensors():
     with pytest.raises(ValueError):
         fp.quantize_act_1x128(torch.zeros(4, 128))
+
+
+def test_requant_pow2_and_grouped_dgrad_validation():
+    """Host-side validation of the entry points added in this round (no device needed)."""
+    lib = fp.lib()
+    A16 = ctypes.c_void_p(1 << 20)
+    # fp8bs_requantize_1x128_to_128x1(q, ldq, s, lds, M, K, qT, ldqT, sT, ldsT, pow2, stream)
+    assert lib.fp8bs_requantize_1x128_to_128x1(None, 256, A16, 64, 64, 256, A16, 64, A16, 256, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_requantize_1x128_to_128x1(A16, 200, A16, 64, 64, 256, A16, 64, A16, 256, 0, None) == L.ERR_SHAPE  # ldq < K
+    assert lib.fp8bs_requantize_1x128_to_128x1(A16, 264, A16, 64, 64, 256, A16, 64, A16, 256, 1, None) == L.ERR_ALIGN  # ldq % 16
+    assert lib.fp8bs_requantize_1x128_to_128x1(A16, 256, A16, 64, 64, 256, A16, 64, A16, 255, 0, None) == L.ERR_SHAPE  # ldsT < K
+    assert lib.fp8bs_requantize_1x128_to_128x1(A16, 256, A16, 64, 0, 256, A16, 64, A16, 256, 0, None) == L.OK         # M == 0
+    # fp8bs_quantize_act_1x128_pow2: same contract as fp8bs_quantize_act_1x128
+    assert lib.fp8bs_quantize_act_1x128_pow2(A16, 2, 10, 128, 128, A16, 128, A16, 10, None) == L.ERR_INVALID_ARG   # dtype
+    assert lib.fp8bs_quantize_act_1x128_pow2(A16, 0, 10, 128, 100, A16, 128, A16, 10, None) == L.ERR_SHAPE         # ldx < K
+    # fp8bs_grouped_gemm_dgrad: same rules as the grouped Fprop
+    assert lib.fp8bs_grouped_gemm_dgrad(0, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_dgrad(4, 10, 256, 500, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_SHAPE
