@@ -1200,100 +1200,153 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
 // as 128-byte qT row segments.
 // ===========================================================================================
 namespace fp8bs {
-constexpr int RQ_ROWS = 8;                      // tokens per thread
-constexpr int RQ_GROUPS = 128 / RQ_ROWS;        // row groups per tile (warps per CTA)
+// Persistent, TMA-fed: a producer warp streams 128-token x 128-channel code tiles (16 KB) into a
+// 4-stage ring; 8 consumer warps (thread: 4 channels = one code word x 16 tokens) dequantize, reduce
+// the column amax through shared memory, encode, stage the codes per channel and write 128-byte qT
+// row segments.  2 CTAs per SM.
+struct RQCfg {
+    static constexpr int STAGES = 4, CONSUMERS = 8, THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int TILE_BYTES = 128 * 128;
+    static constexpr int QSTR = 144;                         // code staging row pitch (bytes)
+    static constexpr int OFF_Q = STAGES * TILE_BYTES;
+    static constexpr int OFF_RED = OFF_Q + 128 * QSTR;      // partial amax [8][128]
+    static constexpr int OFF_SC = OFF_RED + 8 * 128 * 4;    // tile scales [128]
+    static constexpr int OFF_BAR = OFF_SC + 128 * 4;
+    static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
+};
+
 template <bool kPow2>
-__global__ void __launch_bounds__(32 * RQ_GROUPS, 2)
-k_requant_1x128_to_128x1(const uint8_t* __restrict__ q, int64_t ldq, const float* __restrict__ s, int64_t lds,
+__global__ void __launch_bounds__(RQCfg::THREADS, 2)
+k_requant_1x128_to_128x1(const __grid_constant__ CUtensorMap tmQ, const float* __restrict__ s, int64_t lds,
                          int64_t M, int64_t K, uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
+    using P = RQCfg;
+    extern __shared__ __align__(128) uint8_t smem[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
-    __shared__ float red[RQ_GROUPS][128];
-    __shared__ float scl[128];
-    constexpr int QS = 144;                        // code staging row pitch (bytes): 128 tokens + 16
-    __shared__ __align__(16) uint8_t stage[128 * QS];
-    const int tid = threadIdx.x, wc = tid & 31, rg = tid >> 5;
-    const int64_t KB = (K + 127) / 128;
-    const int64_t mb = blockIdx.x / KB, kb = blockIdx.x % KB;
-    const int64_t m0 = mb * 128 + rg * RQ_ROWS, k0 = kb * 128 + 4 * wc;
-    float v[RQ_ROWS][4];
-    float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    uint32_t w[RQ_ROWS];
-    float sr[RQ_ROWS];
-#pragma unroll
-    for (int r = 0; r < RQ_ROWS; ++r) {          // all loads first (RQ_ROWS in flight per thread)
-        const int64_t m = m0 + r;
-        const bool in = m < M && k0 < K;
-        w[r] = in ? __ldg(reinterpret_cast<const uint32_t*>(q + m * ldq + k0)) : 0u;
-        sr[r] = in ? __ldg(s + kb * lds + m) : 0.0f;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + P::OFF_BAR;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < P::STAGES; ++i) { mbar_init(bar0 + 8 * i, 1); mbar_init(bar0 + 8 * (P::STAGES + i), P::CONSUMERS); }
+        fence_mbar_init();
     }
+    __syncthreads();
+    const int64_t KB = (K + 127) / 128, MB = (M + 127) / 128;
+    const int64_t ntiles = MB * KB;
+    if (warp == P::CONSUMERS) {                          // producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tmQ);
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int st = it % P::STAGES;
+                mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
+                mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
+                tma_load_2d(sbase + st * P::TILE_BYTES, &tmQ, bar0 + 8 * st, (int)((t % KB) * 128), (int)((t / KB) * 128));
+            }
+        }
+        return;
+    }
+    float (*red)[128] = reinterpret_cast<float (*)[128]>(smem + P::OFF_RED);
+    float* scl = reinterpret_cast<float*>(smem + P::OFF_SC);
+    uint8_t* stage = smem + P::OFF_Q;
+    const int tid = threadIdx.x, wc = tid & 31, rg = tid >> 5;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % P::STAGES;
+        const int64_t mb = t / KB, kb = t - mb * KB;
+        const int64_t m0 = mb * 128 + rg * 16, k0 = kb * 128 + 4 * wc;
+        // row scales of this thread's 16 tokens (the same for the whole warp: broadcast loads)
+        float sr[16];
 #pragma unroll
-    for (int r = 0; r < RQ_ROWS; ++r) {
-        const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] & 0xFFFFu), __NV_E4M3);
-        const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] >> 16), __NV_E4M3);
-        const float2 d01 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
-        const float2 d23 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
-        const float d[4] = {d01.x, d01.y, d23.x, d23.y};
+        for (int r = 0; r < 16; ++r) sr[r] = (m0 + r < M) ? __ldg(s + kb * lds + m0 + r) : 0.0f;
+        mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
+        uint32_t w[16];
+        const uint32_t tile = sbase + st * P::TILE_BYTES;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) w[r] = lds32(tile + (rg * 16 + r) * 128 + wc * 4);
+        // TMA-written stage read with ld.shared: proxy fence before the release (gemm.cu release_scales)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));
+        float v[16][4];
+        float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] & 0xFFFFu), __NV_E4M3);
+            const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] >> 16), __NV_E4M3);
+            const float2 d01 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
+            const float2 d23 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+            const float d[4] = {d01.x, d01.y, d23.x, d23.y};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[r][j] = __fmul_rn(d[j], sr[r]);                 // TMA zero-fills codes past M / K
+                a4[j] = fmaxf(a4[j], fabsf(v[r][j]));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[rg][4 * wc + j] = a4[j];
+        named_bar_sync(1, 32 * P::CONSUMERS);
+        if (tid < 128) {
+            float a = red[0][tid];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) a = fmaxf(a, red[i][tid]);
+            const float sc = group_scale_t<kPow2>(a);
+            scl[tid] = sc;
+            if (kb * 128 + tid < K) sT[mb * ldsT + kb * 128 + tid] = sc;
+        }
+        named_bar_sync(1, 32 * P::CONSUMERS);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            v[r][j] = (k0 + j < K) ? __fmul_rn(d[j], sr[r]) : 0.0f;
-            a4[j] = fmaxf(a4[j], fabsf(v[r][j]));
+            const float sc = scl[4 * wc + j];
+            const float rc = __frcp_rn(sc);
+            const bool fast = fast_div_ok(sc);
+            uint32_t code[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float x0 = div_scale(v[4 * u][j], sc, rc, fast), x1 = div_scale(v[4 * u + 1][j], sc, rc, fast);
+                const float x2 = div_scale(v[4 * u + 2][j], sc, rc, fast), x3 = div_scale(v[4 * u + 3][j], sc, rc, fast);
+                code[u] = cvt_e4m3x2(x0, x1) | (cvt_e4m3x2(x2, x3) << 16);
+            }
+            *reinterpret_cast<uint4*>(stage + (4 * wc + j) * P::QSTR + rg * 16) = make_uint4(code[0], code[1], code[2], code[3]);
         }
-    }
+        named_bar_sync(1, 32 * P::CONSUMERS);
+        // 128-byte qT row segments: a warp writes 4 channels per instruction
+        const int64_t mt = mb * 128, kt = kb * 128;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[rg][4 * wc + j] = a4[j];
-    __syncthreads();
-    if (tid < 128) {
-        float a = red[0][tid];
-#pragma unroll
-        for (int i = 1; i < RQ_GROUPS; ++i) a = fmaxf(a, red[i][tid]);
-        const float sc = group_scale_t<kPow2>(a);
-        scl[tid] = sc;
-        if (kb * 128 + tid < K) sT[mb * ldsT + kb * 128 + tid] = sc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (k0 + j >= K) continue;
-        const float sc = scl[4 * wc + j];
-        const float rc = __frcp_rn(sc);
-        const bool fast = fast_div_ok(sc);
-        uint32_t code[RQ_ROWS / 4];
-#pragma unroll
-        for (int u = 0; u < RQ_ROWS / 4; ++u) {
-            const float x0 = div_scale(v[4 * u][j], sc, rc, fast), x1 = div_scale(v[4 * u + 1][j], sc, rc, fast);
-            const float x2 = div_scale(v[4 * u + 2][j], sc, rc, fast), x3 = div_scale(v[4 * u + 3][j], sc, rc, fast);
-            code[u] = cvt_e4m3x2(x0, x1) | (cvt_e4m3x2(x2, x3) << 16);
+        for (int i = 0; i < 1024 / (32 * P::CONSUMERS); ++i) {
+            const int pc = i * 32 * P::CONSUMERS + tid, ch = pc >> 3, off = (pc & 7) * 16;
+            if (kt + ch >= K || mt + off >= M) continue;
+            const uint4 val = *reinterpret_cast<const uint4*>(stage + ch * P::QSTR + off);
+            uint8_t* dst = qT + (kt + ch) * ldqT + mt + off;
+            if (mt + off + 16 <= M) {
+                *reinterpret_cast<uint4*>(dst) = val;
+            } else {
+                const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
+                for (int e = 0; e < 16 && mt + off + e < M; ++e) dst[e] = b[e];
+            }
         }
-        *reinterpret_cast<uint2*>(stage + (4 * wc + j) * QS + rg * RQ_ROWS) = make_uint2(code[0], code[1]);
-    }
-    // Full 128-byte qT row segments per channel (a warp writes 4 channels per instruction) instead of
-    // 8-byte pieces scattered over 32 rows.
-    __syncthreads();
-    const int64_t mt = mb * 128, kt = kb * 128;
-#pragma unroll
-    for (int i = 0; i < 1024 / (32 * RQ_GROUPS); ++i) {
-        const int pc = i * 32 * RQ_GROUPS + tid, ch = pc >> 3, off = (pc & 7) * 16;
-        if (kt + ch >= K || mt + off >= M) continue;
-        const uint4 val = *reinterpret_cast<const uint4*>(stage + ch * QS + off);
-        uint8_t* dst = qT + (kt + ch) * ldqT + mt + off;
-        if (mt + off + 16 <= M) {
-            *reinterpret_cast<uint4*>(dst) = val;
-        } else {
-            const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
-            for (int e = 0; e < 16 && mt + off + e < M; ++e) dst[e] = b[e];
-        }
+        // the staging buffer and red[] are rewritten for the next tile only after the next tile's
+        // first barrier, which every warp reaches after its stores above
     }
 }
 
 cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds, int64_t M, int64_t K,
                                           uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, int pow2, cudaStream_t st) {
+    using P = RQCfg;
+    alignas(64) CUtensorMap tm;
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
+    const uint64_t str[1] = {(uint64_t)ldq};
+    const uint32_t box[2] = {128, 128};
+    if (!make_tmap(&tm, TMAP_U8, 2, q, dims, str, box, 0)) return cudaErrorInvalidValue;
+    static bool attr[2][64] = {{false}};   // per instantiation and device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = pow2 ? k_requant_1x128_to_128x1<true> : k_requant_1x128_to_128x1<false>;
+    if (dev < 0 || dev >= 64 || !attr[pow2 ? 1 : 0][dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM);
+        if (dev >= 0 && dev < 64) attr[pow2 ? 1 : 0][dev] = true;
+    }
     const int64_t tiles = ((M + 127) / 128) * ((K + 127) / 128);
-    if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-    if (pow2)
-        return launch_pdl(k_requant_1x128_to_128x1<true>, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K,
-                          qT, ldqT, sT, ldsT);
-    return launch_pdl(k_requant_1x128_to_128x1<false>, dim3((unsigned)tiles), dim3(32 * RQ_GROUPS), 0, st, q, ldq, s, lds, M, K,
-                      qT, ldqT, sT, ldsT);
+    return launch_pdl(kern, grid_for(tiles, 2, 2), P::THREADS, P::SMEM, st, tm, s, lds, M, K, qT, ldqT, sT, ldsT);
 }
 }  // namespace fp8bs
