@@ -1,0 +1,147 @@
+// tools/mx_probe.cu — probe of tcgen05.mma.kind::mxf8f6f4.block_scale (UE8M0 scale factors in TMEM)
+// for the NEXT-1 design.  Experiments only, not product code.
+// One CTA, M = 128, N = 128, K = 128 (4 MMAs of K = 32, one scale byte per row / column each).
+// A = B = all 1.0 (E4M3 0x38), so D[i,j] = sum_t 32 * 2^(ea(i,t) + eb(j,t) - 254) if the scale
+// factors are read as hypothesised.  Scale factors are written with tcgen05.st.32x32b (each warp its
+// lane quadrant).  Measured on B200 (this round):
+//   H1 (lane i holds row i, byte t = K-step t): wrong outside rows 0..31 x columns 0..31;
+//   H2 (cutlass Sm1xxBlkScaledConfig atom, as tcgen05.cp 32x128b.warpx4 leaves it): the scale factor
+//      of row (or B column) l + 32 r1 for K-step t sits in TMEM lane l of EVERY lane quadrant,
+//      column C + r1, byte t (sf_id = t in the instruction descriptor) -> all 16384 elements exact.
+// So one 128-row K-block (4 K-steps of 32) needs 4 TMEM columns per 128 rows/columns.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mx_probe tools/mx_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cmath>
+#include <cuda_runtime.h>
+#include "../paper_2412_19437_b200/csrc/sm100.cuh"
+
+using namespace fp8bs;
+
+constexpr int M = 128, N = 128, KB = 128;
+constexpr int CA = 256, CB = 260;                 // TMEM columns of the scale factors
+
+__host__ __device__ inline int ea(int i, int t) { return 127 + (i % 3) + t; }        // A scale exponent (biased)
+__host__ __device__ inline int eb(int j, int t) { return 127 + (j % 5) - t; }        // B scale exponent (biased)
+
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// block-scaled instruction descriptor (cute/arch/mma_sm100_desc.hpp InstrDescriptorBlockScaled)
+__host__ __device__ constexpr uint32_t idesc_mx(uint32_t m, uint32_t n, uint32_t a_sf_id, uint32_t b_sf_id) {
+    return (b_sf_id << 4) | (0u << 7) | (0u << 10) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24) | (a_sf_id << 29);
+}
+
+__device__ __forceinline__ void mma_mx(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                 :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+
+// canonical K-major SWIZZLE_128B tile: row r (128 B of K), 8-row groups 1024 B apart, 16-byte chunk
+// c of row r stored at chunk c ^ (r % 8)
+__device__ inline uint32_t sw128_off(int r, int k) {
+    return (r / 8) * 1024 + (r % 8) * 128 + (((k / 16) ^ (r % 8)) * 16) + (k % 16);
+}
+
+__global__ void __launch_bounds__(128, 1) k_probe(float* out, int mode) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t* a = smem;
+    uint8_t* b = smem + M * KB;
+    for (int i = tid; i < M * KB; i += 128) a[sw128_off(i / KB, i % KB)] = 0x38;     // 1.0
+    for (int i = tid; i < N * KB; i += 128) b[sw128_off(i / KB, i % KB)] = 0x38;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) tmem_alloc<512>(smem_u32(&s_tmem));
+    if (tid == 0) { mbar_init(smem_u32(&s_bar), 1); fence_mbar_init(); }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = s_tmem;
+    const int r = warp * 32 + lane;
+    const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+    if (mode == 0) {
+        // H1: lane r holds row / column r, byte t = K-step t
+        uint32_t sfa = 0, sfb = 0;
+        for (int t = 0; t < 4; ++t) {
+            sfa |= (uint32_t)ea(r, t) << (8 * t);
+            sfb |= (uint32_t)eb(r, t) << (8 * t);
+        }
+        tmem_st1(lane_base + CA, sfa);
+        tmem_st1(lane_base + CB, sfb);
+    } else {
+        // H2 (cutlass Sm1xxBlkScaledConfig atom, replicated to the 4 lane quadrants as tcgen05.cp
+        // 32x128b.warpx4 does): lane l (any quadrant) column C + r1 byte t = row / column l + 32 r1, K-step t
+        for (int r1 = 0; r1 < 4; ++r1) {
+            uint32_t sfa = 0, sfb = 0;
+            for (int t = 0; t < 4; ++t) {
+                sfa |= (uint32_t)ea(lane + 32 * r1, t) << (8 * t);
+                sfb |= (uint32_t)eb(lane + 32 * r1, t) << (8 * t);
+            }
+            tmem_st1(lane_base + CA + r1, sfa);
+            tmem_st1(lane_base + CB + r1, sfb);
+        }
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint64_t ad = sdesc_k_sw128(smem_u32(a)), bd = sdesc_k_sw128(smem_u32(b));
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t sfa_addr = tbase + CA + ((uint32_t)t << 30);
+                const uint32_t sfb_addr = tbase + CB + ((uint32_t)t << 30);
+                const uint32_t id = idesc_mx(M, N, (uint32_t)t, (uint32_t)t);
+                mma_mx(tbase, ad + 2 * t, bd + 2 * t, id, sfa_addr, sfb_addr, t > 0 ? 1u : 0u);
+            }
+            mma_commit(smem_u32(&s_bar));
+        }
+        __syncwarp();
+    }
+    mbar_wait(smem_u32(&s_bar), 0);
+    tc_fence_after();
+    uint32_t v[32];
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        FP8BS_TMEM_LD32(lane_base + c0, v);
+        tmem_ld_wait();
+        for (int j = 0; j < 32; ++j) out[r * N + c0 + j] = __uint_as_float(v[j]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+int main() {
+    float* d;
+    cudaMalloc(&d, M * N * sizeof(float));
+    const int smem = 1024 + M * KB + N * KB;
+    cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    float* h = new float[M * N];
+    for (int mode = 0; mode < 2; ++mode) {
+        cudaMemset(d, 0, M * N * sizeof(float));
+        k_probe<<<1, 128, smem>>>(d, mode);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("mode %d: CUDA error %s\n", mode, cudaGetErrorString(e)); return 1; }
+        cudaMemcpy(h, d, M * N * sizeof(float), cudaMemcpyDeviceToHost);
+        int bad = 0;
+        for (int i = 0; i < M; ++i)
+            for (int j = 0; j < N; ++j) {
+                double want = 0;
+                for (int t = 0; t < 4; ++t) want += 32.0 * ldexp(1.0, ea(i, t) + eb(j, t) - 254);
+                if (h[i * N + j] != (float)want) {
+                    if (bad < 6) printf("mode %d: D[%d][%d] = %g, hypothesis %g\n", mode, i, j, h[i * N + j], want);
+                    ++bad;
+                }
+            }
+        printf("mode %d (%s): %d of %d elements differ from the hypothesis\n", mode,
+               mode == 0 ? "H1: lane = row, byte = K-step" : "H2: lane = row % 32 in every quadrant, column += row / 32, byte = K-step", bad, M * N);
+        printf("  samples: D[0][0]=%g D[1][0]=%g D[0][1]=%g D[5][7]=%g D[100][63]=%g\n", h[0], h[N], h[1], h[5 * N + 7], h[100 * N + 63]);
+    }
+    return 0;
+}
