@@ -65,7 +65,9 @@ __global__ void __launch_bounds__(128, 1) k_probe(float* out, int mode) {
     const uint32_t tbase = s_tmem;
     const int r = warp * 32 + lane;
     const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
-    if (mode == 0) {
+    if (mode == 2) {
+        // written below with tcgen05.cp
+    } else if (mode == 0) {
         // H1: lane r holds row / column r, byte t = K-step t
         uint32_t sfa = 0, sfb = 0;
         for (int t = 0; t < 4; ++t) {
@@ -88,11 +90,35 @@ __global__ void __launch_bounds__(128, 1) k_probe(float* out, int mode) {
         }
     }
     tmem_st_wait();
+    // mode 2: the same H2 layout delivered by tcgen05.cp.32x128b.warpx4 from shared memory: a 32-row x
+    // 16-byte atom (row l = bytes [r1][t]), no swizzle, 8-row core matrices 128 B apart (SBO)
+    uint8_t* sfa_s = smem + M * KB + N * KB;
+    uint8_t* sfb_s = sfa_s + 512;
+    if (mode == 2 && tid < 32) {
+        for (int r1 = 0; r1 < 4; ++r1)
+            for (int t = 0; t < 4; ++t) {
+                sfa_s[tid * 16 + 4 * r1 + t] = (uint8_t)ea(tid + 32 * r1, t);
+                sfb_s[tid * 16 + 4 * r1 + t] = (uint8_t)eb(tid + 32 * r1, t);
+            }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 0) {
         if (elect_one()) {
+            if (mode == 2) {
+                auto cpdesc = [](uint32_t addr) -> uint64_t {
+                    uint64_t d = 0;
+                    d |= (uint64_t)((addr >> 4) & 0x3FFF);     // start
+                    d |= (uint64_t)(16 >> 4) << 16;            // LBO (one core matrix along K)
+                    d |= (uint64_t)(128 >> 4) << 32;           // SBO: 8-row core matrices 128 B apart
+                    d |= (uint64_t)1 << 46;                    // sm100 descriptor version
+                    return d;                                  // no swizzle
+                };
+                asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" :: "r"(tbase + CA), "l"(cpdesc(smem_u32(sfa_s))));
+                asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" :: "r"(tbase + CB), "l"(cpdesc(smem_u32(sfb_s))));
+            }
             const uint64_t ad = sdesc_k_sw128(smem_u32(a)), bd = sdesc_k_sw128(smem_u32(b));
             for (int t = 0; t < 4; ++t) {
                 const uint32_t sfa_addr = tbase + CA + ((uint32_t)t << 30);
@@ -120,10 +146,10 @@ __global__ void __launch_bounds__(128, 1) k_probe(float* out, int mode) {
 int main() {
     float* d;
     cudaMalloc(&d, M * N * sizeof(float));
-    const int smem = 1024 + M * KB + N * KB;
+    const int smem = 1024 + M * KB + N * KB + 1024;
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     float* h = new float[M * N];
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 3; ++mode) {
         cudaMemset(d, 0, M * N * sizeof(float));
         k_probe<<<1, 128, smem>>>(d, mode);
         cudaError_t e = cudaDeviceSynchronize();
@@ -140,7 +166,8 @@ int main() {
                 }
             }
         printf("mode %d (%s): %d of %d elements differ from the hypothesis\n", mode,
-               mode == 0 ? "H1: lane = row, byte = K-step" : "H2: lane = row % 32 in every quadrant, column += row / 32, byte = K-step", bad, M * N);
+               mode == 0 ? "H1: lane = row, byte = K-step" : mode == 1 ? "H2: lane = row % 32 in every quadrant, column += row / 32, byte = K-step"
+                                                              : "H2 via tcgen05.cp.32x128b.warpx4 from a 32 x 16-byte smem atom", bad, M * N);
         printf("  samples: D[0][0]=%g D[1][0]=%g D[0][1]=%g D[5][7]=%g D[100][63]=%g\n", h[0], h[N], h[1], h[5 * N + 7], h[100 * N + 63]);
     }
     return 0;
