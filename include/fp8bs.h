@@ -165,6 +165,18 @@ FP8BS_API fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int
                         void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
                         fp8bs_stream_t stream);
 
+/* ---- gemm_mx: the same GEMM for POWER-OF-TWO scales on the tensor core's block scaling ----------
+ * NEXT-1 (P:558, P:565 power-of-two scales; scaling inside the MMA).  Identical arguments,
+ * layouts and validation as fp8bs_gemm, with one precondition: every sA and sB value is an exact power
+ * of two in [2^-127, 2^127] (e.g. from fp8bs_quantize_act_1x128_pow2).  Each scale is passed to
+ * tcgen05.mma.kind::mxf8f6f4.block_scale as its UE8M0 exponent, so there is no FP32 promotion step;
+ * a scale that is not a power of two is silently truncated to its exponent (undefined results). */
+FP8BS_API fp8bs_status fp8bs_gemm_mx(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                           const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                           const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                           void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
+                           fp8bs_stream_t stream);
+
 /* ---- grouped_gemm: MoE expert Fprop over token rows grouped by expert
  * offsets : DEVICE int64 [G+1], offsets[0] = 0, non-decreasing, offsets[G] = total_M; rows
  *           [offsets[e], offsets[e+1]) of A belong to expert e.  Any M_e >= 0 (no token

@@ -60,6 +60,9 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "fp8bs_quantize_act_1x128_pow2"):
             L.fp8bs_quantize_act_1x128_pow2.restype = st
             L.fp8bs_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+        if hasattr(L, "fp8bs_gemm_mx"):
+            L.fp8bs_gemm_mx.restype = st
+            L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
         L.fp8bs_gemm.restype = st
         L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
         L.fp8bs_grouped_gemm.restype = st
@@ -220,9 +223,11 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None
 
 # ------------------------------------------------------------------------ GEMM ----
 def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
-         out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, accumulate: bool = False):
+         out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, accumulate: bool = False,
+         mx: bool = False):
     """D [M,N] (+)= block-scaled A [M,K] x B [N,K]^T (see include/fp8bs.h for the sB layout per
-    layout).  Returns D."""
+    layout).  mx=True: fp8bs_gemm_mx (all scales exact powers of two; UE8M0 block scaling in the
+    tensor core, no promotion).  Returns D."""
     for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
         _cuda2d(t, n)
     M, K = A.shape
@@ -232,9 +237,9 @@ def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: to
     if out is None:
         out = torch.empty(M, N, dtype=out_dtype, device=A.device)
     _cuda2d(out, "out")
-    _check(lib().fp8bs_gemm(layout, M, N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
-                            sB.stride(0), _p(out), _dt(out), out.stride(0), 1 if accumulate else 0, _stream(A)),
-           "fp8bs_gemm")
+    fn, name = (lib().fp8bs_gemm_mx, "fp8bs_gemm_mx") if mx else (lib().fp8bs_gemm, "fp8bs_gemm")
+    _check(fn(layout, M, N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
+              sB.stride(0), _p(out), _dt(out), out.stride(0), 1 if accumulate else 0, _stream(A)), name)
     return out
 
 

@@ -198,10 +198,29 @@ static fp8bs_status check_gemm_common(int64_t M, int64_t N, int64_t K, const uin
     return FP8BS_OK;
 }
 
+static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                              const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                              const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream);
+
 fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                         const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
                         void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    return gemm_impl(0, layout, M, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ddt, ldd, accumulate, stream);
+}
+
+fp8bs_status fp8bs_gemm_mx(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                           const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                           const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                           void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    return gemm_impl(1, layout, M, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ddt, ldd, accumulate, stream);
+}
+
+static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                              const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                              const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
     if (layout != FP8BS_FPROP && layout != FP8BS_DGRAD && layout != FP8BS_WGRAD)
         return fail(FP8BS_ERR_INVALID_ARG, "layout=%d", (int)layout);
     fp8bs_status c = check_gemm_common(M, N, K, A, lda, sA, ldsA, B, ldb, sB, D, ddt, ldd);
@@ -225,9 +244,9 @@ fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = accumulate ? 1 : 0;
     a.grouped = 0; a.G = 0; a.offsets = nullptr;
     const char* detail = nullptr;
-    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
-    return from_cuda(e, "gemm launch");
+    return from_cuda(e, mx ? "gemm_mx launch" : "gemm launch");
 }
 
 size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K) {

@@ -63,5 +63,7 @@ struct GemmArgs {
 // Returns cudaSuccess or the launch error; *detail gets a static message on host-side failures
 // (tensor-map encoding).
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail);
+// power-of-two scales on the tensor core's UE8M0 block scaling (gemm_mx.cu)
+cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** detail);
 
 }  // namespace fp8bs

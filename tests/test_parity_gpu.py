@@ -435,3 +435,49 @@ def test_gemm_C1_full_size_deterministic(layout):
     for _ in range(4):
         D = fp.gemm(layout, A, sA, B, sB, out_dtype=torch.float32)
         assert torch.equal(D.view(torch.int32), ref.view(torch.int32)), "nondeterministic GEMM output"
+
+
+# ------------------------------------------- power-of-two scales on the MMA's block scaling ----
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_mx_closed_form_bitexact(layout, M, N, K):
+    """fp8bs_gemm_mx (UE8M0 block-scaled tcgen05.mma, no promotion) on the closed-form operands:
+    small-integer codes and power-of-two scales make every partial sum exact, so the FP32 output
+    equals the oracle bit for bit; ragged M and N (partial 128 x 224 tiles)."""
+    A = W.codes_small(M, K, seed=M)
+    B = W.codes_small(N, K, seed=N + 1)
+    sA = W.scales_pow2(K // 128, M, seed=3)
+    sB = W.scales_pow2(*scale_b_shape(layout, N, K), seed=4)
+    O = oracle.gemm(layout, A, sA, B, sB)
+    D = fp.gemm(layout, dev(A), dev_scales(sA), dev(B), dev(sB), out_dtype=torch.float32, mx=True)
+    torch.cuda.synchronize()
+    assert_bits_equal(D, O.to(torch.float32), "closed-form MX GEMM")
+
+
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD], ids=["fprop", "dgrad"])
+def test_gemm_mx_pow2_quantized_vs_oracle_and_bf16(layout):
+    """Activations quantized with power-of-two 1x128 scales and pow2 weight scales:
+    within 1e-3 of the FP64 oracle; the BF16 output is the RNE of the same kernel's FP32 output."""
+    M, N, K = 640, 1000, 1536
+    qa, sa = oracle.quantize_act_1x128_pow2(W.outlier_act(M, K, seed=21))
+    qb = W.codes_small(N, K, seed=22)
+    sb = W.scales_pow2(*scale_b_shape(layout, N, K), seed=23) * 2.0 ** -9
+    O = oracle.gemm(layout, qa, sa, qb, sb)
+    D = fp.gemm(layout, dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32, mx=True)
+    Db = fp.gemm(layout, dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.bfloat16, mx=True)
+    torch.cuda.synchronize()
+    assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+    assert torch.equal(Db.cpu().view(torch.int16), D.cpu().to(torch.bfloat16).view(torch.int16))
+
+
+def test_gemm_mx_wgrad_accumulate():
+    M, N, K = 384, 448, 512
+    A = W.codes_small(M, K, seed=31)
+    B = W.codes_small(N, K, seed=32)
+    sA = W.scales_pow2(K // 128, M, seed=33)
+    sB = W.scales_pow2(K // 128, N, seed=34)
+    O = oracle.gemm(fp.WGRAD, A, sA, B, sB)
+    D = torch.full((M, N), 3.0, device=DEV)
+    fp.gemm(fp.WGRAD, dev(A), dev_scales(sA), dev(B), dev_scales(sB), out=D, accumulate=True, mx=True)
+    torch.cuda.synchronize()
+    assert_bits_equal(D, (O + 3.0).to(torch.float32), "MX Wgrad accumulate")
