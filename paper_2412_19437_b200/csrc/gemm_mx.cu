@@ -10,16 +10,20 @@
 // tensor core (one scale byte per row / column per 32-element K-step, our per-128 scale repeated 4x)
 // and the FP32 accumulator stays in TMEM for the whole K loop: there is no promotion step.
 //
-// One CTA per 128 x 224 output tile (persistent):
-//   w0  TMA producer: A (128 x 128 B) and B (224 x 128 B) K-blocks into a 4-stage ring;
+// One CTA per 128 x 224 output tile (persistent); CTAs run in clusters of two on m tiles 2u, 2u + 1 of
+// the same n tile, each loading half of the shared B tile and multicasting it into both (L2 -> SM
+// operand traffic 44 -> 30 KB per K-block per SM):
+//   w0  TMA producer: A (128 x 128 B) and its B half (112 x 128 B, multicast) into a 4-stage ring; a
+//       stage is refilled only when both CTAs' MMAs have read it;
 //   w1, w3, w8, w9  scale-factor producers, one per ring stage (a warp's K-blocks are a ring cycle
-//       apart, so its parity waits never alias and its global scale loads, issued before the wait,
-//       have a whole cycle to land): per K-block the UE8M0 atoms in the stage (SFA: 32 lanes x 16 B,
-//       byte [r1][t] = row l + 32 r1; SFB the same for columns, two atoms) from the FP32 scales;
+//       apart, so its parity waits never alias): per K-block the UE8M0 atoms in the stage (SFA: 32
+//       lanes x 16 B, byte [r1][t] = row l + 32 r1; SFB the same for columns, two atoms) from FP32
+//       scales loaded a ring cycle ahead and converted only after the wait;
 //   w2  MMA issuer: tcgen05.cp.32x128b.warpx4 of the three atoms into TMEM, then 4 block-scaled MMAs
 //       (K = 32, sf_id = K-step) into one of two 224-column accumulators; commits release the stage
-//       and, after the last K-block, hand the accumulator to the epilogue (tools/mx_probe.cu pins the
-//       scale-factor TMEM layout: row l + 32 r1 -> lane l of every quadrant, column + r1, byte t);
+//       in both CTAs and, after the last K-block, hand the accumulator to the epilogue
+//       (tools/mx_probe.cu pins the scale-factor TMEM layout: row l + 32 r1 -> lane l of every
+//       quadrant, column + r1, byte t);
 //   w4..w7 epilogue: each drains its lane quadrant (32 rows x 224 columns) in 32-column chunks through
 //       a staging buffer and TMA stores (reduce-add for Wgrad accumulate), then frees the accumulator.
 // TMEM: 2 x 224 accumulator columns + 12 scale-factor columns (512 allocated).
@@ -28,6 +32,19 @@
 
 #include "sm100.cuh"
 #include "internal.h"
+
+#ifndef FP8BS_MX_PF
+#define FP8BS_MX_PF 1    // owned K-blocks whose scales are in flight ahead of the one being written (2, 3: same speed)
+#endif
+#ifndef FP8BS_MX_NFAST
+#define FP8BS_MX_NFAST 2 // tile order: 0 m fastest, 1 n fastest, 2 n fastest when M > N (the smaller operand re-streams from L2)
+#endif
+#ifndef FP8BS_MX_MC
+#define FP8BS_MX_MC 1    // CTA pairs along M sharing each B tile by TMA multicast (0: independent CTAs)
+#endif
+#ifndef FP8BS_MX_DBG
+#define FP8BS_MX_DBG 0   // experiments (tools/): 1 = skip the output stores, 2 = constant scale atoms (no loads)
+#endif
 
 namespace fp8bs {
 namespace mx {
@@ -45,20 +62,31 @@ constexpr int NBAR = 2 * STAGES + 4;             // full, empty, accfull[2], acc
 constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
 constexpr int NSF = STAGES;                      // scale-factor warps 1, 3, 8, 9: warp k owns stage k
 constexpr int THREADS = 32 * 10;
+constexpr int MX_PF = FP8BS_MX_PF;
 constexpr uint32_t ACC_COLS = 256;               // accumulator b at columns [256 b, 256 b + 224)
 constexpr uint32_t SF_COL = 480;                 // SFA [480, 484), SFB [484, 492)
 
 struct Params {
-    int M, N, K, KB, num_m, num_n, layout, n_fast;
+    int M, N, K, KB, num_m, num_n, layout, rast_n, gm;
     const float* sA; int64_t ldsA;
     const float* sB; int64_t ldsB;
     int accumulate;
 };
 
-// Tile order: the operand with fewer rows stays L2-resident while the other streams once (m fastest
-// when M <= N; n fastest otherwise, e.g. Wgrad's 18432 x 7168).
-__device__ __forceinline__ int tile_m(const Params& p, int t) { return p.n_fast ? t / p.num_n : t % p.num_m; }
-__device__ __forceinline__ int tile_n(const Params& p, int t) { return p.n_fast ? t % p.num_n : t / p.num_m; }
+// Tile order (as the promotion kernel's banded raster, gemm.cu get_tile_dense): the operand with fewer
+// rows stays L2-resident, in bands of gm tiles when it is larger than ~48 MB; inside a band consecutive
+// tiles walk the resident operand fastest so concurrent CTAs share each streamed tile through L2.
+// (m fastest for Wgrad's 18432 x 7168 read 1.23 GB of DRAM for 104 MB of operands: 2124 TFLOP/s;
+// n fastest 2421.)
+__device__ __forceinline__ void tile_mn(const Params& p, int t, int& m, int& n) {
+    const int nres = p.rast_n ? p.num_n : p.num_m, nstr = p.rast_n ? p.num_m : p.num_n;
+    const int band = t / (p.gm * nstr);
+    const int gb = min(p.gm, nres - band * p.gm);
+    const int local = t - band * p.gm * nstr;
+    const int ires = band * p.gm + local % gb, istr = local / gb;
+    m = p.rast_n ? istr : ires;
+    n = p.rast_n ? ires : istr;
+}
 
 __device__ __forceinline__ uint32_t ue8m0(float s) { return (__float_as_uint(s) >> 23) & 0xFFu; }
 
@@ -85,7 +113,13 @@ __device__ __forceinline__ void mma_mx(uint32_t d, uint64_t a, uint64_t b, uint3
                  :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
 }
 
-template <bool kOutF32>
+// Arrive once on the barrier at this offset in both CTAs of the pair when the MMAs complete.
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(bar), "h"((uint16_t)3) : "memory");
+}
+
+template <bool kOutF32, bool kMc>
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmD, const Params p) {
@@ -101,14 +135,21 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     auto accempty_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    // kMc: the two CTAs of a cluster take m tiles 2u and 2u + 1 of the same n tile; each loads its
+    // half of the B tile and multicasts it into both, so a stage is free only when BOTH CTAs' MMAs
+    // have read it (each commit arrives on the empty barrier of both CTAs: count 2)
+    constexpr int MC = kMc ? 2 : 1;
+    const uint32_t rank = kMc ? cluster_ctarank() : 0;
+    const int cid = kMc ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, ncl = kMc ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(full_bar(s), 2); mbar_init(empty_bar(s), 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(full_bar(s), 2); mbar_init(empty_bar(s), MC); }
         for (int b = 0; b < 2; ++b) { mbar_init(accfull_bar(b), 1); mbar_init(accempty_bar(b), 4); }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
+    if constexpr (kMc) cluster_sync();              // the peer's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int ntiles = p.num_m * p.num_n;
@@ -117,8 +158,10 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // ---------------- TMA producer ----------------
         if (lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmD); }
         int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int m0 = tile_m(p, t) * BM, n0 = tile_n(p, t) * BN;
+        for (int t = cid; t < ntiles; t += ncl) {
+            int tm, tn;
+            tile_mn(p, t, tm, tn);
+            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
             for (int kb = 0; kb < p.KB; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
@@ -126,39 +169,59 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t st = sbase + s * STAGE;
                     mbar_arrive_expect_tx(full_bar(s), A_BYTES + B_BYTES);
                     tma_load_2d(st, &tmA, full_bar(s), kb * BK, m0);
-                    tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0);
+                    if constexpr (kMc)
+                        tma_load_2d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kb * BK, n0 + (int)rank * (BN / 2), 3);
+                    else
+                        tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0);
                 }
                 __syncwarp();
             }
+        }
+        if constexpr (kMc) {
+            // the peer's last commits arrive on this CTA's empty barriers: wait for them before exit
+            for (int i = 0; i < STAGES; ++i, ++it) mbar_wait(empty_bar(it % STAGES), ((it / STAGES) & 1) ^ 1);
         }
     } else if (warp == 1 || warp == 3 || warp >= 8) {
         // ---------------- scale-factor atoms ----------------
         const int slot = warp == 1 ? 0 : warp == 3 ? 1 : warp - 6;
         // this warp's K-blocks: global iteration it = slot, slot + NSF, ... (tile it / KB of this CTA's
-        // sequence, K-block it % KB); the scale values of the next one are loaded while the current
-        // one waits for its stage, so each load has two ring cycles to land
-        auto load = [&](int it, uint32_t* wa, uint32_t* wb) -> bool {
-            const int t = blockIdx.x + (it / p.KB) * gridDim.x, kb = it % p.KB;
+        // sequence, K-block it % KB).  The raw FP32 scales of the next MX_PF owned K-blocks are in flight
+        // while the current one waits for its stage: they are converted only after the wait, so no
+        // load is consumed at issue (converting at load time stalled each warp on its loads: Wgrad's
+        // 1187 TFLOP/s became 2254 with constant atoms)
+        auto load = [&](int it, float* fa, float* fb) -> bool {
+            const int t = cid + (it / p.KB) * ncl, kb = it % p.KB;
             if (t >= ntiles) return false;
-            const int m0 = tile_m(p, t) * BM, n0 = tile_n(p, t) * BN;
+            int tm, tn;
+            tile_mn(p, t, tm, tn);
+            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
 #pragma unroll
             for (int r1 = 0; r1 < 4; ++r1) {
                 const int i = m0 + lane + 32 * r1;
-                wa[r1] = i < p.M ? ue8m0(__ldg(p.sA + (int64_t)kb * p.ldsA + i)) * 0x01010101u : 127u * 0x01010101u;
+                fa[r1] = ((FP8BS_MX_DBG & 2) || i >= p.M) ? 1.0f : __ldg(p.sA + (int64_t)kb * p.ldsA + i);
             }
 #pragma unroll
-            for (int r1 = 0; r1 < 8; ++r1) {
+            for (int r1 = 0; r1 < 7; ++r1) {
                 const int j = n0 + lane + 32 * r1;
-                wb[r1] = (r1 < BN / 32 && j < p.N) ? ue8m0(scale_b(p, kb, j)) * 0x01010101u : 127u * 0x01010101u;
+                fb[r1] = ((FP8BS_MX_DBG & 2) || j >= p.N) ? 1.0f : scale_b(p, kb, j);
             }
             return true;
         };
-        uint32_t wa[4], wb[8], na[4], nb[8];
-        bool have = load(slot, wa, wb);
-        for (int it = slot; have; it += NSF) {
-            const bool more = load(it + NSF, na, nb);          // in flight during the wait below
+        constexpr int PF = MX_PF;
+        float fa[PF + 1][4], fb[PF + 1][7];
+        bool have[PF + 1];
+#pragma unroll
+        for (int d = 0; d < PF; ++d) have[d] = load(slot + d * NSF, fa[d], fb[d]);
+        for (int it = slot; have[0]; it += NSF) {
+            have[PF] = load(it + PF * NSF, fa[PF], fb[PF]);    // in flight during the wait below
             const int s = it % STAGES;
             uint8_t* sf = smem + s * STAGE + A_BYTES + B_BYTES;
+            uint32_t wa[4], wb[8];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) wa[r] = ue8m0(fa[0][r]) * 0x01010101u;
+#pragma unroll
+            for (int r = 0; r < 7; ++r) wb[r] = ue8m0(fb[0][r]) * 0x01010101u;
+            wb[7] = 127u * 0x01010101u;                        // columns 224..255 of the atom: unused
             mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
             *reinterpret_cast<uint4*>(sf + lane * 16) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
             *reinterpret_cast<uint4*>(sf + 512 + lane * 16) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
@@ -167,16 +230,19 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             __syncwarp();
             if (lane == 0) mbar_arrive(full_bar(s));
 #pragma unroll
-            for (int r = 0; r < 4; ++r) wa[r] = na[r];
+            for (int d = 0; d < PF; ++d) {
+                have[d] = have[d + 1];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) wb[r] = nb[r];
-            have = more;
+                for (int r = 0; r < 4; ++r) fa[d][r] = fa[d + 1][r];
+#pragma unroll
+                for (int r = 0; r < 7; ++r) fb[d][r] = fb[d + 1][r];
+            }
         }
     } else if (warp == 2) {
         // ---------------- MMA issuer ----------------
         constexpr uint32_t idesc0 = idesc_mx(BM, BN, 0);
         int it = 0, tl = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        for (int t = cid; t < ntiles; t += ncl, ++tl) {
             const int b = tl & 1;
             mbar_wait(accempty_bar(b), ((tl >> 1) & 1) ^ 1);
             tc_fence_after();
@@ -198,7 +264,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         mma_mx(d, ad + 2 * k, bd + 2 * k, id, tmem_base + SF_COL + ((uint32_t)k << 30),
                                tmem_base + SF_COL + 4 + ((uint32_t)k << 30), (kb > 0 || k > 0) ? 1u : 0u);
                     }
-                    mma_commit(empty_bar(s));
+                    if constexpr (kMc) mma_commit_mc(empty_bar(s));
+                    else mma_commit(empty_bar(s));
                     if (kb == p.KB - 1) mma_commit(accfull_bar(b));
                 }
                 __syncwarp();
@@ -210,9 +277,11 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint32_t ebuf0 = sbase + OFF_EPI + (warp - 4) * EPI_WARP;
         int chunk = 0;                                  // running chunk count: alternates the two buffers
         int tl = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        for (int t = cid; t < ntiles; t += ncl, ++tl) {
             const int b = tl & 1;
-            const int m0 = tile_m(p, t) * BM, n0 = tile_n(p, t) * BN;
+            int tm, tn;
+            tile_mn(p, t, tm, tn);
+            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
             mbar_wait(accfull_bar(b), (tl >> 1) & 1);
             tc_fence_after();
             const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + ACC_COLS * b;
@@ -249,7 +318,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 __syncwarp();
                 if (lane == 0) {
                     const int col = n0 + 32 * c, row = m0 + quad * 32;
-                    if (col < p.N && row < p.M) {
+                    if (col < p.N && row < p.M && !(FP8BS_MX_DBG & 1)) {
                         if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, row);
                         else tma_store_2d(&tmD, ebuf, col, row);
                     }
@@ -282,7 +351,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     {
         const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
         const uint64_t str[1] = {(uint64_t)a.ldb};
-        const uint32_t box[2] = {BK, BN};
+        const uint32_t box[2] = {BK, FP8BS_MX_MC ? BN / 2 : BN};
         if (!make_tmap(&tB, TMAP_U8, 2, a.B, dims, str, box, 128)) { *detail = "tensor map B"; return cudaErrorInvalidValue; }
     }
     {
@@ -297,12 +366,19 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     }
     Params p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
-    p.num_m = (int)((a.M + BM - 1) / BM); p.num_n = (int)((a.N + BN - 1) / BN);
-    p.n_fast = 0;   // m fastest for every shape: n-fastest measured slower for Wgrad (1156 vs 1216 TFLOP/s)
+    constexpr int MC = FP8BS_MX_MC ? 2 : 1;
+    p.num_m = (int)((a.M + BM * MC - 1) / (BM * MC)); p.num_n = (int)((a.N + BN - 1) / BN);   // m units of MC tiles
+    p.rast_n = FP8BS_MX_NFAST == 2 ? (a.M > a.N ? 1 : 0) : FP8BS_MX_NFAST;
+    {
+        const int64_t res_rows = p.rast_n ? BN : BM * MC, nres = p.rast_n ? p.num_n : p.num_m;
+        const int64_t gb = (48ll << 20) / (res_rows * a.K);
+        p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
+    }
     p.layout = a.layout; p.sA = a.sA; p.ldsA = a.ldsA; p.sB = a.sB; p.ldsB = a.ldsB; p.accumulate = a.accumulate;
-    const int64_t tiles = (int64_t)p.num_m * p.num_n;
-    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    auto kern = a.out_f32 ? k_gemm_mx<true> : k_gemm_mx<false>;
+    const int64_t units = (int64_t)p.num_m * p.num_n;
+    const int64_t max_units = num_sms() / MC;
+    const int grid = (int)(units < max_units ? units : max_units) * MC;
+    auto kern = a.out_f32 ? k_gemm_mx<true, FP8BS_MX_MC != 0> : k_gemm_mx<false, FP8BS_MX_MC != 0>;
     static bool attr[2][64] = {{false}};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -311,7 +387,21 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < 64) attr[a.out_f32 ? 1 : 0][dev] = true;
     }
-    return launch_pdl(kern, dim3(grid), dim3(THREADS), SMEM, st, tA, tB, tD, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (internal.h launch_pdl)
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = MC; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tD, p);
+    if (e != cudaSuccess) return e;
+    return cudaPeekAtLastError();
 }
 
 }  // namespace fp8bs

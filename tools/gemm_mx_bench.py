@@ -22,7 +22,30 @@ def timeit(fn, iters=10):
     return a.elapsed_time(b) / iters
 
 
+def diag():
+    """MX kernel only, Wgrad's slowness pulled apart: layout x shape x output type."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(0)
+    p2 = lambda *s: 2.0 ** torch.randint(-10, -2, s, device=dev, generator=g).float()  # noqa: E731
+    for name, L, (M, N, K), dt in (("fprop C1 bf16", fp.FPROP, (4096, 18432, 7168), torch.bfloat16),
+                                   ("fprop C1 f32", fp.FPROP, (4096, 18432, 7168), torch.float32),
+                                   ("fprop wgshape bf16", fp.FPROP, (18432, 7168, 4096), torch.bfloat16),
+                                   ("fprop wgshape f32", fp.FPROP, (18432, 7168, 4096), torch.float32),
+                                   ("fprop 4096x7168x18432 f32", fp.FPROP, (4096, 7168, 18432), torch.float32),
+                                   ("wgrad f32", fp.WGRAD, (18432, 7168, 4096), torch.float32),
+                                   ("wgrad K=8192 f32", fp.WGRAD, (18432, 7168, 8192), torch.float32)):
+        A = torch.randint(0, 120, (M, K), dtype=torch.uint8, device=dev, generator=g)
+        B = torch.randint(0, 120, (N, K), dtype=torch.uint8, device=dev, generator=g)
+        sA = p2(K // 128, M)
+        sB = p2(N // 128, K // 128) if L == fp.FPROP else p2(K // 128, N)
+        out = torch.empty(M, N, dtype=dt, device=dev)
+        ms = timeit(lambda: fp.gemm(L, A, sA, B, sB, out=out, mx=True))
+        print(f"{name:28s} {ms * 1e3:7.1f} us {2.0 * M * N * K / ms / 1e9:6.0f} TFLOP/s", flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "diag":
+        return diag()
     dev = "cuda"
     T, IN, OUT = 4096, 7168, 18432
     g = torch.Generator(device=dev).manual_seed(0)
