@@ -108,11 +108,13 @@ class ClockSampler:
 
 # ------------------------------------------------------------------- dense step ----
 class DenseStep:
-    """Preallocated buffers + the 6 launches of one FP8 Linear training step."""
+    """Preallocated buffers + the 6 launches of one FP8 Linear training step.  pow2: the power-of-two
+    scale recipe end to end: pow2 quantizers and the UE8M0 block-scaled GEMM."""
 
-    def __init__(self, dev, T=T_TOK, IN=D_IN, OUT=D_OUT, seed=0):
+    def __init__(self, dev, T=T_TOK, IN=D_IN, OUT=D_OUT, seed=0, pow2=False):
         import paper_2412_19437_b200 as fp
         self.fp = fp
+        self.pow2 = pow2
         self.T, self.IN, self.OUT = T, IN, OUT
         self.h_x = W.gaussian_act(T, IN, seed=seed)                 # BF16 activations
         self.h_w = W.master_weight(OUT, IN, seed=seed + 1)          # FP32 master weight (P:487)
@@ -146,22 +148,22 @@ class DenseStep:
         self.d2h_bytes = self.y.numel() * 2 + self.dx.numel() * 2 + self.dw.numel() * 4
 
     def q_x(self):
-        self.fp.quantize_act_dual(self.x, self.xq, self.sx, self.xqT, self.sxT)
+        self.fp.quantize_act_dual(self.x, self.xq, self.sx, self.xqT, self.sxT, pow2=self.pow2)
 
     def q_w(self):
-        self.fp.quantize_weight_128x128(self.w, True, self.wq, self.sw, self.wqT)
+        self.fp.quantize_weight_128x128(self.w, True, self.wq, self.sw, self.wqT, pow2=self.pow2)
 
     def g_fprop(self):
-        self.fp.gemm(self.fp.FPROP, self.xq, self.sx, self.wq, self.sw, out=self.y)
+        self.fp.gemm(self.fp.FPROP, self.xq, self.sx, self.wq, self.sw, out=self.y, mx=self.pow2)
 
     def q_dy(self):
-        self.fp.quantize_act_dual(self.dy, self.dyq, self.sdy, self.dyqT, self.sdyT)
+        self.fp.quantize_act_dual(self.dy, self.dyq, self.sdy, self.dyqT, self.sdyT, pow2=self.pow2)
 
     def g_dgrad(self):
-        self.fp.gemm(self.fp.DGRAD, self.dyq, self.sdy, self.wqT, self.sw, out=self.dx)
+        self.fp.gemm(self.fp.DGRAD, self.dyq, self.sdy, self.wqT, self.sw, out=self.dx, mx=self.pow2)
 
     def g_wgrad(self):
-        self.fp.gemm(self.fp.WGRAD, self.dyqT, self.sdyT, self.xqT, self.sxT, out=self.dw)
+        self.fp.gemm(self.fp.WGRAD, self.dyqT, self.sdyT, self.xqT, self.sxT, out=self.dw, mx=self.pow2)
 
     def run(self):
         for _, fn, _, _ in self.launches:
@@ -341,7 +343,43 @@ def time_dense(args, world, rank, dev):
     }
     if args.e2e:
         result["e2e"] = time_e2e(args, world, st, dev)
+    if args.pow2:
+        del st
+        result["pow2_recipe"] = time_pow2_recipe(args, dev)
     return result
+
+
+def time_pow2_recipe(args, dev):
+    """Context line, not the headline: the same C1 step on the power-of-two scale recipe (P:558, P:565;
+    pow2 dual / weight quantizers, UE8M0 block-scaled GEMM fp8bs_gemm_mx), timed like the main step
+    on this rank's stream after it (per-launch CUDA events, inputs larger than L2)."""
+    st = DenseStep(dev, pow2=True)
+    stream = torch.cuda.current_stream()
+    steps = min(args.steps, 50)
+    for _ in range(args.warmup):
+        st.run()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in st.launches]
+          for _ in range(steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(steps):
+        for i, (_, fn, _, _) in enumerate(st.launches):
+            ev[k][i][0].record(stream)
+            fn()
+            ev[k][i][1].record(stream)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    per = {}
+    for i, (name, _, kind, amount) in enumerate(st.launches):
+        d = statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(steps))
+        per[name] = {"ms": d, "achieved": amount / (d * 1e-3) / (1e12 if kind == "tensor" else 1e9),
+                     "unit": "TFLOP/s" if kind == "tensor" else "GB/s"}
+    return {"value": st.flops * steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
+            "steps": steps, "recipe": "power-of-two scales (P:558, P:565): fp8bs_quantize_act_dual_pow2, "
+            "fp8bs_quantize_weight_128x128_pow2, fp8bs_gemm_mx (UE8M0 block scaling, no promotion step)",
+            "kernels": per}
 
 
 def time_e2e(args, world, st, dev):
@@ -419,6 +457,7 @@ def main():
     ap.add_argument("--workload", default="dense", choices=["dense", "ep"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-pow2", dest="pow2", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -116,6 +116,16 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, i
                                      uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
                                      fp8bs_stream_t stream);
 
+/* ---- quantize_act_dual_pow2: the dual quantizer with power-of-two scales --------------------
+ * As fp8bs_quantize_act_dual, every scale (both groupings) the smallest 2^e with 448 * 2^e >= amax
+ * (reading R23, see fp8bs_quantize_act_1x128_pow2).  The outputs feed fp8bs_gemm_mx
+ * (UE8M0 block scaling) or fp8bs_gemm.  Same layouts, ownership and errors; fused for BF16 x with
+ * 16-byte aligned rows and K % 16 == 0, a generic two-pass kernel otherwise. */
+FP8BS_API fp8bs_status fp8bs_quantize_act_dual_pow2(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                          uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                          uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
+                                          fp8bs_stream_t stream);
+
 /* ---- requantize_1x128_to_128x1: FP8 -> FP8 re-quantization of a cached activation ---------
  * P:558 (§3.3.3) and P:672-673 (§3.5.2): the FP8 activations kept from the forward pass are "read
  * out, dequantized, transposed, re-quantized into 128x1 tiles" for the Wgrad GEMM.
@@ -143,6 +153,14 @@ FP8BS_API fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t
 FP8BS_API fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
                                            uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                            uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream);
+
+/* ---- quantize_weight_128x128_pow2: 128x128 blocks with power-of-two scales -------------------
+ * As fp8bs_quantize_weight_128x128, s[nb*ldsw + kb] = the smallest 2^e with 448 * 2^e >= block amax
+ * (the power-of-two option of P:558 / P:565 applied to the weights so that a whole layer runs on
+ * UE8M0 scales, fp8bs_gemm_mx).  Same layouts, ownership and errors. */
+FP8BS_API fp8bs_status fp8bs_quantize_weight_128x128_pow2(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                                uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                                uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream);
 
 /* ---- gemm: block-scaled FP8 GEMM, FP32 accumulation -----
  * D[i,j] (+)= sum_kb sA(kb,i) * sB(kb,j) * sum_{c in kb} dec(A[i,c]) * dec(B[j,c])

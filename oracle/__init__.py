@@ -58,6 +58,8 @@ def lib():
         L.oracle_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
         L.oracle_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, i32]
         L.oracle_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
+        L.oracle_quantize_act_128x1_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64]
+        L.oracle_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
         L.oracle_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32]
         L.oracle_grouped_gemm.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, i32]
         L.oracle_rel_err_normwise.restype = ctypes.c_double
@@ -123,26 +125,28 @@ def quantize_act_1x128_pow2(x: torch.Tensor):
     return q, s
 
 
-def quantize_act_128x1(x: torch.Tensor):
-    """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C])."""
+def quantize_act_128x1(x: torch.Tensor, pow2: bool = False):
+    """x [M,C] -> (qT uint8 [C,M], sT fp32 [ceil(M/128), C]).  pow2: power-of-two scales."""
     x = x.contiguous()
     M, C = x.shape
     qT = torch.empty(C, M, dtype=torch.uint8)
     sT = torch.empty((M + 127) // 128, C, dtype=torch.float32)
-    lib().oracle_quantize_act_128x1(_ptr(x), _dt(x), M, C, C, _ptr(qT), M, _ptr(sT), C)
+    fn = lib().oracle_quantize_act_128x1_pow2 if pow2 else lib().oracle_quantize_act_128x1
+    fn(_ptr(x), _dt(x), M, C, C, _ptr(qT), M, _ptr(sT), C)
     return qT, sT
 
 
-def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True):
-    """w [N,K] -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None)."""
+def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, pow2: bool = False):
+    """w [N,K] -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None).
+    pow2: power-of-two scales."""
     w = w.contiguous()
     N, K = w.shape
     KB = (K + 127) // 128
     q = torch.empty(N, K, dtype=torch.uint8)
     s = torch.empty((N + 127) // 128, KB, dtype=torch.float32)
     qT = torch.empty(K, N, dtype=torch.uint8) if want_t else None
-    lib().oracle_quantize_weight_128x128(_ptr(w), _dt(w), N, K, K, _ptr(q), K, _ptr(s), KB,
-                                         _ptr(qT), N)
+    fn = lib().oracle_quantize_weight_128x128_pow2 if pow2 else lib().oracle_quantize_weight_128x128
+    fn(_ptr(w), _dt(w), N, K, K, _ptr(q), K, _ptr(s), KB, _ptr(qT), N)
     return q, s, qT
 
 

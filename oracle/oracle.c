@@ -150,6 +150,11 @@ void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int
                                uint8_t* qT, int64_t ldq, float* sT, int64_t lds) {
     quantize_128x1(x, xdt, M, C, ldx, qT, ldq, sT, lds, group_scale);
 }
+/* 128x1 with power-of-two scales */
+void oracle_quantize_act_128x1_pow2(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                                    uint8_t* qT, int64_t ldq, float* sT, int64_t lds) {
+    quantize_128x1(x, xdt, M, C, ldx, qT, ldq, sT, lds, group_scale_pow2);
+}
 static void quantize_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
                            uint8_t* qT, int64_t ldq, float* sT, int64_t lds, float (*scale)(float)) {
     int64_t MB = (M + 127) / 128;
@@ -166,9 +171,23 @@ static void quantize_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t
 }
 
 /* 128x128 blocks: per 128 output channels nb, per 128 input channels kb. */
+static void quantize_weight(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                            uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                            uint8_t* qT, int64_t ldqT, float (*scale)(float));
 void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
                                     uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                     uint8_t* qT, int64_t ldqT) {
+    quantize_weight(w, wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, group_scale);
+}
+/* 128x128 with power-of-two scales (the P:558 / P:565 option applied to the weights) */
+void oracle_quantize_weight_128x128_pow2(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                                         uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                         uint8_t* qT, int64_t ldqT) {
+    quantize_weight(w, wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, group_scale_pow2);
+}
+static void quantize_weight(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                            uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                            uint8_t* qT, int64_t ldqT, float (*scale)(float)) {
     int64_t NB = (N + 127) / 128, KB = (K + 127) / 128;
     for (int64_t nb = 0; nb < NB; ++nb) {
         int64_t n0 = nb * 128, n1 = n0 + 128 < N ? n0 + 128 : N;
@@ -177,7 +196,7 @@ void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K
             float amax = 0.0f;
             for (int64_t n = n0; n < n1; ++n)
                 for (int64_t k = k0; k < k1; ++k) amax = fmaxf(amax, fabsf(load_elem(w, wdt, n * ldw + k)));
-            float sc = group_scale(amax);
+            float sc = scale(amax);
             s[nb * ldsw + kb] = sc;
             for (int64_t n = n0; n < n1; ++n)
                 for (int64_t k = k0; k < k1; ++k) {

@@ -44,6 +44,12 @@ void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int
 void oracle_quantize_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
                                     uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
                                     uint8_t* qT, int64_t ldqT);
+/* power-of-two scale variants of the two above (same scale rule as oracle_quantize_act_1x128_pow2) */
+void oracle_quantize_act_128x1_pow2(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,
+                                    uint8_t* qT, int64_t ldq, float* sT, int64_t lds);
+void oracle_quantize_weight_128x128_pow2(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw,
+                                         uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                         uint8_t* qT, int64_t ldqT);
 
 /* FP8 1x128 (q[m*ldq+k], s[(k/128)*lds+m]) -> dequantize to FP32 -> 128x1 (qT[k*ldqT+m],
  * sT[(m/128)*ldsT+k]).  P:558. */

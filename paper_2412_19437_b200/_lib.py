@@ -60,6 +60,13 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "fp8bs_quantize_act_1x128_pow2"):
             L.fp8bs_quantize_act_1x128_pow2.restype = st
             L.fp8bs_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+        for name in ("fp8bs_quantize_act_dual_pow2",):
+            if hasattr(L, name):
+                getattr(L, name).argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+                getattr(L, name).restype = st
+        if hasattr(L, "fp8bs_quantize_weight_128x128_pow2"):
+            L.fp8bs_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+            L.fp8bs_quantize_weight_128x128_pow2.restype = st
         if hasattr(L, "fp8bs_gemm_mx"):
             L.fp8bs_gemm_mx.restype = st
             L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
@@ -186,9 +193,10 @@ def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor
     return qT, sT
 
 
-def quantize_act_dual(x: torch.Tensor, q=None, s=None, qT=None, sT=None):
+def quantize_act_dual(x: torch.Tensor, q=None, s=None, qT=None, sT=None, pow2: bool = False):
     """x [M,K] -> (q [M,K], s [ceil(K/128), M], qT [K,M], sT [ceil(M/128), K]): both groupings from one
-    read of x (bit-identical to quantize_act_1x128 + quantize_act_128x1)."""
+    read of x (bit-identical to quantize_act_1x128 + quantize_act_128x1).  pow2: power-of-two scales
+    (fp8bs_quantize_act_dual_pow2)."""
     _cuda2d(x, "x")
     M, K = x.shape
     if q is None:
@@ -199,13 +207,15 @@ def quantize_act_dual(x: torch.Tensor, q=None, s=None, qT=None, sT=None):
         qT = torch.empty(K, M, dtype=torch.uint8, device=x.device)
     if sT is None:
         sT = torch.empty((M + 127) // 128, _pad4(K), dtype=torch.float32, device=x.device)[:, :K]
-    _check(lib().fp8bs_quantize_act_dual(_p(x), _dt(x), M, K, x.stride(0), _p(q), q.stride(0), _p(s), s.stride(0),
-                                         _p(qT), qT.stride(0), _p(sT), sT.stride(0), _stream(x)), "fp8bs_quantize_act_dual")
+    name = "fp8bs_quantize_act_dual_pow2" if pow2 else "fp8bs_quantize_act_dual"
+    _check(getattr(lib(), name)(_p(x), _dt(x), M, K, x.stride(0), _p(q), q.stride(0), _p(s), s.stride(0),
+                                _p(qT), qT.stride(0), _p(sT), sT.stride(0), _stream(x)), name)
     return q, s, qT, sT
 
 
-def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None, qT=None):
-    """w [N,K] FP32/BF16 -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None)."""
+def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None, qT=None, pow2: bool = False):
+    """w [N,K] FP32/BF16 -> (q uint8 [N,K], s fp32 [ceil(N/128), ceil(K/128)], qT uint8 [K,N] or None).
+    pow2: power-of-two scales (fp8bs_quantize_weight_128x128_pow2)."""
     _cuda2d(w, "w")
     N, K = w.shape
     if q is None:
@@ -214,10 +224,10 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None
         s = torch.empty((N + 127) // 128, (K + 127) // 128, dtype=torch.float32, device=w.device)
     if want_t and qT is None:
         qT = torch.empty(K, N, dtype=torch.uint8, device=w.device)
-    _check(lib().fp8bs_quantize_weight_128x128(_p(w), _dt(w), N, K, w.stride(0), _p(q), q.stride(0), _p(s),
-                                               s.stride(0), _p(qT) if want_t else None,
-                                               qT.stride(0) if want_t else 0, _stream(w)),
-           "fp8bs_quantize_weight_128x128")
+    name = "fp8bs_quantize_weight_128x128_pow2" if pow2 else "fp8bs_quantize_weight_128x128"
+    _check(getattr(lib(), name)(_p(w), _dt(w), N, K, w.stride(0), _p(q), q.stride(0), _p(s),
+                                s.stride(0), _p(qT) if want_t else None,
+                                qT.stride(0) if want_t else 0, _stream(w)), name)
     return q, s, (qT if want_t else None)
 
 

@@ -134,9 +134,10 @@ fp8bs_status fp8bs_quantize_act_128x1(const void* x, fp8bs_dtype xdt, int64_t M,
                      "quantize_act_128x1 launch");
 }
 
-fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
-                                    uint8_t* q, int64_t ldq, float* s, int64_t lds,
-                                    uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+static fp8bs_status quantize_act_dual_impl(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                           uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, int pow2,
+                                           fp8bs_stream_t stream) {
     if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
     if (M < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size M=%lld K=%lld", (long long)M, (long long)K);
     if (M == 0 || K == 0) return ok();
@@ -145,8 +146,20 @@ fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, 
         return fail(FP8BS_ERR_SHAPE, "need ldx>=K, ldq>=K, lds>=M, ldqT>=M, ldsT>=K");
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
-    return from_cuda(launch_quant_act_dual(x, (int)xdt, M, K, ldx, q, ldq, s, lds, qT, ldqT, sT, ldsT, (cudaStream_t)stream),
-                     "quantize_act_dual launch");
+    return from_cuda(launch_quant_act_dual(x, (int)xdt, M, K, ldx, q, ldq, s, lds, qT, ldqT, sT, ldsT, pow2, (cudaStream_t)stream),
+                     pow2 ? "quantize_act_dual_pow2 launch" : "quantize_act_dual launch");
+}
+
+fp8bs_status fp8bs_quantize_act_dual(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                    uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                    uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+    return quantize_act_dual_impl(x, xdt, M, K, ldx, q, ldq, s, lds, qT, ldqT, sT, ldsT, 0, stream);
+}
+
+fp8bs_status fp8bs_quantize_act_dual_pow2(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
+                                         uint8_t* q, int64_t ldq, float* s, int64_t lds,
+                                         uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, fp8bs_stream_t stream) {
+    return quantize_act_dual_impl(x, xdt, M, K, ldx, q, ldq, s, lds, qT, ldqT, sT, ldsT, 1, stream);
 }
 
 fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds,
@@ -164,9 +177,9 @@ fp8bs_status fp8bs_requantize_1x128_to_128x1(const uint8_t* q, int64_t ldq, cons
                      "requantize_1x128_to_128x1 launch");
 }
 
-fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
-                                           uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
-                                           uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {
+static fp8bs_status quantize_weight_impl(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                         uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                         uint8_t* qT, int64_t ldqT, int pow2, fp8bs_stream_t stream) {
     if (!valid_dtype(wdt)) return fail(FP8BS_ERR_INVALID_ARG, "wdt=%d", (int)wdt);
     if (N < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
     if (N == 0 || K == 0) return ok();
@@ -175,8 +188,20 @@ fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64
     if (qT && ldqT < N) return fail(FP8BS_ERR_SHAPE, "need ldqT>=N");
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
-    return from_cuda(launch_quant_weight_128x128(w, (int)wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, (cudaStream_t)stream),
-                     "quantize_weight_128x128 launch");
+    return from_cuda(launch_quant_weight_128x128(w, (int)wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, pow2, (cudaStream_t)stream),
+                     pow2 ? "quantize_weight_128x128_pow2 launch" : "quantize_weight_128x128 launch");
+}
+
+fp8bs_status fp8bs_quantize_weight_128x128(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                           uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                           uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {
+    return quantize_weight_impl(w, wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, 0, stream);
+}
+
+fp8bs_status fp8bs_quantize_weight_128x128_pow2(const void* w, fp8bs_dtype wdt, int64_t N, int64_t K, int64_t ldw,
+                                                uint8_t* q, int64_t ldq, float* s, int64_t ldsw,
+                                                uint8_t* qT, int64_t ldqT, fp8bs_stream_t stream) {
+    return quantize_weight_impl(w, wdt, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, 1, stream);
 }
 
 static fp8bs_status check_gemm_common(int64_t M, int64_t N, int64_t K, const uint8_t* A, int64_t lda, const float* sA,

@@ -18,10 +18,10 @@ cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C,
                                    int64_t ldq, float* sT, int64_t lds, cudaStream_t st);
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
                                   float* s, int64_t lds, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
-                                  cudaStream_t st);
+                                  int pow2, cudaStream_t st);
 cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw, uint8_t* q,
                                         int64_t ldq, float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT,
-                                        cudaStream_t st);
+                                        int pow2, cudaStream_t st);
 
 cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const float* s, int64_t lds, int64_t M, int64_t K,
                                           uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT, int pow2, cudaStream_t st);

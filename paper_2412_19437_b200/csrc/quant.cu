@@ -508,6 +508,7 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
 // 16-byte code stores (128-byte row segments) and one coalesced 512-byte scale vector per tile.
 // Outputs are bit-identical to the two separate kernels.
 // ===========================================================================================
+template <bool kPow2 = false>
 __global__ void __launch_bounds__(QTCfg<__nv_bfloat16>::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
 k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C,
                      uint8_t* __restrict__ q, int64_t ldq, float* __restrict__ s, int64_t lds,
@@ -566,7 +567,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             for (int e = 0; e < 16; ++e) amax = fmaxf(amax, fabsf(f[e]));
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            const float sc = group_scale(amax);
+            const float sc = group_scale_t<kPow2>(amax);
             const float r = __frcp_rn(sc);
             uint32_t w4[4];
             if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w4);   // warp-uniform
@@ -601,7 +602,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             const int ch = wc * P::CPW + j;
             const float* red = reinterpret_cast<const float*>(smem + P::OFF_RED);
             const float a = fmaxf(fmaxf(red[ch], red[P::CH + ch]), fmaxf(red[2 * P::CH + ch], red[3 * P::CH + ch]));
-            sc[j] = group_scale(a);
+            sc[j] = group_scale_t<kPow2>(a);
             fast = fast && fast_div_ok(sc[j]);
             if (rg == 0 && (full || c0 + ch < C)) sT[(int64_t)mb * ldsT + c0 + ch] = sc[j];
         }
@@ -678,7 +679,7 @@ struct QWCfg {
     static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
 };
 
-template <typename T>
+template <typename T, bool kPow2 = false>
 __global__ void __launch_bounds__(QWCfg<T>::THREADS)
 k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K, uint8_t* __restrict__ q, int64_t ldq,
                    float* __restrict__ s, int64_t ldsw, uint8_t* __restrict__ qT, int64_t ldqT) {
@@ -744,7 +745,7 @@ k_quant_weight_tma(const __grid_constant__ CUtensorMap tmW, int64_t N, int64_t K
         amax = rb[0];
 #pragma unroll
         for (int i = 1; i < P::CONSUMERS; ++i) amax = fmaxf(amax, rb[i]);
-        const float sc = group_scale(amax);
+        const float sc = group_scale_t<kPow2>(amax);
         const float rc = __frcp_rn(sc);
         const bool fast = fast_div_ok(sc);                  // block-uniform
         // Interior block (every block of the C1/C2 weights): branch-free stores from one base pointer
@@ -1116,7 +1117,7 @@ cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C,
 
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
                                   float* s, int64_t lds, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
-                                  cudaStream_t st) {
+                                  int pow2, cudaStream_t st) {
     using Q = QTCfg<__nv_bfloat16>;
     // fused path: BF16 (a 128-channel tile row is one 1x128 group), 16-byte aligned rows and codes
     bool fused = xdt == 0 && aligned16(x) && ((ldx * 2) % 16 == 0) && (K % 16 == 0) && aligned16(q) && (ldq % 16 == 0) &&
@@ -1128,25 +1129,39 @@ cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, 
         const uint32_t box[2] = {(uint32_t)Q::CH, 128};
         fused = make_tmap(&tm, TMAP_BF16, 2, x, dims, str, box, 0);
     }
+    if (!fused && pow2) {   // two passes over x, generic kernel (power-of-two scales)
+        const int64_t g1 = M * ((K + 127) / 128), g2 = ((M + 127) / 128) * K;
+        if (xdt == 0) {
+            const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+            k_quant_generic<__nv_bfloat16, true><<<grid_for(g1, 16, 16), 128, 0, st>>>(xb, M, K, ldx, 1, 1, 128, q, ldq, 1, nullptr, 0, 0, s, 1, lds);
+            k_quant_generic<__nv_bfloat16, true><<<grid_for(g2, 16, 16), 128, 0, st>>>(xb, M, K, ldx, 1, 128, 1, qT, 1, ldqT, nullptr, 0, 0, sT, ldsT, 1);
+        } else {
+            const auto* xf = reinterpret_cast<const float*>(x);
+            k_quant_generic<float, true><<<grid_for(g1, 16, 16), 128, 0, st>>>(xf, M, K, ldx, 1, 1, 128, q, ldq, 1, nullptr, 0, 0, s, 1, lds);
+            k_quant_generic<float, true><<<grid_for(g2, 16, 16), 128, 0, st>>>(xf, M, K, ldx, 1, 128, 1, qT, 1, ldqT, nullptr, 0, 0, sT, ldsT, 1);
+        }
+        return cudaPeekAtLastError();
+    }
     if (!fused) {   // two passes over x
         cudaError_t e = launch_quant_act_1x128(x, xdt, M, K, ldx, q, ldq, s, lds, st);
         if (e != cudaSuccess) return e;
         return launch_quant_act_128x1(x, xdt, M, K, ldx, qT, ldqT, sT, ldsT, st);
     }
-    static bool attr[64] = {false};
+    auto kern = pow2 ? k_quant_act_dual_tma<true> : k_quant_act_dual_tma<false>;
+    static bool attr[2][64] = {{false}};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || !attr[dev]) {
-        cudaFuncSetAttribute(k_quant_act_dual_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
-        if (dev >= 0 && dev < 64) attr[dev] = true;
+    if (dev < 0 || dev >= 64 || !attr[pow2 ? 1 : 0][dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+        if (dev >= 0 && dev < 64) attr[pow2 ? 1 : 0][dev] = true;
     }
     const int64_t tiles = ((M + 127) / 128) * ((K + Q::CH - 1) / Q::CH);
-    return launch_pdl(k_quant_act_dual_tma, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, K, q, ldq, s, lds, qT, ldqT, sT, ldsT);
+    return launch_pdl(kern, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, K, q, ldq, s, lds, qT, ldqT, sT, ldsT);
 }
 
 template <typename T>
 static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, uint8_t* q, int64_t ldq,
-                              float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT, cudaStream_t st) {
+                              float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT, int pow2, cudaStream_t st) {
     using P = TW<T>;
     const bool fast = aligned16(w) && ((ldw * (int64_t)sizeof(T)) % 16 == 0) && (K % P::E == 0) &&
                       (reinterpret_cast<uintptr_t>(q) % P::E == 0) && (ldq % P::E == 0) &&
@@ -1162,14 +1177,18 @@ static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, 
     }
     if (tma) {
         using Q = QWCfg<T>;
-        static bool attr_tma[64] = {false};
+        auto kern = pow2 ? k_quant_weight_tma<T, true> : k_quant_weight_tma<T, false>;
+        static bool attr_tma[2][64] = {{false}};
         int dev = 0;
         cudaGetDevice(&dev);
-        if (dev < 0 || dev >= 64 || !attr_tma[dev]) {
-            cudaFuncSetAttribute(k_quant_weight_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
-            if (dev >= 0 && dev < 64) attr_tma[dev] = true;
+        if (dev < 0 || dev >= 64 || !attr_tma[pow2 ? 1 : 0][dev]) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+            if (dev >= 0 && dev < 64) attr_tma[pow2 ? 1 : 0][dev] = true;
         }
-        return launch_pdl(k_quant_weight_tma<T>, grid_for(blocks, 1, 1), Q::THREADS, Q::SMEM, st, tm, N, K, q, ldq, s, ldsw, qT, ldqT);
+        return launch_pdl(kern, grid_for(blocks, 1, 1), Q::THREADS, Q::SMEM, st, tm, N, K, q, ldq, s, ldsw, qT, ldqT);
+    } else if (pow2) {
+        k_quant_generic<T, true><<<grid_for(blocks, 16, 16), 128, 0, st>>>(
+            reinterpret_cast<const T*>(w), N, K, ldw, 1, 128, 128, q, ldq, 1, qT, 1, ldqT, s, ldsw, 1);
     } else if (fast) {
         k_quant_weight_128x128<T><<<grid_for(blocks, 4, 4), 256, 0, st>>>(
             reinterpret_cast<const T*>(w), N, K, ldw, q, ldq, s, ldsw, qT, ldqT);
@@ -1182,9 +1201,9 @@ static cudaError_t launch_w_t(const void* w, int64_t N, int64_t K, int64_t ldw, 
 
 cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64_t K, int64_t ldw, uint8_t* q,
                                         int64_t ldq, float* s, int64_t ldsw, uint8_t* qT, int64_t ldqT,
-                                        cudaStream_t st) {
-    if (wdt == 0) return launch_w_t<__nv_bfloat16>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, st);
-    return launch_w_t<float>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, st);
+                                        int pow2, cudaStream_t st) {
+    if (wdt == 0) return launch_w_t<__nv_bfloat16>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, pow2, st);
+    return launch_w_t<float>(w, N, K, ldw, q, ldq, s, ldsw, qT, ldqT, pow2, st);
 }
 
 }  // namespace fp8bs

@@ -24,13 +24,18 @@ __device__ __forceinline__ float group_scale(float amax) {
 // element saturates; e >= -149 (the smallest subnormal; amax < 448 * 2^-149 then still fits); 1
 // when amax is 0; non-finite amax gives amax (like group_scale's amax / 448).
 __device__ __forceinline__ float group_scale_pow2(float amax) {
+    // amax = m * 2^E, m in [1, 2): 448 * 2^e = 1.75 * 2^(e+8) >= amax first holds at e = E - 8 when
+    // m <= 1.75 (mantissa field <= 0x600000), else at e = E - 7.  Integer ops only (the FP64
+    // ilogb / ldexp search cost the dual quantizer a quarter of its bandwidth).
     if (amax == 0.0f) return 1.0f;
     if (!(amax <= 3.4028234663852886e38f)) return amax;
-    const double a = amax;
-    int e = ilogb(a) - 9;                       // 448 * 2^e < amax here
-    while (ldexp(448.0, e) < a) ++e;            // at most three steps
+    uint32_t b = __float_as_uint(amax);
+    int bias = 0;
+    if ((b >> 23) == 0) { b = __float_as_uint(amax * 0x1p64f); bias = 64; }   // subnormal: exact rescale
+    const int E = (int)(b >> 23) - 127 - bias;
+    int e = E - 8 + ((b & 0x7FFFFFu) > 0x600000u ? 1 : 0);
     if (e < -149) e = -149;
-    return ldexpf(1.0f, e);
+    return e >= -126 ? __uint_as_float((uint32_t)(e + 127) << 23) : __uint_as_float(1u << (e + 149));
 }
 template <bool kPow2>
 __device__ __forceinline__ float group_scale_t(float amax) {

@@ -514,6 +514,36 @@ def test_pow2_quantizer_vs_exact_rationals_and_bruteforce(kind):
             assert np.array_equal(q[m, kb * 128:(kb + 1) * 128].numpy(), brute_encode(quot))
 
 
+@pytest.mark.parametrize("kind", ["gauss", "outlier", "special"])
+def test_pow2_128x1_and_weight_vs_exact_rationals_and_bruteforce(kind):
+    """The 128x1 and 128x128 power-of-two quantizers == the same independent composition as above over
+    their groups: exact-rational pow2 scale per group (a 128-token column segment; a 128x128 block),
+    the exact quotient, brute-force nearest E4M3 code; the weight's transposed copy is q's transpose."""
+    M, C = 300, 260
+    x = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act}[kind](M, C, seed=14).float()
+    qT, sT = oracle.quantize_act_128x1(x, pow2=True)
+    qw, sw, qwT = oracle.quantize_weight_128x128(x, pow2=True)
+    xn = x.numpy()
+    for mb in range((M + 127) // 128):
+        for c in range(C):
+            v = xn[mb * 128:(mb + 1) * 128, c]
+            sc = _pow2_scale_exact(float(np.max(np.abs(v))))
+            assert float(sT[mb, c]) == np.float32(sc)
+            quot = (v.astype(np.float64) / sc).astype(np.float32)
+            assert np.all(np.abs(quot) <= 448.0)
+            assert np.array_equal(qT[c, mb * 128:(mb + 1) * 128].numpy(), brute_encode(quot))
+    for nb in range((M + 127) // 128):
+        for kb in range((C + 127) // 128):
+            v = xn[nb * 128:(nb + 1) * 128, kb * 128:(kb + 1) * 128]
+            sc = _pow2_scale_exact(float(np.max(np.abs(v))))
+            assert float(sw[nb, kb]) == np.float32(sc)
+            quot = (v.astype(np.float64) / sc).astype(np.float32)
+            assert np.all(np.abs(quot) <= 448.0)
+            assert np.array_equal(qw[nb * 128:(nb + 1) * 128, kb * 128:(kb + 1) * 128].numpy(),
+                                  brute_encode(quot.reshape(-1)).reshape(quot.shape))
+    assert torch.equal(qwT, qw.t().contiguous())
+
+
 def test_requantize_pow2_loses_nothing():
     """P:558's rationale for power-of-two scales: re-quantizing pow2-scaled FP8 into 128x1 tiles with
     pow2 scales only shifts exponents, so every dequantized value whose new quotient stays in E4M3's

@@ -481,3 +481,64 @@ def test_gemm_mx_wgrad_accumulate():
     fp.gemm(fp.WGRAD, dev(A), dev_scales(sA), dev(B), dev_scales(sB), out=D, accumulate=True, mx=True)
     torch.cuda.synchronize()
     assert_bits_equal(D, (O + 3.0).to(torch.float32), "MX Wgrad accumulate")
+
+
+# --------------------------------------------- power-of-two recipe, whole layer (NEXT-1) ----
+@pytest.mark.parametrize("name,M,K,kind,dtype", DUAL_CASES[:5], ids=[c[0] for c in DUAL_CASES[:5]])
+def test_quantize_act_dual_pow2_bitexact(name, M, K, kind, dtype):
+    """Both groupings with power-of-two scales: bit-exact vs the oracle's pow2 1x128
+    and 128x1 quantizers, fused kernel and two-pass fallback."""
+    x = make_act(kind, M, K, dtype, seed=5)
+    q_ref, s_ref = oracle.quantize_act_1x128_pow2(x)
+    qT_ref, sT_ref = oracle.quantize_act_128x1(x, pow2=True)
+    q, s, qT, sT = fp.quantize_act_dual(dev(x), pow2=True)
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "pow2 1x128 scales")
+    assert_bits_equal(q, q_ref, "pow2 1x128 codes")
+    assert_bits_equal(sT, sT_ref, "pow2 128x1 scales")
+    assert_bits_equal(qT, qT_ref, "pow2 128x1 codes")
+
+
+@pytest.mark.parametrize("name,N,K,dtype", W_CASES, ids=[c[0] for c in W_CASES])
+def test_quantize_weight_pow2_bitexact(name, N, K, dtype):
+    w = W.master_weight(N, K, seed=2, dtype=dtype)
+    q_ref, s_ref, qT_ref = oracle.quantize_weight_128x128(w, pow2=True)
+    q, s, qT = fp.quantize_weight_128x128(dev(w), pow2=True)
+    torch.cuda.synchronize()
+    assert_bits_equal(s, s_ref, "pow2 scales")
+    assert_bits_equal(q, q_ref, "pow2 codes")
+    assert_bits_equal(qT, qT_ref, "pow2 transposed codes")
+
+
+@pytest.mark.parametrize("T,IN,OUT", [(256, 384, 640), (384, 1152, 520)])
+def test_pow2_training_step_through_mx(T, IN, OUT):
+    """One FP8 Linear training step on the power-of-two recipe, every step on the GPU: dual pow2
+    quantization of X and dY, pow2 weight quantization, Fprop / Dgrad / Wgrad on the UE8M0 GEMM.
+    Quantized operands bit-exact vs the oracle; each GEMM within 1e-3 of the oracle's FP64 GEMM on the
+    oracle's codes."""
+    x = W.outlier_act(T, IN, seed=41)
+    dy = W.gaussian_act(T, OUT, seed=42)
+    w = W.master_weight(OUT, IN, seed=43)
+    xq, xs, xqT, xsT = fp.quantize_act_dual(dev(x), pow2=True)
+    dq, ds, dqT, dsT = fp.quantize_act_dual(dev(dy), pow2=True)
+    wq, ws, wqT = fp.quantize_weight_128x128(dev(w), pow2=True)
+    y = fp.gemm(fp.FPROP, xq, xs, wq, ws, out_dtype=torch.float32, mx=True)
+    dx = fp.gemm(fp.DGRAD, dq, ds, wqT, ws, out_dtype=torch.float32, mx=True) if OUT % 128 == 0 else None
+    dw = fp.gemm(fp.WGRAD, dqT, dsT, xqT, xsT, out_dtype=torch.float32, mx=True) if T % 128 == 0 else None
+    torch.cuda.synchronize()
+    rxq, rxs = oracle.quantize_act_1x128_pow2(x)
+    rwq, rws, rwqT = oracle.quantize_weight_128x128(w, pow2=True)
+    assert_bits_equal(xq, rxq, "X codes")
+    assert_bits_equal(wq, rwq, "W codes")
+    assert oracle.rel_err_normwise(y.cpu().double(), oracle.gemm(fp.FPROP, rxq, rxs, rwq, rws)) <= TOL
+    if dx is not None:
+        rdq, rds = oracle.quantize_act_1x128_pow2(dy)
+        assert_bits_equal(dq, rdq, "dY codes")
+        O = oracle.gemm(fp.DGRAD, rdq, rds, rwqT, rws)
+        assert oracle.rel_err_normwise(dx.cpu().double(), O) <= TOL
+    if dw is not None:
+        rdqT, rdsT = oracle.quantize_act_128x1(dy, pow2=True)
+        rxqT, rxsT = oracle.quantize_act_128x1(x, pow2=True)
+        assert_bits_equal(dqT, rdqT, "dY^T codes")
+        O = oracle.gemm(fp.WGRAD, rdqT, rdsT, rxqT, rxsT)
+        assert oracle.rel_err_normwise(dw.cpu().double(), O) <= TOL
