@@ -35,6 +35,10 @@
 #include "sm100.cuh"
 #include "internal.h"
 
+#ifndef FP8BS_BAND_MB
+#define FP8BS_BAND_MB 48   // L2 budget of the resident operand's band (raster)
+#endif
+
 namespace fp8bs {
 
 constexpr int BM = 128, BK = 128;     // rows per CTA, K-block (= N_C)
@@ -764,7 +768,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         p.rast_n = a.M > a.N ? 1 : 0;
         const int64_t res_rows = p.rast_n ? (int64_t)BN : (int64_t)C::ROWS;   // rows per resident tile
         const int nres = p.rast_n ? p.num_n : p.num_m;
-        int64_t gb = (48ll << 20) / (res_rows * a.K);
+        int64_t gb = ((int64_t)FP8BS_BAND_MB << 20) / (res_rows * a.K);
         p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
     }
     {

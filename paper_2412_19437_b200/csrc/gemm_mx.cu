@@ -46,16 +46,27 @@
 #define FP8BS_MX_DBG 0   // experiments (tools/): 1 = skip the output stores, 2 = constant scale atoms (no loads)
 #endif
 
+#ifndef FP8BS_BAND_MB
+#define FP8BS_BAND_MB 48   // L2 budget of the resident operand's band (raster)
+#endif
+
 namespace fp8bs {
 namespace mx {
 
 constexpr int BM = 128, BN = 224, BK = 128;
-constexpr int STAGES = 4;
+#ifndef FP8BS_MX_STAGES
+#define FP8BS_MX_STAGES 4
+#endif
+#ifndef FP8BS_MX_EPIBUF
+#define FP8BS_MX_EPIBUF 2
+#endif
+constexpr int STAGES = FP8BS_MX_STAGES;           // 3 or 4
+constexpr int EPIBUF = FP8BS_MX_EPIBUF;           // staging buffers per epilogue warp (2 or 4)
 constexpr int A_BYTES = BM * BK;                 // 16 KB
 constexpr int B_BYTES = BN * BK;                 // 28 KB
 constexpr int SF_BYTES = 3 * 512;                // SFA atom + 2 SFB atoms
 constexpr int STAGE = ((A_BYTES + B_BYTES + SF_BYTES + 1023) / 1024) * 1024;
-constexpr int EPI_WARP = 2 * 32 * 128;           // two 32 rows x 128 B staging buffers per epilogue warp
+constexpr int EPI_WARP = EPIBUF * 32 * 128;      // 32 rows x 128 B staging buffers per epilogue warp
 constexpr int OFF_EPI = STAGES * STAGE;
 constexpr int OFF_BAR = OFF_EPI + 4 * EPI_WARP;
 constexpr int NBAR = 2 * STAGES + 4;             // full, empty, accfull[2], accempty[2]
@@ -184,6 +195,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     } else if (warp == 1 || warp == 3 || warp >= 8) {
         // ---------------- scale-factor atoms ----------------
         const int slot = warp == 1 ? 0 : warp == 3 ? 1 : warp - 6;
+        if (slot >= NSF) goto done;                     // (3 stages: warp 9 idles)
         // this warp's K-blocks: global iteration it = slot, slot + NSF, ... (tile it / KB of this CTA's
         // sequence, K-block it % KB).  The raw FP32 scales of the next MX_PF owned K-blocks are in flight
         // while the current one waits for its stage: they are converted only after the wait, so no
@@ -287,7 +299,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + ACC_COLS * b;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c, ++chunk) {
-                const uint32_t ebuf = ebuf0 + (chunk & 1) * (32 * 128);
+                const uint32_t ebuf = ebuf0 + (chunk & (EPIBUF - 1)) * (32 * 128);
                 uint32_t v[32];
                 FP8BS_TMEM_LD32(ta + 32 * c, v);
                 tmem_ld_wait();
@@ -296,7 +308,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     __syncwarp();
                     if (lane == 0) mbar_arrive(accempty_bar(b));
                 }
-                if (lane == 0) bulk_wait_group_read<1>();   // the store that last used this buffer has read it
+                if (lane == 0) bulk_wait_group_read<EPIBUF - 1>();   // the store that last used this buffer has read it
                 __syncwarp();
                 if constexpr (kOutF32) {
 #pragma unroll
@@ -328,6 +340,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         if (lane == 0) bulk_wait_group<0>();
     }
+done:
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -371,7 +384,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     p.rast_n = FP8BS_MX_NFAST == 2 ? (a.M > a.N ? 1 : 0) : FP8BS_MX_NFAST;
     {
         const int64_t res_rows = p.rast_n ? BN : BM * MC, nres = p.rast_n ? p.num_n : p.num_m;
-        const int64_t gb = (48ll << 20) / (res_rows * a.K);
+        const int64_t gb = ((int64_t)FP8BS_BAND_MB << 20) / (res_rows * a.K);
         p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
     }
     p.layout = a.layout; p.sA = a.sA; p.ldsA = a.ldsA; p.sB = a.sB; p.ldsB = a.ldsB; p.accumulate = a.accumulate;
