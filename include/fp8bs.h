@@ -211,6 +211,15 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N,
                                 const uint8_t* B, const float* sB,
                                 void* D, fp8bs_dtype ddt, int64_t ldd,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+
+/* ---- grouped_gemm_mx: the MoE expert Fprop on UE8M0 block scaling (NEXT-1) -----
+ * fp8bs_grouped_gemm's arguments, layouts and validation (no workspace), with fp8bs_gemm_mx's
+ * precondition: every sA and sB value is an exact power of two in [2^-127, 2^127] (e.g. from
+ * fp8bs_quantize_act_dual_pow2 / fp8bs_quantize_weight_128x128_pow2).  No promotion step. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                   const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                   const uint8_t* B, const float* sB,
+                                   void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream);
 FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K);
 
 /* ---- grouped_gemm_dgrad: MoE expert Dgrad (NEXT-3; the backward of the grouped Fprop above) ----

@@ -67,6 +67,10 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "fp8bs_quantize_weight_128x128_pow2"):
             L.fp8bs_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
             L.fp8bs_quantize_weight_128x128_pow2.restype = st
+        if hasattr(L, "fp8bs_grouped_gemm_mx"):
+            L.fp8bs_grouped_gemm_mx.restype = st
+            L.fp8bs_grouped_gemm_mx.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32,
+                                                i64, vp]
         if hasattr(L, "fp8bs_gemm_mx"):
             L.fp8bs_gemm_mx.restype = st
             L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
@@ -254,7 +258,8 @@ def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: to
 
 
 def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
-                 out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, layout: int = FPROP):
+                 out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, layout: int = FPROP,
+                 mx: bool = False):
     """MoE expert GEMM over token rows grouped by expert: offsets int64 [G+1] (device), A [R,K],
     sA [K/128, R], B [G,N,K].  FPROP: sB [G,ceil(N/128),K/128] (fp8bs_grouped_gemm).  DGRAD: B holds
     each expert's WqT [in, out], sB [G,K/128,ceil(N/128)] each expert's sW (fp8bs_grouped_gemm_dgrad)."""
@@ -270,6 +275,12 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
         out = torch.empty(R, N, dtype=out_dtype, device=A.device)
     if layout not in (FPROP, DGRAD):
         raise ValueError("grouped layouts: FPROP, DGRAD")
+    if mx:   # power-of-two scales on UE8M0 block scaling (fp8bs_grouped_gemm_mx, FPROP)
+        if layout != FPROP:
+            raise ValueError("grouped_gemm(mx=True): FPROP only")
+        _check(lib().fp8bs_grouped_gemm_mx(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
+                                           _p(sB), _p(out), _dt(out), out.stride(0), _stream(A)), "fp8bs_grouped_gemm_mx")
+        return out
     fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
                 else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))
     _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),

@@ -282,7 +282,7 @@ size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, 
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
-                                        int64_t ldd, fp8bs_stream_t stream);
+                                        int64_t ldd, fp8bs_stream_t stream, int mx = 0);
 
 fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
@@ -291,6 +291,13 @@ fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
     (void)workspace; (void)workspace_bytes;
     return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream);
+}
+
+fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                   const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                   const uint8_t* B, const float* sB,
+                                   void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream) {
+    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1);
 }
 
 fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
@@ -305,7 +312,7 @@ fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
-                                        int64_t ldd, fp8bs_stream_t stream) {
+                                        int64_t ldd, fp8bs_stream_t stream, int mx) {
     if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
     if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
     fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
@@ -321,9 +328,9 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
     a.grouped = 1; a.G = G; a.offsets = offsets;
     const char* detail = nullptr;
-    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
-    return from_cuda(e, "grouped_gemm launch");
+    return from_cuda(e, mx ? "grouped_gemm_mx launch" : "grouped_gemm launch");
 }
 
 }  // extern "C"

@@ -71,6 +71,10 @@ constexpr int OFF_EPI = STAGES * STAGE;
 constexpr int OFF_BAR = OFF_EPI + 4 * EPI_WARP;
 constexpr int NBAR = 2 * STAGES + 4;             // full, empty, accfull[2], accempty[2]
 constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
+constexpr int MAX_G = 1024;                       // grouped: cum[G + 1], off[G + 1] after the barriers
+constexpr int OFF_GRP = OFF_BAR + NBAR * 8 + 16;
+constexpr int SMEM_G = 1024 + OFF_GRP + 2 * (MAX_G + 1) * 4;
+static_assert(SMEM_G <= 232448, "shared memory");
 constexpr int NSF = STAGES;                      // scale-factor warps 1, 3, 8, 9: warp k owns stage k
 constexpr int THREADS = 32 * 10;
 constexpr int MX_PF = FP8BS_MX_PF;
@@ -82,6 +86,9 @@ struct Params {
     const float* sA; int64_t ldsA;
     const float* sB; int64_t ldsB;
     int accumulate;
+    // grouped (MoE expert Fprop): rows [offsets[e], offsets[e+1]) of A use B[e], sB + e * sb_expert_stride
+    int G; const int64_t* offsets; int64_t sb_expert_stride;
+    void* D; int64_t ldd;                       // rows crossing an expert's end are stored directly
 };
 
 // Tile order (as the promotion kernel's banded raster, gemm.cu get_tile_dense): the operand with fewer
@@ -101,8 +108,8 @@ __device__ __forceinline__ void tile_mn(const Params& p, int t, int& m, int& n) 
 
 __device__ __forceinline__ uint32_t ue8m0(float s) { return (__float_as_uint(s) >> 23) & 0xFFu; }
 
-__device__ __forceinline__ float scale_b(const Params& p, int kb, int j) {
-    if (p.layout == 0) return __ldg(p.sB + (int64_t)(j >> 7) * p.ldsB + kb);     // FPROP: [N/128][K/128]
+__device__ __forceinline__ float scale_b(const Params& p, int kb, int j, int e) {
+    if (p.layout == 0) return __ldg(p.sB + (int64_t)e * p.sb_expert_stride + (int64_t)(j >> 7) * p.ldsB + kb);   // FPROP: [(G,) N/128][K/128]
     if (p.layout == 1) return __ldg(p.sB + (int64_t)kb * p.ldsB + (j >> 7));     // DGRAD: [K/128][N/128]
     return __ldg(p.sB + (int64_t)kb * p.ldsB + j);                               // WGRAD: [K/128][N]
 }
@@ -124,13 +131,21 @@ __device__ __forceinline__ void mma_mx(uint32_t d, uint64_t a, uint64_t b, uint3
                  :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
 }
 
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1, int32_t c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask) : "memory");
+}
+
+struct MxTile { int m0, n0, e, row_end; };
+
 // Arrive once on the barrier at this offset in both CTAs of the pair when the MMAs complete.
 __device__ __forceinline__ void mma_commit_mc(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                  :: "r"(bar), "h"((uint16_t)3) : "memory");
 }
 
-template <bool kOutF32, bool kMc>
+template <bool kOutF32, bool kMc, bool kGrouped>
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmD, const Params p) {
@@ -158,21 +173,68 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
+    int* cum = reinterpret_cast<int*>(smem + OFF_GRP);    // grouped: units of experts < e
+    int* off = cum + (MAX_G + 1);                         // grouped: first row of expert e
+    if constexpr (kGrouped) {
+        if (warp == 4) {
+            // unit prefix over experts: cum[e+1] = cum[e] + ceil(M_e / (MC * BM)) * num_n
+            const int G = p.G, per = (G + 31) / 32;
+            const int e0 = lane * per, e1 = min(G, e0 + per);
+            int local = 0;
+            for (int e = e0; e < e1; ++e) {
+                const int64_t a = p.offsets[e], b = p.offsets[e + 1];
+                off[e] = (int)a;
+                local += (int)((b > a ? b - a : 0) + MC * BM - 1) / (MC * BM) * p.num_n;
+            }
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int run = incl - local;
+            for (int e = e0; e < e1; ++e) {
+                cum[e] = run;
+                const int64_t b = p.offsets[e + 1];
+                run += (int)((b > off[e] ? b - off[e] : 0) + MC * BM - 1) / (MC * BM) * p.num_n;
+            }
+            if (lane == 31) { cum[G] = incl; off[G] = (int)p.offsets[G]; }
+        }
+    }
     tc_fence_before();
     __syncthreads();
     if constexpr (kMc) cluster_sync();              // the peer's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int ntiles = p.num_m * p.num_n;
+    const int ntiles = kGrouped ? cum[p.G] : p.num_m * p.num_n;
+    // unit t -> this CTA's tile: rows [m0, m0 + BM) (clipped at row_end), columns [n0, n0 + BN)
+    auto decode = [&](int t, MxTile& tl) {
+        if constexpr (kGrouped) {
+            int lo = 0, hi = p.G;                       // e: cum[e] <= t < cum[e + 1]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (cum[mid] <= t) lo = mid; else hi = mid;
+            }
+            const int seg = off[lo + 1] - off[lo];
+            const int mt = (seg + MC * BM - 1) / (MC * BM), local = t - cum[lo];
+            const bool nfast = seg > p.N;                // as the promotion kernel: smaller operand resident
+            const int pm = nfast ? local / p.num_n : local % mt, n = nfast ? local % p.num_n : local / mt;
+            tl.m0 = off[lo] + (pm * MC + (int)rank) * BM; tl.n0 = n * BN; tl.e = lo; tl.row_end = off[lo + 1];
+        } else {
+            int tm, tn;
+            tile_mn(p, t, tm, tn);
+            tl.m0 = (tm * MC + (int)rank) * BM; tl.n0 = tn * BN; tl.e = 0; tl.row_end = p.M;
+        }
+    };
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmD); }
         int it = 0;
         for (int t = cid; t < ntiles; t += ncl) {
-            int tm, tn;
-            tile_mn(p, t, tm, tn);
-            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
+            MxTile tl;
+            decode(t, tl);
+            const int m0 = tl.m0, n0 = tl.n0;
             for (int kb = 0; kb < p.KB; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
@@ -180,8 +242,12 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t st = sbase + s * STAGE;
                     mbar_arrive_expect_tx(full_bar(s), A_BYTES + B_BYTES);
                     tma_load_2d(st, &tmA, full_bar(s), kb * BK, m0);
-                    if constexpr (kMc)
+                    if constexpr (kMc && kGrouped)
+                        tma_load_3d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kb * BK, n0 + (int)rank * (BN / 2), tl.e, 3);
+                    else if constexpr (kMc)
                         tma_load_2d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kb * BK, n0 + (int)rank * (BN / 2), 3);
+                    else if constexpr (kGrouped)
+                        tma_load_3d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0, tl.e);
                     else
                         tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0);
                 }
@@ -204,9 +270,9 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         auto load = [&](int it, float* fa, float* fb) -> bool {
             const int t = cid + (it / p.KB) * ncl, kb = it % p.KB;
             if (t >= ntiles) return false;
-            int tm, tn;
-            tile_mn(p, t, tm, tn);
-            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
+            MxTile tl;
+            decode(t, tl);
+            const int m0 = tl.m0, n0 = tl.n0;
 #pragma unroll
             for (int r1 = 0; r1 < 4; ++r1) {
                 const int i = m0 + lane + 32 * r1;
@@ -215,7 +281,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int r1 = 0; r1 < 7; ++r1) {
                 const int j = n0 + lane + 32 * r1;
-                fb[r1] = ((FP8BS_MX_DBG & 2) || j >= p.N) ? 1.0f : scale_b(p, kb, j);
+                fb[r1] = ((FP8BS_MX_DBG & 2) || j >= p.N) ? 1.0f : scale_b(p, kb, j, tl.e);
             }
             return true;
         };
@@ -291,9 +357,10 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         int tl = 0;
         for (int t = cid; t < ntiles; t += ncl, ++tl) {
             const int b = tl & 1;
-            int tm, tn;
-            tile_mn(p, t, tm, tn);
-            const int m0 = (tm * MC + (int)rank) * BM, n0 = tn * BN;
+            MxTile ti;
+            decode(t, ti);
+            const int m0 = ti.m0, n0 = ti.n0;
+            const int rows_here = ti.row_end - (m0 + quad * 32);     // rows of this warp's 32 in range
             mbar_wait(accfull_bar(b), (tl >> 1) & 1);
             tc_fence_after();
             const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + ACC_COLS * b;
@@ -307,6 +374,23 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(accempty_bar(b));
+                }
+                if (kGrouped && rows_here < 32) {
+                    // the expert ends inside this warp's 32 rows (rows past it belong to the next
+                    // expert): each lane stores its own row directly
+                    const int col = n0 + 32 * c;
+                    if (lane < rows_here && col < p.N && !(FP8BS_MX_DBG & 1)) {
+                        const int64_t grow = (int64_t)m0 + quad * 32 + lane;
+                        const int ncol = min(32, p.N - col);
+                        if constexpr (kOutF32) {
+                            float* d = reinterpret_cast<float*>(p.D) + grow * p.ldd + col;
+                            for (int j = 0; j < ncol; ++j) d[j] = __uint_as_float(v[j]);
+                        } else {
+                            __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + grow * p.ldd + col;
+                            for (int j = 0; j < ncol; ++j) d[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                        }
+                    }
+                    continue;
                 }
                 if (lane == 0) bulk_wait_group_read<EPIBUF - 1>();   // the store that last used this buffer has read it
                 __syncwarp();
@@ -361,7 +445,12 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         const uint32_t box[2] = {BK, BM};
         if (!make_tmap(&tA, TMAP_U8, 2, a.A, dims, str, box, 128)) { *detail = "tensor map A"; return cudaErrorInvalidValue; }
     }
-    {
+    if (a.grouped) {   // B [G][N][K], contiguous
+        const uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
+        const uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
+        const uint32_t box[3] = {BK, BN, 1};   // grouped runs unpaired (below)
+        if (!make_tmap(&tB, TMAP_U8, 3, a.B, dims, str, box, 128)) { *detail = "tensor map B (grouped)"; return cudaErrorInvalidValue; }
+    } else {
         const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
         const uint64_t str[1] = {(uint64_t)a.ldb};
         const uint32_t box[2] = {BK, FP8BS_MX_MC ? BN / 2 : BN};
@@ -379,7 +468,10 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     }
     Params p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
-    constexpr int MC = FP8BS_MX_MC ? 2 : 1;
+    // Grouped runs without CTA pairs: a pair shares one expert's n tile over 2 x 128 rows, and at the
+    // MoE shapes most experts have <= 128 rows, which left the second CTA idle (C2: 810 vs 1234
+    // TFLOP/s unpaired).
+    const int MC = (FP8BS_MX_MC && !a.grouped) ? 2 : 1;
     p.num_m = (int)((a.M + BM * MC - 1) / (BM * MC)); p.num_n = (int)((a.N + BN - 1) / BN);   // m units of MC tiles
     p.rast_n = FP8BS_MX_NFAST == 2 ? (a.M > a.N ? 1 : 0) : FP8BS_MX_NFAST;
     {
@@ -388,22 +480,29 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
     }
     p.layout = a.layout; p.sA = a.sA; p.ldsA = a.ldsA; p.sB = a.sB; p.ldsB = a.ldsB; p.accumulate = a.accumulate;
-    const int64_t units = (int64_t)p.num_m * p.num_n;
+    p.G = a.grouped ? a.G : 0; p.offsets = a.offsets; p.sb_expert_stride = (int64_t)((a.N + 127) / 128) * KB;
+    p.D = a.D; p.ldd = a.ldd;
+    // grouped: an upper bound on the units (each expert adds at most one partial m unit per n tile)
+    const int64_t units = a.grouped ? (int64_t)(p.num_m + a.G) * p.num_n : (int64_t)p.num_m * p.num_n;
     const int64_t max_units = num_sms() / MC;
     const int grid = (int)(units < max_units ? units : max_units) * MC;
-    auto kern = a.out_f32 ? k_gemm_mx<true, FP8BS_MX_MC != 0> : k_gemm_mx<false, FP8BS_MX_MC != 0>;
-    static bool attr[2][64] = {{false}};
+    constexpr bool kMc = FP8BS_MX_MC != 0;
+    auto kern = a.grouped ? (a.out_f32 ? k_gemm_mx<true, false, true> : k_gemm_mx<false, false, true>)
+                          : (a.out_f32 ? k_gemm_mx<true, kMc, false> : k_gemm_mx<false, kMc, false>);
+    const int smem = a.grouped ? SMEM_G : SMEM;
+    static bool attr[4][64] = {{false}};
+    const int ki = (a.out_f32 ? 1 : 0) + (a.grouped ? 2 : 0);
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || !attr[a.out_f32 ? 1 : 0][dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (dev < 0 || dev >= 64 || !attr[ki][dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        if (dev >= 0 && dev < 64) attr[a.out_f32 ? 1 : 0][dev] = true;
+        if (dev >= 0 && dev < 64) attr[ki][dev] = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (internal.h launch_pdl)

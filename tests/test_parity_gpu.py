@@ -542,3 +542,43 @@ def test_pow2_training_step_through_mx(T, IN, OUT):
         assert_bits_equal(dqT, rdqT, "dY^T codes")
         O = oracle.gemm(fp.WGRAD, rdqT, rdsT, rxqT, rxsT)
         assert oracle.rel_err_normwise(dw.cpu().double(), O) <= TOL
+
+
+def grouped_case_pow2(counts, N, K, seed=0):
+    offsets = torch.zeros(len(counts) + 1, dtype=torch.int64)
+    offsets[1:] = torch.cumsum(torch.tensor(counts, dtype=torch.int64), 0)
+    R = int(offsets[-1])
+    qa, sa = oracle.quantize_act_1x128_pow2(W.outlier_act(R, K, seed=seed))
+    G = len(counts)
+    w = W.expert_weights(G, N, K, seed=seed + 1, dtype=torch.float32)
+    qb = torch.empty(G, N, K, dtype=torch.uint8)
+    sb = torch.empty(G, (N + 127) // 128, K // 128)
+    for e in range(G):
+        qb[e], sb[e], _ = oracle.quantize_weight_128x128(w[e], want_t=False, pow2=True)
+    return offsets, qa, sa, qb, sb
+
+
+GROUPED_MX_COUNTS = [[0, 7, 130, 1, 64, 0, 300], [256, 256], [3], [0, 0, 257],
+                     [int(c) for c in torch.randint(0, 200, (40,), generator=torch.Generator().manual_seed(5))]]
+
+
+@pytest.mark.parametrize("counts", GROUPED_MX_COUNTS, ids=["mixed", "two256", "three", "lead0", "e40"])
+def test_grouped_mx_vs_dense_mx_bitwise_and_oracle(counts):
+    """MoE expert Fprop on UE8M0 block scaling (fp8bs_grouped_gemm_mx), power-of-two scales: per
+    expert bitwise equal to the dense fp8bs_gemm_mx on its segment (experts ending inside a 32-row
+    store block included), within 1e-3 of the oracle, BF16 = RNE of the FP32 output."""
+    N, K = 264, 512
+    offsets, qa, sa, qb, sb = grouped_case_pow2(counts, N, K, seed=7)
+    D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.float32, mx=True)
+    Db = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.bfloat16, mx=True)
+    torch.cuda.synchronize()
+    for e in range(len(counts)):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        De = fp.gemm(fp.FPROP, dev(qa[a:b].contiguous()), dev_scales(sa[:, a:b].contiguous()), dev(qb[e]), dev(sb[e]),
+                     out_dtype=torch.float32, mx=True)
+        assert_bits_equal(D[a:b], De.cpu(), f"expert {e}")
+    O = oracle.grouped_gemm(offsets, qa, sa, qb, sb)
+    assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+    assert torch.equal(Db.cpu().view(torch.int16), D.cpu().to(torch.bfloat16).view(torch.int16))
