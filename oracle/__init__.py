@@ -62,6 +62,8 @@ def lib():
         L.oracle_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64]
         L.oracle_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32]
         L.oracle_grouped_gemm.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, i32]
+        L.oracle_gemm_limited_accum.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                                i32, i32, i32, i32, vp, i32]
         L.oracle_rel_err_normwise.restype = ctypes.c_double
         L.oracle_rel_err_normwise.argtypes = [vp, vp, i64]
         L.oracle_max_threads.restype = ctypes.c_int
@@ -192,6 +194,23 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
     O = torch.empty(nr, N, dtype=torch.float64)
     lib().oracle_grouped_gemm(G, _ptr(offsets), N, K, _ptr(A), K, _ptr(sA), sA.shape[1], _ptr(B),
                               _ptr(sB), _ptr(rows), nr, _ptr(O), threads)
+    return O
+
+
+def gemm_limited_accum(A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+                       bits: int = 14, chunk: int = 32, nc: int = 0, toward_zero: bool = False,
+                       threads: int = 0) -> torch.Tensor:
+    """Hopper limited-accumulation emulation (R24), context only.
+    A [M,K], B [N,K] codes; sA [K/128, M], sB [K/128, N] per-row scales (nc = 0 uses row 0 of
+    each as one tensor-wise scale per row/column).  Returns O float64 [M,N]."""
+    A, B, sA, sB = A.contiguous(), B.contiguous(), sA.contiguous(), sB.contiguous()
+    M, K = A.shape
+    N = B.shape[0]
+    assert B.shape[1] == K and 0 < chunk <= 256
+    assert nc == 0 or (nc % chunk == 0 and 128 % nc == 0)
+    O = torch.empty(M, N, dtype=torch.float64)
+    lib().oracle_gemm_limited_accum(M, N, K, _ptr(A), K, _ptr(sA), sA.shape[1], _ptr(B), K, _ptr(sB),
+                                    sB.shape[1], bits, chunk, nc, int(toward_zero), _ptr(O), threads)
     return O
 
 

@@ -304,6 +304,80 @@ void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K
     (void)threads;
 }
 
+/* ------------------------------------------- limited accumulation (NEXT-4) ---- */
+/* Emulation of the Hopper tensor-core accumulator the paper measured (context only,
+ * DESIGN.md reading R24):
+ *   "FP8 GEMM employs fixed-point accumulation, aligning the mantissa products by
+ *    right-shifting based on the maximum exponent before addition. ... it only uses the
+ *    highest 14 bits of each mantissa product after sign-fill right shifting, and
+ *    truncates bits exceeding this range";
+ *   "to achieve precise FP32 results from the accumulation of 32 FP8xFP8
+ *    multiplications, at least 34-bit precision is required", i.e. one MMA step
+ *    adds `chunk` products into the accumulator;
+ *   promotion: "Once an interval of N_C is reached, these partial results will be copied
+ *    to FP32 registers on CUDA Cores, where full-precision FP32 accumulation is
+ *    performed" and the group scales are multiplied there.
+ * One accumulation step over terms t_0 = acc, t_1..t_chunk = the chunk's exact products:
+ *   E = max_i floor(log2|t_i|) (nonzero t_i);  q = 2^(E - bits + 1);
+ *   each t_i -> floor(t_i / q) * q   (sign-fill right shift = floor, two's complement);
+ *   acc = RN32(sum of the shifted terms)   (the sum itself is exact in binary64 here).
+ * toward_zero = 1 replaces the floor by truncation toward zero (a sign-magnitude shift):
+ * not the paper's words, kept to bracket its "nearly 2%" figure (R24).
+ * nc = 0: no promotion, the limited accumulator runs over all of K and the scales of
+ * block 0 are applied once at the end (tensor-wise scaling: pass one scale per row/col).
+ * nc > 0 (a multiple of chunk dividing 128): the limited accumulator is
+ * restarted every nc elements, multiplied by the group scales of its 128-block and added
+ * into an FP64 accumulator (the oracle's promotion precision, see oracle_gemm). */
+static double shift_floor(double t, double q, int toward_zero) {
+    return (toward_zero ? trunc(t / q) : floor(t / q)) * q;
+}
+
+static double limited_step(double acc, const double* p, int n, int bits, int toward_zero) {
+    int E = INT32_MIN;
+    int e;
+    if (acc != 0.0) { frexp(acc, &e); E = e - 1; }
+    for (int i = 0; i < n; ++i)
+        if (p[i] != 0.0) { frexp(p[i], &e); if (e - 1 > E) E = e - 1; }
+    if (E == INT32_MIN) return 0.0;
+    double q = ldexp(1.0, E - bits + 1);
+    double sum = shift_floor(acc, q, toward_zero);
+    for (int i = 0; i < n; ++i) sum += shift_floor(p[i], q, toward_zero);
+    return (double)(float)sum;
+}
+
+void oracle_gemm_limited_accum(int64_t M, int64_t N, int64_t K,
+                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                               int bits, int chunk, int nc, int toward_zero, double* O, int threads) {
+    dec_table_init();
+#ifdef _OPENMP
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+    for (int64_t i = 0; i < M; ++i) {
+        double p[256];
+        for (int64_t j = 0; j < N; ++j) {
+            const uint8_t* a = A + i * lda;
+            const uint8_t* b = B + j * ldb;
+            double hi = 0.0, acc = 0.0;
+            for (int64_t c0 = 0; c0 < K; c0 += chunk) {
+                int n = (int)(K - c0 < chunk ? K - c0 : chunk);
+                for (int t = 0; t < n; ++t) p[t] = g_dec[a[c0 + t]] * g_dec[b[c0 + t]];
+                acc = limited_step(acc, p, n, bits, toward_zero);
+                int64_t done = c0 + n;
+                if (nc > 0 && (done % nc == 0 || done == K)) {
+                    int64_t kb = (done - 1) / 128;
+                    hi += ((double)sA[kb * ldsA + i] * (double)sB[kb * ldsB + j]) * acc;
+                    acc = 0.0;
+                }
+            }
+            if (nc == 0) hi = ((double)sA[i] * (double)sB[j]) * acc;
+            O[i * N + j] = hi;
+        }
+    }
+    (void)threads;
+}
+
 double oracle_rel_err_normwise(const double* D, const double* O, int64_t n) {
     double num = 0.0, den = 0.0;
     for (int64_t i = 0; i < n; ++i) {

@@ -74,6 +74,18 @@ void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K
                          const uint8_t* B, const float* sB,
                          const int64_t* rows, int64_t nrows, double* O, int threads);
 
+/* Hopper limited-precision accumulation emulation (context only; R24).
+ * A [M,K] codes (ld lda), B [N,K] codes (ld ldb); per-row scales with the WGRAD layout:
+ * sA(kb,i) = sA[kb*ldsA + i], sB(kb,j) = sB[kb*ldsB + j].  bits = retained bits (14 on
+ * H800), chunk = products per accumulation step (32 = one MMA K-step, <= 256),
+ * nc = promotion interval (0 = none: scales of block 0 applied once at the end);
+ * toward_zero = 0: sign-fill shift (floor), 1: truncation toward zero.
+ * O [M,N] FP64. */
+void oracle_gemm_limited_accum(int64_t M, int64_t N, int64_t K,
+                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                               int bits, int chunk, int nc, int toward_zero, double* O, int threads);
+
 /* max_ij |D - O| / max_ij |O|  (reading R14) */
 double oracle_rel_err_normwise(const double* D, const double* O, int64_t n);
 
