@@ -237,6 +237,42 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int6
                                       void* D, fp8bs_dtype ddt, int64_t ldd,
                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
+/* ---- Grouped MoE expert Wgrad (NEXT-3) ------------------------------------------
+ * dW_e [N, K] = sum over expert e's tokens t of dY[t, :]^T X[t, :]   (P:476-481 applied per expert;
+ * Wgrad operands in 128x1 tiles along the tokens).  The contraction is each
+ * expert's own token segment, and its 128x1 groups restart at the expert's first token: a group never
+ * straddles two experts (reading R25).
+ *
+ * Expert-aligned token layout ("padded tokens"): expert e's M_e = offsets[e+1] - offsets[e] tokens
+ * occupy columns [P_e, P_e + M_e) of the transposed operands, P_e = sum_{f<e} roundup(M_f, 128), and
+ * columns [P_e + M_e, P_{e+1}) hold code 0 (which contributes exactly 0).  Mp = P_G.  Group g of the
+ * padded layout is scale row g; every group starts at a multiple of 128, so the Wgrad GEMM of one
+ * expert is a dense WGRAD over K_e = roundup(M_e, 128) columns at an aligned offset.
+ *
+ * offsets are HOST int64 [G+1] (non-decreasing, offsets[0] = 0): the expert counts are known on the
+ * host when the dispatch is planned; the calls loop over the experts on the host and launch the
+ * dense kernels (no device sync).  Errors as the dense calls; FP8BS_ERR_INVALID_ARG on bad offsets. */
+
+/* Mp for the given host offsets (0 if offsets are invalid). */
+FP8BS_API int64_t fp8bs_padded_tokens(int32_t G, const int64_t* offsets);
+
+/* x [offsets[G], C] rows grouped by expert (ldx >= C) -> qT [C, ldq >= Mp] codes in the padded layout
+ * (padding columns written 0), sT [Mp/128, lds >= C] FP32: the 128x1 quantization of each expert's
+ * segment (fp8bs_quantize_act_128x1's contract per segment). */
+FP8BS_API fp8bs_status fp8bs_quantize_act_128x1_grouped(const void* x, fp8bs_dtype xdt, int32_t G,
+                                              const int64_t* offsets, int64_t C, int64_t ldx,
+                                              uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
+                                              fp8bs_stream_t stream);
+
+/* A = dYqT [N, lda >= Mp], sA [Mp/128, ldsA >= N]; B = XqT [K, ldb >= Mp], sB [Mp/128, ldsB >= K], both in
+ * the padded layout.  D [G, N, K] FP32, expert e at D + e*N*ldd (ldd >= K):  D_e (+)= the WGRAD of
+ * expert e (fp8bs_gemm(FP8BS_WGRAD, N, K, roundup(M_e,128), ...) on its columns).  An expert with no
+ * tokens gets D_e = 0 (accumulate = 0) or keeps D_e (accumulate = 1). */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                      const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                      const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                      float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

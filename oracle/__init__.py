@@ -214,6 +214,50 @@ def gemm_limited_accum(A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: t
     return O
 
 
+def padded_offsets(offsets: torch.Tensor) -> torch.Tensor:
+    """P_e = sum_{f<e} roundup(M_f, 128): the expert-aligned token layout (reading R25)."""
+    m = offsets[1:] - offsets[:-1]
+    P = torch.zeros(offsets.numel(), dtype=torch.int64)
+    P[1:] = torch.cumsum((m + 127) // 128 * 128, 0)
+    return P
+
+
+def quantize_act_128x1_grouped(x: torch.Tensor, offsets: torch.Tensor):
+    """128x1 groups that restart at each expert's first token (R25): expert e's rows
+    x[offsets[e]:offsets[e+1]] quantized alone with quantize_act_128x1 and placed at columns
+    [P_e, P_e + M_e) of qT [C, Mp]; padding codes 0, scale rows g = P_e/128 .. P_{e+1}/128 - 1."""
+    offsets = offsets.to(torch.int64)
+    P = padded_offsets(offsets)
+    C, Mp = x.shape[1], int(P[-1])
+    qT = torch.zeros(C, Mp, dtype=torch.uint8)
+    sT = torch.zeros(Mp // 128, C, dtype=torch.float32)
+    for e in range(offsets.numel() - 1):
+        a, b, p = int(offsets[e]), int(offsets[e + 1]), int(P[e])
+        if b == a:
+            continue
+        q, s_ = quantize_act_128x1(x[a:b])
+        qT[:, p:p + b - a] = q
+        sT[p // 128:p // 128 + s_.shape[0]] = s_
+    return qT, sT
+
+
+def grouped_gemm_wgrad(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor,
+                       sB: torch.Tensor, threads: int = 0) -> torch.Tensor:
+    """dW_e = WGRAD over expert e's token columns [P_e, P_e + roundup(M_e,128)) of the expert-aligned
+    layout: A = dYqT [N, Mp], sA [Mp/128, N]; B = XqT [K, Mp], sB [Mp/128, K].  Returns [G, N, K] FP64;
+    an expert without tokens gets zeros."""
+    offsets = offsets.to(torch.int64)
+    P = padded_offsets(offsets)
+    G, N, K = offsets.numel() - 1, A.shape[0], B.shape[0]
+    O = torch.zeros(G, N, K, dtype=torch.float64)
+    for e in range(G):
+        p, q = int(P[e]), int(P[e + 1])
+        if q == p:
+            continue
+        O[e] = gemm(2, A[:, p:q], sA[p // 128:q // 128], B[:, p:q], sB[p // 128:q // 128], threads=threads)
+    return O
+
+
 def rel_err_normwise(D: torch.Tensor, O: torch.Tensor) -> float:
     D = D.to(torch.float64).contiguous()
     O = O.to(torch.float64).contiguous()

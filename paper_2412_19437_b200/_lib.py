@@ -82,6 +82,14 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
             L.fp8bs_grouped_gemm_dgrad.restype = st
             L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
+        if hasattr(L, "fp8bs_grouped_gemm_wgrad"):
+            L.fp8bs_padded_tokens.restype = i64
+            L.fp8bs_padded_tokens.argtypes = [ctypes.c_int32, vp]
+            L.fp8bs_quantize_act_128x1_grouped.restype = st
+            L.fp8bs_quantize_act_128x1_grouped.argtypes = [vp, i32, ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp]
+            L.fp8bs_grouped_gemm_wgrad.restype = st
+            L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                                   vp, i64, i32, vp]
         L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
         L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
         _lib = L
@@ -180,6 +188,56 @@ def quantize_act_128x1(x: torch.Tensor, qT: torch.Tensor | None = None, sT: torc
     _check(lib().fp8bs_quantize_act_128x1(_p(x), _dt(x), M, C, x.stride(0), _p(qT), qT.stride(0), _p(sT),
                                           sT.stride(0), _stream(x)), "fp8bs_quantize_act_128x1")
     return qT, sT
+
+
+def _host_offsets(offsets) -> torch.Tensor:
+    """Expert offsets as a contiguous CPU int64 tensor (the grouped Wgrad calls take HOST offsets)."""
+    off = torch.as_tensor(offsets, dtype=torch.int64).cpu().contiguous()
+    if off.dim() != 1 or off.numel() < 1:
+        raise ValueError("offsets must be int64 [G+1]")
+    return off
+
+
+def padded_tokens(offsets) -> int:
+    """Mp = sum_e roundup(M_e, 128): token columns of the expert-aligned layout (include/fp8bs.h)."""
+    off = _host_offsets(offsets)
+    return int(lib().fp8bs_padded_tokens(off.numel() - 1, off.data_ptr()))
+
+
+def quantize_act_128x1_grouped(x: torch.Tensor, offsets, qT: torch.Tensor | None = None,
+                               sT: torch.Tensor | None = None):
+    """x [R,C] rows grouped by expert (host offsets [G+1]) -> (qT uint8 [C,Mp], sT fp32 [Mp/128, C]) in
+    the expert-aligned layout: 128x1 groups restart at each expert (fp8bs_quantize_act_128x1_grouped)."""
+    _cuda2d(x, "x")
+    off = _host_offsets(offsets)
+    G, C = off.numel() - 1, x.shape[1]
+    Mp = padded_tokens(off)
+    if qT is None:
+        qT = torch.empty(C, Mp, dtype=torch.uint8, device=x.device)
+    if sT is None:
+        sT = torch.empty(Mp // 128, _pad4(C), dtype=torch.float32, device=x.device)[:, :C]
+    _check(lib().fp8bs_quantize_act_128x1_grouped(_p(x), _dt(x), G, off.data_ptr(), C, x.stride(0), _p(qT),
+                                                  qT.stride(0), _p(sT), sT.stride(0), _stream(x)),
+           "fp8bs_quantize_act_128x1_grouped")
+    return qT, sT
+
+
+def grouped_gemm_wgrad(offsets, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+                       out: torch.Tensor | None = None, accumulate: bool = False):
+    """Per-expert dW_e [N,K] (+)= WGRAD over expert e's tokens: A = dYqT [N,Mp], B = XqT [K,Mp], sA [Mp/128,N],
+    sB [Mp/128,K] in the expert-aligned layout; out FP32 [G,N,K] (fp8bs_grouped_gemm_wgrad)."""
+    for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
+        _cuda2d(t, n)
+    off = _host_offsets(offsets)
+    G, N, K = off.numel() - 1, A.shape[0], B.shape[0]
+    if out is None:
+        out = torch.empty(G, N, K, dtype=torch.float32, device=A.device)
+    if out.dtype != torch.float32 or not out.is_cuda or out.stride(2) != 1 or out.stride(0) != N * out.stride(1):
+        raise ValueError("out must be a CUDA float32 [G,N,K] tensor with unit column stride and stacked experts")
+    _check(lib().fp8bs_grouped_gemm_wgrad(G, off.data_ptr(), N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
+                                          B.stride(0), _p(sB), sB.stride(0), _p(out), out.stride(1),
+                                          1 if accumulate else 0, _stream(A)), "fp8bs_grouped_gemm_wgrad")
+    return out
 
 
 def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor | None = None,

@@ -1,6 +1,7 @@
 // api.cu — C-ABI entry points of libfp8bs.so (include/fp8bs.h): argument validation, device
 // check, then kernel launch on the caller's stream.  Validation runs before any CUDA call so a
 // failing call has no side effects (and the validation paths are testable without a GPU).
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -331,6 +332,94 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
     return from_cuda(e, mx ? "grouped_gemm_mx launch" : "grouped_gemm launch");
+}
+
+/* ---- grouped MoE expert Wgrad on the expert-aligned (padded) token layout (NEXT-3) ---- */
+static int64_t padded_tokens(int32_t G, const int64_t* off) {
+    if (G < 0 || !off || off[0] != 0) return -1;
+    int64_t p = 0;
+    for (int32_t e = 0; e < G; ++e) {
+        int64_t m = off[e + 1] - off[e];
+        if (m < 0) return -1;
+        p += (m + 127) / 128 * 128;
+    }
+    return p;
+}
+
+int64_t fp8bs_padded_tokens(int32_t G, const int64_t* offsets) {
+    int64_t p = padded_tokens(G, offsets);
+    return p < 0 ? 0 : p;
+}
+
+fp8bs_status fp8bs_quantize_act_128x1_grouped(const void* x, fp8bs_dtype xdt, int32_t G, const int64_t* offsets,
+                                              int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq, float* sT,
+                                              int64_t lds, fp8bs_stream_t stream) {
+    if (!valid_dtype(xdt)) return fail(FP8BS_ERR_INVALID_ARG, "xdt=%d", (int)xdt);
+    const int64_t Mp = padded_tokens(G, offsets);
+    if (Mp < 0) return fail(FP8BS_ERR_INVALID_ARG, "offsets must be host int64 [G+1], offsets[0]=0, non-decreasing");
+    if (C < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative C");
+    if (Mp == 0 || C == 0) return ok();
+    if (!x || !qT || !sT) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldx < C || ldq < Mp || lds < C) return fail(FP8BS_ERR_SHAPE, "need ldx>=C, ldq>=Mp=%lld, lds>=C", (long long)Mp);
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    const size_t esz = xdt == FP8BS_BF16 ? 2 : 4;
+    cudaStream_t st = (cudaStream_t)stream;
+    {   /* one launch over every expert's token blocks (BF16, aligned rows); else a loop per expert */
+        std::vector<int64_t> pad(G + 1, 0);
+        for (int32_t e = 0; e < G; ++e) pad[e + 1] = pad[e] + (offsets[e + 1] - offsets[e] + 127) / 128 * 128;
+        cudaError_t err = launch_quant_act_128x1_grouped(x, (int)xdt, G, offsets, pad.data(), C, ldx, qT, ldq, sT, lds, st);
+        if (err == cudaSuccess) return ok();
+        if (err != cudaErrorNotSupported) return from_cuda(err, "quantize_act_128x1_grouped launch");
+        (void)cudaGetLastError();
+    }
+    int64_t p = 0;
+    for (int32_t e = 0; e < G; ++e) {
+        const int64_t m = offsets[e + 1] - offsets[e], mp = (m + 127) / 128 * 128;
+        if (m == 0) continue;
+        cudaError_t err = launch_quant_act_128x1((const char*)x + (size_t)offsets[e] * ldx * esz, (int)xdt, m, C, ldx,
+                                                 qT + p, ldq, sT + (p / 128) * lds, lds, st);
+        if (err != cudaSuccess) return from_cuda(err, "quantize_act_128x1_grouped launch");
+        if (mp > m) {   /* zero codes in the padding columns: they add exactly 0 to the Wgrad */
+            err = cudaMemset2DAsync(qT + p + m, (size_t)ldq, 0, (size_t)(mp - m), (size_t)C, st);
+            if (err != cudaSuccess) return from_cuda(err, "quantize_act_128x1_grouped padding");
+        }
+        p += mp;
+    }
+    return ok();
+}
+
+fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                      const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                      const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                      float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    const int64_t Mp = padded_tokens(G, offsets);
+    if (Mp < 0) return fail(FP8BS_ERR_INVALID_ARG, "offsets must be host int64 [G+1], offsets[0]=0, non-decreasing");
+    if (N < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
+    if (G == 0 || N == 0 || K == 0) return ok();
+    if (!D) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (Mp > 0 && (lda < Mp || ldb < Mp)) return fail(FP8BS_ERR_SHAPE, "need lda, ldb >= Mp=%lld", (long long)Mp);
+    if (ldd < K) return fail(FP8BS_ERR_SHAPE, "need ldd >= K");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t p = 0;
+    for (int32_t e = 0; e < G; ++e) {
+        const int64_t m = offsets[e + 1] - offsets[e], mp = (m + 127) / 128 * 128;
+        float* De = D + (size_t)e * N * ldd;
+        if (m == 0) {
+            if (!accumulate) {
+                fp8bs_status d = check_device();
+                if (d != FP8BS_OK) return d;
+                cudaError_t err = cudaMemset2DAsync(De, (size_t)ldd * 4, 0, (size_t)K * 4, (size_t)N, st);
+                if (err != cudaSuccess) return from_cuda(err, "grouped_gemm_wgrad zero fill");
+            }
+            continue;
+        }
+        fp8bs_status r = gemm_impl(0, FP8BS_WGRAD, N, K, mp, A + p, lda, sA + (p / 128) * ldsA, ldsA,
+                                   B + p, ldb, sB + (p / 128) * ldsB, ldsB, De, FP8BS_FP32, ldd, accumulate, stream);
+        if (r != FP8BS_OK) return r;
+        p += mp;
+    }
+    return ok();
 }
 
 }  // extern "C"

@@ -14,6 +14,9 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 cudaError_t launch_quant_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q,
                                    int64_t ldq, float* s, int64_t lds, cudaStream_t st);
+cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, const int64_t* off, const int64_t* pad,
+                                           int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
+                                           cudaStream_t st);
 cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx, uint8_t* qT,
                                    int64_t ldq, float* sT, int64_t lds, cudaStream_t st);
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,

@@ -396,10 +396,37 @@ __device__ __forceinline__ void column_amax(const uint32_t* w, float* red) {
     }
 }
 
-template <typename T>
+// Token-block maps of the 128x1 quantizer: which source rows feed output token block mb.
+// Dense: rows [128 mb, 128 mb + 128) (TMA zero-fills past M).  Grouped (expert-aligned layout, R25):
+// output block mb lies in expert e's padded range [pad[e], pad[e+1]); its rows start at
+// off[e] + 128 mb - pad[e] and only cnt = min(128, off[e+1] - src) of them belong to e (the rest are
+// masked to +0, which gives amax-neutral zeros and code 0 in the padding).
+struct DenseRows {
+    __device__ __forceinline__ void at(int mb, int64_t, int64_t& src, int& cnt) const { src = (int64_t)mb * 128; cnt = 128; }
+};
+struct GroupRows {
+    static constexpr int MAXG = 1024;
+    int G;
+    int off[MAXG + 1];
+    int pad[MAXG + 1];
+    __device__ __forceinline__ void at(int mb, int64_t, int64_t& src, int& cnt) const {
+        const int m0 = mb * 128;
+        int lo = 0, hi = G - 1;               // last e with pad[e] <= m0 (empty experts have pad[e] == pad[e+1])
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pad[mid] <= m0) lo = mid; else hi = mid - 1;
+        }
+        // lo is non-empty: an empty lo < G-1 has pad[lo+1] == pad[lo] <= m0, so lo+1 would have been chosen
+        src = (int64_t)off[lo] + (m0 - pad[lo]);
+        const int64_t left = (int64_t)off[lo + 1] - src;
+        cnt = left < 128 ? (int)left : 128;
+    }
+};
+
+template <typename T, class Rows>
 __global__ void __launch_bounds__(QTCfg<T>::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
 k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C, uint8_t* __restrict__ qT,
-                      int64_t ldq, float* __restrict__ sT, int64_t lds) {
+                      int64_t ldq, float* __restrict__ sT, int64_t lds, const __grid_constant__ Rows rows) {
     using P = QTCfg<T>;
     extern __shared__ __align__(128) uint8_t smem[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
@@ -422,7 +449,10 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
                 const int st = it % P::STAGES;
                 mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
                 mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
-                tma_load_2d(sbase + st * P::TILE_BYTES, &tmX, bar0 + 8 * st, (t % NCB) * P::CH, (t / NCB) * 128);
+                int64_t src;
+                int cnt;
+                rows.at(t / NCB, M, src, cnt);
+                tma_load_2d(sbase + st * P::TILE_BYTES, &tmX, bar0 + 8 * st, (t % NCB) * P::CH, (int)src);
             }
         }
         return;
@@ -437,6 +467,14 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
         uint32_t w[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) w[r] = lds32(sbase + st * P::TILE_BYTES + (rg * 32 + r) * 256 + wc * 4);
+        if constexpr (!std::is_same<Rows, DenseRows>::value) {   // rows of the next expert -> +0
+            int64_t src;
+            int cnt;
+            rows.at(mb, M, src, cnt);
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                if (rg * 32 + r >= cnt) w[r] = 0u;
+        }
         // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
         // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
         // does not; see gemm.cu release_scales)
@@ -1085,11 +1123,12 @@ static cudaError_t launch_128x1_t(const void* x, int64_t M, int64_t C, int64_t l
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 64 || !attr_tma[dev]) {
-            cudaFuncSetAttribute(k_quant_act_128x1_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+            cudaFuncSetAttribute(k_quant_act_128x1_tma<T, DenseRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
             if (dev >= 0 && dev < 64) attr_tma[dev] = true;
         }
         const int64_t tiles = ((M + 127) / 128) * ((C + Q::CH - 1) / Q::CH);
-        return launch_pdl(k_quant_act_128x1_tma<T>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, C, qT, ldq, sT, lds);
+        return launch_pdl(k_quant_act_128x1_tma<T, DenseRows>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm, M, C, qT, ldq,
+                          sT, lds, DenseRows{});
     } else if (fast) {
         static bool attr_set[64] = {false};   // per device; idempotent, benign race
         int dev = 0;
@@ -1113,6 +1152,38 @@ cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C,
                                    int64_t ldq, float* sT, int64_t lds, cudaStream_t st) {
     if (xdt == 0) return launch_128x1_t<__nv_bfloat16>(x, M, C, ldx, qT, ldq, sT, lds, st);
     return launch_128x1_t<float>(x, M, C, ldx, qT, ldq, sT, lds, st);
+}
+
+// Grouped 128x1 (expert-aligned layout, R25): one launch over all experts' token blocks.  Returns
+// cudaErrorNotSupported when the fused TMA path does not apply (the caller then loops per expert).
+cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, const int64_t* off, const int64_t* pad,
+                                           int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
+                                           cudaStream_t st) {
+    if (xdt != 0 || G > GroupRows::MAXG || off[G] >= (1ll << 31) || pad[G] >= (1ll << 31)) return cudaErrorNotSupported;
+    using Q = QTCfg<__nv_bfloat16>;
+    using P = T128x1<__nv_bfloat16>;
+    const int64_t R = off[G], Mp = pad[G];
+    if (!(aligned16(x) && ((ldx * 2) % 16 == 0) && (C % P::E == 0) && aligned16(qT) && (ldq % 16 == 0)) || R == 0)
+        return cudaErrorNotSupported;
+    alignas(64) CUtensorMap tm;
+    const uint64_t dims[2] = {(uint64_t)C, (uint64_t)R};
+    const uint64_t str[1] = {(uint64_t)ldx * 2};
+    const uint32_t box[2] = {(uint32_t)Q::CH, 128};
+    if (!make_tmap(&tm, TMAP_BF16, 2, x, dims, str, box, 0)) return cudaErrorNotSupported;
+    static thread_local GroupRows* rp = nullptr;   // host staging of the 8 KB kernel parameter
+    if (!rp) rp = new GroupRows();
+    rp->G = G;
+    for (int e = 0; e <= G; ++e) { rp->off[e] = (int)off[e]; rp->pad[e] = (int)pad[e]; }
+    static bool attr[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+        cudaFuncSetAttribute(k_quant_act_128x1_tma<__nv_bfloat16, GroupRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    const int64_t tiles = (Mp / 128) * ((C + Q::CH - 1) / Q::CH);
+    return launch_pdl(k_quant_act_128x1_tma<__nv_bfloat16, GroupRows>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm,
+                      Mp, C, qT, ldq, sT, lds, *rp);
 }
 
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,

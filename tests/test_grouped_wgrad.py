@@ -1,0 +1,167 @@
+"""Grouped MoE expert Wgrad: dW_e = dY_e^T X_e over each expert's own tokens, with
+the Wgrad operands in 128x1 tiles along the tokens whose groups restart at each
+expert's first token (reading R25), on the expert-aligned ("padded") token layout of
+include/fp8bs.h.
+
+CPU: the oracle's grouped functions pinned by properties the definition fixes (segment = dense
+quantization of that expert alone, invariance under reordering the experts, the one-expert case equals
+the dense path, padding adds nothing, the dequantized product is close to the unquantized one) and the
+host-side validation of the C-ABI.  GPU: the CUDA path through the C-ABI vs the oracle (codes and scales
+bit-exact; dW within 1e-3 normwise per expert; bitwise equal to per-expert dense fp8bs_gemm WGRAD calls).
+"""
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+TOL = 1e-3
+# expert token counts: empty experts, a 1-token expert, exact multiples of 128, ragged tails
+COUNTS = [[0, 5, 128, 200, 0, 300, 1, 256], [130], [0, 0, 77]]
+
+
+def _offsets(counts):
+    off = torch.zeros(len(counts) + 1, dtype=torch.int64)
+    off[1:] = torch.cumsum(torch.tensor(counts, dtype=torch.int64), 0)
+    return off
+
+
+def _problem(counts, C_in=256, N_out=384, seed=0):
+    off = _offsets(counts)
+    R = int(off[-1])
+    x = W.gaussian_act(R, C_in, seed=seed)
+    dy = W.grad_out(R, N_out, seed=seed + 1)
+    return off, x, dy
+
+
+def test_grouped_128x1_is_per_expert_dense():
+    off, x, _ = _problem(COUNTS[0])
+    qT, sT = oracle.quantize_act_128x1_grouped(x, off)
+    P = oracle.padded_offsets(off)
+    assert int(P[-1]) == sum((c + 127) // 128 * 128 for c in COUNTS[0])
+    for e in range(len(COUNTS[0])):
+        a, b, p, q = int(off[e]), int(off[e + 1]), int(P[e]), int(P[e + 1])
+        if a == b:
+            assert p == q
+            continue
+        qd, sd = oracle.quantize_act_128x1(x[a:b])
+        assert torch.equal(qT[:, p:p + b - a], qd)
+        assert torch.equal(qT[:, p + b - a:q], torch.zeros_like(qT[:, p + b - a:q]))   # padding codes 0
+        assert torch.equal(sT[p // 128:q // 128], sd)
+
+
+def test_groups_never_straddle_experts():
+    """Expert e's rows scaled by 10^e: every scale row must see one expert's magnitude only."""
+    counts = [70, 90, 60]
+    off, x, _ = _problem(counts)
+    x = x.float()
+    for e in range(3):
+        x[int(off[e]):int(off[e + 1])] *= 10.0 ** (2 * e)
+    _, sT = oracle.quantize_act_128x1_grouped(x, off)
+    amax = [x[int(off[e]):int(off[e + 1])].abs().amax(0) for e in range(3)]
+    for e in range(3):
+        assert torch.equal(sT[e], (amax[e] / 448.0).float())     # one 128-group per expert here
+
+
+def test_grouped_wgrad_oracle_properties():
+    counts = COUNTS[0]
+    off, x, dy = _problem(counts)
+    XqT, sX = oracle.quantize_act_128x1_grouped(x, off)
+    DqT, sD = oracle.quantize_act_128x1_grouped(dy, off)
+    O = oracle.grouped_gemm_wgrad(off, DqT, sD, XqT, sX)
+    G = len(counts)
+    # (1) permuting the experts permutes the result
+    perm = [3, 0, 7, 2, 5, 1, 6, 4]
+    segs = [(int(off[e]), int(off[e + 1])) for e in range(G)]
+    xp = torch.cat([x[a:b] for a, b in (segs[e] for e in perm)])
+    dyp = torch.cat([dy[a:b] for a, b in (segs[e] for e in perm)])
+    offp = _offsets([counts[e] for e in perm])
+    XqTp, sXp = oracle.quantize_act_128x1_grouped(xp, offp)
+    DqTp, sDp = oracle.quantize_act_128x1_grouped(dyp, offp)
+    Op = oracle.grouped_gemm_wgrad(offp, DqTp, sDp, XqTp, sXp)
+    for i, e in enumerate(perm):
+        assert torch.equal(Op[i], O[e])
+    # (2) empty experts are zero; (3) close to the unquantized per-expert product (E4M3: ~4e-2, §3)
+    for e, (a, b) in enumerate(segs):
+        if a == b:
+            assert not O[e].any()
+            continue
+        exact = dy[a:b].double().T @ x[a:b].double()
+        assert oracle.rel_err_normwise(O[e], exact) < 0.15
+    # (4) one expert with a multiple of 128 tokens: the dense 128x1 + WGRAD path
+    off1, x1, dy1 = _problem([256])
+    XqT1, sX1 = oracle.quantize_act_128x1_grouped(x1, off1)
+    DqT1, sD1 = oracle.quantize_act_128x1_grouped(dy1, off1)
+    qx, sx = oracle.quantize_act_128x1(x1)
+    qd, sd = oracle.quantize_act_128x1(dy1)
+    assert torch.equal(oracle.grouped_gemm_wgrad(off1, DqT1, sD1, XqT1, sX1)[0], oracle.gemm(2, qd, sd, qx, sx))
+
+
+def test_grouped_wgrad_abi_validation():
+    """Host-side argument checks of the grouped Wgrad entry points (no GPU needed: offsets are checked
+    before the device)."""
+    import ctypes
+
+    import paper_2412_19437_b200 as fp
+    L = fp.lib()
+    bad = torch.tensor([0, 5, 3], dtype=torch.int64)          # decreasing
+    nz = torch.tensor([1, 5], dtype=torch.int64)              # offsets[0] != 0
+    for off in (bad, nz):
+        st = L.fp8bs_quantize_act_128x1_grouped(ctypes.c_void_p(16), 0, off.numel() - 1, off.data_ptr(), 128, 128,
+                                                ctypes.c_void_p(16), 4096, ctypes.c_void_p(16), 128, None)
+        assert st == 1, fp.last_error_detail()
+        st = L.fp8bs_grouped_gemm_wgrad(off.numel() - 1, off.data_ptr(), 128, 128, None, 4096, None, 128, None, 4096,
+                                        None, 128, None, 128, 0, None)
+        assert st == 1
+        assert L.fp8bs_padded_tokens(off.numel() - 1, off.data_ptr()) == 0
+    assert fp.padded_tokens([0, 5, 5, 300]) == 128 + 0 + 384
+
+
+# ----------------------------------------------------------------------------------- GPU ----
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16_one_launch", "fp32_per_expert"])
+@pytest.mark.parametrize("counts", COUNTS, ids=["mixed8", "one", "empties"])
+def test_grouped_128x1_gpu_bitexact(counts, dtype):
+    """BF16 takes the single-launch kernel (token-block map over all experts), FP32 the per-expert loop."""
+    import paper_2412_19437_b200 as fp
+    off, x, _ = _problem(counts)
+    x = x.to(dtype)
+    qT_ref, sT_ref = oracle.quantize_act_128x1_grouped(x, off)
+    qT = torch.full((x.shape[1], int(oracle.padded_offsets(off)[-1])), 0x55, dtype=torch.uint8, device="cuda")
+    qT, sT = fp.quantize_act_128x1_grouped(x.cuda(), off, qT=qT)
+    torch.cuda.synchronize()
+    assert torch.equal(qT.cpu(), qT_ref)          # padding overwritten with 0
+    assert torch.equal(sT.cpu().view(torch.int32), sT_ref.view(torch.int32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("counts", COUNTS, ids=["mixed8", "one", "empties"])
+def test_grouped_wgrad_gpu_vs_oracle_and_dense(counts):
+    import paper_2412_19437_b200 as fp
+    off, x, dy = _problem(counts, C_in=448, N_out=640)
+    XqT, sX = oracle.quantize_act_128x1_grouped(x, off)
+    DqT, sD = oracle.quantize_act_128x1_grouped(dy, off)
+    O = oracle.grouped_gemm_wgrad(off, DqT, sD, XqT, sX)
+    XqT_d, sX_d = fp.quantize_act_128x1_grouped(x.cuda(), off)
+    DqT_d, sD_d = fp.quantize_act_128x1_grouped(dy.cuda(), off)
+    G, N, K = len(counts), dy.shape[1], x.shape[1]
+    D = torch.full((G, N, K), float("nan"), device="cuda")
+    fp.grouped_gemm_wgrad(off, DqT_d, sD_d, XqT_d, sX_d, out=D)
+    torch.cuda.synchronize()
+    P = oracle.padded_offsets(off)
+    for e in range(G):
+        p, q = int(P[e]), int(P[e + 1])
+        if p == q:
+            assert not D[e].any(), "expert without tokens must get dW = 0"
+            continue
+        assert oracle.rel_err_normwise(D[e].cpu().double(), O[e]) <= TOL
+        De = fp.gemm(fp.WGRAD, DqT_d[:, p:q], sD_d[p // 128:q // 128], XqT_d[:, p:q], sX_d[p // 128:q // 128],
+                     out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(D[e].view(torch.int32), De.view(torch.int32))
+    # accumulate: D += dW (experts without tokens keep D)
+    D2 = torch.ones(G, N, K, device="cuda")
+    fp.grouped_gemm_wgrad(off, DqT_d, sD_d, XqT_d, sX_d, out=D2, accumulate=True)
+    torch.cuda.synchronize()
+    for e in range(G):
+        assert oracle.rel_err_normwise(D2[e].cpu().double(), O[e] + 1.0) <= TOL
