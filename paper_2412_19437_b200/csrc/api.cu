@@ -1,6 +1,8 @@
 // api.cu — C-ABI entry points of libfp8bs.so (include/fp8bs.h): argument validation, device
 // check, then kernel launch on the caller's stream.  Validation runs before any CUDA call so a
 // failing call has no side effects (and the validation paths are testable without a GPU).
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 #include <cstdarg>
 #include <cstdio>
@@ -335,6 +337,28 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
 }
 
 /* ---- grouped MoE expert Wgrad on the expert-aligned (padded) token layout (NEXT-3) ---- */
+/* Side streams for the per-expert fork/join of fp8bs_grouped_gemm_wgrad, one set per device, created
+ * on first use and kept for the life of the process. */
+struct ForkStreams {
+    static constexpr int NS = 4;
+    cudaStream_t st[NS];
+    cudaEvent_t start, done[NS];
+};
+static std::mutex g_fork_mutex;
+static ForkStreams* fork_streams(int dev) {
+    static ForkStreams* sets[64] = {nullptr};
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!sets[dev]) {
+        ForkStreams* f = new ForkStreams();
+        bool good = cudaEventCreateWithFlags(&f->start, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < ForkStreams::NS && good; ++i)
+            good = cudaStreamCreateWithFlags(&f->st[i], cudaStreamNonBlocking) == cudaSuccess &&
+                   cudaEventCreateWithFlags(&f->done[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!good) { (void)cudaGetLastError(); delete f; return nullptr; }   /* fall back to the caller's stream */
+        sets[dev] = f;
+    }
+    return sets[dev];
+}
 static int64_t padded_tokens(int32_t G, const int64_t* off) {
     if (G < 0 || !off || off[0] != 0) return -1;
     int64_t p = 0;
@@ -400,26 +424,47 @@ fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t
     if (!D) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
     if (Mp > 0 && (lda < Mp || ldb < Mp)) return fail(FP8BS_ERR_SHAPE, "need lda, ldb >= Mp=%lld", (long long)Mp);
     if (ldd < K) return fail(FP8BS_ERR_SHAPE, "need ldd >= K");
-    cudaStream_t st = (cudaStream_t)stream;
+    fp8bs_status dv = check_device();
+    if (dv != FP8BS_OK) return dv;
+    /* The experts are independent GEMMs: fork them round-robin over side streams so one expert's
+     * last wave overlaps the next expert's first (a single stream leaves a tail per expert), then
+     * join back into the caller's stream.  Event record/wait keep this capturable in a CUDA graph. */
+    std::lock_guard<std::mutex> lock(g_fork_mutex);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static const bool fork_on = !getenv("FP8BS_WGRAD_FORK") || atoi(getenv("FP8BS_WGRAD_FORK")) != 0;   /* A/B knob */
+    ForkStreams* fk = fork_on ? fork_streams(dev) : nullptr;
+    const int ns = fk ? ForkStreams::NS : 1;
+    cudaStream_t caller = (cudaStream_t)stream;
+    if (fk) {
+        if (cudaEventRecord(fk->start, caller) != cudaSuccess) return from_cuda(cudaGetLastError(), "grouped_gemm_wgrad fork");
+        for (int i = 0; i < ns; ++i) cudaStreamWaitEvent(fk->st[i], fk->start, 0);
+    }
+    fp8bs_status result = FP8BS_OK;
     int64_t p = 0;
-    for (int32_t e = 0; e < G; ++e) {
+    int used = 0;
+    for (int32_t e = 0; e < G && result == FP8BS_OK; ++e) {
         const int64_t m = offsets[e + 1] - offsets[e], mp = (m + 127) / 128 * 128;
         float* De = D + (size_t)e * N * ldd;
+        cudaStream_t st = fk ? fk->st[used++ % ns] : caller;
         if (m == 0) {
             if (!accumulate) {
-                fp8bs_status d = check_device();
-                if (d != FP8BS_OK) return d;
                 cudaError_t err = cudaMemset2DAsync(De, (size_t)ldd * 4, 0, (size_t)K * 4, (size_t)N, st);
-                if (err != cudaSuccess) return from_cuda(err, "grouped_gemm_wgrad zero fill");
+                if (err != cudaSuccess) result = from_cuda(err, "grouped_gemm_wgrad zero fill");
             }
             continue;
         }
-        fp8bs_status r = gemm_impl(0, FP8BS_WGRAD, N, K, mp, A + p, lda, sA + (p / 128) * ldsA, ldsA,
-                                   B + p, ldb, sB + (p / 128) * ldsB, ldsB, De, FP8BS_FP32, ldd, accumulate, stream);
-        if (r != FP8BS_OK) return r;
+        result = gemm_impl(0, FP8BS_WGRAD, N, K, mp, A + p, lda, sA + (p / 128) * ldsA, ldsA,
+                           B + p, ldb, sB + (p / 128) * ldsB, ldsB, De, FP8BS_FP32, ldd, accumulate, (fp8bs_stream_t)st);
         p += mp;
     }
-    return ok();
+    if (fk) {   /* join, also after an error, so the caller's stream never runs ahead of launched work */
+        for (int i = 0; i < ns; ++i) {
+            cudaEventRecord(fk->done[i], fk->st[i]);
+            cudaStreamWaitEvent(caller, fk->done[i], 0);
+        }
+    }
+    return result == FP8BS_OK ? ok() : result;
 }
 
 }  // extern "C"
