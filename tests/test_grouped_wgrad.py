@@ -165,3 +165,36 @@ def test_grouped_wgrad_gpu_vs_oracle_and_dense(counts):
     torch.cuda.synchronize()
     for e in range(G):
         assert oracle.rel_err_normwise(D2[e].cpu().double(), O[e] + 1.0) <= TOL
+
+
+@pytest.mark.gpu
+def test_grouped_wgrad_c4_full_size_sampled():
+    """C4's expert shape at the size tools/grouped_wgrad_bench.py times (256 experts, 8192 tokens x
+    top-8 = 65536 rows, skewed routing R16, 7168 -> 2048): GPU quantizer + grouped Wgrad, checked on
+    sampled dW rows of the smallest, the largest and two other experts against the oracle GEMM on the
+    same codes (the oracle quantizer checks the sampled experts' codes bit for bit)."""
+    import paper_2412_19437_b200 as fp
+    G, T, N, K = 256, 8192, 2048, 7168
+    routes = W.route_skewed(T, G, 8, seed=3)
+    _, off = W.group_rows(routes, G)
+    R = int(off[-1])
+    x = W.gaussian_act(R, K, seed=0)
+    dy = W.grad_out(R, N, seed=1)
+    XqT, sX = fp.quantize_act_128x1_grouped(x.cuda(), off)
+    DqT, sD = fp.quantize_act_128x1_grouped(dy.cuda(), off)
+    D = fp.grouped_gemm_wgrad(off, DqT, sD, XqT, sX)
+    torch.cuda.synchronize()
+    m = off[1:] - off[:-1]
+    P = oracle.padded_offsets(off)
+    experts = sorted({int(m.argmin()), int(m.argmax()), 17, 200})
+    g = torch.Generator().manual_seed(4)
+    for e in experts:
+        a, b, p, q = int(off[e]), int(off[e + 1]), int(P[e]), int(P[e + 1])
+        qx, sx = oracle.quantize_act_128x1(x[a:b])
+        qd, sd = oracle.quantize_act_128x1(dy[a:b])
+        assert torch.equal(XqT[:, p:p + b - a].cpu(), qx) and torch.equal(DqT[:, p:p + b - a].cpu(), qd)
+        assert torch.equal(sX[p // 128:q // 128].cpu().view(torch.int32), sx.view(torch.int32))
+        rows = torch.cat([torch.tensor([0, N - 1]), torch.randint(0, N, (6,), generator=g)])
+        pad = lambda c: torch.nn.functional.pad(c, (0, (q - p) - (b - a)))   # zero codes up to roundup(M_e,128)
+        O = oracle.gemm(2, pad(qd), sd, pad(qx), sx, rows=rows)
+        assert oracle.rel_err_normwise(D[e][rows.cuda()].cpu().double(), O) <= TOL
