@@ -340,7 +340,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
 /* Side streams for the per-expert fork/join of fp8bs_grouped_gemm_wgrad, one set per device, created
  * on first use and kept for the life of the process. */
 struct ForkStreams {
-    static constexpr int NS = 4;
+    static constexpr int NS = 4;   /* FP8BS_WGRAD_STREAMS (1-4, default 4) of them are used; 2, 4, 6, 8 measured flat */
     cudaStream_t st[NS];
     cudaEvent_t start, done[NS];
 };
@@ -434,7 +434,8 @@ fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t
     cudaGetDevice(&dev);
     static const bool fork_on = !getenv("FP8BS_WGRAD_FORK") || atoi(getenv("FP8BS_WGRAD_FORK")) != 0;   /* A/B knob */
     ForkStreams* fk = fork_on ? fork_streams(dev) : nullptr;
-    const int ns = fk ? ForkStreams::NS : 1;
+    static const int ns_env = getenv("FP8BS_WGRAD_STREAMS") ? atoi(getenv("FP8BS_WGRAD_STREAMS")) : 4;
+    const int ns = fk ? (ns_env < 1 ? 1 : ns_env > ForkStreams::NS ? ForkStreams::NS : ns_env) : 1;
     cudaStream_t caller = (cudaStream_t)stream;
     if (fk) {
         if (cudaEventRecord(fk->start, caller) != cudaSuccess) return from_cuda(cudaGetLastError(), "grouped_gemm_wgrad fork");
