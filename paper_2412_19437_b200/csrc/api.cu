@@ -389,7 +389,7 @@ fp8bs_status fp8bs_quantize_act_128x1_grouped(const void* x, fp8bs_dtype xdt, in
     if (d != FP8BS_OK) return d;
     const size_t esz = xdt == FP8BS_BF16 ? 2 : 4;
     cudaStream_t st = (cudaStream_t)stream;
-    {   /* one launch over every expert's token blocks (BF16, aligned rows); else a loop per expert */
+    {   /* one launch over every expert's token blocks (16-byte aligned rows); else a loop per expert */
         std::vector<int64_t> pad(G + 1, 0);
         for (int32_t e = 0; e < G; ++e) pad[e + 1] = pad[e] + (offsets[e + 1] - offsets[e] + 127) / 128 * 128;
         cudaError_t err = launch_quant_act_128x1_grouped(x, (int)xdt, G, offsets, pad.data(), C, ldx, qT, ldq, sT, lds, st);

@@ -1154,22 +1154,22 @@ cudaError_t launch_quant_act_128x1(const void* x, int xdt, int64_t M, int64_t C,
     return launch_128x1_t<float>(x, M, C, ldx, qT, ldq, sT, lds, st);
 }
 
-// Grouped 128x1 (expert-aligned layout, R25): one launch over all experts' token blocks.  Returns
-// cudaErrorNotSupported when the fused TMA path does not apply (the caller then loops per expert).
-cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, const int64_t* off, const int64_t* pad,
-                                           int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
-                                           cudaStream_t st) {
-    if (xdt != 0 || G > GroupRows::MAXG || off[G] >= (1ll << 31) || pad[G] >= (1ll << 31)) return cudaErrorNotSupported;
-    using Q = QTCfg<__nv_bfloat16>;
-    using P = T128x1<__nv_bfloat16>;
+// Grouped 128x1 (expert-aligned layout, R25): one launch over all experts' token blocks (BF16 or FP32).
+// Returns cudaErrorNotSupported when the TMA path does not apply (the caller then loops per expert).
+template <typename T>
+static cudaError_t launch_128x1_grouped_t(const void* x, int32_t G, const int64_t* off, const int64_t* pad, int64_t C,
+                                          int64_t ldx, uint8_t* qT, int64_t ldq, float* sT, int64_t lds, cudaStream_t st) {
+    using Q = QTCfg<T>;
+    using P = T128x1<T>;
     const int64_t R = off[G], Mp = pad[G];
-    if (!(aligned16(x) && ((ldx * 2) % 16 == 0) && (C % P::E == 0) && aligned16(qT) && (ldq % 16 == 0)) || R == 0)
+    if (!(aligned16(x) && ((ldx * (int64_t)sizeof(T)) % 16 == 0) && (C % P::E == 0) && aligned16(qT) && (ldq % 16 == 0)) ||
+        R == 0)
         return cudaErrorNotSupported;
     alignas(64) CUtensorMap tm;
     const uint64_t dims[2] = {(uint64_t)C, (uint64_t)R};
-    const uint64_t str[1] = {(uint64_t)ldx * 2};
+    const uint64_t str[1] = {(uint64_t)ldx * sizeof(T)};
     const uint32_t box[2] = {(uint32_t)Q::CH, 128};
-    if (!make_tmap(&tm, TMAP_BF16, 2, x, dims, str, box, 0)) return cudaErrorNotSupported;
+    if (!make_tmap(&tm, sizeof(T) == 2 ? TMAP_BF16 : TMAP_F32, 2, x, dims, str, box, 0)) return cudaErrorNotSupported;
     static thread_local GroupRows* rp = nullptr;   // host staging of the 8 KB kernel parameter
     if (!rp) rp = new GroupRows();
     rp->G = G;
@@ -1178,12 +1178,20 @@ cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, co
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr[dev]) {
-        cudaFuncSetAttribute(k_quant_act_128x1_tma<__nv_bfloat16, GroupRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+        cudaFuncSetAttribute(k_quant_act_128x1_tma<T, GroupRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     const int64_t tiles = (Mp / 128) * ((C + Q::CH - 1) / Q::CH);
-    return launch_pdl(k_quant_act_128x1_tma<__nv_bfloat16, GroupRows>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm,
+    return launch_pdl(k_quant_act_128x1_tma<T, GroupRows>, grid_for(tiles, 2, 2), Q::THREADS, Q::SMEM, st, tm,
                       Mp, C, qT, ldq, sT, lds, *rp);
+}
+
+cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, const int64_t* off, const int64_t* pad,
+                                           int64_t C, int64_t ldx, uint8_t* qT, int64_t ldq, float* sT, int64_t lds,
+                                           cudaStream_t st) {
+    if (G > GroupRows::MAXG || off[G] >= (1ll << 31) || pad[G] >= (1ll << 31)) return cudaErrorNotSupported;
+    if (xdt == 0) return launch_128x1_grouped_t<__nv_bfloat16>(x, G, off, pad, C, ldx, qT, ldq, sT, lds, st);
+    return launch_128x1_grouped_t<float>(x, G, off, pad, C, ldx, qT, ldq, sT, lds, st);
 }
 
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,

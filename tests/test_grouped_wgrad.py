@@ -119,16 +119,23 @@ def test_grouped_wgrad_abi_validation():
 
 # ----------------------------------------------------------------------------------- GPU ----
 @pytest.mark.gpu
-@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16_one_launch", "fp32_per_expert"])
+@pytest.mark.parametrize("dtype,aligned", [(torch.bfloat16, True), (torch.float32, True), (torch.bfloat16, False)],
+                         ids=["bf16_one_launch", "fp32_one_launch", "bf16_unaligned_per_expert"])
 @pytest.mark.parametrize("counts", COUNTS, ids=["mixed8", "one", "empties"])
-def test_grouped_128x1_gpu_bitexact(counts, dtype):
-    """BF16 takes the single-launch kernel (token-block map over all experts), FP32 the per-expert loop."""
+def test_grouped_128x1_gpu_bitexact(counts, dtype, aligned):
+    """Aligned rows take the single-launch kernel (token-block map over all experts); rows whose pitch
+    is not a multiple of 16 bytes take the per-expert loop of the generic kernel."""
     import paper_2412_19437_b200 as fp
     off, x, _ = _problem(counts)
     x = x.to(dtype)
     qT_ref, sT_ref = oracle.quantize_act_128x1_grouped(x, off)
     qT = torch.full((x.shape[1], int(oracle.padded_offsets(off)[-1])), 0x55, dtype=torch.uint8, device="cuda")
-    qT, sT = fp.quantize_act_128x1_grouped(x.cuda(), off, qT=qT)
+    xd = x.cuda()
+    if not aligned:   # row pitch C + 1 elements
+        wide = torch.zeros(x.shape[0], x.shape[1] + 1, dtype=dtype, device="cuda")
+        wide[:, :x.shape[1]] = xd
+        xd = wide[:, :x.shape[1]]
+    qT, sT = fp.quantize_act_128x1_grouped(xd, off, qT=qT)
     torch.cuda.synchronize()
     assert torch.equal(qT.cpu(), qT_ref)          # padding overwritten with 0
     assert torch.equal(sT.cpu().view(torch.int32), sT_ref.view(torch.int32))
