@@ -88,8 +88,9 @@ FP8BS_API fp8bs_status fp8bs_quantize_act_1x128(const void* x, fp8bs_dtype xdt, 
  * P:558 ("integral power of 2" scaling factors for the inputs of the Linear after attention) and
  * P:565 (the activations quantized before MoE dispatch).  As fp8bs_quantize_act_1x128 except
  * s = 2^e, the smallest power of two with 448 * 2^e >= amax (reading R23: rounded up from the exact
- * quotient, so nothing saturates; amax 3.0 -> s = 2^-7, 3.0 / s = 384), e >= -149,
- * 1 for an all-zero tile.  The quotient x / s is then exact before the E4M3 rounding.  Same layouts,
+ * quotient, so nothing saturates; amax 3.0 -> s = 2^-7, 3.0 / s = 384), e >= -127
+ * (reading R26: the smallest UE8M0 value, so the scales are exact inputs of fp8bs_gemm_mx), 1 for an
+ * all-zero tile.  The quotient x / s is then exact before the E4M3 rounding.  Same layouts,
  * ownership and errors as fp8bs_quantize_act_1x128; the scales feed fp8bs_gemm unchanged. */
 FP8BS_API fp8bs_status fp8bs_quantize_act_1x128_pow2(const void* x, fp8bs_dtype xdt, int64_t M, int64_t K, int64_t ldx,
                                            uint8_t* q, int64_t ldq, float* s, int64_t lds, fp8bs_stream_t stream);

@@ -200,7 +200,7 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
 def gemm_limited_accum(A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
                        bits: int = 14, chunk: int = 32, nc: int = 0, toward_zero: bool = False,
                        threads: int = 0) -> torch.Tensor:
-    """Hopper limited-accumulation emulation (P:648-650, P:529-531; DESIGN.md R24), context only.
+    """Hopper limited-accumulation emulation (P:649-651, P:529-531; DESIGN.md R24), context only.
     A [M,K], B [N,K] codes; sA [K/128, M], sB [K/128, N] per-row scales (nc = 0 uses row 0 of
     each as one tensor-wise scale per row/column).  Returns O float64 [M,N]."""
     A, B, sA, sB = A.contiguous(), B.contiguous(), sA.contiguous(), sB.contiguous()

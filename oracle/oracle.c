@@ -103,14 +103,15 @@ static float group_scale(float amax) {
 
 /* power-of-two scale ("integral power of 2"; SPEC S:374 / S:417 round UP): the
  * smallest s = 2^e with 448 * s >= amax, computed on exact values (448 * 2^e is exact in double);
- * e >= -149 (the smallest float subnormal); 1 for an all-zero group; a non-finite amax passes
- * through (as amax / 448 does in group_scale). */
+ * e >= -127, the smallest UE8M0 value, so every pow2 scale is representable by the tensor core's
+ * block-scale format (reading R26; an amax below 448 * 2^-127 then still fits without saturating);
+ * 1 for an all-zero group; a non-finite amax passes through (as amax / 448 does in group_scale). */
 static float group_scale_pow2(float amax) {
     if (amax == 0.0f) return 1.0f;
     if (!isfinite(amax)) return amax;
     int e = -160;
     while (ldexp(448.0, e) < (double)amax) ++e;    /* plain linear search from below */
-    if (e < -149) e = -149;
+    if (e < -127) e = -127;
     return ldexpf(1.0f, e);
 }
 
@@ -310,9 +311,9 @@ void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K
  *   "FP8 GEMM employs fixed-point accumulation, aligning the mantissa products by
  *    right-shifting based on the maximum exponent before addition. ... it only uses the
  *    highest 14 bits of each mantissa product after sign-fill right shifting, and
- *    truncates bits exceeding this range" (P:648-649);
+ *    truncates bits exceeding this range" (P:649-650);
  *   "to achieve precise FP32 results from the accumulation of 32 FP8xFP8
- *    multiplications, at least 34-bit precision is required" (P:650), i.e. one MMA step
+ *    multiplications, at least 34-bit precision is required" (P:651), i.e. one MMA step
  *    adds `chunk` products into the accumulator;
  *   promotion: "Once an interval of N_C is reached, these partial results will be copied
  *    to FP32 registers on CUDA Cores, where full-precision FP32 accumulation is

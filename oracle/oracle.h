@@ -36,7 +36,7 @@ float   oracle_bf16_to_float(uint16_t bits);
 
 void oracle_quantize_act_1x128(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
                                uint8_t* q, int64_t ldq, float* s, int64_t lds);
-/* 1x128 with power-of-two scales: s = smallest 2^e with 448*2^e >= amax (e >= -149; 1 if amax == 0) */
+/* 1x128 with power-of-two scales: s = smallest 2^e with 448*2^e >= amax (e >= -127, R26; 1 if amax == 0) */
 void oracle_quantize_act_1x128_pow2(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx,
                                     uint8_t* q, int64_t ldq, float* s, int64_t lds);
 void oracle_quantize_act_128x1(const void* x, int xdt, int64_t M, int64_t C, int64_t ldx,

@@ -15,6 +15,8 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FP8BS_LIB") or os.path.join(_PKG, "libfp8bs.so")   # FP8BS_LIB: A/B experiments
+# Test-only build of the same sources (-DFP8BS_TEST_HOOKS=1, build.py): adds fp8bs_internal_* hooks.
+TESTHOOKS_PATH = os.path.join(_PKG, "libfp8bs_testhooks.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "fp8bs.h")
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_ALIGN, ERR_UNSUPPORTED, ERR_DEVICE, ERR_CUDA = range(7)
@@ -22,6 +24,7 @@ BF16, FP32 = 0, 1
 FPROP, DGRAD, WGRAD = 0, 1, 2
 
 _lib = None
+_test_lib = None
 
 
 class Fp8bsError(RuntimeError):
@@ -34,66 +37,103 @@ def lib() -> ctypes.CDLL:
     """Load libfp8bs.so (raises if it was not built: there is no fallback path)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2412_19437_b200.build` "
-                              "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
-        i64, vp, i32, st = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int
-        L.fp8bs_abi_version.restype = ctypes.c_int
-        L.fp8bs_status_string.restype = ctypes.c_char_p
-        L.fp8bs_status_string.argtypes = [st]
-        L.fp8bs_last_error_detail.restype = ctypes.c_char_p
-        L.fp8bs_device_supported.restype = st
-        L.fp8bs_device_supported.argtypes = [i32]
-        L.fp8bs_quantize_act_1x128.restype = st
-        L.fp8bs_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
-        L.fp8bs_quantize_act_128x1.restype = st
-        L.fp8bs_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
-        L.fp8bs_quantize_weight_128x128.restype = st
-        if hasattr(L, "fp8bs_quantize_act_dual"):   # (older builds, loaded via FP8BS_LIB for A/B runs, lack it)
-            L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
-            L.fp8bs_quantize_act_dual.restype = st
-        L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
-        if hasattr(L, "fp8bs_requantize_1x128_to_128x1"):
-            L.fp8bs_requantize_1x128_to_128x1.restype = st
-            L.fp8bs_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, i32, vp]
-        if hasattr(L, "fp8bs_quantize_act_1x128_pow2"):
-            L.fp8bs_quantize_act_1x128_pow2.restype = st
-            L.fp8bs_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
-        for name in ("fp8bs_quantize_act_dual_pow2",):
-            if hasattr(L, name):
-                getattr(L, name).argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
-                getattr(L, name).restype = st
-        if hasattr(L, "fp8bs_quantize_weight_128x128_pow2"):
-            L.fp8bs_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
-            L.fp8bs_quantize_weight_128x128_pow2.restype = st
-        if hasattr(L, "fp8bs_grouped_gemm_mx"):
-            L.fp8bs_grouped_gemm_mx.restype = st
-            L.fp8bs_grouped_gemm_mx.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32,
-                                                i64, vp]
-        if hasattr(L, "fp8bs_gemm_mx"):
-            L.fp8bs_gemm_mx.restype = st
-            L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
-        L.fp8bs_gemm.restype = st
-        L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
-        L.fp8bs_grouped_gemm.restype = st
-        L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
-                                         vp, ctypes.c_size_t, vp]
-        if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
-            L.fp8bs_grouped_gemm_dgrad.restype = st
-            L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
-        if hasattr(L, "fp8bs_grouped_gemm_wgrad"):
-            L.fp8bs_padded_tokens.restype = i64
-            L.fp8bs_padded_tokens.argtypes = [ctypes.c_int32, vp]
-            L.fp8bs_quantize_act_128x1_grouped.restype = st
-            L.fp8bs_quantize_act_128x1_grouped.argtypes = [vp, i32, ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp]
-            L.fp8bs_grouped_gemm_wgrad.restype = st
-            L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
-                                                   vp, i64, i32, vp]
-        L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
-        L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
-        _lib = L
+        _lib = _load(LIB_PATH)
     return _lib
+
+
+def testhooks_lib() -> ctypes.CDLL:
+    """The test-only build (tests/ and tools/ only): the same kernels plus fp8bs_internal_* hooks."""
+    global _test_lib
+    if _test_lib is None:
+        _test_lib = _load(TESTHOOKS_PATH)
+        _test_lib.fp8bs_internal_set_gemm_variant.argtypes = [ctypes.c_int]
+        _test_lib.fp8bs_internal_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        _test_lib.fp8bs_internal_debug_timestamps.restype = ctypes.c_int
+    return _test_lib
+
+
+class forced_variant:
+    """Context manager for tests: route every binding call through the test-hooks build with the GEMM
+    tile variant forced (1: one CTA per 128-row tile, 2: CTA pair per 256-row tile)."""
+
+    def __init__(self, v: int):
+        self.v = v
+
+    def __enter__(self):
+        global _lib
+        self.saved = lib()
+        T = testhooks_lib()
+        T.fp8bs_internal_set_gemm_variant(self.v)
+        _lib = T
+        return self
+
+    def __exit__(self, *exc):
+        global _lib
+        _lib.fp8bs_internal_set_gemm_variant(0)
+        _lib = self.saved
+        return False
+
+
+def _load(path: str) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -m paper_2412_19437_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    i64, vp, i32, st = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+    L.fp8bs_abi_version.restype = ctypes.c_int
+    L.fp8bs_status_string.restype = ctypes.c_char_p
+    L.fp8bs_status_string.argtypes = [st]
+    L.fp8bs_last_error_detail.restype = ctypes.c_char_p
+    L.fp8bs_device_supported.restype = st
+    L.fp8bs_device_supported.argtypes = [i32]
+    L.fp8bs_quantize_act_1x128.restype = st
+    L.fp8bs_quantize_act_1x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+    L.fp8bs_quantize_act_128x1.restype = st
+    L.fp8bs_quantize_act_128x1.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+    L.fp8bs_quantize_weight_128x128.restype = st
+    if hasattr(L, "fp8bs_quantize_act_dual"):   # (older builds, loaded via FP8BS_LIB for A/B runs, lack it)
+        L.fp8bs_quantize_act_dual.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_quantize_act_dual.restype = st
+    L.fp8bs_quantize_weight_128x128.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+    if hasattr(L, "fp8bs_requantize_1x128_to_128x1"):
+        L.fp8bs_requantize_1x128_to_128x1.restype = st
+        L.fp8bs_requantize_1x128_to_128x1.argtypes = [vp, i64, vp, i64, i64, i64, vp, i64, vp, i64, i32, vp]
+    if hasattr(L, "fp8bs_quantize_act_1x128_pow2"):
+        L.fp8bs_quantize_act_1x128_pow2.restype = st
+        L.fp8bs_quantize_act_1x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp]
+    for name in ("fp8bs_quantize_act_dual_pow2",):
+        if hasattr(L, name):
+            getattr(L, name).argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+            getattr(L, name).restype = st
+    if hasattr(L, "fp8bs_quantize_weight_128x128_pow2"):
+        L.fp8bs_quantize_weight_128x128_pow2.argtypes = [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_quantize_weight_128x128_pow2.restype = st
+    if hasattr(L, "fp8bs_grouped_gemm_mx"):
+        L.fp8bs_grouped_gemm_mx.restype = st
+        L.fp8bs_grouped_gemm_mx.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32,
+                                            i64, vp]
+    if hasattr(L, "fp8bs_gemm_mx"):
+        L.fp8bs_gemm_mx.restype = st
+        L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
+    L.fp8bs_gemm.restype = st
+    L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
+    L.fp8bs_grouped_gemm.restype = st
+    L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
+                                     vp, ctypes.c_size_t, vp]
+    if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
+        L.fp8bs_grouped_gemm_dgrad.restype = st
+        L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
+    if hasattr(L, "fp8bs_grouped_gemm_wgrad"):
+        L.fp8bs_padded_tokens.restype = i64
+        L.fp8bs_padded_tokens.argtypes = [ctypes.c_int32, vp]
+        L.fp8bs_quantize_act_128x1_grouped.restype = st
+        L.fp8bs_quantize_act_128x1_grouped.argtypes = [vp, i32, ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp]
+        L.fp8bs_grouped_gemm_wgrad.restype = st
+        L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                               vp, i64, i32, vp]
+    L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
+    L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
+    return L
 
 
 def header_symbols() -> list[str]:

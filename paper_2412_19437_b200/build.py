@@ -18,6 +18,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfp8bs.so")
+# The same sources built with -DFP8BS_TEST_HOOKS=1: exports fp8bs_internal_* hooks (forced GEMM tile
+# variant, debug timestamps) for tests/ and tools/ only; the product library has none of them.
+TEST_LIB = os.path.join(PKG, "libfp8bs_testhooks.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -39,40 +42,54 @@ def deps():
         os.path.join(ROOT, "include", "fp8bs.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    objs = []
-    procs = []
+def _build_one(lib: str, defines: list[str], verbose: bool) -> list:
+    """Start the nvcc compiles of every source for `lib`; returns (lib, objs, procs)."""
+    tag = os.path.splitext(os.path.basename(lib))[0]
+    objs, procs = [], []
     for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src) + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = os.path.join(CSRC, f"{os.path.basename(src)}.{tag}.o")
+        cmd = [NVCC, *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
+    return [lib, objs, procs]
+
+
+def _link(lib: str, objs: list, procs: list, verbose: bool):
     failed = False
     for src, p in procs:
         out, _ = p.communicate()
         if p.returncode != 0 or verbose:
-            sys.stderr.write(f"--- {os.path.basename(src)}\n{out}")
+            sys.stderr.write(f"--- {os.path.basename(src)} ({os.path.basename(lib)})\n{out}")
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-lpthread", "-ldl", "-lrt"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
+
+
+def build(force: bool = False, verbose: bool = False, test_hooks: bool = True) -> str:
+    """Build libfp8bs.so (and, unless test_hooks=False, libfp8bs_testhooks.so) in parallel."""
+    jobs = []
+    if force or not up_to_date(LIB):
+        jobs.append(_build_one(LIB, [], verbose))
+    if test_hooks and (force or not up_to_date(TEST_LIB)):
+        jobs.append(_build_one(TEST_LIB, ["-DFP8BS_TEST_HOOKS=1"], verbose))
+    for lib, objs, procs in jobs:
+        _link(lib, objs, procs, verbose)
     return LIB
 
 

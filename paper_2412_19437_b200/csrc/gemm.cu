@@ -812,8 +812,11 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     return cudaPeekAtLastError();
 }
 
-int gemm_variant_override = 0;   // test hook (also FP8BS_GEMM_VARIANT): see launch_gemm
-static int g_env_variant = -1;   // FP8BS_GEMM_VARIANT (experiments only; read once)
+#if FP8BS_TEST_HOOKS
+// Test-only build (libfp8bs_testhooks.so): tests force the tile variant through an exported hook.
+// The product library has no such state: the variant follows from the problem shape alone.
+static int g_forced_variant = 0;
+#endif
 
 template <bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
@@ -828,11 +831,10 @@ static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** det
 
 // Variants: 1 = one CTA per 128 x 256 tile, 2 = CTA pair (cta_group::2) per 256 x 256 tile.
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    if (g_env_variant < 0) {
-        const char* e = getenv("FP8BS_GEMM_VARIANT");
-        g_env_variant = e ? atoi(e) : 0;
-    }
-    int v = g_env_variant ? g_env_variant : gemm_variant_override;
+    int v = 0;
+#if FP8BS_TEST_HOOKS
+    v = g_forced_variant;
+#endif
     if (v < 1 || v > 2) {
         // ~128-row experts / small M would waste half of a 256-row pair tile -> one CTA per tile
         if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 2 : 1;
@@ -843,7 +845,10 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
 
 }  // namespace fp8bs
 
-// Experiments only (not in include/fp8bs.h): copy the debug timestamps of the last GEMM launch.
+#if FP8BS_TEST_HOOKS
+// Test-only build (not in include/fp8bs.h, not in libfp8bs.so): copy the debug timestamps of the last
+// GEMM launch (experiment builds with FP8BS_GEMM_DEBUG_BITS & 16), and force the tile variant
+// (1: one CTA per 128-row tile, 2: CTA pair per 256-row tile, 0: by shape) for later launches.
 extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_timestamps(unsigned long long* host, int n) {
     if (!fp8bs::g_ts) return 0;
     if (n > fp8bs::kTsSlots * fp8bs::kTsN) n = fp8bs::kTsSlots * fp8bs::kTsN;
@@ -851,6 +856,5 @@ extern "C" __attribute__((visibility("default"))) int fp8bs_internal_debug_times
     cudaMemcpy(host, fp8bs::g_ts, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return n;
 }
-
-// Experiments only: set the GEMM debug bits / variant for subsequent launches in this process.
-extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_variant(int v) { fp8bs::g_env_variant = v; }
+extern "C" __attribute__((visibility("default"))) void fp8bs_internal_set_gemm_variant(int v) { fp8bs::g_forced_variant = v; }
+#endif

@@ -3,6 +3,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef FP8BS_TEST_HOOKS
+#define FP8BS_TEST_HOOKS 0   // 1 only in libfp8bs_testhooks.so (build.py): exported test hooks
+#endif
+
 namespace fp8bs {
 
 int num_sms();                                   // SM count of the current device (cached per device)

@@ -21,8 +21,9 @@ __device__ __forceinline__ float group_scale(float amax) {
 
 // Power-of-two scale of a group ("integral power of 2"; reading R23: rounded UP, as
 // SPEC S:374/S:417, from the EXACT quotient): the smallest s = 2^e with 448 * s >= amax, so no
-// element saturates; e >= -149 (the smallest subnormal; amax < 448 * 2^-149 then still fits); 1
-// when amax is 0; non-finite amax gives amax (like group_scale's amax / 448).
+// element saturates; e >= -127, the smallest UE8M0 value (reading R26: every pow2 scale is exact in
+// the MMA's block-scale format; amax < 448 * 2^-127 then still fits); 1 when amax is 0; non-finite
+// amax gives amax (like group_scale's amax / 448).
 __device__ __forceinline__ float group_scale_pow2(float amax) {
     // amax = m * 2^E, m in [1, 2): 448 * 2^e = 1.75 * 2^(e+8) >= amax first holds at e = E - 8 when
     // m <= 1.75 (mantissa field <= 0x600000), else at e = E - 7.  Integer ops only (the FP64
@@ -34,7 +35,7 @@ __device__ __forceinline__ float group_scale_pow2(float amax) {
     if ((b >> 23) == 0) { b = __float_as_uint(amax * 0x1p64f); bias = 64; }   // subnormal: exact rescale
     const int E = (int)(b >> 23) - 127 - bias;
     int e = E - 8 + ((b & 0x7FFFFFu) > 0x600000u ? 1 : 0);
-    if (e < -149) e = -149;
+    if (e < -127) e = -127;
     return e >= -126 ? __uint_as_float((uint32_t)(e + 127) << 23) : __uint_as_float(1u << (e + 149));
 }
 template <bool kPow2>

@@ -18,6 +18,19 @@ def test_library_loads_and_exports_header_symbols():
     assert fp.abi_version() == 1
 
 
+def test_product_library_exports_only_header_symbols():
+    """The product library exports exactly the header's functions: the fp8bs_internal_* test hooks
+    live only in the test build (libfp8bs_testhooks.so)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln and "fp8bs_" in ln}
+    assert exported == set(L.header_symbols())
+    hooks = subprocess.run(["nm", "-D", "--defined-only", L.TESTHOOKS_PATH], capture_output=True, text=True,
+                           check=True).stdout
+    assert "fp8bs_internal_set_gemm_variant" in hooks
+
+
 def test_status_strings():
     for st in range(7):
         s = fp.status_string(st)

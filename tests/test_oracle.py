@@ -473,12 +473,12 @@ def test_requantize_closed_form_is_a_transpose():
 
 # ------------------------------------------------------------ power-of-two scales ----
 def _pow2_scale_exact(amax: float) -> float:
-    """Independent reading R23 with exact rationals: the smallest 2^e (e >= -149) with 448 * 2^e >= amax."""
+    """Independent reading R23 with exact rationals: the smallest 2^e (e >= -127, R26) with 448 * 2^e >= amax."""
     from fractions import Fraction
     if amax == 0:
         return 1.0
     a = Fraction(amax)
-    e = -149
+    e = -127
     while Fraction(448) * Fraction(2) ** e < a:
         e += 1
     return float(Fraction(2) ** e)
@@ -560,3 +560,81 @@ def test_requantize_pow2_loses_nothing():
     normal = np.abs(before) >= sT_mk * 2.0 ** -6
     assert normal.mean() > 0.9
     assert np.array_equal(before[normal], after[normal])
+
+
+# ------------------------------------------------- input dtypes and non-finite inputs ----
+def _quant_all(x):
+    q, s = oracle.quantize_act_1x128(x)
+    qT, sT = oracle.quantize_act_128x1(x)
+    qw, sw, qwT = oracle.quantize_weight_128x128(x)
+    p, ps = oracle.quantize_act_1x128_pow2(x)
+    pT, psT = oracle.quantize_act_128x1(x, pow2=True)
+    return q, s, qT, sT, qw, sw, qwT, p, ps, pT, psT
+
+
+@pytest.mark.parametrize("kind", ["gauss", "outlier", "special", "nonfinite"])
+def test_bf16_input_path_equals_fp32_of_the_same_values(kind):
+    """The oracle's BF16 loader (oracle_bf16_to_float) is pinned to torch's BF16 -> FP32 conversion:
+    every quantizer gives bit-identical codes and scales on x_bf16 and on x_bf16.float()."""
+    M, K = 260, 300
+    gen = {"gauss": W.gaussian_act, "outlier": W.outlier_act, "special": W.special_values_act,
+           "nonfinite": W.nonfinite_act}[kind]
+    xb = gen(M, K, seed=21).to(torch.bfloat16)
+    for a, b in zip(_quant_all(xb), _quant_all(xb.float())):
+        if a.dtype == torch.float32:
+            a, b = a.view(torch.int32), b.view(torch.int32)
+        assert torch.equal(a, b)
+
+
+def naive_quant_groups_maxnum(x: np.ndarray, groups):
+    """naive_quant_groups with reading R6 spelled out: the group amax ignores NaN (maxNum; an all-NaN
+    group has amax 0, so s = 1); Inf elements give s = Inf; the quotient is IEEE float32 division
+    (finite / Inf = +-0, Inf / Inf = NaN); NaN encodes to 0x7F, +-Inf saturates."""
+    x = x.astype(np.float32)
+    q = np.zeros(x.shape, dtype=np.uint8)
+    scales = []
+    for idx in groups:
+        v = x[idx]
+        a = np.abs(v[~np.isnan(v)])
+        amax = np.float32(a.max()) if a.size else np.float32(0)
+        with np.errstate(invalid="ignore", over="ignore"):
+            s = np.float32(amax) / np.float32(448.0)
+            if s == 0:
+                s = np.float32(1.0)
+            q[idx] = brute_encode((v / s).astype(np.float32))
+        scales.append(s)
+    return q, scales
+
+
+def test_nonfinite_inputs_follow_reading_R6():
+    """NaN / +-Inf inputs (reading R6) through the 1x128, 128x1 and 128x128 quantizers ==
+    a naive numpy composition with maxNum amax, IEEE division and the brute-force encoder."""
+    M, K = 140, 260
+    x = W.nonfinite_act(M, K, seed=3)
+    xn = x.numpy()
+    rows = [np.ravel_multi_index((np.full(min(128, K - k0), m), np.arange(k0, min(K, k0 + 128))), (M, K))
+            for m in range(M) for k0 in range(0, K, 128)]
+    qn, sn = naive_quant_groups_maxnum(xn.reshape(-1), rows)
+    q, s = oracle.quantize_act_1x128(x)
+    assert np.array_equal(q.numpy().reshape(-1), qn)
+    assert np.array_equal(s.numpy().view(np.int32), np.array(sn, np.float32).reshape(M, -1).T.view(np.int32))
+    cols = [np.ravel_multi_index((np.arange(m0, min(M, m0 + 128)), np.full(min(128, M - m0), c)), (M, K))
+            for c in range(K) for m0 in range(0, M, 128)]
+    qn, sn = naive_quant_groups_maxnum(xn.reshape(-1), cols)
+    qT, sT = oracle.quantize_act_128x1(x)
+    assert np.array_equal(qT.numpy(), qn.reshape(M, K).T)
+    assert np.array_equal(sT.numpy().view(np.int32), np.array(sn, np.float32).reshape(K, -1).T.view(np.int32))
+    blocks = []
+    for n0 in range(0, M, 128):
+        for k0 in range(0, K, 128):
+            nn, kk = np.meshgrid(np.arange(n0, min(M, n0 + 128)), np.arange(k0, min(K, k0 + 128)), indexing="ij")
+            blocks.append(np.ravel_multi_index((nn.ravel(), kk.ravel()), (M, K)))
+    qn, sn = naive_quant_groups_maxnum(xn.reshape(-1), blocks)
+    qw, sw, _ = oracle.quantize_weight_128x128(x)
+    assert np.array_equal(qw.numpy().reshape(-1), qn)
+    assert np.array_equal(sw.numpy().reshape(-1).view(np.int32), np.array(sn, np.float32).view(np.int32))
+    # the special groups of the recipe: all-NaN -> s = 1 and codes 0x7F; Inf group -> s = Inf
+    assert float(s[0, 0]) == 1.0 and torch.all(q[0, :128] == 0x7F)
+    assert math.isinf(float(s[0, 1]))
+    inf = x[1, :128].isinf()
+    assert torch.all(q[1, :128][inf] == 0x7F) and torch.all((q[1, :128][~inf] & 0x7F) == 0)

@@ -35,14 +35,10 @@ def dev_scales(s):
 
 @pytest.fixture(params=[1, 2], ids=["cta1", "pair"])
 def variant(request):
-    """Force the GEMM tile variant (1: one CTA per 128x256 tile, 2: CTA pair per 256x256 tile)
-    through the library's experiment hook, so both paths are covered at every shape."""
-    import ctypes
-    L = fp.lib()
-    L.fp8bs_internal_set_gemm_variant.argtypes = [ctypes.c_int]
-    L.fp8bs_internal_set_gemm_variant(request.param)
-    yield request.param
-    L.fp8bs_internal_set_gemm_variant(0)
+    """Force the GEMM tile variant (1: one CTA per 128x256 tile, 2: CTA pair per 256x256 tile) through
+    the test-hooks build of the same sources, so both paths are covered at every shape."""
+    with fp.forced_variant(request.param):
+        yield request.param
 
 
 def assert_bits_equal(got: torch.Tensor, want: torch.Tensor, what: str):

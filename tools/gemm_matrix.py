@@ -41,8 +41,6 @@ def main():
     debugs = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "0,1").split(",")]
     only = sys.argv[3].split(",") if len(sys.argv) > 3 else None
     dev = "cuda"
-    lib = fp.lib()
-    lib.fp8bs_internal_set_gemm_variant.argtypes = [ctypes.c_int]
     T, IN, OUT = 4096, 7168, 18432
     cases = []
     for name, L, (M, N, K) in (("fprop", fp.FPROP, (T, OUT, IN)), ("dgrad", fp.DGRAD, (T, IN, OUT)),
@@ -85,14 +83,13 @@ def main():
         out4 = torch.empty(R4, N2, dtype=torch.bfloat16, device=dev)
         cases.append(("grouped_C4", 2.0 * R4 * N2 * K2, lambda: fp.grouped_gemm(o4, A4, sA4, B2, sB2, out=out4)))
     for v in variants:
-        lib.fp8bs_internal_set_gemm_variant(v)
-        for d in debugs:
-            for name, flop, fn in cases:
-                if only and name not in only:
-                    continue
-                ms = timeit(fn)
-                print(f"variant={v} debug={d:4d} {name:11s} {ms * 1e3:8.1f} us  {flop / ms / 1e9:7.0f} TFLOP/s", flush=True)
-    lib.fp8bs_internal_set_gemm_variant(0)
+        with fp.forced_variant(v):   # the test-hooks build of the same sources
+            for d in debugs:
+                for name, flop, fn in cases:
+                    if only and name not in only:
+                        continue
+                    ms = timeit(fn)
+                    print(f"variant={v} debug={d:4d} {name:11s} {ms * 1e3:8.1f} us  {flop / ms / 1e9:7.0f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":

@@ -33,10 +33,11 @@ def main():
     sB = {fp.FPROP: torch.rand(N // 128, K // 128, device=dev), fp.DGRAD: torch.rand(K // 128, N // 128, device=dev),
           fp.WGRAD: torch.rand(K // 128, N, device=dev)}[L]
     out = torch.empty(M, N, dtype=torch.float32 if L == fp.WGRAD else torch.bfloat16, device=dev)
-    for _ in range(3):
-        fp.gemm(L, A, sA, B, sB, out=out)
+    with fp.forced_variant(0):   # route through the test-hooks build (its timestamps are read below)
+        for _ in range(3):
+            fp.gemm(L, A, sA, B, sB, out=out)
     torch.cuda.synchronize()
-    lib = fp.lib()
+    lib = fp.testhooks_lib()   # built with -DFP8BS_TEST_HOOKS=1 (and the experiment's debug bits)
     buf = (ctypes.c_ulonglong * (12 * 512))()
     lib.fp8bs_internal_debug_timestamps(buf, 12 * 512)
     t = np.array(buf, dtype=np.int64).reshape(12, 512)

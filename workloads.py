@@ -152,3 +152,52 @@ def special_values_act(M: int, K: int, seed: int = 7) -> torch.Tensor:
         x[1, :128] = 0.0
         x[0, : min(K, 256)] = -0.0
     return x
+
+
+def nonfinite_act(M: int, K: int, seed: int = 8) -> torch.Tensor:
+    """FP32 activations with NaN and +-Inf elements (reading R6): N(0,1) with ~2% NaN,
+    ~1% +Inf and ~1% -Inf scattered, plus whole groups of special content where the shape allows:
+    row 0's first 128 channels all NaN; row 1's first 128 channels +Inf except one finite element;
+    row 2's first 128 channels a single -Inf among zeros; the first 128 tokens of channel 3 hold a
+    NaN and an Inf (a 128x1 group).  Cast to BF16 by the caller if wanted (NaN/Inf survive)."""
+    g = _gen(seed)
+    x = torch.randn(M, K, generator=g, dtype=torch.float32)
+    u = torch.rand(M, K, generator=g)
+    x = torch.where(u < 0.02, torch.full_like(x, float("nan")), x)
+    x = torch.where((u >= 0.02) & (u < 0.03), torch.full_like(x, float("inf")), x)
+    x = torch.where((u >= 0.03) & (u < 0.04), torch.full_like(x, float("-inf")), x)
+    w = min(K, 128)
+    if M >= 1:
+        x[0, :w] = float("nan")
+    if M >= 2:
+        x[1, :w] = float("inf")
+        x[1, 0] = 3.0
+    if M >= 3:
+        x[2, :w] = 0.0
+        x[2, w - 1] = float("-inf")
+    if K >= 4:
+        h = min(M, 128)
+        x[:h, 3] = torch.randn(h, generator=g)
+        x[0, 3] = float("nan")
+        if h > 1:
+            x[h - 1, 3] = float("inf")
+    return x
+
+
+def random_codes(R: int, C: int, seed: int) -> torch.Tensor:
+    """uint8 [R, C] uniformly random FINITE E4M3 codes: random bytes, with the two NaN patterns
+    (0x7F, 0xFF) moved to the neighbouring +-448 codes (0x7E, 0xFE).  Bookkeeping on bit patterns
+    only; used as GEMM operands at full size, where quantizing with the oracle would take minutes."""
+    n = R * C
+    words = torch.randint(-(2 ** 63), 2 ** 63 - 1, ((n + 7) // 8,), generator=_gen(seed), dtype=torch.int64)
+    c = words.view(torch.uint8)[:n].reshape(R, C).clone()
+    c[(c & 0x7F) == 0x7F] -= 1
+    return c
+
+
+def random_scales(*shape: int, seed: int, lo: float = 2.0 ** -12, hi: float = 2.0 ** -6) -> torch.Tensor:
+    """float32 positive scales log-uniform in [lo, hi) (the range of amax/448 for the init-std
+    weights of P:705 up to unit activations)."""
+    u = torch.rand(*shape, generator=_gen(seed), dtype=torch.float64)
+    return torch.exp(torch.log(torch.tensor(lo, dtype=torch.float64)) * (1 - u)
+                     + torch.log(torch.tensor(hi, dtype=torch.float64)) * u).to(torch.float32)
