@@ -329,7 +329,23 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             int it = 0, qh = 0;
             Tile tl;
             for (int t = cid; next_tile(t, tl); t += ncl) {
-                if (h >= tl.nh) { it += p.KB; continue; }
+                if (h >= tl.nh) {
+                    // This half lies past N (last column tile): no MMAs, but the issuer still walks
+                    // the ring in step and releases each stage with its own (empty) commit.  Jumping
+                    // ahead by KB instead let a later parity wait on full_bar pass one or more phases
+                    // early (an mbarrier parity wait only tells apart adjacent phases), so the next
+                    // tile's MMAs read stages still being filled.
+                    for (int kb = 0; kb < p.KB; ++kb, ++it) {
+                        const int s = it % C::kStages;
+                        mbar_wait(full_bar(s), (it / C::kStages) & 1);
+                        if (elect_one()) {
+                            if constexpr (kPair) mma_commit_pair(empty_bar(s), 3);
+                            else mma_commit(empty_bar(s));
+                        }
+                        __syncwarp();
+                    }
+                    continue;
+                }
                 for (int kb = 0; kb < p.KB; ++kb, ++it, ++qh) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
@@ -362,11 +378,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         if constexpr (kPair) mma_commit_pair(pfull_bar(pb), 3);
                         else mma_commit(pfull_bar(pb));
                         // release the smem stage once this half's MMAs have read it (the barrier
-                        // counts one commit per half; a one-half tile commits twice)
-                        for (int c = 0; c < (tl.nh == 1 ? 2 : 1); ++c) {
-                            if constexpr (kPair) mma_commit_pair(empty_bar(s), 3);
-                            else mma_commit(empty_bar(s));
-                        }
+                        // counts one commit per half; an inactive half commits without MMAs)
+                        if constexpr (kPair) mma_commit_pair(empty_bar(s), 3);
+                        else mma_commit(empty_bar(s));
                     }
                     __syncwarp();
                     if (h == 0) FP8BS_TS(2, it);

@@ -253,6 +253,23 @@ def test_gemm_closed_form_bitexact(layout, M, N, K, variant):
     assert_bits_equal(D, O.to(torch.float32), "closed-form GEMM")
 
 
+@pytest.mark.parametrize("layout", [fp.FPROP, fp.DGRAD, fp.WGRAD], ids=["fprop", "dgrad", "wgrad"])
+@pytest.mark.parametrize("N", [320, 576], ids=["n320", "n576"])
+def test_gemm_half_tiles_with_several_tiles_per_cta(layout, N, variant):
+    """Regression: a last column tile with one active N = 128 half (N % 256 in (0, 128]) inside a
+    persistent CTA's walk over SEVERAL tiles.  The inactive half's issuer used to jump KB stages
+    ahead and then pass a full-barrier parity wait a phase early (C3 kv-lora, N = 576, crashed).
+    8192 rows give 192 single-CTA tiles / 96 pair tiles: more than one per CTA (cluster)."""
+    M, K = 8192, 512
+    A = W.codes_small(M, K, seed=N)
+    B = W.codes_small(N, K, seed=N + 1)
+    sA = W.scales_pow2(K // 128, M, seed=5)
+    sB = W.scales_pow2(*scale_b_shape(layout, N, K), seed=6)
+    D = fp.gemm(layout, dev(A), dev(sA), dev(B), dev(sB), out_dtype=torch.float32)
+    O = oracle.gemm(layout, A, sA, B, sB)
+    assert_bits_equal(D, O.to(torch.float32), "closed-form GEMM, half tiles")
+
+
 def quantized_operands(layout, M, N, K, seed=0):
     """Operands as the Linear layer produces them (quantized by the ORACLE, so the GEMM parity
     does not depend on the GPU quantizers)."""
