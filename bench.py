@@ -1,22 +1,25 @@
 #!/usr/bin/env python
-"""bench.py — DeepSeek-V3 FP8 Linear training step on B200 (BASELINE.json configs[1]).
+"""bench.py — DeepSeek-V3 FP8 expert GEMM (BASELINE.json configs[4], the north_star target) on B200.
 
-One STEP = the whole hot path for a Linear W [out=18432, in=7168]
-over T=4096 tokens, synthetic seeded inputs (workloads.py):
-    quantize_act_dual(X)  (1x128 for Fprop + 128x1 for Wgrad, one read of X)
-    quantize_weight_128x128(W) (+ transposed copy for Dgrad)
-    Fprop  Y  = Xq  . Wq^T          (BF16 out)
-    quantize_act_dual(dY) (1x128 for Dgrad + 128x1 for Wgrad, one read of dY)
-    Dgrad  dX = dYq . WqT^T         (BF16 out)
-    Wgrad  dW = dYqT . XqT^T        (FP32 out)
-value = 3 * 2*T*in*out GEMM FLOP per step / device time (TFLOP/s), whole job over all ranks.
-Multi-GPU (torchrun): the dense step does not shard -> independent replicas, "scaling": "weak".
-`--workload ep` times the expert-parallel grouped GEMM (BASELINE configs[4]) instead.
+Headline (default `--workload c4`): the expert-parallel grouped expert GEMM of C4 — 256 routed
+experts (K = 7168 hidden, N = 2048 expert FFN dim), 65536 tokens x top-8 with skewed
+routing (524288 expert rows), experts sharded contiguously over the N ranks (ep.py).  One STEP on
+rank r is the FP8 forward of its share of the expert layer:
+    quantize_act_1x128(X[t0:t1])     the 1x128 cast of the rank's data-parallel token shard, the
+                                     cast the paper applies before dispatch (a-1, a-2)
+    grouped_gemm(offsets, A, sA, Bq, sB) -> BF16   Fprop over the FP8 rows its experts receive
+                                     (a-5..a-8; the rows are the exact gather of the same 1x128
+                                     codes — dispatch itself is out of scope)
+value = sum over ranks of 2 * R_r * N * K GEMM FLOP per step / max-over-ranks step time (TFLOP/s);
+the total problem is fixed ("scaling": "strong").  `roofline` is the grouped GEMM kernel's, from
+CUDA events around each launch inside the timed region.  The C1 dense FP8 Linear training step
+(quantizers + Fprop/Dgrad/Wgrad, BASELINE configs[1]) is timed after it on every rank and reported
+as the sub-object `c1_step` (per-kernel TFLOP/s and GB/s; replicas at N > 1).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload dense|ep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4|c1]
 
-`--impl reference` times the CPU oracle (oracle/, as it stands) on a bounded sample of the same
-workload on the host cores (rank 0 only).
+`--impl reference` times the CPU oracle (oracle/, as it stands) on a bounded sample of the same C4
+step on the host cores (rank 0 only; the other ranks exit without work).
 """
 from __future__ import annotations
 
@@ -37,9 +40,13 @@ import workloads as W  # noqa: E402
 
 METRIC = "FP8 block-scaled GEMM TFLOPS (% of B200 FP8 peak); quantizer HBM GB/s"
 T_TOK, D_IN, D_OUT = 4096, 7168, 18432
-# CPU sample of the same step (cpu_baseline / --impl reference): 128 tokens x all 7168 inputs x
-# the first CPU_OUT output channels.
+# CPU sample of the C1 step (its cpu_baseline): 128 tokens x all 7168 inputs x the first CPU_OUT outputs
 CPU_TOK, CPU_OUT = 128, 2048
+# CPU sample of the C4 step: every CPU_EXPERT_STRIDE-th expert, CPU_ROWS rows each
+CPU_EXPERT_STRIDE, CPU_ROWS = 16, 4
+# A timed region at least this long is "a kernel timed inside a long step": its tensor roofline takes
+# the measured SUSTAINED peak (MEASURED_PEAKS.json: 4 s back to back); shorter regions the burst one.
+SUSTAINED_REGION_S = 1.0
 
 
 def load_peaks():
@@ -50,6 +57,29 @@ def load_peaks():
                 "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "src": "measured"}
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+def fp8_peak(peaks, region_s: float):
+    """Dense FP8 peak = 2 x the measured BF16 peak (the guide's nominal FP8:BF16 ratio): sustained
+    for a timed region of >= SUSTAINED_REGION_S, burst otherwise.  Returns (peak, label)."""
+    sustained = region_s >= SUSTAINED_REGION_S
+    key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
+    return 2.0 * peaks[key], (f"{peaks['src']}: 2 x {key} of MEASURED_PEAKS.json "
+                              f"({'sustained' if sustained else 'burst'}: timed region {region_s:.3f} s "
+                              f"{'>=' if sustained else '<'} {SUSTAINED_REGION_S} s)")
+
+
+def committed_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+    for rnd in ("r02", "r01"):
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", rnd, "traffic.json")))
+        except Exception:
+            continue
+        v = tj.get("dram_bytes_per_launch", {}).get(kernel)
+        if v is not None:
+            return v, tj.get("source")
+    return None, None
 
 
 # ------------------------------------------------------------------------ clocks ----
@@ -170,37 +200,312 @@ class DenseStep:
             fn()
 
 
-def cpu_sample_step():
-    """The same step restricted to CPU_TOK tokens x CPU_OUT output channels, on the CPU oracle.
-    Returns (seconds, GEMM FLOP)."""
+# ------------------------------------------------------------------- timing helpers ----
+def timed_launches(launches, steps, warmup, world, dev):
+    """Run `warmup` untimed steps, then `steps` timed steps of the launch list [(name, fn), ...] on the
+    current stream with a CUDA event pair around each launch, bracketed by barrier + synchronize.
+    Returns (region ms on this rank, per-launch mean ms list, clock summary)."""
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        for _, fn in launches:
+            fn()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
+          for _ in range(steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        start.record(stream)
+        for k in range(steps):
+            for i, (_, fn) in enumerate(launches):
+                ev[k][i][0].record(stream)
+                fn()
+                ev[k][i][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    per = [statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(steps)) for i in range(len(launches))]
+    return start.elapsed_time(stop), per, clk.summary()
+
+
+# ------------------------------------------------------------------------ C1 step ----
+def time_c1(args, world, rank, dev, e2e=False):
+    """The C1 dense FP8 Linear training step (6 launches), replicas at N > 1 ("scaling": "weak")."""
+    peaks = load_peaks()
+    st = DenseStep(dev)
+    ms_local, per_ms, clocks = timed_launches([(n, fn) for n, fn, _, _ in st.launches], args.steps, args.warmup,
+                                              world, dev)
+    ms = max_over_ranks(ms_local, world, dev)
+    peak_t, peak_src = fp8_peak(peaks, ms_local * 1e-3)
+    per = {}
+    for (name, _, kind, amount), d in zip(st.launches, per_ms):
+        if kind == "tensor":
+            ach = amount / (d * 1e-3) / 1e12
+            per[name] = {"ms": d, "achieved": ach, "unit": "TFLOP/s", "peak": peak_t, "frac": ach / peak_t}
+        else:
+            ach = amount / (d * 1e-3) / 1e9
+            per[name] = {"ms": d, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]}
+    dom = max(per, key=lambda n: per[n]["ms"])
+    dk = next(l for l in st.launches if l[0] == dom)
+    traffic, traffic_src = committed_traffic(dom)
+    tensor = dk[2] == "tensor"
+    roof = {"kernel": dom, "bound": "tensor" if tensor else "hbm", "achieved": per[dom]["achieved"],
+            "peak": per[dom]["peak"], "unit": per[dom]["unit"], "frac": per[dom]["frac"],
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_src": traffic_src, "algorithmic": dk[3],
+            "peak_src": peak_src if tensor else f"{peaks['src']}: hbm_gbs of MEASURED_PEAKS.json",
+            "share_of_step": per[dom]["ms"] * args.steps / ms_local}
+    if tensor:
+        sus = 2.0 * peaks["bf16_tflops_sustained"]
+        roof["frac_vs_sustained_peak"] = per[dom]["achieved"] / sus
+    gemm_ms = sum(per[n]["ms"] for n in per if n.startswith("gemm"))
+    q_ms = sum(per[n]["ms"] for n in per if not n.startswith("gemm"))
+    q_bytes = sum(l[3] for l in st.launches if l[2] == "hbm")
+    res = {"workload": "C1 dense FP8 Linear training step (dual-quantize X, quantize W (+WqT), Fprop, dual-quantize dY, "
+                       "Dgrad, Wgrad), BASELINE configs[1]", "tokens": T_TOK, "in": D_IN, "out": D_OUT,
+           "parallelism": "replicas" if world > 1 else "single", "scaling": "weak",
+           "value": world * st.flops * args.steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "ms_per_step": ms / args.steps, "steps": args.steps, "warmup": args.warmup, "dtype": "e4m3",
+           "l2": "inputs larger than L2 (738 MB read per step: X, W, dY)",
+           "roofline": roof, "clocks": clocks, "gpu_launches": len(st.launches) * args.steps,
+           "gemm_tflops": st.flops / (gemm_ms * 1e-3) / 1e12,
+           "quantizer_gbs": q_bytes / (q_ms * 1e-3) / 1e9, "quantizer_frac_hbm": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+           "kernels": per}
+    if e2e:
+        res["e2e"] = time_c1_e2e(args, world, st, dev)
+    if args.pow2:
+        del st
+        res["pow2_recipe"] = time_pow2_recipe(args, world, dev)
+    return res
+
+
+def time_pow2_recipe(args, world, dev):
+    """Context, not the headline: the same C1 step on the power-of-two scale recipe (P:558, P:565;
+    pow2 dual / weight quantizers, UE8M0 block-scaled GEMM fp8bs_gemm_mx), timed like the C1 step."""
+    st = DenseStep(dev, pow2=True)
+    steps = min(args.steps, 50)
+    ms, per_ms, _ = timed_launches([(n, fn) for n, fn, _, _ in st.launches], steps, args.warmup, world, dev)
+    per = {name: {"ms": d, "achieved": amount / (d * 1e-3) / (1e12 if kind == "tensor" else 1e9),
+                  "unit": "TFLOP/s" if kind == "tensor" else "GB/s"}
+           for (name, _, kind, amount), d in zip(st.launches, per_ms)}
+    return {"value": st.flops * steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
+            "steps": steps, "recipe": "power-of-two scales (P:558, P:565): fp8bs_quantize_act_dual_pow2, "
+            "fp8bs_quantize_weight_128x128_pow2, fp8bs_gemm_mx (UE8M0 block scaling, no promotion step)",
+            "kernels": per}
+
+
+def pipelined_e2e(n, warmup, world, dev, h_in, d_sets, h_out_sets, run_compute):
+    """Steps pipelined over two device buffer sets and three streams (H2D, compute, D2H): every step
+    copies its inputs from pinned host memory (h_in: list of host tensors, one set) into its device
+    set, runs the kernels, and copies its outputs back into pinned host memory (alternating sets).
+    d_sets[b] = (inputs list, outputs list).  Timed on the device from the first H2D to the last D2H.
+    Returns max-over-ranks ms for n steps."""
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+
+    def run(nsteps, timed):
+        h2d_done, comp_done, d2h_done = {}, {}, {}
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(nsteps):
+            b = k % 2
+            d_in, d_out = d_sets[b]
+            with torch.cuda.stream(s_in):
+                if k >= 2:
+                    s_in.wait_event(comp_done[k - 2])          # inputs of set b consumed
+                if k == 0 and timed:
+                    t0.record(s_in)
+                for d, h in zip(d_in, h_in):
+                    d.copy_(h, non_blocking=True)
+                h2d_done[k] = ev()
+                h2d_done[k].record(s_in)
+            comp.wait_event(h2d_done[k])
+            if k >= 2:
+                comp.wait_event(d2h_done[k - 2])               # outputs of set b copied out
+            run_compute(b)
+            comp_done[k] = ev()
+            comp_done[k].record(comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[k])
+                for h, d in zip(h_out_sets[b], d_out):
+                    h.copy_(d, non_blocking=True)
+                d2h_done[k] = ev()
+                d2h_done[k].record(s_out)
+        if timed:
+            t1.record(s_out)
+        torch.cuda.synchronize()
+        return t0, t1
+
+    run(max(2, warmup), False)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0, t1 = run(n, True)
+    barrier(world)
+    return max_over_ranks(t0.elapsed_time(t1), world, dev)
+
+
+def time_c1_e2e(args, world, st, dev):
+    """C1 step through the public API with host buffers (X, W, dY in; Y, dX, dW out)."""
+    n = max(4, args.steps // 4)
+    h_in = [st.h_x.pin_memory(), st.h_w.pin_memory(), st.h_dy.pin_memory()]
+    outs0 = [st.y, st.dx, st.dw]
+    sets = [([st.x, st.w, st.dy], outs0),
+            ([torch.empty_like(t) for t in (st.x, st.w, st.dy)], [torch.empty_like(t) for t in outs0])]
+    h_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in outs0] for _ in range(2)]
+
+    def compute(b):
+        (st.x, st.w, st.dy), (st.y, st.dx, st.dw) = sets[b]
+        st.run()
+
+    ms = pipelined_e2e(n, args.warmup, world, dev, h_in, sets, h_out, compute)
+    (st.x, st.w, st.dy), (st.y, st.dx, st.dw) = sets[0]
+    return {"value": world * st.flops * n / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": n,
+            "h2d_bytes_per_step": st.h2d_bytes, "d2h_bytes_per_step": st.d2h_bytes, "ms_per_step": ms / n,
+            "pipelined": "2 buffer sets; H2D, compute and D2H streams overlap across steps"}
+
+
+# ------------------------------------------------------------------------ C4 step ----
+def c4_config(world):
+    return {"workload": "C4 expert-parallel grouped expert GEMM (BASELINE configs[4]): 256 routed experts (K=7168, "
+                        "N=2048) sharded contiguously over ranks, 65536 tokens x top-8 skewed routing (alpha 0.5, seed 3) "
+                        "= 524288 expert rows; step = 1x128 quantize of the rank's token shard + grouped Fprop (BF16 out)",
+            "experts": 256, "hidden": 7168, "expert_ffn": 2048, "tokens": 65536, "top_k": 8, "global_batch": 65536,
+            "parallelism": f"ep{world}",
+            "l2": "inputs larger than L2 (3.76 GB of FP8 rows + 3.76 GB of FP8 expert weights per step at N=1)"}
+
+
+def time_c4(args, world, rank, dev):
+    from paper_2412_19437_b200 import ep
+    peaks = load_peaks()
+    cfg = ep.EPConfig()
+    routes = ep.routes_for(cfg)
+    pb = ep.build_rank_problem(cfg, world, rank, dev, routes, keep_tokens=True)
+    torch.cuda.synchronize()
+    launches = [("quant_act_1x128(X shard)", lambda: ep.quantize_tokens(pb)), ("grouped_gemm_fprop", lambda: ep.run_rank(pb))]
+    ms_local, per_ms, clocks = timed_launches(launches, args.steps, args.warmup, world, dev)
+    ms = max_over_ranks(ms_local, world, dev)
+    K, N = cfg.hidden, cfg.inter
+    R = pb.A.shape[0]
+    rows = gather_ints([R], world, dev)
+    ms_ranks = gather_floats([ms_local / args.steps], world, dev)
+    total_flops = sum(2.0 * r * N * K for r in rows)
+    Tl = pb.t1 - pb.t0
+    q_bytes = Tl * K * 2 + Tl * K + 4 * Tl * (K // 128)          # BF16 in, codes + scales out
+    q_ms, g_ms = per_ms
+    g_ach = pb.flops / (g_ms * 1e-3) / 1e12
+    peak_t, peak_src = fp8_peak(peaks, ms_local * 1e-3)
+    traffic, traffic_src = committed_traffic("grouped_gemm_fprop")
+    alg_bytes = R * K + (pb.e1 - pb.e0) * N * K + 4 * R * (K // 128) + 2 * R * N
+    roof = {"kernel": "grouped_gemm_fprop (k_gemm_bs grouped)", "bound": "tensor", "achieved": g_ach, "peak": peak_t,
+            "unit": "TFLOP/s", "frac": g_ach / peak_t, "peak_src": peak_src,
+            "frac_vs_sustained_peak": g_ach / (2.0 * peaks["bf16_tflops_sustained"]),
+            "algorithmic": pb.flops, "algorithmic_unit": "FLOP per launch (2 * R * N * K)",
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_src": traffic_src, "algorithmic_bytes": alg_bytes,
+            "share_of_step": g_ms * args.steps / ms_local}
+    kernels = {"quant_act_1x128(X shard)": {"ms": q_ms, "achieved": q_bytes / (q_ms * 1e-3) / 1e9, "unit": "GB/s",
+                                            "peak": peaks["hbm_gbs"], "frac": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                            "bytes": q_bytes},
+               "grouped_gemm_fprop": {"ms": g_ms, "achieved": g_ach, "unit": "TFLOP/s", "peak": peak_t, "frac": g_ach / peak_t,
+                                      "flop": pb.flops}}
+    ep_block = {"rows_per_rank": rows, "experts_per_rank": [ep.shard_range(cfg.experts, world, r)[1] - ep.shard_range(cfg.experts, world, r)[0]
+                                                            for r in range(world)],
+                "ms_per_step_per_rank": ms_ranks, "imbalance_max_over_mean": ep.imbalance(rows),
+                "scaling_bound_from_imbalance": 1.0 / ep.imbalance(rows),
+                "collective": "none in the timed path; NCCL all_gather of outputs for verification only"}
+    result = {"metric": METRIC, "value": total_flops * args.steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+              "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "e4m3",
+              "data": "synthetic (seeded Gaussian activations, N(0, 0.006^2) expert weights, skewed top-8 routing)",
+              "config": c4_config(world), "roofline": roof, "clocks": clocks, "gpu_launches": len(launches) * args.steps,
+              "kernels": kernels, "ep": ep_block}
+    # verification, outside the timed region
+    if args.verify:
+        if world > 1:
+            ok = ep.gathered_equals_G1(pb, cfg, world, rank, dev, routes)
+            ep_block["bitwise_equal_to_G1"] = ok
+            ep_block["verify"] = "NCCL all_gather of every rank's output rows; rank 0 recomputes G=1 on its GPU"
+        else:
+            ep_block["split_bitwise_equal_to_G1_on_one_gpu"] = ep.split_equals_G1_on_one_gpu(pb, cfg)
+            ep_block["verify"] = "G=2/4/8 contiguous expert shards as separate launches on one GPU vs the G=1 launch"
+    if args.e2e:
+        result["e2e"] = time_c4_e2e(args, world, pb, dev, rows, N, K)
+    return result, pb
+
+
+def time_c4_e2e(args, world, pb, dev, rows, N, K):
+    """The C4 step through the public API with host buffers: every step uploads the rank's BF16 token
+    shard and its FP8 expert rows + scales from pinned host memory, runs the 2 launches, and downloads
+    the BF16 expert outputs (the expert weights stay resident, as model parameters do)."""
+    from paper_2412_19437_b200 import ep
+    n = max(3, min(8, args.steps // 4))
+    h_in = [pb.x.cpu().pin_memory(), pb.A.cpu().pin_memory(), pb.sA.cpu().pin_memory()]
+    h_out = [[torch.empty(pb.out.shape, dtype=pb.out.dtype).pin_memory()] for _ in range(2)]
+    d0 = ([pb.x, pb.A, pb.sA], [pb.out])
+    sA1 = torch.empty(pb.sA.shape[0], (pb.sA.shape[1] + 3) // 4 * 4 if pb.sA.shape[1] else 4, dtype=torch.float32,
+                      device=dev)[:, :pb.sA.shape[1]]
+    d1 = ([torch.empty_like(pb.x), torch.empty_like(pb.A), sA1], [torch.empty_like(pb.out)])
+    sets = [d0, d1]
+    saved = (pb.x, pb.A, pb.sA, pb.out)
+
+    def compute(b):
+        (pb.x, pb.A, pb.sA), (pb.out,) = sets[b]
+        ep.quantize_tokens(pb)
+        ep.run_rank(pb)
+
+    ms = pipelined_e2e(n, 2, world, dev, h_in, sets, h_out, compute)
+    pb.x, pb.A, pb.sA, pb.out = saved
+    total = sum(2.0 * r * N * K for r in rows)
+    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    return {"value": total * n / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": n, "ms_per_step": ms / n,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": pb.out.numel() * 2,
+            "pipelined": "2 device buffer sets; H2D, compute and D2H streams overlap across steps (PCIe-bound)"}
+
+
+# ------------------------------------------------------------------- CPU oracle ----
+def c4_cpu_sample():
+    """The C4 step on the CPU oracle, restricted to CPU_ROWS rows of every CPU_EXPERT_STRIDE-th expert
+    (16 experts x 4 rows x N=2048 x K=7168): 1x128 quantization of those rows' tokens and the grouped
+    FP64 oracle GEMM.  Expert weights (N(0, 0.006^2), CPU generator) are quantized by the oracle outside
+    the timing, as the GPU path holds its quantized weights.  Returns (seconds, GEMM FLOP, description)."""
     import oracle
-    x = W.gaussian_act(T_TOK, D_IN, seed=0)[:CPU_TOK].contiguous()
-    w = W.master_weight(CPU_OUT, D_IN, seed=1)
-    dy = W.grad_out(CPU_TOK, CPU_OUT, seed=2)
+    from paper_2412_19437_b200 import ep
+    cfg = ep.EPConfig()
+    if not hasattr(c4_cpu_sample, "cache"):
+        experts = list(range(0, cfg.experts, CPU_EXPERT_STRIDE))
+        Bq, sB = [], []
+        for e in experts:
+            w = W.master_weight(cfg.inter, cfg.hidden, seed=cfg.seed + 1000 + e)
+            q, s, _ = oracle.quantize_weight_128x128(w, want_t=False)
+            Bq.append(q)
+            sB.append(s)
+        x = W.gaussian_act(len(experts) * CPU_ROWS, cfg.hidden, seed=0)
+        off = torch.arange(0, len(experts) + 1, dtype=torch.int64) * CPU_ROWS
+        c4_cpu_sample.cache = (x, off, torch.stack(Bq), torch.stack(sB), len(experts))
+    x, off, Bq, sB, ne = c4_cpu_sample.cache
     t0 = time.perf_counter()
-    qx, sx = oracle.quantize_act_1x128(x)
-    qw, sw, qwT = oracle.quantize_weight_128x128(w)
-    oracle.gemm(oracle.FPROP, qx, sx, qw, sw)
-    qdy, sdy = oracle.quantize_act_1x128(dy)
-    oracle.gemm(oracle.DGRAD, qdy, sdy, qwT, sw)
-    qdyT, sdyT = oracle.quantize_act_128x1(dy)
-    qxT, sxT = oracle.quantize_act_128x1(x)
-    oracle.gemm(oracle.WGRAD, qdyT, sdyT, qxT, sxT)
-    return time.perf_counter() - t0, 3 * 2.0 * CPU_TOK * D_IN * CPU_OUT
+    q, s = oracle.quantize_act_1x128(x)
+    oracle.grouped_gemm(off, q, s, Bq, sB)
+    dt = time.perf_counter() - t0
+    return dt, 2.0 * x.shape[0] * cfg.inter * cfg.hidden, (
+        f"C4 step restricted to {CPU_ROWS} rows of each of {ne} experts (every {CPU_EXPERT_STRIDE}th): 1x128 quantize of "
+        f"those {x.shape[0]} token rows + FP64 grouped oracle GEMM (N=2048, K=7168)")
 
 
 def cpu_baseline_block(min_seconds=10.0):
-    """Time the oracle on repeated samples until at least min_seconds of CPU work."""
+    """Time the oracle on repeated C4 samples until at least min_seconds of CPU work."""
     import oracle
-    dt, fl = 0.0, 0.0
+    c4_cpu_sample()   # build the cached sample (weights quantized by the oracle) outside the timing
+    dt, fl, n = 0.0, 0.0, 0
+    desc = ""
     while dt < min_seconds:
-        d, f = cpu_sample_step()
+        d, f, desc = c4_cpu_sample()
         dt += d
         fl += f
+        n += 1
     return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"the C1 step restricted to {CPU_TOK} tokens x {D_IN} in x {CPU_OUT} out channels "
-                      f"(all 8 stages: 3 quantizers + weight quantizer + Fprop/Dgrad/Wgrad FP64 oracle GEMMs), "
-                      f"{fl / 1e9:.2f} GFLOP in {dt:.2f} s"}
+            "sample": f"{desc}; {n} repetitions, {fl / 1e9:.2f} GFLOP in {dt:.2f} s"}
 
 
 # ------------------------------------------------------------------------ main ----
@@ -233,247 +538,90 @@ def max_over_ranks(v: float, world: int, dev) -> float:
     return float(t.item())
 
 
+def gather_ints(v, world, dev):
+    if world == 1:
+        return list(v)
+    import torch.distributed as dist
+    t = torch.tensor(v, dtype=torch.int64, device=dev)
+    lst = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(lst, t)
+    return [int(x) for l in lst for x in l.tolist()]
+
+
+def gather_floats(v, world, dev):
+    if world == 1:
+        return list(v)
+    import torch.distributed as dist
+    t = torch.tensor(v, dtype=torch.float64, device=dev)
+    lst = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(lst, t)
+    return [float(x) for l in lst for x in l.tolist()]
+
+
 def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle as it stands, on a bounded sample of the C4 step, rank 0 only."""
     if rank != 0:
         return
     # torchrun exports OMP_NUM_THREADS=1; rank 0 runs the oracle alone on the box's host cores
     torch.set_num_threads(len(os.sched_getaffinity(0)))   # the process's OpenMP pool (shared with the oracle)
+    c4_cpu_sample()   # sample setup (weights quantized by the oracle) outside the timing
     for _ in range(args.warmup):
-        cpu_sample_step()
-    t, f = 0.0, 0.0
+        c4_cpu_sample()
+    t, f, desc = 0.0, 0.0, ""
     for _ in range(args.steps):
-        d, fl = cpu_sample_step()
+        d, fl, desc = c4_cpu_sample()
         t += d
         f += fl
     import oracle
     v = f / t / 1e12
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_block(args, world),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": c4_config(world) if args.workload == "c4" else {"workload": "C1"},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
-                             "sample": f"each step: the C1 step restricted to {CPU_TOK} tokens x {D_IN} in x "
-                                       f"{CPU_OUT} out channels on the CPU oracle"},
+                             "sample": f"each step: {desc}"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def config_block(args, world):
-    if args.workload == "ep":
-        return {"workload": "C4 expert-parallel grouped GEMM: 256 experts (K=7168, N=2048) sharded over ranks, "
-                            "65536 tokens x top-8, skewed load", "parallelism": f"ep{world}",
-                "l2": "inputs larger than L2"}
-    return {"workload": "C1 dense FP8 Linear training step (quantize + Fprop/Dgrad/Wgrad), BASELINE configs[1]",
-            "tokens": T_TOK, "in": D_IN, "out": D_OUT, "global_batch": T_TOK * world,
-            "parallelism": "replicas" if world > 1 else "single",
-            "l2": "inputs larger than L2 (738 MB read per step: X, W, dY)"}
-
-
-def time_dense(args, world, rank, dev):
-    peaks = load_peaks()
-    st = DenseStep(dev)
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        st.run()
-    torch.cuda.synchronize()
-    nL = len(st.launches)
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nL)]
-          for _ in range(args.steps)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        start.record(stream)
-        for k in range(args.steps):
-            for i, (_, fn, _, _) in enumerate(st.launches):
-                ev[k][i][0].record(stream)
-                fn()
-                ev[k][i][1].record(stream)
-        stop.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_local = start.elapsed_time(stop)
-    ms = max_over_ranks(ms_local, world, dev)
-    per = {}
-    for i, (name, _, kind, amount) in enumerate(st.launches):
-        d = statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
-        if kind == "tensor":
-            ach = amount / (d * 1e-3) / 1e12
-            peak = 2.0 * peaks["bf16_tflops"]       # FP8 = 2x BF16 (guide's nominal ratio)
-            per[name] = {"ms": d, "achieved": ach, "unit": "TFLOP/s", "peak": peak, "frac": ach / peak}
-        else:
-            ach = amount / (d * 1e-3) / 1e9
-            per[name] = {"ms": d, "achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]}
-    dom = max(per, key=lambda n: per[n]["ms"])
-    dk = next(l for l in st.launches if l[0] == dom)
-    traffic, traffic_src = None, None
-    try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
-        traffic = tj["dram_bytes_per_launch"].get(dom)
-        traffic_src = tj["source"]
-    except Exception:
-        pass
-    # Tensor-bound roofline kernel: the guide's sustained peak applies to a kernel timed inside a long
-    # step; the timed region is taken as "long" when the clock sampler saw the power cap.  The burst
-    # fraction is reported next to it.
-    clocks = clk.summary()
-    sustained = dk[2] == "tensor" and "sw_power_cap" in clocks.get("reasons", [])
-    peak_t = 2.0 * (peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"])
-    roof_peak = peak_t if dk[2] == "tensor" else per[dom]["peak"]
-    roof = {"kernel": dom, "bound": "tensor" if dk[2] == "tensor" else "hbm", "achieved": per[dom]["achieved"],
-            "peak": roof_peak, "unit": per[dom]["unit"], "frac": per[dom]["achieved"] / roof_peak, "traffic": traffic,
-            "traffic_unit": "bytes per launch", "traffic_src": traffic_src,
-            "peak_src": f"{peaks['src']}: " + (("2 x bf16_tflops_sustained (timed region power-capped: sw_power_cap)" if sustained
-                                                else "2 x bf16_tflops (burst)") + " of MEASURED_PEAKS.json" if dk[2] == "tensor"
-                                               else "hbm_gbs of MEASURED_PEAKS.json"),
-            "frac_vs_burst_peak": per[dom]["frac"],
-            "share_of_step": per[dom]["ms"] * args.steps / (ms_local)}
-    value = world * st.flops * args.steps / (ms * 1e-3) / 1e12
-    gemm_ms = sum(per[n]["ms"] for n in per if n.startswith("gemm"))
-    q_ms = sum(per[n]["ms"] for n in per if not n.startswith("gemm"))
-    q_bytes = sum(l[3] for l in st.launches if l[2] == "hbm")
-    result = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "e4m3", "data": "synthetic", "config": config_block(args, world),
-        "roofline": roof, "clocks": clocks, "gpu_launches": nL * args.steps,
-        "gemm_tflops": st.flops / (gemm_ms * 1e-3) / 1e12, "gemm_frac_fp8_peak_4500": st.flops / (gemm_ms * 1e-3) / 4.5e15,
-        "quantizer_gbs": q_bytes / (q_ms * 1e-3) / 1e9, "quantizer_frac_hbm": q_bytes / (q_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-        "kernels": per,
-    }
-    if args.e2e:
-        result["e2e"] = time_e2e(args, world, st, dev)
-    if args.pow2:
-        del st
-        result["pow2_recipe"] = time_pow2_recipe(args, dev)
-    return result
-
-
-def time_pow2_recipe(args, dev):
-    """Context line, not the headline: the same C1 step on the power-of-two scale recipe (P:558, P:565;
-    pow2 dual / weight quantizers, UE8M0 block-scaled GEMM fp8bs_gemm_mx), timed like the main step
-    on this rank's stream after it (per-launch CUDA events, inputs larger than L2)."""
-    st = DenseStep(dev, pow2=True)
-    stream = torch.cuda.current_stream()
-    steps = min(args.steps, 50)
-    for _ in range(args.warmup):
-        st.run()
-    torch.cuda.synchronize()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in st.launches]
-          for _ in range(steps)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for k in range(steps):
-        for i, (_, fn, _, _) in enumerate(st.launches):
-            ev[k][i][0].record(stream)
-            fn()
-            ev[k][i][1].record(stream)
-    stop.record(stream)
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    per = {}
-    for i, (name, _, kind, amount) in enumerate(st.launches):
-        d = statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(steps))
-        per[name] = {"ms": d, "achieved": amount / (d * 1e-3) / (1e12 if kind == "tensor" else 1e9),
-                     "unit": "TFLOP/s" if kind == "tensor" else "GB/s"}
-    return {"value": st.flops * steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
-            "steps": steps, "recipe": "power-of-two scales (P:558, P:565): fp8bs_quantize_act_dual_pow2, "
-            "fp8bs_quantize_weight_128x128_pow2, fp8bs_gemm_mx (UE8M0 block scaling, no promotion step)",
-            "kernels": per}
-
-
-def time_e2e(args, world, st, dev):
-    """Same metric through the public API with host buffers: every step copies X, W, dY from pinned
-    host memory to the device, runs the 6 launches, and copies Y, dX, dW back to pinned host memory.
-    Steps are pipelined over two buffer sets and three streams (H2D, compute, D2H): the copies of
-    step k+1's inputs and step k-1's outputs overlap step k's kernels, and PCIe runs both directions
-    at once.  Timed from the first H2D to the last D2H on the device."""
-    n = max(4, args.steps // 4)
-    hx = [st.h_x.pin_memory() for _ in range(2)]
-    hw = [st.h_w.pin_memory() for _ in range(2)]
-    hdy = [st.h_dy.pin_memory() for _ in range(2)]
-    hy = [torch.empty(st.y.shape, dtype=st.y.dtype).pin_memory() for _ in range(2)]
-    hdx = [torch.empty(st.dx.shape, dtype=st.dx.dtype).pin_memory() for _ in range(2)]
-    hdw = [torch.empty(st.dw.shape, dtype=st.dw.dtype).pin_memory() for _ in range(2)]
-    sets = [(st.x, st.w, st.dy, st.y, st.dx, st.dw),
-            tuple(torch.empty_like(t) for t in (st.x, st.w, st.dy, st.y, st.dx, st.dw))]
-    comp = torch.cuda.current_stream()
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
-
-    def run(nsteps, timed):
-        h2d_done, comp_done, d2h_done = {}, {}, {}
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for k in range(nsteps):
-            b = k % 2
-            x, w, dy, y, dx, dw = sets[b]
-            with torch.cuda.stream(s_in):
-                if k >= 2:
-                    s_in.wait_event(comp_done[k - 2])          # inputs of set b consumed
-                if k == 0 and timed:
-                    t0.record(s_in)
-                x.copy_(hx[b], non_blocking=True)
-                w.copy_(hw[b], non_blocking=True)
-                dy.copy_(hdy[b], non_blocking=True)
-                h2d_done[k] = ev()
-                h2d_done[k].record(s_in)
-            comp.wait_event(h2d_done[k])
-            if k >= 2:
-                comp.wait_event(d2h_done[k - 2])               # outputs of set b copied out
-            st.x, st.w, st.dy, st.y, st.dx, st.dw = x, w, dy, y, dx, dw
-            st.run()
-            comp_done[k] = ev()
-            comp_done[k].record(comp)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(comp_done[k])
-                hy[b].copy_(y, non_blocking=True)
-                hdx[b].copy_(dx, non_blocking=True)
-                hdw[b].copy_(dw, non_blocking=True)
-                d2h_done[k] = ev()
-                d2h_done[k].record(s_out)
-        if timed:
-            t1.record(s_out)
-        torch.cuda.synchronize()
-        return t0, t1
-
-    run(max(2, args.warmup // 2), False)
-    barrier(world)
-    torch.cuda.synchronize()
-    t0, t1 = run(n, True)
-    barrier(world)
-    st.x, st.w, st.dy, st.y, st.dx, st.dw = sets[0]
-    ms = max_over_ranks(t0.elapsed_time(t1), world, dev)
-    return {"value": world * st.flops * n / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": n,
-            "h2d_bytes_per_step": st.h2d_bytes, "d2h_bytes_per_step": st.d2h_bytes,
-            "ms_per_step": ms / n, "pipelined": "2 buffer sets; H2D, compute and D2H streams overlap across steps"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="dense", choices=["dense", "ep"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c1"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--no-pow2", dest="pow2", action="store_false")
+    ap.add_argument("--no-c1", dest="c1", action="store_false")
+    ap.add_argument("--no-verify", dest="verify", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    if args.workload == "ep":
-        from paper_2412_19437_b200 import ep
-        result = ep.bench(args, world, rank, dev, barrier, max_over_ranks, ClockSampler, load_peaks)
-        result["config"] = config_block(args, world)
-        result["metric"] = METRIC
+    if args.workload == "c4":
+        result, pb = time_c4(args, world, rank, dev)
+        del pb
+        torch.cuda.empty_cache()
+        if args.c1:
+            result["c1_step"] = time_c1(args, world, rank, dev)
     else:
-        result = time_dense(args, world, rank, dev)
+        c1 = time_c1(args, world, rank, dev, e2e=args.e2e)
+        result = {"metric": METRIC, "value": c1.pop("value"), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                  "warmup": args.warmup, "ms_per_step": c1.pop("ms_per_step"), "higher_is_better": True,
+                  "scaling": c1.pop("scaling"), "vs_baseline": None, "dtype": "e4m3", "data": "synthetic",
+                  "config": {"workload": c1.pop("workload"), "tokens": T_TOK, "in": D_IN, "out": D_OUT,
+                             "global_batch": T_TOK * world, "parallelism": c1.pop("parallelism"), "l2": c1.pop("l2")},
+                  **c1}
     if rank == 0:
         if args.cpu and world == 1:
             result["cpu_baseline"] = cpu_baseline_block()

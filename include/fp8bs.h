@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FP8BS_ABI_VERSION 1
+#define FP8BS_ABI_VERSION 2   /* 2: fp8bs_grouped_gemm{,_dgrad} require their workspace */
 
 #if defined(__GNUC__)
 #define FP8BS_API __attribute__((visibility("default")))
@@ -205,7 +205,12 @@ FP8BS_API fp8bs_status fp8bs_gemm_mx(fp8bs_layout layout, int64_t M, int64_t N, 
  * B   : [G, N, K] uint8 codes, contiguous (expert stride N*K);
  * sB  : [G, ceil(N/128), K/128] FP32, contiguous (FPROP 128x128 scales per expert).
  * D   : [total_M, N], BF16 or FP32, ldd >= N.
- * workspace : unused in ABI v1 (may be NULL); fp8bs_grouped_gemm_workspace_size returns 0.
+ * workspace : DEVICE scratch, 16-byte aligned, of at least fp8bs_grouped_gemm_workspace_size(G,
+ *           total_M, N, K) bytes (16 bytes per 128 x 256 output tile + 16; ~0.3 MB at C4), owned by
+ *           the caller and not read by the host.  The call first launches a one-CTA scheduler that
+ *           writes this launch's tile table there (the (expert, m-tile, n-tile) order, from offsets on
+ *           the device), then the GEMM, both on `stream`: the workspace must not be reused by
+ *           another call until this one has run.  NULL or too small: FP8BS_ERR_INVALID_ARG.
  * 1 <= G <= 1024.  K a multiple of 128.  Same alignment rules as fp8bs_gemm. */
 FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
@@ -214,7 +219,7 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
 /* ---- grouped_gemm_mx: the MoE expert Fprop on UE8M0 block scaling (NEXT-1) -----
- * fp8bs_grouped_gemm's arguments, layouts and validation (no workspace), with fp8bs_gemm_mx's
+ * fp8bs_grouped_gemm's arguments, layouts and validation (it takes no workspace), with fp8bs_gemm_mx's
  * precondition: every sA and sB value is an exact power of two in [2^-127, 2^127] (e.g. from
  * fp8bs_quantize_act_dual_pow2 / fp8bs_quantize_weight_128x128_pow2).  No promotion step. */
 FP8BS_API fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,

@@ -251,11 +251,17 @@ def quantize_act_128x1_grouped(x: torch.Tensor, offsets, qT: torch.Tensor | None
     _cuda2d(x, "x")
     off = _host_offsets(offsets)
     G, C = off.numel() - 1, x.shape[1]
+    if int(off[0]) != 0 or int(off[-1]) != x.shape[0] or bool((off[1:] < off[:-1]).any()):
+        raise ValueError(f"offsets must rise from 0 to x.shape[0] = {x.shape[0]} (got {off[0]}..{off[-1]})")
     Mp = padded_tokens(off)
     if qT is None:
         qT = torch.empty(C, Mp, dtype=torch.uint8, device=x.device)
     if sT is None:
         sT = torch.empty(Mp // 128, _pad4(C), dtype=torch.float32, device=x.device)[:, :C]
+    if qT.dtype != torch.uint8 or qT.shape[0] < C or qT.shape[1] < Mp:
+        raise ValueError(f"qT must be uint8 of at least [{C}, {Mp}]")
+    if sT.dtype != torch.float32 or sT.shape[0] < Mp // 128 or sT.shape[1] < C:
+        raise ValueError(f"sT must be float32 of at least [{Mp // 128}, {C}]")
     _check(lib().fp8bs_quantize_act_128x1_grouped(_p(x), _dt(x), G, off.data_ptr(), C, x.stride(0), _p(qT),
                                                   qT.stride(0), _p(sT), sT.stride(0), _stream(x)),
            "fp8bs_quantize_act_128x1_grouped")
@@ -357,10 +363,11 @@ def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: to
 
 def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
                  out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, layout: int = FPROP,
-                 mx: bool = False):
+                 mx: bool = False, workspace: torch.Tensor | None = None):
     """MoE expert GEMM over token rows grouped by expert: offsets int64 [G+1] (device), A [R,K],
     sA [K/128, R], B [G,N,K].  FPROP: sB [G,ceil(N/128),K/128] (fp8bs_grouped_gemm).  DGRAD: B holds
-    each expert's WqT [in, out], sB [G,K/128,ceil(N/128)] each expert's sW (fp8bs_grouped_gemm_dgrad)."""
+    each expert's WqT [in, out], sB [G,K/128,ceil(N/128)] each expert's sW (fp8bs_grouped_gemm_dgrad).
+    workspace: device uint8 of fp8bs_grouped_gemm_workspace_size bytes (allocated per call if None)."""
     _cuda2d(A, "A")
     _cuda2d(sA, "sA")
     if offsets.dtype != torch.int64 or not offsets.is_cuda:
@@ -381,6 +388,9 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
         return out
     fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
                 else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))
+    if workspace is None:   # the tile table (torch's caching allocator makes this cheap per call)
+        wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K))
+        workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
     _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
-              _p(out), _dt(out), out.stride(0), None, 0, _stream(A)), name)
+              _p(out), _dt(out), out.stride(0), _p(workspace), workspace.numel(), _stream(A)), name)
     return out

@@ -278,22 +278,24 @@ static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N,
 }
 
 size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K) {
-    (void)G; (void)total_M; (void)N; (void)K;
-    return 0;
+    (void)K;
+    if (G < 1 || total_M < 0 || N < 0) return 0;
+    return grouped_workspace_bytes(G, total_M, N);
 }
 
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
-                                        int64_t ldd, fp8bs_stream_t stream, int mx = 0);
+                                        int64_t ldd, fp8bs_stream_t stream, int mx = 0, void* workspace = nullptr,
+                                        size_t workspace_bytes = 0);
 
 fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                 const uint8_t* B, const float* sB,
                                 void* D, fp8bs_dtype ddt, int64_t ldd,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
-    (void)workspace; (void)workspace_bytes;
-    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream);
+    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 0,
+                               workspace, workspace_bytes);
 }
 
 fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
@@ -308,20 +310,28 @@ fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int
                                       const uint8_t* B, const float* sB,
                                       void* D, fp8bs_dtype ddt, int64_t ldd,
                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
-    (void)workspace; (void)workspace_bytes;
-    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream);
+    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 0,
+                               workspace, workspace_bytes);
 }
 
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
-                                        int64_t ldd, fp8bs_stream_t stream, int mx) {
+                                        int64_t ldd, fp8bs_stream_t stream, int mx, void* workspace,
+                                        size_t workspace_bytes) {
     if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
     if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
     fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
     if (c != FP8BS_OK) return c;
     if (total_M == 0 || N == 0) return ok();
     if (K % 16) return fail(FP8BS_ERR_ALIGN, "K must be a multiple of 16");
+    if (!mx) {
+        const size_t need = grouped_workspace_bytes(G, total_M, N);
+        if (!workspace || workspace_bytes < need)
+            return fail(FP8BS_ERR_INVALID_ARG, "workspace of %zu bytes needed (fp8bs_grouped_gemm_workspace_size), got %zu%s",
+                        need, workspace_bytes, workspace ? "" : " (NULL)");
+        if (!aligned16(workspace)) return fail(FP8BS_ERR_ALIGN, "workspace must be 16-byte aligned");
+    }
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
     GemmArgs a{};
@@ -329,7 +339,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = K; a.sB = sB;
     a.ldsB = layout == FP8BS_DGRAD ? (N + 127) / 128 : K / 128;
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
-    a.grouped = 1; a.G = G; a.offsets = offsets;
+    a.grouped = 1; a.G = G; a.offsets = offsets; a.workspace = workspace;
     const char* detail = nullptr;
     cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);

@@ -44,7 +44,7 @@ namespace fp8bs {
 constexpr int BM = 128, BK = 128;     // rows per CTA, K-block (= N_C)
 constexpr int BN = 256;               // tile columns, issued as two N = 128 MMA halves
 constexpr int HN = 128;               // columns per half (= one TMEM slot, = one weight block)
-constexpr int kMaxGroups = 1024;
+constexpr int kMaxGroups = 1024;   // experts per grouped launch (one scheduler thread each)
 
 #ifndef FP8BS_NPW
 #define FP8BS_NPW 8
@@ -94,10 +94,14 @@ struct Cfg {
     static constexpr int REG_LAUNCH = NPW == 8 ? 168 : 96;  // 65536 / THREADS rounded down to 8
     static constexpr int REG_OTHER = 24, REG_PROMO = NPW == 8 ? 240 : 112;   // setmaxnreg split of the launch pool
     static_assert((REG_LAUNCH - REG_OTHER) * 128 >= (REG_PROMO - REG_LAUNCH) * 32 * NPW, "setmaxnreg.inc would wait forever: the CTA's pool is fixed at launch");
-    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NSLOT;
+    // grouped: a 4-entry ring of dynamically claimed tile indices (full / empty barrier per entry)
+    static constexpr int kTQ = 4;
+    // warps that take each claimed tile from the ring: leader CTA w1, w2 (issuers), w3, the NPW
+    // promotion warps; the peer CTA w0 (its A/B producer), w3, the promotion warps
+    static constexpr int TQ_CONSUMERS = kPair ? (3 + NPW) + (2 + NPW) : 3 + NPW;
+    static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NSLOT + 2 * kTQ;
     static constexpr int OFF_EPI = kStages * STAGE;
     static constexpr int SMEM_DENSE = 1024 + OFF_EPI + NPW * EPI_WARP_BYTES;
-    static constexpr int SMEM_GROUPED = SMEM_DENSE + 2 * (kMaxGroups + 1) * 4;
 };
 
 struct KParams {
@@ -108,6 +112,7 @@ struct KParams {
     int NB;                       // ceil(N/128)
     void* D; int64_t ldd; int accumulate;
     int G; const int64_t* offsets;
+    void* tiles;                  // grouped: TileTable in the caller's workspace
     int gm;                       // raster band width (dense): tiles of the resident operand per band
     int rast_n;                   // 1: n-fastest (B resident, A streamed), 0: m-fastest
     int debug;                    // unused (debug bits are compile-time: FP8BS_GEMM_DEBUG_BITS): 1 skip promotion math,
@@ -129,6 +134,9 @@ constexpr int kTsSlots = 12;
 #endif
 #ifndef FP8BS_WG_NOSB
 #define FP8BS_WG_NOSB 0
+#endif
+#ifndef FP8BS_STATIC_SCHED
+#define FP8BS_STATIC_SCHED 0   // experiments: 1 = grouped tiles on the static schedule too (A/B builds)
 #endif
 #ifndef FP8BS_GEMM_DEBUG_BITS
 #define FP8BS_GEMM_DEBUG_BITS 0
@@ -159,26 +167,82 @@ __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl
     return true;
 }
 
-// cum[e] = number of tiles of experts < e; off[e] = first row of expert e.
-template <int ROWS>
-__device__ __forceinline__ bool get_tile_grouped(const KParams& p, const int* cum, const int* off, int t, Tile& tl) {
-    if (t >= cum[p.G]) return false;
-    int lo = 0, hi = p.G;                       // find e: cum[e] <= t < cum[e+1]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (cum[mid] <= t) lo = mid; else hi = mid;
-    }
-    const int e = lo;
-    const int seg = off[e + 1] - off[e];
-    const int mt = (seg + ROWS - 1) / ROWS;
-    const int local = t - cum[e];
-    // per expert, keep the smaller operand L2-resident: an expert with more rows than N walks its
-    // n-tiles fastest (its A rows are read once, B_e stays in L2); small experts walk m fastest
-    const bool nfast = seg > p.N;
-    const int m = nfast ? local / p.num_n : local % mt, n = nfast ? local % p.num_n : local / mt;
-    tl.row0 = off[e] + m * ROWS; tl.row_end = off[e + 1]; tl.n0 = n * BN; tl.e = e;
-    tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
+// Grouped (MoE) tile table, written by k_grouped_schedule into the caller's workspace before the GEMM
+// runs (same stream, PDL): tiles[t] = {first row of the cluster tile, (rows of its expert left in the
+// tile, capped at 2 x rows) << 22 | (expert & 63) << 16 | n-tile, expert >> 6, 0}; ntiles = number of
+// entries (n-tiles < 65536, experts <= 1024).  Every role decodes tile t with one 16-byte L2 load, so the
+// GEMM kernel itself holds no per-expert state: the in-kernel prefix scan it replaced made ptxas
+// spill promotion accumulators.
+struct TileTable { int ntiles; int next; int pad[2]; int4 t[1]; };   // next: the dynamic claim counter
+
+__device__ __forceinline__ bool get_tile_table(const TileTable* tt, int N, int t, Tile& tl) {
+    // the count and the entry are re-read per tile (L2 hits) rather than held in registers
+    if (t >= __ldcg(&tt->ntiles)) return false;
+    const int2 v = __ldcg(reinterpret_cast<const int2*>(&tt->t[t]));   // L2 only: written by the previous grid
+    tl.row0 = v.x;
+    tl.row_end = v.x + (int)((uint32_t)v.y >> 22);     // rows of the expert left in the tile (<= 512)
+    tl.n0 = (v.y & 0xFFFF) * BN;
+    tl.e = (v.y >> 16) & 0x3F;                         // low 6 bits of the expert; the rest in .z
+    tl.e |= __ldcg(reinterpret_cast<const int*>(&tt->t[t]) + 2) << 6;
+    tl.nh = (N - tl.n0 > HN) ? 2 : 1;
     return true;
+}
+
+// One CTA of 1024 threads (G <= 1024): thread e counts expert e's tiles, ceil(M_e/rows) x num_n, a
+// block scan places them expert by expert, then all threads write the entries (tile t's expert by
+// binary search over the scanned starts).  Inside an expert the smaller operand stays L2-resident:
+// more rows than N walks the n-tiles fastest (A rows read once, B_e resident), fewer walks m fastest.
+#ifndef FP8BS_GROUPED_ORDER
+#define FP8BS_GROUPED_ORDER 0   // experiments: 1 always m-fastest, 2 always n-fastest
+#endif
+__global__ void __launch_bounds__(1024) k_grouped_schedule(const int64_t* __restrict__ offsets, int G, int rows,
+                                                           int num_n, int N, TileTable* tt) {
+    griddep_wait();
+    griddep_launch_dependents();
+    __shared__ int warp_sum[32];
+    __shared__ int start[kMaxGroups + 1];      // first tile of expert e; start[G] = total
+    __shared__ int row0[kMaxGroups + 1];
+    const int e = threadIdx.x, lane = e & 31, w = e >> 5;
+    int64_t a = 0, b = 0;
+    if (e < G) { a = offsets[e]; b = offsets[e + 1]; }
+    const int seg = b > a ? (int)(b - a) : 0;
+    const int cnt = ((seg + rows - 1) / rows) * num_n;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_sum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int v = warp_sum[lane], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += u;
+        }
+        warp_sum[lane] = x - v;                            // exclusive prefix of the warp sums
+    }
+    __syncthreads();
+    if (e < G) { start[e] = warp_sum[w] + incl - cnt; row0[e] = (int)a; }
+    if (e == G - 1) { start[G] = warp_sum[w] + incl; row0[G] = (int)b; tt->ntiles = start[G]; tt->next = 0; }
+    __syncthreads();
+    const int total = start[G];
+    for (int t = e; t < total; t += blockDim.x) {
+        int lo = 0, hi = G;                                // expert x: start[x] <= t < start[x + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (start[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int x = lo, l = t - start[x];
+        const int sg = row0[x + 1] - row0[x], mt = (sg + rows - 1) / rows;
+        const bool nfast = FP8BS_GROUPED_ORDER == 1 ? false : FP8BS_GROUPED_ORDER == 2 ? true : sg > N;
+        const int m = nfast ? l / num_n : l % mt, n = nfast ? l % num_n : l / mt;
+        const int r0 = row0[x] + m * rows;
+        const int left = min(row0[x + 1] - r0, 2 * rows);  // only < rows (a crossing tile) matters
+        tt->t[t] = make_int4(r0, (left << 22) | ((x & 0x3F) << 16) | n, x >> 6, 0);
+    }
 }
 
 template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
@@ -198,6 +262,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         uint8_t scale[C::kSStages * C::SSTAGE];
         uint64_t bar[C::NBAR];
         uint32_t tmem;
+        int tq[C::kTQ];            // grouped: claimed tile indices
     };
     __shared__ StaticSmem s_static;
     uint8_t* s_scale = s_static.scale;
@@ -214,10 +279,10 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     auto sempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + C::kSStages + s); };
     auto pfull_bar  = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + b); };
     auto pempty_bar = [&](int b) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + C::NSLOT + b); };
+    auto tqfull_bar  = [&](int q) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + 2 * C::NSLOT + q); };
+    auto tqempty_bar = [&](int q) { return bar0 + 8u * (2 * C::kStages + 2 * C::kSStages + 2 * C::NSLOT + C::kTQ + q); };
     uint32_t* tmem_slot = &s_static.tmem;
     uint8_t* s_epi = smem + C::OFF_EPI;                // epilogue staging (1024-aligned, dynamic)
-    int* cum = reinterpret_cast<int*>(smem + C::OFF_EPI + C::NPW * C::EPI_WARP_BYTES);
-    int* off = cum + (kMaxGroups + 1);
 
     // warp index broadcast from lane 0 so the compiler knows role branches are warp-uniform
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -228,6 +293,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 2); }
         for (int s = 0; s < C::kSStages; ++s) { mbar_init(sfull_bar(s), 1); mbar_init(sempty_bar(s), C::NPW); }
         for (int b = 0; b < C::NSLOT; ++b) { mbar_init(pfull_bar(b), 1); mbar_init(pempty_bar(b), (C::NPW / 2) * C::CS); }
+        for (int q = 0; q < C::kTQ; ++q) { mbar_init(tqfull_bar(q), 1); mbar_init(tqempty_bar(q), C::TQ_CONSUMERS); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -238,36 +304,6 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if constexpr (kPair) tmem_alloc_pair<C::TMEM_COLS>(smem_u32(tmem_slot));
         else tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_slot));
     }
-    if constexpr (kGrouped) {
-        if (warp == 4) {
-            // tile prefix over experts: cum[e+1] = cum[e] + ceil(M_e/ROWS) * num_n
-            const int G = p.G;
-            const int per = (G + 31) / 32;
-            const int e0 = lane * per, e1 = min(G, e0 + per);
-            int local = 0;
-            for (int e = e0; e < e1; ++e) {
-                const int64_t a = p.offsets[e], b = p.offsets[e + 1];
-                const int seg = b > a ? (int)(b - a) : 0;
-                off[e] = (int)a;
-                local += ((seg + C::ROWS - 1) / C::ROWS) * p.num_n;
-            }
-            int incl = local;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            int run = incl - local;
-            for (int e = e0; e < e1; ++e) {
-                cum[e] = run;
-                const int a = off[e];
-                const int64_t b = p.offsets[e + 1];
-                const int seg = b > a ? (int)(b - a) : 0;
-                run += ((seg + C::ROWS - 1) / C::ROWS) * p.num_n;
-            }
-            if (lane == 31) { cum[G] = incl; off[G] = (int)p.offsets[G]; }
-        }
-    }
     tc_fence_before();
     __syncthreads();
     if constexpr (kPair) cluster_sync();        // peer barriers initialised before any remote arrive / TMA
@@ -275,8 +311,61 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint32_t tmem_base = *tmem_slot;
 
     auto next_tile = [&](int t, Tile& tl) -> bool {
-        if constexpr (kGrouped) return get_tile_grouped<C::ROWS>(p, cum, off, t, tl);
+        if constexpr (kGrouped) return get_tile_table(reinterpret_cast<const TileTable*>(p.tiles), p.N, t, tl);
         else return get_tile_dense<C::ROWS>(p, t, tl);
+    };
+
+    // Tile order.  Dense: static, cluster c takes tiles c, c + ncl, ...  Grouped: dynamic — the
+    // leader's producer thread claims the next tile index with an atomic on the workspace counter
+    // and hands it to every role of both CTAs through the tq ring, so the tiles in flight at any time
+    // are consecutive in the table (a static schedule let clusters drift apart over the ~220 tiles
+    // each runs at C4 and lose the L2 sharing of A rows between the n-tiles of an m-tile: DRAM read
+    // 4.5x the operands).  The claimer runs one tile ahead so the atomic's latency is off the path.
+    TileTable* ttw = reinterpret_cast<TileTable*>(p.tiles);
+    auto tq_publish = [&](int j) -> int {            // leader w0, one lane: claim tile #j of this cluster
+        const int q = j % C::kTQ;
+        mbar_wait(tqempty_bar(q), ((j / C::kTQ) & 1) ^ 1);
+        const int t = atomicAdd(&ttw->next, 1);
+        const uint32_t a = smem_u32(&s_static.tq[q]);
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(t) : "memory");
+        mbar_arrive(tqfull_bar(q));
+        if constexpr (kPair) {
+            st_shared_cluster_u32(mapa_shared(a, 1), (uint32_t)t);
+            mbar_arrive_release_cluster(mapa_shared(tqfull_bar(q), 1));
+        }
+        return t;
+    };
+    auto tq_take = [&](int j) -> int {               // every other role, whole warp: tile #j
+        // addresses rebuilt from an opaque base at each call: hoisted out of the tile loop they
+        // would stay live across the K loop and push the promotion warps' accumulators into spills
+        const int q = j % C::kTQ;
+        const uint32_t b = opaque_u32(bar0) + 8u * (2 * C::kStages + 2 * C::kSStages + 2 * C::NSLOT + q);
+        mbar_wait_acquire_cluster(b, (j / C::kTQ) & 1);
+        const int t = (int)lds_u32(opaque_u32(sring) + (uint32_t)offsetof(StaticSmem, tq) + 4u * q);
+        __syncwarp();
+        if (elect_one()) {
+            const uint32_t e = b + 8u * C::kTQ;
+            if (kPair && cluster_ctarank() != 0) mbar_arrive_release_cluster(e & kPeerBitMask);
+            else mbar_arrive(e);
+        }
+        __syncwarp();
+        return t;
+    };
+    int t_next = 0;                                  // claimer: tile #j+1, claimed ahead
+    // the leader's producer warp (lane 0 claims, the warp gets the index)
+    auto tile_index_claim = [&](int j) -> int {
+        if constexpr (!kGrouped || FP8BS_STATIC_SCHED) return cid + j * ncl;
+        int t = 0;
+        if (lane == 0) {
+            t = j == 0 ? tq_publish(0) : t_next;
+            if (t < __ldcg(&ttw->ntiles)) t_next = tq_publish(j + 1);
+        }
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    // every other role
+    auto tile_index = [&](int j) -> int {
+        if constexpr (!kGrouped || FP8BS_STATIC_SCHED) return cid + j * ncl;
+        return tq_take(j);
     };
 
     if (warp < 4) {
@@ -289,7 +378,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // ---------------- TMA producer: A and the two B halves (this CTA's rows) ----------------
             int it = 0;
             Tile tl;
-            for (int t = cid; next_tile(t, tl); t += ncl) {
+            auto tix = [&](int j) { return rank == 0 ? tile_index_claim(j) : tile_index(j); };
+            for (int j = 0, t = tix(0); next_tile(t, tl); t = tix(++j)) {
                 const int arow = tl.row0 + (int)rank * BM;
                 const int brow = tl.n0 + (int)rank * C::BH_ROWS;
                 for (int kb = 0; kb < p.KB; ++kb, ++it) {
@@ -328,7 +418,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, HN);
             int it = 0, qh = 0;
             Tile tl;
-            for (int t = cid; next_tile(t, tl); t += ncl) {
+            for (int j = 0, t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
                 if (h >= tl.nh) {
                     // This half lies past N (last column tile): no MMAs, but the issuer still walks
                     // the ring in step and releases each stage with its own (empty) commit.  Jumping
@@ -392,7 +482,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             int sit = 0;
             if ((kDbg & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
-            for (int t = cid; next_tile(t, tl); t += ncl) {
+            for (int j = 0, t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
                 const float* sbp = p.sB;
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
                 const int arow = tl.row0 + (int)rank * BM;
@@ -444,7 +534,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint32_t sb_off = C::SA_BYTES + 4u * (kWgrad ? h * HN + gg * NC : h);
         int sit = 0, qh = 0;                            // K-block, slot uses of this half
         Tile tl;
-        for (int t = cid; next_tile(t, tl); t += ncl) {
+        // every tile advances sit by exactly KB, so the tile's sequence number is sit / KB (one
+        // register fewer than a counter: the accumulators are at the edge of the 240-register budget)
+        for (int t = tile_index(0); next_tile(t, tl); t = tile_index(sit / p.KB)) {
             const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
             const bool active = h < tl.nh;
             if (!active) {
@@ -590,7 +682,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             bool unrolled = false;
             // dense Fprop/Dgrad only: in the Wgrad and grouped kernels the unrolled body makes ptxas
             // spill loop state into local memory (measured: Wgrad -7%, grouped C4 -20%)
-            if constexpr (!kWgrad && !kGrouped) unrolled = p.KB % C::kSStages == 0;
+            if constexpr (!kWgrad) unrolled = p.KB % C::kSStages == 0;
             if (unrolled) {
                 // K-blocks in groups of kSStages (8): the scale stage is the index in the group, the TMEM
                 // slot alternates 2h, 2h + 1 and its phase flips every 2 K-blocks (sit and qh are
@@ -626,62 +718,52 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             } else if (active && rows_here > 0 && !(kDbg & 1024)) {
                 constexpr int ESZ = kOutF32 ? 4 : 2;
                 constexpr int CW = 128 / ESZ;                   // columns per 128-byte chunk
-                if (!kGrouped || rows_here >= 32) {
-                    const uint32_t ebuf0 = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
+                // every warp stages its chunk the same way (one code path over acc); only the store
+                // differs: a whole 32-row block goes out as one TMA store, the rows of a grouped warp
+                // that crosses its expert's end are copied out of the staging buffer by the lanes
+                const bool full = !kGrouped || rows_here >= 32;
+                const uint32_t ebuf0 = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
 #pragma unroll
-                    for (int c = 0; c < NC / CW; ++c) {
-                        const uint32_t ebuf = ebuf0 + (c % C::EPI_BUFS) * (32 * 128);
-                        // the store that last used this buffer has read it
-                        if (lane == 0) bulk_wait_group_read<C::EPI_BUFS - 1>();
-                        __syncwarp();
+                for (int c = 0; c < NC / CW; ++c) {
+                    const uint32_t ebuf = ebuf0 + (c % C::EPI_BUFS) * (32 * 128);
+                    // the store that last used this buffer has read it
+                    if (lane == 0) bulk_wait_group_read<C::EPI_BUFS - 1>();
+                    __syncwarp();
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {                   // 16-byte units of this lane's row
-                            uint32_t w[4];
-                            if constexpr (kOutF32) {
+                    for (int u = 0; u < 8; ++u) {                   // 16-byte units of this lane's row
+                        uint32_t w[4];
+                        if constexpr (kOutF32) {
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(acc[c * CW + 4 * u + k]);
-                            } else {
+                            for (int k = 0; k < 4; ++k) w[k] = __float_as_uint(acc[c * CW + 4 * u + k]);
+                        } else {
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[c * CW + 8 * u + 2 * k], acc[c * CW + 8 * u + 2 * k + 1]);
-                                    w[k] = *reinterpret_cast<uint32_t*>(&b2);
-                                }
+                            for (int k = 0; k < 4; ++k) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[c * CW + 8 * u + 2 * k], acc[c * CW + 8 * u + 2 * k + 1]);
+                                w[k] = *reinterpret_cast<uint32_t*>(&b2);
                             }
-                            sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                         }
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            const int col = tl.n0 + h * HN + gg * NC + c * CW;
-                            if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, grow0);
-                            else tma_store_2d(&tmD, ebuf, col, grow0);
-                            bulk_commit_group();
-                        }
+                        sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
-                } else if (row < tl.row_end - arow) {
-                    const int grow = arow + row;
-                    const int col0 = tl.n0 + h * HN + gg * NC;
-                    if constexpr (kOutF32) {
-                        float* drow = reinterpret_cast<float*>(p.D) + (int64_t)grow * p.ldd + col0;
-#pragma unroll
-                        for (int i = 0; i < NC / 4; ++i) {
-                            if (col0 + 4 * i < p.N)
-                                *reinterpret_cast<float4*>(drow + 4 * i) = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-                        }
-                    } else {
-                        __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.D) + (int64_t)grow * p.ldd + col0;
-#pragma unroll
-                        for (int i = 0; i < NC / 8; ++i) {
-                            if (col0 + 8 * i < p.N) {
-                                uint32_t w[4];
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k], acc[8 * i + 2 * k + 1]);
-                                    w[k] = *reinterpret_cast<uint32_t*>(&b2);
-                                }
-                                *reinterpret_cast<uint4*>(drow + 8 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+                    const int col = tl.n0 + h * HN + gg * NC + c * CW;
+                    if (kGrouped && !full) {
+                        __syncwarp();
+                        for (int i = lane; i < rows_here * 8; i += 32) {
+                            const int r = i >> 3, u = i & 7;
+                            if (col + u * (16 / ESZ) < p.N) {
+                                const uint4 v = lds_u32x4(ebuf + r * 128 + ((u ^ (r & 7)) << 4));
+                                uint8_t* dst = reinterpret_cast<uint8_t*>(p.D) + ((int64_t)(grow0 + r) * p.ldd + col) * ESZ + u * 16;
+                                *reinterpret_cast<uint4*>(dst) = v;
                             }
                         }
+                        __syncwarp();                               // buffer reads done before its reuse
+                        continue;
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, grow0);
+                        else tma_store_2d(&tmD, ebuf, col, grow0);
+                        bulk_commit_group();
                     }
                 }
             }
@@ -776,7 +858,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else if (a.layout == 0) { p.sb_nb_stride = a.ldsB; p.sb_kb_stride = 1; p.sb_expert_stride = 0; }
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
-    p.G = a.G; p.offsets = a.offsets;
+    p.G = a.G; p.offsets = a.offsets; p.tiles = a.workspace;
     {
         // keep the smaller operand resident; band it to ~48 MB of L2 when it is larger than that
         p.rast_n = a.M > a.N ? 1 : 0;
@@ -799,7 +881,13 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     const int64_t max_clusters = num_sms() / C::CS;
     int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
     if (clusters < 1) clusters = 1;
-    const int smem = kGrouped ? C::SMEM_GROUPED : C::SMEM_DENSE;
+    const int smem = C::SMEM_DENSE;
+    if (kGrouped) {
+        // the tile table for this launch (k_grouped_schedule), then the GEMM; both PDL
+        cudaError_t e = launch_pdl(k_grouped_schedule, dim3(1), dim3(kMaxGroups), 0, st, a.offsets, a.G, C::ROWS,
+                                   p.num_n, p.N, reinterpret_cast<TileTable*>(a.workspace));
+        if (e != cudaSuccess) return e;
+    }
     auto kern = k_gemm_bs<kWgrad, kOutF32, kGrouped, kPair>;
     static bool attr[64] = {false};   // per device
     int dev = 0;
@@ -841,6 +929,12 @@ static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** det
     if (a.layout == 2) return launch_cfg<true, true, false, kPair>(a, st, detail);
     return a.out_f32 ? launch_cfg<false, true, false, kPair>(a, st, detail)
                      : launch_cfg<false, false, false, kPair>(a, st, detail);
+}
+
+size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N) {
+    // TileTable header + one int4 per tile; 128-row tiles bound both variants
+    const int64_t tiles = ((total_M + BM - 1) / BM + G) * ((N + BN - 1) / BN);
+    return (size_t)(16 + 16 * (tiles > 0 ? tiles : 1));
 }
 
 // Variants: 1 = one CTA per 128 x 256 tile, 2 = CTA pair (cta_group::2) per 256 x 256 tile.

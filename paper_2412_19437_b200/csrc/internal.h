@@ -65,7 +65,9 @@ struct GemmArgs {
     void* D; int out_f32; int64_t ldd; int accumulate;
     // grouped
     int grouped; int32_t G; const int64_t* offsets;
+    void* workspace;         // grouped: >= grouped_workspace_bytes(G, M, N) of device memory (tile table)
 };
+size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
 
 // Returns cudaSuccess or the launch error; *detail gets a static message on host-side failures
 // (tensor-map encoding).

@@ -86,13 +86,27 @@ class RankProblem:
     sB: torch.Tensor            # f32 [G_local, N/128, K/128]
     out: torch.Tensor           # bf16 [R_local, N]
     flops: float
+    t0: int = 0                 # this rank's data-parallel token shard [t0, t1) ...
+    t1: int = 0
+    x: torch.Tensor | None = None    # ... its BF16 activations [t1 - t0, K] (device)
+    xq: torch.Tensor | None = None   # ... and the 1x128 codes / scales the step writes
+    xs: torch.Tensor | None = None
+    ws: torch.Tensor | None = None   # the grouped GEMM's workspace (tile table), allocated once
 
 
-def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: torch.Tensor | None = None) -> RankProblem:
+def token_shard(T: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous data-parallel token shard of `rank` (the tokens whose activations it quantizes
+    before dispatch)."""
+    return shard_range(T, world, rank)
+
+
+def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: torch.Tensor | None = None,
+                       keep_tokens: bool = False) -> RankProblem:
     """Everything rank `rank` needs, regenerated from the seeds (identical on every rank).
     Activations: N(0,1) BF16 from a seeded CUDA generator; quantized 1x128 ONCE per token (the
     paper quantizes before dispatch) and the FP8 rows + per-row scales are gathered —
-    exact, because 1x128 scales are per row."""
+    exact, because 1x128 scales are per row.  keep_tokens: also keep the rank's data-parallel token
+    shard (BF16) and output buffers for its 1x128 codes / scales (bench.py's C4 step quantizes it)."""
     import paper_2412_19437_b200 as fp
     if routes is None:
         routes = routes_for(cfg)
@@ -103,6 +117,8 @@ def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: tor
     g.manual_seed(cfg.seed + 100)
     x = torch.randn(cfg.tokens, K, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
     xq, xs = fp.quantize_act_1x128(x)
+    t0, t1 = token_shard(cfg.tokens, world, rank)
+    xsh = x[t0:t1].clone() if keep_tokens else None
     del x
     tokd = tok.to(device)
     R = tok.numel()
@@ -119,59 +135,69 @@ def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: tor
         w = (torch.randn(N, K, generator=ge, device=device, dtype=torch.float32) * 0.006).to(torch.bfloat16)
         fp.quantize_weight_128x128(w, want_t=False, q=Bq[i], s=sB[i])
     out = torch.empty(R, N, dtype=torch.bfloat16, device=device)
-    return RankProblem(e0, e1, offsets.to(device), tok, A, sA, Bq, sB, out, 2.0 * R * N * K)
+    pb = RankProblem(e0, e1, offsets.to(device), tok, A, sA, Bq, sB, out, 2.0 * R * N * K, t0, t1)
+    wsb = int(fp.lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K)) if G > 0 else 16
+    pb.ws = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=device)
+    if keep_tokens:
+        Tl = t1 - t0
+        pb.x = xsh
+        pb.xq = torch.empty(Tl, K, dtype=torch.uint8, device=device)
+        pb.xs = torch.empty(K // 128, (Tl + 3) // 4 * 4 if Tl else 4, dtype=torch.float32, device=device)[:, :Tl]
+    return pb
+
+
+def quantize_tokens(pb: RankProblem):
+    """The C4 step's first launch: 1x128 quantization of this rank's token shard (a-1, a-2)."""
+    import paper_2412_19437_b200 as fp
+    if pb.x is not None and pb.x.shape[0] > 0:
+        fp.quantize_act_1x128(pb.x, pb.xq, pb.xs)
 
 
 def run_rank(pb: RankProblem):
-    """The timed unit: one grouped GEMM over this rank's experts."""
+    """The C4 step's GEMM: one grouped launch over this rank's experts."""
     import paper_2412_19437_b200 as fp
     if pb.A.shape[0] == 0:
         return pb.out
-    return fp.grouped_gemm(pb.offsets, pb.A, pb.sA, pb.Bq, pb.sB, out=pb.out)
+    return fp.grouped_gemm(pb.offsets, pb.A, pb.sA, pb.Bq, pb.sB, out=pb.out, workspace=pb.ws)
 
 
-def bench(args, world, rank, dev, barrier, max_over_ranks, ClockSampler, load_peaks):
-    """bench.py --workload ep: time the per-rank grouped GEMM, report whole-job TFLOP/s."""
-    cfg = EPConfig()
-    routes = routes_for(cfg)
-    pb = build_rank_problem(cfg, world, rank, dev, routes)
+def split_equals_G1_on_one_gpu(pb: RankProblem, cfg: EPConfig, splits=(2, 4, 8)) -> dict:
+    """On ONE GPU holding the whole (G = 1) problem: for each G in `splits`, run the G contiguous expert
+    shards as separate grouped launches on their own rows and compare the concatenation with the
+    G = 1 output bitwise (the partition bench.py times at N GPUs, without NCCL)."""
+    import paper_2412_19437_b200 as fp
+    off = pb.offsets.cpu()
+    ref = run_rank(pb).clone()
+    res = {}
+    for G in splits:
+        parts = []
+        for r in range(G):
+            e0, e1 = shard_range(cfg.experts, G, r)
+            a, b = int(off[e0]), int(off[e1])
+            sa = torch.empty(pb.sA.shape[0], (b - a + 3) // 4 * 4 if b > a else 4, dtype=torch.float32,
+                             device=pb.A.device)[:, :b - a]
+            sa.copy_(pb.sA[:, a:b])
+            if b > a:
+                parts.append(fp.grouped_gemm((pb.offsets[e0:e1 + 1] - off[e0]).contiguous(), pb.A[a:b], sa,
+                                             pb.Bq[e0:e1], pb.sB[e0:e1]))
+        got = torch.cat(parts)
+        res[str(G)] = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+    return res
+
+
+def gathered_equals_G1(pb: RankProblem, cfg: EPConfig, world: int, rank: int, device, routes) -> bool | None:
+    """N > 1: NCCL all_gather of every rank's output rows (verification only, outside any timed
+    region); rank 0 rebuilds the G = 1 problem on its own GPU and compares bitwise.  Returns the
+    verdict on rank 0, None elsewhere."""
+    parts = gather_rows(pb.out, world)
+    if rank != 0:
+        return None
+    got = torch.cat(parts)
+    del parts
+    ref_pb = build_rank_problem(cfg, 1, 0, device, routes)
+    ref = run_rank(ref_pb)
     torch.cuda.synchronize()
-    for _ in range(args.warmup):
-        run_rank(pb)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    with ClockSampler(dev.index or 0) as clk:
-        a.record(stream)
-        for _ in range(args.steps):
-            run_rank(pb)
-        b.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_local = a.elapsed_time(b)
-    ms = max_over_ranks(ms_local, world, dev)
-    rows = [0] * world
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([pb.A.shape[0]], dtype=torch.int64, device=dev)
-        lst = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(lst, t)
-        rows = [int(x.item()) for x in lst]
-    else:
-        rows = [pb.A.shape[0]]
-    total_flops = sum(2.0 * r * cfg.inter * cfg.hidden for r in rows)
-    value = total_flops * args.steps / (ms * 1e-3) / 1e12
-    peaks = load_peaks()
-    local_tflops = pb.flops * args.steps / (ms_local * 1e-3) / 1e12
-    peak = 2.0 * peaks["bf16_tflops"]
-    return {"value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "e4m3", "data": "synthetic",
-            "roofline": {"kernel": "grouped_gemm", "bound": "tensor", "achieved": local_tflops, "peak": peak,
-                         "unit": "TFLOP/s", "frac": local_tflops / peak, "traffic": None,
-                         "peak_src": f"{peaks['src']}: 2 x bf16_tflops (burst)"},
-            "clocks": clk.summary(), "gpu_launches": args.steps,
-            "ep": {"rows_per_rank": rows, "imbalance_max_over_mean": imbalance(rows),
-                   "experts_per_rank": cfg.experts // world}}
+    ok = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+    del ref_pb, ref, got
+    torch.cuda.empty_cache()
+    return ok

@@ -15,7 +15,7 @@ def test_library_loads_and_exports_header_symbols():
     assert len(syms) >= 10
     for name in syms:
         assert hasattr(lib, name), name
-    assert fp.abi_version() == 1
+    assert fp.abi_version() == 2
 
 
 def test_product_library_exports_only_header_symbols():
@@ -109,7 +109,14 @@ def test_grouped_validation():
     assert lib.fp8bs_grouped_gemm(2000, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
     assert lib.fp8bs_grouped_gemm(4, 10, 256, 512, None, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
     assert lib.fp8bs_grouped_gemm(4, 10, 256, 500, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_SHAPE
-    assert lib.fp8bs_grouped_gemm_workspace_size(4, 10, 256, 512) == 0
+    # ABI 2: a device workspace for the tile table is required (16 B per 128 x 256 tile + 16)
+    ws = lib.fp8bs_grouped_gemm_workspace_size(4, 10, 256, 512)
+    assert ws == 16 + 16 * ((1 + 4) * 1)
+    assert lib.fp8bs_grouped_gemm(4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm(4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, A16, ws - 16, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm(4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256,
+                                  ctypes.c_void_p((1 << 20) + 8), ws, None) == L.ERR_ALIGN
+    assert lib.fp8bs_grouped_gemm_dgrad(4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
 
 
 def test_python_binding_rejects_cpu_tensors():
