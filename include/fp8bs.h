@@ -256,8 +256,10 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int6
  * expert is a dense WGRAD over K_e = roundup(M_e, 128) columns at an aligned offset.
  *
  * offsets are HOST int64 [G+1] (non-decreasing, offsets[0] = 0): the expert counts are known on the
- * host when the dispatch is planned; the calls loop over the experts on the host and launch the
- * dense kernels (no device sync).  Errors as the dense calls; FP8BS_ERR_INVALID_ARG on bad offsets. */
+ * host when the dispatch is planned (no device sync).  fp8bs_grouped_gemm_wgrad is ONE persistent
+ * launch over every expert's (m, n) tiles, each contracting over its own expert's token blocks; the
+ * expert blocks travel in the kernel's parameters (G <= 1024).  Every argument is validated before
+ * the launch.  Errors as the dense calls; FP8BS_ERR_INVALID_ARG on bad offsets. */
 
 /* Mp for the given host offsets (0 if offsets are invalid). */
 FP8BS_API int64_t fp8bs_padded_tokens(int32_t G, const int64_t* offsets);

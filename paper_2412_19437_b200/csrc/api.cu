@@ -2,7 +2,6 @@
 // check, then kernel launch on the caller's stream.  Validation runs before any CUDA call so a
 // failing call has no side effects (and the validation paths are testable without a GPU).
 #include <cstdlib>
-#include <mutex>
 #include <vector>
 #include <cstdarg>
 #include <cstdio>
@@ -347,28 +346,6 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
 }
 
 /* ---- grouped MoE expert Wgrad on the expert-aligned (padded) token layout (NEXT-3) ---- */
-/* Side streams for the per-expert fork/join of fp8bs_grouped_gemm_wgrad, one set per device, created
- * on first use and kept for the life of the process. */
-struct ForkStreams {
-    static constexpr int NS = 4;   /* FP8BS_WGRAD_STREAMS (1-4, default 4) of them are used; 2, 4, 6, 8 measured flat */
-    cudaStream_t st[NS];
-    cudaEvent_t start, done[NS];
-};
-static std::mutex g_fork_mutex;
-static ForkStreams* fork_streams(int dev) {
-    static ForkStreams* sets[64] = {nullptr};
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!sets[dev]) {
-        ForkStreams* f = new ForkStreams();
-        bool good = cudaEventCreateWithFlags(&f->start, cudaEventDisableTiming) == cudaSuccess;
-        for (int i = 0; i < ForkStreams::NS && good; ++i)
-            good = cudaStreamCreateWithFlags(&f->st[i], cudaStreamNonBlocking) == cudaSuccess &&
-                   cudaEventCreateWithFlags(&f->done[i], cudaEventDisableTiming) == cudaSuccess;
-        if (!good) { (void)cudaGetLastError(); delete f; return nullptr; }   /* fall back to the caller's stream */
-        sets[dev] = f;
-    }
-    return sets[dev];
-}
 static int64_t padded_tokens(int32_t G, const int64_t* off) {
     if (G < 0 || !off || off[0] != 0) return -1;
     int64_t p = 0;
@@ -427,55 +404,52 @@ fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t
                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                       const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
                                       float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    /* every argument is checked here, before the single launch: a failing call enqueues nothing */
+    if (G < 0 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [0, 1024]", (int)G);
     const int64_t Mp = padded_tokens(G, offsets);
     if (Mp < 0) return fail(FP8BS_ERR_INVALID_ARG, "offsets must be host int64 [G+1], offsets[0]=0, non-decreasing");
     if (N < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
     if (G == 0 || N == 0 || K == 0) return ok();
+    if (N > 0x7fffffff / G || K > 0x7fffffff || Mp > 0x7fffffff) return fail(FP8BS_ERR_SHAPE, "sizes must be < 2^31");
     if (!D) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
-    if (Mp > 0 && (lda < Mp || ldb < Mp)) return fail(FP8BS_ERR_SHAPE, "need lda, ldb >= Mp=%lld", (long long)Mp);
     if (ldd < K) return fail(FP8BS_ERR_SHAPE, "need ldd >= K");
+    if (!aligned16(D) || (ldd * 4) % 16 || K % 4) return fail(FP8BS_ERR_ALIGN, "D must be 16-byte aligned, ldd and K multiples of 4");
+    if (Mp > 0) {
+        if (!A || !sA || !B || !sB) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+        if (lda < Mp || ldb < Mp) return fail(FP8BS_ERR_SHAPE, "need lda, ldb >= Mp=%lld", (long long)Mp);
+        if (ldsA < N || ldsB < K) return fail(FP8BS_ERR_SHAPE, "need ldsA >= N, ldsB >= K");
+        if (!aligned16(A) || !aligned16(B) || !aligned16(sA) || !aligned16(sB))
+            return fail(FP8BS_ERR_ALIGN, "A, B, sA, sB must be 16-byte aligned");
+        if (lda % 16 || ldb % 16 || ldsA % 4 || ldsB % 4)
+            return fail(FP8BS_ERR_ALIGN, "lda, ldb must be multiples of 16 and ldsA, ldsB of 4");
+    }
     fp8bs_status dv = check_device();
     if (dv != FP8BS_OK) return dv;
-    /* The experts are independent GEMMs: fork them round-robin over side streams so one expert's
-     * last wave overlaps the next expert's first (a single stream leaves a tail per expert), then
-     * join back into the caller's stream.  Event record/wait keep this capturable in a CUDA graph. */
-    std::lock_guard<std::mutex> lock(g_fork_mutex);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static const bool fork_on = !getenv("FP8BS_WGRAD_FORK") || atoi(getenv("FP8BS_WGRAD_FORK")) != 0;   /* A/B knob */
-    ForkStreams* fk = fork_on ? fork_streams(dev) : nullptr;
-    static const int ns_env = getenv("FP8BS_WGRAD_STREAMS") ? atoi(getenv("FP8BS_WGRAD_STREAMS")) : 4;
-    const int ns = fk ? (ns_env < 1 ? 1 : ns_env > ForkStreams::NS ? ForkStreams::NS : ns_env) : 1;
-    cudaStream_t caller = (cudaStream_t)stream;
-    if (fk) {
-        if (cudaEventRecord(fk->start, caller) != cudaSuccess) return from_cuda(cudaGetLastError(), "grouped_gemm_wgrad fork");
-        for (int i = 0; i < ns; ++i) cudaStreamWaitEvent(fk->st[i], fk->start, 0);
-    }
-    fp8bs_status result = FP8BS_OK;
+    /* One persistent launch over (expert, n-tile, m-tile) tiles; tile of expert e contracts over its
+     * own token blocks [P_e/128, P_e/128 + roundup(M_e,128)/128) — none for an expert without tokens,
+     * whose tiles then write zeros (or add nothing when accumulating).  No side streams, no state. */
+    std::vector<int> kb(2 * (size_t)G);
     int64_t p = 0;
-    int used = 0;
-    for (int32_t e = 0; e < G && result == FP8BS_OK; ++e) {
-        const int64_t m = offsets[e + 1] - offsets[e], mp = (m + 127) / 128 * 128;
-        float* De = D + (size_t)e * N * ldd;
-        cudaStream_t st = fk ? fk->st[used++ % ns] : caller;
-        if (m == 0) {
-            if (!accumulate) {
-                cudaError_t err = cudaMemset2DAsync(De, (size_t)ldd * 4, 0, (size_t)K * 4, (size_t)N, st);
-                if (err != cudaSuccess) result = from_cuda(err, "grouped_gemm_wgrad zero fill");
-            }
-            continue;
-        }
-        result = gemm_impl(0, FP8BS_WGRAD, N, K, mp, A + p, lda, sA + (p / 128) * ldsA, ldsA,
-                           B + p, ldb, sB + (p / 128) * ldsB, ldsB, De, FP8BS_FP32, ldd, accumulate, (fp8bs_stream_t)st);
+    for (int32_t e = 0; e < G; ++e) {
+        const int64_t mp = (offsets[e + 1] - offsets[e] + 127) / 128 * 128;
+        kb[2 * e] = (int)(p / 128);
+        kb[2 * e + 1] = (int)(mp / 128);
         p += mp;
     }
-    if (fk) {   /* join, also after an error, so the caller's stream never runs ahead of launched work */
-        for (int i = 0; i < ns; ++i) {
-            cudaEventRecord(fk->done[i], fk->st[i]);
-            cudaStreamWaitEvent(caller, fk->done[i], 0);
-        }
+    GemmArgs a{};
+    a.layout = FP8BS_WGRAD; a.M = N; a.N = K; a.K = Mp > 0 ? Mp : 128;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = ldb; a.sB = sB; a.ldsB = ldsB;
+    a.D = D; a.out_f32 = 1; a.ldd = ldd; a.accumulate = accumulate ? 1 : 0;
+    a.grouped = 1; a.G = G; a.offsets = nullptr; a.workspace = nullptr; a.gw_kb = kb.data();
+    if (Mp == 0) {   /* no tokens at all: the tensor maps still need valid (never read) operands */
+        if (accumulate) return ok();
+        cudaError_t err = cudaMemset2DAsync(D, (size_t)ldd * 4, 0, (size_t)K * 4, (size_t)(N * G), (cudaStream_t)stream);
+        return from_cuda(err, "grouped_gemm_wgrad zero fill");
     }
-    return result == FP8BS_OK ? ok() : result;
+    const char* detail = nullptr;
+    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
+    return from_cuda(e, "grouped_gemm_wgrad launch");
 }
 
 }  // extern "C"

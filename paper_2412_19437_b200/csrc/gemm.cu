@@ -147,7 +147,16 @@ constexpr int kDbg = FP8BS_GEMM_DEBUG_BITS;
 constexpr bool kTrace = kDbg != 0;
 #define FP8BS_TS(slot, kb) do { if ((kDbg & 16) && blockIdx.x == 0 && (kb) < kTsN) p.ts[(slot) * kTsN + (kb)] = clock64(); } while (0)
 
-struct Tile { int row0, row_end, n0, e, nh; };   // row0: first row of the CLUSTER tile; nh: halves in range
+// row0: first row of A of the CLUSTER tile; nh: halves in range.  Grouped Wgrad only: orow0 / row_end
+// are rows of the stacked [G x M, N] output, kb0 / kbn the tile's contraction blocks (its expert's).
+struct Tile { int row0, row_end, n0, e, nh; int orow0, kb0, kbn; };
+
+// Grouped Wgrad (one launch over all experts): expert e's token blocks in the padded layout —
+// .x = first 128-token block, .y = number of blocks (0 for an expert without tokens).  Passed by value
+// (kernel parameter space, 8 KB at 1024 experts).
+template <int kG>
+struct GWSched { int2 e[kG]; };
+constexpr int kGWMax = 1024;
 
 template <int ROWS>
 __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
@@ -164,6 +173,23 @@ __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl
     const int m = p.rast_n ? istr : ires, n = p.rast_n ? ires : istr;
     tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n * BN; tl.e = 0;
     tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
+    return true;
+}
+
+// Grouped Wgrad tiles: expert-major, m fastest inside an expert (the smaller operand dYqT_e stays in
+// L2 while the n-tiles of XqT_e stream past it); every expert has num_m x num_n tiles, an expert without
+// tokens included (its tiles write zeros, or add nothing when accumulating).
+template <int ROWS, int kG>
+__device__ __forceinline__ bool get_tile_gw(const KParams& p, const GWSched<kG>& gw, int t, Tile& tl) {
+    const int per = p.num_m * p.num_n;
+    if (t >= p.G * per) return false;
+    const int e = t / per, l = t - e * per;
+    const int m = l % p.num_m, n = l / p.num_m;
+    tl.row0 = m * ROWS; tl.n0 = n * BN; tl.e = e;
+    tl.orow0 = e * p.M + tl.row0; tl.row_end = e * p.M + p.M;
+    tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
+    const int2 k = gw.e[e];
+    tl.kb0 = k.x; tl.kbn = k.y;
     return true;
 }
 
@@ -249,8 +275,11 @@ template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 __global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-          const __grid_constant__ CUtensorMap tmD, const KParams p) {
+          const __grid_constant__ CUtensorMap tmD, const KParams p,
+          const __grid_constant__ GWSched<(kWgrad && kGrouped) ? kGWMax : 1> gw) {
     using C = Cfg<kPair, kWgrad>;
+    // grouped Wgrad: one launch over every expert, each tile with its expert's contraction blocks
+    constexpr bool kGW = kWgrad && kGrouped;
     extern __shared__ uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
@@ -311,9 +340,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint32_t tmem_base = *tmem_slot;
 
     auto next_tile = [&](int t, Tile& tl) -> bool {
-        if constexpr (kGrouped) return get_tile_table(reinterpret_cast<const TileTable*>(p.tiles), p.N, t, tl);
+        if constexpr (kGW) return get_tile_gw<C::ROWS>(p, gw, t, tl);
+        else if constexpr (kGrouped) return get_tile_table(reinterpret_cast<const TileTable*>(p.tiles), p.N, t, tl);
         else return get_tile_dense<C::ROWS>(p, t, tl);
     };
+    // contraction blocks of a tile and their first block (only grouped Wgrad tiles differ)
+    auto nkb = [&](const Tile& tl) -> int { if constexpr (kGW) return tl.kbn; else return p.KB; };
+    auto kbase = [&](const Tile& tl) -> int { if constexpr (kGW) return tl.kb0; else return 0; };
 
     // Tile order.  Dense: static, cluster c takes tiles c, c + ncl, ...  Grouped: dynamic — the
     // leader's producer thread claims the next tile index with an atomic on the workspace counter
@@ -354,7 +387,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int t_next = 0;                                  // claimer: tile #j+1, claimed ahead
     // the leader's producer warp (lane 0 claims, the warp gets the index)
     auto tile_index_claim = [&](int j) -> int {
-        if constexpr (!kGrouped || FP8BS_STATIC_SCHED) return cid + j * ncl;
+        if constexpr (!kGrouped || kGW || FP8BS_STATIC_SCHED) return cid + j * ncl;
         int t = 0;
         if (lane == 0) {
             t = j == 0 ? tq_publish(0) : t_next;
@@ -364,7 +397,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     };
     // every other role
     auto tile_index = [&](int j) -> int {
-        if constexpr (!kGrouped || FP8BS_STATIC_SCHED) return cid + j * ncl;
+        if constexpr (!kGrouped || kGW || FP8BS_STATIC_SCHED) return cid + j * ncl;
         return tq_take(j);
     };
 
@@ -382,25 +415,25 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int j = 0, t = tix(0); next_tile(t, tl); t = tix(++j)) {
                 const int arow = tl.row0 + (int)rank * BM;
                 const int brow = tl.n0 + (int)rank * C::BH_ROWS;
-                for (int kb = 0; kb < p.KB; ++kb, ++it) {
+                for (int kb = 0; kb < nkb(tl); ++kb, ++it) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(empty_bar(s), ph ^ 1);
                     const uint32_t sa = sbase + s * C::STAGE;
-                    const int kc = ((kDbg & 4)) ? 0 : kb * BK;
+                    const int kc = ((kDbg & 4)) ? 0 : (kbase(tl) + kb) * BK;
                     if (elect_one()) {
                         if constexpr (kPair) {
                             if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (C::A_BYTES + tl.nh * C::BH_BYTES));
                             tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
                             for (int h = 0; h < tl.nh; ++h) {
-                                if constexpr (kGrouped) tma_load_3d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
+                                if constexpr (kGrouped && !kWgrad) tma_load_3d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
                                 else tma_load_2d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN);
                             }
                         } else {
                             mbar_arrive_expect_tx(full_bar(s), C::A_BYTES + tl.nh * C::BH_BYTES);
                             tma_load_2d(sa, &tmA, full_bar(s), kc, arow);
                             for (int h = 0; h < tl.nh; ++h) {
-                                if constexpr (kGrouped) tma_load_3d(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
+                                if constexpr (kGrouped && !kWgrad) tma_load_3d(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
                                 else tma_load_2d(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN);
                             }
                         }
@@ -425,7 +458,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     // ahead by KB instead let a later parity wait on full_bar pass one or more phases
                     // early (an mbarrier parity wait only tells apart adjacent phases), so the next
                     // tile's MMAs read stages still being filled.
-                    for (int kb = 0; kb < p.KB; ++kb, ++it) {
+                    for (int kb = 0; kb < nkb(tl); ++kb, ++it) {
                         const int s = it % C::kStages;
                         mbar_wait(full_bar(s), (it / C::kStages) & 1);
                         if (elect_one()) {
@@ -436,7 +469,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                     continue;
                 }
-                for (int kb = 0; kb < p.KB; ++kb, ++it, ++qh) {
+                for (int kb = 0; kb < nkb(tl); ++kb, ++it, ++qh) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     const int pb = 2 * h + (qh & 1);
@@ -487,7 +520,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
                 const int arow = tl.row0 + (int)rank * BM;
                 const int nb0 = tl.n0 / 128;
-                for (int kb0 = 0; kb0 < p.KB; kb0 += 32) {
+                for (int kb0 = 0; kb0 < nkb(tl); kb0 += 32) {
                     // lane j holds the 2 block scalars the tile's columns need at K-block kb0 + j
                     float v0 = 0.0f, v1 = 0.0f;
                     if constexpr (!kWgrad) {
@@ -497,7 +530,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                             if (nb0 + 1 < p.NB) v1 = __ldg(sbp + (nb0 + 1) * p.sb_nb_stride + kb * p.sb_kb_stride);
                         }
                     }
-                    const int nk = min(32, p.KB - kb0);
+                    const int nk = min(32, nkb(tl) - kb0);
                     for (int j = 0; j < nk; ++j, ++sit) {
                         const int ss = sit % C::kSStages;
                         const uint32_t sph = (sit / C::kSStages) & 1;
@@ -511,8 +544,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                                 sbs[0] = b0; sbs[1] = b1;
                             }
                             mbar_arrive_expect_tx(sfull_bar(ss), C::SA_BOX * 4 + (kWgrad ? BN * 4 : 0));
-                            tma_load_2d(sst, &tmSA, sfull_bar(ss), arow & ~3, kb0 + j);
-                            if constexpr (kWgrad) tma_load_2d(sst + C::SA_BYTES, &tmSB, sfull_bar(ss), tl.n0, kb0 + j);
+                            tma_load_2d(sst, &tmSA, sfull_bar(ss), arow & ~3, kbase(tl) + kb0 + j);
+                            if constexpr (kWgrad) tma_load_2d(sst + C::SA_BYTES, &tmSB, sfull_bar(ss), tl.n0, kbase(tl) + kb0 + j);
                         }
                         __syncwarp();
                     }
@@ -536,13 +569,15 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         Tile tl;
         // every tile advances sit by exactly KB, so the tile's sequence number is sit / KB (one
         // register fewer than a counter: the accumulators are at the edge of the 240-register budget)
-        for (int t = tile_index(0); next_tile(t, tl); t = tile_index(sit / p.KB)) {
+        int jt = 0;                                     // grouped Wgrad: tiles walked (KB varies per tile)
+        auto next_j = [&]() -> int { if constexpr (kGW) return ++jt; else return sit / p.KB; };
+        for (int t = tile_index(0); next_tile(t, tl); t = tile_index(next_j())) {
             const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
             const bool active = h < tl.nh;
             if (!active) {
                 // this half lies past N (last column tile): only keep the scale ring moving (the
                 // issuer skips its MMAs and slot uses too)
-                for (int kb = 0; kb < p.KB; ++kb, ++sit) {
+                for (int kb = 0; kb < nkb(tl); ++kb, ++sit) {
                     if (!(kDbg & 512)) {
                         mbar_wait(sfull_bar(sit & (C::kSStages - 1)), (sit / C::kSStages) & 1);
                         if (elect_one()) mbar_arrive(sempty_bar(sit & (C::kSStages - 1)));
@@ -696,13 +731,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                 }
             } else {
-                for (int kb = 0; kb < p.KB; ++kb, ++sit, ++qh) {
+                for (int kb = 0; kb < nkb(tl); ++kb, ++sit, ++qh) {
                     promote_kb(sit & (C::kSStages - 1), (sit / C::kSStages) & 1, 2 * h + (qh & 1), (qh >> 1) & 1, sit);
                     release_scales(sit & (C::kSStages - 1));
                 }
             }
             // ---------------- epilogue ----------------
-            const int arow = tl.row0 + (int)rank * BM;
+            const int arow = (kGW ? tl.orow0 : tl.row0) + (int)rank * BM;   // output rows
             // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or
             // 64 BF16 columns) in its own SWIZZLE_128B buffer and writes them with asynchronous TMA
             // stores (reduce-add for Wgrad's D += acc): a warp store used to touch 32 rows at once.
@@ -752,7 +787,14 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                             if (col + u * (16 / ESZ) < p.N) {
                                 const uint4 v = lds_u32x4(ebuf + r * 128 + ((u ^ (r & 7)) << 4));
                                 uint8_t* dst = reinterpret_cast<uint8_t*>(p.D) + ((int64_t)(grow0 + r) * p.ldd + col) * ESZ + u * 16;
-                                *reinterpret_cast<uint4*>(dst) = v;
+                                if (kOutF32 && p.accumulate) {          // Wgrad D += dW: this lane owns these 4 floats
+                                    float4 o = *reinterpret_cast<const float4*>(dst);
+                                    o.x += __uint_as_float(v.x); o.y += __uint_as_float(v.y);
+                                    o.z += __uint_as_float(v.z); o.w += __uint_as_float(v.w);
+                                    *reinterpret_cast<float4*>(dst) = o;
+                                } else {
+                                    *reinterpret_cast<uint4*>(dst) = v;
+                                }
                             }
                         }
                         __syncwarp();                               // buffer reads done before its reuse
@@ -795,6 +837,7 @@ template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
     using C = Cfg<kPair, kWgrad>;
     const int KB = (int)(a.K / BK);
+    constexpr bool kGW = kWgrad && kGrouped;   // grouped Wgrad: A = dYqT [M, Mp], D = [G x M, N]
     const int64_t rows = a.M;   // total rows of A (total_M for grouped)
     CUtensorMap tA, tB, tSA, tSB;
     {
@@ -805,7 +848,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
             *detail = "cuTensorMapEncodeTiled failed for A"; return cudaErrorInvalidValue;
         }
     }
-    if (kGrouped) {
+    if (kGrouped && !kWgrad) {
         uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
         uint32_t box[3] = {BK, (uint32_t)C::BH_ROWS, 1};
@@ -841,7 +884,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     CUtensorMap tD;
     {
         const uint64_t esz = kOutF32 ? 4 : 2;
-        uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)rows};
+        uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)(kGW ? rows * a.G : rows)};   // grouped Wgrad: experts stacked
         uint64_t str[1] = {(uint64_t)a.ldd * esz};
         uint32_t box[2] = {(uint32_t)(128 / esz), 32};
         if (!make_tmap(&tD, kOutF32 ? TMAP_F32 : TMAP_BF16, 2, a.D, dims, str, box, 128)) {
@@ -876,13 +919,14 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     }
 
     int64_t tiles_ub;
-    if (kGrouped) tiles_ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;
+    if (kGW) tiles_ub = (int64_t)a.G * p.num_m * p.num_n;
+    else if (kGrouped) tiles_ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;
     else tiles_ub = (int64_t)p.num_m * p.num_n;
     const int64_t max_clusters = num_sms() / C::CS;
     int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
     if (clusters < 1) clusters = 1;
     const int smem = C::SMEM_DENSE;
-    if (kGrouped) {
+    if (kGrouped && !kWgrad) {
         // the tile table for this launch (k_grouped_schedule), then the GEMM; both PDL
         cudaError_t e = launch_pdl(k_grouped_schedule, dim3(1), dim3(kMaxGroups), 0, st, a.offsets, a.G, C::ROWS,
                                    p.num_n, p.N, reinterpret_cast<TileTable*>(a.workspace));
@@ -909,7 +953,13 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, p);
+    GWSched<kGW ? kGWMax : 1> gw;
+    if constexpr (kGW) {
+        for (int e = 0; e < a.G; ++e) gw.e[e] = make_int2(a.gw_kb[2 * e], a.gw_kb[2 * e + 1]);
+    } else {
+        gw.e[0] = make_int2(0, 0);
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, p, gw);
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
 }
@@ -922,6 +972,7 @@ static int g_forced_variant = 0;
 
 template <bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
+    if (a.grouped && a.layout == 2) return launch_cfg<true, true, true, kPair>(a, st, detail);
     if (a.grouped) {
         return a.out_f32 ? launch_cfg<false, true, true, kPair>(a, st, detail)
                          : launch_cfg<false, false, true, kPair>(a, st, detail);
@@ -945,7 +996,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
 #endif
     if (v < 1 || v > 2) {
         // ~128-row experts / small M would waste half of a 256-row pair tile -> one CTA per tile
-        if (a.grouped) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 2 : 1;
+        // (grouped Wgrad: a.M is one expert's output rows — the dense per-expert choice)
+        if (a.grouped && a.layout != 2) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 2 : 1;
         else v = (a.M <= 128) ? 1 : 2;
     }
     return v == 1 ? launch_v<false>(a, st, detail) : launch_v<true>(a, st, detail);

@@ -66,6 +66,7 @@ struct GemmArgs {
     // grouped
     int grouped; int32_t G; const int64_t* offsets;
     void* workspace;         // grouped: >= grouped_workspace_bytes(G, M, N) of device memory (tile table)
+    const int* gw_kb;        // grouped Wgrad (layout 2): host [G][2] = {first 128-token block, blocks} per expert
 };
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
 

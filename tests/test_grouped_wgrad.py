@@ -205,3 +205,41 @@ def test_grouped_wgrad_c4_full_size_sampled():
         pad = lambda c: torch.nn.functional.pad(c, (0, (q - p) - (b - a)))   # zero codes up to roundup(M_e,128)
         O = oracle.gemm(2, pad(qd), sd, pad(qx), sx, rows=rows)
         assert oracle.rel_err_normwise(D[e][rows.cuda()].cpu().double(), O) <= TOL
+
+
+@pytest.mark.gpu
+def test_grouped_calls_capture_in_a_cuda_graph():
+    """The grouped Wgrad is one launch and the grouped Fprop two (tile scheduler + GEMM), with no host
+    synchronisation and no library state: both capture into a CUDA graph, and a replay is bitwise equal
+    to the eager call (the side-stream fork it replaced had no such test)."""
+    import paper_2412_19437_b200 as fp
+    counts = [0, 1, 300, 128, 257, 0, 700]
+    off, x, dy = _problem(counts, C_in=384, N_out=256)
+    XqT, sX = fp.quantize_act_128x1_grouped(x.cuda(), off)
+    DqT, sD = fp.quantize_act_128x1_grouped(dy.cuda(), off)
+    G, N, K = len(counts), dy.shape[1], x.shape[1]
+    eager = fp.grouped_gemm_wgrad(off, DqT, sD, XqT, sX)
+    qx, sx = fp.quantize_act_1x128(x.cuda())
+    Bq = torch.randint(0, 0x7E, (G, N, K), dtype=torch.uint8, device="cuda")
+    sB = torch.rand(G, N // 128, K // 128, device="cuda") * 1e-3
+    doff = off.cuda()
+    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(G, x.shape[0], N, K)), dtype=torch.uint8,
+                     device="cuda")
+    eager_f = fp.grouped_gemm(doff, qx, sx, Bq, sB, workspace=ws)
+    torch.cuda.synchronize()
+    out_w = torch.full_like(eager, float("nan"))
+    out_f = torch.empty_like(eager_f)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fp.grouped_gemm_wgrad(off, DqT, sD, XqT, sX, out=out_w)
+            fp.grouped_gemm(doff, qx, sx, Bq, sB, out=out_f, workspace=ws)
+    for _ in range(2):
+        out_w.fill_(float("nan"))
+        out_f.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out_w.view(torch.int32), eager.view(torch.int32))
+        assert torch.equal(out_f.view(torch.int16), eager_f.view(torch.int16))
