@@ -67,6 +67,11 @@ def lib():
         L.oracle_rel_err_normwise.restype = ctypes.c_double
         L.oracle_rel_err_normwise.argtypes = [vp, vp, i64]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_exp32.restype = ctypes.c_float
+        L.oracle_exp32.argtypes = [ctypes.c_float]
+        L.oracle_swiglu32.restype = ctypes.c_float
+        L.oracle_swiglu32.argtypes = [ctypes.c_float, ctypes.c_float]
+        L.oracle_swiglu_quant_1x128.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64]
         _lib = L
     return _lib
 
@@ -150,6 +155,31 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, pow2: bool = F
     fn = lib().oracle_quantize_weight_128x128_pow2 if pow2 else lib().oracle_quantize_weight_128x128
     fn(_ptr(w), _dt(w), N, K, K, _ptr(q), K, _ptr(s), KB, _ptr(qT), N)
     return q, s, qT
+
+
+def exp32(x: float) -> float:
+    """The fixed binary32 exp sequence of reading R27 (oracle.c oracle_exp32)."""
+    return lib().oracle_exp32(x)
+
+
+def swiglu32(g: float, u: float) -> float:
+    """RN(RN(g / RN(1 + exp32(-g))) * u) (reading R27)."""
+    return lib().oracle_swiglu32(g, u)
+
+
+def swiglu_quant_1x128(H: torch.Tensor, cache: bool = True):
+    """Up-projection output H float32 [M, 2I] (gate / up interleaved per 128 channels, R27) ->
+    (qy uint8 [M, I], sy fp32 [I/128, M], qh uint8 [M, 2I] or None, sh fp32 [2I/128, M] or None):
+    the 1x128-quantized SwiGLU output and (cache=True) the 1x128-quantized H."""
+    H = H.to(torch.float32).contiguous()
+    M, N2 = H.shape
+    I = N2 // 2
+    qy = torch.empty(M, I, dtype=torch.uint8)
+    sy = torch.empty(I // 128, M, dtype=torch.float32)
+    qh = torch.empty(M, N2, dtype=torch.uint8) if cache else None
+    sh = torch.empty(N2 // 128, M, dtype=torch.float32) if cache else None
+    lib().oracle_swiglu_quant_1x128(_ptr(H), M, I, N2, _ptr(qy), I, _ptr(sy), M, _ptr(qh), N2, _ptr(sh), M)
+    return qy, sy, qh, sh
 
 
 def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, pow2: bool = False):

@@ -390,6 +390,73 @@ double oracle_rel_err_normwise(const double* D, const double* O, int64_t n) {
     return num / den;
 }
 
+/* ------------------------------------------------- SwiGLU epilogue (NEXT-2) ---- */
+/* exp(x) in binary32 by ONE fixed sequence of IEEE round-to-nearest operations (reading R27), so
+ * that a GPU epilogue evaluating the same sequence (fmaf = correctly rounded fused multiply-add)
+ * reproduces it bit for bit: Cody-Waite reduction x = k ln2 + r with k = RNE(RN(x * log2 e)) and
+ * ln2 split into a 16-bit head (k * head exact for |k| < 256) and a tail, a degree-7 Taylor
+ * polynomial of exp(r) in Horner form (|r| <= ~0.35: truncation < 1e-8 relative), and the scaling by
+ * 2^k as two exact power-of-two products (the second one rounds once when the result is
+ * subnormal).  Accuracy vs the C library's exp: <= 2 ulp (tests/test_oracle.py).  Overflow -> +Inf,
+ * x < -104 -> +0, NaN -> NaN. */
+static float pow2i(int n) {            /* 2^n for n in [-126, 127]: the exponent field */
+    union { uint32_t u; float f; } v;
+    v.u = (uint32_t)(n + 127) << 23;
+    return v.f;
+}
+float oracle_exp32(float x) {
+    if (isnan(x)) return x;
+    if (x > 88.72283935546875f) return INFINITY;
+    if (x < -104.0f) return 0.0f;
+    const float k = rintf(x * 1.44269502162933349609375f);
+    float r = fmaf(k, -0.693145751953125f, x);
+    r = fmaf(k, -1.428606765330187045037746429443359375e-06f, r);
+    float p = 1.98412701138295233249664306640625e-4f;         /* 1/7! */
+    p = fmaf(p, r, 1.388888922519981861114501953125e-3f);     /* 1/6! */
+    p = fmaf(p, r, 8.3333337679505348205566406250e-3f);       /* 1/5! */
+    p = fmaf(p, r, 4.16666679084300994873046875e-2f);         /* 1/4! */
+    p = fmaf(p, r, 1.666666716337203979492187500e-1f);        /* 1/3! */
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    const int ki = (int)k, k1 = ki / 2, k2 = ki - k1;          /* |k1|, |k2| <= 76 */
+    return (p * pow2i(k1)) * pow2i(k2);
+}
+
+/* SwiGLU (SiLU-gated linear unit: silu(g) * u, silu(g) = g * sigmoid(g) = g / (1 + exp(-g))) of
+ * one (gate, up) pair in binary32, in this order (reading R27):
+ *   e = exp32(-g);  d = RN(1 + e);  s = RN(g / d);  y = RN(s * u). */
+float oracle_swiglu32(float g, float u) {
+    const float e = oracle_exp32(-g);
+    const float d = 1.0f + e;
+    const float sg = g / d;
+    return sg * u;
+}
+
+/* The FP8 epilogue of an expert up-projection (NEXT-2; "we cache the inputs of the SwiGLU
+ * operator ... stored in FP8 with our fine-grained quantization method", and every Fprop input is FP8,
+ * Fig. fp8_framework P:453-460 — so the down-projection's input is the 1x128-quantized SwiGLU output).
+ * H [M, 2I] (ld ldh) is the up-projection's binary32 output with gate and up interleaved per 128
+ * channels: output block j (channels [128 j, 128 j + 128)) has gate = columns [256 j, 256 j + 128) and
+ * up = columns [256 j + 128, 256 j + 256) (reading R27).  I % 128 == 0.
+ *   y[m][128 j + c] = swiglu32(H[m][256 j + c], H[m][256 j + 128 + c]);
+ *   (qy, sy) = 1x128 quantization of y (the same contract as oracle_quantize_act_1x128);
+ *   (qh, sh) = 1x128 quantization of H itself — the FP8 cache of the SwiGLU inputs; skipped
+ *   when qh == NULL. */
+void oracle_swiglu_quant_1x128(const float* H, int64_t M, int64_t I, int64_t ldh,
+                               uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                               uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh) {
+    float* y = (float*)malloc((size_t)(M > 0 ? M : 1) * (size_t)(I > 0 ? I : 1) * sizeof(float));
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t c = 0; c < I; ++c) {
+            const int64_t j = c / 128, cc = c % 128;
+            y[m * I + c] = oracle_swiglu32(H[m * ldh + 256 * j + cc], H[m * ldh + 256 * j + 128 + cc]);
+        }
+    quantize_1x128(y, 1 /* FP32 */, M, I, I, qy, ldqy, sy, ldsy, group_scale);
+    if (qh) quantize_1x128(H, 1, M, 2 * I, ldh, qh, ldqh, sh, ldsh, group_scale);
+    free(y);
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -638,3 +638,69 @@ def test_nonfinite_inputs_follow_reading_R6():
     assert math.isinf(float(s[0, 1]))
     inf = x[1, :128].isinf()
     assert torch.all(q[1, :128][inf] == 0x7F) and torch.all((q[1, :128][~inf] & 0x7F) == 0)
+
+
+# ------------------------------------------------------ SwiGLU FP8 epilogue (NEXT-2, R27) ----
+def _ulp_err(a: float, ref: float) -> float:
+    """|a - ref| in units of the binary32 ulp at ref (normal range)."""
+    if ref == 0:
+        return abs(a)
+    e = math.frexp(abs(ref))[1] - 1
+    return abs(a - ref) / 2.0 ** (max(e, -126) - 23)
+
+
+def test_exp32_accuracy_and_specials():
+    """The fixed binary32 exp sequence of R27 stays within 2 ulp of the C library's double exp (rounded
+    to binary32) over the whole normal range; exact at 0; overflow -> Inf, far underflow -> +0."""
+    g = torch.Generator().manual_seed(5)
+    xs = (torch.rand(200000, generator=g, dtype=torch.float64) * 175.0 - 87.0).to(torch.float32).tolist()
+    xs += [0.0, -0.0, 1.0, -1.0, 0.5, 0.3465735902799727, -0.3465735902799727, 88.0, -87.0]
+    worst = 0.0
+    for x in xs:
+        worst = max(worst, _ulp_err(oracle.exp32(x), float(np.float32(math.exp(x)))))
+    assert worst <= 2.0, worst
+    assert oracle.exp32(0.0) == 1.0 and oracle.exp32(-0.0) == 1.0
+    assert math.isinf(oracle.exp32(89.0)) and math.isinf(oracle.exp32(float("inf")))
+    assert oracle.exp32(-110.0) == 0.0 and oracle.exp32(float("-inf")) == 0.0
+    assert math.isnan(oracle.exp32(float("nan")))
+
+
+def test_swiglu32_matches_double_silu():
+    """swiglu32(g, u) = RN(RN(g / RN(1 + exp32(-g))) * u) is within 4 ulp of the double-precision
+    g * sigmoid(g) * u, and follows the closed forms: g = 0 -> 0; g >= 20 -> exactly RN(g * u)
+    (exp(-g) < ulp(1)/2, so 1 + e rounds to 1); g <= -104 -> signed zero."""
+    g = torch.Generator().manual_seed(6)
+    gs = (torch.randn(20000, generator=g) * 4).tolist()
+    us = (torch.randn(20000, generator=g) * 2).tolist()
+    worst = 0.0
+    for a, b in zip(gs, us):
+        a, b = float(np.float32(a)), float(np.float32(b))
+        ref = a / (1.0 + math.exp(-a)) * b
+        worst = max(worst, _ulp_err(oracle.swiglu32(a, b), float(np.float32(ref))))
+    assert worst <= 4.0, worst
+    assert oracle.swiglu32(0.0, 3.0) == 0.0
+    for a, b in ((20.0, 3.0), (32.0, -1.5), (100.0, 0.25), (1000.0, 7.0)):
+        assert oracle.swiglu32(a, b) == float(np.float32(a * b))
+    assert oracle.swiglu32(-200.0, 5.0) == 0.0 and math.copysign(1.0, oracle.swiglu32(-200.0, 5.0)) == -1.0
+
+
+def test_swiglu_quant_is_the_composition():
+    """oracle.swiglu_quant_1x128 = elementwise swiglu32 over the interleaved (gate, up) blocks,
+    followed by the pinned 1x128 quantizer; the cache output is the 1x128 quantizer applied to H."""
+    M, I = 37, 256
+    H = W.gaussian_act(M, 2 * I, seed=12, dtype=torch.float32) * 3
+    H[0, :128] = 0.0                    # gate 0 -> y = 0 for output block 0 of row 0 -> s = 1
+    H[1, 256:384] = 25.0                # gate >= 20 -> y = RN(g * u) exactly
+    qy, sy, qh, sh = oracle.swiglu_quant_1x128(H)
+    y = torch.empty(M, I, dtype=torch.float32)
+    Hl = H.tolist()
+    for m in range(M):
+        for c in range(I):
+            j, cc = divmod(c, 128)
+            y[m, c] = oracle.swiglu32(Hl[m][256 * j + cc], Hl[m][256 * j + 128 + cc])
+    rq, rs = oracle.quantize_act_1x128(y)
+    assert torch.equal(qy, rq) and torch.equal(sy.view(torch.int32), rs.view(torch.int32))
+    hq, hs = oracle.quantize_act_1x128(H)
+    assert torch.equal(qh, hq) and torch.equal(sh.view(torch.int32), hs.view(torch.int32))
+    assert float(sy[0, 0]) == 1.0 and not (qy[0, :128] & 0x7F).any()
+    assert torch.equal(y[1, 128:256], (25.0 * H[1, 384:512]).to(torch.float32))
