@@ -243,6 +243,35 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int6
                                       void* D, fp8bs_dtype ddt, int64_t ldd,
                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
+/* ---- gemm_swiglu: the up-projection with its SwiGLU FP8 epilogue (NEXT-2) ---------------------
+ * "we cache the inputs of the SwiGLU operator and recompute its output in the backward pass.
+ * These activations are also stored in FP8 with our fine-grained quantization method"; and every
+ * Fprop input is FP8 (Fig. fp8_framework), so the down-projection consumes the SwiGLU
+ * output quantized 1x128.  One FPROP GEMM (operands, layouts, alignment and errors as fp8bs_gemm
+ * FPROP) whose epilogue, instead of writing H = A x B^T, writes from H's FP32 accumulators:
+ *   y  [M, I] E4M3 codes (qy, ldqy >= I, 16-byte aligned rows) and sy [I/128, ldsy >= M] FP32: the
+ *      1x128 quantization (the fp8bs_quantize_act_1x128 contract) of y = swiglu32(gate, up);
+ *   qh [M, N] codes + sh [N/128, ldsh >= M] (optional, both NULL to skip): H itself quantized 1x128,
+ *      the FP8 cache of the SwiGLU inputs.
+ * N = 2I, a multiple of 256: B's rows come in (gate, up) blocks of 128 — output channels
+ * [128 j, 128 j + 128) take gate = H columns [256 j, 256 j + 128) and up = [256 j + 128, 256 j + 256).
+ * swiglu32(g, u) = RN(RN(g / RN(1 + exp32(-g))) * u) in binary32 with exp32 the fixed Cody-Waite /
+ * degree-7 sequence of DESIGN.md reading R27 (so the codes are reproducible bit for bit).  No BF16
+ * (or FP32) H ever reaches memory. */
+FP8BS_API fp8bs_status fp8bs_gemm_swiglu(int64_t M, int64_t N, int64_t K,
+                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                               uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                               uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh, fp8bs_stream_t stream);
+/* The same epilogue on the grouped (MoE) expert up-projection: fp8bs_grouped_gemm's arguments, layouts,
+ * workspace and validation, with the outputs of fp8bs_gemm_swiglu over the total_M expert rows. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_swiglu(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                       const uint8_t* B, const float* sB,
+                                       uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                                       uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh,
+                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+
 /* ---- Grouped MoE expert Wgrad (NEXT-3) ------------------------------------------
  * dW_e [N, K] = sum over expert e's tokens t of dY[t, :]^T X[t, :]   (P:476-481 applied per expert;
  * Wgrad operands in 128x1 tiles along the tokens).  The contraction is each

@@ -69,6 +69,8 @@ def lib():
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_exp32.restype = ctypes.c_float
         L.oracle_exp32.argtypes = [ctypes.c_float]
+        L.oracle_rcp32.restype = ctypes.c_float
+        L.oracle_rcp32.argtypes = [ctypes.c_float]
         L.oracle_swiglu32.restype = ctypes.c_float
         L.oracle_swiglu32.argtypes = [ctypes.c_float, ctypes.c_float]
         L.oracle_swiglu_quant_1x128.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64]
@@ -162,8 +164,13 @@ def exp32(x: float) -> float:
     return lib().oracle_exp32(x)
 
 
+def rcp32(d: float) -> float:
+    """The fixed binary32 reciprocal sequence of reading R27 (d in [1, 2^125))."""
+    return lib().oracle_rcp32(d)
+
+
 def swiglu32(g: float, u: float) -> float:
-    """RN(RN(g / RN(1 + exp32(-g))) * u) (reading R27)."""
+    """RN(RN(g * rcp32(RN(1 + exp32(-g)))) * u) (reading R27)."""
     return lib().oracle_swiglu32(g, u)
 
 

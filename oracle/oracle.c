@@ -391,45 +391,49 @@ double oracle_rel_err_normwise(const double* D, const double* O, int64_t n) {
 }
 
 /* ------------------------------------------------- SwiGLU epilogue (NEXT-2) ---- */
-/* exp(x) in binary32 by ONE fixed sequence of IEEE round-to-nearest operations (reading R27), so
- * that a GPU epilogue evaluating the same sequence (fmaf = correctly rounded fused multiply-add)
- * reproduces it bit for bit: Cody-Waite reduction x = k ln2 + r with k = RNE(RN(x * log2 e)) and
- * ln2 split into a 16-bit head (k * head exact for |k| < 256) and a tail, a degree-7 Taylor
- * polynomial of exp(r) in Horner form (|r| <= ~0.35: truncation < 1e-8 relative), and the scaling by
- * 2^k as two exact power-of-two products (the second one rounds once when the result is
- * subnormal).  Accuracy vs the C library's exp: <= 2 ulp (tests/test_oracle.py).  Overflow -> +Inf,
- * x < -104 -> +0, NaN -> NaN. */
-static float pow2i(int n) {            /* 2^n for n in [-126, 127]: the exponent field */
-    union { uint32_t u; float f; } v;
-    v.u = (uint32_t)(n + 127) << 23;
-    return v.f;
-}
+/* exp(x) in binary32 by ONE fixed, branch-free sequence of IEEE round-to-nearest operations (reading
+ * R27), so that a GPU epilogue evaluating the same sequence (fmaf = correctly rounded fused
+ * multiply-add) reproduces it bit for bit:
+ *   x is clamped to [-86, 86] (NaN becomes -86: callers carry NaN through their own operands);
+ *   t = x log2(e) as an unevaluated pair th + tl (th = RN(x L2E), tl = the FMA residual of that
+ *   product + x L2E_LO); k = RNE(th); f = RN((th - k) + tl) (th - k is exact);
+ *   2^f by the degree-7 Taylor polynomial of exp(f ln 2) in Horner form (|f| <= 0.5: truncation
+ *   < 6e-9 relative), then times 2^k by adding k to the exponent field (the result is normal for
+ *   |x| <= 86).  Accuracy vs the C library's exp: <= 2 ulp (tests/test_oracle.py). */
+static float bits_f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t f_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 float oracle_exp32(float x) {
-    if (isnan(x)) return x;
-    if (x > 88.72283935546875f) return INFINITY;
-    if (x < -104.0f) return 0.0f;
-    const float k = rintf(x * 1.44269502162933349609375f);
-    float r = fmaf(k, -0.693145751953125f, x);
-    r = fmaf(k, -1.428606765330187045037746429443359375e-06f, r);
-    float p = 1.98412701138295233249664306640625e-4f;         /* 1/7! */
-    p = fmaf(p, r, 1.388888922519981861114501953125e-3f);     /* 1/6! */
-    p = fmaf(p, r, 8.3333337679505348205566406250e-3f);       /* 1/5! */
-    p = fmaf(p, r, 4.16666679084300994873046875e-2f);         /* 1/4! */
-    p = fmaf(p, r, 1.666666716337203979492187500e-1f);        /* 1/3! */
-    p = fmaf(p, r, 0.5f);
-    p = fmaf(p, r, 1.0f);
-    p = fmaf(p, r, 1.0f);
-    const int ki = (int)k, k1 = ki / 2, k2 = ki - k1;          /* |k1|, |k2| <= 76 */
-    return (p * pow2i(k1)) * pow2i(k2);
+    x = fminf(fmaxf(x, -86.0f), 86.0f);
+    const float L2E = 1.44269502162933349609375f, L2E_LO = 1.925963033500011079013347625732421875e-08f;
+    const float th = x * L2E;
+    const float tl = fmaf(x, L2E_LO, fmaf(x, L2E, -th));
+    const float k = rintf(th);
+    const float f = (th - k) + tl;
+    float p = 1.5252733804059840e-5f;                        /* ln2^7 / 7! */
+    p = fmaf(p, f, 1.5403530393381608e-4f);                  /* ln2^6 / 6! */
+    p = fmaf(p, f, 1.3333558146428443e-3f);                  /* ln2^5 / 5! */
+    p = fmaf(p, f, 9.6181291076284772e-3f);                  /* ln2^4 / 4! */
+    p = fmaf(p, f, 5.5504108664821580e-2f);                  /* ln2^3 / 3! */
+    p = fmaf(p, f, 2.4022650695910071e-1f);                  /* ln2^2 / 2! */
+    p = fmaf(p, f, 6.9314718055994531e-1f);                  /* ln2 */
+    p = fmaf(p, f, 1.0f);
+    return bits_f(f_bits(p) + ((uint32_t)(int32_t)k << 23));
+}
+
+/* 1/d for d in [1, 2^125) by a fixed sequence (reading R27): the bit-level first guess
+ * 0x7EF311C3 - bits(d) and three Newton steps r += r (1 - d r), each residual by one FMA. */
+float oracle_rcp32(float d) {
+    float r = bits_f(0x7EF311C3u - f_bits(d));
+    for (int i = 0; i < 3; ++i) r = fmaf(r, fmaf(-d, r, 1.0f), r);
+    return r;
 }
 
 /* SwiGLU (SiLU-gated linear unit: silu(g) * u, silu(g) = g * sigmoid(g) = g / (1 + exp(-g))) of
  * one (gate, up) pair in binary32, in this order (reading R27):
- *   e = exp32(-g);  d = RN(1 + e);  s = RN(g / d);  y = RN(s * u). */
+ *   e = exp32(-g);  d = RN(1 + e);  s = RN(g * rcp32(d));  y = RN(s * u). */
 float oracle_swiglu32(float g, float u) {
-    const float e = oracle_exp32(-g);
-    const float d = 1.0f + e;
-    const float sg = g / d;
+    const float d = 1.0f + oracle_exp32(-g);
+    const float sg = g * oracle_rcp32(d);
     return sg * u;
 }
 

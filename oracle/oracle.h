@@ -74,11 +74,12 @@ void oracle_grouped_gemm(int32_t G, const int64_t* offsets, int64_t N, int64_t K
                          const uint8_t* B, const float* sB,
                          const int64_t* rows, int64_t nrows, double* O, int threads);
 
-/* SwiGLU FP8 epilogue of an up-projection (NEXT-2; R27).  exp32: the fixed binary32
- * exp sequence; swiglu32: RN(RN(g / RN(1 + exp32(-g))) * u).  H [M, 2I] FP32 with gate/up interleaved
+/* SwiGLU FP8 epilogue of an up-projection (NEXT-2; R27).  exp32 / rcp32: the fixed
+ * binary32 sequences; swiglu32: RN(RN(g * rcp32(RN(1 + exp32(-g)))) * u).  H [M, 2I] FP32 with gate/up interleaved
  * per 128 channels -> y [M, I] quantized 1x128 (qy, sy[(c/128)*ldsy + m]); qh/sh (optional, NULL to
  * skip): H itself quantized 1x128 (the FP8 cache of the SwiGLU inputs). */
 float oracle_exp32(float x);
+float oracle_rcp32(float d);
 float oracle_swiglu32(float g, float u);
 void oracle_swiglu_quant_1x128(const float* H, int64_t M, int64_t I, int64_t ldh,
                                uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,

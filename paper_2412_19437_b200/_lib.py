@@ -131,6 +131,13 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_grouped_gemm_wgrad.restype = st
         L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
                                                vp, i64, i32, vp]
+    if hasattr(L, "fp8bs_gemm_swiglu"):
+        L.fp8bs_gemm_swiglu.restype = st
+        L.fp8bs_gemm_swiglu.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                        vp, i64, vp]
+        L.fp8bs_grouped_gemm_swiglu.restype = st
+        L.fp8bs_grouped_gemm_swiglu.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i64,
+                                                vp, i64, vp, i64, vp, i64, vp, ctypes.c_size_t, vp]
     L.fp8bs_grouped_gemm_workspace_size.restype = ctypes.c_size_t
     L.fp8bs_grouped_gemm_workspace_size.argtypes = [ctypes.c_int32, i64, i64, i64]
     return L
@@ -394,3 +401,57 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
     _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
               _p(out), _dt(out), out.stride(0), _p(workspace), workspace.numel(), _stream(A)), name)
     return out
+
+
+def _swiglu_outputs(R: int, N2: int, dev, cache: bool, qy, sy, qh, sh):
+    I = N2 // 2
+    if qy is None:
+        qy = torch.empty(R, I, dtype=torch.uint8, device=dev)
+    if sy is None:
+        sy = torch.empty(I // 128, _pad4(R), dtype=torch.float32, device=dev)[:, :R]
+    if cache and qh is None:
+        qh = torch.empty(R, N2, dtype=torch.uint8, device=dev)
+    if cache and sh is None:
+        sh = torch.empty(N2 // 128, _pad4(R), dtype=torch.float32, device=dev)[:, :R]
+    return qy, sy, qh, sh
+
+
+def gemm_swiglu(A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor, cache: bool = True,
+                qy=None, sy=None, qh=None, sh=None):
+    """Up-projection with the SwiGLU FP8 epilogue (fp8bs_gemm_swiglu): A [M,K] codes, sA [K/128, M],
+    B [2I, K] codes with (gate, up) row blocks of 128, sB [2I/128, K/128].  Returns (qy [M, I] codes,
+    sy [I/128, M], qh [M, 2I] codes or None, sh [2I/128, M] or None)."""
+    for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
+        _cuda2d(t, n)
+    M, K = A.shape
+    N2 = B.shape[0]
+    qy, sy, qh, sh = _swiglu_outputs(M, N2, A.device, cache, qy, sy, qh, sh)
+    _check(lib().fp8bs_gemm_swiglu(M, N2, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
+                                   sB.stride(0), _p(qy), qy.stride(0), _p(sy), sy.stride(0), _p(qh),
+                                   qh.stride(0) if qh is not None else 0, _p(sh), sh.stride(0) if sh is not None else 0,
+                                   _stream(A)), "fp8bs_gemm_swiglu")
+    return qy, sy, qh, sh
+
+
+def grouped_gemm_swiglu(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+                        cache: bool = True, qy=None, sy=None, qh=None, sh=None, workspace: torch.Tensor | None = None):
+    """The grouped (MoE) expert up-projection with the SwiGLU FP8 epilogue (fp8bs_grouped_gemm_swiglu):
+    offsets int64 [G+1] (device), A [R,K], sA [K/128, R], B [G, 2I, K], sB [G, 2I/128, K/128]."""
+    _cuda2d(A, "A")
+    _cuda2d(sA, "sA")
+    if offsets.dtype != torch.int64 or not offsets.is_cuda:
+        raise ValueError("offsets must be a CUDA int64 tensor")
+    if not (B.is_cuda and B.is_contiguous() and sB.is_cuda and sB.is_contiguous()):
+        raise ValueError("B and sB must be contiguous CUDA tensors")
+    G, N2, K = B.shape
+    R = A.shape[0]
+    qy, sy, qh, sh = _swiglu_outputs(R, N2, A.device, cache, qy, sy, qh, sh)
+    if workspace is None:
+        wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N2, K))
+        workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
+    _check(lib().fp8bs_grouped_gemm_swiglu(G, R, N2, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
+                                           _p(sB), _p(qy), qy.stride(0), _p(sy), sy.stride(0), _p(qh),
+                                           qh.stride(0) if qh is not None else 0, _p(sh),
+                                           sh.stride(0) if sh is not None else 0, _p(workspace), workspace.numel(),
+                                           _stream(A)), "fp8bs_grouped_gemm_swiglu")
+    return qy, sy, qh, sh

@@ -345,6 +345,80 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     return from_cuda(e, mx ? "grouped_gemm_mx launch" : "grouped_gemm launch");
 }
 
+/* ---- SwiGLU FP8 epilogue of an up-projection (NEXT-2; reading R27) ---- */
+static fp8bs_status check_swiglu_out(int64_t M, int64_t N2, uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                                     uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh) {
+    if (N2 % 256) return fail(FP8BS_ERR_SHAPE, "N = 2I must be a multiple of 256 (gate/up blocks of 128)");
+    if (!qy || !sy) return fail(FP8BS_ERR_INVALID_ARG, "null pointer (qy, sy)");
+    if ((qh == nullptr) != (sh == nullptr)) return fail(FP8BS_ERR_INVALID_ARG, "qh and sh: both or neither");
+    if (ldqy < N2 / 2 || ldsy < M) return fail(FP8BS_ERR_SHAPE, "need ldqy >= N/2, ldsy >= M");
+    if (!aligned16(qy) || ldqy % 16) return fail(FP8BS_ERR_ALIGN, "qy must be 16-byte aligned, ldqy a multiple of 16");
+    if (reinterpret_cast<uintptr_t>(sy) % 4) return fail(FP8BS_ERR_ALIGN, "sy must be 4-byte aligned");
+    if (qh) {
+        if (ldqh < N2 || ldsh < M) return fail(FP8BS_ERR_SHAPE, "need ldqh >= N, ldsh >= M");
+        if (!aligned16(qh) || ldqh % 16) return fail(FP8BS_ERR_ALIGN, "qh must be 16-byte aligned, ldqh a multiple of 16");
+        if (reinterpret_cast<uintptr_t>(sh) % 4) return fail(FP8BS_ERR_ALIGN, "sh must be 4-byte aligned");
+    }
+    return FP8BS_OK;
+}
+
+fp8bs_status fp8bs_gemm_swiglu(int64_t M, int64_t N, int64_t K,
+                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                               uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                               uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh, fp8bs_stream_t stream) {
+    /* the GEMM operands as an FPROP with BF16 output (the output pointer is qy, checked below) */
+    fp8bs_status c = check_gemm_common(M, N, K, A, lda, sA, ldsA, B, ldb, sB, qy, FP8BS_BF16, N);
+    if (c != FP8BS_OK) return c;
+    if (M == 0 || N == 0) return ok();
+    if (ldsB < K / 128) return fail(FP8BS_ERR_SHAPE, "FPROP needs ldsB >= K/128");
+    c = check_swiglu_out(M, N, qy, ldqy, sy, ldsy, qh, ldqh, sh, ldsh);
+    if (c != FP8BS_OK) return c;
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    GemmArgs a{};
+    a.layout = FP8BS_FPROP; a.M = M; a.N = N; a.K = K;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = ldb; a.sB = sB; a.ldsB = ldsB;
+    a.D = qy; a.out_f32 = 0; a.ldd = ldqy; a.accumulate = 0;
+    a.swiglu = 1; a.sy = sy; a.ldsy = ldsy; a.qh = qh; a.ldqh = ldqh; a.sh = sh; a.ldsh = ldsh;
+    const char* detail = nullptr;
+    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
+    return from_cuda(e, "gemm_swiglu launch");
+}
+
+fp8bs_status fp8bs_grouped_gemm_swiglu(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                       const uint8_t* B, const float* sB,
+                                       uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
+                                       uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh,
+                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
+    if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
+    fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, qy, FP8BS_BF16, N);
+    if (c != FP8BS_OK) return c;
+    if (total_M == 0 || N == 0) return ok();
+    c = check_swiglu_out(total_M, N, qy, ldqy, sy, ldsy, qh, ldqh, sh, ldsh);
+    if (c != FP8BS_OK) return c;
+    const size_t need = grouped_workspace_bytes(G, total_M, N);
+    if (!workspace || workspace_bytes < need)
+        return fail(FP8BS_ERR_INVALID_ARG, "workspace of %zu bytes needed (fp8bs_grouped_gemm_workspace_size), got %zu",
+                    need, workspace_bytes);
+    if (!aligned16(workspace)) return fail(FP8BS_ERR_ALIGN, "workspace must be 16-byte aligned");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    GemmArgs a{};
+    a.layout = FP8BS_FPROP; a.M = total_M; a.N = N; a.K = K;
+    a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = K; a.sB = sB; a.ldsB = K / 128;
+    a.D = qy; a.out_f32 = 0; a.ldd = ldqy; a.accumulate = 0;
+    a.grouped = 1; a.G = G; a.offsets = offsets; a.workspace = workspace;
+    a.swiglu = 1; a.sy = sy; a.ldsy = ldsy; a.qh = qh; a.ldqh = ldqh; a.sh = sh; a.ldsh = ldsh;
+    const char* detail = nullptr;
+    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
+    return from_cuda(e, "grouped_gemm_swiglu launch");
+}
+
 /* ---- grouped MoE expert Wgrad on the expert-aligned (padded) token layout (NEXT-3) ---- */
 static int64_t padded_tokens(int32_t G, const int64_t* off) {
     if (G < 0 || !off || off[0] != 0) return -1;

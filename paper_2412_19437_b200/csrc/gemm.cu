@@ -111,6 +111,9 @@ struct KParams {
     int64_t sb_nb_stride, sb_kb_stride, sb_expert_stride;
     int NB;                       // ceil(N/128)
     void* D; int64_t ldd; int accumulate;
+    // SwiGLU epilogue (kOutSwiglu): D = qy codes [M, N/2] (ldd), sy [N/256][ldsy]; qh codes [M, N]
+    // (ldqh) and sh [N/128][ldsh] — the FP8 cache of H — when qh != nullptr
+    float* sy; int64_t ldsy; uint8_t* qh; int64_t ldqh; float* sh; int64_t ldsh;
     int G; const int64_t* offsets;
     void* tiles;                  // grouped: TileTable in the caller's workspace
     int gm;                       // raster band width (dense): tiles of the resident operand per band
@@ -271,15 +274,183 @@ __global__ void __launch_bounds__(1024) k_grouped_schedule(const int64_t* __rest
     }
 }
 
-template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
+// ------------------------------------------------------------------------------------------
+// SwiGLU FP8 epilogue (NEXT-2; reading R27).  The up-projection's columns come in
+// (gate, up) pairs of 128: a 256-column tile is exactly gate block j (half 0) and up block j (half
+// 1), so the promotion warps of a (gate, up) pair — same TMEM lane quadrant, hence the same 32 rows —
+// hold matching values, and one thread holds one row of a 1x128 group in its 128 accumulators.
+// ------------------------------------------------------------------------------------------
+// exp, 1/d and SwiGLU in binary32 by the fixed, branch-free sequences of reading R27 — operation
+// for operation oracle_exp32 / oracle_rcp32 / oracle_swiglu32 (fused multiply-adds are correctly
+// rounded on both sides), evaluated two elements at a time with the packed FP32 instructions, so the
+// epilogue is bit-reproducible against the oracle:
+//   x = clamp(-g, -86, 86); th = RN(x L2E), tl = fma(x, L2E_LO, fma(x, L2E, -th)); k = RNE(th);
+//   f = RN(RN(th - k) + tl); 2^f by a degree-7 Taylor polynomial (Horner, FMA); e = 2^f * 2^k via the
+//   exponent field; d = RN(1 + e); r = 0x7EF311C3 - bits(d), then three r = fma(r, fma(-d, r, 1), r);
+//   y = RN(RN(g r) u).
+__device__ __forceinline__ float2 swiglu32x2(const float2 g, const float2 u) {
+    const float2 x = make_float2(fminf(fmaxf(-g.x, -86.0f), 86.0f), fminf(fmaxf(-g.y, -86.0f), 86.0f));
+    const float2 L2E = make_float2(1.44269502162933349609375f, 1.44269502162933349609375f);
+    const float2 L2E_LO = make_float2(1.925963033500011079013347625732421875e-08f, 1.925963033500011079013347625732421875e-08f);
+    const float2 th = __fmul2_rn(x, L2E);
+    const float2 tl = __ffma2_rn(x, L2E_LO, __ffma2_rn(x, L2E, make_float2(-th.x, -th.y)));
+    const float2 k = make_float2(rintf(th.x), rintf(th.y));
+    const float2 f = __fadd2_rn(__fadd2_rn(th, make_float2(-k.x, -k.y)), tl);
+    float2 q = make_float2(1.5252733804059840e-5f, 1.5252733804059840e-5f);
+    q = __ffma2_rn(q, f, make_float2(1.5403530393381608e-4f, 1.5403530393381608e-4f));
+    q = __ffma2_rn(q, f, make_float2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
+    q = __ffma2_rn(q, f, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
+    q = __ffma2_rn(q, f, make_float2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
+    q = __ffma2_rn(q, f, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+    q = __ffma2_rn(q, f, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+    q = __ffma2_rn(q, f, make_float2(1.0f, 1.0f));
+    const float2 e = make_float2(__uint_as_float(__float_as_uint(q.x) + ((uint32_t)(int32_t)k.x << 23)),
+                                 __uint_as_float(__float_as_uint(q.y) + ((uint32_t)(int32_t)k.y << 23)));
+    const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), e);
+    float2 r = make_float2(__uint_as_float(0x7EF311C3u - __float_as_uint(d.x)), __uint_as_float(0x7EF311C3u - __float_as_uint(d.y)));
+    const float2 nd = make_float2(-d.x, -d.y), one = make_float2(1.0f, 1.0f);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r = __ffma2_rn(r, __ffma2_rn(nd, r, one), r);
+    return __fmul2_rn(__fmul2_rn(g, r), u);
+}
+
+// One thread's row of a 1x128 group in registers: v[0 .. 16 U) quantized with scale sc (RN32 of the
+// quotient, then RNE to E4M3 saturating: the quantizers' exact contract) and written as U 16-byte
+// stores to dst (the row's codes; rows are the lanes, so a warp's store touches 32 rows: the code rows
+// are short — 64 or 128 bytes — and staging them through shared memory for a TMA store cost a wait
+// on the TMA engine, which the producer's loads keep busy, on every tile).
+template <int U>
+__device__ __forceinline__ void encode_row_store(const float* v, float sc, uint8_t* dst, bool store) {
+    const float r = __frcp_rn(sc);
+    // warp-uniform choice (as the quantizer kernels): a per-lane branch around the IEEE-division
+    // slow path cost the epilogue ~40% of the GEMM's time
+    if (__all_sync(0xffffffffu, fast_div_ok(sc))) {
+        const float2 r2 = make_float2(r, r), ns2 = make_float2(-sc, -sc);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float* f = v + 16 * u + 4 * i;
+                const float2 a = div_scale2_fast(make_float2(f[0], f[1]), r2, ns2);
+                const float2 b = div_scale2_fast(make_float2(f[2], f[3]), r2, ns2);
+                w[i] = cvt_e4m3x2(a.x, a.y) | (cvt_e4m3x2(b.x, b.y) << 16);
+            }
+            if (store) *reinterpret_cast<uint4*>(dst + 16 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return;
+    }
+    const bool fast = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float* f = v + 16 * u + 4 * i;
+            if (fast) {
+                const float2 r2 = make_float2(r, r), ns2 = make_float2(-sc, -sc);
+                const float2 a = div_scale2_fast(make_float2(f[0], f[1]), r2, ns2);
+                const float2 b = div_scale2_fast(make_float2(f[2], f[3]), r2, ns2);
+                w[i] = cvt_e4m3x2(a.x, a.y) | (cvt_e4m3x2(b.x, b.y) << 16);
+            } else {
+                w[i] = cvt_e4m3x2(__fdiv_rn(f[0], sc), __fdiv_rn(f[1], sc)) |
+                       (cvt_e4m3x2(__fdiv_rn(f[2], sc), __fdiv_rn(f[3], sc)) << 16);
+            }
+        }
+        if (store) *reinterpret_cast<uint4*>(dst + 16 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+// maxNum of |v[0 .. n)| (the quantizers' amax)
+template <int N>
+__device__ __forceinline__ float row_amax(const float* v) {
+    float a = 0.0f;
+#pragma unroll
+    for (int j = 0; j < N; ++j) a = fmaxf(a, fabsf(v[j]));
+    return a;
+}
+
+template <int kH>
+__device__ __forceinline__ void swiglu_exchange(float (&acc)[128], int lane, uint32_t ebuf, uint32_t pbuf,
+                                                uint32_t pair_bar) {
+    constexpr int mine = kH == 0 ? 0 : 64, theirs = 64 - mine;
+#pragma unroll
+    for (int rd = 0; rd < 2; ++rd) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float* v = acc + theirs + 32 * rd + 4 * u;
+            sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), __float_as_uint(v[0]), __float_as_uint(v[1]),
+                      __float_as_uint(v[2]), __float_as_uint(v[3]));
+        }
+        named_bar_sync(pair_bar, 64);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint4 w = lds_u32x4(pbuf + lane * 128 + ((u ^ (lane & 7)) << 4));
+            float* a = acc + mine + 32 * rd + 4 * u;
+            const float2 o0 = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
+            const float2 o1 = make_float2(__uint_as_float(w.z), __uint_as_float(w.w));
+            const float2 m0 = make_float2(a[0], a[1]), m1 = make_float2(a[2], a[3]);
+            const float2 y0 = kH == 0 ? swiglu32x2(m0, o0) : swiglu32x2(o0, m0);
+            const float2 y1 = kH == 0 ? swiglu32x2(m1, o1) : swiglu32x2(o1, m1);
+            a[0] = y0.x; a[1] = y0.y; a[2] = y1.x; a[3] = y1.y;
+        }
+        named_bar_sync(pair_bar, 64);
+    }
+}
+
+// The epilogue of one (gate, up) warp pair (h = 0 gate, 1 up; ebuf = this warp's 4 KB staging buffer,
+// pbuf = the partner's); lane = one row (row < rows_here of the tile's expert: the rest belong to
+// the next expert and are not written):
+//   1. (p.qh) each warp quantizes its own 128 columns 1x128 — the FP8 cache of the SwiGLU inputs;
+//   2. the warps split the SwiGLU: the gate warp forms output columns [0, 64), the up warp [64, 128),
+//      each receiving the partner's operand through the partner's staging buffer (32 columns per
+//      round, two rounds, between pair barriers);
+//   3. the row amax of y meets through the up warp's buffer; each warp writes its 64 codes, the gate
+//      warp the row's scale.
+__device__ __forceinline__ void swiglu_epilogue(float (&acc)[128], int h, int quad, int lane, const Tile& tl,
+                                                int grow0, int rows_here, const KParams& p, uint32_t ebuf,
+                                                uint32_t pbuf) {
+    const uint32_t pair_bar = 1 + quad;   // named barrier of the (gate, up) pair: 64 threads
+    const bool row_ok = lane < rows_here;
+    const int64_t grow = grow0 + lane;
+    if (p.qh) {
+        const float sc = group_scale(row_amax<128>(acc));
+        const int col = tl.n0 + h * HN;
+        encode_row_store<8>(acc, sc, p.qh + grow * p.ldqh + col, row_ok);   // (whole warp: warp-uniform branch inside)
+        if (row_ok) p.sh[(int64_t)(col / 128) * p.ldsh + grow] = sc;
+    }
+    // 2. (h is a template argument: a runtime offset into acc would move it to local memory)
+    if (h == 0) swiglu_exchange<0>(acc, lane, ebuf, pbuf, pair_bar);
+    else swiglu_exchange<1>(acc, lane, ebuf, pbuf, pair_bar);
+    // 3. row amax over both halves (slots in the up warp's buffer, free after the exchange's last barrier)
+    const uint32_t up_buf = h == 0 ? pbuf : ebuf;
+    const float am = h == 0 ? row_amax<64>(acc) : row_amax<64>(acc + 64);
+    asm volatile("st.shared.f32 [%0], %1;" :: "r"(up_buf + 128u * h + 4u * lane), "f"(am) : "memory");
+    named_bar_sync(pair_bar, 64);
+    const float sc = group_scale(fmaxf(am, lds_f32(up_buf + 128u * (h ^ 1) + 4u * lane)));
+    named_bar_sync(pair_bar, 64);                // the slots are read before the next tile's exchange
+    const int col = tl.n0 / 2;                   // output channels of this tile: [n0 / 2, n0 / 2 + 128)
+    uint8_t* dst = reinterpret_cast<uint8_t*>(p.D) + grow * p.ldd + col;
+    if (h == 0) {
+        encode_row_store<4>(acc, sc, dst, row_ok);
+        if (row_ok) p.sy[(int64_t)(col / 128) * p.ldsy + grow] = sc;
+    } else {
+        encode_row_store<4>(acc + 64, sc, dst + 64, row_ok);
+    }
+}
+
+// kOut: 0 BF16 output, 1 FP32 output, 2 the SwiGLU FP8 epilogue (kOutSwiglu).
+constexpr int kOutBF16 = 0, kOutFP32 = 1, kOutSwiglu = 2;
+template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
 __global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-          const __grid_constant__ CUtensorMap tmD, const KParams p,
+          const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmD2, const KParams p,
           const __grid_constant__ GWSched<(kWgrad && kGrouped) ? kGWMax : 1> gw) {
     using C = Cfg<kPair, kWgrad>;
     // grouped Wgrad: one launch over every expert, each tile with its expert's contraction blocks
     constexpr bool kGW = kWgrad && kGrouped;
+    constexpr bool kOutF32 = kOut == kOutFP32;
+    constexpr bool kSwiglu = kOut == kOutSwiglu;
     extern __shared__ uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
@@ -745,6 +916,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // end stores its rows directly (rows past row_end belong to the next expert).
             const int grow0 = arow + quad * 32;
             const int rows_here = tl.row_end - grow0;
+            if constexpr (kSwiglu) {
+                static_assert(NC == 128 && C::EPI_BUFS == 1, "SwiGLU epilogue: 8 promotion warps, one staging buffer each");
+                // both warps of a (gate, up) pair share quad, hence rows_here
+                if (rows_here > 0) swiglu_epilogue(acc, h, quad, lane, tl, grow0, rows_here, p,
+                                                   smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES,
+                                                   smem_u32(s_epi) + (warp - 4 + (h == 0 ? 4 : -4)) * C::EPI_WARP_BYTES);
+            } else
             if ((kDbg & 2048) && active) {       // experiment: keep the math, skip the stores
                 float x = 0.0f;
 #pragma unroll
@@ -833,9 +1011,10 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
 
 static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)
 
-template <bool kWgrad, bool kOutF32, bool kGrouped, bool kPair>
+template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
     using C = Cfg<kPair, kWgrad>;
+    constexpr bool kOutF32 = kOut == kOutFP32, kSwiglu = kOut == kOutSwiglu;
     const int KB = (int)(a.K / BK);
     constexpr bool kGW = kWgrad && kGrouped;   // grouped Wgrad: A = dYqT [M, Mp], D = [G x M, N]
     const int64_t rows = a.M;   // total rows of A (total_M for grouped)
@@ -881,8 +1060,24 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     } else {
         tSB = tSA;
     }
-    CUtensorMap tD;
-    {
+    CUtensorMap tD, tD2;
+    if constexpr (kSwiglu) {
+        // codes: y [M, N/2] (D) and the H cache [M, N] (qh), 32 rows x 128 bytes per store
+        uint64_t dims[2] = {(uint64_t)(a.N / 2), (uint64_t)rows};
+        uint64_t str[1] = {(uint64_t)a.ldd};
+        uint32_t box[2] = {128, 32};
+        if (!make_tmap(&tD, TMAP_U8, 2, a.D, dims, str, box, 128)) {
+            *detail = "cuTensorMapEncodeTiled failed for the SwiGLU codes"; return cudaErrorInvalidValue;
+        }
+        tD2 = tD;
+        if (a.qh) {
+            uint64_t dh[2] = {(uint64_t)a.N, (uint64_t)rows};
+            uint64_t sh[1] = {(uint64_t)a.ldqh};
+            if (!make_tmap(&tD2, TMAP_U8, 2, a.qh, dh, sh, box, 128)) {
+                *detail = "cuTensorMapEncodeTiled failed for the SwiGLU input cache"; return cudaErrorInvalidValue;
+            }
+        }
+    } else {
         const uint64_t esz = kOutF32 ? 4 : 2;
         uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)(kGW ? rows * a.G : rows)};   // grouped Wgrad: experts stacked
         uint64_t str[1] = {(uint64_t)a.ldd * esz};
@@ -890,9 +1085,11 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         if (!make_tmap(&tD, kOutF32 ? TMAP_F32 : TMAP_BF16, 2, a.D, dims, str, box, 128)) {
             *detail = "cuTensorMapEncodeTiled failed for D"; return cudaErrorInvalidValue;
         }
+        tD2 = tD;
     }
     KParams p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
+    p.sy = a.sy; p.ldsy = a.ldsy; p.qh = a.qh; p.ldqh = a.ldqh; p.sh = a.sh; p.ldsh = a.ldsh;
     p.num_m = (int)((a.M + C::ROWS - 1) / C::ROWS); p.num_n = (int)((a.N + BN - 1) / BN);
     p.NB = (int)((a.N + 127) / 128);
     p.sB = a.sB;
@@ -932,7 +1129,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
                                    p.num_n, p.N, reinterpret_cast<TileTable*>(a.workspace));
         if (e != cudaSuccess) return e;
     }
-    auto kern = k_gemm_bs<kWgrad, kOutF32, kGrouped, kPair>;
+    auto kern = k_gemm_bs<kWgrad, kOut, kGrouped, kPair>;
     static bool attr[64] = {false};   // per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -959,7 +1156,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     } else {
         gw.e[0] = make_int2(0, 0);
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, p, gw);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tSA, tSB, tD, tD2, p, gw);
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
 }
@@ -972,14 +1169,18 @@ static int g_forced_variant = 0;
 
 template <bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
-    if (a.grouped && a.layout == 2) return launch_cfg<true, true, true, kPair>(a, st, detail);
-    if (a.grouped) {
-        return a.out_f32 ? launch_cfg<false, true, true, kPair>(a, st, detail)
-                         : launch_cfg<false, false, true, kPair>(a, st, detail);
+    if (a.grouped && a.layout == 2) return launch_cfg<true, kOutFP32, true, kPair>(a, st, detail);
+    if (a.swiglu) {
+        return a.grouped ? launch_cfg<false, kOutSwiglu, true, kPair>(a, st, detail)
+                         : launch_cfg<false, kOutSwiglu, false, kPair>(a, st, detail);
     }
-    if (a.layout == 2) return launch_cfg<true, true, false, kPair>(a, st, detail);
-    return a.out_f32 ? launch_cfg<false, true, false, kPair>(a, st, detail)
-                     : launch_cfg<false, false, false, kPair>(a, st, detail);
+    if (a.grouped) {
+        return a.out_f32 ? launch_cfg<false, kOutFP32, true, kPair>(a, st, detail)
+                         : launch_cfg<false, kOutBF16, true, kPair>(a, st, detail);
+    }
+    if (a.layout == 2) return launch_cfg<true, kOutFP32, false, kPair>(a, st, detail);
+    return a.out_f32 ? launch_cfg<false, kOutFP32, false, kPair>(a, st, detail)
+                     : launch_cfg<false, kOutBF16, false, kPair>(a, st, detail);
 }
 
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N) {

@@ -67,6 +67,9 @@ struct GemmArgs {
     int grouped; int32_t G; const int64_t* offsets;
     void* workspace;         // grouped: >= grouped_workspace_bytes(G, M, N) of device memory (tile table)
     const int* gw_kb;        // grouped Wgrad (layout 2): host [G][2] = {first 128-token block, blocks} per expert
+    // SwiGLU FP8 epilogue (FPROP; N = 2I, gate / up interleaved per 128 columns): D = y codes [M, I]
+    // (ldd), sy [I/128][ldsy]; optional FP8 cache of H: qh [M, N] (ldqh), sh [N/128][ldsh]
+    int swiglu; float* sy; int64_t ldsy; uint8_t* qh; int64_t ldqh; float* sh; int64_t ldsh;
 };
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
 
