@@ -17,7 +17,7 @@ fi
 C4="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-c1 --no-verify"
 C1="python bench.py --workload c1 --steps 2 --warmup 3 --no-e2e --no-cpu --no-pow2"
 timeout -s KILL 600 $C4 > $OUT/plain_c4_$TAG.log 2>&1 && \
-timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_quant|k_grouped|k_gemm' -c 2000 --csv \
     --log-file $OUT/launches_c4_$TAG.csv $C4 > $OUT/ncu_launches_c4_$TAG.log 2>&1; echo "ncu c4 launches rc=$?"
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_bs -s 3 -c 1 \
     -o $OUT/prof_grouped_$TAG $C4 > $OUT/ncu_grouped_$TAG.log 2>&1; echo "ncu grouped rc=$?"
