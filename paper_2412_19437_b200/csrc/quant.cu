@@ -341,6 +341,10 @@ k_quant_act_128x1(const T* __restrict__ x, int64_t M, int64_t C, int64_t ldx,
 // row groups, packed Markstein encode of row pairs (cvt of rows r, r+1 gives adjacent code bytes of
 // the transposed row directly), codes staged per channel and written as 128-byte rows of qT.
 // ===========================================================================================
+#ifndef FP8BS_DUAL_UNROLL
+#define FP8BS_DUAL_UNROLL 1
+#endif
+constexpr int kDualUnroll = FP8BS_DUAL_UNROLL;   // row passes of the dual quantizer in flight (experiments)
 template <typename T>
 struct QTCfg {
     static constexpr int CH = 256 / (int)sizeof(T);         // channels per tile: 128 BF16 / 64 FP32
@@ -352,6 +356,26 @@ struct QTCfg {
     static constexpr int QSTR = 144;
     static constexpr int OFF_Q = STAGES * TILE_BYTES;       // code staging [CH][QSTR]
     static constexpr int OFF_RED = OFF_Q + CH * QSTR;       // partial amax [4][CH]
+    static constexpr int OFF_BAR = OFF_RED + 4 * CH * 4;
+    static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
+};
+
+// The dual quantizer's stages: three 32 KB tiles in flight per CTA (two CTAs per SM), the 128x1
+// codes staged in the first 18 KB of the tile's own stage once its columns are in registers (the
+// stage is released after the copy-out) instead of a separate buffer — measured: with two stages
+// plus a separate 18 KB buffer the kernel waited on DRAM latency (4 tiles in flight per SM).
+#ifndef FP8BS_DUAL_STAGES
+#define FP8BS_DUAL_STAGES 3
+#endif
+struct QDCfg {
+    static constexpr int CH = 128, CPW = 2;                 // BF16: channels per tile, per 32-bit word
+    static constexpr int TILE_BYTES = 128 * 256;
+    static constexpr int STAGES = FP8BS_DUAL_STAGES;
+    static constexpr int CONSUMERS = 8;
+    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int QSTR = 144;                        // code staging [CH][QSTR] inside the stage
+    static_assert(CH * QSTR <= TILE_BYTES, "codes staged inside the stage");
+    static constexpr int OFF_RED = STAGES * TILE_BYTES;     // partial amax [4][CH]
     static constexpr int OFF_BAR = OFF_RED + 4 * CH * 4;
     static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
 };
@@ -547,12 +571,12 @@ k_quant_act_128x1_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_
 // Outputs are bit-identical to the two separate kernels.
 // ===========================================================================================
 template <bool kPow2 = false>
-__global__ void __launch_bounds__(QTCfg<__nv_bfloat16>::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
+__global__ void __launch_bounds__(QDCfg::THREADS, 2)   // 2 CTAs/SM: <= 112 registers
 k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t C,
                      uint8_t* __restrict__ q, int64_t ldq, float* __restrict__ s, int64_t lds,
                      uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
     using T = __nv_bfloat16;
-    using P = QTCfg<T>;
+    using P = QDCfg;
     extern __shared__ __align__(128) uint8_t smem[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
@@ -594,7 +618,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         uint8_t* qrow = q + (m0 + warp * 4 + sub) * ldq + c0 + li * 16;     // + pass * 32 rows
         float* srow = s + (int64_t)cb * lds + m0 + warp * 4 + sub;
         // ---- 1x128 along the channels: rows of the tile ----
-#pragma unroll 1
+#pragma unroll kDualUnroll
         for (int pass = 0; pass < 4; ++pass) {
             const int row = pass * 32 + warp * 4 + sub;
             float f[16];
@@ -625,12 +649,8 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         uint32_t w[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) w[r] = lds32(tile + (rg * 32 + r) * 256 + wc * 4);
-        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a proxy
-        // fence keeps the producer's next TMA into it behind these reads (an mbarrier arrive alone
-        // does not; see gemm.cu release_scales)
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
+        // (the stage stays held: its first 18 KB stage the 128x1 codes below, after the barrier that
+        // follows every thread's column loads; it is released after the copy-out)
         float sc[P::CPW];
         column_amax<T>(w, reinterpret_cast<float*>(smem + P::OFF_RED) + rg * P::CH + wc * P::CPW);
         named_bar_sync(1, 32 * P::CONSUMERS);
@@ -664,7 +684,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
                               (cvt_e4m3x2(__fdiv_rn(word_elem<T>(w[4 * k + 2], j), sc[j]), __fdiv_rn(word_elem<T>(w[4 * k + 3], j), sc[j])) << 16);
                 }
             }
-            const uint32_t qa = sbase + P::OFF_Q + (wc * P::CPW + j) * P::QSTR + rg * 32;
+            const uint32_t qa = tile + (wc * P::CPW + j) * P::QSTR + rg * 32;
             sts128(qa, make_uint4(code[0], code[1], code[2], code[3]));
             sts128(qa + 16, make_uint4(code[4], code[5], code[6], code[7]));
         }
@@ -672,10 +692,16 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         if (full) {
             // thread -> channel i * 32 + tid / 8, tokens (tid & 7) * 16 .. + 16 of the tile
             uint8_t* tb = qT + (c0 + (tid >> 3)) * ldqT + m0 + (tid & 7) * 16;
-            const uint32_t qs = sbase + P::OFF_Q + (tid >> 3) * P::QSTR + (tid & 7) * 16;
+            const uint32_t qs = tile + (tid >> 3) * P::QSTR + (tid & 7) * 16;
 #pragma unroll
             for (int i = 0; i < P::CH * 8 / (32 * P::CONSUMERS); ++i)
                 *reinterpret_cast<uint4*>(tb + (int64_t)(i * 32) * ldqT) = lds128(qs + i * 32 * P::QSTR);
+            // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a
+            // proxy fence keeps the producer's next TMA into it behind these reads (an mbarrier
+            // arrive alone does not; see gemm.cu release_scales)
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
             continue;
         }
 #pragma unroll
@@ -683,7 +709,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             const int idx = i * 32 * P::CONSUMERS + tid, chl = idx >> 3, pk = idx & 7;
             const int64_t c = c0 + chl, m = m0 + pk * 16;
             if (c < C && m < M) {
-                const uint4 val = lds128(sbase + P::OFF_Q + chl * P::QSTR + pk * 16);
+                const uint4 val = lds128(tile + chl * P::QSTR + pk * 16);
                 uint8_t* dst = qT + c * ldqT + m;
                 if (m + 16 <= M) {
                     *reinterpret_cast<uint4*>(dst) = val;
@@ -693,6 +719,12 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
                 }
             }
         }
+        // the stage was written by TMA (async proxy) and read with ld.shared (generic proxy): a
+        // proxy fence keeps the producer's next TMA into it behind these reads (an mbarrier
+        // arrive alone does not; see gemm.cu release_scales)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));     // stage consumed
     }
 }
 
@@ -1197,7 +1229,7 @@ cudaError_t launch_quant_act_128x1_grouped(const void* x, int xdt, int32_t G, co
 cudaError_t launch_quant_act_dual(const void* x, int xdt, int64_t M, int64_t K, int64_t ldx, uint8_t* q, int64_t ldq,
                                   float* s, int64_t lds, uint8_t* qT, int64_t ldqT, float* sT, int64_t ldsT,
                                   int pow2, cudaStream_t st) {
-    using Q = QTCfg<__nv_bfloat16>;
+    using Q = QDCfg;
     // fused path: BF16 (a 128-channel tile row is one 1x128 group), 16-byte aligned rows and codes
     bool fused = xdt == 0 && aligned16(x) && ((ldx * 2) % 16 == 0) && (K % 16 == 0) && aligned16(q) && (ldq % 16 == 0) &&
                  aligned16(qT) && (ldqT % 16 == 0) && (M * ((K + Q::CH - 1) / Q::CH) / 128 < (1ll << 31));
