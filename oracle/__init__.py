@@ -74,6 +74,9 @@ def lib():
         L.oracle_swiglu32.restype = ctypes.c_float
         L.oracle_swiglu32.argtypes = [ctypes.c_float, ctypes.c_float]
         L.oracle_swiglu_quant_1x128.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64]
+        L.oracle_float_to_bf16.restype = ctypes.c_uint16
+        L.oracle_float_to_bf16.argtypes = [ctypes.c_float]
+        L.oracle_combine_bf16.argtypes = [i64, i32, i64, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -187,6 +190,18 @@ def swiglu_quant_1x128(H: torch.Tensor, cache: bool = True):
     sh = torch.empty(N2 // 128, M, dtype=torch.float32) if cache else None
     lib().oracle_swiglu_quant_1x128(_ptr(H), M, I, N2, _ptr(qy), I, _ptr(sy), M, _ptr(qh), N2, _ptr(sh), M)
     return qy, sy, qh, sh
+
+
+def combine_bf16(y: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    """MoE combine (R28): y BF16 [T * top_k, N] (token t's k-th expert output at row
+    t * top_k + k), g FP32 [T, top_k] -> BF16 [T, N], fmaf-accumulated in k order from 0."""
+    T, top_k = g.shape
+    N = y.shape[1]
+    y = y.to(torch.bfloat16).contiguous()
+    g = g.to(torch.float32).contiguous()
+    out = torch.empty(T, N, dtype=torch.bfloat16)
+    lib().oracle_combine_bf16(T, top_k, N, _ptr(y), _ptr(g), _ptr(out))
+    return out
 
 
 def requantize_1x128_to_128x1(q: torch.Tensor, s: torch.Tensor, pow2: bool = False):

@@ -461,6 +461,30 @@ void oracle_swiglu_quant_1x128(const float* H, int64_t M, int64_t I, int64_t ldh
     free(y);
 }
 
+/* ------------------------------------------------ MoE combine (NEXT-3) ---- */
+/* binary32 -> BF16 bits, round to nearest even (NaN -> a quiet NaN of the same sign). */
+uint16_t oracle_float_to_bf16(float f) {
+    uint32_t u = f_bits(f);
+    if (isnan(f)) return (uint16_t)((u >> 16) | 0x40);
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7FFFu + lsb;                         /* ties to even on the 16 dropped bits */
+    return (uint16_t)(u >> 16);
+}
+
+/* The BF16 combine of routed-expert outputs (h'_t = u_t + sum_i g_{i,t} FFN_i(u_t); P:565-567:
+ * the combine runs in BF16): y holds, for token t, its top_k expert outputs at rows t * top_k + k
+ * (BF16 [T * top_k, N]); g [T, top_k] FP32 gates.  out[t][n] = BF16_RNE(acc), acc = 0.0f and
+ * acc = fmaf(g[t][k], y[t*top_k + k][n], acc) for k = 0 .. top_k - 1 (reading R28). */
+void oracle_combine_bf16(int64_t T, int top_k, int64_t N, const uint16_t* y, const float* g, uint16_t* out) {
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t n = 0; n < N; ++n) {
+            float acc = 0.0f;
+            for (int k = 0; k < top_k; ++k)
+                acc = fmaf(g[t * top_k + k], oracle_bf16_to_float(y[(t * top_k + k) * N + n]), acc);
+            out[t * N + n] = oracle_float_to_bf16(acc);
+        }
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

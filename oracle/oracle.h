@@ -85,6 +85,11 @@ void oracle_swiglu_quant_1x128(const float* H, int64_t M, int64_t I, int64_t ldh
                                uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
                                uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh);
 
+/* MoE combine (NEXT-3; R28): out[t] = BF16_RNE(sum_k g[t][k] y[t*top_k+k])
+ * accumulated with fmaf in k order from 0.0f; y, out BF16 bits. */
+uint16_t oracle_float_to_bf16(float f);
+void oracle_combine_bf16(int64_t T, int top_k, int64_t N, const uint16_t* y, const float* g, uint16_t* out);
+
 /* Hopper limited-precision accumulation emulation (context only; R24).
  * A [M,K] codes (ld lda), B [N,K] codes (ld ldb); per-row scales with the WGRAD layout:
  * sA(kb,i) = sA[kb*ldsA + i], sB(kb,j) = sB[kb*ldsB + j].  bits = retained bits (14 on

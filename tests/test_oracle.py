@@ -709,3 +709,38 @@ def test_swiglu_quant_is_the_composition():
     assert torch.equal(qh, hq) and torch.equal(sh.view(torch.int32), hs.view(torch.int32))
     assert float(sy[0, 0]) == 1.0 and not (qy[0, :128] & 0x7F).any()
     assert torch.equal(y[1, 128:256], (25.0 * H[1, 384:512]).to(torch.float32))
+
+
+# ------------------------------------------------------------------ MoE combine (NEXT-3, R28) ----
+def test_float_to_bf16_is_torch_rne():
+    """The oracle's binary32 -> BF16 rounding equals torch's (round to nearest even) on random, tie,
+    subnormal and special values."""
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(20000, generator=g) * 10.0 ** torch.randint(-40, 38, (20000,), generator=g).float()
+    ties = (torch.randint(0, 0x7F7F, (2000,), generator=g).to(torch.int32) << 16 | 0x8000).view(torch.float32)
+    x = torch.cat([x, ties, torch.tensor([0.0, -0.0, float("inf"), -float("inf"), 1e-45, 3.4e38])])
+    got = torch.tensor([oracle.lib().oracle_float_to_bf16(float(v)) for v in x.tolist()], dtype=torch.int32)
+    want = x.to(torch.bfloat16).view(torch.int16).to(torch.int32) & 0xFFFF
+    assert torch.equal(got, want)
+    assert (oracle.lib().oracle_float_to_bf16(float("nan")) & 0x7FC0) == 0x7FC0
+
+
+def test_combine_bf16_closed_form_and_numpy():
+    """combine_bf16: one-hot gates select one expert row exactly; unit gates on exactly representable
+    values give the exact sum; random gates agree with a float64 numpy composition within BF16's
+    rounding (the fmaf chain stays within 2^-20 relative before the final BF16 rounding)."""
+    T, k, N = 33, 8, 256
+    g = torch.Generator().manual_seed(10)
+    y = (torch.randn(T * k, N, generator=g) * 3).to(torch.bfloat16)
+    onehot = torch.zeros(T, k)
+    pick = torch.randint(0, k, (T,), generator=g)
+    onehot[torch.arange(T), pick] = 1.0
+    out = oracle.combine_bf16(y, onehot)
+    assert torch.equal(out.view(torch.int16), y.view(T, k, N)[torch.arange(T), pick].view(torch.int16))
+    yi = torch.randint(-8, 9, (T * k, N), generator=g).to(torch.bfloat16)
+    out = oracle.combine_bf16(yi, torch.ones(T, k))
+    assert torch.equal(out.float(), yi.float().view(T, k, N).sum(1))
+    gates = torch.rand(T, k, generator=g)
+    out = oracle.combine_bf16(y, gates)
+    ref = (y.double().view(T, k, N) * gates.double()[:, :, None]).sum(1)
+    assert torch.all((out.double() - ref).abs() <= ref.abs() * 2.0 ** -8 + 1e-30)
