@@ -243,6 +243,36 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int6
                                       void* D, fp8bs_dtype ddt, int64_t ldd,
                                       void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
+/* ---- Expert-parallel exchange over NVLink (NEXT-3; §3.3.4) ---------------------------
+ * "we quantize the activation before MoE up-projections into FP8 and then apply dispatch components
+ * ... the combine components ... retained in BF16".  The expert GEMM's rows live on the
+ * rank that owns the expert; these calls move them there and back with the kernels WRITING straight
+ * into the destination GPU's memory over NVLink / NVSwitch (one warp per row, 16-byte stores).
+ * recv_* are DEVICE arrays indexed by rank of pointers into each rank's receive buffer, mapped into the
+ * calling process (peer pointers: torch symmetric memory, CUDA IPC; the caller's own entry may point to
+ * local memory).  The calls only enqueue on `stream`: the caller orders them across GPUs (a barrier
+ * after the senders' kernels, before the receiver reads).  Rows with dst_rank < 0 are not sent.
+ *
+ * dispatch_fp8: token slot i (token i / top_k, its (i % top_k)-th expert; n_slots = tokens * top_k)
+ *   -> rank dst_rank[i], receive row dst_row[i]: the token's K codes xq [tokens, ldxq] to recv_q[r] +
+ *   row * ld_recv_q, and its K/128 scales xs [K/128, ldxs] (the 1x128 quantizer's layout) to
+ *   recv_s[r] + row * (K/128) (row-major: one contiguous run per row over the link).  K % 128 == 0.
+ * scales_rows_to_blocks: the received row-major [R][KB] scales -> the GEMM's [KB][ldd >= R].
+ * combine_push_bf16: expert output row i (BF16 y [R, ldy]) -> rank dst_rank[i]'s combine buffer row
+ *   dst_slot[i] (= token * top_k + k there), recv_y[r] + dst_slot[i] * ld_recv_y.  N % 8 == 0.
+ * combine_reduce_bf16: out[t] = BF16_RNE(sum_k gates[t][k] buf[t * top_k + k]) with the sum an FP32
+ *   fused multiply-add chain in k order from 0 (reading R28); buf, out BF16, gates FP32 [T, top_k]. */
+FP8BS_API fp8bs_status fp8bs_dispatch_fp8(int64_t n_slots, int32_t top_k, int64_t K, const uint8_t* xq, int64_t ldxq,
+                                const float* xs, int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row,
+                                uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, fp8bs_stream_t stream);
+FP8BS_API fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,
+                                         fp8bs_stream_t stream);
+FP8BS_API fp8bs_status fp8bs_combine_push_bf16(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,
+                                     const int64_t* dst_slot, void* const* recv_y, int64_t ld_recv_y,
+                                     fp8bs_stream_t stream);
+FP8BS_API fp8bs_status fp8bs_combine_reduce_bf16(int64_t T, int32_t top_k, int64_t N, const void* buf, int64_t ldb,
+                                       const float* gates, void* out, int64_t ldo, fp8bs_stream_t stream);
+
 /* ---- gemm_swiglu: the up-projection with its SwiGLU FP8 epilogue (NEXT-2) ---------------------
  * "we cache the inputs of the SwiGLU operator and recompute its output in the backward pass.
  * These activations are also stored in FP8 with our fine-grained quantization method"; and every

@@ -131,6 +131,15 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_grouped_gemm_wgrad.restype = st
         L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
                                                vp, i64, i32, vp]
+    if hasattr(L, "fp8bs_dispatch_fp8"):
+        L.fp8bs_dispatch_fp8.restype = st
+        L.fp8bs_dispatch_fp8.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
+        L.fp8bs_scales_rows_to_blocks.restype = st
+        L.fp8bs_scales_rows_to_blocks.argtypes = [i64, i64, vp, vp, i64, vp]
+        L.fp8bs_combine_push_bf16.restype = st
+        L.fp8bs_combine_push_bf16.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, vp]
+        L.fp8bs_combine_reduce_bf16.restype = st
+        L.fp8bs_combine_reduce_bf16.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, vp, i64, vp]
     if hasattr(L, "fp8bs_gemm_swiglu"):
         L.fp8bs_gemm_swiglu.restype = st
         L.fp8bs_gemm_swiglu.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64,
@@ -455,3 +464,51 @@ def grouped_gemm_swiglu(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor
                                            sh.stride(0) if sh is not None else 0, _p(workspace), workspace.numel(),
                                            _stream(A)), "fp8bs_grouped_gemm_swiglu")
     return qy, sy, qh, sh
+
+
+# --------------------------------------------------------- expert-parallel exchange ----
+def dispatch_fp8(xq: torch.Tensor, xs: torch.Tensor, top_k: int, dst_rank: torch.Tensor, dst_row: torch.Tensor,
+                 recv_q_ptrs: int, ld_recv_q: int, recv_s_ptrs: int):
+    """fp8bs_dispatch_fp8: the local tokens' 1x128 codes xq [T, K] and scales xs [K/128, T] to every
+    (token, k) slot's destination rank / row.  recv_*_ptrs: device addresses of [world] pointer arrays
+    (peer pointers, e.g. torch symmetric memory's buffer_ptrs_dev)."""
+    _cuda2d(xq, "xq")
+    _cuda2d(xs, "xs")
+    T, K = xq.shape
+    if dst_rank.dtype != torch.int32 or dst_row.dtype != torch.int64 or dst_rank.numel() != T * top_k \
+            or dst_row.numel() != T * top_k or not (dst_rank.is_cuda and dst_row.is_cuda):
+        raise ValueError("dst_rank int32 / dst_row int64 CUDA tensors of T * top_k slots")
+    _check(lib().fp8bs_dispatch_fp8(T * top_k, top_k, K, _p(xq), xq.stride(0), _p(xs), xs.stride(0), _p(dst_rank),
+                                    _p(dst_row), ctypes.c_void_p(recv_q_ptrs), ld_recv_q, ctypes.c_void_p(recv_s_ptrs),
+                                    _stream(xq)), "fp8bs_dispatch_fp8")
+
+
+def scales_rows_to_blocks(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Row-major [R, KB] scales -> [KB, R] (row pitch padded to a multiple of 4) (fp8bs_scales_rows_to_blocks)."""
+    _cuda2d(src, "src")
+    R, KB = src.shape
+    if out is None:
+        out = torch.empty(KB, _pad4(R), dtype=torch.float32, device=src.device)[:, :R]
+    _check(lib().fp8bs_scales_rows_to_blocks(R, KB, _p(src), _p(out), out.stride(0), _stream(src)),
+           "fp8bs_scales_rows_to_blocks")
+    return out
+
+
+def combine_push_bf16(y: torch.Tensor, dst_rank: torch.Tensor, dst_slot: torch.Tensor, recv_y_ptrs: int, ld_recv_y: int):
+    """fp8bs_combine_push_bf16: expert output rows y [R, N] BF16 to their token owners' combine buffers."""
+    _cuda2d(y, "y")
+    R, N = y.shape
+    _check(lib().fp8bs_combine_push_bf16(R, N, _p(y), y.stride(0), _p(dst_rank), _p(dst_slot),
+                                         ctypes.c_void_p(recv_y_ptrs), ld_recv_y, _stream(y)), "fp8bs_combine_push_bf16")
+
+
+def combine_reduce_bf16(buf: torch.Tensor, gates: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[t] = BF16(sum_k gates[t, k] * buf[t * top_k + k]) (fp8bs_combine_reduce_bf16; R28)."""
+    _cuda2d(buf, "buf")
+    T, top_k = gates.shape
+    N = buf.shape[1]
+    if out is None:
+        out = torch.empty(T, N, dtype=torch.bfloat16, device=buf.device)
+    _check(lib().fp8bs_combine_reduce_bf16(T, top_k, N, _p(buf), buf.stride(0), _p(gates.contiguous()), _p(out),
+                                           out.stride(0), _stream(buf)), "fp8bs_combine_reduce_bf16")
+    return out

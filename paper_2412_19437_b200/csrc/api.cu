@@ -345,6 +345,62 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     return from_cuda(e, mx ? "grouped_gemm_mx launch" : "grouped_gemm launch");
 }
 
+/* ---- expert-parallel exchange over NVLink peer memory (NEXT-3) ---- */
+fp8bs_status fp8bs_dispatch_fp8(int64_t n_slots, int32_t top_k, int64_t K, const uint8_t* xq, int64_t ldxq,
+                                const float* xs, int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row,
+                                uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, fp8bs_stream_t stream) {
+    if (n_slots < 0 || K < 0 || top_k < 1) return fail(FP8BS_ERR_INVALID_ARG, "negative size or top_k < 1");
+    if (n_slots == 0 || K == 0) return ok();
+    if (n_slots % top_k) return fail(FP8BS_ERR_SHAPE, "n_slots must be a multiple of top_k (slots of whole tokens)");
+    if (K % 128) return fail(FP8BS_ERR_SHAPE, "K must be a multiple of 128 (whole 1x128 groups)");
+    if (!xq || !xs || !dst_rank || !dst_row || !recv_q || !recv_s) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldxq < K || ld_recv_q < K || ldxs < n_slots / top_k) return fail(FP8BS_ERR_SHAPE, "need ldxq, ld_recv_q >= K, ldxs >= tokens");
+    if (!aligned16(xq) || ldxq % 16 || ld_recv_q % 16) return fail(FP8BS_ERR_ALIGN, "xq 16-byte aligned, ldxq and ld_recv_q multiples of 16");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_dispatch_fp8(n_slots, top_k, K, xq, ldxq, xs, ldxs, dst_rank, dst_row, recv_q, ld_recv_q, recv_s,
+                                         (cudaStream_t)stream), "dispatch_fp8 launch");
+}
+
+fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,
+                                         fp8bs_stream_t stream) {
+    if (R < 0 || KB < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
+    if (R == 0 || KB == 0) return ok();
+    if (!src || !dst) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldd < R) return fail(FP8BS_ERR_SHAPE, "need ldd >= R");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_rows_to_blocks(R, KB, src, dst, ldd, (cudaStream_t)stream), "scales_rows_to_blocks launch");
+}
+
+fp8bs_status fp8bs_combine_push_bf16(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,
+                                     const int64_t* dst_slot, void* const* recv_y, int64_t ld_recv_y,
+                                     fp8bs_stream_t stream) {
+    if (R < 0 || N < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
+    if (R == 0 || N == 0) return ok();
+    if (!y || !dst_rank || !dst_slot || !recv_y) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldy < N || ld_recv_y < N) return fail(FP8BS_ERR_SHAPE, "need ldy, ld_recv_y >= N");
+    if (!aligned16(y) || N % 8 || ldy % 8 || ld_recv_y % 8) return fail(FP8BS_ERR_ALIGN, "y 16-byte aligned; N, ldy, ld_recv_y multiples of 8");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_combine_push(R, N, y, ldy, dst_rank, dst_slot, recv_y, ld_recv_y, (cudaStream_t)stream),
+                     "combine_push_bf16 launch");
+}
+
+fp8bs_status fp8bs_combine_reduce_bf16(int64_t T, int32_t top_k, int64_t N, const void* buf, int64_t ldb,
+                                       const float* gates, void* out, int64_t ldo, fp8bs_stream_t stream) {
+    if (T < 0 || N < 0 || top_k < 1) return fail(FP8BS_ERR_INVALID_ARG, "negative size or top_k < 1");
+    if (T == 0 || N == 0) return ok();
+    if (!buf || !gates || !out) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldb < N || ldo < N) return fail(FP8BS_ERR_SHAPE, "need ldb, ldo >= N");
+    if (!aligned16(buf) || !aligned16(out) || N % 8 || ldb % 8 || ldo % 8)
+        return fail(FP8BS_ERR_ALIGN, "buf, out 16-byte aligned; N, ldb, ldo multiples of 8");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_combine_reduce(T, top_k, N, buf, ldb, gates, out, ldo, (cudaStream_t)stream),
+                     "combine_reduce_bf16 launch");
+}
+
 /* ---- SwiGLU FP8 epilogue of an up-projection (NEXT-2; reading R27) ---- */
 static fp8bs_status check_swiglu_out(int64_t M, int64_t N2, uint8_t* qy, int64_t ldqy, float* sy, int64_t ldsy,
                                      uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh) {

@@ -55,6 +55,16 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// expert-parallel exchange (ep.cu)
+cudaError_t launch_dispatch_fp8(int64_t n, int top_k, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
+                                int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
+                                int64_t ld_rq, float* const* recv_s, cudaStream_t st);
+cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st);
+cudaError_t launch_combine_push(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,
+                                const int64_t* dst_slot, void* const* recv_y, int64_t ld_recv_y, cudaStream_t st);
+cudaError_t launch_combine_reduce(int64_t T, int top_k, int64_t N, const void* buf, int64_t ldb, const float* g, void* out,
+                                  int64_t ldo, cudaStream_t st);
+
 struct GemmArgs {
     int layout;              // 0 FPROP, 1 DGRAD, 2 WGRAD
     int64_t M, N, K;

@@ -201,3 +201,99 @@ def gathered_equals_G1(pb: RankProblem, cfg: EPConfig, world: int, rank: int, de
     del ref_pb, ref, got
     torch.cuda.empty_cache()
     return ok
+
+
+# ------------------------------------------------------------------------------------------
+# The exchange steps (NEXT-3): FP8 dispatch of each token's 1x128 codes to the ranks
+# owning its experts, BF16 combine of the expert outputs back to the token's owner, both written
+# by the sender straight into the receiver's memory over NVLink (fp8bs_dispatch_fp8 /
+# fp8bs_combine_push_bf16 on torch symmetric-memory buffers).  Tokens are data-parallel: rank r
+# owns tokens token_shard(T, world, r).
+# ------------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class ExchangePlan:
+    """Where every slot goes (pure bookkeeping from the routes; identical on every rank)."""
+    t0: int; t1: int                 # this rank's tokens
+    e0: int; e1: int                 # this rank's experts
+    dst_rank: torch.Tensor           # int32 [(t1 - t0) * top_k]: owner of slot (t, j)'s expert
+    dst_row: torch.Tensor            # int64 [...]: its row in the owner's expert-grouped receive buffer
+    offsets: torch.Tensor            # int64 [e1 - e0 + 1]: this rank's received rows per expert
+    c_rank: torch.Tensor             # int32 [R_local]: token owner of each received row
+    c_slot: torch.Tensor             # int64 [R_local]: its slot (t - t0(owner)) * top_k + j there
+    rows: int                        # R_local
+
+
+def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int) -> ExchangePlan:
+    T, k = routes.shape
+    flat_e = routes.reshape(-1).to(torch.int64)
+    flat_t = torch.arange(T, dtype=torch.int64).repeat_interleave(k)
+    order = torch.argsort(flat_e * T + flat_t, stable=True)          # global row -> flat slot (as group_rows)
+    pos = torch.empty_like(order)
+    pos[order] = torch.arange(order.numel(), dtype=torch.int64)      # flat slot -> global row
+    counts = torch.bincount(flat_e, minlength=E)
+    offsets = torch.zeros(E + 1, dtype=torch.int64)
+    offsets[1:] = torch.cumsum(counts, 0)
+    e_start = torch.tensor([shard_range(E, world, r)[0] for r in range(world)] + [E], dtype=torch.int64)
+    owner_of_e = torch.searchsorted(e_start, torch.arange(E), right=True) - 1
+    t_start = torch.tensor([token_shard(T, world, r)[0] for r in range(world)] + [T], dtype=torch.int64)
+    t0, t1 = token_shard(T, world, rank)
+    e0, e1 = shard_range(E, world, rank)
+    sl = slice(t0 * k, t1 * k)
+    owner = owner_of_e[flat_e[sl]]
+    dst_row = pos[sl] - offsets[e_start[owner]]
+    g0, g1 = int(offsets[e0]), int(offsets[e1])
+    slots = order[g0:g1]                                              # flat slots of this rank's rows
+    tok = slots // k
+    tok_owner = torch.searchsorted(t_start, tok, right=True) - 1
+    c_slot = (tok - t_start[tok_owner]) * k + slots % k
+    return ExchangePlan(t0, t1, e0, e1, owner.to(torch.int32), dst_row, (offsets[e0:e1 + 1] - g0).clone(),
+                        tok_owner.to(torch.int32), c_slot, g1 - g0)
+
+
+class Exchange:
+    """Symmetric-memory receive buffers of the exchange (rendezvous over `group`): FP8 codes + row-major
+    scales for dispatch, BF16 expert outputs per token slot for combine."""
+
+    def __init__(self, group, device, max_rows: int, max_slots: int, K: int, N: int):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.K, self.N = K, N
+        self.recv_q = symm_mem.empty(max_rows, K, dtype=torch.uint8, device=device)
+        self.recv_s = symm_mem.empty(max_rows, K // 128, dtype=torch.float32, device=device)
+        self.recv_y = symm_mem.empty(max_slots, N, dtype=torch.bfloat16, device=device)
+        self.hq = symm_mem.rendezvous(self.recv_q, group)
+        self.hs = symm_mem.rendezvous(self.recv_s, group)
+        self.hy = symm_mem.rendezvous(self.recv_y, group)
+
+    def barrier(self):
+        """Every rank's kernels enqueued so far (their peer writes) complete before what follows."""
+        self.hq.barrier(channel=0)
+
+
+def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: torch.Tensor, top_k: int,
+                Bq: torch.Tensor, sB: torch.Tensor, ws: torch.Tensor | None = None, keep: dict | None = None):
+    """The expert layer's FP8 forward on this rank: 1x128 quantization of its tokens ->
+    FP8 dispatch over NVLink -> grouped Fprop over the received rows -> BF16 combine over NVLink ->
+    gate-weighted sum.  keep (optional dict) receives the intermediate tensors for verification."""
+    import paper_2412_19437_b200 as fp
+    xq, xs = fp.quantize_act_1x128(x_local)
+    fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, ex.K, ex.hs.buffer_ptrs_dev)
+    ex.barrier()
+    R = plan.rows
+    A = ex.recv_q[:R]
+    sA = fp.scales_rows_to_blocks(ex.recv_s[:R])
+    y = fp.grouped_gemm(plan.offsets_dev, A, sA, Bq, sB, workspace=ws)
+    fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, ex.N)
+    ex.barrier()
+    out = fp.combine_reduce_bf16(ex.recv_y[:(plan.t1 - plan.t0) * top_k], gates)
+    if keep is not None:
+        keep.update(xq=xq, xs=xs, A=A, sA=sA, y=y, out=out)
+    return out
+
+
+def plan_to_device(plan: ExchangePlan, device) -> ExchangePlan:
+    plan.dst_rank_dev = plan.dst_rank.to(device)
+    plan.dst_row_dev = plan.dst_row.to(device)
+    plan.offsets_dev = plan.offsets.to(device)
+    plan.c_rank_dev = plan.c_rank.to(device)
+    plan.c_slot_dev = plan.c_slot.to(device)
+    return plan

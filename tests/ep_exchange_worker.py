@@ -1,0 +1,107 @@
+"""Worker of tests/test_ep_exchange_gpu.py (torchrun, one process per GPU): the expert layer's FP8
+forward with the NVLink exchange (ep.moe_forward) on a seeded problem, checked on every rank:
+  * dispatch: the received FP8 rows and scales == a host gather of every rank's 1x128 codes (bitwise);
+  * expert GEMM: == the grouped GEMM on the host-gathered rows (bitwise);
+  * combine: == oracle.combine_bf16 of the gathered expert outputs with the rank's gates (bitwise).
+Then times the two exchanges alone (CUDA events) and reports bytes moved over NVLink per second.
+    torchrun --nproc-per-node 2 tests/ep_exchange_worker.py [tokens experts top_k K N] > result.json"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import torch.distributed as dist
+
+import oracle
+import paper_2412_19437_b200 as fp
+import workloads as W
+from paper_2412_19437_b200 import ep
+
+
+def main():
+    T, E, top_k, K, N = (int(a) for a in (sys.argv[1:6] if len(sys.argv) > 5 else (4096, 16, 4, 1024, 512)))
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    routes = W.route_skewed(T, E, top_k, seed=3)
+    tok, off = W.group_rows(routes, E)
+    plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
+    plan = ep.plan_to_device(plans[rank], dev)
+    x = W.gaussian_act(T, K, seed=0)
+    B = W.random_codes(E * N, K, seed=5).reshape(E, N, K)
+    sB = W.random_scales(E, N // 128, K // 128, seed=6)
+    g = torch.rand(T, top_k, generator=torch.Generator().manual_seed(7))
+    gates = g / g.sum(1, keepdim=True)
+    t0, t1, e0, e1 = plan.t0, plan.t1, plan.e0, plan.e1
+    x_local = x[t0:t1].to(dev)
+    Bq, sBl = B[e0:e1].contiguous().to(dev), sB[e0:e1].contiguous().to(dev)
+    gl = gates[t0:t1].contiguous().to(dev)
+    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(e1 - e0, max(plan.rows, 1), N, K)) + 16,
+                     dtype=torch.uint8, device=dev)
+    ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * top_k for p in plans), K, N)
+    keep = {}
+    out = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, keep=keep)
+    torch.cuda.synchronize()
+    # ---- verification (NCCL all_gather outside the measured calls) ----
+    def gather_cat(t, dim=0):
+        parts = ep.gather_rows(t.transpose(0, dim).contiguous() if dim else t.contiguous(), world)
+        cat = torch.cat(parts)
+        return cat.transpose(0, dim) if dim else cat
+    xq_all = gather_cat(keep["xq"])                       # [T, K] in token order
+    xs_all = gather_cat(keep["xs"], dim=1)                # [KB, T]
+    rows = tok[int(off[e0]):int(off[e1])].to(dev)
+    A_ref = xq_all.index_select(0, rows)
+    sA_ref = xs_all.index_select(1, rows)
+    res = {"rank": rank, "rows": plan.rows, "tokens": t1 - t0}
+    res["dispatch_codes_bitwise"] = bool(torch.equal(keep["A"], A_ref))
+    res["dispatch_scales_bitwise"] = bool(torch.equal(keep["sA"].contiguous().view(torch.int32), sA_ref.contiguous().view(torch.int32)))
+    sa_pad = torch.empty(sA_ref.shape[0], (plan.rows + 3) // 4 * 4, dtype=torch.float32, device=dev)[:, :plan.rows]
+    sa_pad.copy_(sA_ref)
+    y_ref = fp.grouped_gemm(plan.offsets_dev, A_ref.contiguous(), sa_pad, Bq, sBl)
+    res["expert_gemm_bitwise"] = bool(torch.equal(keep["y"].view(torch.int16), y_ref.view(torch.int16)))
+    y_all = gather_cat(keep["y"])                         # [T * top_k, N], global expert-grouped order
+    order = torch.argsort(routes.reshape(-1).to(torch.int64) * T + torch.arange(T).repeat_interleave(top_k), stable=True)
+    pos = torch.empty_like(order)
+    pos[order] = torch.arange(order.numel())
+    y_slots = y_all.cpu()[pos[t0 * top_k:t1 * top_k]]    # this rank's slots (t, j), t in [t0, t1)
+    ref = oracle.combine_bf16(y_slots, gates[t0:t1])
+    res["combine_bitwise_vs_oracle"] = bool(torch.equal(out.cpu().view(torch.int16), ref.view(torch.int16)))
+    # ---- timing of the exchanges alone ----
+    xq, xs = keep["xq"], keep["xs"]
+    remote_slots = int((plan.dst_rank != rank).sum())
+    remote_rows = int((plan.c_rank != rank).sum())
+
+    def timeit(fn, iters=20):
+        for _ in range(3):
+            fn()
+        ex.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / iters
+    ms_d = timeit(lambda: fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, K,
+                                          ex.hs.buffer_ptrs_dev))
+    ms_c = timeit(lambda: fp.combine_push_bf16(keep["y"], plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, N))
+    res["dispatch_ms"] = ms_d
+    res["dispatch_remote_GBps"] = remote_slots * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9
+    res["dispatch_total_GBps"] = (t1 - t0) * top_k * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9
+    res["combine_ms"] = ms_c
+    res["combine_remote_GBps"] = remote_rows * N * 2 / (ms_c * 1e-3) / 1e9
+    ex.barrier()
+    torch.cuda.synchronize()
+    allres = [None] * world
+    dist.all_gather_object(allres, res)
+    if rank == 0:
+        print(json.dumps({"world": world, "T": T, "E": E, "top_k": top_k, "K": K, "N": N, "ranks": allres}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,3 +89,29 @@ def test_gather_rows_gloo_world2():
     expert = torch.repeat_interleave(torch.arange(8), offsets[1:] - offsets[:-1])
     assert torch.equal(out[:, 0].long(), tok)
     assert torch.equal(out[:, 1].long(), expert)
+
+
+def test_exchange_plan_routes_every_slot_to_its_expert_row_and_back():
+    """ep.exchange_plan (NEXT-3 bookkeeping), for 1, 2 and 4 ranks: every (token, slot) of a rank's
+    token shard is sent to the rank owning its expert, at the row that the single-process grouping
+    (W.group_rows) gives that pair; every received row is sent back to its token's owner at the slot
+    (t - t0) * top_k + j; the receive rows of each rank cover its experts' rows exactly once."""
+    T, E, k = 600, 16, 4
+    routes = W.route_skewed(T, E, k, alpha=1.0, seed=3)
+    tok, off = W.group_rows(routes, E)
+    for world in (1, 2, 4):
+        plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
+        assert sum(p.rows for p in plans) == T * k
+        hit = [torch.zeros(p.rows, dtype=torch.int64) for p in plans]
+        for r, p in enumerate(plans):
+            assert torch.equal(p.offsets, off[p.e0:p.e1 + 1] - off[p.e0])
+            for i in range(p.dst_rank.numel()):
+                t, j = p.t0 + i // k, i % k
+                o, row = int(p.dst_rank[i]), int(p.dst_row[i])
+                q = plans[o]
+                assert q.e0 <= int(routes[t, j]) < q.e1
+                assert int(tok[row + int(off[q.e0])]) == t
+                hit[o][row] += 1
+                # and back: the received row returns to slot i of rank r
+                assert int(q.c_rank[row]) == r and int(q.c_slot[row]) == i
+        assert all(bool((h == 1).all()) for h in hit)
