@@ -463,6 +463,75 @@ def time_c4_e2e(args, world, pb, dev, rows, N, K):
             "pipelined": "2 device buffer sets; H2D, compute and D2H streams overlap across steps (PCIe-bound)"}
 
 
+def time_moe_forward(args, world, rank, dev, pb):
+    """N > 1, context (not the headline): the expert layer's whole FP8 forward with the NVLink exchange
+    (ep.moe_forward, NEXT-3): 1x128 quantization of the rank's tokens -> FP8 dispatch written into the
+    expert owners' memory -> grouped Fprop -> BF16 combine written back -> gate-weighted sum.  CUDA events
+    around each phase, max over ranks; dispatch / combine GB/s count the bytes that cross NVLink."""
+    import torch.distributed as dist
+    from paper_2412_19437_b200 import ep
+    import paper_2412_19437_b200 as fp
+    cfg = ep.EPConfig()
+    routes = ep.routes_for(cfg)
+    T, E, k, K, N = cfg.tokens, cfg.experts, cfg.top_k, cfg.hidden, cfg.inter
+    plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
+    plan = ep.plan_to_device(plans[rank], dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 100)
+    x = torch.randn(T, K, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    x_local = x[plan.t0:plan.t1].contiguous()
+    del x
+    gg = torch.rand(plan.t1 - plan.t0, k, generator=g, device=dev)
+    gates = (gg / gg.sum(1, keepdim=True)).contiguous()
+    ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * k for p in plans), K, N)
+    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(plan.e1 - plan.e0, 1), max(plan.rows, 1), N, K)) + 16,
+                     dtype=torch.uint8, device=dev)
+    steps = min(args.steps, 10)
+    for _ in range(args.warmup):
+        ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws)
+    torch.cuda.synchronize()
+    barrier(world)
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / steps, world, dev)
+    keep = {}
+    ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, keep=keep)
+    torch.cuda.synchronize()
+    xq, xs, y = keep["xq"], keep["xs"], keep["y"]
+
+    def phase(fn, iters=10):
+        fn()
+        ex.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / iters, world, dev)
+    ms_d = phase(lambda: fp.dispatch_fp8(xq, xs, k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, K,
+                                         ex.hs.buffer_ptrs_dev))
+    ms_c = phase(lambda: fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, N))
+    remote_d = gather_ints([int((plan.dst_rank != rank).sum())], world, dev)
+    remote_c = gather_ints([int((plan.c_rank != rank).sum())], world, dev)
+    rows = gather_ints([plan.rows], world, dev)
+    fl = sum(2.0 * r * N * K for r in rows)
+    ex.barrier()
+    torch.cuda.synchronize()
+    return {"what": "whole expert-layer FP8 forward per rank: quantize tokens -> NVLink FP8 dispatch -> grouped Fprop -> "
+                    "NVLink BF16 combine -> gate-weighted sum (ep.moe_forward; symmetric-memory barriers between)",
+            "ms_per_step": ms, "steps": steps, "value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s (expert GEMM flop / step)",
+            "dispatch_ms": ms_d, "dispatch_remote_GBps_per_rank": max(remote_d) * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9,
+            "combine_ms": ms_c, "combine_remote_GBps_per_rank": max(remote_c) * N * 2 / (ms_c * 1e-3) / 1e9,
+            "nvlink_reference_GBps_per_direction": 770}
+
+
 # ------------------------------------------------------------------- CPU oracle ----
 def c4_cpu_sample():
     """The C4 step on the CPU oracle, restricted to CPU_ROWS rows of every CPU_EXPERT_STRIDE-th expert
@@ -596,6 +665,7 @@ def main():
     ap.add_argument("--no-pow2", dest="pow2", action="store_false")
     ap.add_argument("--no-c1", dest="c1", action="store_false")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
+    ap.add_argument("--no-exchange", dest="exchange", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -610,6 +680,8 @@ def main():
     torch.cuda.set_device(dev)
     if args.workload == "c4":
         result, pb = time_c4(args, world, rank, dev)
+        if world > 1 and args.exchange:
+            result["c4_moe_forward"] = time_moe_forward(args, world, rank, dev, pb)
         del pb
         torch.cuda.empty_cache()
         if args.c1:
