@@ -302,6 +302,14 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_swiglu(int32_t G, int64_t total_M, int
                                        uint8_t* qh, int64_t ldqh, float* sh, int64_t ldsh,
                                        void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
+/* ---- grouped_gemm_dgrad_mx: the MoE expert Dgrad on UE8M0 block scaling (NEXT-1) ----------------
+ * fp8bs_grouped_gemm_dgrad's arguments and layouts (it takes no workspace), with fp8bs_gemm_mx's
+ * precondition: every sA and sB value an exact power of two in [2^-127, 2^127]. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                         const uint8_t* B, const float* sB,
+                                         void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream);
+
 /* ---- Grouped MoE expert Wgrad (NEXT-3) ------------------------------------------
  * dW_e [N, K] = sum over expert e's tokens t of dY[t, :]^T X[t, :]   (P:476-481 applied per expert;
  * Wgrad operands in 128x1 tiles along the tokens).  The contraction is each

@@ -112,6 +112,9 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_grouped_gemm_mx.restype = st
         L.fp8bs_grouped_gemm_mx.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32,
                                             i64, vp]
+    if hasattr(L, "fp8bs_grouped_gemm_dgrad_mx"):
+        L.fp8bs_grouped_gemm_dgrad_mx.restype = st
+        L.fp8bs_grouped_gemm_dgrad_mx.argtypes = L.fp8bs_grouped_gemm_mx.argtypes
     if hasattr(L, "fp8bs_gemm_mx"):
         L.fp8bs_gemm_mx.restype = st
         L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
@@ -396,11 +399,11 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
         out = torch.empty(R, N, dtype=out_dtype, device=A.device)
     if layout not in (FPROP, DGRAD):
         raise ValueError("grouped layouts: FPROP, DGRAD")
-    if mx:   # power-of-two scales on UE8M0 block scaling (fp8bs_grouped_gemm_mx, FPROP)
-        if layout != FPROP:
-            raise ValueError("grouped_gemm(mx=True): FPROP only")
-        _check(lib().fp8bs_grouped_gemm_mx(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
-                                           _p(sB), _p(out), _dt(out), out.stride(0), _stream(A)), "fp8bs_grouped_gemm_mx")
+    if mx:   # power-of-two scales on UE8M0 block scaling (fp8bs_grouped_gemm_mx / _dgrad_mx)
+        fn, name = ((lib().fp8bs_grouped_gemm_mx, "fp8bs_grouped_gemm_mx") if layout == FPROP
+                    else (lib().fp8bs_grouped_gemm_dgrad_mx, "fp8bs_grouped_gemm_dgrad_mx"))
+        _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB), _p(out), _dt(out),
+                  out.stride(0), _stream(A)), name)
         return out
     fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
                 else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))

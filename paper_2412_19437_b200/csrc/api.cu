@@ -304,6 +304,13 @@ fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_
     return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1);
 }
 
+fp8bs_status fp8bs_grouped_gemm_dgrad_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                         const uint8_t* B, const float* sB,
+                                         void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream) {
+    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1);
+}
+
 fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                       const uint8_t* B, const float* sB,

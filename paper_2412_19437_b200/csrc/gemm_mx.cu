@@ -110,7 +110,7 @@ __device__ __forceinline__ uint32_t ue8m0(float s) { return (__float_as_uint(s) 
 
 __device__ __forceinline__ float scale_b(const Params& p, int kb, int j, int e) {
     if (p.layout == 0) return __ldg(p.sB + (int64_t)e * p.sb_expert_stride + (int64_t)(j >> 7) * p.ldsB + kb);   // FPROP: [(G,) N/128][K/128]
-    if (p.layout == 1) return __ldg(p.sB + (int64_t)kb * p.ldsB + (j >> 7));     // DGRAD: [K/128][N/128]
+    if (p.layout == 1) return __ldg(p.sB + (int64_t)e * p.sb_expert_stride + (int64_t)kb * p.ldsB + (j >> 7));   // DGRAD: [(G,) K/128][N/128]
     return __ldg(p.sB + (int64_t)kb * p.ldsB + j);                               // WGRAD: [K/128][N]
 }
 

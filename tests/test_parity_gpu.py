@@ -595,3 +595,31 @@ def test_grouped_mx_vs_dense_mx_bitwise_and_oracle(counts):
     O = oracle.grouped_gemm(offsets, qa, sa, qb, sb)
     assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
     assert torch.equal(Db.cpu().view(torch.int16), D.cpu().to(torch.bfloat16).view(torch.int16))
+
+
+@pytest.mark.parametrize("counts", [[0, 1, 300, 128, 257, 0, 40], [700]], ids=["ragged", "one"])
+def test_grouped_dgrad_mx_closed_form_bitexact(counts):
+    """MoE expert Dgrad on UE8M0 block scaling (fp8bs_grouped_gemm_dgrad_mx, NEXT-1): closed-form
+    operands (codes {0, +-1, +-2}, power-of-two scales) keep every product and sum exact, so each
+    expert's rows equal the oracle's DGRAD on its segment bit for bit, and the dense fp8bs_gemm_mx
+    DGRAD on the segment."""
+    G, out_c, in_c = len(counts), 384, 264                # contraction = out
+    offsets = torch.zeros(G + 1, dtype=torch.int64)
+    offsets[1:] = torch.cumsum(torch.tensor(counts, dtype=torch.int64), 0)
+    R = int(offsets[-1])
+    qa = W.codes_small(R, out_c, seed=3)
+    sa = W.scales_pow2(out_c // 128, R, seed=4)
+    qbT = torch.stack([W.codes_small(in_c, out_c, seed=10 + e) for e in range(G)])
+    sb = torch.stack([W.scales_pow2(out_c // 128, (in_c + 127) // 128, seed=30 + e) for e in range(G)])
+    D = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qbT), dev(sb), out_dtype=torch.float32,
+                        layout=fp.DGRAD, mx=True)
+    torch.cuda.synchronize()
+    for e in range(G):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        O = oracle.gemm(oracle.DGRAD, qa[a:b].contiguous(), sa[:, a:b].contiguous(), qbT[e], sb[e])
+        assert_bits_equal(D[a:b], O.to(torch.float32), f"expert {e} vs oracle")
+        De = fp.gemm(fp.DGRAD, dev(qa[a:b].contiguous()), dev_scales(sa[:, a:b].contiguous()), dev(qbT[e]), dev(sb[e]),
+                     out_dtype=torch.float32, mx=True)
+        assert_bits_equal(D[a:b], De.cpu(), f"expert {e} vs dense mx")
