@@ -29,7 +29,8 @@ def timeit(fn, iters=5):
 def main():
     dev = "cuda"
     G, N, K = 256, 2048, 7168
-    for name, T, skew in (("C4 skewed 8192 tokens x top-8", 8192, True), ("C2 uniform 4096 tokens x top-8", 4096, False)):
+    for name, T, skew in (("C4 skewed 65536 tokens x top-8", 65536, True), ("C4 skewed 8192 tokens x top-8", 8192, True),
+                          ("C2 uniform 4096 tokens x top-8", 4096, False)):
         routes = W.route_skewed(T, G, 8, seed=3) if skew else W.route_uniform(T, G, 8, seed=3)
         _, offsets = W.group_rows(routes, G)
         R = int(offsets[-1])
