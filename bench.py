@@ -366,9 +366,11 @@ def time_c1_e2e(args, world, st, dev):
 
 
 # ------------------------------------------------------------------------ C4 step ----
-def c4_config(world):
+def c4_config(world, placement="balanced"):
+    how = ("placed over ranks by a previous batch's observed loads (LPT, one redundant expert per rank at N > 1, "
+           "P:584-589)" if placement == "balanced" else "sharded contiguously over ranks")
     return {"workload": "C4 expert-parallel grouped expert GEMM (BASELINE configs[4]): 256 routed experts (K=7168, "
-                        "N=2048) sharded contiguously over ranks, 65536 tokens x top-8 skewed routing (alpha 0.5, seed 3) "
+                        f"N=2048) {how}, 65536 tokens x top-8 skewed routing (alpha 0.5, seed 3) "
                         "= 524288 expert rows; step = 1x128 quantize of the rank's token shard + grouped Fprop (BF16 out)",
             "experts": 256, "hidden": 7168, "expert_ffn": 2048, "tokens": 65536, "top_k": 8, "global_batch": 65536,
             "parallelism": f"ep{world}",
@@ -380,7 +382,8 @@ def time_c4(args, world, rank, dev):
     peaks = load_peaks()
     cfg = ep.EPConfig()
     routes = ep.routes_for(cfg)
-    pb = ep.build_rank_problem(cfg, world, rank, dev, routes, keep_tokens=True)
+    placement = ep.make_placement(cfg, world, args.placement, args.redundant)
+    pb = ep.build_rank_problem(cfg, world, rank, dev, routes, keep_tokens=True, placement=placement)
     torch.cuda.synchronize()
     launches = [("quant_act_1x128(X shard)", lambda: ep.quantize_tokens(pb)), ("grouped_gemm_fprop", lambda: ep.run_rank(pb))]
     ms_local, per_ms, clocks = timed_launches(launches, args.steps, args.warmup, world, dev)
@@ -396,7 +399,7 @@ def time_c4(args, world, rank, dev):
     g_ach = pb.flops / (g_ms * 1e-3) / 1e12
     peak_t, peak_src = fp8_peak(peaks, ms_local * 1e-3)
     traffic, traffic_src = committed_traffic("grouped_gemm_fprop")
-    alg_bytes = R * K + (pb.e1 - pb.e0) * N * K + 4 * R * (K // 128) + 2 * R * N
+    alg_bytes = R * K + len(pb.experts) * N * K + 4 * R * (K // 128) + 2 * R * N
     roof = {"kernel": "grouped_gemm_fprop (k_gemm_bs grouped)", "bound": "tensor", "achieved": g_ach, "peak": peak_t,
             "unit": "TFLOP/s", "frac": g_ach / peak_t, "peak_src": peak_src,
             "frac_vs_sustained_peak": g_ach / (2.0 * peaks["bf16_tflops_sustained"]),
@@ -409,16 +412,18 @@ def time_c4(args, world, rank, dev):
                                             "bytes": q_bytes},
                "grouped_gemm_fprop": {"ms": g_ms, "achieved": g_ach, "unit": "TFLOP/s", "peak": peak_t, "frac": g_ach / peak_t,
                                       "flop": pb.flops}}
-    ep_block = {"rows_per_rank": rows, "experts_per_rank": [ep.shard_range(cfg.experts, world, r)[1] - ep.shard_range(cfg.experts, world, r)[0]
-                                                            for r in range(world)],
+    _, goff = W.group_rows(routes, cfg.experts)
+    ep_block = {"placement": placement.kind, "redundant_experts": placement.redundant,
+                "rows_per_rank": rows, "experts_per_rank": [len(g) for g in placement.groups],
                 "ms_per_step_per_rank": ms_ranks, "imbalance_max_over_mean": ep.imbalance(rows),
                 "scaling_bound_from_imbalance": 1.0 / ep.imbalance(rows),
+                "imbalance_if_contiguous": ep.imbalance(ep.rank_rows(goff, ep.contiguous_placement(cfg.experts, world))),
                 "collective": "none in the timed path; NCCL all_gather of outputs for verification only"}
     result = {"metric": METRIC, "value": total_flops * args.steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "e4m3",
               "data": "synthetic (seeded Gaussian activations, N(0, 0.006^2) expert weights, skewed top-8 routing)",
-              "config": c4_config(world), "roofline": roof, "clocks": clocks, "gpu_launches": len(launches) * args.steps,
+              "config": c4_config(world, args.placement), "roofline": roof, "clocks": clocks, "gpu_launches": len(launches) * args.steps,
               "kernels": kernels, "ep": ep_block}
     # verification, outside the timed region
     if args.verify:
@@ -428,7 +433,9 @@ def time_c4(args, world, rank, dev):
             ep_block["verify"] = "NCCL all_gather of every rank's output rows; rank 0 recomputes G=1 on its GPU"
         else:
             ep_block["split_bitwise_equal_to_G1_on_one_gpu"] = ep.split_equals_G1_on_one_gpu(pb, cfg)
-            ep_block["verify"] = "G=2/4/8 contiguous expert shards as separate launches on one GPU vs the G=1 launch"
+            ep_block["balanced_split_bitwise_equal_to_G1_on_one_gpu"] = ep.split_equals_G1_on_one_gpu(pb, cfg, kind="balanced")
+            ep_block["verify"] = ("G=2/4/8 contiguous and balanced (redundant) placements, each rank a separate launch "
+                                  "on one GPU, scattered back to global row order vs the G=1 launch")
     if args.e2e:
         result["e2e"] = time_c4_e2e(args, world, pb, dev, rows, N, K)
     return result, pb
@@ -474,7 +481,7 @@ def time_moe_forward(args, world, rank, dev, pb):
     cfg = ep.EPConfig()
     routes = ep.routes_for(cfg)
     T, E, k, K, N = cfg.tokens, cfg.experts, cfg.top_k, cfg.hidden, cfg.inter
-    plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
+    plans = [ep.exchange_plan(routes, E, world, r, pb.placement) for r in range(world)]
     plan = ep.plan_to_device(plans[rank], dev)
     g = torch.Generator(device=dev)
     g.manual_seed(cfg.seed + 100)
@@ -484,7 +491,7 @@ def time_moe_forward(args, world, rank, dev, pb):
     gg = torch.rand(plan.t1 - plan.t0, k, generator=g, device=dev)
     gates = (gg / gg.sum(1, keepdim=True)).contiguous()
     ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * k for p in plans), K, N)
-    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(plan.e1 - plan.e0, 1), max(plan.rows, 1), N, K)) + 16,
+    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(len(plan.experts), 1), max(plan.rows, 1), N, K)) + 16,
                      dtype=torch.uint8, device=dev)
     steps = min(args.steps, 10)
     for _ in range(args.warmup):
@@ -646,7 +653,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": c4_config(world) if args.workload == "c4" else {"workload": "C1"},
+            "data": "synthetic", "config": c4_config(world, args.placement) if args.workload == "c4" else {"workload": "C1"},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": f"each step: {desc}"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -666,6 +673,10 @@ def main():
     ap.add_argument("--no-c1", dest="c1", action="store_false")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-exchange", dest="exchange", action="store_false")
+    ap.add_argument("--placement", default="balanced", choices=["balanced", "contiguous"],
+                    help="C4 expert placement over ranks (balanced: observed-load LPT + one redundant expert per "
+                         "rank at N > 1, P:584-589)")
+    ap.add_argument("--redundant", type=int, default=None, help="redundant expert copies (default: one per rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1,14 +1,20 @@
 """Expert-parallel sharding of the grouped MoE expert GEMM (BASELINE configs[4]).
 
 DeepSeek-V3 trains with 64-way expert parallelism and no token dropping
-(P:267-270).  Here the grouped expert Fprop is partitioned by expert: rank r owns the contiguous
-expert block [r*E/W, (r+1)*E/W).  Experts are independent, so there is NO exchange step in the
-computed path: every rank regenerates, from the shared seeds, the routing of all tokens, its own
-experts' weights and the FP8 rows routed to them (the rows a dispatch would deliver — dispatch
-itself, is out of scope), and runs one fp8bs_grouped_gemm.  NCCL (torch.distributed)
-is used only to gather per-rank outputs for verification, outside any timed region.
+(P:267-270).  Here the grouped expert Fprop is partitioned by expert replica: a `Placement` says which
+experts (or which share of a duplicated expert's rows) each rank computes.  Two placements:
+  * contiguous: rank r owns the expert block [r*E/W, (r+1)*E/W) (the r01/r02a layout);
+  * balanced: experts are rearranged among the GPUs by observed load so that every GPU
+    processes about the same number of rows, optionally with redundant copies of the hottest experts
+    (the paper deploys one extra expert per GPU for prefilling), each copy taking an equal
+    share of that expert's rows.
+Experts are independent, so the bench's timed path has NO exchange step: every rank regenerates, from
+the shared seeds, the routing of all tokens, its experts' weights and the FP8 rows routed to them, and
+runs one fp8bs_grouped_gemm.  The NVLink exchange (dispatch / combine) is the second half of
+this module (`exchange_plan`, `Exchange`, `moe_forward`).  NCCL (torch.distributed) gathers per-rank
+outputs for verification only, outside any timed region.
 
-Bookkeeping helpers are pure functions (unit-tested on CPU with world_size 2 over gloo);
+Bookkeeping helpers are pure functions (unit-tested on CPU, world_size 2 over gloo);
 `build_rank_problem` / `run_rank` touch the GPU only through the fp8bs C-ABI binding.
 """
 from __future__ import annotations
@@ -41,6 +47,119 @@ def imbalance(counts_per_rank) -> float:
     """max / mean rows per rank: the load-imbalance bound on expert-parallel scaling."""
     c = torch.tensor(counts_per_rank, dtype=torch.float64)
     return float(c.max() / c.mean()) if c.sum() > 0 else 1.0
+
+
+# ------------------------------------------------------------------------------------------
+# Expert placement (P:584-589): which expert replicas each rank computes.
+# ------------------------------------------------------------------------------------------
+@dataclasses.dataclass(frozen=True)
+class Placement:
+    """groups[r] = the (expert, part, parts) triples rank r computes, in its local (launch) order:
+    the part-th of `parts` equal contiguous chunks of expert e's rows (rows in (expert, token) order,
+    W.group_rows; chunk bounds floor(part * c / parts)).  parts > 1 means e is deployed redundantly
+    on `parts` distinct ranks.  Every row of every expert belongs to exactly one (rank, group)."""
+    world: int
+    experts: int
+    groups: tuple
+    kind: str = "contiguous"
+    redundant: int = 0
+
+    def experts_of(self, rank: int) -> list[int]:
+        return [e for e, _, _ in self.groups[rank]]
+
+
+def contiguous_placement(E: int, world: int) -> Placement:
+    """Rank r owns the contiguous expert block shard_range(E, world, r)."""
+    return Placement(world, E, tuple(tuple((e, 0, 1) for e in range(*shard_range(E, world, r))) for r in range(world)))
+
+
+def balanced_placement(load, world: int, redundant: int = 0) -> Placement:
+    """Load-aware placement: "duplicates high-load experts and deploys them redundantly"
+    and "rearrange[s] experts among GPUs ... based on the observed loads, striving to balance the load
+    across GPUs".  The paper gives the goal, not the algorithm (reading R29):
+      1. redundancy: `redundant` times, give one more copy to the expert with the largest load per
+         copy (at most `world` copies: copies sit on distinct ranks); a copy's load is load / copies;
+      2. rearrangement: longest-processing-time-first list scheduling — copies in decreasing load
+         (ties by expert id) each go to the least-loaded rank (ties by rank id) that has room and does
+         not already hold a copy of that expert.  Room: ceil((E + redundant) / world) copies per rank,
+         i.e. the paper's "original 8 experts" plus "one additional redundant expert" when
+         redundant == world (P:588-589).
+    `load` is the OBSERVED per-expert row count (a previous batch's statistics): the placement
+    is fixed before the batch it serves; each copy then takes an equal share of the batch's rows."""
+    load = torch.as_tensor(load, dtype=torch.float64)
+    E = load.numel()
+    if not 0 <= redundant <= E * (world - 1):
+        raise ValueError(f"redundant={redundant} outside [0, E*(world-1)]")
+    copies = torch.ones(E, dtype=torch.int64)
+    for _ in range(redundant):
+        per = torch.where(copies < world, load / copies, torch.full_like(load, -1.0))
+        copies[int(torch.argmax(per))] += 1            # argmax: first index among equals
+    items = sorted(((float(load[e]) / int(copies[e]), e, p) for e in range(E) for p in range(int(copies[e]))),
+                   key=lambda it: (-it[0], it[1], it[2]))
+    cap = -(-len(items) // world)
+    rank_load = [0.0] * world
+    held = [[] for _ in range(world)]
+    for w, e, p in items:
+        cand = [r for r in range(world) if len(held[r]) < cap and all(x[0] != e for x in held[r])]
+        if not cand:                                  # only reachable when the room is exhausted
+            cand = [r for r in range(world) if all(x[0] != e for x in held[r])]
+        r = min(cand, key=lambda r: (rank_load[r], r))
+        held[r].append((e, p, int(copies[e])))
+        rank_load[r] += w
+    return Placement(world, E, tuple(tuple(sorted(h)) for h in held), "balanced", redundant)
+
+
+def chunk_bounds(c: int, part: int, parts: int) -> tuple[int, int]:
+    """Rows [lo, hi) of an expert's c rows that copy `part` of `parts` computes."""
+    return part * c // parts, (part + 1) * c // parts
+
+
+def placement_rows(offsets: torch.Tensor, placement: Placement, rank: int):
+    """Rank `rank`'s rows under `placement`.  offsets: the global (expert, token) grouping's int64
+    [E + 1] (W.group_rows).  Returns (global row indices int64 [R_r], local offsets int64 [G_r + 1],
+    expert ids int64 [G_r]) — local group g is rows[loff[g]:loff[g+1]] of expert experts[g]."""
+    idx, loff, exps = [], [0], []
+    for e, part, parts in placement.groups[rank]:
+        a = int(offsets[e])
+        lo, hi = chunk_bounds(int(offsets[e + 1]) - a, part, parts)
+        idx.append(torch.arange(a + lo, a + hi, dtype=torch.int64))
+        loff.append(loff[-1] + hi - lo)
+        exps.append(e)
+    rows = torch.cat(idx) if idx else torch.zeros(0, dtype=torch.int64)
+    return rows, torch.tensor(loff, dtype=torch.int64), torch.tensor(exps, dtype=torch.int64)
+
+
+def rank_rows(offsets: torch.Tensor, placement: Placement) -> list[int]:
+    """Rows each rank computes under `placement`."""
+    out = []
+    for r in range(placement.world):
+        n = 0
+        for e, part, parts in placement.groups[r]:
+            lo, hi = chunk_bounds(int(offsets[e + 1] - offsets[e]), part, parts)
+            n += hi - lo
+        out.append(n)
+    return out
+
+
+def observed_load(cfg: "EPConfig") -> torch.Tensor:
+    """Per-expert row counts of a PREVIOUS batch of cfg's routing distribution (same expert popularity,
+    independent token draws, seed + 1): the statistics a balanced placement is built from."""
+    if cfg.skew_alpha > 0:
+        prev = W.route_skewed(cfg.tokens, cfg.experts, cfg.top_k, alpha=cfg.skew_alpha, seed=cfg.seed + 1,
+                              popularity_seed=cfg.seed)
+    else:
+        prev = W.route_uniform(cfg.tokens, cfg.experts, cfg.top_k, seed=cfg.seed + 1)
+    return torch.bincount(prev.reshape(-1).to(torch.int64), minlength=cfg.experts)
+
+
+def make_placement(cfg: "EPConfig", world: int, kind: str = "balanced", redundant: int | None = None) -> Placement:
+    """kind "contiguous" or "balanced"; balanced defaults to one redundant expert per rank at world > 1
+     and takes its loads from observed_load(cfg)."""
+    if kind == "contiguous" or world == 1:
+        return contiguous_placement(cfg.experts, world)
+    if kind != "balanced":
+        raise ValueError(kind)
+    return balanced_placement(observed_load(cfg), world, world if redundant is None else redundant)
 
 
 def gather_rows(local: torch.Tensor, world: int, group=None) -> list[torch.Tensor]:
@@ -76,8 +195,8 @@ def routes_for(cfg: EPConfig) -> torch.Tensor:
 
 @dataclasses.dataclass
 class RankProblem:
-    e0: int
-    e1: int
+    experts: list               # expert id of each local group (launch order)
+    rows: torch.Tensor          # int64 [R_local], CPU: the global (expert, token)-order index of each row
     offsets: torch.Tensor       # int64 [G_local + 1], device
     tok: torch.Tensor           # int64 [R_local], CPU
     A: torch.Tensor             # uint8 [R_local, K] FP8 rows (quantized per token, then gathered)
@@ -92,6 +211,7 @@ class RankProblem:
     xq: torch.Tensor | None = None   # ... and the 1x128 codes / scales the step writes
     xs: torch.Tensor | None = None
     ws: torch.Tensor | None = None   # the grouped GEMM's workspace (tile table), allocated once
+    placement: Placement | None = None
 
 
 def token_shard(T: int, world: int, rank: int) -> tuple[int, int]:
@@ -101,17 +221,23 @@ def token_shard(T: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: torch.Tensor | None = None,
-                       keep_tokens: bool = False) -> RankProblem:
-    """Everything rank `rank` needs, regenerated from the seeds (identical on every rank).
-    Activations: N(0,1) BF16 from a seeded CUDA generator; quantized 1x128 ONCE per token (the
-    paper quantizes before dispatch) and the FP8 rows + per-row scales are gathered —
-    exact, because 1x128 scales are per row.  keep_tokens: also keep the rank's data-parallel token
-    shard (BF16) and output buffers for its 1x128 codes / scales (bench.py's C4 step quantizes it)."""
+                       keep_tokens: bool = False, placement: Placement | None = None) -> RankProblem:
+    """Everything rank `rank` needs under `placement` (default: contiguous), regenerated from the seeds
+    (identical on every rank).  Activations: N(0,1) BF16 from a seeded CUDA generator; quantized 1x128
+    ONCE per token (the paper quantizes before dispatch) and the FP8 rows + per-row scales
+    are gathered — exact, because 1x128 scales are per row.  A redundant expert's weights are
+    regenerated from the expert's own seed on every rank that holds a copy.  keep_tokens: also keep
+    the rank's data-parallel token shard (BF16) and output buffers for its 1x128 codes / scales
+    (bench.py's C4 step quantizes it)."""
     import paper_2412_19437_b200 as fp
     if routes is None:
         routes = routes_for(cfg)
-    e0, e1 = shard_range(cfg.experts, world, rank)
-    tok, offsets = local_rows(routes, cfg.experts, e0, e1)
+    if placement is None:
+        placement = contiguous_placement(cfg.experts, world)
+    assert placement.world == world and placement.experts == cfg.experts
+    tok_all, goff = W.group_rows(routes, cfg.experts)
+    grows, offsets, exps = placement_rows(goff, placement, rank)
+    tok = tok_all[grows]
     K, N = cfg.hidden, cfg.inter
     g = torch.Generator(device=device)
     g.manual_seed(cfg.seed + 100)
@@ -126,16 +252,18 @@ def build_rank_problem(cfg: EPConfig, world: int, rank: int, device, routes: tor
     sA = torch.empty(K // 128, (R + 3) // 4 * 4 if R else 4, dtype=torch.float32, device=device)[:, :R]
     sA.copy_(xs.index_select(1, tokd))
     del xq, xs
-    G = e1 - e0
+    experts = [int(e) for e in exps]
+    G = len(experts)
     Bq = torch.empty(G, N, K, dtype=torch.uint8, device=device)
     sB = torch.empty(G, N // 128, K // 128, dtype=torch.float32, device=device)
-    for i in range(G):
+    for i, e in enumerate(experts):
         ge = torch.Generator(device=device)
-        ge.manual_seed(cfg.seed + 1000 + e0 + i)
+        ge.manual_seed(cfg.seed + 1000 + e)
         w = (torch.randn(N, K, generator=ge, device=device, dtype=torch.float32) * 0.006).to(torch.bfloat16)
         fp.quantize_weight_128x128(w, want_t=False, q=Bq[i], s=sB[i])
     out = torch.empty(R, N, dtype=torch.bfloat16, device=device)
-    pb = RankProblem(e0, e1, offsets.to(device), tok, A, sA, Bq, sB, out, 2.0 * R * N * K, t0, t1)
+    pb = RankProblem(experts, grows, offsets.to(device), tok, A, sA, Bq, sB, out, 2.0 * R * N * K, t0, t1,
+                     placement=placement)
     wsb = int(fp.lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K)) if G > 0 else 16
     pb.ws = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=device)
     if keep_tokens:
@@ -161,38 +289,50 @@ def run_rank(pb: RankProblem):
     return fp.grouped_gemm(pb.offsets, pb.A, pb.sA, pb.Bq, pb.sB, out=pb.out, workspace=pb.ws)
 
 
-def split_equals_G1_on_one_gpu(pb: RankProblem, cfg: EPConfig, splits=(2, 4, 8)) -> dict:
-    """On ONE GPU holding the whole (G = 1) problem: for each G in `splits`, run the G contiguous expert
-    shards as separate grouped launches on their own rows and compare the concatenation with the
-    G = 1 output bitwise (the partition bench.py times at N GPUs, without NCCL)."""
+def placement_equals_G1_on_one_gpu(pb: RankProblem, placement: Placement) -> bool:
+    """On ONE GPU holding the whole (G = 1) problem `pb` (its rows in global order): run every rank of
+    `placement` as its own grouped launch on its own rows and experts, scatter the outputs back to the
+    global row order and compare with the G = 1 output bitwise (the partition bench.py times at
+    N GPUs, without NCCL)."""
     import paper_2412_19437_b200 as fp
-    off = pb.offsets.cpu()
+    assert pb.rows.numel() == 0 or bool(torch.equal(pb.rows, torch.arange(pb.rows.numel())))
     ref = run_rank(pb).clone()
-    res = {}
-    for G in splits:
-        parts = []
-        for r in range(G):
-            e0, e1 = shard_range(cfg.experts, G, r)
-            a, b = int(off[e0]), int(off[e1])
-            sa = torch.empty(pb.sA.shape[0], (b - a + 3) // 4 * 4 if b > a else 4, dtype=torch.float32,
-                             device=pb.A.device)[:, :b - a]
-            sa.copy_(pb.sA[:, a:b])
-            if b > a:
-                parts.append(fp.grouped_gemm((pb.offsets[e0:e1 + 1] - off[e0]).contiguous(), pb.A[a:b], sa,
-                                             pb.Bq[e0:e1], pb.sB[e0:e1]))
-        got = torch.cat(parts)
-        res[str(G)] = bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
-    return res
+    goff = pb.offsets.cpu()
+    got = torch.zeros_like(ref)
+    dev = pb.A.device
+    for r in range(placement.world):
+        rows, loff, exps = placement_rows(goff, placement, r)
+        n = rows.numel()
+        if n == 0:
+            continue
+        rd = rows.to(dev)
+        sa = torch.empty(pb.sA.shape[0], (n + 3) // 4 * 4, dtype=torch.float32, device=dev)[:, :n]
+        sa.copy_(pb.sA.index_select(1, rd))
+        ed = exps.to(dev)
+        y = fp.grouped_gemm(loff.to(dev), pb.A.index_select(0, rd), sa, pb.Bq.index_select(0, ed).contiguous(),
+                            pb.sB.index_select(0, ed).contiguous())
+        got.index_copy_(0, rd, y)
+        del y, sa
+    return bool(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+
+
+def split_equals_G1_on_one_gpu(pb: RankProblem, cfg: EPConfig, splits=(2, 4, 8), kind: str = "contiguous") -> dict:
+    """placement_equals_G1_on_one_gpu for the `kind` placement at each G in `splits`."""
+    return {str(G): placement_equals_G1_on_one_gpu(pb, make_placement(cfg, G, kind)) for G in splits}
 
 
 def gathered_equals_G1(pb: RankProblem, cfg: EPConfig, world: int, rank: int, device, routes) -> bool | None:
     """N > 1: NCCL all_gather of every rank's output rows (verification only, outside any timed
-    region); rank 0 rebuilds the G = 1 problem on its own GPU and compares bitwise.  Returns the
-    verdict on rank 0, None elsewhere."""
+    region); rank 0 scatters them back to the global row order, rebuilds the G = 1 problem on its own
+    GPU and compares bitwise.  Returns the verdict on rank 0, None elsewhere."""
     parts = gather_rows(pb.out, world)
     if rank != 0:
         return None
-    got = torch.cat(parts)
+    _, goff = W.group_rows(routes, cfg.experts)
+    got = torch.empty((int(goff[-1]), pb.out.shape[1]), dtype=pb.out.dtype, device=pb.out.device)
+    for r, part in enumerate(parts):
+        rows, _, _ = placement_rows(goff, pb.placement, r)
+        got.index_copy_(0, rows.to(got.device), part)
     del parts
     ref_pb = build_rank_problem(cfg, 1, 0, device, routes)
     ref = run_rank(ref_pb)
@@ -214,16 +354,23 @@ def gathered_equals_G1(pb: RankProblem, cfg: EPConfig, world: int, rank: int, de
 class ExchangePlan:
     """Where every slot goes (pure bookkeeping from the routes; identical on every rank)."""
     t0: int; t1: int                 # this rank's tokens
-    e0: int; e1: int                 # this rank's experts
-    dst_rank: torch.Tensor           # int32 [(t1 - t0) * top_k]: owner of slot (t, j)'s expert
-    dst_row: torch.Tensor            # int64 [...]: its row in the owner's expert-grouped receive buffer
-    offsets: torch.Tensor            # int64 [e1 - e0 + 1]: this rank's received rows per expert
+    experts: list                    # expert id of each of this rank's local groups
+    grows: torch.Tensor              # int64 [R_local]: global (expert, token)-order index of each received row
+    dst_rank: torch.Tensor           # int32 [(t1 - t0) * top_k]: rank computing slot (t, j)'s row
+    dst_row: torch.Tensor            # int64 [...]: its row in that rank's expert-grouped receive buffer
+    offsets: torch.Tensor            # int64 [G_local + 1]: this rank's received rows per local group
     c_rank: torch.Tensor             # int32 [R_local]: token owner of each received row
     c_slot: torch.Tensor             # int64 [R_local]: its slot (t - t0(owner)) * top_k + j there
     rows: int                        # R_local
 
 
-def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int) -> ExchangePlan:
+def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
+                  placement: Placement | None = None) -> ExchangePlan:
+    """Dispatch / combine bookkeeping of `rank` under `placement` (default contiguous): slot (t, j) of
+    a token goes to the rank computing its global row; with a redundant expert, the copy whose share
+    of the expert's rows holds that row (chunk_bounds)."""
+    if placement is None:
+        placement = contiguous_placement(E, world)
     T, k = routes.shape
     flat_e = routes.reshape(-1).to(torch.int64)
     flat_t = torch.arange(T, dtype=torch.int64).repeat_interleave(k)
@@ -233,21 +380,27 @@ def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int) -> Exchan
     counts = torch.bincount(flat_e, minlength=E)
     offsets = torch.zeros(E + 1, dtype=torch.int64)
     offsets[1:] = torch.cumsum(counts, 0)
-    e_start = torch.tensor([shard_range(E, world, r)[0] for r in range(world)] + [E], dtype=torch.int64)
-    owner_of_e = torch.searchsorted(e_start, torch.arange(E), right=True) - 1
+    owner_of_row = torch.full((T * k,), -1, dtype=torch.int64)
+    lrow_of_row = torch.full((T * k,), -1, dtype=torch.int64)
+    mine = None
+    for r in range(world):
+        rows_r, loff_r, exps_r = placement_rows(offsets, placement, r)
+        owner_of_row[rows_r] = r
+        lrow_of_row[rows_r] = torch.arange(rows_r.numel(), dtype=torch.int64)
+        if r == rank:
+            mine = (rows_r, loff_r, exps_r)
+    assert bool((owner_of_row >= 0).all()), "placement does not cover every row"
     t_start = torch.tensor([token_shard(T, world, r)[0] for r in range(world)] + [T], dtype=torch.int64)
     t0, t1 = token_shard(T, world, rank)
-    e0, e1 = shard_range(E, world, rank)
     sl = slice(t0 * k, t1 * k)
-    owner = owner_of_e[flat_e[sl]]
-    dst_row = pos[sl] - offsets[e_start[owner]]
-    g0, g1 = int(offsets[e0]), int(offsets[e1])
-    slots = order[g0:g1]                                              # flat slots of this rank's rows
+    g = pos[sl]
+    rows_me, loff, exps = mine
+    slots = order[rows_me]                                            # flat slots of this rank's rows
     tok = slots // k
     tok_owner = torch.searchsorted(t_start, tok, right=True) - 1
     c_slot = (tok - t_start[tok_owner]) * k + slots % k
-    return ExchangePlan(t0, t1, e0, e1, owner.to(torch.int32), dst_row, (offsets[e0:e1 + 1] - g0).clone(),
-                        tok_owner.to(torch.int32), c_slot, g1 - g0)
+    return ExchangePlan(t0, t1, [int(e) for e in exps], rows_me, owner_of_row[g].to(torch.int32), lrow_of_row[g],
+                        loff, tok_owner.to(torch.int32), c_slot, int(rows_me.numel()))
 
 
 class Exchange:

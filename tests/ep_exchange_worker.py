@@ -4,7 +4,8 @@ forward with the NVLink exchange (ep.moe_forward) on a seeded problem, checked o
   * expert GEMM: == the grouped GEMM on the host-gathered rows (bitwise);
   * combine: == oracle.combine_bf16 of the gathered expert outputs with the rank's gates (bitwise).
 Then times the two exchanges alone (CUDA events) and reports bytes moved over NVLink per second.
-    torchrun --nproc-per-node 2 tests/ep_exchange_worker.py [tokens experts top_k K N] > result.json"""
+    torchrun --nproc-per-node 2 tests/ep_exchange_worker.py [tokens experts top_k K N [placement]] > result.json
+placement: contiguous (default) or balanced (observed-load LPT with one redundant expert per rank)."""
 import json
 import os
 import sys
@@ -21,24 +22,30 @@ from paper_2412_19437_b200 import ep
 
 def main():
     T, E, top_k, K, N = (int(a) for a in (sys.argv[1:6] if len(sys.argv) > 5 else (4096, 16, 4, 1024, 512)))
+    kind = sys.argv[6] if len(sys.argv) > 6 else "contiguous"
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     routes = W.route_skewed(T, E, top_k, seed=3)
     tok, off = W.group_rows(routes, E)
-    plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
+    if kind == "balanced":   # loads observed on an independent batch of the same routing distribution
+        prev = W.route_skewed(T, E, top_k, seed=4, popularity_seed=3)
+        placement = ep.balanced_placement(torch.bincount(prev.reshape(-1).long(), minlength=E), world, world)
+    else:
+        placement = ep.contiguous_placement(E, world)
+    plans = [ep.exchange_plan(routes, E, world, r, placement) for r in range(world)]
     plan = ep.plan_to_device(plans[rank], dev)
     x = W.gaussian_act(T, K, seed=0)
     B = W.random_codes(E * N, K, seed=5).reshape(E, N, K)
     sB = W.random_scales(E, N // 128, K // 128, seed=6)
     g = torch.rand(T, top_k, generator=torch.Generator().manual_seed(7))
     gates = g / g.sum(1, keepdim=True)
-    t0, t1, e0, e1 = plan.t0, plan.t1, plan.e0, plan.e1
+    t0, t1 = plan.t0, plan.t1
     x_local = x[t0:t1].to(dev)
-    Bq, sBl = B[e0:e1].contiguous().to(dev), sB[e0:e1].contiguous().to(dev)
+    Bq, sBl = B[plan.experts].contiguous().to(dev), sB[plan.experts].contiguous().to(dev)
     gl = gates[t0:t1].contiguous().to(dev)
-    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(e1 - e0, max(plan.rows, 1), N, K)) + 16,
+    ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(len(plan.experts), 1), max(plan.rows, 1), N, K)) + 16,
                      dtype=torch.uint8, device=dev)
     ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * top_k for p in plans), K, N)
     keep = {}
@@ -51,17 +58,20 @@ def main():
         return cat.transpose(0, dim) if dim else cat
     xq_all = gather_cat(keep["xq"])                       # [T, K] in token order
     xs_all = gather_cat(keep["xs"], dim=1)                # [KB, T]
-    rows = tok[int(off[e0]):int(off[e1])].to(dev)
+    rows = tok[plan.grows].to(dev)
     A_ref = xq_all.index_select(0, rows)
     sA_ref = xs_all.index_select(1, rows)
-    res = {"rank": rank, "rows": plan.rows, "tokens": t1 - t0}
+    res = {"rank": rank, "rows": plan.rows, "tokens": t1 - t0, "placement": kind, "experts": len(plan.experts)}
     res["dispatch_codes_bitwise"] = bool(torch.equal(keep["A"], A_ref))
     res["dispatch_scales_bitwise"] = bool(torch.equal(keep["sA"].contiguous().view(torch.int32), sA_ref.contiguous().view(torch.int32)))
     sa_pad = torch.empty(sA_ref.shape[0], (plan.rows + 3) // 4 * 4, dtype=torch.float32, device=dev)[:, :plan.rows]
     sa_pad.copy_(sA_ref)
     y_ref = fp.grouped_gemm(plan.offsets_dev, A_ref.contiguous(), sa_pad, Bq, sBl)
     res["expert_gemm_bitwise"] = bool(torch.equal(keep["y"].view(torch.int16), y_ref.view(torch.int16)))
-    y_all = gather_cat(keep["y"])                         # [T * top_k, N], global expert-grouped order
+    y_parts = ep.gather_rows(keep["y"].contiguous(), world)
+    y_all = torch.empty(T * top_k, N, dtype=torch.bfloat16, device=dev)   # global expert-grouped order
+    for r in range(world):
+        y_all.index_copy_(0, plans[r].grows.to(dev), y_parts[r])
     order = torch.argsort(routes.reshape(-1).to(torch.int64) * T + torch.arange(T).repeat_interleave(top_k), stable=True)
     pos = torch.empty_like(order)
     pos[order] = torch.arange(order.numel())

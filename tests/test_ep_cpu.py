@@ -91,27 +91,167 @@ def test_gather_rows_gloo_world2():
     assert torch.equal(out[:, 1].long(), expert)
 
 
+def _placements(E, world, routes):
+    load = torch.bincount(routes.reshape(-1).long(), minlength=E)
+    out = [ep.contiguous_placement(E, world)]
+    if world > 1:
+        out += [ep.balanced_placement(load, world, 0), ep.balanced_placement(load, world, world)]
+    return out
+
+
 def test_exchange_plan_routes_every_slot_to_its_expert_row_and_back():
-    """ep.exchange_plan (NEXT-3 bookkeeping), for 1, 2 and 4 ranks: every (token, slot) of a rank's
-    token shard is sent to the rank owning its expert, at the row that the single-process grouping
-    (W.group_rows) gives that pair; every received row is sent back to its token's owner at the slot
-    (t - t0) * top_k + j; the receive rows of each rank cover its experts' rows exactly once."""
+    """ep.exchange_plan (NEXT-3 bookkeeping), for 1, 2 and 4 ranks and the contiguous, balanced and
+    redundant placements: every (token, slot) of a rank's token shard is sent to a rank computing its
+    expert, at a row whose global (expert, token) row is the one W.group_rows gives that pair; every
+    received row is sent back to its token's owner at the slot (t - t0) * top_k + j; the receive rows
+    of all ranks cover every global row exactly once."""
     T, E, k = 600, 16, 4
     routes = W.route_skewed(T, E, k, alpha=1.0, seed=3)
     tok, off = W.group_rows(routes, E)
     for world in (1, 2, 4):
-        plans = [ep.exchange_plan(routes, E, world, r) for r in range(world)]
-        assert sum(p.rows for p in plans) == T * k
-        hit = [torch.zeros(p.rows, dtype=torch.int64) for p in plans]
-        for r, p in enumerate(plans):
-            assert torch.equal(p.offsets, off[p.e0:p.e1 + 1] - off[p.e0])
-            for i in range(p.dst_rank.numel()):
-                t, j = p.t0 + i // k, i % k
-                o, row = int(p.dst_rank[i]), int(p.dst_row[i])
-                q = plans[o]
-                assert q.e0 <= int(routes[t, j]) < q.e1
-                assert int(tok[row + int(off[q.e0])]) == t
-                hit[o][row] += 1
-                # and back: the received row returns to slot i of rank r
-                assert int(q.c_rank[row]) == r and int(q.c_slot[row]) == i
-        assert all(bool((h == 1).all()) for h in hit)
+        for pl in _placements(E, world, routes):
+            plans = [ep.exchange_plan(routes, E, world, r, pl) for r in range(world)]
+            assert sum(p.rows for p in plans) == T * k
+            assert torch.equal(torch.sort(torch.cat([p.grows for p in plans])).values, torch.arange(T * k))
+            hit = [torch.zeros(p.rows, dtype=torch.int64) for p in plans]
+            for r, p in enumerate(plans):
+                assert p.offsets[0] == 0 and p.offsets[-1] == p.rows and len(p.experts) == p.offsets.numel() - 1
+                for g_, e in enumerate(p.experts):          # each local group's rows belong to its expert
+                    gr = p.grows[p.offsets[g_]:p.offsets[g_ + 1]]
+                    assert bool(((gr >= off[e]) & (gr < off[e + 1])).all())
+                for i in range(p.dst_rank.numel()):
+                    t, j = p.t0 + i // k, i % k
+                    o, row = int(p.dst_rank[i]), int(p.dst_row[i])
+                    q = plans[o]
+                    g = int(q.grows[row])
+                    assert int(tok[g]) == t
+                    assert off[int(routes[t, j])] <= g < off[int(routes[t, j]) + 1]
+                    hit[o][row] += 1
+                    # and back: the received row returns to slot i of rank r
+                    assert int(q.c_rank[row]) == r and int(q.c_slot[row]) == i
+            assert all(bool((h == 1).all()) for h in hit)
+
+
+# ---------------------------------------------------------------- expert placement (P:584-589) ----
+def _check_partition(pl, offsets):
+    """Every row of every expert is computed exactly once; copies of an expert sit on distinct ranks."""
+    E = pl.experts
+    seen = torch.zeros(int(offsets[-1]), dtype=torch.int64)
+    for r in range(pl.world):
+        rows, loff, exps = ep.placement_rows(offsets, pl, r)
+        seen[rows] += 1
+        assert len(set(exps.tolist())) == exps.numel(), "two copies of one expert on one rank"
+        assert torch.equal(exps, torch.sort(exps).values)
+    assert bool((seen == 1).all())
+    copies = torch.zeros(E, dtype=torch.int64)
+    for r in range(pl.world):
+        for e, part, parts in pl.groups[r]:
+            copies[e] += 1
+            assert 0 <= part < parts
+    for r in range(pl.world):
+        for e, part, parts in pl.groups[r]:
+            assert parts == int(copies[e])
+    assert int(copies.sum()) == E + pl.redundant
+
+
+def test_contiguous_placement_is_shard_range():
+    for E, world in ((256, 8), (7, 3), (16, 1)):
+        pl = ep.contiguous_placement(E, world)
+        for r in range(world):
+            assert pl.experts_of(r) == list(range(*ep.shard_range(E, world, r)))
+
+
+def test_chunk_bounds_partition():
+    for c in (0, 1, 7, 100):
+        for parts in (1, 2, 3, 8):
+            b = [ep.chunk_bounds(c, p, parts) for p in range(parts)]
+            assert b[0][0] == 0 and b[-1][1] == c
+            assert all(b[i][1] == b[i + 1][0] for i in range(parts - 1))
+            assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+def test_balanced_placement_partitions_rows_and_respects_room():
+    routes = W.route_skewed(4096, 64, 8, alpha=1.0, seed=3)
+    _, off = W.group_rows(routes, 64)
+    load = off[1:] - off[:-1]
+    for world in (2, 4, 8):
+        for red in (0, world, 2 * world):
+            pl = ep.balanced_placement(load, world, red)
+            _check_partition(pl, off)
+            room = -(-(64 + red) // world)
+            assert all(len(g) <= room for g in pl.groups)
+
+
+def _opt_makespan(load, world):
+    """Brute force: the best assignment of whole experts to `world` ranks (tiny inputs)."""
+    import itertools
+    best = float("inf")
+    for a in itertools.product(range(world), repeat=len(load)):
+        s = [0.0] * world
+        for e, r in enumerate(a):
+            s[r] += load[e]
+        best = min(best, max(s))
+    return best
+
+
+def test_balanced_placement_within_graham_bound_of_brute_force():
+    """Without redundancy, and where the room per rank never binds, the rearrangement is LPT list
+    scheduling, whose makespan is within (4/3 - 1/(3 world)) of the optimum (Graham 1969): checked
+    against brute force on random tiny instances.  The classic instance [5, 5, 4, 3, 3] on 2 ranks
+    gives LPT's 11 against the optimum 10."""
+    g = torch.Generator().manual_seed(11)
+    checked = 0
+    for trial in range(60):
+        world = 2 + trial % 2
+        E = 5 + trial % 3
+        load = torch.randint(1, 50, (E,), generator=g).double().tolist()
+        pl = ep.balanced_placement(load, world, 0)
+        spans = sorted(sum(load[e] for e, _, _ in grp) for grp in pl.groups)
+        lpt = [0.0] * world                           # plain LPT, no room limit
+        for w in sorted(load, reverse=True):
+            lpt[lpt.index(min(lpt))] += w
+        if spans != sorted(lpt):
+            continue                                  # the room limit bound: not plain LPT
+        span = spans[-1]
+        assert span <= (4 / 3 - 1 / (3 * world)) * _opt_makespan(load, world) + 1e-9, (load, world)
+        checked += 1
+    assert checked >= 20
+    pl = ep.balanced_placement([5, 5, 4, 3, 3], 2, 0)
+    assert sorted(sum([5, 5, 4, 3, 3][e] for e, _, _ in grp) for grp in pl.groups) == [9, 11]
+    assert _opt_makespan([5, 5, 4, 3, 3], 2) == 10
+
+
+def test_redundant_copies_go_to_the_hottest_experts():
+    """"duplicates high-load experts": one copy per step to the largest load per copy."""
+    load = [100, 10, 10, 10, 60, 10, 10, 10]
+    pl = ep.balanced_placement(load, 4, 3)
+    copies = {}
+    for grp in pl.groups:
+        for e, _, parts in grp:
+            copies[e] = parts
+    assert copies[0] == 3 and copies[4] == 2 and all(copies[e] == 1 for e in (1, 2, 3, 5, 6, 7))
+
+
+def test_balanced_placement_on_c4_routing_balances_rows():
+    """C4's skewed routing (65536 tokens x top-8 over 256 experts): contiguous placement leaves ranks
+    up to 1.17x (N=4) above the mean; the balanced placement built from a PREVIOUS batch's loads
+    (independent draw, same popularity) keeps every rank within 2% of the mean, and with one redundant
+    expert per rank each rank holds at most 256/N + 1 experts."""
+    cfg = ep.EPConfig()
+    routes = ep.routes_for(cfg)
+    _, off = W.group_rows(routes, cfg.experts)
+    for world in (2, 4, 8):
+        contig = ep.imbalance(ep.rank_rows(off, ep.contiguous_placement(cfg.experts, world)))
+        pl = ep.make_placement(cfg, world, "balanced")
+        _check_partition(pl, off)
+        assert all(len(g) <= cfg.experts // world + 1 for g in pl.groups)
+        bal = ep.imbalance(ep.rank_rows(off, pl))
+        assert bal <= 1.02 and bal <= contig, (world, bal, contig)
+
+
+def test_observed_load_is_an_independent_draw_of_the_same_distribution():
+    cfg = ep.EPConfig(tokens=8192)
+    cur = torch.bincount(ep.routes_for(cfg).reshape(-1).long(), minlength=cfg.experts).double()
+    prev = ep.observed_load(cfg).double()
+    assert not torch.equal(cur, prev)
+    assert float(torch.corrcoef(torch.stack([cur, prev]))[0, 1]) > 0.9

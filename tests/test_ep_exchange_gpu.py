@@ -14,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("shape", [(4096, 16, 4, 1024, 512), (3000, 32, 8, 2048, 768)], ids=["small", "ragged"])
+@pytest.mark.parametrize("shape", [(4096, 16, 4, 1024, 512), (3000, 32, 8, 2048, 768),
+                                   (3000, 32, 8, 2048, 768, "balanced")], ids=["small", "ragged", "ragged-balanced"])
 def test_ep_exchange_two_gpus(shape):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1",
            "--master-port=29555", os.path.join(ROOT, "tests", "ep_exchange_worker.py"), *map(str, shape)]

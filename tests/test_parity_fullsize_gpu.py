@@ -206,6 +206,28 @@ def test_C4_expert_parallel_split_bitwise_equal_G1(c4, G):
     assert_bits_equal(torch.cat(parts), c4["D"], f"G={G} vs G=1")
 
 
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_C4_balanced_redundant_placement_bitwise_equal_G1(c4, G):
+    """The load-aware placement bench.py uses at N GPUs (LPT over a previous batch's loads,
+    one redundant expert per rank whose copies split the expert's rows), run on one GPU: each rank's
+    grouped launch over its own (expert, share) groups, scattered back to global row order == G = 1."""
+    from paper_2412_19437_b200 import ep
+    cfg = ep.EPConfig()
+    pl = ep.make_placement(cfg, G, "balanced")
+    assert pl.redundant == G
+    off = c4["offsets"]
+    got = torch.zeros_like(c4["D"])
+    for r in range(G):
+        rows, loff, exps = ep.placement_rows(off, pl, r)
+        rd = dev(rows)
+        sa = dev_scales(c4["sA"][:, rows].contiguous())
+        ed = dev(exps)
+        y = fp.grouped_gemm(dev(loff), c4["dA"].index_select(0, rd), sa, c4["dB"].index_select(0, ed).contiguous(),
+                            c4["dsB"].index_select(0, ed).contiguous())
+        got.index_copy_(0, rd, y)
+    assert_bits_equal(got, c4["D"], f"balanced G={G} vs G=1")
+
+
 # ------------------------------------------------------------------- non-finite inputs ----
 NF_SHAPES = [("flat_tma", 256, 1024, 0), ("strided", 200, 1024, 64), ("generic", 130, 1001, 0)]
 

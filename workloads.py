@@ -96,10 +96,16 @@ def route_uniform(T: int, E: int, top_k: int, seed: int = 3) -> torch.Tensor:
     return _gumbel_topk(torch.zeros(E), T, top_k, _gen(seed))
 
 
-def route_skewed(T: int, E: int, top_k: int, alpha: float = 0.5, seed: int = 3) -> torch.Tensor:
-    """[T, top_k] expert ids with Zipf-like skew."""
+def route_skewed(T: int, E: int, top_k: int, alpha: float = 0.5, seed: int = 3,
+                 popularity_seed: int | None = None) -> torch.Tensor:
+    """[T, top_k] expert ids with Zipf-like skew.  The popularity order of the
+    experts is drawn from `seed` unless `popularity_seed` is given: two batches with the same
+    popularity_seed and different seeds are independent draws of one routing distribution (the
+    "observed statistics" of a previous batch)."""
     g = _gen(seed)
     perm = torch.randperm(E, generator=g)
+    if popularity_seed is not None:
+        perm = torch.randperm(E, generator=_gen(popularity_seed))
     rank = torch.empty(E, dtype=torch.float64)
     rank[perm] = torch.arange(E, dtype=torch.float64)
     logw = -alpha * torch.log(rank + 1.0)
