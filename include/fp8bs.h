@@ -184,6 +184,29 @@ FP8BS_API fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int
                         void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
                         fp8bs_stream_t stream);
 
+/* ---- gemm_ws: fp8bs_gemm with a workspace for the split-K tail --------------------------------
+ * Same arguments, layouts, validation and result definition as fp8bs_gemm, plus
+ * workspace : DEVICE scratch, 16-byte aligned, owned by the caller, of at least
+ *             fp8bs_gemm_workspace_size(layout, M, N, K) bytes (<= 19.4 MB on a 148-SM B200), or NULL.
+ * When the last wave of output tiles would fill at most half of the SMs (C1's Dgrad: 448 tiles on 74
+ * CTA pairs = 6 waves + 4 tiles), those tail tiles are cut along K into S chunks of consecutive
+ * K-blocks (S = clusters / tail tiles, >= 4 K-blocks each); every chunk is promoted exactly like a whole
+ * tile over its own K-blocks into an FP32 partial in the workspace, and a reduce kernel
+ * adds the S partials in chunk order in FP32 and writes D (BF16 RNE or FP32; WGRAD accumulate:
+ * D + sum).  Only the FP32 summation order of the tail tiles differs from fp8bs_gemm (R30):
+ * deterministic, and the same error bound.  Three kernels on `stream` instead of one; the workspace
+ * must not be reused until they have run.  workspace == NULL, or a shape without such a tail
+ * (fp8bs_gemm_workspace_size == 0): identical to fp8bs_gemm.  workspace_bytes below the required size:
+ * FP8BS_ERR_INVALID_ARG; misaligned: FP8BS_ERR_ALIGN (both before any launch). */
+FP8BS_API fp8bs_status fp8bs_gemm_ws(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                           const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                           const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                           void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
+                           void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+/* Bytes fp8bs_gemm_ws needs for this shape on the CURRENT device (its SM count decides the waves); 0
+ * when there is no split-K tail or the arguments are invalid. */
+FP8BS_API size_t fp8bs_gemm_workspace_size(fp8bs_layout layout, int64_t M, int64_t N, int64_t K);
+
 /* ---- gemm_mx: the same GEMM for POWER-OF-TWO scales on the tensor core's block scaling ----------
  * NEXT-1 (P:558, P:565 power-of-two scales; scaling inside the MMA).  Identical arguments,
  * layouts and validation as fp8bs_gemm, with one precondition: every sA and sB value is an exact power

@@ -120,6 +120,12 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_gemm_mx.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
     L.fp8bs_gemm.restype = st
     L.fp8bs_gemm.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp]
+    if hasattr(L, "fp8bs_gemm_ws"):
+        L.fp8bs_gemm_ws.restype = st
+        L.fp8bs_gemm_ws.argtypes = [i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i32, i64, i32, vp,
+                                    ctypes.c_size_t, vp]
+        L.fp8bs_gemm_workspace_size.restype = ctypes.c_size_t
+        L.fp8bs_gemm_workspace_size.argtypes = [i32, i64, i64, i64]
     L.fp8bs_grouped_gemm.restype = st
     L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
                                      vp, ctypes.c_size_t, vp]
@@ -359,12 +365,19 @@ def quantize_weight_128x128(w: torch.Tensor, want_t: bool = True, q=None, s=None
 
 
 # ------------------------------------------------------------------------ GEMM ----
+def gemm_workspace_size(layout: int, M: int, N: int, K: int) -> int:
+    """fp8bs_gemm_workspace_size: bytes of the split-K tail workspace for this shape (0: none)."""
+    return int(lib().fp8bs_gemm_workspace_size(layout, M, N, K))
+
+
 def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
          out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, accumulate: bool = False,
-         mx: bool = False):
+         mx: bool = False, workspace="auto"):
     """D [M,N] (+)= block-scaled A [M,K] x B [N,K]^T (see include/fp8bs.h for the sB layout per
     layout).  mx=True: fp8bs_gemm_mx (all scales exact powers of two; UE8M0 block scaling in the
-    tensor core, no promotion).  Returns D."""
+    tensor core, no promotion).  workspace: "auto" (default) allocates the split-K tail workspace when
+    the shape has one (fp8bs_gemm_ws), a device uint8 tensor is used as that workspace, None runs
+    fp8bs_gemm (every tile promoted over all of K in order).  Returns D."""
     for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
         _cuda2d(t, n)
     M, K = A.shape
@@ -374,9 +387,23 @@ def gemm(layout: int, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: to
     if out is None:
         out = torch.empty(M, N, dtype=out_dtype, device=A.device)
     _cuda2d(out, "out")
-    fn, name = (lib().fp8bs_gemm_mx, "fp8bs_gemm_mx") if mx else (lib().fp8bs_gemm, "fp8bs_gemm")
-    _check(fn(layout, M, N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
-              sB.stride(0), _p(out), _dt(out), out.stride(0), 1 if accumulate else 0, _stream(A)), name)
+    args = (layout, M, N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB),
+            sB.stride(0), _p(out), _dt(out), out.stride(0), 1 if accumulate else 0)
+    if mx:
+        _check(lib().fp8bs_gemm_mx(*args, _stream(A)), "fp8bs_gemm_mx")
+        return out
+    if isinstance(workspace, str):
+        if workspace != "auto":
+            raise ValueError("workspace: 'auto', None or a device uint8 tensor")
+        wsb = gemm_workspace_size(layout, M, N, K) if M > 0 and N > 0 else 0
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=A.device) if wsb > 0 else None
+    if workspace is None:
+        _check(lib().fp8bs_gemm(*args, _stream(A)), "fp8bs_gemm")
+    else:
+        if not workspace.is_cuda:
+            raise ValueError("workspace must be a CUDA tensor")
+        _check(lib().fp8bs_gemm_ws(*args, _p(workspace), workspace.numel() * workspace.element_size(), _stream(A)),
+               "fp8bs_gemm_ws")
     return out
 
 

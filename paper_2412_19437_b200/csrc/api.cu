@@ -228,13 +228,29 @@ static fp8bs_status check_gemm_common(int64_t M, int64_t N, int64_t K, const uin
 static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
-                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream);
+                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream,
+                              void* workspace = nullptr, size_t workspace_bytes = 0);
 
 fp8bs_status fp8bs_gemm(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                         const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
                         void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
     return gemm_impl(0, layout, M, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ddt, ldd, accumulate, stream);
+}
+
+size_t fp8bs_gemm_workspace_size(fp8bs_layout layout, int64_t M, int64_t N, int64_t K) {
+    if (layout != FP8BS_FPROP && layout != FP8BS_DGRAD && layout != FP8BS_WGRAD) return 0;
+    if (M <= 0 || N <= 0 || K <= 0 || K % 128 || M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return 0;
+    return split_workspace_bytes(M, N, K);
+}
+
+fp8bs_status fp8bs_gemm_ws(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
+                           const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                           const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                           void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate,
+                           void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    return gemm_impl(0, layout, M, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ddt, ldd, accumulate, stream,
+                     workspace, workspace_bytes);
 }
 
 fp8bs_status fp8bs_gemm_mx(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
@@ -247,7 +263,8 @@ fp8bs_status fp8bs_gemm_mx(fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
 static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N, int64_t K,
                               const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                               const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
-                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+                              void* D, fp8bs_dtype ddt, int64_t ldd, int accumulate, fp8bs_stream_t stream,
+                              void* workspace, size_t workspace_bytes) {
     if (layout != FP8BS_FPROP && layout != FP8BS_DGRAD && layout != FP8BS_WGRAD)
         return fail(FP8BS_ERR_INVALID_ARG, "layout=%d", (int)layout);
     fp8bs_status c = check_gemm_common(M, N, K, A, lda, sA, ldsA, B, ldb, sB, D, ddt, ldd);
@@ -263,6 +280,12 @@ static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N,
     }
     if (accumulate && ddt != FP8BS_FP32) return fail(FP8BS_ERR_UNSUPPORTED, "accumulate requires FP32 output");
     if (accumulate && layout != FP8BS_WGRAD) return fail(FP8BS_ERR_UNSUPPORTED, "accumulate is supported for WGRAD only");
+    if (workspace) {
+        if (!aligned16(workspace)) return fail(FP8BS_ERR_ALIGN, "workspace must be 16-byte aligned");
+        const size_t need = split_workspace_bytes(M, N, K);
+        if (workspace_bytes < need)
+            return fail(FP8BS_ERR_INVALID_ARG, "workspace of %zu bytes < fp8bs_gemm_workspace_size = %zu", workspace_bytes, need);
+    }
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
     GemmArgs a{};
@@ -270,6 +293,7 @@ static fp8bs_status gemm_impl(int mx, fp8bs_layout layout, int64_t M, int64_t N,
     a.A = A; a.lda = lda; a.sA = sA; a.ldsA = ldsA; a.B = B; a.ldb = ldb; a.sB = sB; a.ldsB = ldsB;
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = accumulate ? 1 : 0;
     a.grouped = 0; a.G = 0; a.offsets = nullptr;
+    if (workspace) { a.split_ws = workspace; a.split_ws_bytes = workspace_bytes; }
     const char* detail = nullptr;
     cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);

@@ -118,6 +118,10 @@ struct KParams {
     void* tiles;                  // grouped: TileTable in the caller's workspace
     int gm;                       // raster band width (dense): tiles of the resident operand per band
     int rast_n;                   // 1: n-fastest (B resident, A streamed), 0: m-fastest
+    int tile_end;                 // dense: tiles [0, tile_end) of the raster belong to this launch
+    // split-K tail (kOutSplit): units u < split_units are (tile split_t0 + u / split_s, K-chunk u % split_s);
+    // unit u writes its FP32 partial tile to rows [u * ROWS, (u + 1) * ROWS) of the workspace (BN columns)
+    int split_t0, split_s, split_units;
     int debug;                    // unused (debug bits are compile-time: FP8BS_GEMM_DEBUG_BITS): 1 skip promotion math,
                                   // 2 skip MMAs, 4 TMA always re-reads K-block 0 (L2-resident),
                                   // 16 record clock64 timestamps of CTA 0, 64 MMA ignores slot release,
@@ -162,8 +166,7 @@ struct GWSched { int2 e[kG]; };
 constexpr int kGWMax = 1024;
 
 template <int ROWS>
-__device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
-    if (t >= p.num_m * p.num_n) return false;
+__host__ __device__ __forceinline__ void decode_dense(const KParams& p, int t, Tile& tl) {
     // Banded raster.  The operand with fewer bytes stays L2-resident and the other streams from
     // DRAM once: inside a band of gm tiles of the resident operand, consecutive tiles walk the
     // resident operand fastest, so the concurrent clusters share each streamed tile through L2.
@@ -176,6 +179,28 @@ __device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl
     const int m = p.rast_n ? istr : ires, n = p.rast_n ? ires : istr;
     tl.row0 = m * ROWS; tl.row_end = p.M; tl.n0 = n * BN; tl.e = 0;
     tl.nh = (p.N - tl.n0 > HN) ? 2 : 1;
+}
+
+template <int ROWS>
+__device__ __forceinline__ bool get_tile_dense(const KParams& p, int t, Tile& tl) {
+    if (t >= p.tile_end) return false;
+    decode_dense<ROWS>(p, t, tl);
+    return true;
+}
+
+// Split-K tail (reading R30): when the last wave of a dense GEMM would leave most
+// clusters idle, its tiles are cut along K into split_s chunks of consecutive K-blocks; unit u is
+// chunk u % split_s of tail tile u / split_s and writes its FP32 partial (promoted exactly as a whole
+// tile would be, over its own K-blocks) into its own workspace slab; k_splitk_reduce sums the chunks
+// in chunk order and writes D.
+template <int ROWS>
+__device__ __forceinline__ bool get_tile_split(const KParams& p, int u, Tile& tl) {
+    if (u >= p.split_units) return false;
+    const int i = u / p.split_s, c = u - i * p.split_s;
+    decode_dense<ROWS>(p, p.split_t0 + i, tl);
+    tl.kb0 = c * p.KB / p.split_s;
+    tl.kbn = (c + 1) * p.KB / p.split_s - tl.kb0;
+    tl.orow0 = u * ROWS; tl.row_end = tl.orow0 + ROWS;
     return true;
 }
 
@@ -439,7 +464,7 @@ __device__ __forceinline__ void swiglu_epilogue(float (&acc)[128], int h, int qu
 }
 
 // kOut: 0 BF16 output, 1 FP32 output, 2 the SwiGLU FP8 epilogue (kOutSwiglu).
-constexpr int kOutBF16 = 0, kOutFP32 = 1, kOutSwiglu = 2;
+constexpr int kOutBF16 = 0, kOutFP32 = 1, kOutSwiglu = 2, kOutSplit = 3;   // kOutSplit: FP32 partials of the split-K tail
 template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
 __global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -449,8 +474,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     using C = Cfg<kPair, kWgrad>;
     // grouped Wgrad: one launch over every expert, each tile with its expert's contraction blocks
     constexpr bool kGW = kWgrad && kGrouped;
-    constexpr bool kOutF32 = kOut == kOutFP32;
+    constexpr bool kSplit = kOut == kOutSplit;
+    static_assert(!(kSplit && kGrouped), "the split-K tail is for dense launches");
+    constexpr bool kOutF32 = kOut == kOutFP32 || kSplit;
     constexpr bool kSwiglu = kOut == kOutSwiglu;
+    constexpr bool kKR = kGW || kSplit;   // tiles carry their own contraction-block range
     extern __shared__ uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
@@ -512,12 +540,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     auto next_tile = [&](int t, Tile& tl) -> bool {
         if constexpr (kGW) return get_tile_gw<C::ROWS>(p, gw, t, tl);
+        else if constexpr (kSplit) return get_tile_split<C::ROWS>(p, t, tl);
         else if constexpr (kGrouped) return get_tile_table(reinterpret_cast<const TileTable*>(p.tiles), p.N, t, tl);
         else return get_tile_dense<C::ROWS>(p, t, tl);
     };
-    // contraction blocks of a tile and their first block (only grouped Wgrad tiles differ)
-    auto nkb = [&](const Tile& tl) -> int { if constexpr (kGW) return tl.kbn; else return p.KB; };
-    auto kbase = [&](const Tile& tl) -> int { if constexpr (kGW) return tl.kb0; else return 0; };
+    // contraction blocks of a tile and their first block (grouped Wgrad and split-K tiles differ)
+    auto nkb = [&](const Tile& tl) -> int { if constexpr (kKR) return tl.kbn; else return p.KB; };
+    auto kbase = [&](const Tile& tl) -> int { if constexpr (kKR) return tl.kb0; else return 0; };
 
     // Tile order.  Dense: static, cluster c takes tiles c, c + ncl, ...  Grouped: dynamic — the
     // leader's producer thread claims the next tile index with an atomic on the workspace counter
@@ -695,8 +724,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     // lane j holds the 2 block scalars the tile's columns need at K-block kb0 + j
                     float v0 = 0.0f, v1 = 0.0f;
                     if constexpr (!kWgrad) {
-                        const int kb = kb0 + lane;
-                        if (kb < p.KB) {
+                        const int kb = kbase(tl) + kb0 + lane;
+                        if (kb < kbase(tl) + nkb(tl)) {
                             v0 = __ldg(sbp + nb0 * p.sb_nb_stride + kb * p.sb_kb_stride);
                             if (nb0 + 1 < p.NB) v1 = __ldg(sbp + (nb0 + 1) * p.sb_nb_stride + kb * p.sb_kb_stride);
                         }
@@ -741,7 +770,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // every tile advances sit by exactly KB, so the tile's sequence number is sit / KB (one
         // register fewer than a counter: the accumulators are at the edge of the 240-register budget)
         int jt = 0;                                     // grouped Wgrad: tiles walked (KB varies per tile)
-        auto next_j = [&]() -> int { if constexpr (kGW) return ++jt; else return sit / p.KB; };
+        auto next_j = [&]() -> int { if constexpr (kKR) return ++jt; else return sit / p.KB; };
         for (int t = tile_index(0); next_tile(t, tl); t = tile_index(next_j())) {
             const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
             const bool active = h < tl.nh;
@@ -888,7 +917,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             bool unrolled = false;
             // dense Fprop/Dgrad only: in the Wgrad and grouped kernels the unrolled body makes ptxas
             // spill loop state into local memory (measured: Wgrad -7%, grouped C4 -20%)
-            if constexpr (!kWgrad) unrolled = p.KB % C::kSStages == 0;
+            if constexpr (!kWgrad && !kSplit) unrolled = p.KB % C::kSStages == 0;
             if (unrolled) {
                 // K-blocks in groups of kSStages (8): the scale stage is the index in the group, the TMEM
                 // slot alternates 2h, 2h + 1 and its phase flips every 2 K-blocks (sit and qh are
@@ -908,7 +937,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
             }
             // ---------------- epilogue ----------------
-            const int arow = (kGW ? tl.orow0 : tl.row0) + (int)rank * BM;   // output rows
+            const int arow = (kKR ? tl.orow0 : tl.row0) + (int)rank * BM;   // output rows
             // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or
             // 64 BF16 columns) in its own SWIZZLE_128B buffer and writes them with asynchronous TMA
             // stores (reduce-add for Wgrad's D += acc): a warp store used to touch 32 rows at once.
@@ -957,7 +986,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                         sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
-                    const int col = tl.n0 + h * HN + gg * NC + c * CW;
+                    const int col = (kSplit ? 0 : tl.n0) + h * HN + gg * NC + c * CW;   // split: the unit's slab
                     if (kGrouped && !full) {
                         __syncwarp();
                         for (int i = lane; i < rows_here * 8; i += 32) {
@@ -1000,6 +1029,41 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
 }
 
+// Split-K tail, second step: D tile (+)= sum over chunks c = 0..S-1, in that order, of the FP32
+// partials.  One thread per 4 columns of a row; block (x, i): rows 4x..4x+3 of tail tile i.
+template <int ROWS>
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ part, const KParams p,
+                                                      void* D, int64_t ldd, int out_f32, int accumulate) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int i = blockIdx.y;
+    const int r = blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int c4 = threadIdx.x & 63;
+    Tile tl;
+    decode_dense<ROWS>(p, p.split_t0 + i, tl);
+    const int row = tl.row0 + r, col = tl.n0 + 4 * c4;
+    if (row >= p.M || col >= p.N) return;
+    const float4* src = reinterpret_cast<const float4*>(part) + ((int64_t)i * p.split_s * ROWS + r) * (BN / 4) + c4;
+    float4 acc = __ldcg(src);
+    for (int c = 1; c < p.split_s; ++c) {
+        const float4 v = __ldcg(src + (int64_t)c * ROWS * (BN / 4));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (out_f32) {
+        float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(D) + (int64_t)row * ldd + col);
+        if (accumulate) {
+            const float4 o = *d;
+            acc.x = o.x + acc.x; acc.y = o.y + acc.y; acc.z = o.z + acc.z; acc.w = o.w + acc.w;
+        }
+        *d = acc;
+    } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&lo); w.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(D) + (int64_t)row * ldd + col) = w;
+    }
+}
+
 // ===========================================================================================
 // host side: tensor maps + launch
 // ===========================================================================================
@@ -1011,10 +1075,44 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const voi
 
 static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEBUG & 16)
 
+// Split-K tail plan of a dense launch (get_tile_split): tiles [t0, t0 + units / S) of the raster, each
+// cut into S chunks along K.  Used when the last wave would fill at most half of the clusters: S =
+// clusters / tail tiles (so the units fill one wave), and only when it saves at least kSplitMinSaved
+// K-blocks of the tail tile's time (the partial slabs and the reduce launch cost a few microseconds).
+struct SplitPlan { int t0 = 0, S = 0, units = 0; };
+constexpr int kSplitMinKB = 4, kSplitMinSaved = 16;
+
+static SplitPlan split_plan(int64_t M, int64_t N, int64_t K, int rows, int clusters) {
+    SplitPlan sp;
+    const int64_t tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN);
+    const int KB = (int)(K / BK);
+    if (clusters < 2 || tiles <= 0) return sp;
+    const int64_t rem = tiles % clusters;
+    if (rem == 0) return sp;
+    int S = (int)(clusters / rem);
+    if (S > KB / kSplitMinKB) S = KB / kSplitMinKB;
+    if (S < 2 || KB - KB / S < kSplitMinSaved) return sp;
+    sp.t0 = (int)(tiles - rem); sp.S = S; sp.units = (int)rem * S;
+    return sp;
+}
+static size_t split_bytes(const SplitPlan& sp, int rows) { return (size_t)sp.units * rows * BN * 4; }
+
+// dense raster parameters (shared by the GEMM launches and the split-K reduce)
+static void dense_raster(const GemmArgs& a, int rows, KParams& p) {
+    p.num_m = (int)((a.M + rows - 1) / rows); p.num_n = (int)((a.N + BN - 1) / BN);
+    // keep the smaller operand resident; band it to ~48 MB of L2 when it is larger than that
+    p.rast_n = a.M > a.N ? 1 : 0;
+    const int64_t res_rows = p.rast_n ? (int64_t)BN : (int64_t)rows;   // rows per resident tile
+    const int nres = p.rast_n ? p.num_n : p.num_m;
+    int64_t gb = ((int64_t)FP8BS_BAND_MB << 20) / (res_rows * a.K);
+    p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
+}
+
 template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
-static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail) {
+static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail, const SplitPlan* sp = nullptr) {
     using C = Cfg<kPair, kWgrad>;
-    constexpr bool kOutF32 = kOut == kOutFP32, kSwiglu = kOut == kOutSwiglu;
+    constexpr bool kSplit = kOut == kOutSplit;
+    constexpr bool kOutF32 = kOut == kOutFP32 || kSplit, kSwiglu = kOut == kOutSwiglu;
     const int KB = (int)(a.K / BK);
     constexpr bool kGW = kWgrad && kGrouped;   // grouped Wgrad: A = dYqT [M, Mp], D = [G x M, N]
     const int64_t rows = a.M;   // total rows of A (total_M for grouped)
@@ -1077,6 +1175,15 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
                 *detail = "cuTensorMapEncodeTiled failed for the SwiGLU input cache"; return cudaErrorInvalidValue;
             }
         }
+    } else if constexpr (kSplit) {
+        // the units' FP32 partial slabs: [units x ROWS, BN] in the caller's workspace
+        uint64_t dims[2] = {(uint64_t)BN, (uint64_t)sp->units * C::ROWS};
+        uint64_t str[1] = {(uint64_t)BN * 4};
+        uint32_t box[2] = {32, 32};
+        if (!make_tmap(&tD, TMAP_F32, 2, a.split_ws, dims, str, box, 128)) {
+            *detail = "cuTensorMapEncodeTiled failed for the split-K workspace"; return cudaErrorInvalidValue;
+        }
+        tD2 = tD;
     } else {
         const uint64_t esz = kOutF32 ? 4 : 2;
         uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)(kGW ? rows * a.G : rows)};   // grouped Wgrad: experts stacked
@@ -1090,7 +1197,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     KParams p{};
     p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = KB;
     p.sy = a.sy; p.ldsy = a.ldsy; p.qh = a.qh; p.ldqh = a.ldqh; p.sh = a.sh; p.ldsh = a.ldsh;
-    p.num_m = (int)((a.M + C::ROWS - 1) / C::ROWS); p.num_n = (int)((a.N + BN - 1) / BN);
+    dense_raster(a, C::ROWS, p);
     p.NB = (int)((a.N + 127) / 128);
     p.sB = a.sB;
     if (kGrouped && a.layout == 1) { p.sb_nb_stride = 1; p.sb_kb_stride = p.NB; p.sb_expert_stride = (int64_t)p.NB * KB; }   // grouped Dgrad
@@ -1099,13 +1206,10 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.G = a.G; p.offsets = a.offsets; p.tiles = a.workspace;
-    {
-        // keep the smaller operand resident; band it to ~48 MB of L2 when it is larger than that
-        p.rast_n = a.M > a.N ? 1 : 0;
-        const int64_t res_rows = p.rast_n ? (int64_t)BN : (int64_t)C::ROWS;   // rows per resident tile
-        const int nres = p.rast_n ? p.num_n : p.num_m;
-        int64_t gb = ((int64_t)FP8BS_BAND_MB << 20) / (res_rows * a.K);
-        p.gm = (int)(gb < 1 ? 1 : (gb > nres ? nres : gb));
+    p.tile_end = sp ? sp->t0 : p.num_m * p.num_n;
+    if constexpr (kSplit) {
+        p.split_t0 = sp->t0; p.split_s = sp->S; p.split_units = sp->units;
+        p.accumulate = 0;                      // the reduce adds into D
     }
     {
         if (kDbg & 16) {
@@ -1118,7 +1222,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     int64_t tiles_ub;
     if (kGW) tiles_ub = (int64_t)a.G * p.num_m * p.num_n;
     else if (kGrouped) tiles_ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;
-    else tiles_ub = (int64_t)p.num_m * p.num_n;
+    else if (kSplit) tiles_ub = sp->units;
+    else tiles_ub = p.tile_end;
     const int64_t max_clusters = num_sms() / C::CS;
     int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
     if (clusters < 1) clusters = 1;
@@ -1167,6 +1272,36 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
 static int g_forced_variant = 0;
 #endif
 
+// A dense launch, with the split-K tail when the caller passed a workspace and the shape has one:
+// the full waves (if any), the tail units, then the reduce — three kernels on `st`, chained by PDL.
+template <bool kWgrad, int kOut, bool kPair>
+static cudaError_t launch_dense(const GemmArgs& a, cudaStream_t st, const char** detail) {
+    using C = Cfg<kPair, kWgrad>;
+    const SplitPlan sp = split_plan(a.M, a.N, a.K, C::ROWS, num_sms() / C::CS);
+    if (sp.S < 2 || !a.split_ws || a.split_ws_bytes < split_bytes(sp, C::ROWS))
+        return launch_cfg<kWgrad, kOut, false, kPair>(a, st, detail);
+    cudaError_t e;
+    if (sp.t0 > 0 && (e = launch_cfg<kWgrad, kOut, false, kPair>(a, st, detail, &sp)) != cudaSuccess) return e;
+    if ((e = launch_cfg<kWgrad, kOutSplit, false, kPair>(a, st, detail, &sp)) != cudaSuccess) return e;
+    KParams p{};
+    p.M = (int)a.M; p.N = (int)a.N; p.K = (int)a.K; p.KB = (int)(a.K / BK);
+    dense_raster(a, C::ROWS, p);
+    p.split_t0 = sp.t0; p.split_s = sp.S; p.split_units = sp.units;
+    e = launch_pdl(k_splitk_reduce<C::ROWS>, dim3(C::ROWS / 4, sp.units / sp.S), dim3(256), 0, st,
+                   static_cast<const float*>(a.split_ws), p, a.D, a.ldd, a.out_f32, a.accumulate);
+    if (e != cudaSuccess) return e;
+    return cudaPeekAtLastError();
+}
+
+size_t split_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+    // either tile variant (the test build can force one): the larger of the two plans
+    size_t b = 0;
+    const SplitPlan s1 = split_plan(M, N, K, BM, num_sms()), s2 = split_plan(M, N, K, 2 * BM, num_sms() / 2);
+    if (s1.S >= 2) b = split_bytes(s1, BM);
+    if (s2.S >= 2 && split_bytes(s2, 2 * BM) > b) b = split_bytes(s2, 2 * BM);
+    return b;
+}
+
 template <bool kPair>
 static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** detail) {
     if (a.grouped && a.layout == 2) return launch_cfg<true, kOutFP32, true, kPair>(a, st, detail);
@@ -1178,9 +1313,9 @@ static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** det
         return a.out_f32 ? launch_cfg<false, kOutFP32, true, kPair>(a, st, detail)
                          : launch_cfg<false, kOutBF16, true, kPair>(a, st, detail);
     }
-    if (a.layout == 2) return launch_cfg<true, kOutFP32, false, kPair>(a, st, detail);
-    return a.out_f32 ? launch_cfg<false, kOutFP32, false, kPair>(a, st, detail)
-                     : launch_cfg<false, kOutBF16, false, kPair>(a, st, detail);
+    if (a.layout == 2) return launch_dense<true, kOutFP32, kPair>(a, st, detail);
+    return a.out_f32 ? launch_dense<false, kOutFP32, kPair>(a, st, detail)
+                     : launch_dense<false, kOutBF16, kPair>(a, st, detail);
 }
 
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N) {

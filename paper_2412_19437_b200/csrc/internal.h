@@ -80,8 +80,11 @@ struct GemmArgs {
     // SwiGLU FP8 epilogue (FPROP; N = 2I, gate / up interleaved per 128 columns): D = y codes [M, I]
     // (ldd), sy [I/128][ldsy]; optional FP8 cache of H: qh [M, N] (ldqh), sh [N/128][ldsh]
     int swiglu; float* sy; int64_t ldsy; uint8_t* qh; int64_t ldqh; float* sh; int64_t ldsh;
+    // dense: optional split-K tail workspace (>= split_workspace_bytes(M, N, K)), nullptr = unsplit
+    void* split_ws; size_t split_ws_bytes;
 };
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
+size_t split_workspace_bytes(int64_t M, int64_t N, int64_t K);   // 0: no split-K tail for this shape
 
 // Returns cudaSuccess or the launch error; *detail gets a static message on host-side failures
 // (tensor-map encoding).

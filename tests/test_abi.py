@@ -140,3 +140,22 @@ def test_requant_pow2_and_grouped_dgrad_validation():
     # fp8bs_grouped_gemm_dgrad: same rules as the grouped Fprop
     assert lib.fp8bs_grouped_gemm_dgrad(0, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_INVALID_ARG
     assert lib.fp8bs_grouped_gemm_dgrad(4, 10, 256, 500, A16, A16, 512, A16, 16, A16, A16, A16, 0, 256, None, 0, None) == L.ERR_SHAPE
+
+
+def test_gemm_ws_workspace_size_and_validation():
+    """fp8bs_gemm_workspace_size / fp8bs_gemm_ws (split-K tail, reading R30), host side only.  Without a
+    device the SM count falls back to B200's 148: C1's Dgrad (448 pair tiles on 74 clusters = 6 waves +
+    4 tiles) cuts its 4 tail tiles into 18 chunks -> 72 units of 256 x 256 FP32; C1's Fprop tail fills
+    57% of a wave -> no split (0 bytes)."""
+    lib = fp.lib()
+    assert L.gemm_workspace_size(L.DGRAD, 4096, 7168, 18432) == 72 * 256 * 256 * 4
+    assert L.gemm_workspace_size(L.FPROP, 4096, 18432, 7168) == 0
+    assert L.gemm_workspace_size(L.FPROP, 4096, 18432, 7100) == 0        # invalid K
+    assert L.gemm_workspace_size(7, 4096, 7168, 18432) == 0
+    A16 = ctypes.c_void_p(1 << 20)
+    args = (L.DGRAD, 4096, 7168, 18432, A16, 18432, A16, 4096, A16, 18432, A16, 56, A16, 0, 7168, 0)
+    need = L.gemm_workspace_size(L.DGRAD, 4096, 7168, 18432)
+    assert lib.fp8bs_gemm_ws(*args, A16, need - 16, None) == L.ERR_INVALID_ARG
+    assert "workspace" in fp.last_error_detail()
+    assert lib.fp8bs_gemm_ws(*args, ctypes.c_void_p((1 << 20) + 8), need, None) == L.ERR_ALIGN
+    assert lib.fp8bs_gemm_ws(*args[:5], 100, *args[6:], A16, need, None) == L.ERR_SHAPE      # lda < K first
