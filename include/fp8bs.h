@@ -371,6 +371,17 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offset
                                       const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
                                       float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream);
 
+/* ---- grouped_gemm_wgrad_mx: the grouped expert Wgrad on UE8M0 block scaling (NEXT-1) --
+ * Identical arguments, layouts, validation and result definition as fp8bs_grouped_gemm_wgrad, with the
+ * fp8bs_gemm_mx precondition: every sA and sB value is an exact power of two in [2^-127, 2^127] (e.g.
+ * the pow2 128x1 quantization of each expert's tokens), applied inside tcgen05.mma.kind::mxf8f6f4 with
+ * no promotion step.  One persistent launch over every expert's (m, n) tiles (CTA pairs along m sharing
+ * the B tile by multicast); an expert without tokens gets D_e = 0 (accumulate: D_e unchanged). */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_wgrad_mx(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                         const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                         float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

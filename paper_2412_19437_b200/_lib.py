@@ -140,6 +140,9 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_grouped_gemm_wgrad.restype = st
         L.fp8bs_grouped_gemm_wgrad.argtypes = [ctypes.c_int32, vp, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
                                                vp, i64, i32, vp]
+        if hasattr(L, "fp8bs_grouped_gemm_wgrad_mx"):
+            L.fp8bs_grouped_gemm_wgrad_mx.restype = st
+            L.fp8bs_grouped_gemm_wgrad_mx.argtypes = L.fp8bs_grouped_gemm_wgrad.argtypes
     if hasattr(L, "fp8bs_dispatch_fp8"):
         L.fp8bs_dispatch_fp8.restype = st
         L.fp8bs_dispatch_fp8.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
@@ -294,9 +297,10 @@ def quantize_act_128x1_grouped(x: torch.Tensor, offsets, qT: torch.Tensor | None
 
 
 def grouped_gemm_wgrad(offsets, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
-                       out: torch.Tensor | None = None, accumulate: bool = False):
+                       out: torch.Tensor | None = None, accumulate: bool = False, mx: bool = False):
     """Per-expert dW_e [N,K] (+)= WGRAD over expert e's tokens: A = dYqT [N,Mp], B = XqT [K,Mp], sA [Mp/128,N],
-    sB [Mp/128,K] in the expert-aligned layout; out FP32 [G,N,K] (fp8bs_grouped_gemm_wgrad)."""
+    sB [Mp/128,K] in the expert-aligned layout; out FP32 [G,N,K] (fp8bs_grouped_gemm_wgrad).  mx=True:
+    power-of-two scales on UE8M0 block scaling (fp8bs_grouped_gemm_wgrad_mx)."""
     for t, n in ((A, "A"), (B, "B"), (sA, "sA"), (sB, "sB")):
         _cuda2d(t, n)
     off = _host_offsets(offsets)
@@ -305,9 +309,10 @@ def grouped_gemm_wgrad(offsets, A: torch.Tensor, sA: torch.Tensor, B: torch.Tens
         out = torch.empty(G, N, K, dtype=torch.float32, device=A.device)
     if out.dtype != torch.float32 or not out.is_cuda or out.stride(2) != 1 or out.stride(0) != N * out.stride(1):
         raise ValueError("out must be a CUDA float32 [G,N,K] tensor with unit column stride and stacked experts")
-    _check(lib().fp8bs_grouped_gemm_wgrad(G, off.data_ptr(), N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
-                                          B.stride(0), _p(sB), sB.stride(0), _p(out), out.stride(1),
-                                          1 if accumulate else 0, _stream(A)), "fp8bs_grouped_gemm_wgrad")
+    fn, name = ((lib().fp8bs_grouped_gemm_wgrad_mx, "fp8bs_grouped_gemm_wgrad_mx") if mx
+                else (lib().fp8bs_grouped_gemm_wgrad, "fp8bs_grouped_gemm_wgrad"))
+    _check(fn(G, off.data_ptr(), N, K, _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), B.stride(0), _p(sB), sB.stride(0),
+              _p(out), out.stride(1), 1 if accumulate else 0, _stream(A)), name)
     return out
 
 

@@ -561,10 +561,29 @@ fp8bs_status fp8bs_quantize_act_128x1_grouped(const void* x, fp8bs_dtype xdt, in
     return ok();
 }
 
+static fp8bs_status grouped_wgrad_impl(int mx, int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                       const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                       float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream);
+
 fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                       const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
                                       float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    return grouped_wgrad_impl(0, G, offsets, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ldd, accumulate, stream);
+}
+
+fp8bs_status fp8bs_grouped_gemm_wgrad_mx(int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                         const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                         float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
+    return grouped_wgrad_impl(1, G, offsets, N, K, A, lda, sA, ldsA, B, ldb, sB, ldsB, D, ldd, accumulate, stream);
+}
+
+static fp8bs_status grouped_wgrad_impl(int mx, int32_t G, const int64_t* offsets, int64_t N, int64_t K,
+                                       const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                       const uint8_t* B, int64_t ldb, const float* sB, int64_t ldsB,
+                                       float* D, int64_t ldd, int accumulate, fp8bs_stream_t stream) {
     /* every argument is checked here, before the single launch: a failing call enqueues nothing */
     if (G < 0 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [0, 1024]", (int)G);
     const int64_t Mp = padded_tokens(G, offsets);
@@ -608,9 +627,9 @@ fp8bs_status fp8bs_grouped_gemm_wgrad(int32_t G, const int64_t* offsets, int64_t
         return from_cuda(err, "grouped_gemm_wgrad zero fill");
     }
     const char* detail = nullptr;
-    cudaError_t e = launch_gemm(a, (cudaStream_t)stream, &detail);
+    cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
-    return from_cuda(e, "grouped_gemm_wgrad launch");
+    return from_cuda(e, mx ? "grouped_gemm_wgrad_mx launch" : "grouped_gemm_wgrad launch");
 }
 
 }  // extern "C"

@@ -137,7 +137,13 @@ __device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const void* tmap, u
         :: "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask) : "memory");
 }
 
-struct MxTile { int m0, n0, e, row_end; };
+struct MxTile { int m0, n0, e, row_end, kb0, kbn; };
+
+// Grouped Wgrad (one launch over every expert): expert e's 128-token blocks in the padded layout, .x =
+// first block, .y = blocks (0 for an expert without tokens).  Kernel parameter space (8 KB at 1024).
+template <int kG>
+struct GWs { int2 e[kG]; };
+constexpr int kGWMax = 1024;
 
 // Arrive once on the barrier at this offset in both CTAs of the pair when the MMAs complete.
 __device__ __forceinline__ void mma_commit_mc(uint32_t bar) {
@@ -145,10 +151,13 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t bar) {
                  :: "r"(bar), "h"((uint16_t)3) : "memory");
 }
 
-template <bool kOutF32, bool kMc, bool kGrouped>
+// kGW: grouped Wgrad — tiles (expert, m, n) with m fastest inside an expert, each contracting over its
+// expert's own token blocks gw.e[e]; output rows of expert e at e * M (D = [G x M, N]).
+template <bool kOutF32, bool kMc, bool kGrouped, bool kGW>
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-          const __grid_constant__ CUtensorMap tmD, const Params p) {
+          const __grid_constant__ CUtensorMap tmD, const Params p, const __grid_constant__ GWs<kGW ? kGWMax : 1> gw) {
+    static_assert(!(kGW && kGrouped), "grouped Wgrad has its own tile map");
     extern __shared__ uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
@@ -206,7 +215,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if constexpr (kMc) cluster_sync();              // the peer's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int ntiles = kGrouped ? cum[p.G] : p.num_m * p.num_n;
+    const int ntiles = kGrouped ? cum[p.G] : kGW ? p.G * p.num_m * p.num_n : p.num_m * p.num_n;
     // unit t -> this CTA's tile: rows [m0, m0 + BM) (clipped at row_end), columns [n0, n0 + BN)
     auto decode = [&](int t, MxTile& tl) {
         if constexpr (kGrouped) {
@@ -220,10 +229,18 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const bool nfast = seg > p.N;                // as the promotion kernel: smaller operand resident
             const int pm = nfast ? local / p.num_n : local % mt, n = nfast ? local % p.num_n : local / mt;
             tl.m0 = off[lo] + (pm * MC + (int)rank) * BM; tl.n0 = n * BN; tl.e = lo; tl.row_end = off[lo + 1];
+            tl.kb0 = 0; tl.kbn = p.KB;
+        } else if constexpr (kGW) {
+            const int per = p.num_m * p.num_n, e = t / per, l = t - e * per;
+            const int pm = l % p.num_m, n = l / p.num_m;
+            tl.m0 = (pm * MC + (int)rank) * BM; tl.n0 = n * BN; tl.e = e; tl.row_end = p.M;
+            const int2 k = gw.e[e];
+            tl.kb0 = k.x; tl.kbn = k.y;
         } else {
             int tm, tn;
             tile_mn(p, t, tm, tn);
             tl.m0 = (tm * MC + (int)rank) * BM; tl.n0 = tn * BN; tl.e = 0; tl.row_end = p.M;
+            tl.kb0 = 0; tl.kbn = p.KB;
         }
     };
 
@@ -235,21 +252,22 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             MxTile tl;
             decode(t, tl);
             const int m0 = tl.m0, n0 = tl.n0;
-            for (int kb = 0; kb < p.KB; ++kb, ++it) {
+            for (int kb = 0; kb < tl.kbn; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
                 if (elect_one()) {
                     const uint32_t st = sbase + s * STAGE;
+                    const int kc = (tl.kb0 + kb) * BK;
                     mbar_arrive_expect_tx(full_bar(s), A_BYTES + B_BYTES);
-                    tma_load_2d(st, &tmA, full_bar(s), kb * BK, m0);
+                    tma_load_2d(st, &tmA, full_bar(s), kc, m0);
                     if constexpr (kMc && kGrouped)
-                        tma_load_3d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kb * BK, n0 + (int)rank * (BN / 2), tl.e, 3);
+                        tma_load_3d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2), tl.e, 3);
                     else if constexpr (kMc)
-                        tma_load_2d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kb * BK, n0 + (int)rank * (BN / 2), 3);
+                        tma_load_2d_mc(st + A_BYTES + rank * (B_BYTES / 2), &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2), 3);
                     else if constexpr (kGrouped)
-                        tma_load_3d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0, tl.e);
+                        tma_load_3d(st + A_BYTES, &tmB, full_bar(s), kc, n0, tl.e);
                     else
-                        tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kb * BK, n0);
+                        tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kc, n0);
                 }
                 __syncwarp();
             }
@@ -267,11 +285,28 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // while the current one waits for its stage: they are converted only after the wait, so no
         // load is consumed at issue (converting at load time stalled each warp on its loads: Wgrad's
         // 1187 TFLOP/s became 2254 with constant atoms)
+        // kGW: tiles have different K-block counts, so the CTA's global iteration `it` is mapped to
+        // (tile, K-block) with a cursor that only moves forward (load() is called with increasing it)
+        int cur_t = cid, cur_base = 0;
         auto load = [&](int it, float* fa, float* fb) -> bool {
-            const int t = cid + (it / p.KB) * ncl, kb = it % p.KB;
-            if (t >= ntiles) return false;
+            int t, kb;
             MxTile tl;
-            decode(t, tl);
+            if constexpr (kGW) {
+                for (;;) {
+                    if (cur_t >= ntiles) return false;
+                    decode(cur_t, tl);
+                    if (it < cur_base + tl.kbn) break;
+                    cur_base += tl.kbn;
+                    cur_t += ncl;
+                }
+                t = cur_t;
+                kb = tl.kb0 + (it - cur_base);
+            } else {
+                t = cid + (it / p.KB) * ncl; kb = it % p.KB;
+                if (t >= ntiles) return false;
+                decode(t, tl);
+            }
+            (void)t;
             const int m0 = tl.m0, n0 = tl.n0;
 #pragma unroll
             for (int r1 = 0; r1 < 4; ++r1) {
@@ -322,10 +357,17 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         int it = 0, tl = 0;
         for (int t = cid; t < ntiles; t += ncl, ++tl) {
             const int b = tl & 1;
+            int kbn = p.KB;
+            if constexpr (kGW) { MxTile ti; decode(t, ti); kbn = ti.kbn; }
             mbar_wait(accempty_bar(b), ((tl >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d = tmem_base + ACC_COLS * b;
-            for (int kb = 0; kb < p.KB; ++kb, ++it) {
+            if (kGW && kbn == 0) {                      // expert without tokens: no MMAs; the epilogue writes 0
+                if (elect_one()) mma_commit(accfull_bar(b));
+                __syncwarp();
+                continue;
+            }
+            for (int kb = 0; kb < kbn; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(full_bar(s), (it / STAGES) & 1);
                 tc_fence_after();
@@ -344,7 +386,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                     if constexpr (kMc) mma_commit_mc(empty_bar(s));
                     else mma_commit(empty_bar(s));
-                    if (kb == p.KB - 1) mma_commit(accfull_bar(b));
+                    if (kb == kbn - 1) mma_commit(accfull_bar(b));
                 }
                 __syncwarp();
             }
@@ -361,6 +403,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             decode(t, ti);
             const int m0 = ti.m0, n0 = ti.n0;
             const int rows_here = ti.row_end - (m0 + quad * 32);     // rows of this warp's 32 in range
+            const int orow = kGW ? ti.e * p.M : 0;                   // grouped Wgrad: expert e's output rows
+            const bool zero = kGW && ti.kbn == 0;                     // expert without tokens
             mbar_wait(accfull_bar(b), (tl >> 1) & 1);
             tc_fence_after();
             const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + ACC_COLS * b;
@@ -375,16 +419,22 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     __syncwarp();
                     if (lane == 0) mbar_arrive(accempty_bar(b));
                 }
-                if (kGrouped && rows_here < 32) {
+                if (zero) {
+                    if (p.accumulate) continue;      // D += 0
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0u;
+                }
+                if ((kGrouped || kGW) && rows_here < 32) {
                     // the expert ends inside this warp's 32 rows (rows past it belong to the next
                     // expert): each lane stores its own row directly
                     const int col = n0 + 32 * c;
                     if (lane < rows_here && col < p.N && !(FP8BS_MX_DBG & 1)) {
-                        const int64_t grow = (int64_t)m0 + quad * 32 + lane;
+                        const int64_t grow = (int64_t)orow + m0 + quad * 32 + lane;
                         const int ncol = min(32, p.N - col);
                         if constexpr (kOutF32) {
                             float* d = reinterpret_cast<float*>(p.D) + grow * p.ldd + col;
-                            for (int j = 0; j < ncol; ++j) d[j] = __uint_as_float(v[j]);
+                            if (p.accumulate) for (int j = 0; j < ncol; ++j) d[j] += __uint_as_float(v[j]);
+                            else for (int j = 0; j < ncol; ++j) d[j] = __uint_as_float(v[j]);
                         } else {
                             __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + grow * p.ldd + col;
                             for (int j = 0; j < ncol; ++j) d[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
@@ -415,8 +465,9 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (lane == 0) {
                     const int col = n0 + 32 * c, row = m0 + quad * 32;
                     if (col < p.N && row < p.M && !(FP8BS_MX_DBG & 1)) {
-                        if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, row);
-                        else tma_store_2d(&tmD, ebuf, col, row);
+                        const int srow = orow + row;
+                        if (kOutF32 && p.accumulate) tma_reduce_add_2d(&tmD, ebuf, col, srow);
+                        else tma_store_2d(&tmD, ebuf, col, srow);
                     }
                     bulk_commit_group();
                 }
@@ -438,6 +489,7 @@ done:
 cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** detail) {
     using namespace mx;
     const int KB = (int)(a.K / BK);
+    const bool gw = a.grouped && a.layout == 2;   // grouped Wgrad: dense-shaped operands, per-expert K ranges
     CUtensorMap tA, tB, tD;
     {
         const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.M};
@@ -445,7 +497,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         const uint32_t box[2] = {BK, BM};
         if (!make_tmap(&tA, TMAP_U8, 2, a.A, dims, str, box, 128)) { *detail = "tensor map A"; return cudaErrorInvalidValue; }
     }
-    if (a.grouped) {   // B [G][N][K], contiguous
+    if (a.grouped && !gw) {   // B [G][N][K], contiguous
         const uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         const uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
         const uint32_t box[3] = {BK, BN, 1};   // grouped runs unpaired (below)
@@ -459,7 +511,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     {
         // 32 rows x 32 columns per store: FP32 128 B (SWIZZLE_128B staging), BF16 64 B (SWIZZLE_64B)
         const uint64_t esz = a.out_f32 ? 4 : 2;
-        const uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)a.M};
+        const uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)(gw ? a.M * a.G : a.M)};   // grouped Wgrad: experts stacked
         const uint64_t str[1] = {(uint64_t)a.ldd * esz};
         const uint32_t box[2] = {32, 32};
         if (!make_tmap(&tD, a.out_f32 ? TMAP_F32 : TMAP_BF16, 2, a.D, dims, str, box, a.out_f32 ? 128 : 64)) {
@@ -471,7 +523,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     // Grouped runs without CTA pairs: a pair shares one expert's n tile over 2 x 128 rows, and at the
     // MoE shapes most experts have <= 128 rows, which left the second CTA idle (C2: 810 vs 1234
     // TFLOP/s unpaired).
-    const int MC = (FP8BS_MX_MC && !a.grouped) ? 2 : 1;
+    const int MC = (FP8BS_MX_MC && (!a.grouped || gw)) ? 2 : 1;
     p.num_m = (int)((a.M + BM * MC - 1) / (BM * MC)); p.num_n = (int)((a.N + BN - 1) / BN);   // m units of MC tiles
     p.rast_n = FP8BS_MX_NFAST == 2 ? (a.M > a.N ? 1 : 0) : FP8BS_MX_NFAST;
     {
@@ -481,14 +533,44 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     }
     p.layout = a.layout; p.sA = a.sA; p.ldsA = a.ldsA; p.sB = a.sB; p.ldsB = a.ldsB; p.accumulate = a.accumulate;
     p.G = a.grouped ? a.G : 0; p.offsets = a.offsets; p.sb_expert_stride = (int64_t)((a.N + 127) / 128) * KB;
+    if (gw) p.rast_n = 0;   // m fastest inside an expert (decode): its dYqT_e stays in L2 while XqT_e streams
     p.D = a.D; p.ldd = a.ldd;
     // grouped: an upper bound on the units (each expert adds at most one partial m unit per n tile)
-    const int64_t units = a.grouped ? (int64_t)(p.num_m + a.G) * p.num_n : (int64_t)p.num_m * p.num_n;
+    const int64_t units = gw ? (int64_t)a.G * p.num_m * p.num_n
+                        : a.grouped ? (int64_t)(p.num_m + a.G) * p.num_n : (int64_t)p.num_m * p.num_n;
     const int64_t max_units = num_sms() / MC;
     const int grid = (int)(units < max_units ? units : max_units) * MC;
     constexpr bool kMc = FP8BS_MX_MC != 0;
-    auto kern = a.grouped ? (a.out_f32 ? k_gemm_mx<true, false, true> : k_gemm_mx<false, false, true>)
-                          : (a.out_f32 ? k_gemm_mx<true, kMc, false> : k_gemm_mx<false, kMc, false>);
+    if (gw) {
+        GWs<kGWMax> g;
+        for (int e = 0; e < a.G; ++e) g.e[e] = make_int2(a.gw_kb[2 * e], a.gw_kb[2 * e + 1]);
+        auto kern = k_gemm_mx<true, kMc, false, true>;
+        static bool attr_gw[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_gw[dev]) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+            if (e != cudaSuccess) return e;
+            if (dev >= 0 && dev < 64) attr_gw[dev] = true;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = MC; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tD, p, g);
+        if (e != cudaSuccess) return e;
+        return cudaPeekAtLastError();
+    }
+    auto kern = a.grouped ? (a.out_f32 ? k_gemm_mx<true, false, true, false> : k_gemm_mx<false, false, true, false>)
+                          : (a.out_f32 ? k_gemm_mx<true, kMc, false, false> : k_gemm_mx<false, kMc, false, false>);
     const int smem = a.grouped ? SMEM_G : SMEM;
     static bool attr[4][64] = {{false}};
     const int ki = (a.out_f32 ? 1 : 0) + (a.grouped ? 2 : 0);
@@ -511,7 +593,9 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     at[1].val.clusterDim.x = MC; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tD, p);
+    GWs<1> g0;
+    g0.e[0] = make_int2(0, 0);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tD, p, g0);
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
 }

@@ -243,3 +243,89 @@ def test_grouped_calls_capture_in_a_cuda_graph():
         torch.cuda.synchronize()
         assert torch.equal(out_w.view(torch.int32), eager.view(torch.int32))
         assert torch.equal(out_f.view(torch.int16), eager_f.view(torch.int16))
+
+
+# ----------------------------------------------------------- grouped Wgrad on UE8M0 (NEXT-1) ----
+def _grouped_pow2_128x1(x, off):
+    """The expert-aligned 128x1 layout with POWER-OF-TWO scales (R23): each expert's tokens quantized
+    alone by the oracle's pow2 128x1 function (the grouped definition: segment = dense quantization of
+    that expert, pinned above), codes 0 in the padding."""
+    P = oracle.padded_offsets(off)
+    C, Mp = x.shape[1], int(P[-1])
+    qT = torch.zeros(C, Mp, dtype=torch.uint8)
+    sT = torch.zeros(Mp // 128, C, dtype=torch.float32)
+    for e in range(off.numel() - 1):
+        a, b, p = int(off[e]), int(off[e + 1]), int(P[e])
+        if a == b:
+            continue
+        q, s = oracle.quantize_act_128x1(x[a:b], pow2=True)
+        qT[:, p:p + b - a] = q
+        sT[p // 128:p // 128 + s.shape[0]] = s
+    return qT, sT
+
+
+def _dev_rows(t):
+    """Device copy with the row pitch padded to 16 bytes (the GEMM's alignment rule)."""
+    r, c = t.shape
+    align = 16 // t.element_size()
+    buf = torch.zeros(r, (c + align - 1) // align * align, dtype=t.dtype, device="cuda")
+    buf[:, :c] = t.cuda()
+    return buf[:, :c]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("counts", COUNTS + [[300, 0, 1000, 129]], ids=["mixed8", "one", "empties", "wide"])
+def test_grouped_wgrad_mx_vs_oracle_and_dense_mx(counts):
+    """fp8bs_grouped_gemm_wgrad_mx: within 1e-3 of the oracle per expert, bitwise equal to the dense
+    UE8M0 WGRAD (fp8bs_gemm_mx) on each expert's own columns, zero for experts without tokens, and
+    D += dW when accumulating."""
+    import paper_2412_19437_b200 as fp
+    off, x, dy = _problem(counts, C_in=448, N_out=640)
+    XqT, sX = _grouped_pow2_128x1(x, off)
+    DqT, sD = _grouped_pow2_128x1(dy, off)
+    O = oracle.grouped_gemm_wgrad(off, DqT, sD, XqT, sX)
+    XqT_d, sX_d, DqT_d, sD_d = _dev_rows(XqT), _dev_rows(sX), _dev_rows(DqT), _dev_rows(sD)
+    G, N, K = len(counts), dy.shape[1], x.shape[1]
+    D = torch.full((G, N, K), float("nan"), device="cuda")
+    fp.grouped_gemm_wgrad(off, DqT_d, sD_d, XqT_d, sX_d, out=D, mx=True)
+    torch.cuda.synchronize()
+    P = oracle.padded_offsets(off)
+    for e in range(G):
+        p, q = int(P[e]), int(P[e + 1])
+        if p == q:
+            assert not D[e].any(), "expert without tokens must get dW = 0"
+            continue
+        assert oracle.rel_err_normwise(D[e].cpu().double(), O[e]) <= TOL
+        De = fp.gemm(fp.WGRAD, DqT_d[:, p:q], sD_d[p // 128:q // 128], XqT_d[:, p:q], sX_d[p // 128:q // 128],
+                     out_dtype=torch.float32, mx=True)
+        torch.cuda.synchronize()
+        assert torch.equal(D[e].view(torch.int32), De.view(torch.int32)), f"expert {e}"
+    D2 = torch.ones(G, N, K, device="cuda")
+    fp.grouped_gemm_wgrad(off, DqT_d, sD_d, XqT_d, sX_d, out=D2, accumulate=True, mx=True)
+    torch.cuda.synchronize()
+    for e in range(G):
+        assert torch.equal(D2[e].view(torch.int32), (D[e] + 1.0).view(torch.int32)) if int(P[e]) < int(P[e + 1]) \
+            else bool((D2[e] == 1.0).all())
+
+
+@pytest.mark.gpu
+def test_grouped_wgrad_mx_closed_form_bitexact():
+    """Codes of {0, +-1, +-2} with power-of-two scales: every product and sum is exact, so the grouped
+    UE8M0 Wgrad must equal the oracle bit for bit on every expert (ragged experts included)."""
+    import paper_2412_19437_b200 as fp
+    counts = [130, 0, 384, 7, 1000]
+    off = _offsets(counts)
+    P = oracle.padded_offsets(off)
+    Mp, N, K = int(P[-1]), 384, 704
+    A = W.codes_small(N, Mp, seed=21)
+    B = W.codes_small(K, Mp, seed=22)
+    for e in range(len(counts)):       # padding columns hold code 0 (as the grouped quantizer writes)
+        a, b, p, q = int(off[e]), int(off[e + 1]), int(P[e]), int(P[e + 1])
+        A[:, p + b - a:q] = 0
+        B[:, p + b - a:q] = 0
+    sA = W.scales_pow2(Mp // 128, N, seed=23)
+    sB = W.scales_pow2(Mp // 128, K, seed=24)
+    O = oracle.grouped_gemm_wgrad(off, A, sA, B, sB)
+    D = fp.grouped_gemm_wgrad(off, _dev_rows(A), _dev_rows(sA), _dev_rows(B), _dev_rows(sB), mx=True)
+    torch.cuda.synchronize()
+    assert torch.equal(D.cpu().view(torch.int32), O.to(torch.float32).view(torch.int32))

@@ -42,6 +42,9 @@ def main():
         out = torch.empty(G, N, K, dtype=torch.float32, device=dev)
         ms_q = timeit(lambda: fp.quantize_act_128x1_grouped(x, offsets, qT=XqT, sT=sX))
         ms_w = timeit(lambda: fp.grouped_gemm_wgrad(offsets, DqT, sD, XqT, sX, out=out))
+        # UE8M0 form (fp8bs_grouped_gemm_wgrad_mx) on power-of-two scales (the same codes; timing only)
+        sDp, sXp = torch.exp2(torch.floor(torch.log2(sD))), torch.exp2(torch.floor(torch.log2(sX)))
+        ms_mx = timeit(lambda: fp.grouped_gemm_wgrad(offsets, DqT, sDp, XqT, sXp, out=out, mx=True))
         # dense Wgrad over the same R rows (one expert), for comparison
         qx, sx = fp.quantize_act_128x1(x[: R // 128 * 128])
         qd, sd = fp.quantize_act_128x1(dy[: R // 128 * 128])
@@ -52,7 +55,7 @@ def main():
         qbytes = R * K * 2 + Mp * K + Mp // 128 * K * 4
         m = offsets[1:] - offsets[:-1]
         print(f"{name}: R={R} Mp={Mp} M_e in [{int(m.min())},{int(m.max())}] | grouped wgrad {ms_w:.3f} ms "
-              f"{fl / ms_w / 1e9:.0f} TFLOP/s (out {G * N * K * 4 / 1e9:.1f} GB FP32) | dense same rows {ms_d:.3f} ms "
+              f"{fl / ms_w / 1e9:.0f} TFLOP/s (out {G * N * K * 4 / 1e9:.1f} GB FP32) | mx {ms_mx:.3f} ms {fl / ms_mx / 1e9:.0f} | dense same rows {ms_d:.3f} ms "
               f"{fl_d / ms_d / 1e9:.0f} TFLOP/s | grouped 128x1 quant X {ms_q * 1e3:.0f} us {qbytes / ms_q / 1e6:.0f} GB/s",
               flush=True)
         del XqT, DqT, out, x, dy, qx, qd
