@@ -504,21 +504,27 @@ def time_moe_forward(args, world, rank, dev, pb):
     ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(len(plan.experts), 1), max(plan.rows, 1), N, K)) + 16,
                      dtype=torch.uint8, device=dev)
     steps = min(args.steps, 10)
-    for _ in range(args.warmup):
-        ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws)
-    torch.cuda.synchronize()
-    barrier(world)
     stream = torch.cuda.current_stream()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = max_over_ranks(a.elapsed_time(b) / steps, world, dev)
+
+    def layer_ms(fused):
+        for _ in range(args.warmup):
+            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=fused)
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=fused)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b) / steps, world, dev)
+    ms_unfused = layer_ms(False)
+    ms = layer_ms(True)
     keep = {}
-    ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, keep=keep)
+    ref_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, keep=keep, fused=False).clone()
+    fused_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=True)
     torch.cuda.synchronize()
+    fused_ok = gather_ints([int(torch.equal(fused_out.view(torch.int16), ref_out.view(torch.int16)))], world, dev)
     xq, xs, y = keep["xq"], keep["xs"], keep["y"]
 
     def phase(fn, iters=10):
@@ -541,9 +547,11 @@ def time_moe_forward(args, world, rank, dev, pb):
     fl = sum(2.0 * r * N * K for r in rows)
     ex.barrier()
     torch.cuda.synchronize()
-    return {"what": "whole expert-layer FP8 forward per rank: quantize tokens -> NVLink FP8 dispatch -> grouped Fprop -> "
-                    "NVLink BF16 combine -> gate-weighted sum (ep.moe_forward; symmetric-memory barriers between)",
+    return {"what": "whole expert-layer FP8 forward per rank: quantize tokens -> NVLink FP8 dispatch -> grouped Fprop "
+                    "whose epilogue stores each BF16 row into its token owner's combine buffer (fused combine send) -> "
+                    "gate-weighted sum (ep.moe_forward; symmetric-memory barriers between)",
             "ms_per_step": ms, "steps": steps, "value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s (expert GEMM flop / step)",
+            "ms_per_step_unfused": ms_unfused, "fused_bitwise_equal_unfused_all_ranks": all(bool(v) for v in fused_ok),
             "dispatch_ms": ms_d, "dispatch_remote_GBps_per_rank": max(remote_d) * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9,
             "combine_ms": ms_c, "combine_remote_GBps_per_rank": max(remote_c) * N * 2 / (ms_c * 1e-3) / 1e9,
             "nvlink_reference_GBps_per_direction": 770}

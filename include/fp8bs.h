@@ -251,6 +251,22 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t
                                    void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream);
 FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K);
 
+/* ---- grouped_gemm_scatter: the MoE expert Fprop with the combine's send fused into its epilogue ----
+ * (NEXT-3; "combine components ... retained in BF16").  Computes exactly fp8bs_grouped_gemm's
+ * BF16 output (same arguments, validation, workspace and result bits), but row r of it is written to
+ *   dst_base[dst_rank[r]] + dst_row[r] * ldd   (BF16 elements, row of N values)
+ * instead of D: dst_base is a DEVICE array of destination base pointers (e.g. every rank's symmetric-
+ * memory combine buffer, written over NVLink by the epilogue's stores), dst_rank DEVICE int32 [total_M]
+ * indexes it, dst_row DEVICE int64 [total_M] is the row there.  Destinations must be 16-byte aligned,
+ * ldd*2 a multiple of 16, N a multiple of 8; rows must not overlap (undefined otherwise).  The stores
+ * are complete and visible to the peers when the kernel completes (order them with the peers before
+ * reading, e.g. a symmetric-memory barrier).  NULL table / rank / row: FP8BS_ERR_INVALID_ARG. */
+FP8BS_API fp8bs_status fp8bs_grouped_gemm_scatter(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                        const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                        const uint8_t* B, const float* sB,
+                                        void* const* dst_base, const int32_t* dst_rank, const int64_t* dst_row,
+                                        int64_t ldd, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+
 /* ---- grouped_gemm_dgrad: MoE expert Dgrad (NEXT-3; the backward of the grouped Fprop above) ----
  * dX rows of expert e = dY rows of e (1x128 along the expert's output channels) x W_e:
  * offsets, A = dYq [total_M, K] (K = the experts' output width, the contraction), sA [K/128, ldsA],

@@ -129,6 +129,10 @@ def _load(path: str) -> ctypes.CDLL:
     L.fp8bs_grouped_gemm.restype = st
     L.fp8bs_grouped_gemm.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32, i64,
                                      vp, ctypes.c_size_t, vp]
+    if hasattr(L, "fp8bs_grouped_gemm_scatter"):
+        L.fp8bs_grouped_gemm_scatter.restype = st
+        L.fp8bs_grouped_gemm_scatter.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, vp,
+                                                 vp, i64, vp, ctypes.c_size_t, vp]
     if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
         L.fp8bs_grouped_gemm_dgrad.restype = st
         L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
@@ -445,6 +449,30 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
     _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
               _p(out), _dt(out), out.stride(0), _p(workspace), workspace.numel(), _stream(A)), name)
     return out
+
+
+def grouped_gemm_scatter(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
+                         dst_ptrs: int, dst_rank: torch.Tensor, dst_row: torch.Tensor, ldd: int,
+                         workspace: torch.Tensor | None = None):
+    """fp8bs_grouped_gemm_scatter: the grouped expert Fprop (BF16) whose output row r is stored at
+    dst_ptrs[dst_rank[r]] + dst_row[r] * ldd — dst_ptrs a device address of a pointer table (e.g. a
+    symmetric-memory handle's buffer_ptrs_dev), dst_rank int32 / dst_row int64 device [R]."""
+    _cuda2d(A, "A")
+    _cuda2d(sA, "sA")
+    if offsets.dtype != torch.int64 or not offsets.is_cuda:
+        raise ValueError("offsets must be a CUDA int64 tensor")
+    if not (B.is_cuda and B.is_contiguous() and sB.is_cuda and sB.is_contiguous()):
+        raise ValueError("B and sB must be contiguous CUDA tensors")
+    if dst_rank.dtype != torch.int32 or dst_row.dtype != torch.int64 or not (dst_rank.is_cuda and dst_row.is_cuda):
+        raise ValueError("dst_rank must be CUDA int32 and dst_row CUDA int64")
+    G, N, K = B.shape
+    R = A.shape[0]
+    if workspace is None:
+        wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K))
+        workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
+    _check(lib().fp8bs_grouped_gemm_scatter(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
+                                            _p(sB), ctypes.c_void_p(dst_ptrs), _p(dst_rank), _p(dst_row), ldd,
+                                            _p(workspace), workspace.numel(), _stream(A)), "fp8bs_grouped_gemm_scatter")
 
 
 def _swiglu_outputs(R: int, N2: int, dev, cache: bool, qy, sy, qh, sh):

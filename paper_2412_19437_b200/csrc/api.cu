@@ -310,7 +310,8 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
                                         int64_t ldd, fp8bs_stream_t stream, int mx = 0, void* workspace = nullptr,
-                                        size_t workspace_bytes = 0);
+                                        size_t workspace_bytes = 0, void* const* sc_base = nullptr,
+                                        const int32_t* sc_rank = nullptr, const int64_t* sc_row = nullptr);
 
 fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
@@ -344,11 +345,23 @@ fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int
                                workspace, workspace_bytes);
 }
 
+fp8bs_status fp8bs_grouped_gemm_scatter(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
+                                        const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
+                                        const uint8_t* B, const float* sB,
+                                        void* const* dst_base, const int32_t* dst_rank, const int64_t* dst_row,
+                                        int64_t ldd, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    if (!dst_base || !dst_rank || !dst_row) return fail(FP8BS_ERR_INVALID_ARG, "null destination table");
+    /* no D: the common checks see A in its place (validated there); the rows go through the table */
+    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, (void*)A,
+                               FP8BS_BF16, ldd, stream, 0, workspace, workspace_bytes, dst_base, dst_rank, dst_row);
+}
+
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
                                         int64_t ldd, fp8bs_stream_t stream, int mx, void* workspace,
-                                        size_t workspace_bytes) {
+                                        size_t workspace_bytes, void* const* sc_base, const int32_t* sc_rank,
+                                        const int64_t* sc_row) {
     if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
     if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
     fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
@@ -370,6 +383,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     a.ldsB = layout == FP8BS_DGRAD ? (N + 127) / 128 : K / 128;
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
     a.grouped = 1; a.G = G; a.offsets = offsets; a.workspace = workspace;
+    a.sc_base = sc_base; a.sc_rank = sc_rank; a.sc_row = sc_row;
     const char* detail = nullptr;
     cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);

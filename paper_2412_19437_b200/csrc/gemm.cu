@@ -119,6 +119,8 @@ struct KParams {
     int gm;                       // raster band width (dense): tiles of the resident operand per band
     int rast_n;                   // 1: n-fastest (B resident, A streamed), 0: m-fastest
     int tile_end;                 // dense: tiles [0, tile_end) of the raster belong to this launch
+    // kOutScatter: row r of the output goes to sc_base[sc_rank[r]] + sc_row[r] * ldd (BF16 elements)
+    void* const* sc_base; const int32_t* sc_rank; const int64_t* sc_row;
     // split-K tail (kOutSplit): units u < split_units are (tile split_t0 + u / split_s, K-chunk u % split_s);
     // unit u writes its FP32 partial tile to rows [u * ROWS, (u + 1) * ROWS) of the workspace (BN columns)
     int split_t0, split_s, split_units;
@@ -464,7 +466,9 @@ __device__ __forceinline__ void swiglu_epilogue(float (&acc)[128], int h, int qu
 }
 
 // kOut: 0 BF16 output, 1 FP32 output, 2 the SwiGLU FP8 epilogue (kOutSwiglu).
-constexpr int kOutBF16 = 0, kOutFP32 = 1, kOutSwiglu = 2, kOutSplit = 3;   // kOutSplit: FP32 partials of the split-K tail
+// kOutSplit: FP32 partials of the split-K tail; kOutScatter: BF16 rows scattered to (rank, row) destinations
+// through a pointer table (the MoE combine's send fused into the grouped epilogue, NVLink peer stores)
+constexpr int kOutBF16 = 0, kOutFP32 = 1, kOutSwiglu = 2, kOutSplit = 3, kOutScatter = 4;
 template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
 __global__ void __launch_bounds__(Cfg<kPair, kWgrad>::THREADS, 1)
 k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -478,6 +482,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     static_assert(!(kSplit && kGrouped), "the split-K tail is for dense launches");
     constexpr bool kOutF32 = kOut == kOutFP32 || kSplit;
     constexpr bool kSwiglu = kOut == kOutSwiglu;
+    constexpr bool kScatter = kOut == kOutScatter;
+    static_assert(!kScatter || (kGrouped && !kWgrad), "the scatter epilogue is the grouped Fprop's");
     constexpr bool kKR = kGW || kSplit;   // tiles carry their own contraction-block range
     extern __shared__ uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
@@ -963,7 +969,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 // every warp stages its chunk the same way (one code path over acc); only the store
                 // differs: a whole 32-row block goes out as one TMA store, the rows of a grouped warp
                 // that crosses its expert's end are copied out of the staging buffer by the lanes
-                const bool full = !kGrouped || rows_here >= 32;
+                const bool full = !kGrouped || (!kScatter && rows_here >= 32);
                 const uint32_t ebuf0 = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
 #pragma unroll
                 for (int c = 0; c < NC / CW; ++c) {
@@ -989,11 +995,19 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const int col = (kSplit ? 0 : tl.n0) + h * HN + gg * NC + c * CW;   // split: the unit's slab
                     if (kGrouped && !full) {
                         __syncwarp();
-                        for (int i = lane; i < rows_here * 8; i += 32) {
+                        const int nr = rows_here < 32 ? rows_here : 32;
+                        for (int i = lane; i < nr * 8; i += 32) {
                             const int r = i >> 3, u = i & 7;
                             if (col + u * (16 / ESZ) < p.N) {
                                 const uint4 v = lds_u32x4(ebuf + r * 128 + ((u ^ (r & 7)) << 4));
-                                uint8_t* dst = reinterpret_cast<uint8_t*>(p.D) + ((int64_t)(grow0 + r) * p.ldd + col) * ESZ + u * 16;
+                                uint8_t* dst;
+                                if constexpr (kScatter) {   // 8 lanes write one row's 128 bytes to its owner
+                                    const int64_t gr = grow0 + r;
+                                    dst = reinterpret_cast<uint8_t*>(p.sc_base[__ldg(p.sc_rank + gr)]) +
+                                          (__ldg(p.sc_row + gr) * p.ldd + col) * ESZ + u * 16;
+                                } else {
+                                    dst = reinterpret_cast<uint8_t*>(p.D) + ((int64_t)(grow0 + r) * p.ldd + col) * ESZ + u * 16;
+                                }
                                 if (kOutF32 && p.accumulate) {          // Wgrad D += dW: this lane owns these 4 floats
                                     float4 o = *reinterpret_cast<const float4*>(dst);
                                     o.x += __uint_as_float(v.x); o.y += __uint_as_float(v.y);
@@ -1111,7 +1125,7 @@ static void dense_raster(const GemmArgs& a, int rows, KParams& p) {
 template <bool kWgrad, int kOut, bool kGrouped, bool kPair>
 static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** detail, const SplitPlan* sp = nullptr) {
     using C = Cfg<kPair, kWgrad>;
-    constexpr bool kSplit = kOut == kOutSplit;
+    constexpr bool kSplit = kOut == kOutSplit, kScatter = kOut == kOutScatter;
     constexpr bool kOutF32 = kOut == kOutFP32 || kSplit, kSwiglu = kOut == kOutSwiglu;
     const int KB = (int)(a.K / BK);
     constexpr bool kGW = kWgrad && kGrouped;   // grouped Wgrad: A = dYqT [M, Mp], D = [G x M, N]
@@ -1175,6 +1189,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
                 *detail = "cuTensorMapEncodeTiled failed for the SwiGLU input cache"; return cudaErrorInvalidValue;
             }
         }
+    } else if constexpr (kScatter) {
+        tD = tA; tD2 = tA;                 // no D tensor: rows are stored through the pointer table
     } else if constexpr (kSplit) {
         // the units' FP32 partial slabs: [units x ROWS, BN] in the caller's workspace
         uint64_t dims[2] = {(uint64_t)BN, (uint64_t)sp->units * C::ROWS};
@@ -1205,6 +1221,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else if (a.layout == 0) { p.sb_nb_stride = a.ldsB; p.sb_kb_stride = 1; p.sb_expert_stride = 0; }
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
+    p.sc_base = a.sc_base; p.sc_rank = a.sc_rank; p.sc_row = a.sc_row;
     p.G = a.G; p.offsets = a.offsets; p.tiles = a.workspace;
     p.tile_end = sp ? sp->t0 : p.num_m * p.num_n;
     if constexpr (kSplit) {
@@ -1310,6 +1327,7 @@ static cudaError_t launch_v(const GemmArgs& a, cudaStream_t st, const char** det
                          : launch_cfg<false, kOutSwiglu, false, kPair>(a, st, detail);
     }
     if (a.grouped) {
+        if (a.sc_base) return launch_cfg<false, kOutScatter, true, kPair>(a, st, detail);
         return a.out_f32 ? launch_cfg<false, kOutFP32, true, kPair>(a, st, detail)
                          : launch_cfg<false, kOutBF16, true, kPair>(a, st, detail);
     }

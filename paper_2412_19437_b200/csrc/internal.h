@@ -82,6 +82,8 @@ struct GemmArgs {
     int swiglu; float* sy; int64_t ldsy; uint8_t* qh; int64_t ldqh; float* sh; int64_t ldsh;
     // dense: optional split-K tail workspace (>= split_workspace_bytes(M, N, K)), nullptr = unsplit
     void* split_ws; size_t split_ws_bytes;
+    // grouped Fprop, BF16: row r stored at sc_base[sc_rank[r]] + sc_row[r] * ldd instead of D (nullptr: D)
+    void* const* sc_base; const int32_t* sc_rank; const int64_t* sc_row;
 };
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
 size_t split_workspace_bytes(int64_t M, int64_t N, int64_t K);   // 0: no split-K tail for this shape

@@ -423,10 +423,14 @@ class Exchange:
 
 
 def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: torch.Tensor, top_k: int,
-                Bq: torch.Tensor, sB: torch.Tensor, ws: torch.Tensor | None = None, keep: dict | None = None):
+                Bq: torch.Tensor, sB: torch.Tensor, ws: torch.Tensor | None = None, keep: dict | None = None,
+                fused: bool = True):
     """The expert layer's FP8 forward on this rank: 1x128 quantization of its tokens ->
     FP8 dispatch over NVLink -> grouped Fprop over the received rows -> BF16 combine over NVLink ->
-    gate-weighted sum.  keep (optional dict) receives the intermediate tensors for verification."""
+    gate-weighted sum.  fused (default): the grouped Fprop's epilogue stores each BF16 output row
+    straight into its token owner's combine buffer (fp8bs_grouped_gemm_scatter), so the combine's
+    send overlaps the GEMM and y never exists in HBM; fused=False runs the GEMM into y and then
+    fp8bs_combine_push_bf16.  keep (optional dict) receives the intermediate tensors for verification."""
     import paper_2412_19437_b200 as fp
     xq, xs = fp.quantize_act_1x128(x_local)
     fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, ex.K, ex.hs.buffer_ptrs_dev)
@@ -434,8 +438,14 @@ def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: 
     R = plan.rows
     A = ex.recv_q[:R]
     sA = fp.scales_rows_to_blocks(ex.recv_s[:R])
-    y = fp.grouped_gemm(plan.offsets_dev, A, sA, Bq, sB, workspace=ws)
-    fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, ex.N)
+    y = None
+    if fused:
+        if R > 0:
+            fp.grouped_gemm_scatter(plan.offsets_dev, A, sA, Bq, sB, ex.hy.buffer_ptrs_dev, plan.c_rank_dev,
+                                    plan.c_slot_dev, ex.N, workspace=ws)
+    else:
+        y = fp.grouped_gemm(plan.offsets_dev, A, sA, Bq, sB, workspace=ws)
+        fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, ex.N)
     ex.barrier()
     out = fp.combine_reduce_bf16(ex.recv_y[:(plan.t1 - plan.t0) * top_k], gates)
     if keep is not None:

@@ -49,7 +49,11 @@ def main():
                      dtype=torch.uint8, device=dev)
     ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * top_k for p in plans), K, N)
     keep = {}
-    out = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, keep=keep)
+    out = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, keep=keep, fused=False)
+    torch.cuda.synchronize()
+    out = out.clone()
+    # the fused form (combine's send in the grouped GEMM's epilogue) must give the same bits
+    out_fused = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True).clone()
     torch.cuda.synchronize()
     # ---- verification (NCCL all_gather outside the measured calls) ----
     def gather_cat(t, dim=0):
@@ -78,6 +82,7 @@ def main():
     y_slots = y_all.cpu()[pos[t0 * top_k:t1 * top_k]]    # this rank's slots (t, j), t in [t0, t1)
     ref = oracle.combine_bf16(y_slots, gates[t0:t1])
     res["combine_bitwise_vs_oracle"] = bool(torch.equal(out.cpu().view(torch.int16), ref.view(torch.int16)))
+    res["fused_scatter_bitwise_vs_unfused"] = bool(torch.equal(out_fused.view(torch.int16), out.view(torch.int16)))
     # ---- timing of the exchanges alone ----
     xq, xs = keep["xq"], keep["xs"]
     remote_slots = int((plan.dst_rank != rank).sum())
@@ -103,6 +108,8 @@ def main():
     res["dispatch_total_GBps"] = (t1 - t0) * top_k * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9
     res["combine_ms"] = ms_c
     res["combine_remote_GBps"] = remote_rows * N * 2 / (ms_c * 1e-3) / 1e9
+    res["layer_ms_unfused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=False), 10)
+    res["layer_ms_fused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True), 10)
     ex.barrier()
     torch.cuda.synchronize()
     allres = [None] * world

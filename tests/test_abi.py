@@ -159,3 +159,14 @@ def test_gemm_ws_workspace_size_and_validation():
     assert "workspace" in fp.last_error_detail()
     assert lib.fp8bs_gemm_ws(*args, ctypes.c_void_p((1 << 20) + 8), need, None) == L.ERR_ALIGN
     assert lib.fp8bs_gemm_ws(*args[:5], 100, *args[6:], A16, need, None) == L.ERR_SHAPE      # lda < K first
+
+
+def test_grouped_gemm_scatter_validation():
+    lib = fp.lib()
+    A16 = ctypes.c_void_p(1 << 20)
+    ws = lib.fp8bs_grouped_gemm_workspace_size(4, 10, 256, 512)
+    args = (4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16)
+    assert lib.fp8bs_grouped_gemm_scatter(*args, None, A16, A16, 256, A16, ws, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, None, A16, 256, A16, ws, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 200, A16, ws, None) == L.ERR_SHAPE       # ldd < N
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 256, A16, ws - 16, None) == L.ERR_INVALID_ARG
