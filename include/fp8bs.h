@@ -260,12 +260,20 @@ FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, i
  * indexes it, dst_row DEVICE int64 [total_M] is the row there.  Destinations must be 16-byte aligned,
  * ldd*2 a multiple of 16, N a multiple of 8; rows must not overlap (undefined otherwise).  The stores
  * are complete and visible to the peers when the kernel completes (order them with the peers before
- * reading, e.g. a symmetric-memory barrier).  NULL table / rank / row: FP8BS_ERR_INVALID_ARG. */
+ * reading, e.g. a symmetric-memory barrier).  NULL table / rank / row: FP8BS_ERR_INVALID_ARG.
+ * Streamed operands (overlap with fp8bs_dispatch_fp8_stream): ready != NULL is a DEVICE uint32 array
+ * [ready_chunks]; the rows (and scales) of local expert group e are read only once
+ * ready[e * ready_chunks / G] >= ready_target (wrap-safe compare, acquire at system scope), so a
+ * dispatch still writing A / sA from other GPUs can run concurrently.  max_sms > 0 caps the GEMM's
+ * persistent grid at that many SMs (required with ready: the SMs left run the dispatch it waits for,
+ * otherwise the two could deadlock); ready_chunks >= 1.  ready == NULL, max_sms == 0: the plain
+ * grouped Fprop with the scatter epilogue. */
 FP8BS_API fp8bs_status fp8bs_grouped_gemm_scatter(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                         const uint8_t* B, const float* sB,
                                         void* const* dst_base, const int32_t* dst_rank, const int64_t* dst_row,
-                                        int64_t ldd, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
+                                        int64_t ldd, const uint32_t* ready, uint32_t ready_target, int32_t ready_chunks,
+                                        int32_t max_sms, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
 /* ---- grouped_gemm_dgrad: MoE expert Dgrad (NEXT-3; the backward of the grouped Fprop above) ----
  * dX rows of expert e = dY rows of e (1x128 along the expert's output channels) x W_e:
@@ -304,6 +312,26 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int6
 FP8BS_API fp8bs_status fp8bs_dispatch_fp8(int64_t n_slots, int32_t top_k, int64_t K, const uint8_t* xq, int64_t ldxq,
                                 const float* xs, int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row,
                                 uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, fp8bs_stream_t stream);
+/* dispatch_fp8_stream: the dispatch of fp8bs_dispatch_fp8 restructured so the receivers' grouped GEMM
+ * can run concurrently (fp8bs_grouped_gemm_scatter with ready flags).  The sender's slots come as a
+ * DEVICE send list sorted by (chunk, destination rank, destination row): entry j sends local token
+ * send_tok[j] (its K codes of xq and its K/128 scales xs[kb * ldxs + token]) to rank send_rank[j], row
+ * send_row[j]; chunk_off DEVICE int64 [chunks + 1] delimits the chunks in the list (chunk c of a receiver
+ * = the rows of its local groups e with e * chunks / G == c).  Codes go to recv_q[rank] + row * ld_recv_q;
+ * scales go straight into the receiver's GEMM layout recv_s[rank][kb * ld_recv_s + row] (no
+ * fp8bs_scales_rows_to_blocks).  When every CTA of this call has finished chunk c (counted in
+ * local_done[c], DEVICE uint32 [chunks] scratch of this rank, zeroed on `stream` by the call), one
+ * release-add (system scope) increments flags[o][c] on every rank o (flags: DEVICE array of world
+ * pointers to uint32 [chunks] in each rank's memory).  The flags are monotonic: zero them once, then call
+ * with epoch = 1, 2, ... (one per forward, every rank); a receiver's chunk c is complete when its
+ * flags[c] reaches world * epoch.  ctas CTAs of 128 threads, one per SM (114 KB of shared memory each
+ * for the bulk-copy rings; a plain launch meant to run concurrently with the GEMM on another stream). */
+FP8BS_API fp8bs_status fp8bs_dispatch_fp8_stream(int32_t chunks, const int64_t* chunk_off, const int64_t* send_tok,
+                                       const int32_t* send_rank, const int64_t* send_row, int64_t K,
+                                       const uint8_t* xq, int64_t ldxq, const float* xs, int64_t ldxs,
+                                       uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, int64_t ld_recv_s,
+                                       uint32_t* local_done, uint32_t* const* flags, int32_t world, uint32_t epoch,
+                                       int32_t ctas, fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,
                                          fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_combine_push_bf16(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,

@@ -132,7 +132,8 @@ def _load(path: str) -> ctypes.CDLL:
     if hasattr(L, "fp8bs_grouped_gemm_scatter"):
         L.fp8bs_grouped_gemm_scatter.restype = st
         L.fp8bs_grouped_gemm_scatter.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, vp,
-                                                 vp, i64, vp, ctypes.c_size_t, vp]
+                                                 vp, i64, vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, vp,
+                                                 ctypes.c_size_t, vp]
     if hasattr(L, "fp8bs_grouped_gemm_dgrad"):
         L.fp8bs_grouped_gemm_dgrad.restype = st
         L.fp8bs_grouped_gemm_dgrad.argtypes = L.fp8bs_grouped_gemm.argtypes
@@ -147,6 +148,10 @@ def _load(path: str) -> ctypes.CDLL:
         if hasattr(L, "fp8bs_grouped_gemm_wgrad_mx"):
             L.fp8bs_grouped_gemm_wgrad_mx.restype = st
             L.fp8bs_grouped_gemm_wgrad_mx.argtypes = L.fp8bs_grouped_gemm_wgrad.argtypes
+    if hasattr(L, "fp8bs_dispatch_fp8_stream"):
+        L.fp8bs_dispatch_fp8_stream.restype = st
+        L.fp8bs_dispatch_fp8_stream.argtypes = [ctypes.c_int32, vp, vp, vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                                vp, vp, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, vp]
     if hasattr(L, "fp8bs_dispatch_fp8"):
         L.fp8bs_dispatch_fp8.restype = st
         L.fp8bs_dispatch_fp8.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
@@ -453,10 +458,12 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
 
 def grouped_gemm_scatter(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: torch.Tensor, sB: torch.Tensor,
                          dst_ptrs: int, dst_rank: torch.Tensor, dst_row: torch.Tensor, ldd: int,
-                         workspace: torch.Tensor | None = None):
+                         workspace: torch.Tensor | None = None, ready: torch.Tensor | None = None,
+                         ready_target: int = 0, ready_chunks: int = 0, max_sms: int = 0):
     """fp8bs_grouped_gemm_scatter: the grouped expert Fprop (BF16) whose output row r is stored at
     dst_ptrs[dst_rank[r]] + dst_row[r] * ldd — dst_ptrs a device address of a pointer table (e.g. a
-    symmetric-memory handle's buffer_ptrs_dev), dst_rank int32 / dst_row int64 device [R]."""
+    symmetric-memory handle's buffer_ptrs_dev), dst_rank int32 / dst_row int64 device [R].  ready (device
+    int32/uint32 [ready_chunks]), ready_target, max_sms: streamed operands (include/fp8bs.h)."""
     _cuda2d(A, "A")
     _cuda2d(sA, "sA")
     if offsets.dtype != torch.int64 or not offsets.is_cuda:
@@ -472,7 +479,21 @@ def grouped_gemm_scatter(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tenso
         workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
     _check(lib().fp8bs_grouped_gemm_scatter(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B),
                                             _p(sB), ctypes.c_void_p(dst_ptrs), _p(dst_rank), _p(dst_row), ldd,
+                                            _p(ready), ready_target & 0xFFFFFFFF, ready_chunks, max_sms,
                                             _p(workspace), workspace.numel(), _stream(A)), "fp8bs_grouped_gemm_scatter")
+
+
+def dispatch_fp8_stream(chunk_off: torch.Tensor, send_tok: torch.Tensor, send_rank: torch.Tensor, send_row: torch.Tensor,
+                        xq: torch.Tensor, xs: torch.Tensor, recv_q_ptrs: int, ld_recv_q: int, recv_s_ptrs: int,
+                        ld_recv_s: int, local_done: torch.Tensor, flag_ptrs: int, world: int, epoch: int, ctas: int = 32):
+    """fp8bs_dispatch_fp8_stream (include/fp8bs.h): the chunked dispatch a concurrent grouped GEMM waits on."""
+    _cuda2d(xq, "xq")
+    K = xq.shape[1]
+    _check(lib().fp8bs_dispatch_fp8_stream(chunk_off.numel() - 1, _p(chunk_off), _p(send_tok), _p(send_rank), _p(send_row),
+                                           K, _p(xq), xq.stride(0), _p(xs), xs.stride(0), ctypes.c_void_p(recv_q_ptrs),
+                                           ld_recv_q, ctypes.c_void_p(recv_s_ptrs), ld_recv_s, _p(local_done),
+                                           ctypes.c_void_p(flag_ptrs), world, epoch & 0xFFFFFFFF, ctas, _stream(xq)),
+           "fp8bs_dispatch_fp8_stream")
 
 
 def _swiglu_outputs(R: int, N2: int, dev, cache: bool, qy, sy, qh, sh):

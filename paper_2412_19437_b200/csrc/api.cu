@@ -306,12 +306,16 @@ size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, 
     return grouped_workspace_bytes(G, total_M, N);
 }
 
+// streamed-operand arguments of fp8bs_grouped_gemm_scatter (internal.h GemmArgs::ready / max_sms)
+struct StreamArgs { const uint32_t* ready; uint32_t target; int32_t chunks; int32_t max_sms; };
+
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
                                         const int64_t* offsets, const uint8_t* A, int64_t lda, const float* sA,
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
                                         int64_t ldd, fp8bs_stream_t stream, int mx = 0, void* workspace = nullptr,
                                         size_t workspace_bytes = 0, void* const* sc_base = nullptr,
-                                        const int32_t* sc_rank = nullptr, const int64_t* sc_row = nullptr);
+                                        const int32_t* sc_rank = nullptr, const int64_t* sc_row = nullptr,
+                                        const StreamArgs* sa_stream = nullptr);
 
 fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                 const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
@@ -349,11 +353,17 @@ fp8bs_status fp8bs_grouped_gemm_scatter(int32_t G, int64_t total_M, int64_t N, i
                                         const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                         const uint8_t* B, const float* sB,
                                         void* const* dst_base, const int32_t* dst_rank, const int64_t* dst_row,
-                                        int64_t ldd, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+                                        int64_t ldd, const uint32_t* ready, uint32_t ready_target, int32_t ready_chunks,
+                                        int32_t max_sms, void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
     if (!dst_base || !dst_rank || !dst_row) return fail(FP8BS_ERR_INVALID_ARG, "null destination table");
+    if (ready && ready_chunks < 1) return fail(FP8BS_ERR_INVALID_ARG, "ready_chunks=%d must be >= 1", (int)ready_chunks);
+    if (max_sms < 0) return fail(FP8BS_ERR_INVALID_ARG, "max_sms=%d < 0", (int)max_sms);
+    if (ready && max_sms == 0)
+        return fail(FP8BS_ERR_INVALID_ARG, "streamed operands need max_sms > 0 (SMs left for the dispatch it waits for)");
+    const StreamArgs sa{ready, ready_target, ready_chunks, max_sms};
     /* no D: the common checks see A in its place (validated there); the rows go through the table */
     return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, (void*)A,
-                               FP8BS_BF16, ldd, stream, 0, workspace, workspace_bytes, dst_base, dst_rank, dst_row);
+                               FP8BS_BF16, ldd, stream, 0, workspace, workspace_bytes, dst_base, dst_rank, dst_row, &sa);
 }
 
 static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, int64_t N, int64_t K,
@@ -361,7 +371,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
                                         int64_t ldsA, const uint8_t* B, const float* sB, void* D, fp8bs_dtype ddt,
                                         int64_t ldd, fp8bs_stream_t stream, int mx, void* workspace,
                                         size_t workspace_bytes, void* const* sc_base, const int32_t* sc_rank,
-                                        const int64_t* sc_row) {
+                                        const int64_t* sc_row, const StreamArgs* sa_stream) {
     if (G < 1 || G > 1024) return fail(FP8BS_ERR_INVALID_ARG, "G=%d must be in [1, 1024]", (int)G);
     if (!offsets) return fail(FP8BS_ERR_INVALID_ARG, "offsets is NULL");
     fp8bs_status c = check_gemm_common(total_M, N, K, A, lda, sA, ldsA, B, K, sB, D, ddt, ldd);
@@ -384,6 +394,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     a.D = D; a.out_f32 = ddt == FP8BS_FP32; a.ldd = ldd; a.accumulate = 0;
     a.grouped = 1; a.G = G; a.offsets = offsets; a.workspace = workspace;
     a.sc_base = sc_base; a.sc_rank = sc_rank; a.sc_row = sc_row;
+    if (sa_stream) { a.ready = sa_stream->ready; a.ready_target = sa_stream->target; a.ready_chunks = sa_stream->chunks; a.max_sms = sa_stream->max_sms; }
     const char* detail = nullptr;
     cudaError_t e = mx ? launch_gemm_mx(a, (cudaStream_t)stream, &detail) : launch_gemm(a, (cudaStream_t)stream, &detail);
     if (e != cudaSuccess && detail) return fail(FP8BS_ERR_CUDA, "%s", detail);
@@ -405,6 +416,26 @@ fp8bs_status fp8bs_dispatch_fp8(int64_t n_slots, int32_t top_k, int64_t K, const
     if (d != FP8BS_OK) return d;
     return from_cuda(launch_dispatch_fp8(n_slots, top_k, K, xq, ldxq, xs, ldxs, dst_rank, dst_row, recv_q, ld_recv_q, recv_s,
                                          (cudaStream_t)stream), "dispatch_fp8 launch");
+}
+
+fp8bs_status fp8bs_dispatch_fp8_stream(int32_t chunks, const int64_t* chunk_off, const int64_t* send_tok,
+                                       const int32_t* send_rank, const int64_t* send_row, int64_t K,
+                                       const uint8_t* xq, int64_t ldxq, const float* xs, int64_t ldxs,
+                                       uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, int64_t ld_recv_s,
+                                       uint32_t* local_done, uint32_t* const* flags, int32_t world, uint32_t epoch,
+                                       int32_t ctas, fp8bs_stream_t stream) {
+    if (chunks < 1 || chunks > 1024) return fail(FP8BS_ERR_INVALID_ARG, "chunks=%d must be in [1, 1024]", (int)chunks);
+    if (world < 1 || ctas < 1 || epoch == 0) return fail(FP8BS_ERR_INVALID_ARG, "need world >= 1, ctas >= 1, epoch >= 1");
+    if (K <= 0 || K % 128) return fail(FP8BS_ERR_SHAPE, "K must be a positive multiple of 128 (whole 1x128 groups)");
+    if (!chunk_off || !send_tok || !send_rank || !send_row || !xq || !xs || !recv_q || !recv_s || !local_done || !flags)
+        return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
+    if (ldxq < K || ld_recv_q < K || ldxs < 0 || ld_recv_s < 0) return fail(FP8BS_ERR_SHAPE, "need ldxq, ld_recv_q >= K");
+    if (!aligned16(xq) || ldxq % 16 || ld_recv_q % 16) return fail(FP8BS_ERR_ALIGN, "xq 16-byte aligned, ldxq and ld_recv_q multiples of 16");
+    fp8bs_status d = check_device();
+    if (d != FP8BS_OK) return d;
+    return from_cuda(launch_dispatch_stream(chunks, chunk_off, send_tok, send_rank, send_row, K, xq, ldxq, xs, ldxs, recv_q,
+                                            ld_recv_q, recv_s, ld_recv_s, local_done, flags, world, epoch, ctas,
+                                            (cudaStream_t)stream), "dispatch_fp8_stream launch");
 }
 
 fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,

@@ -46,6 +46,108 @@ __global__ void __launch_bounds__(256) k_dispatch_fp8(int64_t n, int top_k, int6
     }
 }
 
+// Streamed dispatch (overlapped with the expert GEMM on the receivers): the sender's slots come as a
+// SEND LIST sorted by (chunk, destination rank, destination row); chunk c of a receiver is the rows of
+// its local expert groups g with g * C / G == c, so every receiver's GEMM can start on chunk c as soon as
+// all senders have delivered it.  Per entry: the token's K codes (a warp per row, 16-byte stores) and its
+// KB scales written straight into the receiver's [KB][ld_rs] GEMM layout (lane = entry: 32 consecutive
+// destination rows give 128-byte stores per contraction block).  After its part of chunk c every CTA
+// fences (system scope) and counts itself on local_done[c]; the CTA that completes the count publishes the
+// chunk with one release-add on every receiver's flag[c].  local_done is zeroed on the stream before every
+// call; the flags are monotonic: after call number `epoch` (1, 2, ...) each flag[c] = world * epoch.
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// The codes of a row travel by TMA bulk copies (global -> shared -> peer global, one elected lane per
+// warp driving a per-warp ring of kDsStages row buffers): a warp then keeps several rows in flight with a
+// handful of instructions, so a dispatch confined to a few SMs still fills the link (per-lane 16-byte
+// peer stores reached ~15-20 GB/s per SM, i.e. ~40 SMs taken from the concurrent GEMM).
+// Measured (C4, 2 GPUs, the dispatch alone): ~18-30 GB/s per SM whatever the ring shape (4 warps x 4
+// stages, 3 loads ahead: 6.7 ms on 8 SMs, 2.1 ms on 32, 1.6 ms on 128; 2 warps x 8 stages, 2 ahead: 12.4 ms
+// on 8 SMs), like per-lane 16-byte peer stores: a dispatch confined to few SMs cannot fill the link.
+constexpr int kDsWarps = 4, kDsStages = 4, kDsAhead = 3;
+
+__global__ void __launch_bounds__(32 * kDsWarps) k_dispatch_stream(int C, const int64_t* __restrict__ chunk_off,
+                                                         const int64_t* __restrict__ send_tok, const int32_t* __restrict__ send_rank,
+                                                         const int64_t* __restrict__ send_row, int64_t K, int64_t KB,
+                                                         const uint8_t* __restrict__ xq, int64_t ldxq,
+                                                         const float* __restrict__ xs, int64_t ldxs,
+                                                         uint8_t* const* __restrict__ recv_q, int64_t ld_rq,
+                                                         float* const* __restrict__ recv_s, int64_t ld_rs,
+                                                         uint32_t* __restrict__ local_done, uint32_t* const* __restrict__ flags,
+                                                         int world, uint32_t epoch) {
+    extern __shared__ __align__(128) uint8_t dsmem[];
+    griddep_wait();
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rowb = (uint32_t)((K + 127) / 128 * 128);           // one staged row, 128-byte aligned
+    const uint32_t ring = smem_u32(dsmem) + (uint32_t)warp * kDsStages * rowb;
+    const uint32_t bar0 = smem_u32(dsmem) + (uint32_t)kDsWarps * kDsStages * rowb + (uint32_t)warp * kDsStages * 8;
+    if (lane == 0) {
+        for (int i = 0; i < kDsStages; ++i) mbar_init(bar0 + 8 * i, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t nload = 0;                                                // rows loaded by this warp so far (ring position)
+    for (int c = 0; c < C; ++c) {
+        const int64_t s0 = chunk_off[c], s1 = chunk_off[c + 1];
+        const int64_t nb = (s1 - s0 + 31) / 32;
+        for (int64_t b = (int64_t)blockIdx.x * kDsWarps + warp; b < nb; b += (int64_t)gridDim.x * kDsWarps) {
+            const int64_t e0 = s0 + b * 32;
+            const int n = (int)min((int64_t)32, s1 - e0);
+            int64_t tok = 0, row = 0;
+            int rk = 0;
+            if (lane < n) { tok = send_tok[e0 + lane]; rk = send_rank[e0 + lane]; row = send_row[e0 + lane]; }
+            // codes: lane 0 streams the n rows through the ring, loads kDsAhead rows ahead of the stores.
+            // Step j: store row j - kDsAhead from its stage, then load row j into stage (j mod S) once the
+            // store of row j - S (issued at step j - S + kDsAhead, followed by S - kDsAhead newer store
+            // groups) has read it.
+            const uint32_t base = nload;
+            for (int j = 0; j < n + kDsAhead; ++j) {
+                const int jj = j - kDsAhead;
+                const int64_t tj = __shfl_sync(0xffffffffu, tok, j < n ? j : 0);
+                const int64_t rwj = __shfl_sync(0xffffffffu, row, jj >= 0 ? jj : 0);
+                const int rkj = __shfl_sync(0xffffffffu, rk, jj >= 0 ? jj : 0);
+                if (lane == 0) {
+                    if (jj >= 0) {
+                        const uint32_t q = (base + (uint32_t)jj) % kDsStages;
+                        mbar_wait(bar0 + 8 * q, ((base + (uint32_t)jj) / kDsStages) & 1u);
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                     :: "l"(recv_q[rkj] + rwj * ld_rq), "r"(ring + q * rowb), "r"((uint32_t)K) : "memory");
+                        bulk_commit_group();
+                    }
+                    if (j < n) {
+                        const uint32_t q = (base + (uint32_t)j) % kDsStages;
+                        bulk_wait_group_read<kDsStages - kDsAhead>();
+                        mbar_arrive_expect_tx(bar0 + 8 * q, (uint32_t)K);
+                        bulk_load(ring + q * rowb, xq + tj * ldxq, (uint32_t)K, bar0 + 8 * q);
+                    }
+                }
+            }
+            nload = base + (uint32_t)n;
+            if (lane < n) {                             // scales: lane = entry, one store per contraction block
+                float* ds = recv_s[rk] + row;
+                for (int64_t kb = 0; kb < KB; ++kb) ds[kb * ld_rs] = xs[kb * ldxs + tok];
+            }
+        }
+        // chunk c: this warp's bulk stores complete (written at the destination), then ordered before
+        // the count with the generic proxy at system scope
+        if (lane == 0) bulk_wait_group<0>();
+        __syncwarp();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t old = atomicAdd(local_done + c, 1u);
+            if (old == gridDim.x - 1u) {                // the last CTA of this rank to finish chunk c
+                __threadfence_system();
+                for (int o = 0; o < world; ++o) red_release_sys_add(flags[o] + c, 1u);
+            }
+        }
+    }
+}
+
 // Row-major [R][KB] scales -> the GEMM's contraction-block-major [KB][ldd] layout (32 x 32 tiles through
 // shared memory: both sides coalesced).
 __global__ void __launch_bounds__(256) k_rows_to_blocks(int64_t R, int64_t KB, const float* __restrict__ src,
@@ -127,6 +229,27 @@ cudaError_t launch_dispatch_fp8(int64_t n, int top_k, int64_t K, const uint8_t* 
                                 int64_t ld_rq, float* const* recv_s, cudaStream_t st) {
     return launch_pdl(k_dispatch_fp8, dim3(rows_grid(n)), dim3(256), 0, st, n, top_k, K, K / 128, xq, ldxq, xs, ldxs,
                       dst_rank, dst_row, recv_q, ld_rq, recv_s);
+}
+cudaError_t launch_dispatch_stream(int C, const int64_t* chunk_off, const int64_t* send_tok, const int32_t* send_rank,
+                                  const int64_t* send_row, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
+                                  int64_t ldxs, uint8_t* const* recv_q, int64_t ld_rq, float* const* recv_s, int64_t ld_rs,
+                                  uint32_t* local_done, uint32_t* const* flags, int world, uint32_t epoch, int ctas,
+                                  cudaStream_t st) {
+    // plain launch (no PDL attribute): it runs concurrently with the GEMM on another stream
+    const size_t rowb = (size_t)((K + 127) / 128 * 128);
+    const size_t smem = (size_t)kDsWarps * kDsStages * (rowb + 8);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_dispatch_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    // the per-chunk CTA counts start from zero every call (the flags are the monotonic counters)
+    cudaError_t e0 = cudaMemsetAsync(local_done, 0, (size_t)C * sizeof(uint32_t), st);
+    if (e0 != cudaSuccess) return e0;
+    k_dispatch_stream<<<ctas, 32 * kDsWarps, smem, st>>>(C, chunk_off, send_tok, send_rank, send_row, K, K / 128, xq, ldxq,
+                                                         xs, ldxs, recv_q, ld_rq, recv_s, ld_rs, local_done, flags, world,
+                                                         epoch);
+    return cudaPeekAtLastError();
 }
 cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st) {
     return launch_pdl(k_rows_to_blocks, dim3((unsigned)((R + 31) / 32), (unsigned)((KB + 31) / 32)), dim3(256), 0, st,

@@ -121,6 +121,9 @@ struct KParams {
     int tile_end;                 // dense: tiles [0, tile_end) of the raster belong to this launch
     // kOutScatter: row r of the output goes to sc_base[sc_rank[r]] + sc_row[r] * ldd (BF16 elements)
     void* const* sc_base; const int32_t* sc_rank; const int64_t* sc_row;
+    // grouped, streamed operands (a dispatch still writing A / sA): the rows of local group e may be
+    // read once ready[e * ready_chunks / G] >= ready_target (wrap-safe); ready == nullptr: no waits
+    const uint32_t* ready; uint32_t ready_target; int ready_chunks;
     // split-K tail (kOutSplit): units u < split_units are (tile split_t0 + u / split_s, K-chunk u % split_s);
     // unit u writes its FP32 partial tile to rows [u * ROWS, (u + 1) * ROWS) of the workspace (BN columns)
     int split_t0, split_s, split_units;
@@ -204,6 +207,19 @@ __device__ __forceinline__ bool get_tile_split(const KParams& p, int u, Tile& tl
     tl.kbn = (c + 1) * p.KB / p.split_s - tl.kb0;
     tl.orow0 = u * ROWS; tl.row_end = tl.orow0 + ROWS;
     return true;
+}
+
+// Streamed operands: spin (acquire, system scope: the writers are other GPUs' dispatch kernels) until the
+// tile's chunk is published, then order those generic-proxy writes before this thread's TMA reads.
+__device__ __forceinline__ void wait_chunk_ready(const KParams& p, int e) {
+    const uint32_t* f = p.ready + (e * p.ready_chunks) / p.G;
+    uint32_t v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - p.ready_target) >= 0) break;
+        __nanosleep(256);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Grouped Wgrad tiles: expert-major, m fastest inside an expert (the smaller operand dYqT_e stays in
@@ -619,6 +635,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             Tile tl;
             auto tix = [&](int j) { return rank == 0 ? tile_index_claim(j) : tile_index(j); };
             for (int j = 0, t = tix(0); next_tile(t, tl); t = tix(++j)) {
+                if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
                 const int arow = tl.row0 + (int)rank * BM;
                 const int brow = tl.n0 + (int)rank * C::BH_ROWS;
                 for (int kb = 0; kb < nkb(tl); ++kb, ++it) {
@@ -722,6 +739,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if ((kDbg & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
             for (int j = 0, t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
+                if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
                 const float* sbp = p.sB;
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
                 const int arow = tl.row0 + (int)rank * BM;
@@ -1222,6 +1240,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.sc_base = a.sc_base; p.sc_rank = a.sc_rank; p.sc_row = a.sc_row;
+    p.ready = a.ready; p.ready_target = a.ready_target; p.ready_chunks = a.ready_chunks;
     p.G = a.G; p.offsets = a.offsets; p.tiles = a.workspace;
     p.tile_end = sp ? sp->t0 : p.num_m * p.num_n;
     if constexpr (kSplit) {
@@ -1241,7 +1260,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else if (kGrouped) tiles_ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;
     else if (kSplit) tiles_ub = sp->units;
     else tiles_ub = p.tile_end;
-    const int64_t max_clusters = num_sms() / C::CS;
+    int64_t max_clusters = num_sms() / C::CS;
+    if (a.max_sms > 0 && a.max_sms / C::CS < max_clusters) max_clusters = a.max_sms / C::CS;   // SMs left to a concurrent kernel
     int clusters = (int)(tiles_ub < max_clusters ? tiles_ub : max_clusters);
     if (clusters < 1) clusters = 1;
     const int smem = C::SMEM_DENSE;

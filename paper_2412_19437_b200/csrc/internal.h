@@ -59,6 +59,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 cudaError_t launch_dispatch_fp8(int64_t n, int top_k, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
                                 int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
                                 int64_t ld_rq, float* const* recv_s, cudaStream_t st);
+cudaError_t launch_dispatch_stream(int C, const int64_t* chunk_off, const int64_t* send_tok, const int32_t* send_rank,
+                                  const int64_t* send_row, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
+                                  int64_t ldxs, uint8_t* const* recv_q, int64_t ld_rq, float* const* recv_s, int64_t ld_rs,
+                                  uint32_t* local_done, uint32_t* const* flags, int world, uint32_t epoch, int ctas,
+                                  cudaStream_t st);
 cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st);
 cudaError_t launch_combine_push(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,
                                 const int64_t* dst_slot, void* const* recv_y, int64_t ld_recv_y, cudaStream_t st);
@@ -84,6 +89,9 @@ struct GemmArgs {
     void* split_ws; size_t split_ws_bytes;
     // grouped Fprop, BF16: row r stored at sc_base[sc_rank[r]] + sc_row[r] * ldd instead of D (nullptr: D)
     void* const* sc_base; const int32_t* sc_rank; const int64_t* sc_row;
+    // grouped, streamed A / sA: wait for ready[e * ready_chunks / G] >= ready_target (nullptr: no waits);
+    // max_sms > 0 caps the persistent grid (the SMs left run the concurrent dispatch)
+    const uint32_t* ready; uint32_t ready_target; int ready_chunks; int max_sms;
 };
 size_t grouped_workspace_bytes(int32_t G, int64_t total_M, int64_t N);
 size_t split_workspace_bytes(int64_t M, int64_t N, int64_t K);   // 0: no split-K tail for this shape

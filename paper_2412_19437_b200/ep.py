@@ -362,10 +362,17 @@ class ExchangePlan:
     c_rank: torch.Tensor             # int32 [R_local]: token owner of each received row
     c_slot: torch.Tensor             # int64 [R_local]: its slot (t - t0(owner)) * top_k + j there
     rows: int                        # R_local
+    # streamed dispatch (fp8bs_dispatch_fp8_stream): this rank's slots sorted by (chunk, dst rank, dst
+    # row), chunk c of a receiver = the rows of its local groups g with g * chunks // G == c
+    chunks: int = 8
+    send_tok: torch.Tensor | None = None    # int64 [S]: local token (t - t0) of entry j
+    send_rank: torch.Tensor | None = None   # int32 [S]
+    send_row: torch.Tensor | None = None    # int64 [S]
+    chunk_off: torch.Tensor | None = None   # int64 [chunks + 1]: entries of chunk c are [chunk_off[c], chunk_off[c+1])
 
 
 def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
-                  placement: Placement | None = None) -> ExchangePlan:
+                  placement: Placement | None = None, chunks: int = 8) -> ExchangePlan:
     """Dispatch / combine bookkeeping of `rank` under `placement` (default contiguous): slot (t, j) of
     a token goes to the rank computing its global row; with a redundant expert, the copy whose share
     of the expert's rows holds that row (chunk_bounds)."""
@@ -382,11 +389,16 @@ def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
     offsets[1:] = torch.cumsum(counts, 0)
     owner_of_row = torch.full((T * k,), -1, dtype=torch.int64)
     lrow_of_row = torch.full((T * k,), -1, dtype=torch.int64)
+    chunk_of_row = torch.zeros(T * k, dtype=torch.int64)
     mine = None
     for r in range(world):
         rows_r, loff_r, exps_r = placement_rows(offsets, placement, r)
         owner_of_row[rows_r] = r
         lrow_of_row[rows_r] = torch.arange(rows_r.numel(), dtype=torch.int64)
+        G_r = loff_r.numel() - 1
+        if G_r > 0:
+            grp = torch.repeat_interleave(torch.arange(G_r, dtype=torch.int64), loff_r[1:] - loff_r[:-1])
+            chunk_of_row[rows_r] = grp * chunks // G_r
         if r == rank:
             mine = (rows_r, loff_r, exps_r)
     assert bool((owner_of_row >= 0).all()), "placement does not cover every row"
@@ -399,23 +411,49 @@ def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
     tok = slots // k
     tok_owner = torch.searchsorted(t_start, tok, right=True) - 1
     c_slot = (tok - t_start[tok_owner]) * k + slots % k
-    return ExchangePlan(t0, t1, [int(e) for e in exps], rows_me, owner_of_row[g].to(torch.int32), lrow_of_row[g],
-                        loff, tok_owner.to(torch.int32), c_slot, int(rows_me.numel()))
+    d_rank, d_row, d_chunk = owner_of_row[g], lrow_of_row[g], chunk_of_row[g]
+    key = (d_chunk * world + d_rank) * (T * k) + d_row
+    order_s = torch.argsort(key, stable=True)
+    chunk_off = torch.zeros(chunks + 1, dtype=torch.int64)
+    chunk_off[1:] = torch.cumsum(torch.bincount(d_chunk, minlength=chunks), 0)
+    return ExchangePlan(t0, t1, [int(e) for e in exps], rows_me, d_rank.to(torch.int32), d_row,
+                        loff, tok_owner.to(torch.int32), c_slot, int(rows_me.numel()), chunks,
+                        order_s // k, d_rank[order_s].to(torch.int32), d_row[order_s], chunk_off)
 
 
 class Exchange:
     """Symmetric-memory receive buffers of the exchange (rendezvous over `group`): FP8 codes + row-major
-    scales for dispatch, BF16 expert outputs per token slot for combine."""
+    scales for dispatch, BF16 expert outputs per token slot for combine; for the streamed dispatch also
+    the scales in the GEMM's [K/128][ld] layout, the per-chunk ready flags (uint32, zeroed once) and two
+    combine buffers used alternately (a peer's GEMM of forward n+1 may write while this rank still reads
+    forward n's)."""
 
-    def __init__(self, group, device, max_rows: int, max_slots: int, K: int, N: int):
+    def __init__(self, group, device, max_rows: int, max_slots: int, K: int, N: int, chunks: int = 8,
+                 dispatch_ctas: int = 32):
+        import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
-        self.K, self.N = K, N
+        self.K, self.N, self.chunks, self.ctas = K, N, chunks, dispatch_ctas
+        self.world = dist.get_world_size(group)
         self.recv_q = symm_mem.empty(max_rows, K, dtype=torch.uint8, device=device)
         self.recv_s = symm_mem.empty(max_rows, K // 128, dtype=torch.float32, device=device)
+        self.ld_sb = max(4, (max_rows + 3) // 4 * 4)
+        self.recv_sb = symm_mem.empty(K // 128, self.ld_sb, dtype=torch.float32, device=device)
         self.recv_y = symm_mem.empty(max_slots, N, dtype=torch.bfloat16, device=device)
+        self.recv_y2 = symm_mem.empty(max_slots, N, dtype=torch.bfloat16, device=device)
+        self.flags = symm_mem.empty(chunks, dtype=torch.int32, device=device)
+        self.flags.zero_()
         self.hq = symm_mem.rendezvous(self.recv_q, group)
         self.hs = symm_mem.rendezvous(self.recv_s, group)
+        self.hsb = symm_mem.rendezvous(self.recv_sb, group)
         self.hy = symm_mem.rendezvous(self.recv_y, group)
+        self.hy2 = symm_mem.rendezvous(self.recv_y2, group)
+        self.hf = symm_mem.rendezvous(self.flags, group)
+        self.local_done = torch.zeros(chunks, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self.dstream = torch.cuda.Stream(device=device)
+        self.num_sms = torch.cuda.get_device_properties(device).multi_processor_count
+        torch.cuda.synchronize(device)
+        self.hf.barrier(channel=0)          # every rank's flags are zero before anyone can signal them
 
     def barrier(self):
         """Every rank's kernels enqueued so far (their peer writes) complete before what follows."""
@@ -424,30 +462,55 @@ class Exchange:
 
 def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: torch.Tensor, top_k: int,
                 Bq: torch.Tensor, sB: torch.Tensor, ws: torch.Tensor | None = None, keep: dict | None = None,
-                fused: bool = True):
+                fused: bool = True, streamed: bool = False):
     """The expert layer's FP8 forward on this rank: 1x128 quantization of its tokens ->
     FP8 dispatch over NVLink -> grouped Fprop over the received rows -> BF16 combine over NVLink ->
     gate-weighted sum.  fused (default): the grouped Fprop's epilogue stores each BF16 output row
     straight into its token owner's combine buffer (fp8bs_grouped_gemm_scatter), so the combine's
     send overlaps the GEMM and y never exists in HBM; fused=False runs the GEMM into y and then
-    fp8bs_combine_push_bf16.  keep (optional dict) receives the intermediate tensors for verification."""
+    fp8bs_combine_push_bf16.  streamed (implies fused): the dispatch runs on its own stream and SMs
+    (fp8bs_dispatch_fp8_stream, chunk by chunk in the receivers' expert order, scales straight into the
+    GEMM's layout) while the GEMM, on the remaining SMs, waits per chunk on the ready flags the senders
+    publish: no barrier and no scale re-layout between dispatch and GEMM.  keep (optional dict)
+    receives the intermediate tensors for verification."""
     import paper_2412_19437_b200 as fp
     xq, xs = fp.quantize_act_1x128(x_local)
-    fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, ex.K, ex.hs.buffer_ptrs_dev)
-    ex.barrier()
     R = plan.rows
-    A = ex.recv_q[:R]
-    sA = fp.scales_rows_to_blocks(ex.recv_s[:R])
     y = None
-    if fused:
+    buf = ex.recv_y
+    if streamed:
+        ex.epoch += 1
+        hy = ex.hy if ex.epoch % 2 else ex.hy2
+        buf = ex.recv_y if ex.epoch % 2 else ex.recv_y2
+        main = torch.cuda.current_stream()
+        ex.dstream.wait_stream(main)
+        with torch.cuda.stream(ex.dstream):
+            fp.dispatch_fp8_stream(plan.chunk_off_dev, plan.send_tok_dev, plan.send_rank_dev, plan.send_row_dev, xq, xs,
+                                   ex.hq.buffer_ptrs_dev, ex.K, ex.hsb.buffer_ptrs_dev, ex.ld_sb, ex.local_done,
+                                   ex.hf.buffer_ptrs_dev, ex.world, ex.epoch, ex.ctas)
+        A = ex.recv_q[:R]
+        sA = ex.recv_sb[:, :R]
         if R > 0:
-            fp.grouped_gemm_scatter(plan.offsets_dev, A, sA, Bq, sB, ex.hy.buffer_ptrs_dev, plan.c_rank_dev,
-                                    plan.c_slot_dev, ex.N, workspace=ws)
+            fp.grouped_gemm_scatter(plan.offsets_dev, A, sA, Bq, sB, hy.buffer_ptrs_dev, plan.c_rank_dev, plan.c_slot_dev,
+                                    ex.N, workspace=ws, ready=ex.flags, ready_target=ex.world * ex.epoch,
+                                    ready_chunks=plan.chunks, max_sms=ex.num_sms - ex.ctas)
+        main.wait_stream(ex.dstream)
+        xq.record_stream(ex.dstream)
+        xs.record_stream(ex.dstream)
     else:
-        y = fp.grouped_gemm(plan.offsets_dev, A, sA, Bq, sB, workspace=ws)
-        fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, ex.N)
+        fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, ex.K, ex.hs.buffer_ptrs_dev)
+        ex.barrier()
+        A = ex.recv_q[:R]
+        sA = fp.scales_rows_to_blocks(ex.recv_s[:R])
+        if fused:
+            if R > 0:
+                fp.grouped_gemm_scatter(plan.offsets_dev, A, sA, Bq, sB, ex.hy.buffer_ptrs_dev, plan.c_rank_dev,
+                                        plan.c_slot_dev, ex.N, workspace=ws)
+        else:
+            y = fp.grouped_gemm(plan.offsets_dev, A, sA, Bq, sB, workspace=ws)
+            fp.combine_push_bf16(y, plan.c_rank_dev, plan.c_slot_dev, ex.hy.buffer_ptrs_dev, ex.N)
     ex.barrier()
-    out = fp.combine_reduce_bf16(ex.recv_y[:(plan.t1 - plan.t0) * top_k], gates)
+    out = fp.combine_reduce_bf16(buf[:(plan.t1 - plan.t0) * top_k], gates)
     if keep is not None:
         keep.update(xq=xq, xs=xs, A=A, sA=sA, y=y, out=out)
     return out
@@ -459,4 +522,8 @@ def plan_to_device(plan: ExchangePlan, device) -> ExchangePlan:
     plan.offsets_dev = plan.offsets.to(device)
     plan.c_rank_dev = plan.c_rank.to(device)
     plan.c_slot_dev = plan.c_slot.to(device)
+    plan.send_tok_dev = plan.send_tok.to(device)
+    plan.send_rank_dev = plan.send_rank.to(device)
+    plan.send_row_dev = plan.send_row.to(device)
+    plan.chunk_off_dev = plan.chunk_off.to(device)
     return plan

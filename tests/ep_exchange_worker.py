@@ -47,13 +47,18 @@ def main():
     gl = gates[t0:t1].contiguous().to(dev)
     ws = torch.empty(int(fp.lib().fp8bs_grouped_gemm_workspace_size(max(len(plan.experts), 1), max(plan.rows, 1), N, K)) + 16,
                      dtype=torch.uint8, device=dev)
-    ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * top_k for p in plans), K, N)
+    ex = ep.Exchange(dist.group.WORLD, dev, max(p.rows for p in plans), max((p.t1 - p.t0) * top_k for p in plans), K, N,
+                     dispatch_ctas=int(os.environ.get("FP8BS_EP_CTAS", "32")))
     keep = {}
     out = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, keep=keep, fused=False)
     torch.cuda.synchronize()
     out = out.clone()
     # the fused form (combine's send in the grouped GEMM's epilogue) must give the same bits
     out_fused = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True).clone()
+    torch.cuda.synchronize()
+    # the streamed form (dispatch overlapped with the GEMM through per-chunk ready flags), twice: the
+    # second call exercises the monotonic counters and the other combine buffer
+    outs_streamed = [ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True).clone() for _ in range(3)]
     torch.cuda.synchronize()
     # ---- verification (NCCL all_gather outside the measured calls) ----
     def gather_cat(t, dim=0):
@@ -83,6 +88,7 @@ def main():
     ref = oracle.combine_bf16(y_slots, gates[t0:t1])
     res["combine_bitwise_vs_oracle"] = bool(torch.equal(out.cpu().view(torch.int16), ref.view(torch.int16)))
     res["fused_scatter_bitwise_vs_unfused"] = bool(torch.equal(out_fused.view(torch.int16), out.view(torch.int16)))
+    res["streamed_bitwise_vs_unfused"] = all(bool(torch.equal(o.view(torch.int16), out.view(torch.int16))) for o in outs_streamed)
     # ---- timing of the exchanges alone ----
     xq, xs = keep["xq"], keep["xs"]
     remote_slots = int((plan.dst_rank != rank).sum())
@@ -108,8 +114,18 @@ def main():
     res["dispatch_total_GBps"] = (t1 - t0) * top_k * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9
     res["combine_ms"] = ms_c
     res["combine_remote_GBps"] = remote_rows * N * 2 / (ms_c * 1e-3) / 1e9
+    for c in (8, 32, 128):              # the streamed dispatch alone (no GEMM waiting on it), by CTA count
+        def ds():
+            ex.epoch += 1
+            fp.dispatch_fp8_stream(plan.chunk_off_dev, plan.send_tok_dev, plan.send_rank_dev, plan.send_row_dev, xq, xs,
+                                   ex.hq.buffer_ptrs_dev, ex.K, ex.hsb.buffer_ptrs_dev, ex.ld_sb, ex.local_done,
+                                   ex.hf.buffer_ptrs_dev, ex.world, ex.epoch, c)
+        res[f"dispatch_stream_ms_ctas{c}"] = timeit(ds, 10)
     res["layer_ms_unfused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=False), 10)
     res["layer_ms_fused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True), 10)
+    res["layer_ms_streamed"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True), 10)
+    res["streamed_after_timing_bitwise"] = bool(torch.equal(
+        ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True).view(torch.int16), out.view(torch.int16)))
     ex.barrier()
     torch.cuda.synchronize()
     allres = [None] * world

@@ -166,7 +166,17 @@ def test_grouped_gemm_scatter_validation():
     A16 = ctypes.c_void_p(1 << 20)
     ws = lib.fp8bs_grouped_gemm_workspace_size(4, 10, 256, 512)
     args = (4, 10, 256, 512, A16, A16, 512, A16, 16, A16, A16)
-    assert lib.fp8bs_grouped_gemm_scatter(*args, None, A16, A16, 256, A16, ws, None) == L.ERR_INVALID_ARG
-    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, None, A16, 256, A16, ws, None) == L.ERR_INVALID_ARG
-    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 200, A16, ws, None) == L.ERR_SHAPE       # ldd < N
-    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 256, A16, ws - 16, None) == L.ERR_INVALID_ARG
+    plain = (None, 0, 0, 0)   # ready, ready_target, ready_chunks, max_sms
+    assert lib.fp8bs_grouped_gemm_scatter(*args, None, A16, A16, 256, *plain, A16, ws, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, None, A16, 256, *plain, A16, ws, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 200, *plain, A16, ws, None) == L.ERR_SHAPE       # ldd < N
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 256, *plain, A16, ws - 16, None) == L.ERR_INVALID_ARG
+    # streamed operands: ready flags need chunks >= 1 and an SM cap (the dispatch they wait for needs SMs)
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 256, A16, 1, 0, 100, A16, ws, None) == L.ERR_INVALID_ARG
+    assert lib.fp8bs_grouped_gemm_scatter(*args, A16, A16, A16, 256, A16, 1, 4, 0, A16, ws, None) == L.ERR_INVALID_ARG
+    # fp8bs_dispatch_fp8_stream: host checks before any launch
+    d = (8, A16, A16, A16, A16, 7168, A16, 7168, A16, 16, A16, 7168, A16, 16, A16, A16)
+    assert lib.fp8bs_dispatch_fp8_stream(*d, 2, 1, 32, None) == L.ERR_DEVICE or torch.cuda.is_available()
+    assert lib.fp8bs_dispatch_fp8_stream(0, *d[1:], 2, 1, 32, None) == L.ERR_INVALID_ARG            # chunks
+    assert lib.fp8bs_dispatch_fp8_stream(*d, 2, 0, 32, None) == L.ERR_INVALID_ARG                    # epoch 0
+    assert lib.fp8bs_dispatch_fp8_stream(*d[:5], 7000, *d[6:], 2, 1, 32, None) == L.ERR_SHAPE        # K % 128

@@ -132,6 +132,40 @@ def test_exchange_plan_routes_every_slot_to_its_expert_row_and_back():
             assert all(bool((h == 1).all()) for h in hit)
 
 
+def test_exchange_plan_send_list_for_the_streamed_dispatch():
+    """The streamed dispatch's send list: a permutation of the rank's slots carrying the same (rank, row)
+    as dst_rank / dst_row, sorted by (chunk, rank, row), with chunk c = (receiver's local group) *
+    chunks // G_receiver and chunk_off delimiting the chunks."""
+    T, E, k = 600, 16, 4
+    routes = W.route_skewed(T, E, k, alpha=1.0, seed=3)
+    for world in (1, 2, 4):
+        for pl in _placements(E, world, routes):
+            for chunks in (1, 3, 8):
+                plans = [ep.exchange_plan(routes, E, world, r, pl, chunks=chunks) for r in range(world)]
+                for r, p in enumerate(plans):
+                    S = p.dst_rank.numel()
+                    assert p.send_tok.numel() == S and int(p.chunk_off[-1]) == S and int(p.chunk_off[0]) == 0
+                    assert torch.equal(torch.sort(p.send_tok * k).values // k, torch.sort(p.send_tok).values)
+                    slot = torch.zeros(S, dtype=torch.int64)
+                    for c in range(chunks):
+                        a, b = int(p.chunk_off[c]), int(p.chunk_off[c + 1])
+                        for j in range(a, b):
+                            o, row = int(p.send_rank[j]), int(p.send_row[j])
+                            q = plans[o]
+                            g = int(torch.searchsorted(q.offsets, torch.tensor(row), right=True)) - 1
+                            assert g * chunks // (q.offsets.numel() - 1) == c
+                        key = p.send_rank[a:b].long() * (T * k) + p.send_row[a:b]
+                        assert bool((key[1:] > key[:-1]).all())
+                    # same (token, dst) multiset as the slot table
+                    want = sorted(zip(p.dst_rank.tolist(), p.dst_row.tolist()))
+                    got = sorted(zip(p.send_rank.tolist(), p.send_row.tolist()))
+                    assert want == got
+                    for j in range(S):
+                        t = int(p.send_tok[j])
+                        assert any(int(p.dst_rank[t * k + i]) == int(p.send_rank[j]) and
+                                   int(p.dst_row[t * k + i]) == int(p.send_row[j]) for i in range(k))
+
+
 # ---------------------------------------------------------------- expert placement (P:584-589) ----
 def _check_partition(pl, offsets):
     """Every row of every expert is computed exactly once; copies of an expert sit on distinct ranks."""
