@@ -506,25 +506,28 @@ def time_moe_forward(args, world, rank, dev, pb):
     steps = min(args.steps, 10)
     stream = torch.cuda.current_stream()
 
-    def layer_ms(fused):
+    def layer_ms(**kw):
         for _ in range(args.warmup):
-            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=fused)
+            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, **kw)
         torch.cuda.synchronize()
         barrier(world)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(steps):
-            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=fused)
+            ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, **kw)
         b.record(stream)
         torch.cuda.synchronize()
         return max_over_ranks(a.elapsed_time(b) / steps, world, dev)
-    ms_unfused = layer_ms(False)
-    ms = layer_ms(True)
+    ms_unfused = layer_ms(fused=False)
+    ms_fused = layer_ms(fused=True, dedup=False)
+    ms = layer_ms(dedup=True)
     keep = {}
     ref_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, keep=keep, fused=False).clone()
-    fused_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=True)
+    fused_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, fused=True, dedup=False).clone()
+    dedup_out = ep.moe_forward(ex, plan, x_local, gates, k, pb.Bq, pb.sB, ws=ws, dedup=True)
     torch.cuda.synchronize()
-    fused_ok = gather_ints([int(torch.equal(fused_out.view(torch.int16), ref_out.view(torch.int16)))], world, dev)
+    fused_ok = gather_ints([int(torch.equal(fused_out.view(torch.int16), ref_out.view(torch.int16)) and
+                                torch.equal(dedup_out.view(torch.int16), ref_out.view(torch.int16)))], world, dev)
     xq, xs, y = keep["xq"], keep["xs"], keep["y"]
 
     def phase(fn, iters=10):
@@ -547,11 +550,13 @@ def time_moe_forward(args, world, rank, dev, pb):
     fl = sum(2.0 * r * N * K for r in rows)
     ex.barrier()
     torch.cuda.synchronize()
-    return {"what": "whole expert-layer FP8 forward per rank: quantize tokens -> NVLink FP8 dispatch -> grouped Fprop "
-                    "whose epilogue stores each BF16 row into its token owner's combine buffer (fused combine send) -> "
-                    "gate-weighted sum (ep.moe_forward; symmetric-memory barriers between)",
+    return {"what": "whole expert-layer FP8 forward per rank: quantize tokens -> NVLink FP8 dispatch, each (token, rank) "
+                    "pair once -> local expansion to expert rows -> grouped Fprop whose epilogue stores each BF16 row into "
+                    "its token owner's combine buffer (fused combine send) -> gate-weighted sum (ep.moe_forward(dedup=True); "
+                    "symmetric-memory barriers between)",
             "ms_per_step": ms, "steps": steps, "value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s (expert GEMM flop / step)",
-            "ms_per_step_unfused": ms_unfused, "fused_bitwise_equal_unfused_all_ranks": all(bool(v) for v in fused_ok),
+            "ms_per_step_unfused": ms_unfused, "ms_per_step_fused_per_slot_dispatch": ms_fused,
+            "fused_bitwise_equal_unfused_all_ranks": all(bool(v) for v in fused_ok),
             "dispatch_ms": ms_d, "dispatch_remote_GBps_per_rank": max(remote_d) * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9,
             "combine_ms": ms_c, "combine_remote_GBps_per_rank": max(remote_c) * N * 2 / (ms_c * 1e-3) / 1e9,
             "nvlink_reference_GBps_per_direction": 770}

@@ -332,6 +332,19 @@ FP8BS_API fp8bs_status fp8bs_dispatch_fp8_stream(int32_t chunks, const int64_t* 
                                        uint8_t* const* recv_q, int64_t ld_recv_q, float* const* recv_s, int64_t ld_recv_s,
                                        uint32_t* local_done, uint32_t* const* flags, int32_t world, uint32_t epoch,
                                        int32_t ctas, fp8bs_stream_t stream);
+/* send_rows / expand_rows: the token-once dispatch.  A token routed to several experts on one rank
+ * crosses the link once (top-8 over 4 ranks: ~3.6 distinct ranks per token, 45% of the per-slot rows).
+ * send_rows: entry i sends local token tok[i] (DEVICE int64 [n]) — its K codes of xq and K/128 scales
+ *   xs[kb * ldxs + token] — to rank dst_rank[i], row dst_row[i] of that rank's TOKEN buffer (codes at
+ *   recv_q[r] + row * ld_recv_q, scales row-major at recv_s[r] + row * (K/128)); dst_rank < 0: skipped.
+ * expand_rows (local): expert row i of A [R, lda] <- token-buffer row idx[i] (DEVICE int64 [R]) of
+ *   tq [*, ld_tq] (codes) and ts [*, K/128] (row-major scales), the scales written transposed into
+ *   the GEMM's layout sA[kb * ldsA + i] (ldsA >= R).  Both K % 128 == 0, 16-byte aligned code rows. */
+FP8BS_API fp8bs_status fp8bs_send_rows(int64_t n, const int64_t* tok, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
+                             int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
+                             int64_t ld_recv_q, float* const* recv_s, fp8bs_stream_t stream);
+FP8BS_API fp8bs_status fp8bs_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ld_tq, const float* ts,
+                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,
                                          fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_combine_push_bf16(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,

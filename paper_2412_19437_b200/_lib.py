@@ -152,6 +152,11 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_dispatch_fp8_stream.restype = st
         L.fp8bs_dispatch_fp8_stream.argtypes = [ctypes.c_int32, vp, vp, vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64,
                                                 vp, vp, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, vp]
+    if hasattr(L, "fp8bs_send_rows"):
+        L.fp8bs_send_rows.restype = st
+        L.fp8bs_send_rows.argtypes = [i64, vp, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
+        L.fp8bs_expand_rows.restype = st
+        L.fp8bs_expand_rows.argtypes = [i64, vp, i64, vp, i64, vp, vp, i64, vp, i64, vp]
     if hasattr(L, "fp8bs_dispatch_fp8"):
         L.fp8bs_dispatch_fp8.restype = st
         L.fp8bs_dispatch_fp8.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
@@ -481,6 +486,29 @@ def grouped_gemm_scatter(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tenso
                                             _p(sB), ctypes.c_void_p(dst_ptrs), _p(dst_rank), _p(dst_row), ldd,
                                             _p(ready), ready_target & 0xFFFFFFFF, ready_chunks, max_sms,
                                             _p(workspace), workspace.numel(), _stream(A)), "fp8bs_grouped_gemm_scatter")
+
+
+def send_rows(tok: torch.Tensor, xq: torch.Tensor, xs: torch.Tensor, dst_rank: torch.Tensor, dst_row: torch.Tensor,
+              recv_q_ptrs: int, ld_recv_q: int, recv_s_ptrs: int):
+    """fp8bs_send_rows: each (token, destination rank) pair once into the receivers' token buffers."""
+    _cuda2d(xq, "xq")
+    _check(lib().fp8bs_send_rows(tok.numel(), _p(tok), xq.shape[1], _p(xq), xq.stride(0), _p(xs), xs.stride(0),
+                                 _p(dst_rank), _p(dst_row), ctypes.c_void_p(recv_q_ptrs), ld_recv_q,
+                                 ctypes.c_void_p(recv_s_ptrs), _stream(xq)), "fp8bs_send_rows")
+
+
+def expand_rows(idx: torch.Tensor, tq: torch.Tensor, ts: torch.Tensor, A: torch.Tensor | None = None,
+                sA: torch.Tensor | None = None):
+    """fp8bs_expand_rows: expert rows A [R, K] and sA [K/128, R] from the token buffer (tq, row-major ts)."""
+    _cuda2d(tq, "tq")
+    R, K = idx.numel(), tq.shape[1]
+    if A is None:
+        A = torch.empty(R, K, dtype=torch.uint8, device=tq.device)
+    if sA is None:
+        sA = torch.empty(K // 128, _pad4(R), dtype=torch.float32, device=tq.device)[:, :R]
+    _check(lib().fp8bs_expand_rows(R, _p(idx), K, _p(tq), tq.stride(0), _p(ts), _p(A), A.stride(0), _p(sA), sA.stride(0),
+                                   _stream(tq)), "fp8bs_expand_rows")
+    return A, sA
 
 
 def dispatch_fp8_stream(chunk_off: torch.Tensor, send_tok: torch.Tensor, send_rank: torch.Tensor, send_row: torch.Tensor,

@@ -148,6 +148,60 @@ __global__ void __launch_bounds__(32 * kDsWarps) k_dispatch_stream(int C, const 
     }
 }
 
+// Token-once dispatch: send entry i = local token tok[i] -> rank dst_rank[i], token-buffer row dst_row[i]
+// (codes + row-major scales, as k_dispatch_fp8); each (token, destination rank) pair is sent once.
+__global__ void __launch_bounds__(256) k_send_rows(int64_t n, const int64_t* __restrict__ tok, int64_t K, int64_t KB,
+                                                   const uint8_t* __restrict__ xq, int64_t ldxq,
+                                                   const float* __restrict__ xs, int64_t ldxs,
+                                                   const int32_t* __restrict__ dst_rank, const int64_t* __restrict__ dst_row,
+                                                   uint8_t* const* __restrict__ recv_q, int64_t ld_rq,
+                                                   float* const* __restrict__ recv_s) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += nw) {
+        const int r = dst_rank[i];
+        if (r < 0) continue;
+        const int64_t row = dst_row[i], t = tok[i];
+        const uint8_t* src = xq + t * ldxq;
+        uint8_t* dst = recv_q[r] + row * ld_rq;
+        for (int64_t c = (int64_t)lane * 16; c < K; c += 512)
+            *reinterpret_cast<uint4*>(dst + c) = ldg_nc_v4(src + c);
+        float* ds = recv_s[r] + row * KB;
+        for (int64_t kb = lane; kb < KB; kb += 32) ds[kb] = xs[kb * ldxs + t];
+    }
+}
+
+// Receiver side of the token-once dispatch: expert row i <- token-buffer row idx[i]: the codes (a warp per
+// row, 16-byte vectors) and the scales, transposed into the GEMM's [KB][ldsA] layout (lane = row of a
+// batch of 32 consecutive rows: 128-byte stores per contraction block).
+__global__ void __launch_bounds__(256) k_expand_rows(int64_t R, const int64_t* __restrict__ idx, int64_t K, int64_t KB,
+                                                     const uint8_t* __restrict__ tq, int64_t ldtq,
+                                                     const float* __restrict__ ts, uint8_t* __restrict__ A, int64_t lda,
+                                                     float* __restrict__ sA, int64_t ldsA) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (R + 31) / 32, nw = (int64_t)gridDim.x * 8;
+    for (int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); b < nb; b += nw) {
+        const int64_t i0 = b * 32;
+        const int n = (int)min((int64_t)32, R - i0);
+        const int64_t my = lane < n ? idx[i0 + lane] : 0;
+        for (int j = 0; j < n; ++j) {
+            const int64_t src_row = __shfl_sync(0xffffffffu, my, j);
+            const uint8_t* src = tq + src_row * ldtq;
+            uint8_t* dst = A + (i0 + j) * lda;
+            for (int64_t c = (int64_t)lane * 16; c < K; c += 512)
+                *reinterpret_cast<uint4*>(dst + c) = ldg_nc_v4(src + c);
+        }
+        if (lane < n) {
+            const float* s = ts + my * KB;
+            for (int64_t kb = 0; kb < KB; ++kb) sA[kb * ldsA + i0 + lane] = s[kb];
+        }
+    }
+}
+
 // Row-major [R][KB] scales -> the GEMM's contraction-block-major [KB][ldd] layout (32 x 32 tiles through
 // shared memory: both sides coalesced).
 __global__ void __launch_bounds__(256) k_rows_to_blocks(int64_t R, int64_t KB, const float* __restrict__ src,
@@ -250,6 +304,17 @@ cudaError_t launch_dispatch_stream(int C, const int64_t* chunk_off, const int64_
                                                          xs, ldxs, recv_q, ld_rq, recv_s, ld_rs, local_done, flags, world,
                                                          epoch);
     return cudaPeekAtLastError();
+}
+cudaError_t launch_send_rows(int64_t n, const int64_t* tok, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
+                             int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
+                             int64_t ld_rq, float* const* recv_s, cudaStream_t st) {
+    return launch_pdl(k_send_rows, dim3(rows_grid(n)), dim3(256), 0, st, n, tok, K, K / 128, xq, ldxq, xs, ldxs, dst_rank,
+                      dst_row, recv_q, ld_rq, recv_s);
+}
+cudaError_t launch_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ldtq, const float* ts,
+                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, cudaStream_t st) {
+    return launch_pdl(k_expand_rows, dim3(rows_grid((R + 31) / 32)), dim3(256), 0, st, R, idx, K, K / 128, tq, ldtq, ts, A,
+                      lda, sA, ldsA);
 }
 cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st) {
     return launch_pdl(k_rows_to_blocks, dim3((unsigned)((R + 31) / 32), (unsigned)((KB + 31) / 32)), dim3(256), 0, st,

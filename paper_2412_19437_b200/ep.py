@@ -369,6 +369,14 @@ class ExchangePlan:
     send_rank: torch.Tensor | None = None   # int32 [S]
     send_row: torch.Tensor | None = None    # int64 [S]
     chunk_off: torch.Tensor | None = None   # int64 [chunks + 1]: entries of chunk c are [chunk_off[c], chunk_off[c+1])
+    # token-once dispatch (fp8bs_send_rows + fp8bs_expand_rows): each (token, destination rank) pair is sent
+    # once, into the receiver's token buffer (rows grouped by source rank, tokens in order); the receiver
+    # expands them into its expert-grouped rows
+    u_tok: torch.Tensor | None = None       # int64 [U]: local token (t - t0) of send entry j
+    u_rank: torch.Tensor | None = None      # int32 [U]: destination rank
+    u_row: torch.Tensor | None = None       # int64 [U]: row in the destination's token buffer
+    x_idx: torch.Tensor | None = None       # int64 [R_local]: token-buffer row of each of this rank's expert rows
+    tok_rows: int = 0                       # rows of this rank's token buffer
 
 
 def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
@@ -416,9 +424,25 @@ def exchange_plan(routes: torch.Tensor, E: int, world: int, rank: int,
     order_s = torch.argsort(key, stable=True)
     chunk_off = torch.zeros(chunks + 1, dtype=torch.int64)
     chunk_off[1:] = torch.cumsum(torch.bincount(d_chunk, minlength=chunks), 0)
+    # token-once dispatch: the distinct (token, destination rank) pairs, sorted by token; a receiver's
+    # token-buffer row of a pair is its index among the pairs with that receiver (source ranks own
+    # contiguous token ranges, so the rows come grouped by source rank)
+    slot_rank = owner_of_row[pos]                                     # [T * k] destination rank of every slot
+    pair = torch.unique(flat_t * world + slot_rank)                   # sorted: by token, then rank
+    p_tok, p_rank = pair // world, pair % world
+    p_row = torch.empty_like(pair)
+    for o in range(world):
+        m = p_rank == o
+        p_row[m] = torch.arange(int(m.sum()), dtype=torch.int64)
+    mine_p = (p_tok >= t0) & (p_tok < t1)
+    recv_p = p_rank == rank
+    tb_row = torch.full((T,), -1, dtype=torch.int64)                  # token -> its row in MY token buffer
+    tb_row[p_tok[recv_p]] = p_row[recv_p]
+    x_idx = tb_row[tok]
     return ExchangePlan(t0, t1, [int(e) for e in exps], rows_me, d_rank.to(torch.int32), d_row,
                         loff, tok_owner.to(torch.int32), c_slot, int(rows_me.numel()), chunks,
-                        order_s // k, d_rank[order_s].to(torch.int32), d_row[order_s], chunk_off)
+                        order_s // k, d_rank[order_s].to(torch.int32), d_row[order_s], chunk_off,
+                        p_tok[mine_p] - t0, p_rank[mine_p].to(torch.int32), p_row[mine_p], x_idx, int(recv_p.sum()))
 
 
 class Exchange:
@@ -440,6 +464,9 @@ class Exchange:
         self.recv_sb = symm_mem.empty(K // 128, self.ld_sb, dtype=torch.float32, device=device)
         self.recv_y = symm_mem.empty(max_slots, N, dtype=torch.bfloat16, device=device)
         self.recv_y2 = symm_mem.empty(max_slots, N, dtype=torch.bfloat16, device=device)
+        # token-once dispatch: token buffers (a token's row arrives once per rank; rows <= expert rows)
+        self.tok_q = symm_mem.empty(max_rows, K, dtype=torch.uint8, device=device)
+        self.tok_s = symm_mem.empty(max_rows, K // 128, dtype=torch.float32, device=device)
         self.flags = symm_mem.empty(chunks, dtype=torch.int32, device=device)
         self.flags.zero_()
         self.hq = symm_mem.rendezvous(self.recv_q, group)
@@ -448,6 +475,8 @@ class Exchange:
         self.hy = symm_mem.rendezvous(self.recv_y, group)
         self.hy2 = symm_mem.rendezvous(self.recv_y2, group)
         self.hf = symm_mem.rendezvous(self.flags, group)
+        self.htq = symm_mem.rendezvous(self.tok_q, group)
+        self.hts = symm_mem.rendezvous(self.tok_s, group)
         self.local_done = torch.zeros(chunks, dtype=torch.int32, device=device)
         self.epoch = 0
         self.dstream = torch.cuda.Stream(device=device)
@@ -462,7 +491,7 @@ class Exchange:
 
 def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: torch.Tensor, top_k: int,
                 Bq: torch.Tensor, sB: torch.Tensor, ws: torch.Tensor | None = None, keep: dict | None = None,
-                fused: bool = True, streamed: bool = False):
+                fused: bool = True, streamed: bool = False, dedup: bool = True):
     """The expert layer's FP8 forward on this rank: 1x128 quantization of its tokens ->
     FP8 dispatch over NVLink -> grouped Fprop over the received rows -> BF16 combine over NVLink ->
     gate-weighted sum.  fused (default): the grouped Fprop's epilogue stores each BF16 output row
@@ -471,8 +500,11 @@ def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: 
     fp8bs_combine_push_bf16.  streamed (implies fused): the dispatch runs on its own stream and SMs
     (fp8bs_dispatch_fp8_stream, chunk by chunk in the receivers' expert order, scales straight into the
     GEMM's layout) while the GEMM, on the remaining SMs, waits per chunk on the ready flags the senders
-    publish: no barrier and no scale re-layout between dispatch and GEMM.  keep (optional dict)
-    receives the intermediate tensors for verification."""
+    publish: no barrier and no scale re-layout between dispatch and GEMM.  dedup (default; with fused,
+    not streamed): each (token, destination rank) pair crosses the link once (fp8bs_send_rows into the
+    receivers' token buffers), and each receiver expands its expert rows locally (fp8bs_expand_rows, the
+    scales straight into the GEMM layout).  keep (optional dict) receives the intermediate tensors for
+    verification."""
     import paper_2412_19437_b200 as fp
     xq, xs = fp.quantize_act_1x128(x_local)
     R = plan.rows
@@ -497,6 +529,15 @@ def moe_forward(ex: Exchange, plan: ExchangePlan, x_local: torch.Tensor, gates: 
         main.wait_stream(ex.dstream)
         xq.record_stream(ex.dstream)
         xs.record_stream(ex.dstream)
+    elif dedup and fused:
+        fp.send_rows(plan.u_tok_dev, xq, xs, plan.u_rank_dev, plan.u_row_dev, ex.htq.buffer_ptrs_dev, ex.K,
+                     ex.hts.buffer_ptrs_dev)
+        ex.barrier()
+        A, sA = ex.recv_q[:R], ex.recv_sb[:, :R]
+        if R > 0:
+            fp.expand_rows(plan.x_idx_dev, ex.tok_q[:plan.tok_rows], ex.tok_s[:plan.tok_rows], A=A, sA=sA)
+            fp.grouped_gemm_scatter(plan.offsets_dev, A, sA, Bq, sB, ex.hy.buffer_ptrs_dev, plan.c_rank_dev,
+                                    plan.c_slot_dev, ex.N, workspace=ws)
     else:
         fp.dispatch_fp8(xq, xs, top_k, plan.dst_rank_dev, plan.dst_row_dev, ex.hq.buffer_ptrs_dev, ex.K, ex.hs.buffer_ptrs_dev)
         ex.barrier()
@@ -526,4 +567,8 @@ def plan_to_device(plan: ExchangePlan, device) -> ExchangePlan:
     plan.send_rank_dev = plan.send_rank.to(device)
     plan.send_row_dev = plan.send_row.to(device)
     plan.chunk_off_dev = plan.chunk_off.to(device)
+    plan.u_tok_dev = plan.u_tok.to(device)
+    plan.u_rank_dev = plan.u_rank.to(device)
+    plan.u_row_dev = plan.u_row.to(device)
+    plan.x_idx_dev = plan.x_idx.to(device)
     return plan

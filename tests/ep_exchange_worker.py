@@ -54,11 +54,12 @@ def main():
     torch.cuda.synchronize()
     out = out.clone()
     # the fused form (combine's send in the grouped GEMM's epilogue) must give the same bits
-    out_fused = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True).clone()
+    out_fused = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True, dedup=False).clone()
     torch.cuda.synchronize()
     # the streamed form (dispatch overlapped with the GEMM through per-chunk ready flags), twice: the
     # second call exercises the monotonic counters and the other combine buffer
     outs_streamed = [ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True).clone() for _ in range(3)]
+    out_dedup = ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, dedup=True).clone()
     torch.cuda.synchronize()
     # ---- verification (NCCL all_gather outside the measured calls) ----
     def gather_cat(t, dim=0):
@@ -88,6 +89,7 @@ def main():
     ref = oracle.combine_bf16(y_slots, gates[t0:t1])
     res["combine_bitwise_vs_oracle"] = bool(torch.equal(out.cpu().view(torch.int16), ref.view(torch.int16)))
     res["fused_scatter_bitwise_vs_unfused"] = bool(torch.equal(out_fused.view(torch.int16), out.view(torch.int16)))
+    res["dedup_bitwise_vs_unfused"] = bool(torch.equal(out_dedup.view(torch.int16), out.view(torch.int16)))
     res["streamed_bitwise_vs_unfused"] = all(bool(torch.equal(o.view(torch.int16), out.view(torch.int16))) for o in outs_streamed)
     # ---- timing of the exchanges alone ----
     xq, xs = keep["xq"], keep["xs"]
@@ -114,7 +116,7 @@ def main():
     res["dispatch_total_GBps"] = (t1 - t0) * top_k * (K + 4 * (K // 128)) / (ms_d * 1e-3) / 1e9
     res["combine_ms"] = ms_c
     res["combine_remote_GBps"] = remote_rows * N * 2 / (ms_c * 1e-3) / 1e9
-    for c in (8, 32, 128):              # the streamed dispatch alone (no GEMM waiting on it), by CTA count
+    for c in (32,):                     # the streamed dispatch alone (no GEMM waiting on it)
         def ds():
             ex.epoch += 1
             fp.dispatch_fp8_stream(plan.chunk_off_dev, plan.send_tok_dev, plan.send_rank_dev, plan.send_row_dev, xq, xs,
@@ -122,7 +124,10 @@ def main():
                                    ex.hf.buffer_ptrs_dev, ex.world, ex.epoch, c)
         res[f"dispatch_stream_ms_ctas{c}"] = timeit(ds, 10)
     res["layer_ms_unfused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=False), 10)
-    res["layer_ms_fused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True), 10)
+    res["layer_ms_fused"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, fused=True, dedup=False), 10)
+    res["layer_ms_dedup"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, dedup=True), 10)
+    res["send_rows_ms"] = timeit(lambda: fp.send_rows(plan.u_tok_dev, xq, xs, plan.u_rank_dev, plan.u_row_dev,
+                                                      ex.htq.buffer_ptrs_dev, K, ex.hts.buffer_ptrs_dev))
     res["layer_ms_streamed"] = timeit(lambda: ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True), 10)
     res["streamed_after_timing_bitwise"] = bool(torch.equal(
         ep.moe_forward(ex, plan, x_local, gl, top_k, Bq, sBl, ws=ws, streamed=True).view(torch.int16), out.view(torch.int16)))

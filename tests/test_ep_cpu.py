@@ -289,3 +289,33 @@ def test_observed_load_is_an_independent_draw_of_the_same_distribution():
     prev = ep.observed_load(cfg).double()
     assert not torch.equal(cur, prev)
     assert float(torch.corrcoef(torch.stack([cur, prev]))[0, 1]) > 0.9
+
+
+def test_exchange_plan_token_once_dispatch():
+    """Token-once dispatch bookkeeping: every (token, destination rank) pair appears exactly once across
+    the senders' lists, the receiver's token-buffer rows are 0..tok_rows-1 exactly once, and expanding
+    the token buffer with x_idx reproduces, for every expert row, the token the per-slot plan gives it."""
+    T, E, k = 600, 16, 4
+    routes = W.route_skewed(T, E, k, alpha=1.0, seed=3)
+    tok, off = W.group_rows(routes, E)
+    for world in (1, 2, 4):
+        for pl in _placements(E, world, routes):
+            plans = [ep.exchange_plan(routes, E, world, r, pl) for r in range(world)]
+            # token buffer of each receiver: which global token each row holds
+            held = [torch.full((p.tok_rows,), -1, dtype=torch.int64) for p in plans]
+            seen = set()
+            for r, p in enumerate(plans):
+                for j in range(p.u_tok.numel()):
+                    t, o, row = int(p.u_tok[j]) + p.t0, int(p.u_rank[j]), int(p.u_row[j])
+                    assert (t, o) not in seen
+                    seen.add((t, o))
+                    assert held[o][row] == -1
+                    held[o][row] = t
+            for o, p in enumerate(plans):
+                assert bool((held[o] >= 0).all())
+                assert torch.equal(held[o][p.x_idx], tok[p.grows])       # expanded rows = the rows' tokens
+            # pairs = distinct (token, rank of one of its expert rows)
+            want = set()
+            for o, p in enumerate(plans):
+                want |= {(int(t), o) for t in tok[p.grows]}
+            assert seen == want

@@ -24,5 +24,6 @@ def test_ep_exchange_two_gpus(shape):
     res = json.loads(p.stdout.strip().splitlines()[-1])
     for r in res["ranks"]:
         for key in ("dispatch_codes_bitwise", "dispatch_scales_bitwise", "expert_gemm_bitwise", "combine_bitwise_vs_oracle",
-                    "fused_scatter_bitwise_vs_unfused", "streamed_bitwise_vs_unfused", "streamed_after_timing_bitwise"):
+                    "fused_scatter_bitwise_vs_unfused", "streamed_bitwise_vs_unfused", "streamed_after_timing_bitwise",
+                    "dedup_bitwise_vs_unfused"):
             assert r[key], (key, r)
