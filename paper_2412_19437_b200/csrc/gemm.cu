@@ -1110,9 +1110,10 @@ static unsigned long long* g_ts = nullptr;   // debug timestamps (FP8BS_GEMM_DEB
 // Split-K tail plan of a dense launch (get_tile_split): tiles [t0, t0 + units / S) of the raster, each
 // cut into S chunks along K.  Used when the last wave would fill at most half of the clusters: S =
 // clusters / tail tiles (so the units fill one wave), and only when it saves at least kSplitMinSaved
-// K-blocks of the tail tile's time (the partial slabs and the reduce launch cost a few microseconds).
+// K-blocks of the tail tile's time: the second launch and the reduce cost ~20 us, about 40 K-blocks of a
+// wave (measured: C1 Dgrad saves 136 and gains 10%; C1 Wgrad would save 24 and lost 4 us net).
 struct SplitPlan { int t0 = 0, S = 0, units = 0; };
-constexpr int kSplitMinKB = 4, kSplitMinSaved = 16;
+constexpr int kSplitMinKB = 4, kSplitMinSaved = 40;
 
 static SplitPlan split_plan(int64_t M, int64_t N, int64_t K, int rows, int clusters) {
     SplitPlan sp;

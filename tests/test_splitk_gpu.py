@@ -23,7 +23,7 @@ DEV = "cuda"
 
 # (M, N, K): a few tiles (no full wave); 78 pair / 156 single-CTA tiles = one wave + a small tail;
 # a ragged WGRAD-like shape.  Every one has a split-K tail on a 148-SM B200 (asserted below).
-SHAPES = [(300, 512, 8192), (3300, 1400, 4096), (1000, 776, 8192)]
+SHAPES = [(300, 512, 8192), (3300, 1400, 8192), (1000, 776, 8192)]
 
 
 @pytest.fixture(params=[1, 2], ids=["cta1", "pair"])
@@ -135,7 +135,7 @@ def test_split_workspace_too_small_is_rejected():
 
 def test_split_graph_capture():
     """The three launches (full waves, tail units, reduce) capture into a CUDA graph and replay."""
-    M, N, K = 3300, 1400, 4096
+    M, N, K = 3300, 1400, 8192
     qa, sa, qb, sb = operands(fp.DGRAD, M, N, K, seed=2)
     args = (fp.DGRAD, dev(qa), dev(sa), dev(qb), dev(sb))
     ref = fp.gemm(*args, out_dtype=torch.float32)

@@ -24,7 +24,8 @@ timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k re
 timeout -s KILL 600 $C1 > $OUT/plain_c1_$TAG.log 2>&1 && \
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
     --log-file $OUT/launches_c1_$TAG.csv $C1 > $OUT/ncu_launches_c1_$TAG.log 2>&1; echo "ncu c1 launches rc=$?"
-timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_gemm_bs -s 9 -c 3 \
+# per C1 step: fprop, dgrad (full waves), dgrad (split-K tail), split-K reduce, wgrad; skip the 3 warm-up steps
+timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:'k_gemm_bs|k_splitk' -s 15 -c 5 \
     -o $OUT/prof_gemm_$TAG $C1 > $OUT/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
 timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_quant -s 9 -c 3 \
     -o $OUT/prof_quant_$TAG $C1 > $OUT/ncu_quant_$TAG.log 2>&1; echo "ncu quant rc=$?"

@@ -19,7 +19,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-C1 = ["quant_act_dual(X)", "quant_weight_128x128(W)+T", "gemm_fprop", "quant_act_dual(dY)", "gemm_dgrad", "gemm_wgrad"]
+C1 = ["quant_act_dual(X)", "quant_weight_128x128(W)+T", "gemm_fprop", "quant_act_dual(dY)", "gemm_dgrad",
+      "gemm_dgrad (split-K tail)", "gemm_dgrad (split-K reduce)", "gemm_wgrad"]
+C1_GEMMS = ["gemm_fprop", "gemm_dgrad", "gemm_dgrad (split-K tail)", "gemm_dgrad (split-K reduce)", "gemm_wgrad"]
 C4 = ["quant_act_1x128(X shard)", "k_grouped_schedule", "grouped_gemm_fprop"]
 METRICS = [
     ("gpu__time_duration.sum", "time (us)", "us"),
@@ -102,7 +104,8 @@ def sass_histogram():
         m = re.search(r"k_gemm_bsILb(\d)ELi(\d)ELb(\d)ELb(\d)E", f)
         if m:
             w, o, g, pr = m.groups()
-            return (f"k_gemm_bs<{'wgrad' if w == '1' else 'fprop/dgrad'}, {['bf16', 'fp32', 'swiglu-fp8'][int(o)]} out, "
+            return (f"k_gemm_bs<{'wgrad' if w == '1' else 'fprop/dgrad'}, "
+                    f"{['bf16', 'fp32', 'swiglu-fp8', 'split-K fp32 partial', 'scatter bf16'][int(o)]} out, "
                     f"{'grouped' if g == '1' else 'dense'}, {'cta pair' if pr == '1' else '1 cta'}>")
         m = re.search(r"k_gemm_mxILb(\d)ELb(\d)ELb(\d)E", f)
         if m:
@@ -139,10 +142,10 @@ def main():
         md += ["", f"## ncu launch list, {name.upper()}: the last step (gpu__time_duration, --clock-control none)", "",
                "| launch | kernel | ncu us (cold, serialised) | share (ncu) | share (bench CUDA events) |", "|---|---|---|---|---|"]
         for n, (k, t) in zip(steps, last):
-            share = f"{100 * ev[n] / ev_tot:.1f}%" if n in ev and ev_tot else "(inside the GEMM's launch)"
+            share = f"{100 * ev[n] / ev_tot:.1f}%" if n in ev and ev_tot else "(inside the GEMM call's events)"
             md.append(f"| {n} | `{k[:70]}` | {t:.1f} | {100 * t / tot:.1f}% | {share} |")
     for rep, names, title in ((f"prof_grouped_{tag}.ncu-rep", ["grouped_gemm_fprop"], "C4 grouped GEMM, `ncu --set full` (one launch)"),
-                              (f"prof_gemm_{tag}.ncu-rep", ["gemm_fprop", "gemm_dgrad", "gemm_wgrad"], "C1 GEMMs, `ncu --set full`"),
+                              (f"prof_gemm_{tag}.ncu-rep", C1_GEMMS, "C1 GEMMs, `ncu --set full`"),
                               (f"prof_quant_{tag}.ncu-rep", ["quant_act_dual(X)", "quant_weight_128x128(W)+T", "quant_act_dual(dY)"],
                                "C1 quantizers, `ncu --set full`")):
         path = os.path.join(OUT, rep)
