@@ -452,31 +452,59 @@ def time_c4(args, world, rank, dev):
 
 
 def time_c4_e2e(args, world, pb, dev, rows, N, K):
-    """The C4 step through the public API with host buffers: every step uploads the rank's BF16 token
-    shard and its FP8 expert rows + scales from pinned host memory, runs the 2 launches, and downloads
-    the BF16 expert outputs (the expert weights stay resident, as model parameters do)."""
+    """The C4 step through the public API with host buffers, as a user holding BF16 tokens and the router's
+    output runs it: every step uploads, from pinned host memory, the BF16 rows of the distinct tokens this
+    rank's expert rows use and the row -> token index, then runs 1x128 quantization of those tokens ->
+    fp8bs_expand_rows (gather into expert-grouped FP8 rows, scales into the GEMM layout) -> the grouped
+    Fprop, and downloads the BF16 expert outputs.  The expert weights stay resident, as model parameters
+    do.  The output is checked bitwise against the device-timed step's (1x128 scales are per row, so
+    quantizing the gathered tokens gives the same codes)."""
+    import paper_2412_19437_b200 as fp
     from paper_2412_19437_b200 import ep
+    cfg = ep.EPConfig()
     n = max(3, min(8, args.steps // 4))
-    h_in = [pb.x.cpu().pin_memory(), pb.A.cpu().pin_memory(), pb.sA.cpu().pin_memory()]
-    h_out = [[torch.empty(pb.out.shape, dtype=pb.out.dtype).pin_memory()] for _ in range(2)]
-    d0 = ([pb.x, pb.A, pb.sA], [pb.out])
-    sA1 = torch.empty(pb.sA.shape[0], (pb.sA.shape[1] + 3) // 4 * 4 if pb.sA.shape[1] else 4, dtype=torch.float32,
-                      device=dev)[:, :pb.sA.shape[1]]
-    d1 = ([torch.empty_like(pb.x), torch.empty_like(pb.A), sA1], [torch.empty_like(pb.out)])
-    sets = [d0, d1]
-    saved = (pb.x, pb.A, pb.sA, pb.out)
+    uniq, inv = torch.unique(pb.tok, return_inverse=True)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 100)                      # the token batch of build_rank_problem
+    x = torch.randn(cfg.tokens, K, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    h_x = x.index_select(0, uniq.to(dev)).cpu().pin_memory()
+    del x
+    h_idx = inv.to(torch.int64).contiguous().pin_memory()
+    U, R, KB = uniq.numel(), pb.A.shape[0], K // 128
+    p4 = lambda m: (m + 3) // 4 * 4  # noqa: E731
+
+    def dset():
+        ins = [torch.empty(U, K, dtype=torch.bfloat16, device=dev), torch.empty(R, dtype=torch.int64, device=dev)]
+        scratch = (torch.empty(U, K, dtype=torch.uint8, device=dev),
+                   torch.empty(KB, p4(U), dtype=torch.float32, device=dev)[:, :U],
+                   torch.empty(R, K, dtype=torch.uint8, device=dev),
+                   torch.empty(KB, p4(R), dtype=torch.float32, device=dev)[:, :R])
+        return ins, [torch.empty(R, N, dtype=torch.bfloat16, device=dev)], scratch
+    d = [dset(), dset()]
+    sets = [(d[0][0], d[0][1]), (d[1][0], d[1][1])]
+    h_out = [[torch.empty(R, N, dtype=torch.bfloat16).pin_memory()] for _ in range(2)]
 
     def compute(b):
-        (pb.x, pb.A, pb.sA), (pb.out,) = sets[b]
-        ep.quantize_tokens(pb)
-        ep.run_rank(pb)
+        (xb, idxb), (outb,), (xq, xs, A, sA) = d[b]
+        if R == 0:
+            return
+        fp.quantize_act_1x128(xb, xq, xs)
+        fp.expand_rows(idxb, xq, xs, A=A, sA=sA, ts_layout="blocks")
+        fp.grouped_gemm(pb.offsets, A, sA, pb.Bq, pb.sB, out=outb, workspace=pb.ws)
 
-    ms = pipelined_e2e(n, 2, world, dev, h_in, sets, h_out, compute)
-    pb.x, pb.A, pb.sA, pb.out = saved
+    ms = pipelined_e2e(n, 2, world, dev, [h_x, h_idx], sets, h_out, compute)
+    ep.run_rank(pb)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(h_out[(n - 1) % 2][0].view(torch.int16), pb.out.cpu().view(torch.int16)))
+    del d, sets
+    torch.cuda.empty_cache()
     total = sum(2.0 * r * N * K for r in rows)
-    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    h2d = h_x.numel() * 2 + h_idx.numel() * 8
     return {"value": total * n / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "steps": n, "ms_per_step": ms / n,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": pb.out.numel() * 2,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": R * N * 2,
+            "inputs": f"BF16 rows of the {U} distinct tokens this rank's expert rows use + the row -> token index",
+            "step": "1x128 quantize -> fp8bs_expand_rows (gather) -> grouped Fprop; BF16 expert outputs downloaded",
+            "bitwise_equal_device_step": same,
             "pipelined": "2 device buffer sets; H2D, compute and D2H streams overlap across steps (PCIe-bound)"}
 
 

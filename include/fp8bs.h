@@ -338,13 +338,16 @@ FP8BS_API fp8bs_status fp8bs_dispatch_fp8_stream(int32_t chunks, const int64_t* 
  *   xs[kb * ldxs + token] — to rank dst_rank[i], row dst_row[i] of that rank's TOKEN buffer (codes at
  *   recv_q[r] + row * ld_recv_q, scales row-major at recv_s[r] + row * (K/128)); dst_rank < 0: skipped.
  * expand_rows (local): expert row i of A [R, lda] <- token-buffer row idx[i] (DEVICE int64 [R]) of
- *   tq [*, ld_tq] (codes) and ts [*, K/128] (row-major scales), the scales written transposed into
- *   the GEMM's layout sA[kb * ldsA + i] (ldsA >= R).  Both K % 128 == 0, 16-byte aligned code rows. */
+ *   tq [*, ld_tq] (codes) and the scales of that token at ts[t * ts_row_stride + kb * ts_kb_stride]
+ *   (row-major token buffer: (K/128, 1); the 1x128 quantizer's own [K/128][lds] layout: (1, lds)),
+ *   written transposed into the GEMM's layout sA[kb * ldsA + i] (ldsA >= R).  Both K % 128 == 0,
+ *   16-byte aligned code rows. */
 FP8BS_API fp8bs_status fp8bs_send_rows(int64_t n, const int64_t* tok, int64_t K, const uint8_t* xq, int64_t ldxq, const float* xs,
                              int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
                              int64_t ld_recv_q, float* const* recv_s, fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ld_tq, const float* ts,
-                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, fp8bs_stream_t stream);
+                               int64_t ts_row_stride, int64_t ts_kb_stride, uint8_t* A, int64_t lda, float* sA, int64_t ldsA,
+                               fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,
                                          fp8bs_stream_t stream);
 FP8BS_API fp8bs_status fp8bs_combine_push_bf16(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,

@@ -156,7 +156,7 @@ def _load(path: str) -> ctypes.CDLL:
         L.fp8bs_send_rows.restype = st
         L.fp8bs_send_rows.argtypes = [i64, vp, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
         L.fp8bs_expand_rows.restype = st
-        L.fp8bs_expand_rows.argtypes = [i64, vp, i64, vp, i64, vp, vp, i64, vp, i64, vp]
+        L.fp8bs_expand_rows.argtypes = [i64, vp, i64, vp, i64, vp, i64, i64, vp, i64, vp, i64, vp]
     if hasattr(L, "fp8bs_dispatch_fp8"):
         L.fp8bs_dispatch_fp8.restype = st
         L.fp8bs_dispatch_fp8.argtypes = [i64, ctypes.c_int32, i64, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]
@@ -498,16 +498,18 @@ def send_rows(tok: torch.Tensor, xq: torch.Tensor, xs: torch.Tensor, dst_rank: t
 
 
 def expand_rows(idx: torch.Tensor, tq: torch.Tensor, ts: torch.Tensor, A: torch.Tensor | None = None,
-                sA: torch.Tensor | None = None):
-    """fp8bs_expand_rows: expert rows A [R, K] and sA [K/128, R] from the token buffer (tq, row-major ts)."""
+                sA: torch.Tensor | None = None, ts_layout: str = "rows"):
+    """fp8bs_expand_rows: expert rows A [R, K] and sA [K/128, R] from the token codes tq and scales ts —
+    ts_layout "rows": a row-major token buffer [tokens, K/128]; "blocks": the 1x128 quantizer's [K/128, lds]."""
     _cuda2d(tq, "tq")
     R, K = idx.numel(), tq.shape[1]
     if A is None:
         A = torch.empty(R, K, dtype=torch.uint8, device=tq.device)
     if sA is None:
         sA = torch.empty(K // 128, _pad4(R), dtype=torch.float32, device=tq.device)[:, :R]
-    _check(lib().fp8bs_expand_rows(R, _p(idx), K, _p(tq), tq.stride(0), _p(ts), _p(A), A.stride(0), _p(sA), sA.stride(0),
-                                   _stream(tq)), "fp8bs_expand_rows")
+    rs, ks = (ts.stride(0), ts.stride(1)) if ts_layout == "rows" else (ts.stride(1), ts.stride(0))
+    _check(lib().fp8bs_expand_rows(R, _p(idx), K, _p(tq), tq.stride(0), _p(ts), rs, ks, _p(A), A.stride(0), _p(sA),
+                                   sA.stride(0), _stream(tq)), "fp8bs_expand_rows")
     return A, sA
 
 

@@ -454,17 +454,20 @@ fp8bs_status fp8bs_send_rows(int64_t n, const int64_t* tok, int64_t K, const uin
 }
 
 fp8bs_status fp8bs_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ld_tq, const float* ts,
-                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, fp8bs_stream_t stream) {
+                               int64_t ts_row_stride, int64_t ts_kb_stride, uint8_t* A, int64_t lda, float* sA, int64_t ldsA,
+                               fp8bs_stream_t stream) {
     if (R < 0 || K < 0) return fail(FP8BS_ERR_INVALID_ARG, "negative size");
     if (R == 0 || K == 0) return ok();
     if (K % 128) return fail(FP8BS_ERR_SHAPE, "K must be a multiple of 128 (whole 1x128 groups)");
     if (!idx || !tq || !ts || !A || !sA) return fail(FP8BS_ERR_INVALID_ARG, "null pointer");
     if (ld_tq < K || lda < K || ldsA < R) return fail(FP8BS_ERR_SHAPE, "need ld_tq, lda >= K and ldsA >= R");
+    if (ts_row_stride < 0 || ts_kb_stride < 0) return fail(FP8BS_ERR_SHAPE, "negative scale strides");
     if (!aligned16(tq) || !aligned16(A) || ld_tq % 16 || lda % 16)
         return fail(FP8BS_ERR_ALIGN, "tq, A 16-byte aligned, ld_tq and lda multiples of 16");
     fp8bs_status d = check_device();
     if (d != FP8BS_OK) return d;
-    return from_cuda(launch_expand_rows(R, idx, K, tq, ld_tq, ts, A, lda, sA, ldsA, (cudaStream_t)stream), "expand_rows launch");
+    return from_cuda(launch_expand_rows(R, idx, K, tq, ld_tq, ts, ts_row_stride, ts_kb_stride, A, lda, sA, ldsA,
+                                        (cudaStream_t)stream), "expand_rows launch");
 }
 
 fp8bs_status fp8bs_scales_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd,

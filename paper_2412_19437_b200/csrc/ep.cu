@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(256) k_send_rows(int64_t n, const int64_t* __r
 // batch of 32 consecutive rows: 128-byte stores per contraction block).
 __global__ void __launch_bounds__(256) k_expand_rows(int64_t R, const int64_t* __restrict__ idx, int64_t K, int64_t KB,
                                                      const uint8_t* __restrict__ tq, int64_t ldtq,
-                                                     const float* __restrict__ ts, uint8_t* __restrict__ A, int64_t lda,
+                                                     const float* __restrict__ ts, int64_t ts_rs, int64_t ts_ks,
+                                                     uint8_t* __restrict__ A, int64_t lda,
                                                      float* __restrict__ sA, int64_t ldsA) {
     griddep_wait();
     griddep_launch_dependents();
@@ -196,8 +197,8 @@ __global__ void __launch_bounds__(256) k_expand_rows(int64_t R, const int64_t* _
                 *reinterpret_cast<uint4*>(dst + c) = ldg_nc_v4(src + c);
         }
         if (lane < n) {
-            const float* s = ts + my * KB;
-            for (int64_t kb = 0; kb < KB; ++kb) sA[kb * ldsA + i0 + lane] = s[kb];
+            const float* s = ts + my * ts_rs;
+            for (int64_t kb = 0; kb < KB; ++kb) sA[kb * ldsA + i0 + lane] = s[kb * ts_ks];
         }
     }
 }
@@ -312,9 +313,10 @@ cudaError_t launch_send_rows(int64_t n, const int64_t* tok, int64_t K, const uin
                       dst_row, recv_q, ld_rq, recv_s);
 }
 cudaError_t launch_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ldtq, const float* ts,
-                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, cudaStream_t st) {
-    return launch_pdl(k_expand_rows, dim3(rows_grid((R + 31) / 32)), dim3(256), 0, st, R, idx, K, K / 128, tq, ldtq, ts, A,
-                      lda, sA, ldsA);
+                               int64_t ts_rs, int64_t ts_ks, uint8_t* A, int64_t lda, float* sA, int64_t ldsA,
+                               cudaStream_t st) {
+    return launch_pdl(k_expand_rows, dim3(rows_grid((R + 31) / 32)), dim3(256), 0, st, R, idx, K, K / 128, tq, ldtq, ts,
+                      ts_rs, ts_ks, A, lda, sA, ldsA);
 }
 cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st) {
     return launch_pdl(k_rows_to_blocks, dim3((unsigned)((R + 31) / 32), (unsigned)((KB + 31) / 32)), dim3(256), 0, st,

@@ -68,7 +68,8 @@ cudaError_t launch_send_rows(int64_t n, const int64_t* tok, int64_t K, const uin
                              int64_t ldxs, const int32_t* dst_rank, const int64_t* dst_row, uint8_t* const* recv_q,
                              int64_t ld_rq, float* const* recv_s, cudaStream_t st);
 cudaError_t launch_expand_rows(int64_t R, const int64_t* idx, int64_t K, const uint8_t* tq, int64_t ldtq, const float* ts,
-                               uint8_t* A, int64_t lda, float* sA, int64_t ldsA, cudaStream_t st);
+                               int64_t ts_rs, int64_t ts_ks, uint8_t* A, int64_t lda, float* sA, int64_t ldsA,
+                               cudaStream_t st);
 cudaError_t launch_rows_to_blocks(int64_t R, int64_t KB, const float* src, float* dst, int64_t ldd, cudaStream_t st);
 cudaError_t launch_combine_push(int64_t R, int64_t N, const void* y, int64_t ldy, const int32_t* dst_rank,
                                 const int64_t* dst_slot, void* const* recv_y, int64_t ld_recv_y, cudaStream_t st);

@@ -50,3 +50,25 @@ def test_scatter_equals_grouped_rows(counts, variant):
         unused = torch.ones(R, dtype=torch.bool)
         unused[row[idx]] = False
         assert bool((bufs[r][unused.cuda()] == -7.0).all()), "rows no expert row maps to must stay untouched"
+
+
+@pytest.mark.parametrize("layout", ["rows", "blocks"])
+def test_expand_rows_gathers_codes_and_transposes_scales(layout):
+    """fp8bs_expand_rows (the receiver side of the token-once dispatch, and bench.py's C4 e2e gather):
+    A[i] == tq[idx[i]] and sA[:, i] == the scales of token idx[i], bit for bit, from a row-major token
+    buffer or from the 1x128 quantizer's [K/128, lds] layout; ragged R (not a multiple of 32)."""
+    U, K, R = 300, 1024, 1000
+    KB = K // 128
+    g = torch.Generator().manual_seed(3)
+    tq = torch.randint(0, 256, (U, K), generator=g, dtype=torch.uint8).cuda()
+    ts_rows = torch.rand(U, KB, generator=g).cuda()
+    idx = torch.randint(0, U, (R,), generator=g).cuda()
+    if layout == "rows":
+        ts = ts_rows
+    else:
+        ts = torch.zeros(KB, (U + 3) // 4 * 4, device="cuda")[:, :U]
+        ts.copy_(ts_rows.T)
+    A, sA = fp.expand_rows(idx, tq, ts, ts_layout=layout)
+    torch.cuda.synchronize()
+    assert torch.equal(A, tq[idx])
+    assert torch.equal(sA.view(torch.int32), ts_rows[idx].T.contiguous().view(torch.int32))
