@@ -30,6 +30,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstddef>
+#include <type_traits>
 #include <cstdlib>
 
 #include "sm100.cuh"
@@ -247,16 +248,18 @@ __device__ __forceinline__ bool get_tile_gw(const KParams& p, const GWSched<kG>&
 // spill promotion accumulators.
 struct TileTable { int ntiles; int next; int pad[2]; int4 t[1]; };   // next: the dynamic claim counter
 
-__device__ __forceinline__ bool get_tile_table(const TileTable* tt, int N, int t, Tile& tl) {
-    // the count and the entry are re-read per tile (L2 hits) rather than held in registers
-    if (t >= __ldcg(&tt->ntiles)) return false;
-    const int2 v = __ldcg(reinterpret_cast<const int2*>(&tt->t[t]));   // L2 only: written by the previous grid
+__device__ __forceinline__ void decode_table_entry(const int4 v, int N, Tile& tl) {
     tl.row0 = v.x;
     tl.row_end = v.x + (int)((uint32_t)v.y >> 22);     // rows of the expert left in the tile (<= 512)
     tl.n0 = (v.y & 0xFFFF) * BN;
-    tl.e = (v.y >> 16) & 0x3F;                         // low 6 bits of the expert; the rest in .z
-    tl.e |= __ldcg(reinterpret_cast<const int*>(&tt->t[t]) + 2) << 6;
+    tl.e = ((v.y >> 16) & 0x3F) | (v.z << 6);          // low 6 bits of the expert; the rest in .z
     tl.nh = (N - tl.n0 > HN) ? 2 : 1;
+}
+
+__device__ __forceinline__ bool get_tile_table(const TileTable* tt, int N, int t, Tile& tl) {
+    // static-schedule experiments (FP8BS_STATIC_SCHED): the count and the entry re-read per tile (L2)
+    if (t >= __ldcg(&tt->ntiles)) return false;
+    decode_table_entry(__ldcg(&tt->t[t]), N, tl);      // L2 only: written by the previous grid
     return true;
 }
 
@@ -512,7 +515,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         uint8_t scale[C::kSStages * C::SSTAGE];
         uint64_t bar[C::NBAR];
         uint32_t tmem;
-        int tq[C::kTQ];            // grouped: claimed tile indices
+        int4 tq[C::kTQ];           // grouped: claimed tiles' table entries (.w = tile index, -1: none left)
     };
     __shared__ StaticSmem s_static;
     uint8_t* s_scale = s_static.scale;
@@ -560,8 +563,16 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    auto next_tile = [&](int t, Tile& tl) -> bool {
-        if constexpr (kGW) return get_tile_gw<C::ROWS>(p, gw, t, tl);
+    // A tile reference: its index (static schedules) or, for the dynamically claimed grouped tiles, the
+    // table entry the claimer shipped through the tq ring (decoded here with no memory access).
+    constexpr bool kDyn = kGrouped && !kGW && !FP8BS_STATIC_SCHED;
+    using TileRef = typename std::conditional<kDyn, int4, int>::type;
+    auto next_tile = [&](const TileRef t, Tile& tl) -> bool {
+        if constexpr (kDyn) {
+            if (t.w < 0) return false;
+            decode_table_entry(t, p.N, tl);
+            return true;
+        } else if constexpr (kGW) return get_tile_gw<C::ROWS>(p, gw, t, tl);
         else if constexpr (kSplit) return get_tile_split<C::ROWS>(p, t, tl);
         else if constexpr (kGrouped) return get_tile_table(reinterpret_cast<const TileTable*>(p.tiles), p.N, t, tl);
         else return get_tile_dense<C::ROWS>(p, t, tl);
@@ -577,26 +588,35 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // each runs at C4 and lose the L2 sharing of A rows between the n-tiles of an m-tile: DRAM read
     // 4.5x the operands).  The claimer runs one tile ahead so the atomic's latency is off the path.
     TileTable* ttw = reinterpret_cast<TileTable*>(p.tiles);
+    // The claimer ships the claimed tile's 16-byte table entry itself (it loads it off the critical path,
+    // one tile ahead): the other roles decode the tile from shared memory instead of waiting on an L2
+    // load at every tile boundary.
     auto tq_publish = [&](int j) -> int {            // leader w0, one lane: claim tile #j of this cluster
         const int q = j % C::kTQ;
         mbar_wait(tqempty_bar(q), ((j / C::kTQ) & 1) ^ 1);
         const int t = atomicAdd(&ttw->next, 1);
+        int4 e = make_int4(0, 0, 0, -1);
+        if (t < __ldcg(&ttw->ntiles)) { e = __ldcg(&ttw->t[t]); e.w = t; }
         const uint32_t a = smem_u32(&s_static.tq[q]);
-        asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(t) : "memory");
+        sts_u32x4(a, (uint32_t)e.x, (uint32_t)e.y, (uint32_t)e.z, (uint32_t)e.w);
         mbar_arrive(tqfull_bar(q));
         if constexpr (kPair) {
-            st_shared_cluster_u32(mapa_shared(a, 1), (uint32_t)t);
+            st_shared_cluster_u32x4(mapa_shared(a, 1), (uint32_t)e.x, (uint32_t)e.y, (uint32_t)e.z, (uint32_t)e.w);
             mbar_arrive_release_cluster(mapa_shared(tqfull_bar(q), 1));
         }
-        return t;
+        return e.w;
     };
-    auto tq_take = [&](int j) -> int {               // every other role, whole warp: tile #j
+    auto tq_entry = [&](int q) -> int4 {
+        const uint4 v = lds_u32x4(opaque_u32(sring) + (uint32_t)offsetof(StaticSmem, tq) + 16u * q);
+        return make_int4((int)v.x, (int)v.y, (int)v.z, (int)v.w);
+    };
+    auto tq_take = [&](int j) -> int4 {              // every other role, whole warp: tile #j
         // addresses rebuilt from an opaque base at each call: hoisted out of the tile loop they
         // would stay live across the K loop and push the promotion warps' accumulators into spills
         const int q = j % C::kTQ;
         const uint32_t b = opaque_u32(bar0) + 8u * (2 * C::kStages + 2 * C::kSStages + 2 * C::NSLOT + q);
         mbar_wait_acquire_cluster(b, (j / C::kTQ) & 1);
-        const int t = (int)lds_u32(opaque_u32(sring) + (uint32_t)offsetof(StaticSmem, tq) + 4u * q);
+        const int4 t = tq_entry(q);
         __syncwarp();
         if (elect_one()) {
             const uint32_t e = b + 8u * C::kTQ;
@@ -606,21 +626,24 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         __syncwarp();
         return t;
     };
-    int t_next = 0;                                  // claimer: tile #j+1, claimed ahead
-    // the leader's producer warp (lane 0 claims, the warp gets the index)
-    auto tile_index_claim = [&](int j) -> int {
-        if constexpr (!kGrouped || kGW || FP8BS_STATIC_SCHED) return cid + j * ncl;
-        int t = 0;
-        if (lane == 0) {
-            t = j == 0 ? tq_publish(0) : t_next;
-            if (t < __ldcg(&ttw->ntiles)) t_next = tq_publish(j + 1);
+    int t_next = 0;                                  // claimer: tile #j+1, claimed ahead (-1: none left)
+    // the leader's producer warp (lane 0 claims, the warp reads the entry back from its own ring slot:
+    // the slot of tile #j is republished only at claim #j + kTQ, after this read)
+    auto tile_index_claim = [&](int j) -> TileRef {
+        if constexpr (!kDyn) return cid + j * ncl;
+        else {
+            if (lane == 0) {
+                const int t = j == 0 ? tq_publish(0) : t_next;
+                if (t >= 0) t_next = tq_publish(j + 1);
+            }
+            __syncwarp();
+            return tq_entry(j % C::kTQ);
         }
-        return __shfl_sync(0xffffffffu, t, 0);
     };
     // every other role
-    auto tile_index = [&](int j) -> int {
-        if constexpr (!kGrouped || kGW || FP8BS_STATIC_SCHED) return cid + j * ncl;
-        return tq_take(j);
+    auto tile_index = [&](int j) -> TileRef {
+        if constexpr (!kDyn) return cid + j * ncl;
+        else return tq_take(j);
     };
 
     if (warp < 4) {
@@ -634,7 +657,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             int it = 0;
             Tile tl;
             auto tix = [&](int j) { return rank == 0 ? tile_index_claim(j) : tile_index(j); };
-            for (int j = 0, t = tix(0); next_tile(t, tl); t = tix(++j)) {
+            int j = 0;
+            for (TileRef t = tix(0); next_tile(t, tl); t = tix(++j)) {
                 if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
                 const int arow = tl.row0 + (int)rank * BM;
                 const int brow = tl.n0 + (int)rank * C::BH_ROWS;
@@ -674,7 +698,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, HN);
             int it = 0, qh = 0;
             Tile tl;
-            for (int j = 0, t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
+            int j = 0;
+            for (TileRef t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
                 if (h >= tl.nh) {
                     // This half lies past N (last column tile): no MMAs, but the issuer still walks
                     // the ring in step and releases each stage with its own (empty) commit.  Jumping
@@ -738,7 +763,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             int sit = 0;
             if ((kDbg & 512)) return;   // experiment: no scale ring traffic (promotion uses stale scales)
             Tile tl;
-            for (int j = 0, t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
+            int j = 0;
+            for (TileRef t = tile_index(0); next_tile(t, tl); t = tile_index(++j)) {
                 if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
                 const float* sbp = p.sB;
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
@@ -795,7 +821,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // register fewer than a counter: the accumulators are at the edge of the 240-register budget)
         int jt = 0;                                     // grouped Wgrad: tiles walked (KB varies per tile)
         auto next_j = [&]() -> int { if constexpr (kKR) return ++jt; else return sit / p.KB; };
-        for (int t = tile_index(0); next_tile(t, tl); t = tile_index(next_j())) {
+        for (TileRef t = tile_index(0); next_tile(t, tl); t = tile_index(next_j())) {
             const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
             const bool active = h < tl.nh;
             if (!active) {

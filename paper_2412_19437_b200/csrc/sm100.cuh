@@ -311,6 +311,9 @@ __device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t bar, uint32_t
 __device__ __forceinline__ void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(cluster_addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_shared_cluster_u32x4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 // An opaque copy (volatile asm): keeps the compiler from hoisting values derived from `v` out of a
 // loop, where they would stay live — and take registers — across the whole loop body.
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
