@@ -125,6 +125,8 @@ struct KParams {
     // grouped, streamed operands (a dispatch still writing A / sA): the rows of local group e may be
     // read once ready[e * ready_chunks / G] >= ready_target (wrap-safe); ready == nullptr: no waits
     const uint32_t* ready; uint32_t ready_target; int ready_chunks;
+    // grouped: expert weights [G][N][K] (the claimer prefetches the next expert's into L2)
+    const uint8_t* Bp; int64_t b_expert_bytes; int b_pf_chunk; int b_pf_last_or_chunk[2];
     // split-K tail (kOutSplit): units u < split_units are (tile split_t0 + u / split_s, K-chunk u % split_s);
     // unit u writes its FP32 partial tile to rows [u * ROWS, (u + 1) * ROWS) of the workspace (BN columns)
     int split_t0, split_s, split_units;
@@ -147,6 +149,9 @@ constexpr int kTsSlots = 12;
 #endif
 #ifndef FP8BS_WG_NOSB
 #define FP8BS_WG_NOSB 0
+#endif
+#ifndef FP8BS_B_PREFETCH
+#define FP8BS_B_PREFETCH 0   // experiment: prefetch the next expert's weights into L2 at an expert's first tile (C4: -0.5%)
 #endif
 #ifndef FP8BS_STATIC_SCHED
 #define FP8BS_STATIC_SCHED 0   // experiments: 1 = grouped tiles on the static schedule too (A/B builds)
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(1024) k_grouped_schedule(const int64_t* __rest
         const int m = nfast ? l / num_n : l % mt, n = nfast ? l % num_n : l / mt;
         const int r0 = row0[x] + m * rows;
         const int left = min(row0[x + 1] - r0, 2 * rows);  // only < rows (a crossing tile) matters
-        tt->t[t] = make_int4(r0, (left << 22) | ((x & 0x3F) << 16) | n, x >> 6, 0);
+        tt->t[t] = make_int4(r0, (left << 22) | ((x & 0x3F) << 16) | n, x >> 6, l == 0 ? 1 : 0);   // .w: expert's first tile
     }
 }
 
@@ -596,7 +601,22 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_wait(tqempty_bar(q), ((j / C::kTQ) & 1) ^ 1);
         const int t = atomicAdd(&ttw->next, 1);
         int4 e = make_int4(0, 0, 0, -1);
-        if (t < __ldcg(&ttw->ntiles)) { e = __ldcg(&ttw->t[t]); e.w = t; }
+        if (t < __ldcg(&ttw->ntiles)) {
+            e = __ldcg(&ttw->t[t]);
+#if FP8BS_B_PREFETCH
+            // the first tile of expert x: start pulling expert x + 1's weights into L2, so its first
+            // tiles (claimed about a wave later) do not wait on DRAM
+            const int x = ((e.y >> 16) & 0x3F) | (e.z << 6);
+            if (e.w && x + 1 < p.G) {
+                const uint8_t* nb = p.Bp + (int64_t)(x + 1) * p.b_expert_bytes;
+#pragma unroll 1
+                for (int c = 0; c < 16; ++c)             // 16 bulk prefetches of b_pf_chunk bytes (the last clipped)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                 :: "l"(nb + (int64_t)c * p.b_pf_chunk), "r"((uint32_t)p.b_pf_last_or_chunk[c == 15]) : "memory");
+            }
+#endif
+            e.w = t;
+        }
         const uint32_t a = smem_u32(&s_static.tq[q]);
         sts_u32x4(a, (uint32_t)e.x, (uint32_t)e.y, (uint32_t)e.z, (uint32_t)e.w);
         mbar_arrive(tqfull_bar(q));
@@ -1267,6 +1287,10 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     else { p.sb_nb_stride = 1; p.sb_kb_stride = a.ldsB; p.sb_expert_stride = 0; }
     p.D = a.D; p.ldd = a.ldd; p.accumulate = a.accumulate;
     p.sc_base = a.sc_base; p.sc_rank = a.sc_rank; p.sc_row = a.sc_row;
+    p.Bp = a.B; p.b_expert_bytes = (int64_t)a.N * a.K;
+    p.b_pf_chunk = (int)(((p.b_expert_bytes + 15) / 16 + 15) / 16 * 16);     // 16 chunks, multiples of 16 bytes
+    p.b_pf_last_or_chunk[0] = p.b_pf_chunk;
+    p.b_pf_last_or_chunk[1] = (int)max((int64_t)16, p.b_expert_bytes - 15 * (int64_t)p.b_pf_chunk);
     p.ready = a.ready; p.ready_target = a.ready_target; p.ready_chunks = a.ready_chunks;
     p.G = a.G; p.offsets = a.offsets; p.tiles = a.workspace;
     p.tile_end = sp ? sp->t0 : p.num_m * p.num_n;
