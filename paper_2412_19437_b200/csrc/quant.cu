@@ -135,13 +135,33 @@ k_quant_act_1x128(const T* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
 // consumer warps encode from shared memory and store codes/scales directly.  Memory traffic is
 // decoupled from the encode arithmetic, so up to 192 KB per SM stays in flight.
 // ===========================================================================================
+#ifndef FP8BS_Q1_EL
+#define FP8BS_Q1_EL 32   // BF16 elements per consumer lane (16: 8 lanes per tile)
+#endif
 template <typename T>
 struct Q1Cfg {
-    static constexpr int EL = 16;                           // elements per lane (8 lanes per tile)
+    // elements per lane: BF16 32 (4 lanes per tile: the per-group scale work — shuffles, the scale
+    // division, its reciprocal — is shared by 32 elements, which keeps the kernel HBM-bound at the
+    // ~1.4 GHz a preceding GEMM leaves the SMs at); FP32 16
+    static constexpr int EL = sizeof(T) == 2 ? FP8BS_Q1_EL : 16;
     static constexpr int L = 128 / EL;
-    static constexpr int VEC = EL * (int)sizeof(T) / 16;    // 16-byte smem loads per lane: 2 / 4
+    static constexpr int VEC = EL * (int)sizeof(T) / 16;    // 16-byte smem loads per lane: 4 / 4
     static constexpr int TILE_BYTES = 128 * (int)sizeof(T);
-    static constexpr int CONSUMERS = 16;                    // warps
+#ifndef FP8BS_Q1_WARPS
+#define FP8BS_Q1_WARPS 16
+#endif
+    // 16 consumer warps (BF16, 32 per lane: 128 tiles = 32 KB per stage, 3 stages).  Measured on C4's
+    // 65536 x 7168 (tools/quant_instep.py, same box, GB/s alone at 1965 MHz / right after the grouped
+    // GEMM at its power-capped clock): 16 per lane x 16 warps 6035 / 4189-4375; 32 per lane x 16 warps
+    // 5461 / 4969-5230; 32 x 8 warps 5297 / 4636-4725; 32 contiguous x 8 warps 6195 / 4113-4165.  The
+    // step's quantizer runs right after the GEMM, so the second column decides.
+    static constexpr int CONSUMERS = FP8BS_Q1_WARPS;
+    // BF16, 32 per lane: lane li of a tile takes the 16-byte chunks li, li + L, ... (2-way shared-memory
+    // bank conflicts like the 16-per-lane contiguous split; contiguous 64-byte runs would be 4-way)
+#ifndef FP8BS_Q1_INTERLEAVE
+#define FP8BS_Q1_INTERLEAVE 1
+#endif
+    static constexpr bool INTERLEAVED = FP8BS_Q1_INTERLEAVE && sizeof(T) == 2 && EL == 32;
     static constexpr int TILES_PER_PASS = CONSUMERS * (32 / L);    // 64
     static constexpr int PASSES = 1;
     static constexpr int CHUNK_TILES = TILES_PER_PASS * PASSES;
@@ -207,7 +227,8 @@ k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __
             float f[C::EL];
 #pragma unroll
             for (int v = 0; v < C::VEC; ++v) {
-                const uint4 u = ok ? lds128(sbase + st * C::CHUNK_BYTES + d * C::TILE_BYTES + li * (C::EL * (int)sizeof(T)) + v * 16)
+                const int cb = C::INTERLEAVED ? (li + C::L * v) * 16 : li * (C::EL * (int)sizeof(T)) + v * 16;
+                const uint4 u = ok ? lds128(sbase + st * C::CHUNK_BYTES + d * C::TILE_BYTES + cb)
                                    : make_uint4(0, 0, 0, 0);
                 Vec<T>::unpack(u, f + v * Vec<T>::E);
             }
@@ -218,12 +239,26 @@ k_quant_act_1x128_tma(const T* __restrict__ x, int64_t M, int64_t K, uint8_t* __
             for (int o = C::L / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
             const float sc = group_scale_t<kPow2>(amax);
             const float r = __frcp_rn(sc);
-            uint32_t w[4];
-            if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w);   // warp-uniform
-            else encode_chunk<16>(f, sc, r, false, w);
+            uint32_t w[C::EL / 4];
+            if (__all_sync(0xffffffffu, fast_div_ok(sc))) {                                     // warp-uniform
+#pragma unroll
+                for (int hh = 0; hh < C::EL / 16; ++hh) encode_chunk<16>(f + 16 * hh, sc, r, true, w + 4 * hh);
+            } else {
+#pragma unroll
+                for (int hh = 0; hh < C::EL / 16; ++hh) encode_chunk<16>(f + 16 * hh, sc, r, false, w + 4 * hh);
+            }
             if (ok) {
                 const int t = t0 + d;
-                *reinterpret_cast<uint4*>(q + (int64_t)t * 128 + li * C::EL) = make_uint4(w[0], w[1], w[2], w[3]);
+                if constexpr (C::INTERLEAVED) {             // chunk li + L*v: 8 codes at (li + L*v) * 8
+#pragma unroll
+                    for (int v = 0; v < C::VEC; ++v)
+                        *reinterpret_cast<uint2*>(q + (int64_t)t * 128 + (li + C::L * v) * 8) = make_uint2(w[2 * v], w[2 * v + 1]);
+                } else {
+#pragma unroll
+                    for (int hh = 0; hh < C::EL / 16; ++hh)
+                        *reinterpret_cast<uint4*>(q + (int64_t)t * 128 + li * C::EL + 16 * hh) =
+                            make_uint4(w[4 * hh], w[4 * hh + 1], w[4 * hh + 2], w[4 * hh + 3]);
+                }
                 if (li == 0) {
                     const int m = t / KB, kb = t - m * KB;
                     s[(int64_t)kb * lds + m] = sc;
