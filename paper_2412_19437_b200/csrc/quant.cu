@@ -379,6 +379,9 @@ k_quant_act_128x1(const T* __restrict__ x, int64_t M, int64_t C, int64_t ldx,
 #ifndef FP8BS_DUAL_UNROLL
 #define FP8BS_DUAL_UNROLL 1
 #endif
+#ifndef FP8BS_DUAL_ROW32
+#define FP8BS_DUAL_ROW32 0   // experiment: dual quantizer row pass with 32 elements per lane (C1: X 35.6 -> 36.7 us, dY 75.9 -> 77.2 us: slower)
+#endif
 constexpr int kDualUnroll = FP8BS_DUAL_UNROLL;   // row passes of the dual quantizer in flight (experiments)
 template <typename T>
 struct QTCfg {
@@ -639,7 +642,14 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         return;
     }
     const int tid = threadIdx.x, wc = tid & 63, rg = tid >> 6;
+#if FP8BS_DUAL_ROW32
+    // row phase: 8 rows per warp pass, 4 lanes per row, 32 elements per lane (the per-row scale work
+    // shared by twice the elements, as in k_quant_act_1x128_tma); lane li takes the 16-byte chunks li,
+    // li + 4, ... of its row (2-way shared-memory conflicts, like the 8-lane split)
+    const int sub = lane >> 2, li = lane & 3;
+#else
     const int sub = lane >> 3, li = lane & 7;          // row phase: 4 rows per warp pass, 8 lanes per row
+#endif
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % P::STAGES;
@@ -650,12 +660,53 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
         // Interior tile (all tiles of M, C multiples of 128): stores through per-thread base pointers
         // advanced by constant strides, without per-store bounds arithmetic.
         const bool full = (m0 + 128 <= M) && (c0 + P::CH <= C);
-        uint8_t* qrow = q + (m0 + warp * 4 + sub) * ldq + c0 + li * 16;     // + pass * 32 rows
-        float* srow = s + (int64_t)cb * lds + m0 + warp * 4 + sub;
+#if FP8BS_DUAL_ROW32
+        constexpr int RPW = 8;                                               // rows per warp per pass
+#else
+        constexpr int RPW = 4;
+#endif
+        uint8_t* qrow = q + (m0 + warp * RPW + sub) * ldq + c0;              // + pass * 8 * RPW rows
+        float* srow = s + (int64_t)cb * lds + m0 + warp * RPW + sub;
         // ---- 1x128 along the channels: rows of the tile ----
 #pragma unroll kDualUnroll
-        for (int pass = 0; pass < 4; ++pass) {
-            const int row = pass * 32 + warp * 4 + sub;
+        for (int pass = 0; pass < 128 / (RPW * P::CONSUMERS); ++pass) {
+            const int row = pass * RPW * P::CONSUMERS + warp * RPW + sub;
+#if FP8BS_DUAL_ROW32
+            float f[32];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) Vec<T>::unpack(lds128(tile + row * 256 + (li + 4 * v) * 16), f + 8 * v);
+            float amax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) amax = fmaxf(amax, fabsf(f[e]));
+#pragma unroll
+            for (int o = 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            const float sc = group_scale_t<kPow2>(amax);
+            const float r = __frcp_rn(sc);
+            uint32_t w8[8];
+            if (__all_sync(0xffffffffu, fast_div_ok(sc))) {                    // warp-uniform
+                encode_chunk<16>(f, sc, r, true, w8);
+                encode_chunk<16>(f + 16, sc, r, true, w8 + 4);
+            } else {
+                encode_chunk<16>(f, sc, r, false, w8);
+                encode_chunk<16>(f + 16, sc, r, false, w8 + 4);
+            }
+            if (full) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    *reinterpret_cast<uint2*>(qrow + pass * RPW * P::CONSUMERS * ldq + (li + 4 * v) * 8) = make_uint2(w8[2 * v], w8[2 * v + 1]);
+                if (li == 0) srow[pass * RPW * P::CONSUMERS] = sc;
+            } else {
+                const int64_t m = m0 + row;
+                if (m < M) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int64_t c = c0 + (li + 4 * v) * 8;
+                        if (c < C) *reinterpret_cast<uint2*>(q + m * ldq + c) = make_uint2(w8[2 * v], w8[2 * v + 1]);
+                    }
+                    if (li == 0) s[(int64_t)cb * lds + m] = sc;
+                }
+            }
+#else
             float f[16];
             Vec<T>::unpack(lds128(tile + row * 256 + li * 32), f);
             Vec<T>::unpack(lds128(tile + row * 256 + li * 32 + 16), f + 8);
@@ -670,7 +721,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
             if (__all_sync(0xffffffffu, fast_div_ok(sc))) encode_chunk<16>(f, sc, r, true, w4);   // warp-uniform
             else encode_chunk<16>(f, sc, r, false, w4);
             if (full) {
-                *reinterpret_cast<uint4*>(qrow + pass * 32 * ldq) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                *reinterpret_cast<uint4*>(qrow + pass * 32 * ldq + li * 16) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                 if (li == 0) srow[pass * 32] = sc;
             } else {
                 const int64_t m = m0 + row, c = c0 + li * 16;
@@ -679,6 +730,7 @@ k_quant_act_dual_tma(const __grid_constant__ CUtensorMap tmX, int64_t M, int64_t
                     if (li == 0) s[(int64_t)cb * lds + m] = sc;
                 }
             }
+#endif
         }
         // ---- 128x1 along the tokens: columns of the tile (as k_quant_act_128x1_tma) ----
         uint32_t w[32];
