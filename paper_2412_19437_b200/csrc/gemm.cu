@@ -83,7 +83,8 @@ struct Cfg {
     static constexpr int EPI_WARP_BYTES = 32 * 128 * EPI_BUFS;
     // Operand stages fill the dynamic shared memory left after the static scale ring, the epilogue
     // buffers and the barriers (227 KB per CTA, 1 KB of alignment slack).
-    static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - FP8BS_NPW * EPI_WARP_BYTES;
+    static constexpr int SCAT_BYTES = 32 * 8;               // scatter epilogue: a warp's 32 row destinations
+    static constexpr int SMEM_FREE = 227 * 1024 - 2048 - kSStages * SSTAGE - FP8BS_NPW * (EPI_WARP_BYTES + SCAT_BYTES);
     static constexpr int kStages = SMEM_FREE / STAGE > 8 ? 8 : SMEM_FREE / STAGE;
     // Promotion warps (FP8BS_NPW, 8 or 16): warp (h, gg, quad) owns rows [32 quad, 32 quad + 32) x
     // NC = 128 * 8 / NPW columns (group gg) of half h.  8 wide warps pay the per-K-block barrier and
@@ -102,7 +103,8 @@ struct Cfg {
     static constexpr int TQ_CONSUMERS = kPair ? (3 + NPW) + (2 + NPW) : 3 + NPW;
     static constexpr int NBAR = 2 * kStages + 2 * kSStages + 2 * NSLOT + 2 * kTQ;
     static constexpr int OFF_EPI = kStages * STAGE;
-    static constexpr int SMEM_DENSE = 1024 + OFF_EPI + NPW * EPI_WARP_BYTES;
+    static constexpr int OFF_SCAT = OFF_EPI + NPW * EPI_WARP_BYTES;
+    static constexpr int SMEM_DENSE = 1024 + OFF_SCAT + NPW * SCAT_BYTES;
 };
 
 struct KParams {
@@ -1035,6 +1037,18 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 // that crosses its expert's end are copied out of the staging buffer by the lanes
                 const bool full = !kGrouped || (!kScatter && rows_here >= 32);
                 const uint32_t ebuf0 = smem_u32(s_epi) + (warp - 4) * C::EPI_WARP_BYTES;
+                // scatter: lane l resolves row l's destination once per tile into shared memory (the
+                // chunks below read it back instead of the rank, slot and pointer table per store)
+                const uint32_t sdst = smem_u32(smem + C::OFF_SCAT) + (warp - 4) * C::SCAT_BYTES;
+                if constexpr (kScatter) {
+                    const int64_t gr = grow0 + lane;
+                    if (lane < rows_here) {
+                        const uint64_t d = reinterpret_cast<uint64_t>(p.sc_base[__ldg(p.sc_rank + gr)]) +
+                                           (uint64_t)(__ldg(p.sc_row + gr) * p.ldd) * ESZ;
+                        asm volatile("st.shared.u64 [%0], %1;" :: "r"(sdst + 8u * lane), "l"(d) : "memory");
+                    }
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int c = 0; c < NC / CW; ++c) {
                     const uint32_t ebuf = ebuf0 + (c % C::EPI_BUFS) * (32 * 128);
@@ -1066,9 +1080,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                                 const uint4 v = lds_u32x4(ebuf + r * 128 + ((u ^ (r & 7)) << 4));
                                 uint8_t* dst;
                                 if constexpr (kScatter) {   // 8 lanes write one row's 128 bytes to its owner
-                                    const int64_t gr = grow0 + r;
-                                    dst = reinterpret_cast<uint8_t*>(p.sc_base[__ldg(p.sc_rank + gr)]) +
-                                          (__ldg(p.sc_row + gr) * p.ldd + col) * ESZ + u * 16;
+                                    uint64_t d;
+                                    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(d) : "r"(sdst + 8u * r));
+                                    dst = reinterpret_cast<uint8_t*>(d) + (int64_t)col * ESZ + u * 16;
                                 } else {
                                     dst = reinterpret_cast<uint8_t*>(p.D) + ((int64_t)(grow0 + r) * p.ldd + col) * ESZ + u * 16;
                                 }
