@@ -479,6 +479,8 @@ def grouped_gemm_scatter(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tenso
         raise ValueError("dst_rank must be CUDA int32 and dst_row CUDA int64")
     G, N, K = B.shape
     R = A.shape[0]
+    if dst_rank.numel() < R or dst_row.numel() < R:
+        raise ValueError("dst_rank / dst_row need one entry per row of A")
     if workspace is None:
         wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K))
         workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
@@ -507,6 +509,10 @@ def expand_rows(idx: torch.Tensor, tq: torch.Tensor, ts: torch.Tensor, A: torch.
         A = torch.empty(R, K, dtype=torch.uint8, device=tq.device)
     if sA is None:
         sA = torch.empty(K // 128, _pad4(R), dtype=torch.float32, device=tq.device)[:, :R]
+    if A.shape[0] < R or A.shape[1] < K or A.dtype != torch.uint8 or sA.shape[0] < K // 128 or sA.shape[1] < R:
+        raise ValueError("A must be uint8 [>= R, >= K] and sA [>= K/128, >= R]")
+    if not (idx.is_cuda and idx.dtype == torch.int64):
+        raise ValueError("idx must be a CUDA int64 tensor")
     rs, ks = (ts.stride(0), ts.stride(1)) if ts_layout == "rows" else (ts.stride(1), ts.stride(0))
     _check(lib().fp8bs_expand_rows(R, _p(idx), K, _p(tq), tq.stride(0), _p(ts), rs, ks, _p(A), A.stride(0), _p(sA),
                                    sA.stride(0), _stream(tq)), "fp8bs_expand_rows")
