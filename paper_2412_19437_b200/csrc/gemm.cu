@@ -270,9 +270,9 @@ __device__ __forceinline__ bool get_tile_table(const TileTable* tt, int N, int t
     return true;
 }
 
-// One CTA of 1024 threads (G <= 1024): thread e counts expert e's tiles, ceil(M_e/rows) x num_n, a
-// block scan places them expert by expert, then all threads write the entries (tile t's expert by
-// binary search over the scanned starts).  Inside an expert the smaller operand stays L2-resident:
+// CTAs of 1024 threads (G <= 1024): in each, thread e counts expert e's tiles, ceil(M_e/rows) x num_n,
+// a block scan places them expert by expert, then the threads write the CTA's share of the entries
+// (tile t's expert by binary search over the scanned starts).  Inside an expert the smaller operand stays L2-resident:
 // more rows than N walks the n-tiles fastest (A rows read once, B_e resident), fewer walks m fastest.
 #ifndef FP8BS_GROUPED_ORDER
 #define FP8BS_GROUPED_ORDER 0   // experiments: 1 always m-fastest, 2 always n-fastest
@@ -308,10 +308,14 @@ __global__ void __launch_bounds__(1024) k_grouped_schedule(const int64_t* __rest
     }
     __syncthreads();
     if (e < G) { start[e] = warp_sum[w] + incl - cnt; row0[e] = (int)a; }
-    if (e == G - 1) { start[G] = warp_sum[w] + incl; row0[G] = (int)b; tt->ntiles = start[G]; tt->next = 0; }
+    if (e == G - 1) {
+        start[G] = warp_sum[w] + incl; row0[G] = (int)b;
+        if (blockIdx.x == 0) { tt->ntiles = start[G]; tt->next = 0; }
+    }
     __syncthreads();
     const int total = start[G];
-    for (int t = e; t < total; t += blockDim.x) {
+    // every CTA redoes the (cheap) scan and fills its share of the entries: one CTA took ~18 us at C4
+    for (int t = blockIdx.x * blockDim.x + e; t < total; t += gridDim.x * blockDim.x) {
         int lo = 0, hi = G;                                // expert x: start[x] <= t < start[x + 1]
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -1332,8 +1336,11 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
     const int smem = C::SMEM_DENSE;
     if (kGrouped && !kWgrad) {
         // the tile table for this launch (k_grouped_schedule), then the GEMM; both PDL
-        cudaError_t e = launch_pdl(k_grouped_schedule, dim3(1), dim3(kMaxGroups), 0, st, a.offsets, a.G, C::ROWS,
-                                   p.num_n, p.N, reinterpret_cast<TileTable*>(a.workspace));
+        const int64_t ub = ((a.M + C::ROWS - 1) / C::ROWS + a.G) * (int64_t)p.num_n;   // tiles, upper bound
+        int64_t sg = (ub + 4 * kMaxGroups - 1) / (4 * kMaxGroups);                    // ~4 entries per thread
+        sg = sg < 1 ? 1 : (sg > num_sms() ? num_sms() : sg);
+        cudaError_t e = launch_pdl(k_grouped_schedule, dim3((unsigned)sg), dim3(kMaxGroups), 0, st, a.offsets, a.G,
+                                   C::ROWS, p.num_n, p.N, reinterpret_cast<TileTable*>(a.workspace));
         if (e != cudaSuccess) return e;
     }
     auto kern = k_gemm_bs<kWgrad, kOut, kGrouped, kPair>;
