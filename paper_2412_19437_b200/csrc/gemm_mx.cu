@@ -42,6 +42,13 @@
 #ifndef FP8BS_MX_MC
 #define FP8BS_MX_MC 1    // CTA pairs along M sharing each B tile by TMA multicast (0: independent CTAs)
 #endif
+#ifndef FP8BS_MX_2CTA
+#define FP8BS_MX_2CTA 1  // the CTA pairs run tcgen05.mma.cta_group::2 (M = 256, each CTA stages half of B) instead of
+                         // two cta_group::1 MMAs over a multicast full B
+#endif
+#ifndef FP8BS_MX_2CTA_RELCL
+#define FP8BS_MX_2CTA_RELCL 0   // cluster-scope release/acquire on the SF atoms' handoff (a MEMBAR per K-block)
+#endif
 #ifndef FP8BS_MX_DBG
 #define FP8BS_MX_DBG 0   // experiments (tools/): 1 = skip the output stores, 2 = constant scale atoms (no loads)
 #endif
@@ -121,6 +128,11 @@ __device__ __forceinline__ uint64_t cp_desc(uint32_t addr) {
 __device__ __forceinline__ void tmem_cp_atom(uint32_t taddr, uint64_t desc) {
     asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" :: "r"(taddr), "l"(desc) : "memory");
 }
+// cta_group::2 (issued by the pair's leader): each CTA's atom at the same shared-memory offset into the
+// same TMEM columns of that CTA
+__device__ __forceinline__ void tmem_cp_atom_pair(uint32_t taddr, uint64_t desc) {
+    asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" :: "r"(taddr), "l"(desc) : "memory");
+}
 // block-scaled instruction descriptor (E4M3 x E4M3, FP32 accumulate, UE8M0 scales)
 __host__ __device__ constexpr uint32_t idesc_mx(uint32_t m, uint32_t n, uint32_t sf_id) {
     return (sf_id << 4) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24) | (sf_id << 29);
@@ -128,6 +140,14 @@ __host__ __device__ constexpr uint32_t idesc_mx(uint32_t m, uint32_t n, uint32_t
 __device__ __forceinline__ void mma_mx(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                 :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+
+// Issued by the pair's leader: D (both CTAs' TMEM, 128 lanes each) (+)= A (128 rows per CTA) x B (N/2 rows per
+// CTA), block-scaled with each CTA's SFA (its rows) and SFB (all N columns, duplicated in both CTAs)
+__device__ __forceinline__ void mma_mx_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
                  :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
 }
 
@@ -174,14 +194,23 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // half of the B tile and multicasts it into both, so a stage is free only when BOTH CTAs' MMAs
     // have read it (each commit arrives on the empty barrier of both CTAs: count 2)
     constexpr int MC = kMc ? 2 : 1;
+    // k2: the pair runs 2-CTA MMAs issued by the leader: each CTA stages its A rows and HALF of the B tile
+    // (TMA completing on the leader's full barrier), its SF atoms (own rows' SFA, all columns' SFB), and
+    // the leader's commits free both CTAs' stages and hand both CTAs their accumulator rows
+    constexpr bool k2 = kMc && !kGrouped && FP8BS_MX_2CTA;
     const uint32_t rank = kMc ? cluster_ctarank() : 0;
     const int cid = kMc ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, ncl = kMc ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(full_bar(s), 2); mbar_init(empty_bar(s), MC); }
-        for (int b = 0; b < 2; ++b) { mbar_init(accfull_bar(b), 1); mbar_init(accempty_bar(b), 4); }
+        // k2 (the leader's barriers count): full = its producer + both CTAs' SF warps; empty = the leader's
+        // multicast commit; accempty = both CTAs' 4 epilogue warps
+        for (int s = 0; s < STAGES; ++s) { mbar_init(full_bar(s), k2 ? 3 : 2); mbar_init(empty_bar(s), k2 ? 1 : MC); }
+        for (int b = 0; b < 2; ++b) { mbar_init(accfull_bar(b), 1); mbar_init(accempty_bar(b), k2 ? 8 : 4); }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 2) {
+        if constexpr (k2) tmem_alloc_pair<512>(smem_u32(tmem_slot));
+        else tmem_alloc<512>(smem_u32(tmem_slot));
+    }
     int* cum = reinterpret_cast<int*>(smem + OFF_GRP);    // grouped: units of experts < e
     int* off = cum + (MAX_G + 1);                         // grouped: first row of expert e
     if constexpr (kGrouped) {
@@ -258,6 +287,11 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (elect_one()) {
                     const uint32_t st = sbase + s * STAGE;
                     const int kc = (tl.kb0 + kb) * BK;
+                    if constexpr (k2) {
+                        if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (A_BYTES + B_BYTES / 2));
+                        tma_load_2d_pair(st, &tmA, full_bar(s), kc, m0);
+                        tma_load_2d_pair(st + A_BYTES, &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2));
+                    } else {
                     mbar_arrive_expect_tx(full_bar(s), A_BYTES + B_BYTES);
                     tma_load_2d(st, &tmA, full_bar(s), kc, m0);
                     if constexpr (kMc && kGrouped)
@@ -268,6 +302,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         tma_load_3d(st + A_BYTES, &tmB, full_bar(s), kc, n0, tl.e);
                     else
                         tma_load_2d(st + A_BYTES, &tmB, full_bar(s), kc, n0);
+                    }
                 }
                 __syncwarp();
             }
@@ -339,9 +374,21 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             *reinterpret_cast<uint4*>(sf + lane * 16) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
             *reinterpret_cast<uint4*>(sf + 512 + lane * 16) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
             *reinterpret_cast<uint4*>(sf + 1024 + lane * 16) = make_uint4(wb[4], wb[5], wb[6], wb[7]);
-            fence_proxy_async_smem();                       // generic writes -> the async proxy (tcgen05.cp)
+            // generic writes -> the async proxy (tcgen05.cp).  k2: the leader's tcgen05.cp.cta_group::2 reads
+            // this CTA's atoms, handed over through the leader's mbarrier: the cluster-wide proxy release
+            // fence for mbarrier-synchronised handoffs (a CTA-scope MEMBAR; a release.cluster arrive costs a
+            // GPU-scope MEMBAR per K-block: 2238 against 2958 TFLOP/s on C1 Fprop)
+            if constexpr (k2) asm volatile("fence.proxy.async::generic.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+            else fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(full_bar(s));
+            if (lane == 0) {
+#if FP8BS_MX_2CTA_RELCL
+                if constexpr (k2) mbar_arrive_release_cluster(mapa_shared(full_bar(s), 0));
+#else
+                if constexpr (k2) mbar_arrive_cluster(full_bar(s) & kPeerBitMask);
+#endif
+                else mbar_arrive(full_bar(s));
+            }
 #pragma unroll
             for (int d = 0; d < PF; ++d) {
                 have[d] = have[d + 1];
@@ -353,7 +400,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
     } else if (warp == 2) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc0 = idesc_mx(BM, BN, 0);
+        if (k2 && rank != 0) goto done;                 // k2: the leader issues for the pair
+        constexpr uint32_t idesc0 = idesc_mx(k2 ? 2 * BM : BM, BN, 0);
         int it = 0, tl = 0;
         for (int t = cid; t < ntiles; t += ncl, ++tl) {
             const int b = tl & 1;
@@ -363,30 +411,52 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tc_fence_after();
             const uint32_t d = tmem_base + ACC_COLS * b;
             if (kGW && kbn == 0) {                      // expert without tokens: no MMAs; the epilogue writes 0
-                if (elect_one()) mma_commit(accfull_bar(b));
+                if (elect_one()) {
+                    if constexpr (k2) mma_commit_pair(accfull_bar(b), 3);
+                    else mma_commit(accfull_bar(b));
+                }
                 __syncwarp();
                 continue;
             }
             for (int kb = 0; kb < kbn; ++kb, ++it) {
                 const int s = it % STAGES;
+#if FP8BS_MX_2CTA_RELCL
+                if constexpr (k2) mbar_wait_acquire_cluster(full_bar(s), (it / STAGES) & 1);
+                else
+#endif
                 mbar_wait(full_bar(s), (it / STAGES) & 1);
+                if constexpr (k2) asm volatile("fence.proxy.async::generic.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t st = sbase + s * STAGE;
                     const uint32_t sf = st + A_BYTES + B_BYTES;
-                    tmem_cp_atom(tmem_base + SF_COL, cp_desc(sf));
-                    tmem_cp_atom(tmem_base + SF_COL + 4, cp_desc(sf + 512));
-                    tmem_cp_atom(tmem_base + SF_COL + 8, cp_desc(sf + 1024));
+                    if constexpr (k2) {
+                        tmem_cp_atom_pair(tmem_base + SF_COL, cp_desc(sf));
+                        tmem_cp_atom_pair(tmem_base + SF_COL + 4, cp_desc(sf + 512));
+                        tmem_cp_atom_pair(tmem_base + SF_COL + 8, cp_desc(sf + 1024));
+                    } else {
+                        tmem_cp_atom(tmem_base + SF_COL, cp_desc(sf));
+                        tmem_cp_atom(tmem_base + SF_COL + 4, cp_desc(sf + 512));
+                        tmem_cp_atom(tmem_base + SF_COL + 8, cp_desc(sf + 1024));
+                    }
                     const uint64_t ad = sdesc_k_sw128(st), bd = sdesc_k_sw128(st + A_BYTES);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint32_t id = idesc0 | ((uint32_t)k << 4) | ((uint32_t)k << 29);
-                        mma_mx(d, ad + 2 * k, bd + 2 * k, id, tmem_base + SF_COL + ((uint32_t)k << 30),
-                               tmem_base + SF_COL + 4 + ((uint32_t)k << 30), (kb > 0 || k > 0) ? 1u : 0u);
+                        if constexpr (k2)
+                            mma_mx_pair(d, ad + 2 * k, bd + 2 * k, id, tmem_base + SF_COL + ((uint32_t)k << 30),
+                                        tmem_base + SF_COL + 4 + ((uint32_t)k << 30), (kb > 0 || k > 0) ? 1u : 0u);
+                        else
+                            mma_mx(d, ad + 2 * k, bd + 2 * k, id, tmem_base + SF_COL + ((uint32_t)k << 30),
+                                   tmem_base + SF_COL + 4 + ((uint32_t)k << 30), (kb > 0 || k > 0) ? 1u : 0u);
                     }
-                    if constexpr (kMc) mma_commit_mc(empty_bar(s));
+                    if constexpr (k2) mma_commit_pair(empty_bar(s), 3);
+                    else if constexpr (kMc) mma_commit_mc(empty_bar(s));
                     else mma_commit(empty_bar(s));
-                    if (kb == kbn - 1) mma_commit(accfull_bar(b));
+                    if (kb == kbn - 1) {
+                        if constexpr (k2) mma_commit_pair(accfull_bar(b), 3);
+                        else mma_commit(accfull_bar(b));
+                    }
                 }
                 __syncwarp();
             }
@@ -417,7 +487,10 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (c == BN / 32 - 1) {              // the accumulator is in registers: free it
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(accempty_bar(b));
+                    if (lane == 0) {
+                        if (k2 && rank != 0) mbar_arrive_cluster(accempty_bar(b) & kPeerBitMask);   // the leader's
+                        else mbar_arrive(accempty_bar(b));
+                    }
                 }
                 if (zero) {
                     if (p.accumulate) continue;      // D += 0
@@ -478,9 +551,11 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 done:
     tc_fence_before();
     __syncthreads();
+    if constexpr (k2) cluster_sync();           // no CTA leaves while the pair may still arrive on it / use its TMEM
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if constexpr (k2) tmem_dealloc_pair<512>(tmem_base);
+        else tmem_dealloc<512>(tmem_base);
     }
 }
 
