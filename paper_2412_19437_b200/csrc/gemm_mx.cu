@@ -197,7 +197,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // k2: the pair runs 2-CTA MMAs issued by the leader: each CTA stages its A rows and HALF of the B tile
     // (TMA completing on the leader's full barrier), its SF atoms (own rows' SFA, all columns' SFB), and
     // the leader's commits free both CTAs' stages and hand both CTAs their accumulator rows
-    constexpr bool k2 = kMc && !kGrouped && FP8BS_MX_2CTA;
+    constexpr bool k2 = kMc && FP8BS_MX_2CTA;
     const uint32_t rank = kMc ? cluster_ctarank() : 0;
     const int cid = kMc ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, ncl = kMc ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     if (threadIdx.x == 0) {
@@ -290,7 +290,10 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     if constexpr (k2) {
                         if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (A_BYTES + B_BYTES / 2));
                         tma_load_2d_pair(st, &tmA, full_bar(s), kc, m0);
-                        tma_load_2d_pair(st + A_BYTES, &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2));
+                        if constexpr (kGrouped)
+                            tma_load_3d_pair(st + A_BYTES, &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2), tl.e);
+                        else
+                            tma_load_2d_pair(st + A_BYTES, &tmB, full_bar(s), kc, n0 + (int)rank * (BN / 2));
                     } else {
                     mbar_arrive_expect_tx(full_bar(s), A_BYTES + B_BYTES);
                     tma_load_2d(st, &tmA, full_bar(s), kc, m0);
@@ -322,7 +325,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // 1187 TFLOP/s became 2254 with constant atoms)
         // kGW: tiles have different K-block counts, so the CTA's global iteration `it` is mapped to
         // (tile, K-block) with a cursor that only moves forward (load() is called with increasing it)
-        int cur_t = cid, cur_base = 0;
+        int cur_t = kGW ? cid : -1, cur_base = 0;
+        MxTile cur_tl;
         auto load = [&](int it, float* fa, float* fb) -> bool {
             int t, kb;
             MxTile tl;
@@ -339,7 +343,10 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             } else {
                 t = cid + (it / p.KB) * ncl; kb = it % p.KB;
                 if (t >= ntiles) return false;
-                decode(t, tl);
+                // the tile changes every KB K-blocks: decode it once (the grouped decode is a binary
+                // search over the experts in shared memory)
+                if (t != cur_t) { decode(t, cur_tl); cur_t = t; }
+                tl = cur_tl;
             }
             (void)t;
             const int m0 = tl.m0, n0 = tl.n0;
@@ -572,10 +579,14 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         const uint32_t box[2] = {BK, BM};
         if (!make_tmap(&tA, TMAP_U8, 2, a.A, dims, str, box, 128)) { *detail = "tensor map A"; return cudaErrorInvalidValue; }
     }
+    // grouped (Fprop / Dgrad): CTA pairs (2-CTA MMAs over 256-row units of one expert) when the experts
+    // average at least 256 rows (C4); otherwise unpaired: a pair shares one expert's n tile over 2 x 128
+    // rows, and at the small-expert MoE shapes that left the second CTA idle (C2: 810 vs 1234 TFLOP/s)
+    const bool gpair = a.grouped && !gw && FP8BS_MX_MC && FP8BS_MX_2CTA && a.M / (a.G > 0 ? a.G : 1) >= 256;
     if (a.grouped && !gw) {   // B [G][N][K], contiguous
         const uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         const uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
-        const uint32_t box[3] = {BK, BN, 1};   // grouped runs unpaired (below)
+        const uint32_t box[3] = {BK, gpair ? BN / 2 : BN, 1};
         if (!make_tmap(&tB, TMAP_U8, 3, a.B, dims, str, box, 128)) { *detail = "tensor map B (grouped)"; return cudaErrorInvalidValue; }
     } else {
         const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
@@ -598,7 +609,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     // Grouped runs without CTA pairs: a pair shares one expert's n tile over 2 x 128 rows, and at the
     // MoE shapes most experts have <= 128 rows, which left the second CTA idle (C2: 810 vs 1234
     // TFLOP/s unpaired).
-    const int MC = (FP8BS_MX_MC && (!a.grouped || gw)) ? 2 : 1;
+    const int MC = (FP8BS_MX_MC && (!a.grouped || gw || gpair)) ? 2 : 1;
     p.num_m = (int)((a.M + BM * MC - 1) / (BM * MC)); p.num_n = (int)((a.N + BN - 1) / BN);   // m units of MC tiles
     p.rast_n = FP8BS_MX_NFAST == 2 ? (a.M > a.N ? 1 : 0) : FP8BS_MX_NFAST;
     {
@@ -644,11 +655,12 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
         if (e != cudaSuccess) return e;
         return cudaPeekAtLastError();
     }
-    auto kern = a.grouped ? (a.out_f32 ? k_gemm_mx<true, false, true, false> : k_gemm_mx<false, false, true, false>)
+    auto kern = a.grouped ? (gpair ? (a.out_f32 ? k_gemm_mx<true, kMc, true, false> : k_gemm_mx<false, kMc, true, false>)
+                                   : (a.out_f32 ? k_gemm_mx<true, false, true, false> : k_gemm_mx<false, false, true, false>))
                           : (a.out_f32 ? k_gemm_mx<true, kMc, false, false> : k_gemm_mx<false, kMc, false, false>);
     const int smem = a.grouped ? SMEM_G : SMEM;
-    static bool attr[4][64] = {{false}};
-    const int ki = (a.out_f32 ? 1 : 0) + (a.grouped ? 2 : 0);
+    static bool attr[6][64] = {{false}};
+    const int ki = (a.out_f32 ? 1 : 0) + (a.grouped ? (gpair ? 4 : 2) : 0);
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr[ki][dev]) {

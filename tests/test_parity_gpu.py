@@ -571,11 +571,13 @@ def grouped_case_pow2(counts, N, K, seed=0):
     return offsets, qa, sa, qb, sb
 
 
+# experts averaging >= 256 rows run on CTA pairs with 2-CTA block-scaled MMAs ("two256", "big-ragged")
 GROUPED_MX_COUNTS = [[0, 7, 130, 1, 64, 0, 300], [256, 256], [3], [0, 0, 257],
-                     [int(c) for c in torch.randint(0, 200, (40,), generator=torch.Generator().manual_seed(5))]]
+                     [int(c) for c in torch.randint(0, 200, (40,), generator=torch.Generator().manual_seed(5))],
+                     [300, 700, 0, 513, 1024, 33]]
 
 
-@pytest.mark.parametrize("counts", GROUPED_MX_COUNTS, ids=["mixed", "two256", "three", "lead0", "e40"])
+@pytest.mark.parametrize("counts", GROUPED_MX_COUNTS, ids=["mixed", "two256", "three", "lead0", "e40", "big-ragged"])
 def test_grouped_mx_vs_dense_mx_bitwise_and_oracle(counts):
     """MoE expert Fprop on UE8M0 block scaling (fp8bs_grouped_gemm_mx), power-of-two scales: per
     expert bitwise equal to the dense fp8bs_gemm_mx on its segment (experts ending inside a 32-row
@@ -597,7 +599,7 @@ def test_grouped_mx_vs_dense_mx_bitwise_and_oracle(counts):
     assert torch.equal(Db.cpu().view(torch.int16), D.cpu().to(torch.bfloat16).view(torch.int16))
 
 
-@pytest.mark.parametrize("counts", [[0, 1, 300, 128, 257, 0, 40], [700]], ids=["ragged", "one"])
+@pytest.mark.parametrize("counts", [[0, 1, 300, 128, 257, 0, 40], [700], [600, 0, 257, 1300]], ids=["ragged", "one", "big-pairs"])
 def test_grouped_dgrad_mx_closed_form_bitexact(counts):
     """MoE expert Dgrad on UE8M0 block scaling (fp8bs_grouped_gemm_dgrad_mx, NEXT-1): closed-form
     operands (codes {0, +-1, +-2}, power-of-two scales) keep every product and sum exact, so each

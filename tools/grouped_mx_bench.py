@@ -27,7 +27,8 @@ def main():
     dev = "cuda"
     g = torch.Generator(device="cpu").manual_seed(0)
     G, N, K = 256, 2048, 7168
-    for name, R, skew in (("C4 skewed 65536 rows", 65536, True), ("C2 uniform 32768 rows", 32768, False)):
+    for name, R, skew in (("C4 skewed 524288 rows", 524288, True), ("C4 skewed 65536 rows", 65536, True),
+                          ("C2 uniform 32768 rows", 32768, False)):
         w = torch.rand(G, generator=g) ** (3.0 if skew else 0.0) + 0.05
         counts = torch.floor(w / w.sum() * R).long()
         counts[0] += R - int(counts.sum())
