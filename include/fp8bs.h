@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FP8BS_ABI_VERSION 2   /* 2: fp8bs_grouped_gemm{,_dgrad} require their workspace */
+#define FP8BS_ABI_VERSION 3   /* 2: fp8bs_grouped_gemm{,_dgrad} require their workspace; 3: so do the _mx forms */
 
 #if defined(__GNUC__)
 #define FP8BS_API __attribute__((visibility("default")))
@@ -242,13 +242,17 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N,
                                 void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
 /* ---- grouped_gemm_mx: the MoE expert Fprop on UE8M0 block scaling (NEXT-1) -----
- * fp8bs_grouped_gemm's arguments, layouts and validation (it takes no workspace), with fp8bs_gemm_mx's
- * precondition: every sA and sB value is an exact power of two in [2^-127, 2^127] (e.g. from
- * fp8bs_quantize_act_dual_pow2 / fp8bs_quantize_weight_128x128_pow2).  No promotion step. */
+ * fp8bs_grouped_gemm's arguments, layouts, validation and workspace (ABI 3: at least
+ * fp8bs_grouped_gemm_workspace_size bytes; the call zeroes its first 4 bytes on `stream` and uses them
+ * as the tile claim counter), with fp8bs_gemm_mx's precondition: every sA and sB value is an exact
+ * power of two in [2^-127, 2^127] (e.g. from fp8bs_quantize_act_dual_pow2 /
+ * fp8bs_quantize_weight_128x128_pow2).  No promotion step; experts averaging >= 256 rows run on CTA
+ * pairs with 2-CTA block-scaled MMAs. */
 FP8BS_API fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                    const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                    const uint8_t* B, const float* sB,
-                                   void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream);
+                                   void* D, fp8bs_dtype ddt, int64_t ldd,
+                                   void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 FP8BS_API size_t fp8bs_grouped_gemm_workspace_size(int32_t G, int64_t total_M, int64_t N, int64_t K);
 
 /* ---- grouped_gemm_scatter: the MoE expert Fprop with the combine's send fused into its epilogue ----
@@ -386,12 +390,13 @@ FP8BS_API fp8bs_status fp8bs_grouped_gemm_swiglu(int32_t G, int64_t total_M, int
                                        void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
 /* ---- grouped_gemm_dgrad_mx: the MoE expert Dgrad on UE8M0 block scaling (NEXT-1) ----------------
- * fp8bs_grouped_gemm_dgrad's arguments and layouts (it takes no workspace), with fp8bs_gemm_mx's
- * precondition: every sA and sB value an exact power of two in [2^-127, 2^127]. */
+ * fp8bs_grouped_gemm_dgrad's arguments, layouts and workspace (as fp8bs_grouped_gemm_mx), with
+ * fp8bs_gemm_mx's precondition: every sA and sB value an exact power of two in [2^-127, 2^127]. */
 FP8BS_API fp8bs_status fp8bs_grouped_gemm_dgrad_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                          const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                          const uint8_t* B, const float* sB,
-                                         void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream);
+                                         void* D, fp8bs_dtype ddt, int64_t ldd,
+                                         void* workspace, size_t workspace_bytes, fp8bs_stream_t stream);
 
 /* ---- Grouped MoE expert Wgrad (NEXT-3) ------------------------------------------
  * dW_e [N, K] = sum over expert e's tokens t of dY[t, :]^T X[t, :]   (P:476-481 applied per expert;

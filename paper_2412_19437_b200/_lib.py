@@ -111,7 +111,7 @@ def _load(path: str) -> ctypes.CDLL:
     if hasattr(L, "fp8bs_grouped_gemm_mx"):
         L.fp8bs_grouped_gemm_mx.restype = st
         L.fp8bs_grouped_gemm_mx.argtypes = [ctypes.c_int32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, vp, i32,
-                                            i64, vp]
+                                            i64, vp, ctypes.c_size_t, vp]
     if hasattr(L, "fp8bs_grouped_gemm_dgrad_mx"):
         L.fp8bs_grouped_gemm_dgrad_mx.restype = st
         L.fp8bs_grouped_gemm_dgrad_mx.argtypes = L.fp8bs_grouped_gemm_mx.argtypes
@@ -445,17 +445,15 @@ def grouped_gemm(offsets: torch.Tensor, A: torch.Tensor, sA: torch.Tensor, B: to
         out = torch.empty(R, N, dtype=out_dtype, device=A.device)
     if layout not in (FPROP, DGRAD):
         raise ValueError("grouped layouts: FPROP, DGRAD")
+    if workspace is None:   # the tile table / claim counter (torch's caching allocator makes this cheap per call)
+        wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K))
+        workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
     if mx:   # power-of-two scales on UE8M0 block scaling (fp8bs_grouped_gemm_mx / _dgrad_mx)
         fn, name = ((lib().fp8bs_grouped_gemm_mx, "fp8bs_grouped_gemm_mx") if layout == FPROP
                     else (lib().fp8bs_grouped_gemm_dgrad_mx, "fp8bs_grouped_gemm_dgrad_mx"))
-        _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB), _p(out), _dt(out),
-                  out.stride(0), _stream(A)), name)
-        return out
-    fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
-                else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))
-    if workspace is None:   # the tile table (torch's caching allocator makes this cheap per call)
-        wsb = int(lib().fp8bs_grouped_gemm_workspace_size(G, R, N, K))
-        workspace = torch.empty((wsb + 15) // 16 * 16, dtype=torch.uint8, device=A.device)
+    else:
+        fn, name = ((lib().fp8bs_grouped_gemm, "fp8bs_grouped_gemm") if layout == FPROP
+                    else (lib().fp8bs_grouped_gemm_dgrad, "fp8bs_grouped_gemm_dgrad"))
     _check(fn(G, R, N, K, _p(offsets), _p(A), A.stride(0), _p(sA), sA.stride(0), _p(B), _p(sB),
               _p(out), _dt(out), out.stride(0), _p(workspace), workspace.numel(), _stream(A)), name)
     return out

@@ -329,15 +329,19 @@ fp8bs_status fp8bs_grouped_gemm(int32_t G, int64_t total_M, int64_t N, int64_t K
 fp8bs_status fp8bs_grouped_gemm_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                    const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                    const uint8_t* B, const float* sB,
-                                   void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream) {
-    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1);
+                                   void* D, fp8bs_dtype ddt, int64_t ldd,
+                                   void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    return grouped_gemm_layout(FP8BS_FPROP, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1,
+                               workspace, workspace_bytes);
 }
 
 fp8bs_status fp8bs_grouped_gemm_dgrad_mx(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
                                          const uint8_t* A, int64_t lda, const float* sA, int64_t ldsA,
                                          const uint8_t* B, const float* sB,
-                                         void* D, fp8bs_dtype ddt, int64_t ldd, fp8bs_stream_t stream) {
-    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1);
+                                         void* D, fp8bs_dtype ddt, int64_t ldd,
+                                         void* workspace, size_t workspace_bytes, fp8bs_stream_t stream) {
+    return grouped_gemm_layout(FP8BS_DGRAD, G, total_M, N, K, offsets, A, lda, sA, ldsA, B, sB, D, ddt, ldd, stream, 1,
+                               workspace, workspace_bytes);
 }
 
 fp8bs_status fp8bs_grouped_gemm_dgrad(int32_t G, int64_t total_M, int64_t N, int64_t K, const int64_t* offsets,
@@ -378,7 +382,7 @@ static fp8bs_status grouped_gemm_layout(int layout, int32_t G, int64_t total_M, 
     if (c != FP8BS_OK) return c;
     if (total_M == 0 || N == 0) return ok();
     if (K % 16) return fail(FP8BS_ERR_ALIGN, "K must be a multiple of 16");
-    if (!mx) {
+    {   /* the tile table (promotion kernel) or the tile claim counter (UE8M0 kernel) */
         const size_t need = grouped_workspace_bytes(G, total_M, N);
         if (!workspace || workspace_bytes < need)
             return fail(FP8BS_ERR_INVALID_ARG, "workspace of %zu bytes needed (fp8bs_grouped_gemm_workspace_size), got %zu%s",

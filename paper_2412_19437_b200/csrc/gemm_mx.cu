@@ -76,10 +76,12 @@ constexpr int STAGE = ((A_BYTES + B_BYTES + SF_BYTES + 1023) / 1024) * 1024;
 constexpr int EPI_WARP = EPIBUF * 32 * 128;      // 32 rows x 128 B staging buffers per epilogue warp
 constexpr int OFF_EPI = STAGES * STAGE;
 constexpr int OFF_BAR = OFF_EPI + 4 * EPI_WARP;
-constexpr int NBAR = 2 * STAGES + 4;             // full, empty, accfull[2], accempty[2]
-constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
-constexpr int MAX_G = 1024;                       // grouped: cum[G + 1], off[G + 1] after the barriers
-constexpr int OFF_GRP = OFF_BAR + NBAR * 8 + 16;
+constexpr int kTQ = 4;                           // grouped: ring of dynamically claimed tile indices
+constexpr int NBAR = 2 * STAGES + 4 + 2 * kTQ;   // full, empty, accfull[2], accempty[2], tqfull, tqempty
+constexpr int OFF_TQ = OFF_BAR + NBAR * 8 + 16;  // (after the barriers and the TMEM address)
+constexpr int SMEM = 1024 + OFF_TQ + kTQ * 4;
+constexpr int MAX_G = 1024;                       // grouped: cum[G + 1], off[G + 1] after the ring
+constexpr int OFF_GRP = OFF_TQ + 16;
 constexpr int SMEM_G = 1024 + OFF_GRP + 2 * (MAX_G + 1) * 4;
 static_assert(SMEM_G <= 232448, "shared memory");
 constexpr int NSF = STAGES;                      // scale-factor warps 1, 3, 8, 9: warp k owns stage k
@@ -96,6 +98,7 @@ struct Params {
     // grouped (MoE expert Fprop): rows [offsets[e], offsets[e+1]) of A use B[e], sB + e * sb_expert_stride
     int G; const int64_t* offsets; int64_t sb_expert_stride;
     void* D; int64_t ldd;                       // rows crossing an expert's end are stored directly
+    int* claim;                                 // grouped: the tile claim counter (caller's workspace, zeroed per launch)
 };
 
 // Tile order (as the promotion kernel's banded raster, gemm.cu get_tile_dense): the operand with fewer
@@ -188,6 +191,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto accfull_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
     auto accempty_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
+    auto tqfull_bar = [&](int q) { return bar0 + 8u * (2 * STAGES + 4 + q); };
+    auto tqempty_bar = [&](int q) { return bar0 + 8u * (2 * STAGES + 4 + kTQ + q); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + NBAR * 8);
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     // kMc: the two CTAs of a cluster take m tiles 2u and 2u + 1 of the same n tile; each loads its
@@ -205,6 +210,9 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // multicast commit; accempty = both CTAs' 4 epilogue warps
         for (int s = 0; s < STAGES; ++s) { mbar_init(full_bar(s), k2 ? 3 : 2); mbar_init(empty_bar(s), k2 ? 1 : MC); }
         for (int b = 0; b < 2; ++b) { mbar_init(accfull_bar(b), 1); mbar_init(accempty_bar(b), k2 ? 8 : 4); }
+        // grouped: each claimed index is read by 4 SF + 4 epilogue warps per CTA, the leader's MMA warp
+        // and the peer's producer (the leader's producer claims)
+        for (int q = 0; q < kTQ; ++q) { mbar_init(tqfull_bar(q), 1); mbar_init(tqempty_bar(q), kMc ? 18 : 9); }
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -245,6 +253,53 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int ntiles = kGrouped ? cum[p.G] : kGW ? p.G * p.num_m * p.num_n : p.num_m * p.num_n;
+    // Grouped: tiles are claimed dynamically, as in the promotion kernel (gemm.cu): the leader's producer
+    // claims the next unit index with an atomic, one ahead, and hands it to every role of both CTAs
+    // through a kTQ-entry ring (a static schedule let the persistent clusters drift apart and re-read
+    // A from DRAM: 24.2 GB per C4 launch against 7.6).  Every role reads index #j in order and
+    // releases the entry at once.  Dense / grouped Wgrad: the static schedule cid, cid + ncl, ...
+    uint32_t* tqv = reinterpret_cast<uint32_t*>(smem + OFF_TQ);
+    auto tq_publish = [&](int j) -> int {            // leader producer, one lane
+        const int q = j % kTQ;
+        mbar_wait(tqempty_bar(q), ((j / kTQ) & 1) ^ 1);
+        const int t = atomicAdd(p.claim, 1);
+        const uint32_t a = smem_u32(tqv + q);
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(a), "r"(t) : "memory");
+        mbar_arrive(tqfull_bar(q));
+        if constexpr (kMc) {
+            st_shared_cluster_u32(mapa_shared(a, 1), (uint32_t)t);
+            mbar_arrive_release_cluster(mapa_shared(tqfull_bar(q), 1));
+        }
+        return t;
+    };
+    auto tq_take = [&](int j) -> int {               // every other role, whole warp
+        const int q = j % kTQ;
+        mbar_wait_acquire_cluster(tqfull_bar(q), (j / kTQ) & 1);
+        const int t = (int)lds_u32(smem_u32(tqv + q));
+        __syncwarp();
+        if (elect_one()) {
+            if (kMc && rank != 0) mbar_arrive_release_cluster(tqempty_bar(q) & kPeerBitMask);
+            else mbar_arrive(tqempty_bar(q));
+        }
+        __syncwarp();
+        return t;
+    };
+    int t_next = 0;
+    auto tile_at = [&](int j) -> int {               // this role's tile #j (>= ntiles: none left)
+        if constexpr (!kGrouped) return cid + j * ncl;
+        else return tq_take(j);
+    };
+    auto tile_at_claim = [&](int j) -> int {         // the leader's producer: claims #j + 1 ahead
+        if constexpr (!kGrouped) return cid + j * ncl;
+        else {
+            int t = 0;
+            if (lane == 0) {
+                t = j == 0 ? tq_publish(0) : t_next;
+                if (t < ntiles) t_next = tq_publish(j + 1);
+            }
+            return __shfl_sync(0xffffffffu, t, 0);
+        }
+    };
     // unit t -> this CTA's tile: rows [m0, m0 + BM) (clipped at row_end), columns [n0, n0 + BN)
     auto decode = [&](int t, MxTile& tl) {
         if constexpr (kGrouped) {
@@ -277,7 +332,8 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // ---------------- TMA producer ----------------
         if (lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmD); }
         int it = 0;
-        for (int t = cid; t < ntiles; t += ncl) {
+        int jj = 0;
+        for (int t = rank == 0 ? tile_at_claim(0) : tile_at(0); t < ntiles; ++jj, t = rank == 0 ? tile_at_claim(jj) : tile_at(jj)) {
             MxTile tl;
             decode(t, tl);
             const int m0 = tl.m0, n0 = tl.n0;
@@ -327,6 +383,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // (tile, K-block) with a cursor that only moves forward (load() is called with increasing it)
         int cur_t = kGW ? cid : -1, cur_base = 0;
         MxTile cur_tl;
+        int sf_j = -1, sf_t = 0;                       // grouped: the last claimed index this warp read
         auto load = [&](int it, float* fa, float* fb) -> bool {
             int t, kb;
             MxTile tl;
@@ -341,7 +398,19 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 t = cur_t;
                 kb = tl.kb0 + (it - cur_base);
             } else {
-                t = cid + (it / p.KB) * ncl; kb = it % p.KB;
+                kb = it % p.KB;
+                if constexpr (kGrouped) {
+                    // walk the claimed indices in order up to tile #(it / KB) (every entry read once)
+                    const int jt = it / p.KB;
+                    while (sf_j < jt) {
+                        if (sf_t >= ntiles) return false;
+                        ++sf_j;
+                        sf_t = tq_take(sf_j);
+                    }
+                    t = sf_t;
+                } else {
+                    t = cid + (it / p.KB) * ncl;
+                }
                 if (t >= ntiles) return false;
                 // the tile changes every KB K-blocks: decode it once (the grouped decode is a binary
                 // search over the experts in shared memory)
@@ -410,7 +479,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (k2 && rank != 0) goto done;                 // k2: the leader issues for the pair
         constexpr uint32_t idesc0 = idesc_mx(k2 ? 2 * BM : BM, BN, 0);
         int it = 0, tl = 0;
-        for (int t = cid; t < ntiles; t += ncl, ++tl) {
+        for (int t = tile_at(0); t < ntiles; t = tile_at(++tl)) {
             const int b = tl & 1;
             int kbn = p.KB;
             if constexpr (kGW) { MxTile ti; decode(t, ti); kbn = ti.kbn; }
@@ -474,7 +543,7 @@ k_gemm_mx(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint32_t ebuf0 = sbase + OFF_EPI + (warp - 4) * EPI_WARP;
         int chunk = 0;                                  // running chunk count: alternates the two buffers
         int tl = 0;
-        for (int t = cid; t < ntiles; t += ncl, ++tl) {
+        for (int t = tile_at(0); t < ntiles; t = tile_at(++tl)) {
             const int b = tl & 1;
             MxTile ti;
             decode(t, ti);
@@ -621,6 +690,12 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     p.G = a.grouped ? a.G : 0; p.offsets = a.offsets; p.sb_expert_stride = (int64_t)((a.N + 127) / 128) * KB;
     if (gw) p.rast_n = 0;   // m fastest inside an expert (decode): its dYqT_e stays in L2 while XqT_e streams
     p.D = a.D; p.ldd = a.ldd;
+    p.claim = static_cast<int*>(a.workspace);
+    if (a.grouped && !gw) {                       // the claim counter starts at 0 every launch
+        if (!a.workspace) { *detail = "grouped UE8M0 GEMM without a workspace"; return cudaErrorInvalidValue; }
+        cudaError_t e0 = cudaMemsetAsync(a.workspace, 0, sizeof(int), st);
+        if (e0 != cudaSuccess) return e0;
+    }
     // grouped: an upper bound on the units (each expert adds at most one partial m unit per n tile)
     const int64_t units = gw ? (int64_t)a.G * p.num_m * p.num_n
                         : a.grouped ? (int64_t)(p.num_m + a.G) * p.num_n : (int64_t)p.num_m * p.num_n;

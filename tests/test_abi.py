@@ -15,7 +15,7 @@ def test_library_loads_and_exports_header_symbols():
     assert len(syms) >= 10
     for name in syms:
         assert hasattr(lib, name), name
-    assert fp.abi_version() == 2
+    assert fp.abi_version() == 3
 
 
 def test_product_library_exports_only_header_symbols():
