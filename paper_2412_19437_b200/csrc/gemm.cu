@@ -155,6 +155,9 @@ constexpr int kTsSlots = 12;
 #ifndef FP8BS_B_PREFETCH
 #define FP8BS_B_PREFETCH 0   // experiment: prefetch the next expert's weights into L2 at an expert's first tile (C4: -0.5%)
 #endif
+#ifndef FP8BS_FOLD
+#define FP8BS_FOLD 1           // grouped pair tiles whose expert ends in the first 128 rows run folded (M = 128)
+#endif
 #ifndef FP8BS_STATIC_SCHED
 #define FP8BS_STATIC_SCHED 0   // experiments: 1 = grouped tiles on the static schedule too (A/B builds)
 #endif
@@ -562,7 +565,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); tma_prefetch_desc(&tmSA); tma_prefetch_desc(&tmD);
-        if (kWgrad) tma_prefetch_desc(&tmSB);
+        if (kWgrad || (kGrouped && kPair)) tma_prefetch_desc(&tmSB);
     }
     if (warp == 2) {
         if constexpr (kPair) tmem_alloc_pair<C::TMEM_COLS>(smem_u32(tmem_slot));
@@ -591,6 +594,16 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // contraction blocks of a tile and their first block (grouped Wgrad and split-K tiles differ)
     auto nkb = [&](const Tile& tl) -> int { if constexpr (kKR) return tl.kbn; else return p.KB; };
     auto kbase = [&](const Tile& tl) -> int { if constexpr (kKR) return tl.kb0; else return 0; };
+    // Folded tiles (grouped Fprop/Dgrad on CTA pairs): a tile whose expert ends within its first 128
+    // rows is issued as tcgen05.mma.cta_group::2 with M = 128 (64 rows per CTA) instead of M = 256,
+    // which halves its MMA work and its promotion.  Each CTA's 64 x 128 accumulator of a half then lies
+    // folded over the 128 TMEM lanes in 64 columns: columns [0, 64) of the half in lanes 0..63,
+    // columns [64, 128) in lanes 64..127 (CUTLASS cute/atom/mma_traits_sm100.hpp, tmem_frg, the
+    // N_SM = 2, M_MMA = 64 "2x2" atom), so the warp of lane quadrant q promotes rows 32 (q & 1) + lane
+    // of the CTA's 64 and columns 64 (q >> 1) + [0, 64) of the half.
+    constexpr bool kFold = FP8BS_FOLD && kGrouped && kPair && !kWgrad && !kSwiglu && C::NC == 128;
+    auto folded = [&](const Tile& tl) -> bool { if constexpr (kFold) return tl.row_end - tl.row0 <= BM; else return false; };
+    auto cta_row0 = [&](const Tile& tl) -> int { return tl.row0 + (int)rank * (folded(tl) ? BM / 2 : BM); };
 
     // Tile order.  Dense: static, cluster c takes tiles c, c + ncl, ...  Grouped: dynamic — the
     // leader's producer thread claims the next tile index with an atomic on the workspace counter
@@ -697,8 +710,11 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             int j = 0;
             for (TileRef t = tix(0); next_tile(t, tl); t = tix(++j)) {
                 if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
-                const int arow = tl.row0 + (int)rank * BM;
+                const int arow = cta_row0(tl);
                 const int brow = tl.n0 + (int)rank * C::BH_ROWS;
+                // folded tiles load 64 rows of A per CTA, through the 64-row map the grouped launch passes
+                // in tmSB's place (the grouped Fprop/Dgrad has no per-column sB map)
+                const bool fold = folded(tl);
                 for (int kb = 0; kb < nkb(tl); ++kb, ++it) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
@@ -707,8 +723,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const int kc = ((kDbg & 4)) ? 0 : (kbase(tl) + kb) * BK;
                     if (elect_one()) {
                         if constexpr (kPair) {
-                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * (C::A_BYTES + tl.nh * C::BH_BYTES));
-                            tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
+                            if (rank == 0) mbar_arrive_expect_tx(full_bar(s), 2 * ((fold ? C::A_BYTES / 2 : C::A_BYTES) + tl.nh * C::BH_BYTES));
+                            if (fold) tma_load_2d_pair(sa, &tmSB, full_bar(s), kc, arow);
+                            else tma_load_2d_pair(sa, &tmA, full_bar(s), kc, arow);
                             for (int h = 0; h < tl.nh; ++h) {
                                 if constexpr (kGrouped && !kWgrad) tma_load_3d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN, tl.e);
                                 else tma_load_2d_pair(sa + C::A_BYTES + h * C::BH_BYTES, &tmB, full_bar(s), kc, brow + h * HN);
@@ -732,7 +749,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // N = 128 MMAs of a K-block (512 cycles at peak) need two issuers.  Each half has its own
             // two TMEM slots (2h, 2h + 1); a stage is released by one commit per half.
             const int h = warp - 1;
-            constexpr uint32_t idesc = idesc_e4m3_f32(C::ROWS, HN);
+            constexpr uint32_t idesc_full = idesc_e4m3_f32(C::ROWS, HN);
             int it = 0, qh = 0;
             Tile tl;
             int j = 0;
@@ -754,6 +771,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                     continue;
                 }
+                const uint32_t idesc = folded(tl) ? idesc_e4m3_f32(C::ROWS / 2, HN) : idesc_full;
                 for (int kb = 0; kb < nkb(tl); ++kb, ++it, ++qh) {
                     const int s = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
@@ -805,7 +823,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if constexpr (kGrouped && !kWgrad) { if (p.ready) wait_chunk_ready(p, tl.e); }
                 const float* sbp = p.sB;
                 if constexpr (kGrouped) sbp += (int64_t)tl.e * p.sb_expert_stride;
-                const int arow = tl.row0 + (int)rank * BM;
+                const int arow = cta_row0(tl);
                 const int nb0 = tl.n0 / 128;
                 for (int kb0 = 0; kb0 < nkb(tl); kb0 += 32) {
                     // lane j holds the 2 block scalars the tile's columns need at K-block kb0 + j
@@ -859,7 +877,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         int jt = 0;                                     // grouped Wgrad: tiles walked (KB varies per tile)
         auto next_j = [&]() -> int { if constexpr (kKR) return ++jt; else return sit / p.KB; };
         for (TileRef t = tile_index(0); next_tile(t, tl); t = tile_index(next_j())) {
-            const uint32_t sa_off = 4u * (((tl.row0 + (int)rank * BM) & 3) + row);   // this row's sA in a stage
+            const bool fold = folded(tl);
+            // this row's sA in a stage (folded: row 32 (quad & 1) + lane of the CTA's 64)
+            const uint32_t sa_off = 4u * ((cta_row0(tl) & 3) + (fold ? (quad & 1) * 32 + lane : row));
             const bool active = h < tl.nh;
             if (!active) {
                 // this half lies past N (last column tile): only keep the scale ring moving (the
@@ -932,7 +952,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                     }
                 };
-                const uint32_t ta = tbase + pb * HN;
+                const uint32_t ta = tbase + pb * HN;   // folded: the lane quadrant's 64 columns start here too
                 if ((kDbg & 8)) {     // experiment: no TMEM reads, no math
                     tc_fence_before();
                     __syncwarp();
@@ -945,17 +965,20 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 uint32_t r0[32], r1[32];
                 if constexpr (NC == 128) {
                     // two 64-column rounds: two tcgen05.ld in flight per wait; the slot is released as
-                    // soon as the second round has landed (32 FFMA2 after the first wait)
+                    // soon as the second round has landed (32 FFMA2 after the first wait).  Folded: one
+                    // round, the slot released before its math.
                     FP8BS_TMEM_LD32(ta, r0);
                     FP8BS_TMEM_LD32(ta + 32, r1);
                     tmem_ld_wait();
-                    fma32(r0, 0);
-                    fma32(r1, 32);
+                    if (!fold) {
+                        fma32(r0, 0);
+                        fma32(r1, 32);
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
-                    FP8BS_TMEM_LD32(ta + 64, r0);
-                    FP8BS_TMEM_LD32(ta + 96, r1);
-                    tmem_ld_wait();
+                        for (int j = 0; j < 64; ++j) asm volatile("" : "+f"(acc[j]));
+                        FP8BS_TMEM_LD32(ta + 64, r0);
+                        FP8BS_TMEM_LD32(ta + 96, r1);
+                        tmem_ld_wait();
+                    }
                 } else {
                     // 64 columns: one 32-column round, its math, then the second round
                     FP8BS_TMEM_LD32(ta, r0);
@@ -987,8 +1010,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     if (kTrace && warp == 7) FP8BS_TS(7, sit);
                 }
                 if constexpr (NC == 128) {
-                    fma32(r0, 64);
-                    fma32(r1, 96);
+                    if (fold) {
+                        fma32(r0, 0);
+                        fma32(r1, 32);
+                    } else {
+                        fma32(r0, 64);
+                        fma32(r1, 96);
+                    }
                 } else {
                     fma32(r1, 32);
                 }
@@ -1024,13 +1052,13 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
             }
             // ---------------- epilogue ----------------
-            const int arow = (kKR ? tl.orow0 : tl.row0) + (int)rank * BM;   // output rows
+            const int arow = kKR ? tl.orow0 + (int)rank * BM : cta_row0(tl);   // output rows
             // Each warp owns 32 rows x 128 columns.  It stages 128-byte-wide column chunks (32 FP32 or
             // 64 BF16 columns) in its own SWIZZLE_128B buffer and writes them with asynchronous TMA
             // stores (reduce-add for Wgrad's D += acc): a warp store used to touch 32 rows at once.
             // TMA clips rows >= M and columns >= N; a grouped warp whose 32 rows cross the expert's
             // end stores its rows directly (rows past row_end belong to the next expert).
-            const int grow0 = arow + quad * 32;
+            const int grow0 = arow + (fold ? (quad & 1) : quad) * 32;
             const int rows_here = tl.row_end - grow0;
             if constexpr (kSwiglu) {
                 static_assert(NC == 128 && C::EPI_BUFS == 1, "SwiGLU epilogue: 8 promotion warps, one staging buffer each");
@@ -1066,6 +1094,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
 #pragma unroll
                 for (int c = 0; c < NC / CW; ++c) {
+                    if (fold && c >= NC / CW / 2) break;         // folded: 64 columns per warp
                     const uint32_t ebuf = ebuf0 + (c % C::EPI_BUFS) * (32 * 128);
                     // the store that last used this buffer has read it
                     if (lane == 0) bulk_wait_group_read<C::EPI_BUFS - 1>();
@@ -1085,7 +1114,7 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                         sts_u32x4(ebuf + lane * 128 + ((u ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
-                    const int col = (kSplit ? 0 : tl.n0) + h * HN + gg * NC + c * CW;   // split: the unit's slab
+                    const int col = (kSplit ? 0 : tl.n0) + h * HN + gg * NC + (fold ? (quad >> 1) * 64 : 0) + c * CW;   // split: the unit's slab
                     if (kGrouped && !full) {
                         __syncwarp();
                         const int nr = rows_here < 32 ? rows_here : 32;
@@ -1262,6 +1291,14 @@ static cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t st, const char** d
         uint32_t box[2] = {(uint32_t)BN, 1};
         if (!make_map(&tSB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a.sB, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) {
             *detail = "cuTensorMapEncodeTiled failed for sB"; return cudaErrorInvalidValue;
+        }
+    } else if (kGrouped && kPair) {
+        // folded tiles (M = 128 over the pair): A with a 64-row box, passed in tmSB's place
+        uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)rows};
+        uint64_t str[1] = {(uint64_t)a.lda};
+        uint32_t box[2] = {BK, BM / 2};
+        if (!make_map(&tSB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a.A, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            *detail = "cuTensorMapEncodeTiled failed for A (64-row box)"; return cudaErrorInvalidValue;
         }
     } else {
         tSB = tSA;
