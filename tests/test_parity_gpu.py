@@ -42,7 +42,7 @@ def variant(request):
 
 
 def assert_bits_equal(got: torch.Tensor, want: torch.Tensor, what: str):
-    got = got.cpu()
+    got, want = got.cpu(), want.cpu()
     if got.dtype == torch.float32:
         got, want = got.view(torch.int32), want.view(torch.int32)
     bad = (got != want).nonzero()
@@ -362,7 +362,12 @@ def grouped_case(counts, N, K, seed=0):
     return offsets, qa, sa, qb, sb
 
 
-@pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [128, 128, 128], [5], [0, 0, 257]])
+# "fold": expert ends on both sides of the folded-tile boundary (a CTA-pair tile whose expert ends within
+# its first 128 rows runs as an M = 128 MMA, 64 rows per CTA; gemm.cu kFold)
+GROUPED_COUNTS = [[0, 7, 130, 1, 64, 0, 300], [128, 128, 128], [5], [0, 0, 257], [127, 128, 129, 255, 320, 384, 385]]
+
+
+@pytest.mark.parametrize("counts", GROUPED_COUNTS, ids=["mixed", "three128", "five", "lead0", "fold"])
 def test_grouped_vs_dense_bitwise_and_oracle(counts, variant):
     N, K = 264, 512
     offsets, qa, sa, qb, sb = grouped_case(counts, N, K)
@@ -377,9 +382,13 @@ def test_grouped_vs_dense_bitwise_and_oracle(counts, variant):
         assert_bits_equal(D[a:b], De.cpu(), f"expert {e}")
     O = oracle.grouped_gemm(offsets, qa, sa, qb, sb)
     assert oracle.rel_err_normwise(D.cpu().double(), O) <= TOL
+    # BF16 output (the bench's) is the RNE of the FP32 output, folded tiles included
+    Db = fp.grouped_gemm(dev(offsets), dev(qa), dev_scales(sa), dev(qb), dev(sb), out_dtype=torch.bfloat16)
+    assert_bits_equal(Db, D.to(torch.bfloat16), "bf16 == RNE(fp32)")
 
 
-@pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [256, 256], [3]])
+@pytest.mark.parametrize("counts", [[0, 7, 130, 1, 64, 0, 300], [256, 256], [3], [127, 128, 129, 255, 320, 384, 385]],
+                         ids=["mixed", "two256", "three", "fold"])
 def test_grouped_dgrad_vs_dense_bitwise_and_oracle(counts, variant):
     """MoE expert Dgrad (fp8bs_grouped_gemm_dgrad): per expert, dX_e = dY_e (1x128 along the expert's
     output channels) x W_e through WqT_e and the expert's sW read [out-block][in-block]; bitwise equal to
