@@ -1489,9 +1489,14 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
     v = g_forced_variant;
 #endif
     if (v < 1 || v > 2) {
-        // ~128-row experts / small M would waste half of a 256-row pair tile -> one CTA per tile
-        // (grouped Wgrad: a.M is one expert's output rows — the dense per-expert choice)
-        if (a.grouped && a.layout != 2) v = (a.M / (a.G > 0 ? a.G : 1) >= 256) ? 2 : 1;
+        // grouped Fprop/Dgrad: pairs from 128 rows per expert on average (an expert ending within a
+        // pair tile's first 128 rows runs it folded, at half the MMA work).  Measured with uniform top-8
+        // routing over 256 experts, K = 7168, N = 2048 (tools/gemm_matrix.py, r02; one CTA / pair, us):
+        // 112 rows per expert 669-687 / 727-746; 128: 815-966 / 788-845 (box to box); 144: 988-1200 /
+        // 922; 160: 1128-1242 / 943; 192: 1268-1370 / 893-936; 224: 1286-1383 / 898-1012; 256:
+        // 1295-1314 / 1157-1166.  The SwiGLU epilogue has no folded tiles: pairs only from 256 rows.
+        // (Grouped Wgrad: a.M is one expert's output rows — the dense per-expert choice.)
+        if (a.grouped && a.layout != 2) v = (a.M / (a.G > 0 ? a.G : 1) >= (a.swiglu ? 256 : 128)) ? 2 : 1;
         else v = (a.M <= 128) ? 1 : 2;
     }
     return v == 1 ? launch_v<false>(a, st, detail) : launch_v<true>(a, st, detail);

@@ -73,6 +73,18 @@ def main():
     o2 = offs.to(dev)
     out2 = torch.empty(R, N2, dtype=torch.bfloat16, device=dev)
     cases.append(("grouped_C2", 2.0 * R * N2 * K2, lambda: fp.grouped_gemm(o2, A2, sA2, B2, sB2, out=out2)))
+    for T2 in [int(t) for t in os.environ.get("GROUPED_T", "2048,8192").split(",")]:
+        # ~64 and ~256 rows per expert (uniform): where the one-CTA / pair variant choice flips
+        name = f"grouped_T{T2}"
+        if only and name not in only:
+            continue
+        _, offsT = W.group_rows(W.route_uniform(T2, E, 8), E)
+        RT = int(offsT[-1])
+        AT = torch.randint(0, 120, (RT, K2), dtype=torch.uint8, device=dev)
+        sAT = torch.rand(K2 // 128, RT, device=dev)
+        oT = offsT.to(dev)
+        outT = torch.empty(RT, N2, dtype=torch.bfloat16, device=dev)
+        cases.append((name, 2.0 * RT * N2 * K2, (lambda oT=oT, AT=AT, sAT=sAT, outT=outT: fp.grouped_gemm(oT, AT, sAT, B2, sB2, out=outT))))
     if only and "grouped_C4" in only:
         # C4 at one GPU: 65536 tokens x top-8, skewed routing (alpha 0.5), all 256 experts
         _, offs4 = W.group_rows(W.route_skewed(65536, E, 8), E)
