@@ -1410,26 +1410,27 @@ cudaError_t launch_quant_weight_128x128(const void* w, int wdt, int64_t N, int64
 // FP8 -> FP8 re-quantization of a cached activation: 1x128 codes + scales -> dequantize -> 128x1
 // (§3.3.3, §3.5.2: the forward's FP8 activations are "read out,
 // dequantized, transposed, re-quantized into 128x1 tiles" for the backward pass).
-// One CTA per 128-token x 128-channel tile (exactly one 1x128 scale group per row).  Thread
-// (wc = tid & 31, rg = tid >> 5): 4 channels (one 32-bit code word) x 8 tokens, 16 warps per CTA.  Dequantized value
-// xhat = RN32(dec(q) * s) (E4M3 -> FP16 -> FP32 is exact, one rounded FP32 multiply); column amax
-// over the tile's 128 tokens via shared memory; codes staged per channel in shared memory and written
-// as 128-byte qT row segments.
+// Work unit: a 128-token x 128-channel tile (exactly one 1x128 scale group per row).  Dequantized
+// value xhat = RN32(dec(q) * s) (E4M3 -> FP16 -> FP32 is exact, one rounded FP32 multiply).
 // ===========================================================================================
 namespace fp8bs {
-// Persistent, TMA-fed: a producer warp streams 128-token x 128-channel code tiles (16 KB) into a
-// 4-stage ring; 8 consumer warps (thread: 4 channels = one code word x 16 tokens) dequantize, reduce
-// the column amax through shared memory, encode, stage the codes per channel and write 128-byte qT
-// row segments.  2 CTAs per SM.
+// Persistent, TMA-fed: lane 0 of warp 0 streams 128-token x 128-channel code tiles (16 KB, SWIZZLE_128B)
+// into a 4-stage ring.  Each of the 8 warps owns 16 channels (one 16-byte chunk of every
+// row) over all 128 tokens, so a channel's 128x1 amax is a warp reduction and the consumers never
+// wait on each other (the previous form, 16 tokens x 4 channels per thread with a shared-memory
+// reduction, paid three CTA barriers per tile).  Lane (cg = lane & 3, tg = lane >> 2): channels
+// 16w + 4cg + [0, 4) of tokens 16tg + [0, 16).  A lane walks its 16 tokens rotated by tg (token
+// 16tg + ((r + tg) & 15) at step r), so the 8 token groups of one ld.shared hit 8 different swizzled
+// 16-byte chunks (no bank conflicts); the channel's 16 codes, packed in that rotated order, are
+// rotated back by tg bytes and stored as one 16-byte run of qT (a warp store covers 4 channels x
+// 128 tokens).  2 CTAs per SM.
 struct RQCfg {
-    static constexpr int STAGES = 4, CONSUMERS = 8, THREADS = 32 * (CONSUMERS + 1);
+    // no separate producer warp: 288 threads would allocate registers as for 320 and leave one CTA
+    // per SM; lane 0 of warp 0 issues the TMA loads, STAGES - 1 tiles ahead
+    static constexpr int STAGES = 4, CONSUMERS = 8, THREADS = 32 * CONSUMERS;
     static constexpr int TILE_BYTES = 128 * 128;
-    static constexpr int QSTR = 144;                         // code staging row pitch (bytes)
-    static constexpr int OFF_Q = STAGES * TILE_BYTES;
-    static constexpr int OFF_RED = OFF_Q + 128 * QSTR;      // partial amax [8][128]
-    static constexpr int OFF_SC = OFF_RED + 8 * 128 * 4;    // tile scales [128]
-    static constexpr int OFF_BAR = OFF_SC + 128 * 4;
-    static constexpr int SMEM = OFF_BAR + 2 * STAGES * 8;
+    static constexpr int OFF_BAR = STAGES * TILE_BYTES;
+    static constexpr int SMEM = 1024 + OFF_BAR + 2 * STAGES * 8;   // + alignment slack (SWIZZLE_128B)
 };
 
 template <bool kPow2>
@@ -1437,9 +1438,10 @@ __global__ void __launch_bounds__(RQCfg::THREADS, 2)
 k_requant_1x128_to_128x1(const __grid_constant__ CUtensorMap tmQ, const float* __restrict__ s, int64_t lds,
                          int64_t M, int64_t K, uint8_t* __restrict__ qT, int64_t ldqT, float* __restrict__ sT, int64_t ldsT) {
     using P = RQCfg;
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     griddep_wait();                 // PDL: previous grid complete, its writes visible
     griddep_launch_dependents();
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + P::OFF_BAR;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -1450,100 +1452,129 @@ k_requant_1x128_to_128x1(const __grid_constant__ CUtensorMap tmQ, const float* _
     __syncthreads();
     const int64_t KB = (K + 127) / 128, MB = (M + 127) / 128;
     const int64_t ntiles = MB * KB;
-    if (warp == P::CONSUMERS) {                          // producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tmQ);
-            int it = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                const int st = it % P::STAGES;
-                mbar_wait(bar0 + 8 * (P::STAGES + st), ((it / P::STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
-                tma_load_2d(sbase + st * P::TILE_BYTES, &tmQ, bar0 + 8 * st, (int)((t % KB) * 128), (int)((t / KB) * 128));
-            }
-        }
-        return;
+    const bool issuer = warp == 0 && lane == 0;
+    auto issue = [&](int64_t tt, int st) {
+        mbar_arrive_expect_tx(bar0 + 8 * st, P::TILE_BYTES);
+        tma_load_2d(sbase + st * P::TILE_BYTES, &tmQ, bar0 + 8 * st, (int)((tt % KB) * 128), (int)((tt / KB) * 128));
+    };
+    if (issuer) {
+        tma_prefetch_desc(&tmQ);
+        for (int i = 0; i < P::STAGES - 1 && blockIdx.x + (int64_t)i * gridDim.x < ntiles; ++i) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
     }
-    float (*red)[128] = reinterpret_cast<float (*)[128]>(smem + P::OFF_RED);
-    float* scl = reinterpret_cast<float*>(smem + P::OFF_SC);
-    uint8_t* stage = smem + P::OFF_Q;
-    const int tid = threadIdx.x, wc = tid & 31, rg = tid >> 5;
+    const int cg = lane & 3, tg = lane >> 2;
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % P::STAGES;
+        if (issuer) {
+            // tile #it + STAGES - 1 into the stage tile #it - 1 used (released by every warp by now, usually)
+            const int64_t tn = t + (int64_t)(P::STAGES - 1) * gridDim.x;
+            if (tn < ntiles) {
+                const int sn = (it + P::STAGES - 1) % P::STAGES;
+                if (it >= 1) mbar_wait(bar0 + 8 * (P::STAGES + sn), ((it - 1) / P::STAGES) & 1);
+                issue(tn, sn);
+            }
+        }
         const int64_t mb = t / KB, kb = t - mb * KB;
-        const int64_t m0 = mb * 128 + rg * 16, k0 = kb * 128 + 4 * wc;
-        // row scales of this thread's 16 tokens (the same for the whole warp: broadcast loads)
+        const int64_t m0 = mb * 128 + 16 * tg;           // this lane's first token
+        // row scales of the lane's tokens in its rotated order (issued before the stage wait)
+        const float* srow = s + kb * lds + m0;
         float sr[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) sr[r] = (m0 + r < M) ? __ldg(s + kb * lds + m0 + r) : 0.0f;
+        for (int r = 0; r < 16; ++r) {
+            const int k = (r + tg) & 15;
+            sr[r] = (m0 + k < M) ? __ldg(srow + k) : 0.0f;
+        }
         mbar_wait(bar0 + 8 * st, (it / P::STAGES) & 1);
-        uint32_t w[16];
         const uint32_t tile = sbase + st * P::TILE_BYTES;
+        uint32_t w[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) w[r] = lds32(tile + (rg * 16 + r) * 128 + wc * 4);
+        for (int r = 0; r < 16; ++r) {
+            const int row = 16 * tg + ((r + tg) & 15);
+            w[r] = lds32(tile + row * 128 + ((warp ^ (row & 7)) << 4) + 4 * cg);
+        }
         // TMA-written stage read with ld.shared: proxy fence before the release (gemm.cu release_scales)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (P::STAGES + st));
-        float v[16][4];
-        float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
+        // xhat = RN32(dec(q) * s): recomputed in the encode pass below rather than kept (64 registers
+        // more would leave one CTA per SM)
+        auto dequant = [&](int r, float* d) __attribute__((always_inline)) {
             const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] & 0xFFFFu), __NV_E4M3);
             const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[r] >> 16), __NV_E4M3);
             const float2 d01 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
             const float2 d23 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
-            const float d[4] = {d01.x, d01.y, d23.x, d23.y};
+            d[0] = __fmul_rn(d01.x, sr[r]); d[1] = __fmul_rn(d01.y, sr[r]);   // TMA zero-fills codes past M / K
+            d[2] = __fmul_rn(d23.x, sr[r]); d[3] = __fmul_rn(d23.y, sr[r]);
+        };
+        float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                v[r][j] = __fmul_rn(d[j], sr[r]);                 // TMA zero-fills codes past M / K
-                a4[j] = fmaxf(a4[j], fabsf(v[r][j]));
-            }
+        for (int r = 0; r < 16; ++r) {
+            float d[4];
+            dequant(r, d);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a4[j] = fmaxf(a4[j], fabsf(d[j]));
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) red[rg][4 * wc + j] = a4[j];
-        named_bar_sync(1, 32 * P::CONSUMERS);
-        if (tid < 128) {
-            float a = red[0][tid];
-#pragma unroll
-            for (int i = 1; i < 8; ++i) a = fmaxf(a, red[i][tid]);
-            const float sc = group_scale_t<kPow2>(a);
-            scl[tid] = sc;
-            if (kb * 128 + tid < K) sT[mb * ldsT + kb * 128 + tid] = sc;
-        }
-        named_bar_sync(1, 32 * P::CONSUMERS);
+        // the channel's amax over the tile's 128 tokens: the warp's 8 token groups
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const float sc = scl[4 * wc + j];
-            const float rc = __frcp_rn(sc);
-            const bool fast = fast_div_ok(sc);
-            uint32_t code[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float x0 = div_scale(v[4 * u][j], sc, rc, fast), x1 = div_scale(v[4 * u + 1][j], sc, rc, fast);
-                const float x2 = div_scale(v[4 * u + 2][j], sc, rc, fast), x3 = div_scale(v[4 * u + 3][j], sc, rc, fast);
-                code[u] = cvt_e4m3x2(x0, x1) | (cvt_e4m3x2(x2, x3) << 16);
-            }
-            *reinterpret_cast<uint4*>(stage + (4 * wc + j) * P::QSTR + rg * 16) = make_uint4(code[0], code[1], code[2], code[3]);
+            for (int o = 4; o < 32; o <<= 1) a4[j] = fmaxf(a4[j], __shfl_xor_sync(0xffffffffu, a4[j], o));
         }
-        named_bar_sync(1, 32 * P::CONSUMERS);
-        // 128-byte qT row segments: a warp writes 4 channels per instruction
-        const int64_t mt = mb * 128, kt = kb * 128;
+        const int64_t c0 = kb * 128 + 16 * warp + 4 * cg;   // this lane's first channel
+        float sc[4], rc[4];
+        bool fast = true;
 #pragma unroll
-        for (int i = 0; i < 1024 / (32 * P::CONSUMERS); ++i) {
-            const int pc = i * 32 * P::CONSUMERS + tid, ch = pc >> 3, off = (pc & 7) * 16;
-            if (kt + ch >= K || mt + off >= M) continue;
-            const uint4 val = *reinterpret_cast<const uint4*>(stage + ch * P::QSTR + off);
-            uint8_t* dst = qT + (kt + ch) * ldqT + mt + off;
-            if (mt + off + 16 <= M) {
-                *reinterpret_cast<uint4*>(dst) = val;
-            } else {
-                const uint8_t* b = reinterpret_cast<const uint8_t*>(&val);
-                for (int e = 0; e < 16 && mt + off + e < M; ++e) dst[e] = b[e];
+        for (int j = 0; j < 4; ++j) {
+            sc[j] = group_scale_t<kPow2>(a4[j]);
+            rc[j] = __frcp_rn(sc[j]);
+            fast = fast && fast_div_ok(sc[j]);
+            if (tg == 0 && c0 + j < K) sT[mb * ldsT + c0 + j] = sc[j];
+        }
+        fast = __all_sync(0xffffffffu, fast);               // warp-uniform branch below
+        const uint32_t rot = 8u * (tg & 3);
+        const bool wrot = tg >= 4;
+        uint32_t code[4][4];                                 // [channel][4-token group]
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float x[4][4];                                   // [token][channel]
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dequant(4 * u + i, x[i]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float y[4];
+                if (fast) {
+                    const float2 r2 = make_float2(rc[j], rc[j]), ns2 = make_float2(-sc[j], -sc[j]);
+                    const float2 a = div_scale2_fast(make_float2(x[0][j], x[1][j]), r2, ns2);
+                    const float2 b = div_scale2_fast(make_float2(x[2][j], x[3][j]), r2, ns2);
+                    y[0] = a.x; y[1] = a.y; y[2] = b.x; y[3] = b.y;
+                } else {
+                    const bool f = fast_div_ok(sc[j]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) y[e] = div_scale(x[e][j], sc[j], rc[j], f);
+                }
+                code[j][u] = cvt_e4m3x2(y[0], y[1]) | (cvt_e4m3x2(y[2], y[3]) << 16);
             }
         }
-        // the staging buffer and red[] are rewritten for the next tile only after the next tile's
-        // first barrier, which every warp reaches after its stores above
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t* c = code[j];
+            // byte r of c is token 16tg + ((r + tg) & 15): rotate the 16 bytes left by tg so that byte
+            // k is token 16tg + k (a whole word for tg >= 4, then tg & 3 bytes)
+            uint32_t d[4], e[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = wrot ? c[(i + 3) & 3] : c[i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[i] = __funnelshift_l(d[(i + 3) & 3], d[i], rot);
+            const int64_t ch = c0 + j;
+            if (ch < K && m0 < M) {
+                uint8_t* dst = qT + ch * ldqT + m0;
+                if (m0 + 16 <= M) {
+                    *reinterpret_cast<uint4*>(dst) = make_uint4(e[0], e[1], e[2], e[3]);
+                } else {
+                    for (int b = 0; b < 16 && m0 + b < M; ++b) dst[b] = (uint8_t)(e[b >> 2] >> (8 * (b & 3)));
+                }
+            }
+        }
     }
 }
 
@@ -1554,7 +1585,7 @@ cudaError_t launch_requant_1x128_to_128x1(const uint8_t* q, int64_t ldq, const f
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
     const uint64_t str[1] = {(uint64_t)ldq};
     const uint32_t box[2] = {128, 128};
-    if (!make_tmap(&tm, TMAP_U8, 2, q, dims, str, box, 0)) return cudaErrorInvalidValue;
+    if (!make_tmap(&tm, TMAP_U8, 2, q, dims, str, box, 128)) return cudaErrorInvalidValue;   // SWIZZLE_128B
     static bool attr[2][64] = {{false}};   // per instantiation and device
     int dev = 0;
     cudaGetDevice(&dev);

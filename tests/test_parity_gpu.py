@@ -151,6 +151,7 @@ REQ_CASES = [
     ("ragged_M_and_K", 300, 1104, "outlier"),      # short last groups on both axes
     ("C1_X", 4096, 7168, "gauss"),                  # the bench's X: the Wgrad operand from cached FP8
     ("special", 256, 384, "special"),               # signed zeros, subnormals, 448 boundary, huge/tiny rows
+    ("short_rows", 5, 144, "outlier"),              # fewer tokens than one lane's 16-token run
 ]
 
 

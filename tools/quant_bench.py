@@ -52,6 +52,11 @@ def main():
     rqT, rsT = e(IN, T), e(T // 128, p4(IN), dt=torch.float32)[:, :IN]
     cases.append(("requant(X)", T * IN * 2 + 4 * T * (IN // 128) + 4 * IN * (T // 128),
                   lambda: fp.requantize_1x128_to_128x1(xq, xs, rqT, rsT)))
+    M3 = 16384                                  # C3's token count: the fixed per-launch cost amortised
+    xq3, xs3 = fp.quantize_act_1x128(W.gaussian_act(M3, IN, seed=0).to(dev))
+    rqT3, rsT3 = e(IN, M3), e(M3 // 128, p4(IN), dt=torch.float32)[:, :IN]
+    cases.append(("requant(C3 X)", M3 * IN * 2 + 4 * M3 * (IN // 128) + 4 * IN * (M3 // 128),
+                  lambda: fp.requantize_1x128_to_128x1(xq3, xs3, rqT3, rsT3)))
     w = W.master_weight(OUT, IN, seed=1).to(dev)
     wq, sw, wqT = e(OUT, IN), e(OUT // 128, IN // 128, dt=torch.float32), e(IN, OUT)
     cases.append(("weight(W)+T", 6 * OUT * IN + 4 * (OUT // 128) * (IN // 128),
