@@ -1425,8 +1425,8 @@ namespace fp8bs {
 // rotated back by tg bytes and stored as one 16-byte run of qT (a warp store covers 4 channels x
 // 128 tokens).  2 CTAs per SM.
 struct RQCfg {
-    // no separate producer warp: 288 threads would allocate registers as for 320 and leave one CTA
-    // per SM; lane 0 of warp 0 issues the TMA loads, STAGES - 1 tiles ahead
+    // no separate producer warp: with 288 threads ncu reported a register block limit of one CTA per
+    // SM (even at 104 registers); lane 0 of warp 0 issues the TMA loads, STAGES - 1 tiles ahead
     static constexpr int STAGES = 4, CONSUMERS = 8, THREADS = 32 * CONSUMERS;
     static constexpr int TILE_BYTES = 128 * 128;
     static constexpr int OFF_BAR = STAGES * TILE_BYTES;
