@@ -639,6 +639,27 @@ def cpu_baseline_block(min_seconds=10.0):
 
 
 # ------------------------------------------------------------------------ main ----
+_OUT_FD = None   # the process's original stdout: the JSON line goes there and nothing else does
+
+
+def keep_stdout_for_the_line():
+    """Route everything else written to stdout (C libraries included: NCCL prints its version banner at
+    communicator init) to stderr, so that stdout carries exactly the one JSON line."""
+    global _OUT_FD
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict):
+    data = (json.dumps(line) + "\n").encode()
+    if _OUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_OUT_FD, data)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -711,7 +732,7 @@ def run_reference(args, world, rank):
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": f"each step: {desc}"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -734,6 +755,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    keep_stdout_for_the_line()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -762,7 +784,7 @@ def main():
     if rank == 0:
         if args.cpu and world == 1:
             result["cpu_baseline"] = cpu_baseline_block()
-        print(json.dumps(result), flush=True)
+        emit(result)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
