@@ -1030,8 +1030,9 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (elect_one() && !((kDbg & 512))) mbar_arrive(sempty_bar(ss));
             };
             bool unrolled = false;
-            // dense Fprop/Dgrad only: in the Wgrad and grouped kernels the unrolled body makes ptxas
-            // spill loop state into local memory (measured: Wgrad -7%, grouped C4 -20%)
+            // Fprop/Dgrad, dense and grouped (K-blocks a multiple of 8): in the Wgrad kernel the unrolled
+            // body makes ptxas spill loop state into local memory (measured: Wgrad -7%); the split-K
+            // units cover arbitrary K-block ranges
             if constexpr (!kWgrad && !kSplit) unrolled = p.KB % C::kSStages == 0;
             if (unrolled) {
                 // K-blocks in groups of kSStages (8): the scale stage is the index in the group, the TMEM
