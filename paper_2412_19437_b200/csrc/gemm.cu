@@ -1495,9 +1495,11 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
         // routing over 256 experts, K = 7168, N = 2048 (tools/gemm_matrix.py, r02; one CTA / pair, us):
         // 112 rows per expert 669-687 / 727-746; 128: 815-966 / 788-845 (box to box); 144: 988-1200 /
         // 922; 160: 1128-1242 / 943; 192: 1268-1370 / 893-936; 224: 1286-1383 / 898-1012; 256:
-        // 1295-1314 / 1157-1166.  The SwiGLU epilogue has no folded tiles: pairs only from 256 rows.
-        // (Grouped Wgrad: a.M is one expert's output rows — the dense per-expert choice.)
-        if (a.grouped && a.layout != 2) v = (a.M / (a.G > 0 ? a.G : 1) >= (a.swiglu ? 256 : 128)) ? 2 : 1;
+        // 1295-1314 / 1157-1166.  The grouped SwiGLU epilogue (no folded tiles; the pair kernel spills
+        // ~300 bytes) runs on single CTAs at every size: uniform routing, 128..2048 rows per expert,
+        // one CTA 11-23% faster (tools/swiglu_bench.py SWIGLU_SWEEP, r02).  (Grouped Wgrad: a.M is
+        // one expert's output rows — the dense per-expert choice.)
+        if (a.grouped && a.layout != 2) v = (!a.swiglu && a.M / (a.G > 0 ? a.G : 1) >= 128) ? 2 : 1;
         else v = (a.M <= 128) ? 1 : 2;
     }
     return v == 1 ? launch_v<false>(a, st, detail) : launch_v<true>(a, st, detail);

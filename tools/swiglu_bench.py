@@ -61,5 +61,28 @@ def main():
         print(f"{name:36s} {ms:7.3f} ms {fl4 / ms / 1e9:6.0f} TFLOP/s  ({R} rows)", flush=True)
 
 
+
+def variant_sweep(tokens):
+    """Grouped SwiGLU (no cache) under both tile variants (the test-hooks build), uniform top-8 routing
+    over 256 experts: where CTA pairs start to pay without folded tiles."""
+    dev = "cuda"
+    K, N2, E = 7168, 4096, 256
+    B4 = torch.randint(0, 0x7E, (E, N2, K), dtype=torch.uint8, device=dev)
+    sB4 = torch.rand(E, N2 // 128, K // 128, device=dev) * 1e-3
+    for T in tokens:
+        _, off = W.group_rows(W.route_uniform(T, E, 8), E)
+        R = int(off[-1])
+        A4 = torch.randint(0, 0x7E, (R, K), dtype=torch.uint8, device=dev)
+        sA4 = torch.rand(K // 128, (R + 3) // 4 * 4, device=dev)[:, :R] * 1e-2
+        o4 = off.to(dev)
+        for v in (1, 2):
+            with fp.forced_variant(v):
+                ms = med_ms(lambda: fp.grouped_gemm_swiglu(o4, A4, sA4, B4, sB4, cache=False))
+            print(f"tokens {T:6d} ({R // E} rows/expert) variant {v}: {ms:7.3f} ms", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if os.environ.get("SWIGLU_SWEEP"):
+        variant_sweep([int(t) for t in os.environ["SWIGLU_SWEEP"].split(",")])
+    else:
+        main()
