@@ -42,6 +42,12 @@
 #ifndef FP8BS_MX_MC
 #define FP8BS_MX_MC 1    // CTA pairs along M sharing each B tile by TMA multicast (0: independent CTAs)
 #endif
+#ifndef FP8BS_MX_GPAIR_ROWS
+// grouped Fprop/Dgrad: CTA pairs from this many rows per expert on average.  Uniform top-8 routing, 256
+// experts, K = 7168, N = 2048 (tools/grouped_mx_sweep.py, r02; one CTA / pair, ms): 128 rows 0.835 /
+// 0.994, 160: 1.041 / 0.994, 192: 1.047 / 1.000, 224: 1.068 / 1.021
+#define FP8BS_MX_GPAIR_ROWS 144
+#endif
 #ifndef FP8BS_MX_2CTA
 #define FP8BS_MX_2CTA 1  // the CTA pairs run tcgen05.mma.cta_group::2 (M = 256, each CTA stages half of B) instead of
                          // two cta_group::1 MMAs over a multicast full B
@@ -651,7 +657,7 @@ cudaError_t launch_gemm_mx(const GemmArgs& a, cudaStream_t st, const char** deta
     // grouped (Fprop / Dgrad): CTA pairs (2-CTA MMAs over 256-row units of one expert) when the experts
     // average at least 256 rows (C4); otherwise unpaired: a pair shares one expert's n tile over 2 x 128
     // rows, and at the small-expert MoE shapes that left the second CTA idle (C2: 810 vs 1234 TFLOP/s)
-    const bool gpair = a.grouped && !gw && FP8BS_MX_MC && FP8BS_MX_2CTA && a.M / (a.G > 0 ? a.G : 1) >= 256;
+    const bool gpair = a.grouped && !gw && FP8BS_MX_MC && FP8BS_MX_2CTA && a.M / (a.G > 0 ? a.G : 1) >= FP8BS_MX_GPAIR_ROWS;
     if (a.grouped && !gw) {   // B [G][N][K], contiguous
         const uint64_t dims[3] = {(uint64_t)a.K, (uint64_t)a.N, (uint64_t)a.G};
         const uint64_t str[2] = {(uint64_t)a.K, (uint64_t)a.K * (uint64_t)a.N};
