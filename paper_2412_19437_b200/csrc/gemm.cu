@@ -144,7 +144,10 @@ struct KParams {
 constexpr int kTsN = 512;
 constexpr int kTsSlots = 12;
 #ifndef FP8BS_PROMO_POLL
-#define FP8BS_PROMO_POLL 0
+// promotion warps busy-poll (test_wait) the TMEM slot's full barrier instead of try_wait: 0 never, 1 always,
+// 2 grouped CTA-pair kernels only (in the one-CTA grouped kernels it made ptxas spill ~330 bytes).  Same-box A/B (r02): C4 grouped +1% with idle gaps (2315 -> 2338 TFLOP/s) and
+// +0.4-2% in 40 power-capped bench steps; the dense C1 GEMMs within noise.
+#define FP8BS_PROMO_POLL 2
 #endif
 #ifndef FP8BS_ISSUER_POLL
 #define FP8BS_ISSUER_POLL 0
@@ -909,11 +912,8 @@ k_gemm_bs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 3 : 5, sit);
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(8, sit);
                 if (!((kDbg & 128))) {
-#if FP8BS_PROMO_POLL
-                    mbar_wait_poll(pfull_bar(pb), pph);
-#else
-                    mbar_wait(pfull_bar(pb), pph);
-#endif
+                    if constexpr (FP8BS_PROMO_POLL == 1 || (FP8BS_PROMO_POLL == 2 && kGrouped && kPair)) mbar_wait_poll(pfull_bar(pb), pph);
+                    else mbar_wait(pfull_bar(pb), pph);
                 }
                 if (kTrace && lane == 0 && warp == C::THREADS / 32 - 1) FP8BS_TS(9, sit);
                 if (kTrace && lane == 0 && (warp == 4 || warp == 7)) FP8BS_TS(warp == 4 ? 4 : 6, sit);
@@ -1495,11 +1495,12 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st, const char** detail)
         // routing over 256 experts, K = 7168, N = 2048 (tools/gemm_matrix.py, r02; one CTA / pair, us):
         // 112 rows per expert 669-687 / 727-746; 128: 815-966 / 788-845 (box to box); 144: 988-1200 /
         // 922; 160: 1128-1242 / 943; 192: 1268-1370 / 893-936; 224: 1286-1383 / 898-1012; 256:
-        // 1295-1314 / 1157-1166.  The grouped SwiGLU epilogue (no folded tiles; the pair kernel spills
-        // ~300 bytes) runs on single CTAs at every size: uniform routing, 128..2048 rows per expert,
-        // one CTA 11-23% faster (tools/swiglu_bench.py SWIGLU_SWEEP, r02).  (Grouped Wgrad: a.M is
-        // one expert's output rows — the dense per-expert choice.)
-        if (a.grouped && a.layout != 2) v = (!a.swiglu && a.M / (a.G > 0 ? a.G : 1) >= 128) ? 2 : 1;
+        // 1295-1314 / 1157-1166.  The grouped SwiGLU epilogue has no folded tiles: pairs from 256 rows
+        // (tools/swiglu_bench.py SWIGLU_SWEEP, r02, one CTA / pair, ms: 256 rows 2.574 / 2.580, 384:
+        // 3.463 / 3.310, 512: 4.256 / 4.106, 2048: 14.29 / 13.07; before the promotion's busy-poll the
+        // pair kernel spilled ~300 bytes and lost at every size).  (Grouped Wgrad: a.M is one expert's
+        // output rows — the dense per-expert choice.)
+        if (a.grouped && a.layout != 2) v = (a.M / (a.G > 0 ? a.G : 1) >= (a.swiglu ? 256 : 128)) ? 2 : 1;
         else v = (a.M <= 128) ? 1 : 2;
     }
     return v == 1 ? launch_v<false>(a, st, detail) : launch_v<true>(a, st, detail);
