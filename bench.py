@@ -659,7 +659,8 @@ def emit(line: dict):
         sys.stdout.write(data.decode())
         sys.stdout.flush()
     else:
-        os.write(_OUT_FD, data)
+        while data:                      # os.write may write fewer bytes than asked
+            data = data[os.write(_OUT_FD, data):]
 
 
 def dist_setup(args):
